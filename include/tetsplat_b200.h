@@ -1,0 +1,129 @@
+/*
+ * tetsplat_b200.h — C ABI of the B200-native TeT-Splatting rasterizer (sm_100a).
+ *
+ * The drop-in boundary for the reference's kernel plugin (tetsplat.kernels.get_backend(),
+ * /root/reference/pkg/src/tetsplat/kernels/__init__.py:91-102) and the per-view
+ * orchestration around it (splat.py, raster.py, losses.py, grid.py).  Every pointer
+ * argument is a DEVICE pointer unless noted; `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  All entry points return 0 on success and a negative TS_E* code on
+ * failure; ts_last_error() gives the message (thread-local).  The Python shim maps
+ * TS_EINVAL to ValueError and the others to RuntimeError, like the reference.
+ *
+ * Layouts (row major, C contiguous):
+ *   sdf f64[N], deform f64[N,3]       N = (R+1)^3, implicit Kuhn grid of resolution R
+ *   gradient buffer f32[N,4]          (d_sdf, d_deform_x, d_deform_y, d_deform_z), ACCUMULATED
+ *   scene arrays (capacity >= count)  see ts_scene_t
+ *   maps f32: normal [H,W,3], depth [H,W], opacity [H,W], color [H,W,3]
+ * Functions that must size their caller-allocated outputs return counts through
+ * HOST pointers and synchronise `stream` (marked [sync]).
+ */
+#ifndef TETSPLAT_B200_H
+#define TETSPLAT_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_OK 0
+#define TS_EINVAL (-1)  /* invalid argument (ValueError in the shim)     */
+#define TS_ENOMEM (-2)  /* device allocation failed                        */
+#define TS_ECUDA (-3)   /* CUDA launch / runtime error                     */
+
+/* Pinhole camera (camera.py:13-67): p_cam = R p + t, pixel = (fx X/Z + cx, fy Y/Z + cy). */
+typedef struct ts_camera {
+  double R[9];
+  double t[3];
+  double fx, fy, cx, cy, near_, far_;
+  int32_t width, height;
+  int32_t pad[2];
+} ts_camera;
+
+/* SplatScene (splat.py:177-200) in device memory.  `records` is the 96-byte FP32
+ * compositing record per splat (derived; see ts_prepare_records). */
+typedef struct ts_scene {
+  int32_t* tet_ids;   /* [K]     */
+  int32_t* vert_ids;  /* [K,4]   */
+  double* proj;       /* [K,4,2] */
+  double* depths;     /* [K,4]   */
+  double* f;          /* [K,4]   */
+  double* normals;    /* [K,3]   */
+  double* mean_depth; /* [K]     */
+  double* alpha_max;  /* [K]     */
+  double* bbox;       /* [K,4]   */
+  void* records;      /* [K] x 96 B */
+} ts_scene;
+
+/* TileBins (raster.py:53-71) plus the B200 extras. */
+typedef struct ts_bins {
+  int64_t* starts;    /* [T+1]  tile ranges (== reference starts)          */
+  int64_t* splat_off; /* [K+1]  exclusive scan of per-splat tile counts     */
+  int32_t* items;     /* [M]    splat indices, sorted by (tile, q, index)   */
+  int32_t* pos_of;    /* [M]    list position of each (splat, tile) pair     */
+  uint8_t* nonmono;   /* [T]    1 when mean depth decreases along the list   */
+  int32_t* witems;    /* [M]    window-resorted lists (valid where nonmono)  */
+} ts_bins;
+
+const char* ts_last_error(void);
+int ts_version(void);
+
+/* K1 prefilter (splat.py:66-69): ids of tets with alpha_max >= threshold, increasing.
+ * out_active capacity 6 R^3.  [sync] */
+int ts_prefilter(const double* sdf, int32_t resolution, double s, double threshold, int32_t* out_active,
+                 int64_t* out_count, void* stream);
+
+/* K2 build_scene (splat.py:203-245) for `active` (n_active ids); outputs capacity
+ * n_active; out_count = visible splats.  [sync] */
+int ts_build_scene(const double* sdf, const double* deform, int32_t resolution, const ts_camera* cam, double s,
+                   const int32_t* active, int64_t n_active, const ts_scene* out, int64_t* out_count, void* stream);
+
+/* Compositing records for a scene given only as FP64 arrays (e.g. uploaded). */
+int ts_prepare_records(const ts_scene* scene, int64_t K, int32_t width, int32_t height, void* stream);
+
+/* K3/K5 bin_and_sort phase 1 (raster.py:104-131,138-139): starts[T+1], splat_off[K+1];
+ * returns M (pairs) and the longest tile list.  tile_size must be 16.  [sync] */
+int ts_bin_count(const double* bbox, const double* mean_depth, int64_t K, const ts_camera* cam, int32_t tile_size,
+                 int64_t* starts, int64_t* splat_off, int64_t* out_M, int64_t* out_max_len, void* stream);
+
+/* K4 bin_and_sort phase 2 (raster.py:132-141): items/pos_of/nonmono of `bins`. */
+int ts_bin_sort(const double* bbox, const double* mean_depth, int64_t K, const ts_camera* cam, int32_t tile_size,
+                const ts_bins* bins, int64_t M, int64_t max_len, void* stream);
+
+/* K6 render_forward (raster.py:149-177 + forward_tiles _core.pyx:98-229).
+ * colors f32[K,3] / color_map may be NULL.  n_proc[H,W]: list entries consumed per pixel
+ * (saved state for the backward); n_blend[H,W]: blended records per pixel. */
+int ts_render_forward(const ts_scene* scene, int64_t K, const float* colors, const ts_bins* bins, int64_t M,
+                      const ts_camera* cam, int32_t n_w, double s, double t_stop, float* normal_map,
+                      float* depth_map, float* opacity_map, float* color_map, int32_t* n_proc, int32_t* n_blend,
+                      void* stream);
+
+/* K7 render_backward (raster.py:206-306 + backward_tiles _core.pyx:344-471): accumulates
+ * dL/d(sdf, deform) into d_vert f32[N,4] and dL/dcolor into d_color f32[6R^3,3] (nullable).
+ * maps = forward outputs {normal, depth, opacity, color|NULL}; d_maps likewise. */
+int ts_render_backward(const ts_scene* scene, int64_t K, const float* colors, const ts_bins* bins, int64_t M,
+                       const ts_camera* cam, double s, const float* const maps[4], const float* const d_maps[4],
+                       const int32_t* n_proc, const double* deform, int32_t resolution, float* d_vert,
+                       float* d_color, void* stream);
+
+/* K8 eikonal_loss (losses.py:25-36): loss (device f64[1], overwritten) and
+ * scale * gradients accumulated into d_vert. */
+int ts_eikonal(const double* sdf, const double* deform, int32_t resolution, const int32_t* tet_set, int64_t n,
+               double scale, float* d_vert, double* loss, void* stream);
+
+/* K8 normal_consistency_loss (losses.py:39-52), same conventions. */
+int ts_normal_consistency(const double* sdf, const double* deform, int32_t resolution, double scale, float* d_vert,
+                          double* loss, void* stream);
+
+/* K9 marching_tetrahedra (grid.py:136-239), phase 1: counts.  [sync] */
+int ts_marching_tets_count(const double* sdf, const double* deform, int32_t resolution, int64_t* out_num_verts,
+                           int64_t* out_num_tris, void* stream);
+
+/* K9 phase 2: vertices f64[V,3] (lexicographic, welded) and triangles i64[F,3]
+ * (degenerates removed; out_num_tris receives the final F).  [sync] */
+int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
+                     int64_t* triangles, int64_t* out_num_tris, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TETSPLAT_B200_H */

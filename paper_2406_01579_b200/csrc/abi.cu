@@ -1,0 +1,226 @@
+// abi.cu — extern "C" entry points (include/tetsplat_b200.h): argument checks, error
+// reporting, and dispatch to the kernels in scene.cu / bin.cu / composite.cu /
+// regularizers.cu / mt.cu.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/tetsplat_b200.h"
+#include "internal.cuh"
+#include "scan.cuh"
+
+using namespace ts;
+
+// ---- error plumbing ------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+static int check_cuda(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? TS_ENOMEM : TS_ECUDA;
+  }
+  return TS_OK;
+}
+
+static Camera to_cam(const ts_camera* c) {
+  Camera k;
+  memcpy(k.R, c->R, sizeof(k.R));
+  memcpy(k.t, c->t, sizeof(k.t));
+  k.fx = c->fx; k.fy = c->fy; k.cx = c->cx; k.cy = c->cy;
+  k.near_ = c->near_; k.far_ = c->far_;
+  k.width = c->width; k.height = c->height;
+  return k;
+}
+
+template <class T>
+static T* dalloc(size_t n, cudaStream_t st) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  if (cudaMallocAsync(&p, n * sizeof(T), st) != cudaSuccess) return nullptr;
+  return p;
+}
+
+#define ST(s) reinterpret_cast<cudaStream_t>(s)
+
+extern "C" {
+
+const char* ts_last_error(void) { return g_err.c_str(); }
+int ts_version(void) { return 1; }
+
+int ts_prefilter(const double* sdf, int32_t R, double s, double thr, int32_t* out, int64_t* count, void* stream) {
+  if (!sdf || !out || !count || R < 1) return fail(TS_EINVAL, "ts_prefilter: bad arguments");
+  cudaStream_t st = ST(stream);
+  const int64_t K = 6ll * R * R * R;
+  int64_t* scratch = dalloc<int64_t>(compact_blocks(K), st);
+  if (!scratch) return fail(TS_ENOMEM, "ts_prefilter: out of device memory");
+  *count = ts_impl_prefilter(sdf, R, s, thr, out, scratch, st);
+  cudaFreeAsync(scratch, st);
+  return check_cuda("ts_prefilter");
+}
+
+int ts_build_scene(const double* sdf, const double* deform, int32_t R, const ts_camera* cam, double s,
+                   const int32_t* active, int64_t n_active, const ts_scene* out, int64_t* count, void* stream) {
+  if (!sdf || !deform || !cam || !out || !count || R < 1 || n_active < 0 || (n_active > 0 && !active))
+    return fail(TS_EINVAL, "ts_build_scene: bad arguments");
+  cudaStream_t st = ST(stream);
+  int64_t* scratch = dalloc<int64_t>(compact_blocks(n_active), st);
+  if (!scratch) return fail(TS_ENOMEM, "ts_build_scene: out of device memory");
+  SceneOut o{out->tet_ids, out->vert_ids, out->proj, out->depths, out->f, out->normals, out->mean_depth,
+             out->alpha_max, out->bbox, reinterpret_cast<SplatRec*>(out->records)};
+  *count = ts_impl_build_scene(sdf, deform, R, to_cam(cam), s, active, n_active, o, scratch, st);
+  cudaFreeAsync(scratch, st);
+  return check_cuda("ts_build_scene");
+}
+
+int ts_prepare_records(const ts_scene* sc, int64_t K, int32_t W, int32_t H, void* stream) {
+  if (!sc || K < 0 || W < 1 || H < 1 || W > 32767 || H > 32767) return fail(TS_EINVAL, "ts_prepare_records: bad arguments");
+  ts_impl_prepare_records(K, sc->proj, sc->depths, sc->f, sc->normals, sc->mean_depth, sc->bbox, W, H,
+                          reinterpret_cast<SplatRec*>(sc->records), ST(stream));
+  return check_cuda("ts_prepare_records");
+}
+
+static int tiles_of(const ts_camera* cam, int tile, int& tx, int& ty) {
+  if (tile != TS_TILE) return fail(TS_EINVAL, "tile_size must be 16 on the B200 rasterizer");
+  if (cam->width < 1 || cam->height < 1 || cam->width > 32767 || cam->height > 32767)
+    return fail(TS_EINVAL, "image size must be in [1, 32767]");
+  tx = (cam->width + TS_TILE - 1) / TS_TILE;
+  ty = (cam->height + TS_TILE - 1) / TS_TILE;
+  return TS_OK;
+}
+
+int ts_bin_count(const double* bbox, const double* md, int64_t K, const ts_camera* cam, int32_t tile,
+                 int64_t* starts, int64_t* splat_off, int64_t* M, int64_t* maxL, void* stream) {
+  if (!cam || !starts || !splat_off || !M || !maxL || K < 0 || (K > 0 && (!bbox || !md)))
+    return fail(TS_EINVAL, "ts_bin_count: bad arguments");
+  int tx, ty;
+  if (int e = tiles_of(cam, tile, tx, ty)) return e;
+  cudaStream_t st = ST(stream);
+  const int64_t T = (int64_t)tx * ty;
+  BinWork w;
+  w.br = reinterpret_cast<BinRec*>(dalloc<int4>(K, st));
+  w.q = dalloc<uint32_t>(K, st);
+  w.splat_cnt = dalloc<int32_t>(K, st);
+  w.tile_cnt = dalloc<int32_t>(T, st);
+  w.scratch = dalloc<int64_t>(compact_blocks(K > T ? K : T), st);
+  w.dev_i64 = dalloc<int64_t>(2, st);
+  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.scratch || !w.dev_i64)
+    return fail(TS_ENOMEM, "ts_bin_count: out of device memory");
+  ts_impl_bin_count(K, bbox, md, tx, ty, cam->near_, cam->far_, w, starts, splat_off, M, maxL, st);
+  cudaFreeAsync(w.br, st); cudaFreeAsync(w.q, st); cudaFreeAsync(w.splat_cnt, st);
+  cudaFreeAsync(w.tile_cnt, st); cudaFreeAsync(w.scratch, st); cudaFreeAsync(w.dev_i64, st);
+  return check_cuda("ts_bin_count");
+}
+
+int ts_bin_sort(const double* bbox, const double* md, int64_t K, const ts_camera* cam, int32_t tile,
+                const ts_bins* b, int64_t M, int64_t maxL, void* stream) {
+  if (!cam || !b || K < 0 || M < 0 || (M > 0 && (!b->items || !b->pos_of || !b->starts || !b->splat_off)) || !b->nonmono)
+    return fail(TS_EINVAL, "ts_bin_sort: bad arguments");
+  int tx, ty;
+  if (int e = tiles_of(cam, tile, tx, ty)) return e;
+  cudaStream_t st = ST(stream);
+  const int64_t T = (int64_t)tx * ty;
+  // recompute per-splat rects/keys (cheap) instead of keeping phase-1 scratch alive
+  BinWork w;
+  w.br = reinterpret_cast<BinRec*>(dalloc<int4>(K, st));
+  w.q = dalloc<uint32_t>(K, st);
+  w.splat_cnt = dalloc<int32_t>(K, st);
+  w.tile_cnt = dalloc<int32_t>(T, st);
+  w.scratch = dalloc<int64_t>(compact_blocks(K > T ? K : T), st);
+  w.dev_i64 = dalloc<int64_t>(2, st);
+  uint64_t* keys = dalloc<uint64_t>(M, st);
+  uint64_t* gs = maxL > 16384 ? dalloc<uint64_t>(2 * M, st) : nullptr;
+  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.scratch || !w.dev_i64 || !keys || (maxL > 16384 && !gs))
+    return fail(TS_ENOMEM, "ts_bin_sort: out of device memory");
+  // phase-1 kernel again for br/q (starts/splat_off are inputs here and are not rewritten)
+  int64_t M2 = 0, L2 = 0;
+  int64_t* st_tmp = dalloc<int64_t>(T + 1, st);
+  int64_t* so_tmp = dalloc<int64_t>(K + 1, st);
+  ts_impl_bin_count(K, bbox, md, tx, ty, cam->near_, cam->far_, w, st_tmp, so_tmp, &M2, &L2, st);
+  cudaFreeAsync(st_tmp, st);
+  cudaFreeAsync(so_tmp, st);
+  if (M2 != M) return fail(TS_EINVAL, "ts_bin_sort: M does not match the scene (call ts_bin_count first)");
+  ts_impl_bin_sort(K, tx, ty, md, w, b->starts, b->splat_off, maxL, keys, gs, b->items, b->pos_of, b->nonmono, st);
+  cudaFreeAsync(w.br, st); cudaFreeAsync(w.q, st); cudaFreeAsync(w.splat_cnt, st);
+  cudaFreeAsync(w.tile_cnt, st); cudaFreeAsync(w.scratch, st); cudaFreeAsync(w.dev_i64, st);
+  cudaFreeAsync(keys, st);
+  if (gs) cudaFreeAsync(gs, st);
+  return check_cuda("ts_bin_sort");
+}
+
+static Scene64 s64_of(const ts_scene* sc) { return Scene64{sc->proj, sc->depths, sc->f, sc->bbox}; }
+static BinsView bv_of(const ts_bins* b) {
+  return BinsView{b->starts, b->splat_off, b->items, b->pos_of, b->nonmono, b->witems};
+}
+
+int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
+                      const ts_camera* cam, int32_t n_w, double s, double t_stop, float* nmap, float* dmap,
+                      float* omap, float* cmap, int32_t* n_proc, int32_t* n_blend, void* stream) {
+  if (n_w < 1) return fail(TS_EINVAL, "resorting window must be >= 1");
+  if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0)
+    return fail(TS_EINVAL, "ts_render_forward: bad arguments");
+  int tx, ty;
+  if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  cudaStream_t st = ST(stream);
+  BinsView bv = bv_of(b);
+  ts_impl_window(tx * ty, bv, M, sc->mean_depth, n_w, st);
+  ts_impl_forward(tx, ty, bv, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
+                  cam->height, (float)s, (float)t_stop, nmap, dmap, omap, cmap, n_proc, n_blend, st);
+  return check_cuda("ts_render_forward");
+}
+
+int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
+                       const ts_camera* cam, double s, const float* const maps[4], const float* const dmaps[4],
+                       const int32_t* n_proc, const double* deform, int32_t R, float* d_vert, float* d_color,
+                       void* stream) {
+  if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert || R < 1 || K < 0 || M < 0)
+    return fail(TS_EINVAL, "ts_render_backward: bad arguments");
+  for (int i = 0; i < 3; ++i)
+    if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward: missing map");
+  int tx, ty;
+  if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
+  const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
+  ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc),
+                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), (float)s, m4, d4, n_proc, d_vert, d_color,
+                   ST(stream));
+  return check_cuda("ts_render_backward");
+}
+
+int ts_eikonal(const double* sdf, const double* deform, int32_t R, const int32_t* tet_set, int64_t n, double scale,
+               float* d_vert, double* loss, void* stream) {
+  if (!sdf || !deform || !d_vert || !loss || R < 1 || n < 0 || (n > 0 && !tet_set))
+    return fail(TS_EINVAL, "ts_eikonal: bad arguments");
+  ts_impl_eikonal(sdf, deform, R, tet_set, n, (float)scale, d_vert, loss, ST(stream));
+  return check_cuda("ts_eikonal");
+}
+
+int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
+                          double* loss, void* stream) {
+  if (!sdf || !deform || !d_vert || !loss || R < 1) return fail(TS_EINVAL, "ts_normal_consistency: bad arguments");
+  ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream));
+  return check_cuda("ts_normal_consistency");
+}
+
+int ts_marching_tets_count(const double* sdf, const double* deform, int32_t R, int64_t* nv, int64_t* nt,
+                           void* stream) {
+  if (!sdf || !deform || !nv || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets_count: bad arguments");
+  int rc = ts_impl_mt_count(sdf, deform, R, nv, nt, ST(stream));
+  if (rc) return fail(rc, "ts_marching_tets_count failed");
+  return check_cuda("ts_marching_tets_count");
+}
+
+int ts_marching_tets(const double* sdf, const double* deform, int32_t R, double* verts, int64_t* tris,
+                     int64_t* nt, void* stream) {
+  if (!sdf || !deform || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets: bad arguments");
+  int rc = ts_impl_mt(sdf, deform, R, verts, tris, nt, ST(stream));
+  if (rc) return fail(rc, "ts_marching_tets failed");
+  return check_cuda("ts_marching_tets");
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+// bin.cu — K3 tile-overlap count/scan/duplicate, K4 per-tile sort, K5 tile ranges.
+//
+// Replaces raster.bin_and_sort (raster.py:104-141).  The reference duplicates splats in
+// splat order, builds key = tile << 32 | q (q = 32-bit fixed-point mean depth) and does
+// one global stable argsort.  Inside one tile that order is exactly "sort by (q, splat
+// index)", a total order, so the B200 design never sorts globally:
+//   count  : per splat, FP64 tile rect (clip(floor(bbox/16))) + q; atomic per-tile counts
+//   scan   : tile counts -> starts[T+1] (== the reference's searchsorted starts, K5)
+//   scatter: (q << 32 | k) keys into each tile's segment (arbitrary order)
+//   sort   : one CTA per tile sorts its segment in shared memory (bitonic, 64-bit keys)
+//            and also emits pos_of (splat -> its list positions, for the deterministic
+//            gradient gather) and a flag telling whether mean depth is non-decreasing
+//            along the list (then the N_w resorting window is the identity, composite.cu).
+// All integer work; HBM/L2-bound.
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace ts {
+
+
+// raster.py:118-121 / 132-134, FP64, numpy order
+__device__ __forceinline__ void tile_rect_q(const double* bb, double md, int tiles_x, int tiles_y, double near_,
+                                            double far_, int& tx0, int& tx1, int& ty0, int& ty1, uint32_t& q) {
+  auto tclip = [](double v, int hi) -> int {
+    double t = floor(v / 16.0);
+    t = t < 0.0 ? 0.0 : t;
+    t = t > (double)hi ? (double)hi : t;
+    return (int)t;
+  };
+  tx0 = tclip(bb[0], tiles_x - 1);
+  tx1 = tclip(bb[2], tiles_x - 1);
+  ty0 = tclip(bb[1], tiles_y - 1);
+  ty1 = tclip(bb[3], tiles_y - 1);
+  double qq = ddiv(dsub(md, near_), dsub(far_, near_));
+  qq = qq < 0.0 ? 0.0 : qq;
+  qq = qq > 1.0 ? 1.0 : qq;
+  q = (uint32_t)(unsigned long long)dmul(qq, 4294967295.0);
+}
+
+__global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const double* __restrict__ md, int tiles_x,
+                            int tiles_y, double near_, double far_, BinRec* __restrict__ br,
+                            uint32_t* __restrict__ qout, int32_t* __restrict__ splat_cnt,
+                            int32_t* __restrict__ tile_cnt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    int tx0, tx1, ty0, ty1;
+    uint32_t q;
+    tile_rect_q(bbox + k * 4, md[k], tiles_x, tiles_y, near_, far_, tx0, tx1, ty0, ty1, q);
+    int nx = tx1 - tx0 + 1, ny = ty1 - ty0 + 1;
+    if (nx < 0) nx = 0;
+    if (ny < 0) ny = 0;
+    br[k] = BinRec{tx0, ty0, nx, ny};
+    qout[k] = q;
+    splat_cnt[k] = nx * ny;
+    for (int y = 0; y < ny; ++y)
+      for (int x = 0; x < nx; ++x) atomicAdd(&tile_cnt[(ty0 + y) * tiles_x + tx0 + x], 1);
+  }
+}
+
+__global__ void k_bin_scatter(int64_t K, const BinRec* __restrict__ br, const uint32_t* __restrict__ q, int tiles_x,
+                              const int64_t* __restrict__ starts, int32_t* __restrict__ cursor,
+                              uint64_t* __restrict__ keys) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    BinRec b = br[k];
+    uint64_t key = ((uint64_t)q[k] << 32) | (uint64_t)(uint32_t)k;
+    for (int y = 0; y < b.ny; ++y)
+      for (int x = 0; x < b.nx; ++x) {
+        int t = (b.ty0 + y) * tiles_x + b.tx0 + x;
+        int slot = atomicAdd(&cursor[t], 1);
+        keys[starts[t] + slot] = key;
+      }
+  }
+}
+
+template <typename Ptr>
+__device__ __forceinline__ void bitonic_sort(Ptr s, int P, int nthreads) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += nthreads) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          uint64_t a = s[i], b = s[ixj];
+          bool asc = (i & k) == 0;
+          if ((a > b) == asc) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ void emit_sorted(uint64_t key, int64_t p, int tile, int tiles_x, const BinRec* br,
+                                            const int64_t* splat_off, int32_t* items, int32_t* pos_of) {
+  int k = (int)(uint32_t)key;
+  items[p] = k;
+  BinRec b = br[k];
+  int tx = tile % tiles_x, ty = tile / tiles_x;
+  int local = (ty - b.ty0) * b.nx + (tx - b.tx0);
+  pos_of[splat_off[k] + local] = (int32_t)p;
+}
+
+// one CTA per tile; handles tiles with lo_len < L <= cap in (dynamic) shared memory
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t lo_len, int64_t cap,
+                                                            const int64_t* __restrict__ starts,
+                                                            const uint64_t* __restrict__ keys, int tiles_x,
+                                                            const BinRec* __restrict__ br,
+                                                            const int64_t* __restrict__ splat_off,
+                                                            const double* __restrict__ md,
+                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
+                                                            uint8_t* __restrict__ nonmono) {
+  extern __shared__ uint64_t s[];
+  __shared__ int bad;
+  const int t = blockIdx.x;
+  if (t >= T) return;
+  const int64_t lo = starts[t], L = starts[t + 1] - lo;
+  if (L <= lo_len || L > cap) return;
+  int P = 1;
+  while (P < L) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += THREADS) s[i] = i < L ? keys[lo + i] : ~0ull;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  bitonic_sort(s, P, THREADS);
+  int mybad = 0;
+  for (int i = threadIdx.x; i < L; i += THREADS) {
+    emit_sorted(s[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+    if (i + 1 < L && md[(uint32_t)s[i]] > md[(uint32_t)s[i + 1]]) mybad = 1;
+  }
+  if (mybad) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
+}
+
+// oversize tiles: bitonic over a padded copy in global scratch (offset 2*lo, size <= 2L)
+__global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, const int64_t* __restrict__ starts,
+                                                           const uint64_t* __restrict__ keys, int tiles_x,
+                                                           const BinRec* __restrict__ br,
+                                                           const int64_t* __restrict__ splat_off,
+                                                           const double* __restrict__ md,
+                                                           uint64_t* __restrict__ scratch,
+                                                           int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
+                                                           uint8_t* __restrict__ nonmono) {
+  __shared__ int bad;
+  const int t = blockIdx.x;
+  if (t >= T) return;
+  const int64_t lo = starts[t], L = starts[t + 1] - lo;
+  if (L <= lo_len) return;
+  int64_t P = 1;
+  while (P < L) P <<= 1;
+  uint64_t* s = scratch + 2 * lo;
+  for (int64_t i = threadIdx.x; i < P; i += 1024) s[i] = i < L ? keys[lo + i] : ~0ull;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int64_t k = 2; k <= P; k <<= 1)
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < P; i += 1024) {
+        int64_t ixj = i ^ j;
+        if (ixj > i) {
+          uint64_t a = s[i], b = s[ixj];
+          bool asc = (i & k) == 0;
+          if ((a > b) == asc) { s[i] = b; s[ixj] = a; }
+        }
+      }
+      __threadfence_block();
+      __syncthreads();
+    }
+  int mybad = 0;
+  for (int64_t i = threadIdx.x; i < L; i += 1024) {
+    emit_sorted(s[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+    if (i + 1 < L && md[(uint32_t)s[i]] > md[(uint32_t)s[i + 1]]) mybad = 1;
+  }
+  if (mybad) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
+}
+
+__global__ void k_max_len(int T, const int64_t* __restrict__ starts, int64_t* __restrict__ out) {
+  int64_t m = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    int64_t L = starts[t + 1] - starts[t];
+    m = L > m ? L : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y > m ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)out, (unsigned long long)m);
+}
+
+}  // namespace ts
+
+using namespace ts;
+
+
+// Phase 1: counts, starts[T+1], splat_off[K+1]; returns M and max tile length (host sync).
+void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tiles_x, int tiles_y, double near_,
+                       double far_, const BinWork& w, int64_t* starts, int64_t* splat_off, int64_t* M_out,
+                       int64_t* maxL_out, cudaStream_t st) {
+  const int T = tiles_x * tiles_y;
+  cudaMemsetAsync(w.tile_cnt, 0, sizeof(int32_t) * T, st);
+  cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t) * 2, st);
+  if (K > 0) {
+    int blocks = (int)((K + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_bin_count<<<blocks, 256, 0, st>>>(K, bbox, md, tiles_x, tiles_y, near_, far_, w.br, w.q, w.splat_cnt,
+                                        w.tile_cnt);
+  }
+  scan_counts(w.tile_cnt, T, starts, w.scratch, st);
+  scan_counts(w.splat_cnt, K, splat_off, w.scratch, st);
+  k_max_len<<<8, 256, 0, st>>>(T, starts, w.dev_i64 + 1);
+  int64_t h[2];
+  cudaMemcpyAsync(&h[0], starts + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[1], w.dev_i64 + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  *M_out = h[0];
+  *maxL_out = h[1];
+}
+
+// Phase 2: scatter keys + per-tile sort.  keys: [M]; gscratch: [2M] only when maxL > 16384.
+void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const BinWork& w, const int64_t* starts,
+                      const int64_t* splat_off, int64_t maxL, uint64_t* keys, uint64_t* gscratch, int32_t* items,
+                      int32_t* pos_of, uint8_t* nonmono, cudaStream_t st) {
+  const int T = tiles_x * tiles_y;
+  cudaMemsetAsync(w.tile_cnt, 0, sizeof(int32_t) * T, st);
+  cudaMemsetAsync(nonmono, 0, T, st);
+  if (K > 0) {
+    int blocks = (int)((K + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_bin_scatter<<<blocks, 256, 0, st>>>(K, w.br, w.q, tiles_x, starts, w.tile_cnt, keys);
+  }
+  if (maxL >= 1) {
+    k_tile_sort_smem<256><<<T, 256, 2048 * sizeof(uint64_t), st>>>(T, 0, 2048, starts, keys, tiles_x, w.br,
+                                                                   splat_off, md, items, pos_of, nonmono);
+    if (maxL > 2048) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_tile_sort_smem<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             16384 * (int)sizeof(uint64_t));
+        attr = true;
+      }
+      k_tile_sort_smem<1024><<<T, 1024, 16384 * sizeof(uint64_t), st>>>(T, 2048, 16384, starts, keys, tiles_x,
+                                                                         w.br, splat_off, md, items, pos_of,
+                                                                         nonmono);
+    }
+    if (maxL > 16384)
+      k_tile_sort_global<<<T, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,
+                                             pos_of, nonmono);
+  }
+}

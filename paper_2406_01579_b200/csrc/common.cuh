@@ -1,0 +1,144 @@
+// common.cuh — shared device helpers for the B200 tetrahedron rasterizer (sm_100a).
+//
+// Conventions
+//  * Geometry that feeds bit-exact decisions (tile rects, depth keys, pixel rects,
+//    degenerate-face tests, the prefilter threshold, Marching Tetrahedra) is computed
+//    in FP64 with the reference's operation order and NO fused multiply-add: the
+//    reference is gcc -O2 on x86-64 without -march, which never contracts.  The
+//    __d*_rn intrinsics are never contracted by nvcc.
+//  * Compositing records are FP32; exactness of their inside/outside decisions is kept
+//    by an error-bounded filter with an exact FP64 fallback (see composite.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define TS_TILE 16
+#define TS_TILE_PX (TS_TILE * TS_TILE)
+
+namespace ts {
+
+// ---- exact FP64 arithmetic (no contraction) ----------------------------------------
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---- camera (camera.py:13-67) -------------------------------------------------------
+struct Camera {
+  double R[9];  // world -> camera rotation, row major
+  double t[3];
+  double fx, fy, cx, cy, near_, far_;
+  int32_t width, height;
+  int32_t pad[2];
+};
+
+// ---- implicit Kuhn grid (grid.py:64-117) --------------------------------------------
+// Vertex id = x + n*y + n^2*z (n = R+1); tet id = cell*6 + p, cell = ix*R^2 + iy*R + iz.
+// Corners: c0 = 0, c1 = e[P0], c2 = c1 + e[P1], c3 = (1,1,1) with the axis permutations
+// of grid.py:18; odd permutations (p = 1, 2, 5) have negative volume and swap v2<->v3
+// (grid.py:100-102).
+__device__ __forceinline__ void tet_vertices(int64_t t, int R, int64_t v[4]) {
+  const int64_t n = R + 1;
+  int64_t cell = t / 6;
+  int p = (int)(t - cell * 6);
+  int64_t ix = cell / ((int64_t)R * R);
+  int64_t rem = cell - ix * (int64_t)R * R;
+  int64_t iy = rem / R;
+  int64_t iz = rem - iy * R;
+  // first and second axis of each permutation: (0,1,2),(0,2,1),(1,0,2),(1,2,0),(2,0,1),(2,1,0)
+  const int a0 = (p < 2) ? 0 : (p < 4 ? 1 : 2);
+  const int a1 = (p == 0 || p == 5) ? 1 : ((p == 1 || p == 3) ? 2 : 0);
+  int64_t c1[3] = {0, 0, 0};
+  c1[a0] = 1;
+  int64_t c2[3] = {c1[0], c1[1], c1[2]};
+  c2[a1] = 1;
+  int64_t base = ix + n * iy + n * n * iz;
+  int64_t v1 = base + c1[0] + n * c1[1] + n * n * c1[2];
+  int64_t v2 = base + c2[0] + n * c2[1] + n * n * c2[2];
+  int64_t v3 = base + 1 + n + n * n;
+  v[0] = base;
+  v[1] = v1;
+  const bool odd = (p == 1 || p == 2 || p == 5);
+  v[2] = odd ? v3 : v2;
+  v[3] = odd ? v2 : v3;
+}
+
+// rest coordinate along one axis: np.linspace(-1, 1, R+1)[i] = i*(2/R) + (-1), last = 1
+__device__ __forceinline__ double grid_coord(int64_t i, int R) {
+  if (i == R) return 1.0;
+  return dadd(dmul((double)i, ddiv(2.0, (double)R)), -1.0);
+}
+
+__device__ __forceinline__ void vertex_position(int64_t vid, int R, const double* __restrict__ deform,
+                                                double p[3]) {
+  const int64_t n = R + 1;
+  int64_t z = vid / (n * n);
+  int64_t r = vid - z * n * n;
+  int64_t y = r / n;
+  int64_t x = r - y * n;
+  p[0] = dadd(grid_coord(x, R), deform[vid * 3 + 0]);
+  p[1] = dadd(grid_coord(y, R), deform[vid * 3 + 1]);
+  p[2] = dadd(grid_coord(z, R), deform[vid * 3 + 2]);
+}
+
+// camera.py:56-67.  p_cam = R p + t (row dot products, left to right), then the pinhole.
+__device__ __forceinline__ void project_point(const Camera& c, const double p[3], double& px,
+                                              double& py, double& z, double pc[3]) {
+  for (int r = 0; r < 3; ++r)
+    pc[r] = dadd(dadd(dadd(dmul(p[0], c.R[r * 3 + 0]), dmul(p[1], c.R[r * 3 + 1])),
+                      dmul(p[2], c.R[r * 3 + 2])),
+                 c.t[r]);
+  z = pc[2];
+  double zs = z > 1e-12 ? z : 1e-12;
+  px = dadd(ddiv(dmul(c.fx, pc[0]), zs), c.cx);
+  py = dadd(ddiv(dmul(c.fy, pc[1]), zs), c.cy);
+}
+
+// In-tet field gradient, cross-product form (_core.pyx:474-514); returns det = 6V.
+__device__ __forceinline__ double tet_gradient(const double P[4][3], const double f[4], double g[3],
+                                               double c1[3], double c2[3], double c3[3]) {
+  double e1[3], e2[3], e3[3];
+  for (int i = 0; i < 3; ++i) {
+    e1[i] = dsub(P[1][i], P[0][i]);
+    e2[i] = dsub(P[2][i], P[0][i]);
+    e3[i] = dsub(P[3][i], P[0][i]);
+  }
+  c1[0] = dsub(dmul(e2[1], e3[2]), dmul(e2[2], e3[1]));
+  c1[1] = dsub(dmul(e2[2], e3[0]), dmul(e2[0], e3[2]));
+  c1[2] = dsub(dmul(e2[0], e3[1]), dmul(e2[1], e3[0]));
+  c2[0] = dsub(dmul(e3[1], e1[2]), dmul(e3[2], e1[1]));
+  c2[1] = dsub(dmul(e3[2], e1[0]), dmul(e3[0], e1[2]));
+  c2[2] = dsub(dmul(e3[0], e1[1]), dmul(e3[1], e1[0]));
+  c3[0] = dsub(dmul(e1[1], e2[2]), dmul(e1[2], e2[1]));
+  c3[1] = dsub(dmul(e1[2], e2[0]), dmul(e1[0], e2[2]));
+  c3[2] = dsub(dmul(e1[0], e2[1]), dmul(e1[1], e2[0]));
+  double det = dadd(dadd(dmul(e1[0], c1[0]), dmul(e1[1], c1[1])), dmul(e1[2], c1[2]));
+  g[0] = g[1] = g[2] = 0.0;
+  if (det != 0.0) {
+    double d1 = dsub(f[1], f[0]), d2 = dsub(f[2], f[0]), d3 = dsub(f[3], f[0]);
+    for (int i = 0; i < 3; ++i)
+      g[i] = ddiv(dadd(dadd(dmul(d1, c1[i]), dmul(d2, c2[i])), dmul(d3, c3[i])), det);
+  }
+  return det;
+}
+
+// softplus with the x > 30 passthrough (splat.py:26-28, _core.pyx:29-32)
+__device__ __forceinline__ double softplus_d(double x) { return x > 30.0 ? x : log1p(exp(x)); }
+
+// ---- warp / block utilities ----------------------------------------------------------
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+}  // namespace ts

@@ -1,0 +1,73 @@
+// internal.cuh — structs and host-side entry points shared between the translation units.
+#pragma once
+#include "records.cuh"
+
+namespace ts {
+
+struct SceneOut {
+  int32_t* tet_ids;   // [K]
+  int32_t* vert_ids;  // [K,4]
+  double* proj;       // [K,4,2]
+  double* depths;     // [K,4]
+  double* f;          // [K,4]
+  double* normals;    // [K,3]
+  double* md;         // [K]
+  double* amax;       // [K]
+  double* bbox;       // [K,4]
+  SplatRec* rec;      // [K]
+};
+
+struct BinRec {  // 16 B per splat: first tile and tile-rect extent
+  int32_t tx0, ty0, nx, ny;
+};
+
+struct BinWork {
+  BinRec* br;          // [K]
+  uint32_t* q;         // [K]
+  int32_t* splat_cnt;  // [K]
+  int32_t* tile_cnt;   // [T]  (also the scatter cursor)
+  int64_t* scratch;    // scan scratch, compact_blocks(max(K,T))
+  int64_t* dev_i64;    // [2]
+};
+
+struct BinsView {
+  const int64_t* starts;
+  const int64_t* splat_off;
+  const int32_t* items;
+  const int32_t* pos_of;
+  const uint8_t* nonmono;
+  int32_t* witems;
+};
+
+}  // namespace ts
+
+int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_t* out_active, int64_t* scratch,
+                          cudaStream_t st);
+int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, const ts::Camera& cam, double s,
+                            const int32_t* active, int64_t n_active, const ts::SceneOut& out, int64_t* scratch,
+                            cudaStream_t st);
+void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths, const double* f,
+                             const double* normals, const double* md, const double* bbox, int width, int height,
+                             ts::SplatRec* rec, cudaStream_t st);
+void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tiles_x, int tiles_y, double near_,
+                       double far_, const ts::BinWork& w, int64_t* starts, int64_t* splat_off, int64_t* M_out,
+                       int64_t* maxL_out, cudaStream_t st);
+void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const ts::BinWork& w,
+                      const int64_t* starts, const int64_t* splat_off, int64_t maxL, uint64_t* keys,
+                      uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st);
+void ts_impl_window(int T, const ts::BinsView& b, int64_t M, const double* md, int n_w, cudaStream_t st);
+void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
+                     const ts::Scene64& S64, int W, int H, float s, float t_stop, float* nmap, float* dmap,
+                     float* omap, float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st);
+void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, int64_t K,
+                      const ts::SplatRec* rec, const float* colors, const ts::Scene64& S64,
+                      const int32_t* vert_ids, const int32_t* tet_ids, const double* deform, int R,
+                      const ts::Camera& cam, float s, const float* maps[4], const float* dmaps[4],
+                      const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st);
+void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
+                     float* d_vert, double* loss, cudaStream_t st);
+void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
+                                double* loss, cudaStream_t st);
+int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);
+int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
+               cudaStream_t st);

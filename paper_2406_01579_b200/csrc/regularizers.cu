@@ -1,0 +1,261 @@
+// regularizers.cu — K8 eikonal + normal-consistency losses and their vertex gradients.
+//
+// eikonal (_core.pyx:544-568, losses.py:25-36): one thread per tet of the active set,
+// FP64 cross-product gradient, (|g|-1)^2, chain to the 4 vertices scattered with one
+// red.global.add.v4.f32 per (tet, vertex) into the shared FP32 [N,4] gradient buffer
+// (scaled by lambda: the fit loop's weighting, fit.py:196-207, fused here).
+//
+// normal consistency (_core.pyx:571-668, losses.py:39-52) is rebuilt as three vertex-
+// centric GATHER passes over the implicit Kuhn grid (no atomics, deterministic):
+//   A: vertex mean of incident unit tet normals -> unit vertex normal (+ count, |mean|)
+//   B: per-vertex edge term  d_n(v) = -sum_{edge neighbours} n(b), projected back
+//      through the normalisation; per-vertex share of sum_edges (1 - n_a.n_b)
+//   C: per-vertex sum over incident tets of the chain through the tet normal
+// Incident tets are visited in increasing tet id and edge neighbours in increasing
+// vertex id, which is the reference's accumulation order, so every per-vertex FP64
+// value is bit-identical to the Cython kernel's (only the scalar loss is summed in a
+// different order).
+#include "internal.cuh"
+
+namespace ts {
+
+constexpr double kEpsNormal = 1e-8;  // field.py:11
+
+__device__ __forceinline__ void load_tet(int64_t t, int R, const double* __restrict__ sdf,
+                                         const double* __restrict__ deform, int64_t v[4], double P[4][3],
+                                         double f[4]) {
+  tet_vertices(t, R, v);
+  for (int c = 0; c < 4; ++c) {
+    vertex_position(v[c], R, deform, P[c]);
+    f[c] = sdf[v[c]];
+  }
+}
+
+// _chain_dg (_core.pyx:517-541): dfs[c] = dL/df_c ; position grad = -dfs[c] * g
+__device__ __forceinline__ void chain_coeffs(double det, const double c1[3], const double c2[3], const double c3[3],
+                                             const double dg[3], double dfs[4]) {
+  double d1 = ddiv(dadd(dadd(dmul(c1[0], dg[0]), dmul(c1[1], dg[1])), dmul(c1[2], dg[2])), det);
+  double d2 = ddiv(dadd(dadd(dmul(c2[0], dg[0]), dmul(c2[1], dg[1])), dmul(c2[2], dg[2])), det);
+  double d3 = ddiv(dadd(dadd(dmul(c3[0], dg[0]), dmul(c3[1], dg[1])), dmul(c3[2], dg[2])), det);
+  dfs[0] = -dadd(dadd(d1, d2), d3);
+  dfs[1] = d1;
+  dfs[2] = d2;
+  dfs[3] = d3;
+}
+
+__device__ __forceinline__ double gnorm3(const double g[3]) {
+  return sqrt(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
+}
+
+template <typename T>
+__device__ __forceinline__ void block_add_to(T v, T* out) {
+  v = warp_sum(v);
+  __shared__ T ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+    atomicAdd(out, t);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __restrict__ tet_set, int R,
+                                                 const double* __restrict__ sdf, const double* __restrict__ deform,
+                                                 float scale, float* __restrict__ d_vert, double* __restrict__ loss) {
+  double local = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v[4];
+    double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+    load_tet(tet_set[i], R, sdf, deform, v, P, f);
+    double det = tet_gradient(P, f, g, c1, c2, c3);
+    double nrm = gnorm3(g);
+    local += dmul(dsub(nrm, 1.0), dsub(nrm, 1.0));
+    if (nrm > kEpsNormal && det != 0.0) {
+      double w = ddiv(dmul(2.0, dsub(nrm, 1.0)), nrm);
+      double dg[3] = {dmul(w, g[0]), dmul(w, g[1]), dmul(w, g[2])};
+      double dfs[4];
+      chain_coeffs(det, c1, c2, c3, dg, dfs);
+      for (int c = 0; c < 4; ++c)
+        red_add_v4(d_vert + v[c] * 4, (float)(scale * dfs[c]), (float)(-scale * dfs[c] * g[0]),
+                   (float)(-scale * dfs[c] * g[1]), (float)(-scale * dfs[c] * g[2]));
+    }
+  }
+  block_add_to(local, loss);
+}
+
+// Incident tets of vertex (x,y,z) in increasing tet id.  Calls fn(tet_id, local_slot).
+template <class Fn>
+__device__ __forceinline__ void for_incident_tets(int64_t vid, int R, Fn&& fn) {
+  const int64_t n = R + 1;
+  const int64_t z = vid / (n * n), r = vid - z * n * n, y = r / n, x = r - y * n;
+  for (int dx = 1; dx >= 0; --dx)
+    for (int dy = 1; dy >= 0; --dy)
+      for (int dz = 1; dz >= 0; --dz) {
+        const int64_t cx = x - dx, cy = y - dy, cz = z - dz;
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= R || cy >= R || cz >= R) continue;
+        const int lc = dx | (dy << 1) | (dz << 2);
+        const int64_t cell = cx * (int64_t)R * R + cy * R + cz;
+        for (int p = 0; p < 6; ++p) {
+          const int a0 = (p < 2) ? 0 : (p < 4 ? 1 : 2);
+          const int a1 = (p == 0 || p == 5) ? 1 : ((p == 1 || p == 3) ? 2 : 0);
+          const int k1 = 1 << a0, k2 = k1 | (1 << a1);
+          if (lc == 0 || lc == 7 || lc == k1 || lc == k2) fn(cell * 6 + p);
+        }
+      }
+}
+
+__device__ __forceinline__ int local_slot(const int64_t v[4], int64_t vid) {
+  return v[0] == vid ? 0 : (v[1] == vid ? 1 : (v[2] == vid ? 2 : 3));
+}
+
+// pass A: nv = normalized mean of incident unit normals; cnt; an (0 = undefined)
+__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, int R, const double* __restrict__ sdf,
+                                                           const double* __restrict__ deform,
+                                                           double* __restrict__ nv, double* __restrict__ cnt,
+                                                           double* __restrict__ an) {
+  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+       vid += (int64_t)gridDim.x * blockDim.x) {
+    double s[3] = {0.0, 0.0, 0.0}, c = 0.0;
+    for_incident_tets(vid, R, [&](int64_t t) {
+      int64_t v[4];
+      double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+      load_tet(t, R, sdf, deform, v, P, f);
+      tet_gradient(P, f, g, c1, c2, c3);
+      double nrm = gnorm3(g);
+      if (nrm < kEpsNormal) return;
+      c = dadd(c, 1.0);
+      for (int i = 0; i < 3; ++i) s[i] = dadd(s[i], ddiv(g[i], nrm));
+    });
+    double a = 0.0;
+    if (c != 0.0) {
+      for (int i = 0; i < 3; ++i) s[i] = ddiv(s[i], c);
+      double m = gnorm3(s);
+      if (!(m < kEpsNormal)) {
+        a = m;
+        for (int i = 0; i < 3; ++i) s[i] = ddiv(s[i], m);
+      }
+    }
+    for (int i = 0; i < 3; ++i) nv[vid * 3 + i] = s[i];
+    cnt[vid] = c;
+    an[vid] = a;
+  }
+}
+
+// pass B: edge penalty and its gradient, pushed back through the vertex normalisation
+__global__ void __launch_bounds__(256) k_nc_edges(int64_t N, int R, const double* __restrict__ nv,
+                                                  const double* __restrict__ an, double* __restrict__ dm,
+                                                  double* __restrict__ loss) {
+  const int64_t n = R + 1;
+  // Kuhn edge offsets (grid.py:106-107) as vertex-id deltas, ascending
+  const int64_t off[7] = {1, n, n + 1, n * n, n * n + 1, n * n + n, n * n + n + 1};
+  const int ox[7] = {1, 0, 1, 0, 1, 0, 1}, oy[7] = {0, 1, 1, 0, 0, 1, 1}, oz[7] = {0, 0, 0, 1, 1, 1, 1};
+  double local = 0.0;
+  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+       vid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = vid / (n * n), r = vid - z * n * n, y = r / n, x = r - y * n;
+    double d[3] = {0.0, 0.0, 0.0};
+    const bool def = an[vid] != 0.0;
+    const double a0 = nv[vid * 3], a1 = nv[vid * 3 + 1], a2 = nv[vid * 3 + 2];
+    // lower neighbours (ascending id = descending delta), then upper ones
+    for (int e = 6; e >= 0; --e) {
+      if (x - ox[e] < 0 || y - oy[e] < 0 || z - oz[e] < 0) continue;
+      const int64_t b = vid - off[e];
+      if (!def || an[b] == 0.0) continue;
+      for (int i = 0; i < 3; ++i) d[i] = dsub(d[i], nv[b * 3 + i]);
+    }
+    for (int e = 0; e < 7; ++e) {
+      if (x + ox[e] >= n || y + oy[e] >= n || z + oz[e] >= n) continue;
+      const int64_t b = vid + off[e];
+      if (!def || an[b] == 0.0) continue;
+      const double b0 = nv[b * 3], b1 = nv[b * 3 + 1], b2 = nv[b * 3 + 2];
+      local += dsub(1.0, dadd(dadd(dmul(a0, b0), dmul(a1, b1)), dmul(a2, b2)));
+      d[0] = dsub(d[0], b0);
+      d[1] = dsub(d[1], b1);
+      d[2] = dsub(d[2], b2);
+    }
+    if (def) {
+      double dot = dadd(dadd(dmul(a0, d[0]), dmul(a1, d[1])), dmul(a2, d[2]));
+      const double av = an[vid];
+      d[0] = ddiv(dsub(d[0], dmul(a0, dot)), av);
+      d[1] = ddiv(dsub(d[1], dmul(a1, dot)), av);
+      d[2] = ddiv(dsub(d[2], dmul(a2, dot)), av);
+    }
+    for (int i = 0; i < 3; ++i) dm[vid * 3 + i] = d[i];
+  }
+  block_add_to(local, loss);
+}
+
+// pass C: per-vertex gather of the tet-normal chain (_core.pyx:651-667)
+__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, int R, const double* __restrict__ sdf,
+                                                 const double* __restrict__ deform, const double* __restrict__ cnt,
+                                                 const double* __restrict__ dm, float scale,
+                                                 float* __restrict__ d_vert) {
+  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+       vid += (int64_t)gridDim.x * blockDim.x) {
+    double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
+    for_incident_tets(vid, R, [&](int64_t t) {
+      int64_t v[4];
+      double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+      load_tet(t, R, sdf, deform, v, P, f);
+      double det = tet_gradient(P, f, g, c1, c2, c3);
+      double nrm = gnorm3(g);
+      if (nrm < kEpsNormal) return;
+      double nt[3] = {ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm)};
+      double dnt[3] = {0.0, 0.0, 0.0};
+      for (int c = 0; c < 4; ++c) {
+        double inv = ddiv(1.0, cnt[v[c]]);
+        for (int i = 0; i < 3; ++i) dnt[i] = dadd(dnt[i], dmul(dm[v[c] * 3 + i], inv));
+      }
+      double dot = dadd(dadd(dmul(nt[0], dnt[0]), dmul(nt[1], dnt[1])), dmul(nt[2], dnt[2]));
+      double dg[3];
+      for (int i = 0; i < 3; ++i) dg[i] = ddiv(dsub(dnt[i], dmul(nt[i], dot)), nrm);
+      if (det == 0.0) return;
+      double dfs[4];
+      chain_coeffs(det, c1, c2, c3, dg, dfs);
+      const int c = local_slot(v, vid);
+      ds = dadd(ds, dfs[c]);
+      for (int i = 0; i < 3; ++i) dp[i] = dsub(dp[i], dmul(dfs[c], g[i]));
+    });
+    float4* o = reinterpret_cast<float4*>(d_vert + vid * 4);
+    float4 cur = *o;
+    cur.x += (float)(scale * ds);
+    cur.y += (float)(scale * dp[0]);
+    cur.z += (float)(scale * dp[1]);
+    cur.w += (float)(scale * dp[2]);
+    *o = cur;
+  }
+}
+
+}  // namespace ts
+
+using namespace ts;
+
+void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
+                     float* d_vert, double* loss, cudaStream_t st) {
+  cudaMemsetAsync(loss, 0, sizeof(double), st);
+  if (n <= 0) return;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_eikonal<<<blocks, 256, 0, st>>>(n, tet_set, R, sdf, deform, scale, d_vert, loss);
+}
+
+void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
+                                double* loss, cudaStream_t st) {
+  const int64_t n = R + 1, N = n * n * n;
+  cudaMemsetAsync(loss, 0, sizeof(double), st);
+  double *nv, *cnt, *an, *dm;
+  cudaMallocAsync(&nv, sizeof(double) * 3 * N, st);
+  cudaMallocAsync(&dm, sizeof(double) * 3 * N, st);
+  cudaMallocAsync(&cnt, sizeof(double) * N, st);
+  cudaMallocAsync(&an, sizeof(double) * N, st);
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_nc_vertex_normals<<<blocks, 256, 0, st>>>(N, R, sdf, deform, nv, cnt, an);
+  k_nc_edges<<<blocks, 256, 0, st>>>(N, R, nv, an, dm, loss);
+  k_nc_grad<<<blocks, 256, 0, st>>>(N, R, sdf, deform, cnt, dm, scale, d_vert);
+  cudaFreeAsync(nv, st);
+  cudaFreeAsync(dm, st);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(an, st);
+}

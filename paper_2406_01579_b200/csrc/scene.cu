@@ -1,0 +1,165 @@
+// scene.cu — K1 prefilter + compaction and K2 projection / splat setup.
+//
+// K1 replaces splat.prefilter (splat.py:66-69 -> alpha_max splat.py:42-55): one FP64
+//    alpha_max per tet of the implicit Kuhn grid, survivors emitted in increasing id.
+// K2 replaces splat.build_scene (splat.py:203-245): projection (camera.py:56-67), the
+//    frustum/image cull (splat.py:216-221), the in-tet gradient normal (field.py:140-177,
+//    cross-product form of _core.pyx:474-514), mean depth, bbox, alpha_max, and the
+//    compact FP32 compositing record — all fused into one order-preserving compaction.
+// Both are HBM-bound gathers: each thread owns one tet, vertex data is reused via L1/L2.
+#include "internal.cuh"
+#include "scan.cuh"
+
+namespace ts {
+
+// alpha_max >= threshold (splat.py:42-55), FP64 with numpy's operation order
+__device__ __forceinline__ bool alpha_max_pass(const double f[4], double s, double thr, double* amax_out) {
+  double fmx = f[0], fmn = f[0];
+  for (int i = 1; i < 4; ++i) {
+    fmx = f[i] > fmx ? f[i] : fmx;
+    fmn = f[i] < fmn ? f[i] : fmn;
+  }
+  double a = dmul(s, fmx), b = dmul(s, fmn);
+  double ratio = exp(dsub(softplus_d(-a), softplus_d(-b)));
+  double am = dsub(1.0, ratio);
+  am = am > 0.0 ? am : 0.0;
+  if (amax_out) *amax_out = am;
+  return am >= thr;
+}
+
+struct PrefilterF {
+  const double* sdf;
+  int R;
+  double s, thr;
+  int32_t* out;
+  __device__ bool pred(int64_t t) const {
+    int64_t v[4];
+    tet_vertices(t, R, v);
+    double f[4] = {sdf[v[0]], sdf[v[1]], sdf[v[2]], sdf[v[3]]};
+    return alpha_max_pass(f, s, thr, nullptr);
+  }
+  __device__ void emit(int64_t t, int64_t pos) const { out[pos] = (int32_t)t; }
+};
+
+
+struct CullF {
+  const int32_t* active;
+  const double* sdf;
+  const double* deform;
+  int R;
+  Camera cam;
+  double s;
+  SceneOut out;
+
+  __device__ void project4(int64_t i, int64_t v[4], double P[4][3], double px[4], double py[4],
+                           double z[4]) const {
+    tet_vertices((int64_t)active[i], R, v);
+    for (int c = 0; c < 4; ++c) {
+      double pc[3];
+      vertex_position(v[c], R, deform, P[c]);
+      project_point(cam, P[c], px[c], py[c], z[c], pc);
+    }
+  }
+  __device__ static void bounds(const double px[4], const double py[4], const double z[4], double& dmin,
+                                double& xmin, double& xmax, double& ymin, double& ymax) {
+    dmin = z[0]; xmin = xmax = px[0]; ymin = ymax = py[0];
+    for (int c = 1; c < 4; ++c) {
+      dmin = z[c] < dmin ? z[c] : dmin;
+      xmin = px[c] < xmin ? px[c] : xmin;
+      xmax = px[c] > xmax ? px[c] : xmax;
+      ymin = py[c] < ymin ? py[c] : ymin;
+      ymax = py[c] > ymax ? py[c] : ymax;
+    }
+  }
+  __device__ bool pred(int64_t i) const {
+    int64_t v[4];
+    double P[4][3], px[4], py[4], z[4];
+    project4(i, v, P, px, py, z);
+    double dmin, xmin, xmax, ymin, ymax;
+    bounds(px, py, z, dmin, xmin, xmax, ymin, ymax);
+    return (dmin > cam.near_) && (dmin <= cam.far_) && (xmax >= 0.0) && (xmin <= (double)cam.width) &&
+           (ymax >= 0.0) && (ymin <= (double)cam.height);
+  }
+  __device__ void emit(int64_t i, int64_t k) const {
+    int64_t v[4];
+    double P[4][3], px[4], py[4], z[4];
+    project4(i, v, P, px, py, z);
+    double dmin, xmin, xmax, ymin, ymax;
+    bounds(px, py, z, dmin, xmin, xmax, ymin, ymax);
+    double f[4], proj[8], bb[4] = {xmin, ymin, xmax, ymax};
+    for (int c = 0; c < 4; ++c) {
+      f[c] = sdf[v[c]];
+      proj[2 * c] = px[c];
+      proj[2 * c + 1] = py[c];
+      out.vert_ids[k * 4 + c] = (int32_t)v[c];
+      out.proj[k * 8 + 2 * c] = px[c];
+      out.proj[k * 8 + 2 * c + 1] = py[c];
+      out.depths[k * 4 + c] = z[c];
+      out.f[k * 4 + c] = f[c];
+      out.bbox[k * 4 + c] = bb[c];
+    }
+    out.tet_ids[k] = active[i];
+    double g[3], c1[3], c2[3], c3[3], nrm[3] = {0.0, 0.0, 0.0};
+    tet_gradient(P, f, g, c1, c2, c3);
+    double gn = sqrt(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
+    if (gn >= 1e-8)
+      for (int c = 0; c < 3; ++c) nrm[c] = ddiv(g[c], gn);
+    for (int c = 0; c < 3; ++c) out.normals[k * 3 + c] = nrm[c];
+    double md = ddiv(dadd(dadd(dadd(z[0], z[1]), z[2]), z[3]), 4.0);
+    out.md[k] = md;
+    double am;
+    alpha_max_pass(f, s, 0.0, &am);
+    out.amax[k] = am;
+    out.rec[k] = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height);
+  }
+};
+
+// Record preparation for a scene that arrived as FP64 arrays (e.g. uploaded).
+__global__ void k_prepare_records(int64_t K, const double* __restrict__ proj, const double* __restrict__ depths,
+                                  const double* __restrict__ f, const double* __restrict__ normals,
+                                  const double* __restrict__ md, const double* __restrict__ bbox, int width,
+                                  int height, SplatRec* __restrict__ rec) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    double p[8], z[4], ff[4], n[3], b[4];
+    for (int i = 0; i < 8; ++i) p[i] = proj[k * 8 + i];
+    for (int i = 0; i < 4; ++i) { z[i] = depths[k * 4 + i]; ff[i] = f[k * 4 + i]; b[i] = bbox[k * 4 + i]; }
+    for (int i = 0; i < 3; ++i) n[i] = normals[k * 3 + i];
+    rec[k] = make_record(p, z, ff, n, md[k], b, width, height);
+  }
+}
+
+}  // namespace ts
+
+using namespace ts;
+
+// host entry points used by abi.cu
+int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_t* out_active,
+                          int64_t* scratch, cudaStream_t st) {
+  const int64_t K = 6ll * R * R * R;
+  PrefilterF f{sdf, R, s, thr, out_active};
+  int64_t* d_total = compact(K, f, scratch, st);
+  int64_t h = 0;
+  cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return h;
+}
+
+int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, const Camera& cam, double s,
+                            const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
+                            cudaStream_t st) {
+  CullF f{active, sdf, deform, R, cam, s, out};
+  int64_t* d_total = compact(n_active, f, scratch, st);
+  int64_t h = 0;
+  cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return h;
+}
+
+void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths, const double* f,
+                             const double* normals, const double* md, const double* bbox, int width, int height,
+                             SplatRec* rec, cudaStream_t st) {
+  if (K <= 0) return;
+  int blocks = (int)((K + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_prepare_records<<<blocks, 256, 0, st>>>(K, proj, depths, f, normals, md, bbox, width, height, rec);
+}

@@ -1,0 +1,68 @@
+"""Eikonal and normal-consistency regularizers + MSE map losses (mirrors losses.py)."""
+from __future__ import annotations
+
+import torch
+
+from . import _native
+from .raster import GradientBuffers, RenderMaps
+
+
+def eikonal_loss(grid, field, tet_set, out: GradientBuffers | None = None, scale: float = 1.0,
+                 stream=None) -> tuple[float, GradientBuffers]:
+    """sum_k (|g_k| - 1)^2 over `tet_set` (losses.py:25-36).  Gradients (times `scale`)
+    are accumulated into `out` when given (the fit loop's lambda weighting fused)."""
+    dev = field.sdf.device
+    out = out if out is not None else GradientBuffers.zeros(grid.num_vertices, dev)
+    tet_set = torch.as_tensor(tet_set, device=dev).to(torch.int32).contiguous()
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    if tet_set.numel() == 0:
+        return 0.0, out
+    _native.check(_native.lib().ts_eikonal(_native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution,
+                                           _native.ptr(tet_set), int(tet_set.numel()), float(scale),
+                                           _native.ptr(out.d_vert), _native.ptr(loss), _native.stream_ptr(stream)))
+    return float(loss.item()), out
+
+
+def eikonal_loss_async(grid, field, tet_set, out, scale, loss, stream=None):
+    """Sync-free variant: loss (device f64[1]) is overwritten, gradients accumulated."""
+    _native.check(_native.lib().ts_eikonal(_native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution,
+                                           _native.ptr(tet_set), int(tet_set.numel()), float(scale),
+                                           _native.ptr(out.d_vert), _native.ptr(loss), _native.stream_ptr(stream)))
+
+
+def normal_consistency_loss(grid, field, out: GradientBuffers | None = None, scale: float = 1.0,
+                            stream=None) -> tuple[float, GradientBuffers]:
+    """Cosine misalignment between vertex normals across grid edges (losses.py:39-52)."""
+    dev = field.sdf.device
+    out = out if out is not None else GradientBuffers.zeros(grid.num_vertices, dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    normal_consistency_loss_async(grid, field, out, scale, loss, stream)
+    return float(loss.item()), out
+
+
+def normal_consistency_loss_async(grid, field, out, scale, loss, stream=None):
+    _native.check(_native.lib().ts_normal_consistency(_native.ptr(field.sdf), _native.ptr(field.deformation),
+                                                      grid.resolution, float(scale), _native.ptr(out.d_vert),
+                                                      _native.ptr(loss), _native.stream_ptr(stream)))
+
+
+def map_mse_loss(rendered: RenderMaps, target: RenderMaps, weights: dict):
+    """losses.py:55-81: weighted per-map MSE and the exact gradient images."""
+    if rendered.opacity.shape != target.opacity.shape:
+        raise ValueError("rendered/target map shapes differ")
+    npix = rendered.opacity.numel()
+    comps, total = {}, 0.0
+    grads = RenderMaps.zeros(*rendered.opacity.shape, with_color=rendered.color is not None,
+                             device=rendered.opacity.device)
+    pairs = [("normal", rendered.normal, target.normal), ("depth", rendered.depth, target.depth),
+             ("opacity", rendered.opacity, target.opacity)]
+    if rendered.color is not None and target.color is not None:
+        pairs.append(("color", rendered.color, target.color))
+    for name, r, t in pairs:
+        diff = r - torch.as_tensor(t, device=r.device, dtype=r.dtype)
+        mse = float((diff * diff).sum()) / npix
+        comps[f"mse_{name}"] = mse
+        w = float(weights.get(name, 1.0))
+        total += w * mse
+        setattr(grads, name, (2.0 / npix) * w * diff)
+    return total, comps, grads

@@ -1,0 +1,235 @@
+"""Tile-based forward rasterizer and analytic backward pass (mirrors raster.py).
+
+All work runs in the sm_100a kernels of libtetsplat_b200.so (csrc/bin.cu, composite.cu);
+this module owns the device buffers and keeps the reference's call signatures.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .splat import ALPHA_CLIP, T_STOP, SplatScene
+
+TILE_SIZE = 16
+DEFAULT_WINDOW = 5
+
+
+@dataclass
+class RenderMaps:
+    """Opacity-premultiplied normal/depth/opacity (and optional color) images, FP32 on the
+    device (raster.py:29-50)."""
+
+    normal: torch.Tensor
+    depth: torch.Tensor
+    opacity: torch.Tensor
+    color: torch.Tensor | None = None
+
+    @classmethod
+    def zeros(cls, height, width, with_color=False, device="cuda"):
+        f = dict(dtype=torch.float32, device=device)
+        return cls(torch.zeros((height, width, 3), **f), torch.zeros((height, width), **f),
+                   torch.zeros((height, width), **f),
+                   torch.zeros((height, width, 3), **f) if with_color else None)
+
+    @classmethod
+    def empty(cls, height, width, with_color=False, device="cuda"):
+        f = dict(dtype=torch.float32, device=device)
+        return cls(torch.empty((height, width, 3), **f), torch.empty((height, width), **f),
+                   torch.empty((height, width), **f),
+                   torch.empty((height, width, 3), **f) if with_color else None)
+
+    def max_abs_difference(self, other: "RenderMaps") -> float:
+        d = max(float((self.normal - other.normal).abs().max()), float((self.depth - other.depth).abs().max()),
+                float((self.opacity - other.opacity).abs().max()))
+        if self.color is not None and other.color is not None:
+            d = max(d, float((self.color - other.color).abs().max()))
+        return d
+
+    def numpy(self):
+        c = lambda t: None if t is None else t.detach().cpu().numpy().astype(np.float64)
+        return c(self.normal), c(self.depth), c(self.opacity), c(self.color)
+
+
+@dataclass
+class TileBins:
+    """Per-tile splat lists sorted by (tile id, quantized mean depth) (raster.py:53-71).
+
+    starts/items equal the reference's bit for bit; pos_of, splat_off, nonmono and witems
+    are the B200 extras (deterministic gradient gather, resorting window)."""
+
+    tile_size: int
+    tiles_x: int
+    tiles_y: int
+    starts: torch.Tensor     # (T+1,) int64
+    items: torch.Tensor      # (M,) int32
+    splat_off: torch.Tensor  # (K+1,) int64
+    pos_of: torch.Tensor     # (M,) int32
+    nonmono: torch.Tensor    # (T,) uint8
+    witems: torch.Tensor     # (M,) int32
+    max_len: int = 0
+
+    @property
+    def num_tiles(self) -> int:
+        return self.tiles_x * self.tiles_y
+
+    @property
+    def num_pairs(self) -> int:
+        return int(self.items.shape[0])
+
+    def tile_list(self, tid: int) -> torch.Tensor:
+        s = self.starts[tid:tid + 2].tolist()
+        return self.items[s[0]:s[1]]
+
+    def max_list_length(self) -> int:
+        return self.max_len
+
+    def abi(self) -> _native.ts_bins:
+        b = _native.ts_bins()
+        for n in ("starts", "splat_off", "items", "pos_of", "nonmono", "witems"):
+            setattr(b, n, getattr(self, n).data_ptr())
+        return b
+
+
+@dataclass
+class GradientBuffers:
+    """Loss derivatives per grid vertex (raster.py:74-91).  Stored interleaved as one FP32
+    [N,4] buffer (d_sdf, d_deform xyz) — the all-reduce payload; d_sdf/d_deform are views."""
+
+    d_vert: torch.Tensor
+    d_color: torch.Tensor | None = None
+
+    @classmethod
+    def zeros(cls, num_vertices, device="cuda", num_tets_color: int | None = None):
+        return cls(torch.zeros((num_vertices, 4), dtype=torch.float32, device=device),
+                   None if num_tets_color is None else
+                   torch.zeros((num_tets_color, 3), dtype=torch.float32, device=device))
+
+    @property
+    def d_sdf(self) -> torch.Tensor:
+        return self.d_vert[:, 0]
+
+    @property
+    def d_deform(self) -> torch.Tensor:
+        return self.d_vert[:, 1:]
+
+    def __iadd__(self, other):
+        self.d_vert += other.d_vert
+        if self.d_color is not None and other.d_color is not None:
+            self.d_color += other.d_color
+        return self
+
+    def scaled(self, w: float) -> "GradientBuffers":
+        return GradientBuffers(self.d_vert * w, None if self.d_color is None else self.d_color * w)
+
+
+@dataclass
+class SavedState:
+    """What the backward needs from the forward (raster.py:94-101).  Instead of per-pixel
+    (idx, alpha) lists the B200 forward keeps the number of list entries each pixel
+    consumed and its final composite (the forward maps)."""
+
+    bins: TileBins
+    n_w: int
+    t_stop: float
+    maps: RenderMaps
+    n_proc: torch.Tensor   # (H,W) int32
+    n_blend: torch.Tensor  # (H,W) int32 — the reference's per-pixel record counts
+
+
+def bin_and_sort(scene: SplatScene, camera, tile_size: int = TILE_SIZE, stream=None) -> TileBins:
+    """Replicate splats into overlapped tiles and sort by (tile id, depth) (raster.py:104-141)."""
+    if tile_size != TILE_SIZE:
+        raise ValueError("the B200 rasterizer uses 16x16 tiles (one 256-thread CTA per tile)")
+    L = _native.lib()
+    dev = scene.mean_depth.device
+    tiles_x = (camera.width + tile_size - 1) // tile_size
+    tiles_y = (camera.height + tile_size - 1) // tile_size
+    T = tiles_x * tiles_y
+    K = len(scene)
+    starts = torch.zeros(T + 1, dtype=torch.int64, device=dev)
+    splat_off = torch.zeros(K + 1, dtype=torch.int64, device=dev)
+    nonmono = torch.zeros(T, dtype=torch.uint8, device=dev)
+    if K == 0:
+        e = torch.zeros(0, dtype=torch.int32, device=dev)
+        return TileBins(tile_size, tiles_x, tiles_y, starts, e, splat_off, e, nonmono, e, 0)
+    cam = camera.abi()
+    sp = _native.stream_ptr(stream)
+    M, maxL = _native.i64(), _native.i64()
+    _native.check(L.ts_bin_count(_native.ptr(scene.bbox), _native.ptr(scene.mean_depth), K, cam, tile_size,
+                                 _native.ptr(starts), _native.ptr(splat_off), M, maxL, sp))
+    M = M.value
+    buf = torch.empty(3 * max(M, 1), dtype=torch.int32, device=dev)
+    bins = TileBins(tile_size, tiles_x, tiles_y, starts, buf[:M], splat_off, buf[M:2 * M], nonmono,
+                    buf[2 * M:3 * M] if M else buf[:0], maxL.value)
+    if M:
+        _native.check(L.ts_bin_sort(_native.ptr(scene.bbox), _native.ptr(scene.mean_depth), K, cam, tile_size,
+                                    bins.abi(), M, bins.max_len, sp))
+    return bins
+
+
+def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT_WINDOW, t_stop: float = T_STOP,
+                   save_state: bool = False, stream=None):
+    """Tile-based forward pass (raster.py:149-177).  Returns (RenderMaps, SavedState | None)."""
+    if n_w < 1:
+        raise ValueError("resorting window must be >= 1")
+    L = _native.lib()
+    dev = scene.mean_depth.device
+    H, W = camera.height, camera.width
+    with_color = scene.colors is not None
+    maps = RenderMaps.empty(H, W, with_color, dev)
+    n_proc = torch.empty((H, W), dtype=torch.int32, device=dev)
+    n_blend = torch.empty((H, W), dtype=torch.int32, device=dev)
+    K = len(scene)
+    if K == 0 or bins.num_pairs == 0:
+        for t in (maps.normal, maps.depth, maps.opacity, maps.color, n_proc, n_blend):
+            if t is not None:
+                t.zero_()
+    else:
+        _native.check(L.ts_render_forward(scene.abi(), K, _native.ptr(scene.colors), bins.abi(), bins.num_pairs,
+                                          camera.abi(), int(n_w), float(scene.steepness), float(t_stop),
+                                          _native.ptr(maps.normal), _native.ptr(maps.depth),
+                                          _native.ptr(maps.opacity), _native.ptr(maps.color),
+                                          _native.ptr(n_proc), _native.ptr(n_blend), _native.stream_ptr(stream)))
+    saved = SavedState(bins, n_w, t_stop, maps, n_proc, n_blend) if save_state else None
+    return maps, saved
+
+
+def _as_f32(t, dev):
+    if t is None:
+        return None
+    return torch.as_tensor(t, device=dev).to(torch.float32).contiguous()
+
+
+def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d_maps: RenderMaps,
+                    out: GradientBuffers | None = None, stream=None) -> GradientBuffers:
+    """Exact reverse-mode pass: map gradients -> per-vertex SDF/deformation gradients
+    (raster.py:206-306).  With `out`, gradients are accumulated into it (fused batch)."""
+    dev = scene.mean_depth.device
+    dn, dd, do = _as_f32(d_maps.normal, dev), _as_f32(d_maps.depth, dev), _as_f32(d_maps.opacity, dev)
+    for arr in (dn, dd, do):
+        if not bool(torch.isfinite(arr).all()):
+            raise ValueError("non-finite incoming map gradients")
+    with_color = scene.colors is not None and d_maps.color is not None
+    dc = _as_f32(d_maps.color, dev) if with_color else None
+    if out is None:
+        out = GradientBuffers.zeros(grid.num_vertices, dev, grid.num_tets if with_color else None)
+    K = len(scene)
+    if K == 0 or saved.bins.num_pairs == 0:
+        return out
+    L = _native.lib()
+    import ctypes
+    maps = (ctypes.c_void_p * 4)(saved.maps.normal.data_ptr(), saved.maps.depth.data_ptr(),
+                                 saved.maps.opacity.data_ptr(),
+                                 saved.maps.color.data_ptr() if with_color else None)
+    dmaps = (ctypes.c_void_p * 4)(dn.data_ptr(), dd.data_ptr(), do.data_ptr(), dc.data_ptr() if with_color else None)
+    _native.check(L.ts_render_backward(scene.abi(), K, _native.ptr(scene.colors), saved.bins.abi(),
+                                       saved.bins.num_pairs, camera.abi(), float(scene.steepness),
+                                       ctypes.cast(maps, ctypes.POINTER(ctypes.c_void_p)),
+                                       ctypes.cast(dmaps, ctypes.POINTER(ctypes.c_void_p)),
+                                       _native.ptr(saved.n_proc), _native.ptr(field.deformation), grid.resolution,
+                                       _native.ptr(out.d_vert), _native.ptr(out.d_color) if with_color else None,
+                                       _native.stream_ptr(stream)))
+    return out

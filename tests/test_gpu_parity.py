@@ -1,0 +1,160 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the golden fixtures of the
+reference and the CPU oracle on identical inputs.
+
+Bars (BASELINE.json north_star): bit-exact tile counts / sorted lists / active sets,
+rendered maps within 1e-4 relative, parameter gradients within 1e-3 relative, where
+relative = max|gpu - ref| / max|ref| (gradcheck.py:136-137).
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import RENDER_CASES, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+MAP_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def ts():
+    import paper_2406_01579_b200 as ts
+    from paper_2406_01579_b200 import _native
+    _native.lib()  # fail loudly when the CUDA library or the device is missing
+    return ts
+
+
+def _setup(ts, G):
+    g = ts.build_grid(int(G["R"]))
+    fs = ts.FieldState.from_numpy(G["sdf"], G["deform"], ts.deform_limit_for(g))
+    S = int(G["S"])
+    cam = ts.orbit_camera(int(G["cam_index"]), int(G["cam_count"]), width=S, height=S)
+    return g, fs, cam
+
+
+def _golden_scene(ts, G, cam, oracle_scene=None):
+    if oracle_scene is None:
+        return ts.scene_from_arrays(G["tet_ids"], G["vert_ids"], G["proj"], G["depths"], G["f"], G["normals"],
+                                    G["mean_depth"], G["alpha_max"], G["bbox"], float(G["s"]), cam)
+    o = oracle_scene
+    return ts.scene_from_arrays(o.tet_ids, o.vert_ids, o.proj, o.depths, o.f, o.normals, o.mean_depth,
+                                o.alpha_max, o.bbox, float(G["s"]), cam)
+
+
+def _oracle_scene(G):
+    from oracle import ts_oracle as O
+    g = O.build_grid(int(G["R"]))
+    fs = O.FieldState(G["sdf"], G["deform"], O.DEFORM_FRACTION * g.cell_edge)
+    S = int(G["S"])
+    cam = O.orbit_camera(int(G["cam_index"]), int(G["cam_count"]), width=S, height=S)
+    return O.build_scene(g, fs, cam, float(G["s"]), active=G["active"])
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_prefilter_bitexact(ts, case):
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    active = ts.prefilter(g, fs, float(G["s"]))
+    assert np.array_equal(active.cpu().numpy().astype(np.int64), G["active"])
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_build_scene(ts, case):
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    sc = ts.build_scene(g, fs, cam, float(G["s"]), active=torch.as_tensor(G["active"]).cuda())
+    assert np.array_equal(sc.tet_ids.cpu().numpy(), G["tet_ids"])
+    md = sc.mean_depth.cpu().numpy()
+    assert np.abs(md - G["mean_depth"]).max() <= 1e-12
+    assert np.abs(sc.bbox.cpu().numpy() - G["bbox"]).max() <= 1e-9
+    if "normals" in G:
+        assert np.abs(sc.normals.cpu().numpy() - G["normals"]).max() <= 1e-9
+        assert np.abs(sc.alpha_max.cpu().numpy() - G["alpha_max"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_bins_bitexact(ts, case):
+    """Stage-level: the reference's own FP64 scene -> identical starts/items."""
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    sc = _golden_scene(ts, G, cam, None if "proj" in G else _oracle_scene(G))
+    b = ts.bin_and_sort(sc, cam)
+    assert np.array_equal(b.starts.cpu().numpy(), G["starts"])
+    assert np.array_equal(b.items.cpu().numpy().astype(np.int64), G["items"])
+    # pos_of is the inverse of the (splat, tile) duplication
+    pos = b.pos_of.cpu().numpy()
+    assert np.array_equal(np.sort(pos), np.arange(len(pos)))
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_forward_backward_stage_parity(ts, case):
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    osc = None if "proj" in G else _oracle_scene(G)
+    sc = _golden_scene(ts, G, cam, osc)
+    b = ts.bin_and_sort(sc, cam)
+    maps, saved = ts.render_forward(sc, b, cam, n_w=5, save_state=True)
+    n, d, o, _ = maps.numpy()
+    assert rel_err(n, G["normal"]) < MAP_TOL
+    assert rel_err(d, G["depth"]) < MAP_TOL
+    assert rel_err(o, G["opacity"]) < MAP_TOL
+    counts = saved.n_blend.cpu().numpy()
+    mism = int((counts != G["counts"]).sum())
+    assert mism == 0, f"{mism} pixels blend a different number of records"
+    if "d_normal" in G:
+        dm = ts.RenderMaps(G["d_normal"], G["d_depth"], G["d_opacity"])
+    else:
+        from oracle import ts_oracle as O
+        S = int(G["S"])
+        w = O.synthetic_dmaps(S, S)
+        dm = ts.RenderMaps(w.normal, w.depth, w.opacity)
+    gb = ts.render_backward(saved, sc, g, fs, cam, dm)
+    assert rel_err(gb.d_sdf.cpu().numpy(), G["d_sdf"]) < GRAD_TOL
+    assert rel_err(gb.d_deform.cpu().numpy(), G["d_deform"]) < GRAD_TOL
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_end_to_end(ts, case):
+    """Field -> GPU prefilter/scene/bins/forward/backward, compared with the reference."""
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    s = float(G["s"])
+    sc = ts.build_scene(g, fs, cam, s)
+    b = ts.bin_and_sort(sc, cam)
+    maps, saved = ts.render_forward(sc, b, cam, save_state=True)
+    n, d, o, _ = maps.numpy()
+    assert rel_err(n, G["normal"]) < MAP_TOL
+    assert rel_err(d, G["depth"]) < MAP_TOL
+    assert rel_err(o, G["opacity"]) < MAP_TOL
+    if "d_normal" in G:
+        dm = ts.RenderMaps(G["d_normal"], G["d_depth"], G["d_opacity"])
+        gb = ts.render_backward(saved, sc, g, fs, cam, dm)
+        assert rel_err(gb.d_sdf.cpu().numpy(), G["d_sdf"]) < GRAD_TOL
+        assert rel_err(gb.d_deform.cpu().numpy(), G["d_deform"]) < GRAD_TOL
+
+
+@pytest.mark.parametrize("case", [c for c in RENDER_CASES])
+def test_regularizers(ts, case):
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    le, ge = ts.eikonal_loss(g, fs, G["active"])
+    ln, gn = ts.normal_consistency_loss(g, fs)
+    assert abs(le - float(G["eik_loss"])) <= 1e-9 * max(1.0, abs(float(G["eik_loss"])))
+    assert abs(ln - float(G["nc_loss"])) <= 1e-9 * max(1.0, abs(float(G["nc_loss"])))
+    assert rel_err(ge.d_sdf.cpu().numpy(), G["eik_d_sdf"]) < 1e-6
+    assert rel_err(ge.d_deform.cpu().numpy(), G["eik_d_deform"]) < 1e-6
+    assert rel_err(gn.d_sdf.cpu().numpy(), G["nc_d_sdf"]) < 1e-6
+    assert rel_err(gn.d_deform.cpu().numpy(), G["nc_d_deform"]) < 1e-6
+
+
+def test_window_sizes_agree_on_monotone_lists(ts):
+    G = load_golden("render_sphere_r16_s100.npz")
+    g, fs, cam = _setup(ts, G)
+    sc = _golden_scene(ts, G, cam)
+    b = ts.bin_and_sort(sc, cam)
+    m1, _ = ts.render_forward(sc, b, cam, n_w=1)
+    m9, _ = ts.render_forward(sc, b, cam, n_w=9)
+    assert torch.equal(m1.normal, m9.normal)
+    with pytest.raises(ValueError):
+        ts.render_forward(sc, b, cam, n_w=0)
