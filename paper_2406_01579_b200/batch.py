@@ -1,0 +1,126 @@
+"""Multi-view fit step on the device, view-sharded across GPUs (fit.py:145-231 hot path).
+
+One iteration = prefilter (K1) once, then per view: build_scene (K2) -> bin_and_sort
+(K3-K5) -> render_forward (K6) -> render_backward (K7) accumulating into one FP32 [N,4]
+gradient buffer; eikonal + normal consistency (K8) fused into the same buffer with their
+lambda weights; then one NCCL all-reduce of that buffer across ranks (views are
+partitioned, parameters replicated — SURVEY.md §8e) and an identical Adam step on every
+rank (fit.py:70-90), followed by the deformation clamp (field.py:40-42).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field as dc_field
+
+import torch
+import torch.distributed as dist
+
+from .losses import eikonal_loss_async, normal_consistency_loss_async
+from .raster import GradientBuffers, RenderMaps, bin_and_sort, render_backward, render_forward
+from .splat import EmptySceneError, build_scene, prefilter
+
+
+def shard_views(n_views: int, rank: int, world: int) -> list[int]:
+    """Contiguous partition of view indices over ranks (the first n % world ranks take one
+    extra view); the union over ranks is range(n_views) exactly once."""
+    base, extra = divmod(n_views, world)
+    lo = rank * base + min(rank, extra)
+    return list(range(lo, lo + base + (1 if rank < extra else 0)))
+
+
+def allreduce_gradients(grads: GradientBuffers, group=None) -> None:
+    """Sum the per-rank vertex gradients (the only data-path collective)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(grads.d_vert, op=dist.ReduceOp.SUM, group=group)
+        if grads.d_color is not None:
+            dist.all_reduce(grads.d_color, op=dist.ReduceOp.SUM, group=group)
+
+
+class Adam:
+    """fit.py:70-90 on the device (FP64 moments, like the reference)."""
+
+    def __init__(self, params, lrs, betas=(0.9, 0.99), eps=1e-8):
+        self.lrs = list(lrs)
+        self.b1, self.b2 = betas
+        self.eps = eps
+        self.t = 0
+        self.m = [torch.zeros_like(p) for p in params]
+        self.v = [torch.zeros_like(p) for p in params]
+
+    @torch.no_grad()
+    def step(self, params, grads):
+        self.t += 1
+        c1 = 1 - self.b1 ** self.t
+        c2 = 1 - self.b2 ** self.t
+        for p, g, m, v, lr in zip(params, grads, self.m, self.v, self.lrs):
+            g = g.to(p.dtype)
+            m.mul_(self.b1).add_(g, alpha=1 - self.b1)
+            v.mul_(self.b2).addcmul_(g, g, value=1 - self.b2)
+            p.addcdiv_(m / c1, (v / c2).sqrt_().add_(self.eps), value=-lr)
+
+
+@dataclass
+class StepConfig:
+    n_w: int = 5
+    lambda_eik: float = 1000.0
+    lambda_nc: float = 1000.0
+    lr_sdf: float = 1e-2
+    lr_deform: float = 1e-3
+    betas: tuple = (0.9, 0.99)
+    optimizer: bool = True
+
+
+@dataclass
+class StepStats:
+    views: int = 0
+    splats: list = dc_field(default_factory=list)
+    pairs: list = dc_field(default_factory=list)
+    active: int = 0
+
+
+class FitStep:
+    """Runs fwd+bwd for this rank's views; `d_maps_fn(view_index, maps)` returns dL/dmaps."""
+
+    def __init__(self, grid, field, cameras, cfg: StepConfig | None = None, group=None):
+        self.grid, self.field, self.cameras = grid, field, cameras
+        self.cfg = cfg or StepConfig()
+        self.group = group
+        dev = field.sdf.device
+        self.grads = GradientBuffers.zeros(grid.num_vertices, dev)
+        self.eik_loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.nc_loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.opt = Adam([field.sdf, field.deformation], [self.cfg.lr_sdf, self.cfg.lr_deform], self.cfg.betas) \
+            if self.cfg.optimizer else None
+
+    def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None):
+        g, f, cfg = self.grid, self.field, self.cfg
+        self.grads.d_vert.zero_()
+        active = prefilter(g, f, s)
+        if active.numel() == 0:
+            raise EmptySceneError("pre-filtering removed every tetrahedron")
+        if stats is not None:
+            stats.active = int(active.numel())
+        for vi in views:
+            cam = self.cameras[vi]
+            scene = build_scene(g, f, cam, s, active=active)
+            if len(scene) == 0:
+                continue
+            bins = bin_and_sort(scene, cam)
+            maps, saved = render_forward(scene, bins, cam, n_w=cfg.n_w, save_state=True)
+            render_backward(saved, scene, g, f, cam, d_maps_fn(vi, maps), out=self.grads)
+            if stats is not None:
+                stats.views += 1
+                stats.splats.append(len(scene))
+                stats.pairs.append(bins.num_pairs)
+        # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce)
+        rank0 = not (dist.is_available() and dist.is_initialized()) or dist.get_rank(self.group) == 0
+        if rank0:
+            if cfg.lambda_eik > 0:
+                eikonal_loss_async(g, f, active, self.grads, cfg.lambda_eik, self.eik_loss)
+            if cfg.lambda_nc > 0:
+                normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss)
+        allreduce_gradients(self.grads, self.group)
+        if self.opt is not None:
+            self.opt.step([f.sdf, f.deformation], [self.grads.d_sdf, self.grads.d_deform])
+            f.clamp_deformation()
+        return self.grads

@@ -170,7 +170,7 @@ int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const 
   BinsView bv = bv_of(b);
   ts_impl_window(tx * ty, bv, M, sc->mean_depth, n_w, st);
   ts_impl_forward(tx, ty, bv, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
-                  cam->height, (float)s, (float)t_stop, nmap, dmap, omap, cmap, n_proc, n_blend, st);
+                  cam->height, s, (float)t_stop, nmap, dmap, omap, cmap, n_proc, n_blend, st);
   return check_cuda("ts_render_forward");
 }
 
@@ -187,7 +187,7 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
   const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
   ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc),
-                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), (float)s, m4, d4, n_proc, d_vert, d_color,
+                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), s, m4, d4, n_proc, d_vert, d_color,
                    ST(stream));
   return check_cuda("ts_render_backward");
 }

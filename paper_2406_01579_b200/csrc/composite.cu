@@ -44,7 +44,7 @@ struct __align__(16) Staged {
   float iz[4], f[4];
   float eux[4], euy[4], cu[4], evx[4], evy[4], cv[4], adet[4];
   float n[3];
-  float pad;
+  float ftol;  // |f_prev - f_next| below this: the sign of alpha is decided in FP64
 };
 static_assert(sizeof(Staged) == 192, "Staged must be 192 bytes");
 
@@ -83,6 +83,15 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
     s.cv[fi] = -(evx * vx[ia] + evy * vy[ia]);
     s.adet[fi] = fabsf(det);
   }
+  // error bound of FP32 f_hit: edge-function error (band/16) over |det|, times depth ratio
+  float fmax = fmaxf(fmaxf(fabsf(s.f[0]), fabsf(s.f[1])), fmaxf(fabsf(s.f[2]), fabsf(s.f[3])));
+  float izmin = fminf(fminf(s.iz[0], s.iz[1]), fminf(s.iz[2], s.iz[3]));
+  float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
+  float admin = 3.4e38f;
+#pragma unroll
+  for (int fi = 0; fi < 4; ++fi)
+    if ((s.flags >> fi) & 1u) admin = fminf(admin, s.adet[fi]);
+  s.ftol = (3.0f * s.band * (izmax / izmin) / admin + 1e-6f) * fmax;
 }
 
 struct Hit {
@@ -123,30 +132,79 @@ __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hi
   return 1;
 }
 
-__device__ __noinline__ int exact_hits(const Scene64& S, int k, int xi, int yi, Hit& h) {
-  double fp, fn;
-  int a, b;
-  int r = splat_hits_exact(S, k, xi + 0.5, yi + 0.5, fp, fn, a, b);
-  if (r) { h.fp = (float)fp; h.fn = (float)fn; h.fip = a; h.fin = b; }
-  return r;
-}
-
 __device__ __forceinline__ float softplus_tail(float x) { return log1pf(expf(-fabsf(x))); }
 
-// alpha = 1 - exp(sp(-s fp) - sp(-s fn)) (_core.pyx:35-36), clip at ALPHA_CLIP (_core.pyx:193-196)
-__device__ __forceinline__ bool alpha_of(float fp, float fn, float s, float& a, float& om, bool& clipped) {
-  float x = -s * fp, y = -s * fn;
-  float d;
-  if (x > 0.f && y > 0.f)
-    d = s * (fn - fp) + (softplus_tail(x) - softplus_tail(y));
-  else
-    d = (fmaxf(x, 0.f) + softplus_tail(x)) - (fmaxf(y, 0.f) + softplus_tail(y));
-  float a_un = -expm1f(d);
-  if (!(a_un > 0.f)) return false;
-  clipped = a_un > kAlphaClipF;
-  if (clipped) { a = kAlphaClipF; om = kOneMinusClipF; }
-  else { a = a_un; om = expf(d); }
+// Outcome of one (pixel, splat) pair: whether it blends, and the values the blend uses.
+struct Blend {
+  float fp, fn;  // SDF at entry / exit
+  int fip, fin;  // entry / exit faces
+  float a, om;   // clipped alpha and 1 - alpha
+  bool clipped;  // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
+};
+
+// Exact replica of the reference decision chain in FP64 (_core.pyx:67-95, 35-36, 190-196).
+__device__ __noinline__ bool blend_exact(const Scene64& S, int k, int xi, int yi, double s, Blend& b) {
+  double fp, fn;
+  int i0, i1;
+  if (!splat_hits_exact(S, k, xi + 0.5, yi + 0.5, fp, fn, i0, i1)) return false;
+  double d = dsub(softplus_d(dmul(-s, fp)), softplus_d(dmul(-s, fn)));
+  double a = dsub(1.0, exp(d));
+  if (a <= 0.0) return false;
+  b.fp = (float)fp;
+  b.fn = (float)fn;
+  b.fip = i0;
+  b.fin = i1;
+  b.clipped = a > 1.0 - 1e-4;
+  if (b.clipped) {
+    b.a = kAlphaClipF;
+    b.om = kOneMinusClipF;
+  } else {
+    b.a = (float)a;
+    b.om = (float)exp(d);
+  }
   return true;
+}
+
+// FP32 fast path with error-bounded decisions; anything within the bounds of a decision
+// threshold (face edges, alpha == 0, alpha == ALPHA_CLIP, FP32 underflow) is re-decided
+// by blend_exact so the blended set matches the FP64 reference.
+__device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, int xi, int yi, float s, double s64,
+                                         const Scene64& S, Blend& b) {
+  Hit h;
+  const int e = eval_hits(r, px, py, h);
+  if (e == 0) return false;
+  if (e == 1) {
+    const float df = h.fp - h.fn;
+    if (df < -r.ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
+    const float x = -s * h.fp, y = -s * h.fn;
+    if (df > r.ftol && !(x < -700.f && y < -700.f)) {
+      float d;
+      if (x > 0.f && y > 0.f)
+        d = s * (h.fn - h.fp) + (softplus_tail(x) - softplus_tail(y));
+      else
+        d = (fmaxf(x, 0.f) + softplus_tail(x)) - (fmaxf(y, 0.f) + softplus_tail(y));
+      const float a_un = -expm1f(d);
+      if (fabsf(a_un - kAlphaClipF) > 2e-6f) {
+        b.fp = h.fp;
+        b.fn = h.fn;
+        b.fip = h.fip;
+        b.fin = h.fin;
+        b.clipped = a_un > kAlphaClipF;
+        if (b.clipped) {
+          b.a = kAlphaClipF;
+          b.om = kOneMinusClipF;
+        } else if (a_un > 0.f) {
+          b.a = a_un;
+          b.om = expf(d);
+        } else {  // FP32 underflow of a positive FP64 alpha (< 1e-38): blends as zero
+          b.a = 0.f;
+          b.om = 1.f;
+        }
+        return true;
+      }
+    }
+  }
+  return blend_exact(S, r.k, xi, yi, s64, b);
 }
 
 __device__ __forceinline__ float sigmoidf_stable(float x) {
@@ -179,7 +237,7 @@ template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-    Scene64 S64, int tiles_x, int W, int H, float s, float t_stop, float* __restrict__ normal_map,
+    Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, float* __restrict__ normal_map,
     float* __restrict__ depth_map, float* __restrict__ opacity_map, float* __restrict__ color_map,
     int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
   __shared__ Staged sh[kChF];
@@ -210,15 +268,10 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
         const Staged& r = sh[j];
         if (xi < r.rx0 || xi > r.rx1 || yi < r.ry0 || yi > r.ry1) continue;
         const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-        Hit h;
-        int e = eval_hits(r, px, py, h);
-        if (e == 2) e = exact_hits(S64, r.k, xi, yi, h);
-        if (!e) continue;
-        float a, om;
-        bool cl;
-        if (!alpha_of(h.fp, h.fn, s, a, om, cl)) continue;
-        acc.add(__fmul_rn(T, a), r, COLOR ? shc[j] : nullptr);
-        T = __fmul_rn(T, om);
+        Blend bl;
+        if (!blend_of(r, px, py, xi, yi, s, s64, S64, bl)) continue;
+        acc.add(__fmul_rn(T, bl.a), r, COLOR ? shc[j] : nullptr);
+        T = __fmul_rn(T, bl.om);
         ++nb;
         if (T < t_stop) {
           done = true;
@@ -328,7 +381,7 @@ template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX) k_backward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-    Scene64 S64, int tiles_x, int W, int H, float s, const float* __restrict__ normal_map,
+    Scene64 S64, int tiles_x, int W, int H, float s, double s64, const float* __restrict__ normal_map,
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
@@ -387,15 +440,11 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_backward(
       bool contrib = false;
       if (base + j < nproc && xi >= r.rx0 && xi <= r.rx1 && yi >= r.ry0 && yi <= r.ry1) {
         const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-        Hit h;
-        int e = eval_hits(r, px, py, h);
-        if (e == 2) e = exact_hits(S64, r.k, xi, yi, h);
-        float a, om;
-        bool cl;
-        if (e && alpha_of(h.fp, h.fn, s, a, om, cl)) {
+        Blend bl;
+        if (blend_of(r, px, py, xi, yi, s, s64, S64, bl)) {
           contrib = true;
           const float* col = COLOR ? shc[j] : nullptr;
-          const float w = __fmul_rn(T, a);
+          const float w = __fmul_rn(T, bl.a);
           P.add(w, r, col);
           gr[19] = g_d * w;
           gr[16] = g_n[0] * w;
@@ -406,26 +455,26 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_backward(
             gr[21] = g_c[1] * w;
             gr[22] = g_c[2] * w;
           }
-          if (!cl) {
-            const float Tom = T * om;
+          if (!bl.clipped) {
+            const float Tom = T * bl.om;
             float G = g_o * (Tom - (C_o - P.o)) + g_d * (Tom * r.md - (C_d - P.d));
 #pragma unroll
             for (int i = 0; i < 3; ++i) G += g_n[i] * (Tom * r.n[i] - (C_n[i] - P.n[i]));
             if (COLOR)
 #pragma unroll
               for (int i = 0; i < 3; ++i) G += g_c[i] * (Tom * col[i] - (C_c[i] - P.c[i]));
-            const float dfp = G * s * sigmoidf_stable(-s * h.fp);
-            const float dfn = -G * s * sigmoidf_stable(-s * h.fn);
-            const float g0 = (h.fip == 0 ? dfp : 0.f) + (h.fin == 0 ? dfn : 0.f);
-            const float g1 = (h.fip == 1 ? dfp : 0.f) + (h.fin == 1 ? dfn : 0.f);
-            const float g2 = (h.fip == 2 ? dfp : 0.f) + (h.fin == 2 ? dfn : 0.f);
-            const float g3 = (h.fip == 3 ? dfp : 0.f) + (h.fin == 3 ? dfn : 0.f);
-            if (h.fip == 0 || h.fin == 0) face_bwd<0>(r, px, py, g0, gr);
-            if (h.fip == 1 || h.fin == 1) face_bwd<1>(r, px, py, g1, gr);
-            if (h.fip == 2 || h.fin == 2) face_bwd<2>(r, px, py, g2, gr);
-            if (h.fip == 3 || h.fin == 3) face_bwd<3>(r, px, py, g3, gr);
+            const float dfp = G * s * sigmoidf_stable(-s * bl.fp);
+            const float dfn = -G * s * sigmoidf_stable(-s * bl.fn);
+            const float g0 = (bl.fip == 0 ? dfp : 0.f) + (bl.fin == 0 ? dfn : 0.f);
+            const float g1 = (bl.fip == 1 ? dfp : 0.f) + (bl.fin == 1 ? dfn : 0.f);
+            const float g2 = (bl.fip == 2 ? dfp : 0.f) + (bl.fin == 2 ? dfn : 0.f);
+            const float g3 = (bl.fip == 3 ? dfp : 0.f) + (bl.fin == 3 ? dfn : 0.f);
+            if (bl.fip == 0 || bl.fin == 0) face_bwd<0>(r, px, py, g0, gr);
+            if (bl.fip == 1 || bl.fin == 1) face_bwd<1>(r, px, py, g1, gr);
+            if (bl.fip == 2 || bl.fin == 2) face_bwd<2>(r, px, py, g2, gr);
+            if (bl.fip == 3 || bl.fin == 3) face_bwd<3>(r, px, py, g3, gr);
           }
-          T = __fmul_rn(T, om);
+          T = __fmul_rn(T, bl.om);
         }
       }
       if (__any_sync(0xffffffffu, contrib)) {
@@ -541,20 +590,20 @@ void ts_impl_window(int T, const BinsView& b, int64_t M, const double* md, int n
 }
 
 void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec* rec, const float* colors,
-                     const Scene64& S64, int W, int H, float s, float t_stop, float* nmap, float* dmap, float* omap,
+                     const Scene64& S64, int W, int H, double s, float t_stop, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x, W,
-                                             H, s, t_stop, nmap, dmap, omap, cmap, n_proc, n_blend);
+                                             H, (float)s, s, t_stop, nmap, dmap, omap, cmap, n_proc, n_blend);
   else
     k_forward<false><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64, tiles_x,
-                                              W, H, s, t_stop, nmap, dmap, omap, nullptr, n_proc, n_blend);
+                                              W, H, (float)s, s, t_stop, nmap, dmap, omap, nullptr, n_proc, n_blend);
 }
 
 void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, int64_t K, const SplatRec* rec,
                       const float* colors, const Scene64& S64, const int32_t* vert_ids, const int32_t* tet_ids,
-                      const double* deform, int R, const Camera& cam, float s, const float* maps[4],
+                      const double* deform, int R, const Camera& cam, double s, const float* maps[4],
                       const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color,
                       cudaStream_t st) {
   const int T = tiles_x * tiles_y;
@@ -564,11 +613,11 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
     k_backward<true><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
-                                              cam.width, cam.height, s, maps[0], maps[1], maps[2], maps[3],
+                                              cam.width, cam.height, (float)s, s, maps[0], maps[1], maps[2], maps[3],
                                               dmaps[0], dmaps[1], dmaps[2], dmaps[3], n_proc, rows);
   else
     k_backward<false><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64, tiles_x,
-                                               cam.width, cam.height, s, maps[0], maps[1], maps[2], nullptr,
+                                               cam.width, cam.height, (float)s, s, maps[0], maps[1], maps[2], nullptr,
                                                dmaps[0], dmaps[1], dmaps[2], nullptr, n_proc, rows);
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 16) blocks = 148 * 16;
