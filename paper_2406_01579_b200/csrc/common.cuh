@@ -88,18 +88,19 @@ __device__ __forceinline__ void tet_corners(uint32_t t, const Grid& G, int xyz[4
   const int iy = (int)(q - ix * (uint32_t)G.R);
   const int a0 = perm_a0(p), a1 = perm_a1(p);
   const bool odd = (p == 1 || p == 2 || p == 5);
-  int c[4][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {1, 1, 1}};
-  c[1][a0] = 1;
-  c[2][a0] = 1;
-  c[2][a1] = 1;
-  const int s2 = odd ? 3 : 2, s3 = odd ? 2 : 3;
-  const int base[3] = {(int)ix, iy, iz};
+  // corner offsets without dynamic register indexing (no local memory)
+  const int c1x = a0 == 0, c1y = a0 == 1, c1z = a0 == 2;
+  const int c2x = c1x | (a1 == 0), c2y = c1y | (a1 == 1), c2z = c1z | (a1 == 2);
+  const int b[3] = {(int)ix, iy, iz};
+  xyz[0][0] = b[0]; xyz[0][1] = b[1]; xyz[0][2] = b[2];
+  xyz[1][0] = b[0] + c1x; xyz[1][1] = b[1] + c1y; xyz[1][2] = b[2] + c1z;
+  const int ex = odd ? 1 : c2x, ey = odd ? 1 : c2y, ez = odd ? 1 : c2z;  // slot 2
+  const int fx = odd ? c2x : 1, fy = odd ? c2y : 1, fz = odd ? c2z : 1;  // slot 3
+  xyz[2][0] = b[0] + ex; xyz[2][1] = b[1] + ey; xyz[2][2] = b[2] + ez;
+  xyz[3][0] = b[0] + fx; xyz[3][1] = b[1] + fy; xyz[3][2] = b[2] + fz;
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int src = k == 2 ? s2 : (k == 3 ? s3 : k);
-    for (int a = 0; a < 3; ++a) xyz[k][a] = base[a] + c[src][a];
+  for (int k = 0; k < 4; ++k)
     vid[k] = (uint32_t)xyz[k][0] + (uint32_t)G.n * ((uint32_t)xyz[k][1] + (uint32_t)G.n * (uint32_t)xyz[k][2]);
-  }
 }
 
 __device__ __forceinline__ void tet_vertices(uint32_t t, const Grid& G, uint32_t vid[4]) {

@@ -41,12 +41,13 @@ struct __align__(16) Staged {
   uint32_t flags;
   int k;
   float md;
-  float iz[4], f[4];
+  float iz[4], df[4];  // 1/z; f_i - f_0
   float eux[4], euy[4], cu[4], evx[4], evy[4], cv[4], adet[4];
   float n[3];
   float fband;  // 3 * band * (z_max / z_min) * max|f|: FP32 f_hit error = fband / |det_face|
-  float ftol0;  // 1e-6 * max|f|: rounding of the stored f samples
-  float pad[3];
+  float ftol0;  // rounding of the stored f deltas
+  float f0;
+  float pad[2];
 };
 static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 
@@ -68,7 +69,7 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
   s.k = k;
   const float vx[4] = {q1.x, q1.y, q1.z, q1.w}, vy[4] = {q2.x, q2.y, q2.z, q2.w};
   const float z[4] = {q3.x, q3.y, q3.z, q3.w};
-  s.f[0] = q4.x; s.f[1] = q4.y; s.f[2] = q4.z; s.f[3] = q4.w;
+  s.f0 = q4.x; s.df[0] = 0.f; s.df[1] = q4.y; s.df[2] = q4.z; s.df[3] = q4.w;
   s.n[0] = q5.x; s.n[1] = q5.y; s.n[2] = q5.z;
   s.md = q5.w;
 #pragma unroll
@@ -90,10 +91,11 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
     s.adet[fi] = fabsf(det);
   }
   // error bound of FP32 f_hit: edge-function error (band/16) over |det|, times depth ratio
-  float fmax = fmaxf(fmaxf(fabsf(s.f[0]), fabsf(s.f[1])), fmaxf(fabsf(s.f[2]), fabsf(s.f[3])));
+  // FP32 f_hit - f_0 = sum(lambda_i df_i): error <= 0.375 band zr / |det| * spread per face
+  float fmax = fmaxf(fabsf(s.df[1]), fmaxf(fabsf(s.df[2]), fabsf(s.df[3])));
   float izmin = fminf(fminf(s.iz[0], s.iz[1]), fminf(s.iz[2], s.iz[3]));
   float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
-  s.fband = 3.0f * s.band * (izmax / izmin) * fmax;
+  s.fband = 0.75f * s.band * (izmax / izmin) * fmax;
   s.ftol0 = 1e-6f * fmax;
 }
 
@@ -121,7 +123,7 @@ __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hi
     float D = wa + wb + wc;
     float rD = 1.0f / D;
     float zp = s.adet[fi] * rD;
-    float fh = (wa * s.f[ia] + wb * s.f[ib] + wc * s.f[ic]) * rD;
+    float fh = (wa * s.df[ia] + wb * s.df[ib] + wc * s.df[ic]) * rD;  // f_hit - f0
     if (nh == 0) {
       zlo = zhi = zp; flo = fhi = fh; lo = hi = fi;
     } else {
@@ -173,36 +175,35 @@ __device__ __noinline__ bool blend_exact(const Scene64& S, int k, int xi, int yi
 // by blend_exact so the blended set matches the FP64 reference.
 __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, int xi, int yi, float s, double s64,
                                          const Scene64& S, Blend& b) {
-  Hit h;
+  Hit h;  // h.fp / h.fn are f - f0 here
   const int e = eval_hits(r, px, py, h);
   if (e == 0) return false;
   if (e == 1) {
-    const float df = h.fp - h.fn;
+    const float dfl = h.fp - h.fn;  // f_prev - f_next, f0 cancels exactly
     const float ftol = r.fband / fminf(r.adet[h.fip], r.adet[h.fin]) + r.ftol0;
-    if (df < -ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
-    const float x = -s * h.fp, y = -s * h.fn;
-    if (df > ftol && !(x < -700.f && y < -700.f)) {
+    if (dfl < -ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
+    if (dfl > ftol) {
+      const float fp = r.f0 + h.fp, fn = r.f0 + h.fn;
+      const float x = -s * fp, y = -s * fn;
       float d;
       if (x > 0.f && y > 0.f)
-        d = s * (h.fn - h.fp) + (softplus_tail(x) - softplus_tail(y));
+        d = -s * dfl + (softplus_tail(x) - softplus_tail(y));
       else
         d = (fmaxf(x, 0.f) + softplus_tail(x)) - (fmaxf(y, 0.f) + softplus_tail(y));
       const float a_un = -expm1f(d);
-      if (fabsf(a_un - kAlphaClipF) > 2e-6f) {
-        b.fp = h.fp;
-        b.fn = h.fn;
+      // alpha > 1e-10 and not at the clip threshold: the FP64 reference decides the same
+      if (d < -1e-10f && fabsf(a_un - kAlphaClipF) > 2e-6f) {
+        b.fp = fp;
+        b.fn = fn;
         b.fip = h.fip;
         b.fin = h.fin;
         b.clipped = a_un > kAlphaClipF;
         if (b.clipped) {
           b.a = kAlphaClipF;
           b.om = kOneMinusClipF;
-        } else if (a_un > 0.f) {
+        } else {
           b.a = a_un;
           b.om = expf(d);
-        } else {  // FP32 underflow of a positive FP64 alpha (< 1e-38): blends as zero
-          b.a = 0.f;
-          b.om = 1.f;
         }
         return true;
       }
@@ -348,11 +349,11 @@ __device__ __forceinline__ void face_bwd(const Staged& r, float px, float py, fl
   float wbar = 1.0f - u - v;
   float w0 = wbar * r.iz[ia], w1 = u * r.iz[ib], w2 = v * r.iz[ic];
   float iS = 1.0f / (w0 + w1 + w2);
-  float fh = (w0 * r.f[ia] + w1 * r.f[ib] + w2 * r.f[ic]) * iS;
+  float fh = (w0 * r.df[ia] + w1 * r.df[ib] + w2 * r.df[ic]) * iS;  // f_hit - f0
   gr[ia] += g * w0 * iS;
   gr[ib] += g * w1 * iS;
   gr[ic] += g * w2 * iS;
-  float dw0 = g * (r.f[ia] - fh) * iS, dw1 = g * (r.f[ib] - fh) * iS, dw2 = g * (r.f[ic] - fh) * iS;
+  float dw0 = g * (r.df[ia] - fh) * iS, dw1 = g * (r.df[ib] - fh) * iS, dw2 = g * (r.df[ic] - fh) * iS;
   gr[4 + ia] += dw0 * (-w0 * r.iz[ia]);
   gr[4 + ib] += dw1 * (-w1 * r.iz[ib]);
   gr[4 + ic] += dw2 * (-w2 * r.iz[ic]);

@@ -23,7 +23,7 @@ struct __align__(16) SplatRec {
   uint32_t flags;   // bits 0-3: face f valid (|det64| >= 2e-12); bit 4: always use fallback
   float vx[4], vy[4];  // projected vertices minus (ix0, iy0)
   float z[4];          // camera-space depths
-  float f[4];          // SDF samples
+  float f[4];          // SDF samples as f0, f1-f0, f2-f0, f3-f0 (deltas keep FP32 error ~ spread)
   float n[3];          // unit normal (zero when undefined)
   float md;            // mean depth
 };
@@ -62,7 +62,7 @@ __device__ inline SplatRec make_record(const double proj[8], const double depths
     r.vy[v] = (float)ay;
     M = fmax(M, fmax(fabs(ax), fabs(ay)));
     r.z[v] = (float)depths[v];
-    r.f[v] = (float)f[v];
+    r.f[v] = v == 0 ? (float)f[0] : (float)dsub(f[v], f[0]);  // f0, then exact-ish deltas
   }
   uint32_t flags = 0;
   for (int fi = 0; fi < 4; ++fi) {
