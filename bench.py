@@ -1,0 +1,464 @@
+"""bench.py — fwd+bwd views/s of the B200 tetrahedron rasterizer (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], "config 3"): 128^3 Kuhn tet grid (12.58 M tets), analytic
+sphere SDF r=0.5, 1024x1024, s=100, an 8-view SDS-style batch per GPU (weak scaling: at N
+GPUs each rank renders 8 of 8N orbit views), upstream map gradients ~ N(0,1).  One step =
+prefilter + 8 x (build_scene, bin_and_sort, render_forward, render_backward) + eikonal +
+normal consistency (lambda 1000 each) + NCCL all-reduce of the vertex gradients + Adam.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints ONE JSON line (rank 0).  `value` = views/s with inputs resident in HBM; `e2e` = the
+same through the public API with host inputs copied in (pinned H2D of the field and the
+map gradients, D2H of the gradients) inside the timed region.  `--impl reference` times the
+reference's CPU implementation (oracle/: the reference's own Cython kernels built from
+/root/reference into oracle/_ref when present, else the plain-C restatement) on the host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd views/sec at 128^3 tet grid, 1024² (1/2/4/8 B200) vs CPU ref"
+R_GRID, IMG, STEEP, VIEWS_PER_GPU = 128, 1024, 100.0, 8
+LAMBDA = 1000.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--resolution", type=int, default=R_GRID)
+    p.add_argument("--image", type=int, default=IMG)
+    p.add_argument("--s", type=float, default=STEEP)
+    return p.parse_args()
+
+
+def config_dict(args, world):
+    return {"workload": f"config 3: {args.resolution}^3 Kuhn tet grid, {args.image}x{args.image}, s={args.s:g}, "
+                        f"{VIEWS_PER_GPU} orbit views per GPU (fwd+bwd + eikonal + normal consistency + "
+                        f"allreduce + Adam)",
+            "grid": args.resolution, "image": args.image, "steepness": args.s, "views_per_gpu": VIEWS_PER_GPU,
+            "global_batch_views": VIEWS_PER_GPU * world, "field": "analytic sphere r=0.5 (synthetic)",
+            "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"views sharded x{world}"}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline
+# ---------------------------------------------------------------------------------------
+
+def cpu_reference_sample(resolution, image, s, n_views_total, view_index=0, warm=False):
+    """One bounded sample of the workload on the host: per-batch work (prefilter, eikonal,
+    normal consistency, Adam-sized update) and ONE view's fwd+bwd.  Returns timings."""
+    from oracle import ts_oracle as O
+    backend = O.default_backend()
+    if warm:  # cheap warm-up of the code paths on a tiny case
+        g = O.build_grid(8)
+        f = O.init_sphere_field(g)
+        cam = O.orbit_camera(0, 8, width=32, height=32)
+        sc = O.build_scene(g, f, cam, s)
+        b = O.bin_and_sort(sc, cam)
+        m, sv = O.render_forward(sc, b, cam, save_state=True, backend=backend)
+        O.render_backward(sv, sc, g, f, cam, O.synthetic_dmaps(32, 32), backend=backend)
+        return None
+    st = cpu_reference_sample.state
+    if st is None or st["R"] != resolution:
+        g = O.build_grid(resolution)
+        f = O.init_sphere_field(g, 0.5)
+        t0 = time.perf_counter()
+        active = O.prefilter(g, f, s)
+        t1 = time.perf_counter()
+        O.eikonal_loss(g, f, active, backend=backend)
+        t2 = time.perf_counter()
+        O.normal_consistency_loss(g, f, backend=backend)
+        t3 = time.perf_counter()
+        st = dict(R=resolution, g=g, f=f, active=active, t_prefilter=t1 - t0, t_eik=t2 - t1, t_nc=t3 - t2,
+                  dm=O.synthetic_dmaps(image, image))
+        cpu_reference_sample.state = st
+    g, f = st["g"], st["f"]
+    cam = O.orbit_camera(view_index % n_views_total, n_views_total, width=image, height=image)
+    t0 = time.perf_counter()
+    sc = O.build_scene(g, f, cam, s, active=st["active"])
+    b = O.bin_and_sort(sc, cam)
+    m, sv = O.render_forward(sc, b, cam, save_state=True, backend=backend)
+    O.render_backward(sv, sc, g, f, cam, st["dm"], backend=backend)
+    t1 = time.perf_counter()
+    return dict(t_view=t1 - t0, t_batch=st["t_prefilter"] + st["t_eik"] + st["t_nc"], backend=backend)
+
+
+cpu_reference_sample.state = None
+
+
+def cpu_kind():
+    from oracle import ts_oracle as O
+    return "reference" if O.default_backend() == "ref" else "port"
+
+
+def cpu_sample_desc(backend):
+    src = ("the reference's own Cython kernels (oracle/_ref, compiled from /root/reference kernels/_core.pyx) "
+           "driven by the numpy restatement of raster.py/splat.py") if backend == "ref" else \
+        "plain-C restatement of the reference kernels (oracle/liboracle.so, OpenMP) + numpy orchestration"
+    return (f"1 view fwd+bwd of config 3 (build_scene, bin_and_sort, render_forward, render_backward incl. "
+            f"vertex chain) + per-batch prefilter/eikonal/normal-consistency amortised over {VIEWS_PER_GPU} "
+            f"views; {src}")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("TETSPLAT_THREADS", str(threads))
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.resolution, args.image, args.s, VIEWS_PER_GPU * world, warm=True)
+    per_view = []
+    tb = None
+    for k in range(args.steps):
+        r = cpu_reference_sample(args.resolution, args.image, args.s, VIEWS_PER_GPU * world, view_index=k)
+        per_view.append(r["t_view"])
+        tb = r["t_batch"]
+        backend = r["backend"]
+    t_view = statistics.mean(per_view)
+    sec_per_view = t_view + tb / VIEWS_PER_GPU
+    value = 1.0 / sec_per_view
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_view, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, world),
+            "cpu_baseline": {"value": value, "unit": "views/s", "cores": int(os.environ["TETSPLAT_THREADS"]),
+                             "kind": "reference" if backend == "ref" else "port", "sample": cpu_sample_desc(backend),
+                             "t_view_s": t_view, "t_batch_s": tb},
+            "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is None:
+            self.result = None
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        self.result = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                       "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def count_my_kernels(fn):
+    """Kernels of libtetsplat_b200 launched by fn() (CUPTI via torch.profiler)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    mine = other = 0
+    per = {}
+    for ev in prof.events():
+        if ev.device_type is None or str(ev.device_type).split(".")[-1] != "CUDA":
+            continue
+        name = ev.name
+        if name.startswith("ts::") or "ts::k_" in name or name.startswith("void ts::"):
+            mine += 1
+            short = name.split("(")[0].replace("void ", "")
+            per[short] = per.get(short, 0) + 1
+        elif "memcpy" not in name.lower() and "memset" not in name.lower():
+            other += 1
+    return mine, other, per
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2406_01579_b200 as ts
+    from paper_2406_01579_b200 import _native
+    from paper_2406_01579_b200.batch import FitStep, StepConfig, StepStats, shard_views
+    _native.lib()
+
+    dev = torch.device("cuda", local)
+    R, S, s = args.resolution, args.image, args.s
+    n_views = VIEWS_PER_GPU * world
+    g = ts.build_grid(R)
+    field = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)), device=dev)
+    cams = [ts.orbit_camera(i, n_views, width=S, height=S) for i in range(n_views)]
+    views = shard_views(n_views, rank, world)
+    gen = torch.Generator(device=dev).manual_seed(1 + rank)
+    dmaps = {vi: ts.RenderMaps(torch.randn((S, S, 3), device=dev, generator=gen),
+                               torch.randn((S, S), device=dev, generator=gen),
+                               torch.randn((S, S), device=dev, generator=gen)) for vi in views}
+    step = FitStep(g, field, cams, StepConfig(lambda_eik=LAMBDA, lambda_nc=LAMBDA))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # the optimizer moves the field; keep the workload fixed by restoring it each step
+    sdf0, def0 = field.sdf.clone(), field.deformation.clone()
+
+    def one_step(stats=None):
+        field.sdf.copy_(sdf0)
+        field.deformation.copy_(def0)
+        step(s, views, lambda vi, m: dmaps[vi], stats)
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+
+    # ---- device-resident timing (value) --------------------------------------------------
+    total_ms = 0.0
+    stats = StepStats()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one_step(stats if k == 0 else None)
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+    barrier()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n_views * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end through the public API with host buffers (e2e) ------------------------
+    h_sdf = sdf0.cpu().pin_memory()
+    h_def = def0.cpu().pin_memory()
+    h_maps = {vi: [m.normal.cpu().pin_memory(), m.depth.cpu().pin_memory(), m.opacity.cpu().pin_memory()]
+              for vi, m in dmaps.items()}
+    d_maps = {vi: ts.RenderMaps.empty(S, S, device=dev) for vi in views}
+    h_grad = torch.empty_like(step.grads.d_vert, device="cpu").pin_memory()
+    h2d = h_sdf.numel() * 8 + h_def.numel() * 8 + sum(sum(t.numel() * 4 for t in v) for v in h_maps.values())
+    d2h = h_grad.numel() * 4
+
+    def e2e_step():
+        field.sdf.copy_(h_sdf, non_blocking=True)
+        field.deformation.copy_(h_def, non_blocking=True)
+        for vi in views:
+            d_maps[vi].normal.copy_(h_maps[vi][0], non_blocking=True)
+            d_maps[vi].depth.copy_(h_maps[vi][1], non_blocking=True)
+            d_maps[vi].opacity.copy_(h_maps[vi][2], non_blocking=True)
+        grads = step(s, views, lambda vi, m: d_maps[vi])
+        h_grad.copy_(grads.d_vert, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    e2e_ms = 0.0
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms += e0.elapsed_time(e1)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = n_views * args.steps / (float(t.item()) / 1e3)
+
+    # ---- per-kernel timing of one view for the roofline (events on the launch stream) ----
+    roof, kernels = roofline_probe(ts, _native, g, field, cams[views[0]], dmaps[views[0]], s, sdf0, def0)
+
+    launches_per_step, other_launches, per_kernel = count_my_kernels(lambda: one_step())
+
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return 0
+    line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (FP64 keys/exact decisions)", "data": "synthetic",
+            "config": config_dict(args, world),
+            "e2e": {"value": e2e_value, "unit": "views/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "gpu_launches_per_step": {"libtetsplat_b200": launches_per_step, "torch_other": other_launches},
+            "clocks": clk.result, "roofline": roof, "kernels": kernels,
+            "workload_counts": {"active_tets": stats.active, "splats_view0": stats.splats[:1],
+                                "pairs_view0": stats.pairs[:1]}}
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, world)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
+    """Average device time of each stage's kernels (CUDA events on the launching stream) and
+    the roofline of the dominant kernel.  Work models: SURVEY.md §8d; DESIGN.md §Roofline."""
+    import torch
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if \
+        os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    fp32_peak = n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s (FMA = 2)
+    field.sdf.copy_(sdf0)
+    field.deformation.copy_(def0)
+    st = torch.cuda.current_stream()
+    reps = 5
+    acc = {k: 0.0 for k in ("prefilter", "build_scene", "bin_and_sort", "render_forward", "render_backward",
+                            "eikonal", "normal_consistency")}
+    cnt = None
+    for r in range(reps + 1):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+        ev[0].record(st)
+        act = ts.prefilter(g, field, s)
+        ev[1].record(st)
+        sc = ts.build_scene(g, field, cam, s, active=act)
+        ev[2].record(st)
+        b = ts.bin_and_sort(sc, cam)
+        ev[3].record(st)
+        _native.debug_counters(True)
+        ev[3].synchronize()
+        e_f0 = torch.cuda.Event(enable_timing=True)
+        e_f0.record(st)
+        maps, sv = ts.render_forward(sc, b, cam, save_state=True)
+        ev[4].record(st)
+        gb = ts.render_backward(sv, sc, g, field, cam, dm)
+        ev[5].record(st)
+        ts.eikonal_loss(g, field, act, out=gb, scale=LAMBDA)
+        ev[6].record(st)
+        ts.normal_consistency_loss(g, field, out=gb, scale=LAMBDA)
+        ev[7].record(st)
+        torch.cuda.synchronize()
+        if r == 0:
+            cnt = _native.debug_counters(True)
+            P_pop = int(sv.n_proc.sum())
+            B = int(sv.n_blend.sum())
+            K_a, K_v, M = int(act.numel()), len(sc), b.num_pairs
+            continue
+        names = list(acc)
+        for i, n in enumerate(names):
+            a0 = e_f0 if n == "render_forward" else ev[i]
+            acc[n] += a0.elapsed_time(ev[i + 1])
+    ms = {k: v / reps for k, v in acc.items()}
+    P_bbox = cnt[2]
+    N = g.num_vertices
+    # algorithmic work per launch
+    fwd_flop = 8 * P_pop + 120 * P_bbox + 19 * B
+    bwd_flop = fwd_flop + 300 * B
+    kern = {
+        "prefilter": {"ms": ms["prefilter"], "bytes": 8 * N + 4 * K_a, "bound": "hbm"},
+        "build_scene": {"ms": ms["build_scene"], "bytes": 32 * N + 4 * K_a + 336 * K_v, "bound": "hbm"},
+        "bin_and_sort": {"ms": ms["bin_and_sort"], "bytes": 40 * K_v + 24 * M + 16 * M, "bound": "hbm"},
+        "render_forward": {"ms": ms["render_forward"], "flop": fwd_flop, "bound": "fp32"},
+        "render_backward": {"ms": ms["render_backward"], "flop": bwd_flop, "bound": "fp32"},
+        "eikonal": {"ms": ms["eikonal"], "bytes": 32 * N + 4 * K_a + 64 * K_a, "bound": "hbm"},
+        "normal_consistency": {"ms": ms["normal_consistency"], "bytes": 32 * N * 3 + 16 * N, "bound": "hbm"},
+    }
+    for k, d in kern.items():
+        if d["bound"] == "hbm":
+            d["achieved_GBs"] = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+            d["frac_of_hbm"] = d["achieved_GBs"] / hbm
+        else:
+            d["achieved_TFLOPs"] = d["flop"] / (d["ms"] * 1e-3) / 1e12
+            d["frac_of_fp32"] = d["achieved_TFLOPs"] / fp32_peak
+    top = max(kern, key=lambda k: kern[k]["ms"])
+    d = kern[top]
+    if d["bound"] == "hbm":
+        roof = {"kernel": top, "bound": "hbm", "achieved": d["achieved_GBs"], "peak": hbm, "unit": "GB/s",
+                "frac": d["frac_of_hbm"], "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_TFLOPs"], "peak": fp32_peak,
+                "unit": "TFLOP/s", "frac": d["frac_of_fp32"], "traffic": None,
+                "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no tensor cores: not a "
+                               f"dense contraction)"}
+    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M,
+             "fp64_fallbacks_edge": cnt[0], "fp64_fallbacks_alpha": cnt[1]}
+    return roof, {"per_view_ms": {k: round(v["ms"], 4) for k, v in kern.items()}, "detail": kern, "counts": extra}
+
+
+def cpu_baseline(args, world):
+    import torch
+    if int(os.environ.get("RANK", "0")) != 0 or world != 1:
+        return None
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("TETSPLAT_THREADS", str(threads))
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    try:
+        r = cpu_reference_sample(args.resolution, args.image, args.s, VIEWS_PER_GPU)
+    except Exception as e:  # the checker must never break the GPU line
+        return {"value": None, "error": str(e)[:200]}
+    v = 1.0 / (r["t_view"] + r["t_batch"] / VIEWS_PER_GPU)
+    return {"value": v, "unit": "views/s", "cores": int(os.environ["TETSPLAT_THREADS"]),
+            "kind": "reference" if r["backend"] == "ref" else "port", "sample": cpu_sample_desc(r["backend"]),
+            "t_view_s": r["t_view"], "t_batch_s": r["t_batch"]}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

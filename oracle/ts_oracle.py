@@ -467,10 +467,23 @@ def render_forward(scene, bins, camera, n_w=DEFAULT_WINDOW, t_stop=T_STOP, save_
     counts = None
     if backend == "ref":
         touched = np.nonzero(np.diff(bins.starts) > 0)[0]
-        records = _load_ref().forward_tiles(
-            *args, bins.starts, bins.items, touched, bins.tile_size, bins.tiles_x, W, H, n_w, s,
-            t_stop, ALPHA_CLIP, maps.normal, maps.depth, maps.opacity, maps.color,
-            bool(save_state or want_counts))
+        core = _load_ref()
+
+        def run(tids):  # raster.py:164-175: chunked tiles over a thread pool (GIL released)
+            return core.forward_tiles(
+                *args, bins.starts, bins.items, tids, bins.tile_size, bins.tiles_x, W, H, n_w, s,
+                t_stop, ALPHA_CLIP, maps.normal, maps.depth, maps.opacity, maps.color,
+                bool(save_state or want_counts))
+
+        nt = n_threads()
+        if nt <= 1 or len(touched) < 2:
+            records = run(touched)
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            records = []
+            with ThreadPoolExecutor(max_workers=nt) as pool:
+                for part in pool.map(run, np.array_split(touched, min(nt * 4, len(touched)))):
+                    records.extend(part)
         if want_counts:
             counts = np.zeros((H, W), np.int32)
             ts = bins.tile_size
@@ -532,9 +545,25 @@ def splat_gradients(saved, scene, camera, d_maps, backend=None):
         records = saved.records
         if records is None:
             raise ValueError("ref backend needs save_state=True records")
-        _load_ref().backward_tiles(*args, records, b.tile_size, b.tiles_x, W, H, s, ALPHA_CLIP,
-                                   *dm, d["d_f"], d["d_proj"], d["d_depths"], d["d_normals"],
-                                   d["d_mean_depth"], d["d_colors"])
+        core = _load_ref()
+
+        def run(recs):  # raster.py:214-247: private per-chunk buffers, ordered merge
+            p = {k: (None if v is None else np.zeros_like(v)) for k, v in d.items()}
+            core.backward_tiles(*args, recs, b.tile_size, b.tiles_x, W, H, s, ALPHA_CLIP, *dm, p["d_f"],
+                                p["d_proj"], p["d_depths"], p["d_normals"], p["d_mean_depth"], p["d_colors"])
+            return p
+
+        nt = n_threads()
+        if nt <= 1 or len(records) < 2:
+            parts = [run(records)]
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            chunks = [c for c in np.array_split(np.arange(len(records)), nt) if len(c)]
+            with ThreadPoolExecutor(max_workers=nt) as pool:
+                parts = list(pool.map(lambda c: run([records[i] for i in c]), chunks))
+        for k in d:
+            if d[k] is not None:
+                d[k] = sum(p[k] for p in parts)
     else:
         rc = _load_c().or_backward(*[_ptr(a) for a in args], K, _ptr(b.starts), _ptr(b.items),
                                    b.tile_size, b.tiles_x, b.tiles_y, W, H, saved.n_w, s,

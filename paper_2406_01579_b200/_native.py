@@ -99,7 +99,7 @@ def i64():
 
 
 def debug_counters(reset: bool = True):
-    """(edge/degenerate FP64 re-decisions, alpha-threshold FP64 re-decisions) since last reset."""
+    """(edge FP64 re-decisions, alpha FP64 re-decisions, forward rect-pass pairs, 0) since last reset."""
     out = (ctypes.c_uint64 * 4)()
     check(lib().ts_debug_counters(out, int(reset)))
-    return int(out[0]), int(out[1])
+    return tuple(int(v) for v in out)

@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
   float T = 1.f;
   Accum<COLOR> acc;
   acc.zero();
+  unsigned nbbox = 0;  // pairs passing the pixel-rect test (roofline work model)
   bool done = !inside;
   int nproc = inside ? L : 0, nb = 0;
   for (int base = 0; base < L; base += kChF) {
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
       for (int j = 0; j < n; ++j) {
         const Staged& r = sh[j];
         if (xi < r.rx0 || xi > r.rx1 || yi < r.ry0 || yi > r.ry1) continue;
+        ++nbbox;
         const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
         Blend bl;
         if (!blend_of(r, px, py, xi, yi, s, s64, S64, bl)) continue;
@@ -305,6 +307,8 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
     n_proc[p] = nproc;
     n_blend[p] = nb;
   }
+  const unsigned wb = warp_sum(nbbox);
+  if ((threadIdx.x & 31) == 0 && wb) atomicAdd(&g_ts_counters[2], (unsigned long long)wb);
 }
 
 // per-tile replay of the reference window (_core.pyx:171-187) for tiles whose list is
