@@ -38,8 +38,25 @@ static Camera to_cam(const ts_camera* c) {
   return k;
 }
 
+// Temporaries come from the device's stream-ordered pool.  Keep freed blocks cached across
+// stream synchronisations (the default release threshold of 0 returns them to the driver
+// at every sync, turning each per-view scratch allocation into fresh page mappings).
+static void keep_pool_warm() {
+  static thread_local int dev_done = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_done == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  dev_done = dev;
+}
+
 template <class T>
 static T* dalloc(size_t n, cudaStream_t st) {
+  keep_pool_warm();
   T* p = nullptr;
   if (n == 0) n = 1;
   if (cudaMallocAsync(&p, n * sizeof(T), st) != cudaSuccess) return nullptr;
@@ -167,6 +184,7 @@ int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const 
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   cudaStream_t st = ST(stream);
+  keep_pool_warm();
   BinsView bv = bv_of(b);
   ts_impl_window(tx * ty, bv, M, sc->mean_depth, n_w, st);
   ts_impl_forward(tx, ty, bv, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
@@ -184,6 +202,7 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
     if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward: missing map");
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  keep_pool_warm();
   const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
   ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc),
@@ -203,6 +222,7 @@ int ts_eikonal(const double* sdf, const double* deform, int32_t R, const int32_t
 int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
                           double* loss, void* stream) {
   if (!sdf || !deform || !d_vert || !loss || R < 1) return fail(TS_EINVAL, "ts_normal_consistency: bad arguments");
+  keep_pool_warm();
   ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream));
   return check_cuda("ts_normal_consistency");
 }
