@@ -1,42 +1,51 @@
 // composite.cu — K6 forward compositing, K7 backward + vertex chain, N_w window.
 //
-// Forward (replaces forward_tiles, _core.pyx:98-229): one 256-thread CTA per 16x16 tile,
-// one pixel per thread.  The tile's list is staged through shared memory in chunks; each
-// staged record carries the four projected faces as sign-normalised edge functions in
-// splat-anchored FP32 coordinates.  Inside/outside decisions that fall within a rigorous
-// FP32 error band of an edge are recomputed with the reference's exact FP64 arithmetic
-// (records.cuh: splat_hits_exact), so the set of blended (pixel, splat) pairs matches the
-// FP64 reference; the blend itself is FP32.  A CTA leaves its loop as soon as every pixel
-// has reached T < t_stop (__syncthreads_and = block-wide ballot).
+// One 256-thread CTA per 16x16 tile.  The tile's list is staged through shared memory in
+// chunks of kCh records.  Each chunk runs in phases that keep all 32 lanes busy:
 //
-// The N_w resorting window (_core.pyx:171-187) pops, for every pixel of a tile, the same
-// sequence — it depends only on the tile list, never on the pixel.  When mean depth is
-// non-decreasing along the list (bin.cu flags it), the window is the identity; otherwise
-// k_window replays the reference's window once per tile into witems.
+//  A (splat-parallel): each warp walks the pixels of its splats' pixel rectangles (the
+//    reference's inclusive bbox test, _core.pyx:80, made exact in FP64 at setup) and decides
+//    hit + opacity for every (pixel, splat) pair, writing a 4-byte code per pair to shared
+//    memory: no blend / clipped / d = log(1 - alpha).  The decision is FP32 on sign-normalised
+//    edge functions in splat-anchored coordinates; any pair within a rigorous FP32 error band
+//    of a decision threshold (face edge, alpha = 0, alpha = ALPHA_CLIP) is re-decided with the
+//    reference's exact FP64 arithmetic (records.cuh: splat_hits_exact), so the set of blended
+//    pairs matches the FP64 reference.
+//  B (pixel-serial): each thread blends its pixel's codes front to back (Eq. 2,
+//    _core.pyx:189-213) with early stop at T < t_stop; the CTA leaves when all pixels stopped.
 //
-// Backward (replaces backward_tiles _core.pyx:344-471 + splat_grads_to_vertices
-// raster.py:253-306): the same CTA/pixel layout walks the list FRONT to back.  The
-// reference's suffix sums are C_final - prefix (C_final = the forward maps), and the
-// d_alpha * d(alpha)/d(f) product is formed as g.(T x (1-a) - suffix) * s * sigmoid, which
-// is the reference's expression with the (1-a) factor cancelled algebraically (no
-// division by 1-a, no reverse walk, no per-pixel record lists).  Per (tile, splat) the
-// 23 gradient scalars are reduced across the warp with a transposed butterfly (31
-// shuffles), across warps with shared-memory atomics, and written to a per-pair row;
-// k_chain gathers each splat's rows in a fixed order (deterministic, atomic-free) and
-// applies the normal chain and the camera chain in FP64, then scatters to vertices with
-// one red.global.add.v4.f32 per (splat, vertex).
+// The per-pixel loop of the reference (_core.pyx:158-229) touches every list entry of the
+// tile; here the expensive hit test runs only on rectangle pixels (dense lanes) and the
+// per-pixel walk is a 16-byte shared-memory rectangle test plus a 4-byte code read.
+//
+// The N_w resorting window (_core.pyx:171-187) pops the same sequence for every pixel of a
+// tile — it depends only on the list.  When mean depth is non-decreasing along the list
+// (bin.cu flags it) the window is the identity; otherwise k_window replays it per tile.
+//
+// Backward (backward_tiles _core.pyx:344-471 + splat_grads_to_vertices raster.py:253-306):
+//  A as above;
+//  B (pixel-serial, FRONT to back): w = T a and the d_alpha chain
+//      G = sum_ch g_ch (T x_ch (1-a) - S_ch),  S_ch = C_final,ch - prefix_ch (inclusive)
+//    which is the reference's d_alpha * (1 - a) with the suffix sums taken from the forward
+//    maps — no division by 1-a, no reverse walk, no per-pixel record lists;
+//  C (item-parallel): each warp compacts the blended (pixel, splat) items of its splats
+//    (ballot) and processes them 32 at a time — face-hit backward (_core.pyx:295-341) into
+//    a 24-float row per item — then a segmented sum over the item rows into the per-(tile,
+//    splat) gradient row.  Rows are written per list position; k_chain gathers each splat's
+//    rows in a fixed order (deterministic, atomic-free), applies the normal and camera chains
+//    in FP64 and scatters to vertices with one red.global.add.v4.f32 per (splat, vertex).
 #include "internal.cuh"
 
 namespace ts {
 
 constexpr float kAlphaClipF = 0.9999f;  // splat.py:14
 constexpr float kOneMinusClipF = 1e-4f;
-constexpr int kChF = 128;  // forward chunk (records per shared-memory stage)
-constexpr int kChB = 64;   // backward chunk
-constexpr int kGr = 24;    // floats per (tile, splat) gradient row
+constexpr int kCh = 32;   // records per shared-memory stage
+constexpr int kGr = 24;   // floats per (tile, splat) gradient row
+constexpr int kWarps = TS_TILE_PX / 32;
 
 struct __align__(16) Staged {
-  int rx0, rx1, ry0, ry1;
+  int rx0, rx1, ry0, ry1;  // pixel rectangle (inclusive)
   float band;
   uint32_t flags;
   int k;
@@ -44,15 +53,15 @@ struct __align__(16) Staged {
   float iz[4], df[4];  // 1/z; f_i - f_0
   float eux[4], euy[4], cu[4], evx[4], evy[4], cv[4], adet[4];
   float n[3];
-  float fband;  // 3 * band * (z_max / z_min) * max|f|: FP32 f_hit error = fband / |det_face|
+  float fband;  // 0.75 band (z_max/z_min) spread(f): FP32 (f_hit - f0) error <= fband / |det_face|
   float ftol0;  // rounding of the stored f deltas
   float f0;
   float pad[2];
 };
 static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 
-// diagnostics: [0] pairs re-decided in FP64 because of an edge / degenerate face,
-// [1] pairs re-decided in FP64 because of an alpha threshold
+// diagnostics: [0] pairs re-decided in FP64 at a face edge / degenerate face,
+// [1] pairs re-decided in FP64 at an alpha threshold, [2] forward rectangle-pass pairs
 __device__ unsigned long long g_ts_counters[4];
 
 __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, Staged& s) {
@@ -69,8 +78,14 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
   s.k = k;
   const float vx[4] = {q1.x, q1.y, q1.z, q1.w}, vy[4] = {q2.x, q2.y, q2.z, q2.w};
   const float z[4] = {q3.x, q3.y, q3.z, q3.w};
-  s.f0 = q4.x; s.df[0] = 0.f; s.df[1] = q4.y; s.df[2] = q4.z; s.df[3] = q4.w;
-  s.n[0] = q5.x; s.n[1] = q5.y; s.n[2] = q5.z;
+  s.f0 = q4.x;
+  s.df[0] = 0.f;
+  s.df[1] = q4.y;
+  s.df[2] = q4.z;
+  s.df[3] = q4.w;
+  s.n[0] = q5.x;
+  s.n[1] = q5.y;
+  s.n[2] = q5.z;
   s.md = q5.w;
 #pragma unroll
   for (int v = 0; v < 4; ++v) s.iz[v] = 1.0f / z[v];
@@ -90,8 +105,6 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
     s.cv[fi] = -(evx * vx[ia] + evy * vy[ia]);
     s.adet[fi] = fabsf(det);
   }
-  // error bound of FP32 f_hit: edge-function error (band/16) over |det|, times depth ratio
-  // FP32 f_hit - f_0 = sum(lambda_i df_i): error <= 0.375 band zr / |det| * spread per face
   float fmax = fmaxf(fabsf(s.df[1]), fmaxf(fabsf(s.df[2]), fabsf(s.df[3])));
   float izmin = fminf(fminf(s.iz[0], s.iz[1]), fminf(s.iz[2], s.iz[3]));
   float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
@@ -100,7 +113,7 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
 }
 
 struct Hit {
-  float fp, fn;
+  float fp, fn;  // f - f0 at entry / exit
   int fip, fin;
 };
 
@@ -123,9 +136,11 @@ __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hi
     float D = wa + wb + wc;
     float rD = 1.0f / D;
     float zp = s.adet[fi] * rD;
-    float fh = (wa * s.df[ia] + wb * s.df[ib] + wc * s.df[ic]) * rD;  // f_hit - f0
+    float fh = (wa * s.df[ia] + wb * s.df[ib] + wc * s.df[ic]) * rD;
     if (nh == 0) {
-      zlo = zhi = zp; flo = fhi = fh; lo = hi = fi;
+      zlo = zhi = zp;
+      flo = fhi = fh;
+      lo = hi = fi;
     } else {
       if (zp < zlo) { zlo = zp; flo = fh; lo = fi; }
       if (zp > zhi) { zhi = zp; fhi = fh; hi = fi; }
@@ -133,7 +148,10 @@ __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hi
     ++nh;
   }
   if (nh < 2) return 0;
-  h.fp = flo; h.fn = fhi; h.fip = lo; h.fin = hi;
+  h.fp = flo;
+  h.fn = fhi;
+  h.fip = lo;
+  h.fin = hi;
   return 1;
 }
 
@@ -143,7 +161,7 @@ __device__ __forceinline__ float softplus_tail(float x) { return log1pf(expf(-fa
 struct Blend {
   float fp, fn;  // SDF at entry / exit
   int fip, fin;  // entry / exit faces
-  float a, om;   // clipped alpha and 1 - alpha
+  float d;       // log(1 - alpha_unclipped)
   bool clipped;  // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
 };
 
@@ -160,22 +178,16 @@ __device__ __noinline__ bool blend_exact(const Scene64& S, int k, int xi, int yi
   b.fip = i0;
   b.fin = i1;
   b.clipped = a > 1.0 - 1e-4;
-  if (b.clipped) {
-    b.a = kAlphaClipF;
-    b.om = kOneMinusClipF;
-  } else {
-    b.a = (float)a;
-    b.om = (float)exp(d);
-  }
+  b.d = (float)d;
   return true;
 }
 
 // FP32 fast path with error-bounded decisions; anything within the bounds of a decision
-// threshold (face edges, alpha == 0, alpha == ALPHA_CLIP, FP32 underflow) is re-decided
-// by blend_exact so the blended set matches the FP64 reference.
+// threshold (face edges, alpha == 0, alpha == ALPHA_CLIP, tiny alpha) is re-decided by
+// blend_exact so the blended set matches the FP64 reference.
 __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, int xi, int yi, float s, double s64,
                                          const Scene64& S, Blend& b) {
-  Hit h;  // h.fp / h.fn are f - f0 here
+  Hit h;
   const int e = eval_hits(r, px, py, h);
   if (e == 0) return false;
   if (e == 1) {
@@ -198,13 +210,7 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
         b.fip = h.fip;
         b.fin = h.fin;
         b.clipped = a_un > kAlphaClipF;
-        if (b.clipped) {
-          b.a = kAlphaClipF;
-          b.om = kOneMinusClipF;
-        } else {
-          b.a = a_un;
-          b.om = expf(d);
-        }
+        b.d = d;
         return true;
       }
     }
@@ -213,6 +219,24 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
     atomicAdd(&g_ts_counters[0], 1ull);
   }
   return blend_exact(S, r.k, xi, yi, s64, b);
+}
+
+// 4-byte code of a pair: +0 no blend, +1 clipped, d = log(1-alpha) <= -0 otherwise
+__device__ __forceinline__ float encode(bool blended, const Blend& b) {
+  if (!blended) return 0.f;
+  if (b.clipped) return 1.f;
+  return b.d > 0.f ? -0.f : (b.d == 0.f ? -0.f : b.d);
+}
+__device__ __forceinline__ bool code_blends(float c) { return __float_as_uint(c) != 0u; }
+__device__ __forceinline__ void decode(float c, float& a, float& om, bool& clipped) {
+  clipped = c > 0.f;
+  if (clipped) {
+    a = kAlphaClipF;
+    om = kOneMinusClipF;
+  } else {
+    a = -expm1f(c);
+    om = expf(c);
+  }
 }
 
 __device__ __forceinline__ float sigmoidf_stable(float x) {
@@ -241,18 +265,57 @@ struct Accum {
   }
 };
 
+// rectangle of splat r inside the tile; false when empty
+__device__ __forceinline__ bool tile_rect(const Staged& r, int tx0, int ty0, int& x0, int& y0, int& nx, int& cnt) {
+  x0 = max(r.rx0, tx0);
+  y0 = max(r.ry0, ty0);
+  const int x1 = min(r.rx1, tx0 + TS_TILE - 1), y1 = min(r.ry1, ty0 + TS_TILE - 1);
+  if (x0 > x1 || y0 > y1) return false;
+  nx = x1 - x0 + 1;
+  cnt = nx * (y1 - y0 + 1);
+  return true;
+}
+
+// Phase A: codes for every (rectangle pixel, splat) of the chunk; `skip` = pixel mask of
+// finished pixels (bit per pixel).  Warp w takes splats w, w + 8, ...
+__device__ __forceinline__ void phase_codes(const Staged* sh, int n, int tx0, int ty0, int W, int H, float s,
+                                            double s64, const Scene64& S, const uint32_t* skip, float (*code)[TS_TILE_PX],
+                                            unsigned& nrect) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < n; j += kWarps) {
+    const Staged& r = sh[j];
+    int x0, y0, nx, cnt;
+    if (!tile_rect(r, tx0, ty0, x0, y0, nx, cnt)) continue;
+    const float inv = 1.0f / (float)nx;
+    for (int it = lane; it < cnt; it += 32) {
+      const int yy = (int)(((float)it + 0.5f) * inv);
+      const int xi = x0 + (it - yy * nx), yi = y0 + yy;
+      const int pix = (yi - ty0) * TS_TILE + (xi - tx0);
+      if ((skip[pix >> 5] >> (pix & 31)) & 1u) continue;
+      if (xi >= W || yi >= H) continue;
+      ++nrect;
+      Blend b;
+      const bool bl = blend_of(r, (float)(xi - r.rx0) + 0.5f, (float)(yi - r.ry0) + 0.5f, xi, yi, s, s64, S, b);
+      code[j][pix] = encode(bl, b);
+    }
+  }
+}
+
 template <bool COLOR>
-__global__ void __launch_bounds__(TS_TILE_PX) k_forward(
+__global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, float* __restrict__ normal_map,
     float* __restrict__ depth_map, float* __restrict__ opacity_map, float* __restrict__ color_map,
     int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
-  __shared__ Staged sh[kChF];
-  __shared__ float shc[COLOR ? kChF : 1][3];
+  __shared__ Staged sh[kCh];
+  __shared__ float code[kCh][TS_TILE_PX];
+  __shared__ float shc[COLOR ? kCh : 1][3];
+  __shared__ uint32_t skip[TS_TILE_PX / 32];
   const int tile = blockIdx.x;
-  const int xi = (tile % tiles_x) * TS_TILE + (threadIdx.x & (TS_TILE - 1));
-  const int yi = (tile / tiles_x) * TS_TILE + (threadIdx.x / TS_TILE);
+  const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
+  const int pix = threadIdx.x;
+  const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
   const bool inside = xi < W && yi < H;
   const int64_t lo = starts[tile];
   const int L = (int)(starts[tile + 1] - lo);
@@ -260,28 +323,35 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
   float T = 1.f;
   Accum<COLOR> acc;
   acc.zero();
-  unsigned nbbox = 0;  // pairs passing the pixel-rect test (roofline work model)
+  unsigned nrect = 0;
   bool done = !inside;
   int nproc = inside ? L : 0, nb = 0;
-  for (int base = 0; base < L; base += kChF) {
-    const int n = min(kChF, L - base);
+  {
+    const unsigned m = __ballot_sync(0xffffffffu, done);
+    if ((threadIdx.x & 31) == 0) skip[threadIdx.x >> 5] = m;
+  }
+  for (int base = 0; base < L; base += kCh) {
+    const int n = min(kCh, L - base);
     if (threadIdx.x < n) {
-      int k = list[base + threadIdx.x];
+      const int k = list[base + threadIdx.x];
       stage(recs, k, sh[threadIdx.x]);
       if (COLOR)
         for (int c = 0; c < 3; ++c) shc[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
     }
     __syncthreads();
+    phase_codes(sh, n, tx0, ty0, W, H, s, s64, S64, skip, code, nrect);
+    __syncthreads();
     if (!done) {
       for (int j = 0; j < n; ++j) {
-        const Staged& r = sh[j];
-        if (xi < r.rx0 || xi > r.rx1 || yi < r.ry0 || yi > r.ry1) continue;
-        ++nbbox;
-        const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-        Blend bl;
-        if (!blend_of(r, px, py, xi, yi, s, s64, S64, bl)) continue;
-        acc.add(__fmul_rn(T, bl.a), r, COLOR ? shc[j] : nullptr);
-        T = __fmul_rn(T, bl.om);
+        const int4 rr = *reinterpret_cast<const int4*>(&sh[j].rx0);
+        if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
+        const float c = code[j][pix];
+        if (!code_blends(c)) continue;
+        float a, om;
+        bool cl;
+        decode(c, a, om, cl);
+        acc.add(__fmul_rn(T, a), sh[j], COLOR ? shc[j] : nullptr);
+        T = __fmul_rn(T, om);
         ++nb;
         if (T < t_stop) {
           done = true;
@@ -290,6 +360,8 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
         }
       }
     }
+    const unsigned m = __ballot_sync(0xffffffffu, done);
+    if ((threadIdx.x & 31) == 0) skip[threadIdx.x >> 5] = m;
     if (__syncthreads_and(done)) break;
   }
   if (inside) {
@@ -307,7 +379,7 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_forward(
     n_proc[p] = nproc;
     n_blend[p] = nb;
   }
-  const unsigned wb = warp_sum(nbbox);
+  const unsigned wb = warp_sum(nrect);
   if ((threadIdx.x & 31) == 0 && wb) atomicAdd(&g_ts_counters[2], (unsigned long long)wb);
 }
 
@@ -343,76 +415,129 @@ __global__ void k_window(int T, const int64_t* __restrict__ starts, const int32_
   }
 }
 
-// backward of one face hit (_core.pyx:295-341) into per-vertex rows gr[0..15]
-template <int FI>
-__device__ __forceinline__ void face_bwd(const Staged& r, float px, float py, float g, float* gr) {
-  constexpr int ia = face_vert(FI, 0), ib = face_vert(FI, 1), ic = face_vert(FI, 2);
-  const float inv_ad = 1.0f / r.adet[FI];
-  float u = fmaf(r.eux[FI], px, fmaf(r.euy[FI], py, r.cu[FI])) * inv_ad;
-  float v = fmaf(r.evx[FI], px, fmaf(r.evy[FI], py, r.cv[FI])) * inv_ad;
-  float wbar = 1.0f - u - v;
-  float w0 = wbar * r.iz[ia], w1 = u * r.iz[ib], w2 = v * r.iz[ic];
-  float iS = 1.0f / (w0 + w1 + w2);
-  float fh = (w0 * r.df[ia] + w1 * r.df[ib] + w2 * r.df[ic]) * iS;  // f_hit - f0
-  gr[ia] += g * w0 * iS;
-  gr[ib] += g * w1 * iS;
-  gr[ic] += g * w2 * iS;
-  float dw0 = g * (r.df[ia] - fh) * iS, dw1 = g * (r.df[ib] - fh) * iS, dw2 = g * (r.df[ic] - fh) * iS;
-  gr[4 + ia] += dw0 * (-w0 * r.iz[ia]);
-  gr[4 + ib] += dw1 * (-w1 * r.iz[ib]);
-  gr[4 + ic] += dw2 * (-w2 * r.iz[ic]);
-  float gu = -dw0 * r.iz[ia] + dw1 * r.iz[ib];
-  float gv = -dw0 * r.iz[ia] + dw2 * r.iz[ic];
-  float qx = (r.eux[FI] * gu + r.evx[FI] * gv) * inv_ad;
-  float qy = (r.euy[FI] * gu + r.evy[FI] * gv) * inv_ad;
-  gr[8 + ia] -= qx * wbar;
-  gr[12 + ia] -= qy * wbar;
-  gr[8 + ib] -= qx * u;
-  gr[12 + ib] -= qy * u;
-  gr[8 + ic] -= qx * v;
-  gr[12 + ic] -= qy * v;
+// backward of one face hit (_core.pyx:295-341) accumulated into an item row (shared memory,
+// per-vertex slots: [0,4) d_f, [4,8) d_depth, [8,12) d_px, [12,16) d_py)
+__device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, float px, float py, float g) {
+  const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
+  const float inv_ad = 1.0f / r.adet[fi];
+  const float eux = r.eux[fi], euy = r.euy[fi], evx = r.evx[fi], evy = r.evy[fi];
+  const float u = fmaf(eux, px, fmaf(euy, py, r.cu[fi])) * inv_ad;
+  const float v = fmaf(evx, px, fmaf(evy, py, r.cv[fi])) * inv_ad;
+  const float wbar = 1.0f - u - v;
+  const float iza = r.iz[ia], izb = r.iz[ib], izc = r.iz[ic];
+  const float fa = r.df[ia], fb = r.df[ib], fc = r.df[ic];
+  const float w0 = wbar * iza, w1 = u * izb, w2 = v * izc;
+  const float iS = 1.0f / (w0 + w1 + w2);
+  const float fh = (w0 * fa + w1 * fb + w2 * fc) * iS;
+  row[ia] += g * w0 * iS;
+  row[ib] += g * w1 * iS;
+  row[ic] += g * w2 * iS;
+  const float dw0 = g * (fa - fh) * iS, dw1 = g * (fb - fh) * iS, dw2 = g * (fc - fh) * iS;
+  row[4 + ia] += dw0 * (-w0 * iza);
+  row[4 + ib] += dw1 * (-w1 * izb);
+  row[4 + ic] += dw2 * (-w2 * izc);
+  const float gu = -dw0 * iza + dw1 * izb;
+  const float gv = -dw0 * iza + dw2 * izc;
+  const float qx = (eux * gu + evx * gv) * inv_ad;
+  const float qy = (euy * gu + evy * gv) * inv_ad;
+  row[8 + ia] -= qx * wbar;
+  row[12 + ia] -= qy * wbar;
+  row[8 + ib] -= qx * u;
+  row[12 + ib] -= qy * u;
+  row[8 + ic] -= qx * v;
+  row[12 + ic] -= qy * v;
 }
 
-// lane L ends with the warp total of value L (transposed butterfly, 31 shuffles)
-__device__ __forceinline__ float warp_transpose_reduce(float (&v)[32]) {
-  const unsigned lane = threadIdx.x & 31u;
+struct BwdSmem {
+  Staged sh[kCh];
+  float wv[kCh][TS_TILE_PX];  // phase A: codes; phase B: w = T a (-0 = blended with w == 0)
+  float Gv[kCh][TS_TILE_PX];  // phase B: G (0 when clipped)
+  float acc[kCh][kGr];        // per-(tile, splat) gradient rows of the chunk
+  float gpx[TS_TILE_PX][8];   // per-pixel upstream gradients: g_d, g_n[3], g_c[3]
+  float col[kCh][3];
+  int buf[kWarps][64];        // per-warp compacted items (j << 8 | pixel)
+  float rows[kWarps][32][kGr];
+  uint32_t skip[TS_TILE_PX / 32];
+  int maxproc;
+};
+
+template <bool COLOR>
+__device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty0, float s, double s64,
+                                              const Scene64& S64) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* row = S.rows[warp][lane];
+  if (lane < m) {
+    const int item = S.buf[warp][lane];
+    const int j = item >> 8, pix = item & 255;
+    const Staged& r = S.sh[j];
+    const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
+    const float w = S.wv[j][pix];
+    const float G = S.Gv[j][pix];
+    const float* gp = S.gpx[pix];
 #pragma unroll
-  for (int h = 16; h >= 1; h >>= 1) {
-    const bool up = lane & h;
-#pragma unroll
-    for (int i = 0; i < h; ++i) {
-      float send = up ? v[i] : v[i + h];
-      float keep = up ? v[i + h] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    for (int i = 0; i < 16; ++i) row[i] = 0.f;
+    row[16] = gp[1] * w;
+    row[17] = gp[2] * w;
+    row[18] = gp[3] * w;
+    row[19] = gp[0] * w;
+    if (COLOR) {
+      row[20] = gp[4] * w;
+      row[21] = gp[5] * w;
+      row[22] = gp[6] * w;
+    }
+    if (G != 0.f) {
+      const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
+      Blend b;
+      if (blend_of(r, px, py, xi, yi, s, s64, S64, b)) {  // same deterministic decision as phase A
+        const float dfp = G * s * sigmoidf_stable(-s * b.fp);
+        const float dfn = -G * s * sigmoidf_stable(-s * b.fn);
+        face_bwd(row, r, b.fip, px, py, dfp);
+        face_bwd(row, r, b.fin, px, py, dfn);
+      }
     }
   }
-  return v[0];
+  __syncwarp();
+  // segmented sum of the item rows into the per-splat rows (items sorted by splat)
+  if (lane < (COLOR ? 23 : 20)) {
+    int cur = -1;
+    float sum = 0.f;
+    for (int i = 0; i < m; ++i) {
+      const int jj = S.buf[warp][i] >> 8;
+      if (jj != cur) {
+        if (cur >= 0) S.acc[cur][lane] += sum;
+        cur = jj;
+        sum = 0.f;
+      }
+      sum += S.rows[warp][i][lane];
+    }
+    if (cur >= 0) S.acc[cur][lane] += sum;
+  }
+  __syncwarp();
 }
 
 template <bool COLOR>
-__global__ void __launch_bounds__(TS_TILE_PX) k_backward(
+__global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, const float* __restrict__ normal_map,
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
-  __shared__ Staged sh[kChB];
-  __shared__ float acc_s[kChB][kGr];
-  __shared__ float shc[COLOR ? kChB : 1][3];
-  __shared__ int maxproc_s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
   const int tile = blockIdx.x;
-  const int xi = (tile % tiles_x) * TS_TILE + (threadIdx.x & (TS_TILE - 1));
-  const int yi = (tile / tiles_x) * TS_TILE + (threadIdx.x / TS_TILE);
+  const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
+  const int pix = threadIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
   const bool inside = xi < W && yi < H;
   const int64_t lo = starts[tile];
   const int L = (int)(starts[tile + 1] - lo);
   const int32_t* list = (nonmono[tile] ? witems : items) + lo;
   const int64_t p = inside ? (int64_t)yi * W + xi : 0;
   const int nproc = inside ? n_proc[p] : 0;
-  if (threadIdx.x == 0) maxproc_s = 0;
+  if (threadIdx.x == 0) S.maxproc = 0;
   __syncthreads();
-  if (nproc > 0) atomicMax(&maxproc_s, nproc);
+  if (nproc > 0) atomicMax(&S.maxproc, nproc);
   float g_o = 0.f, g_d = 0.f, g_n[3] = {0.f, 0.f, 0.f}, g_c[3] = {0.f, 0.f, 0.f};
   float C_o = 0.f, C_d = 0.f, C_n[3] = {0.f, 0.f, 0.f}, C_c[3] = {0.f, 0.f, 0.f};
   if (inside) {
@@ -429,76 +554,108 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_backward(
       }
     }
   }
+  S.gpx[pix][0] = g_d;
+  S.gpx[pix][1] = g_n[0];
+  S.gpx[pix][2] = g_n[1];
+  S.gpx[pix][3] = g_n[2];
+  S.gpx[pix][4] = g_c[0];
+  S.gpx[pix][5] = g_c[1];
+  S.gpx[pix][6] = g_c[2];
   __syncthreads();
-  const int maxproc = maxproc_s;
+  const int maxproc = S.maxproc;
   float T = 1.f;
   Accum<COLOR> P;
   P.zero();
-  for (int base = 0; base < maxproc; base += kChB) {
-    const int n = min(kChB, maxproc - base);
+  unsigned nrect_unused = 0;
+  for (int base = 0; base < maxproc; base += kCh) {
+    const int n = min(kCh, maxproc - base);
     if (threadIdx.x < n) {
-      int k = list[base + threadIdx.x];
-      stage(recs, k, sh[threadIdx.x]);
+      const int k = list[base + threadIdx.x];
+      stage(recs, k, S.sh[threadIdx.x]);
       if (COLOR)
-        for (int c = 0; c < 3; ++c) shc[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
+        for (int c = 0; c < 3; ++c) S.col[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
     }
-    for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&acc_s[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
+    {
+      const unsigned m = __ballot_sync(0xffffffffu, nproc <= base);
+      if (lane == 0) S.skip[warp] = m;
+    }
     __syncthreads();
+    // ---- A: codes ---------------------------------------------------------------------
+    phase_codes(S.sh, n, tx0, ty0, W, H, s, s64, S64, S.skip, S.wv, nrect_unused);
+    __syncthreads();
+    // ---- B: pixel-serial prefix walk -> w, G ----------------------------------------------
     for (int j = 0; j < n; ++j) {
-      const Staged& r = sh[j];
-      float gr[32];
+      const int4 rr = *reinterpret_cast<const int4*>(&S.sh[j].rx0);
+      if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
+      if (base + j >= nproc) {  // past this pixel's early stop: no contribution
+        S.wv[j][pix] = 0.f;
+        continue;
+      }
+      const float c = S.wv[j][pix];
+      if (!code_blends(c)) continue;
+      float a, om;
+      bool cl;
+      decode(c, a, om, cl);
+      const Staged& r = S.sh[j];
+      const float* col = COLOR ? S.col[j] : nullptr;
+      const float w = __fmul_rn(T, a);
+      P.add(w, r, col);
+      float G = 0.f;
+      if (!cl) {
+        const float Tom = T * om;
+        G = g_o * (Tom - (C_o - P.o)) + g_d * (Tom * r.md - (C_d - P.d));
 #pragma unroll
-      for (int i = 0; i < 32; ++i) gr[i] = 0.f;
-      bool contrib = false;
-      if (base + j < nproc && xi >= r.rx0 && xi <= r.rx1 && yi >= r.ry0 && yi <= r.ry1) {
-        const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-        Blend bl;
-        if (blend_of(r, px, py, xi, yi, s, s64, S64, bl)) {
-          contrib = true;
-          const float* col = COLOR ? shc[j] : nullptr;
-          const float w = __fmul_rn(T, bl.a);
-          P.add(w, r, col);
-          gr[19] = g_d * w;
-          gr[16] = g_n[0] * w;
-          gr[17] = g_n[1] * w;
-          gr[18] = g_n[2] * w;
-          if (COLOR) {
-            gr[20] = g_c[0] * w;
-            gr[21] = g_c[1] * w;
-            gr[22] = g_c[2] * w;
+        for (int i = 0; i < 3; ++i) G += g_n[i] * (Tom * r.n[i] - (C_n[i] - P.n[i]));
+        if (COLOR)
+#pragma unroll
+          for (int i = 0; i < 3; ++i) G += g_c[i] * (Tom * col[i] - (C_c[i] - P.c[i]));
+      }
+      S.wv[j][pix] = w == 0.f ? -0.f : w;
+      S.Gv[j][pix] = G;
+      T = __fmul_rn(T, om);
+    }
+    __syncthreads();
+    // ---- C: compacted blended items per warp, 32 at a time ------------------------------
+    {
+      const int per = (n + kWarps - 1) / kWarps;
+      const int j0 = warp * per, j1 = min(n, j0 + per);
+      int cnt = 0;
+      for (int j = j0; j < j1; ++j) {
+        int x0, y0, nx, tot;
+        if (!tile_rect(S.sh[j], tx0, ty0, x0, y0, nx, tot)) continue;
+        const float inv = 1.0f / (float)nx;
+        for (int it0 = 0; it0 < tot; it0 += 32) {
+          const int it = it0 + lane;
+          int q = 0;
+          bool has = false;
+          if (it < tot) {
+            const int yy = (int)(((float)it + 0.5f) * inv);
+            const int xx = x0 + (it - yy * nx), yv = y0 + yy;
+            q = (yv - ty0) * TS_TILE + (xx - tx0);
+            has = xx < W && yv < H && code_blends(S.wv[j][q]);
           }
-          if (!bl.clipped) {
-            const float Tom = T * bl.om;
-            float G = g_o * (Tom - (C_o - P.o)) + g_d * (Tom * r.md - (C_d - P.d));
-#pragma unroll
-            for (int i = 0; i < 3; ++i) G += g_n[i] * (Tom * r.n[i] - (C_n[i] - P.n[i]));
-            if (COLOR)
-#pragma unroll
-              for (int i = 0; i < 3; ++i) G += g_c[i] * (Tom * col[i] - (C_c[i] - P.c[i]));
-            const float dfp = G * s * sigmoidf_stable(-s * bl.fp);
-            const float dfn = -G * s * sigmoidf_stable(-s * bl.fn);
-            const float g0 = (bl.fip == 0 ? dfp : 0.f) + (bl.fin == 0 ? dfn : 0.f);
-            const float g1 = (bl.fip == 1 ? dfp : 0.f) + (bl.fin == 1 ? dfn : 0.f);
-            const float g2 = (bl.fip == 2 ? dfp : 0.f) + (bl.fin == 2 ? dfn : 0.f);
-            const float g3 = (bl.fip == 3 ? dfp : 0.f) + (bl.fin == 3 ? dfn : 0.f);
-            if (bl.fip == 0 || bl.fin == 0) face_bwd<0>(r, px, py, g0, gr);
-            if (bl.fip == 1 || bl.fin == 1) face_bwd<1>(r, px, py, g1, gr);
-            if (bl.fip == 2 || bl.fin == 2) face_bwd<2>(r, px, py, g2, gr);
-            if (bl.fip == 3 || bl.fin == 3) face_bwd<3>(r, px, py, g3, gr);
+          const unsigned m = __ballot_sync(0xffffffffu, has);
+          if (has) S.buf[warp][cnt + __popc(m & ((1u << lane) - 1u))] = (j << 8) | q;
+          cnt += __popc(m);
+          __syncwarp();
+          if (cnt >= 32) {
+            process_items<COLOR>(S, 32, tx0, ty0, s, s64, S64);
+            const int rest = cnt - 32;
+            const int moved = lane < rest ? S.buf[warp][32 + lane] : 0;
+            __syncwarp();
+            if (lane < rest) S.buf[warp][lane] = moved;
+            cnt = rest;
+            __syncwarp();
           }
-          T = __fmul_rn(T, bl.om);
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
-        float tot = warp_transpose_reduce(gr);
-        const int lane = threadIdx.x & 31;
-        if (lane < (COLOR ? 23 : 20)) atomicAdd(&acc_s[j][lane], tot);
-      }
+      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, s, s64, S64);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += TS_TILE_PX) {
       float4* dst = reinterpret_cast<float4*>(rows + (lo + base + t) * kGr);
-      const float4* src = reinterpret_cast<const float4*>(&acc_s[t][0]);
+      const float4* src = reinterpret_cast<const float4*>(&S.acc[t][0]);
 #pragma unroll
       for (int i = 0; i < kGr / 4; ++i) dst[i] = src[i];
     }
@@ -528,7 +685,10 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
 #pragma unroll
       for (int i = 0; i < kGr / 4; ++i) {
         float4 q = __ldg(src + i);
-        a[4 * i] += q.x; a[4 * i + 1] += q.y; a[4 * i + 2] += q.z; a[4 * i + 3] += q.w;
+        a[4 * i] += q.x;
+        a[4 * i + 1] += q.y;
+        a[4 * i + 2] += q.z;
+        a[4 * i + 3] += q.w;
       }
     }
     double dF[4], dZ[4], dPx[4], dPy[4], dPos[4][3];
@@ -552,11 +712,11 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
     double det = tet_gradient(P, f, g, c1, c2, c3);
     double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
     if (gn >= 1e-8 && det != 0.0) {
-      double n[3] = {g[0] / gn, g[1] / gn, g[2] / gn};
+      double nn[3] = {g[0] / gn, g[1] / gn, g[2] / gn};
       double dn[3] = {a[16], a[17], a[18]};
-      double dot = n[0] * dn[0] + n[1] * dn[1] + n[2] * dn[2];
+      double dot = nn[0] * dn[0] + nn[1] * dn[1] + nn[2] * dn[2];
       double dg[3];
-      for (int i = 0; i < 3; ++i) dg[i] = (dn[i] - n[i] * dot) / gn;
+      for (int i = 0; i < 3; ++i) dg[i] = (dn[i] - nn[i] * dot) / gn;
       double d1 = (c1[0] * dg[0] + c1[1] * dg[1] + c1[2] * dg[2]) / det;
       double d2 = (c2[0] * dg[0] + c2[1] * dg[1] + c2[2] * dg[2]) / det;
       double d3 = (c3[0] * dg[0] + c3[1] * dg[1] + c3[2] * dg[2]) / det;
@@ -576,7 +736,8 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
                              -dPx[v] * cam.fx * X / (Z * Z) - dPy[v] * cam.fy * Y / (Z * Z) + dZ[v]};
       for (int j = 0; j < 3; ++j)
         dPos[v][j] += dpc[0] * cam.R[j] + dpc[1] * cam.R[3 + j] + dpc[2] * cam.R[6 + j];
-      red_add_v4(d_vert + (size_t)vid[v] * 4, (float)dF[v], (float)dPos[v][0], (float)dPos[v][1], (float)dPos[v][2]);
+      red_add_v4(d_vert + (size_t)vid[v] * 4, (float)dF[v], (float)dPos[v][0], (float)dPos[v][1],
+                 (float)dPos[v][2]);
     }
     if (COLOR) {
       const int64_t t = tet_ids[k];
@@ -588,7 +749,6 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
 }  // namespace ts
 
 using namespace ts;
-
 
 void ts_impl_window(int T, const BinsView& b, int64_t M, const double* md, int n_w, cudaStream_t st) {
   if (M <= 0) return;
@@ -620,25 +780,33 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
                       cudaStream_t st) {
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
+  static bool attr = false;
+  const int smem = (int)sizeof(BwdSmem);
+  if (!attr) {
+    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
   float* rows = nullptr;
   cudaMallocAsync(&rows, sizeof(float) * kGr * (size_t)M, st);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
-    k_backward<true><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
-                                              cam.width, cam.height, (float)s, s, maps[0], maps[1], maps[2], maps[3],
-                                              dmaps[0], dmaps[1], dmaps[2], dmaps[3], n_proc, rows);
+    k_backward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
+                                                 cam.width, cam.height, (float)s, s, maps[0], maps[1], maps[2],
+                                                 maps[3], dmaps[0], dmaps[1], dmaps[2], dmaps[3], n_proc, rows);
   else
-    k_backward<false><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64, tiles_x,
-                                               cam.width, cam.height, (float)s, s, maps[0], maps[1], maps[2], nullptr,
-                                               dmaps[0], dmaps[1], dmaps[2], nullptr, n_proc, rows);
+    k_backward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
+                                                  tiles_x, cam.width, cam.height, (float)s, s, maps[0], maps[1],
+                                                  maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2], nullptr, n_proc,
+                                                  rows);
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (color)
-    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform, make_grid(R), cam,
-                                          d_vert, d_color);
+    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform,
+                                          make_grid(R), cam, d_vert, d_color);
   else
-    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform, make_grid(R),
-                                           cam, d_vert, nullptr);
+    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform,
+                                           make_grid(R), cam, d_vert, nullptr);
   cudaFreeAsync(rows, st);
 }
 
