@@ -117,36 +117,40 @@ struct Hit {
   int fip, fin;
 };
 
-// 0: no hit, 1: hit, 2: undecided in FP32 (caller takes the exact FP64 path)
+__device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
+
+// 0: no hit, 1: hit, 2: undecided in FP32 (caller takes the exact FP64 path).
+// Branch-free over the four faces so a warp of different pixels never diverges here.
 __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hit& h) {
-  if (s.flags & 16u) return 2;
   const float band = s.band;
+  bool amb = (s.flags & 16u) != 0;
   int nh = 0, lo = -1, hi = -1;
   float zlo = 0.f, zhi = 0.f, flo = 0.f, fhi = 0.f;
 #pragma unroll
   for (int fi = 0; fi < 4; ++fi) {
-    if (!((s.flags >> fi) & 1u)) continue;
-    float u = fmaf(s.eux[fi], px, fmaf(s.euy[fi], py, s.cu[fi]));
-    float v = fmaf(s.evx[fi], px, fmaf(s.evy[fi], py, s.cv[fi]));
-    float w = s.adet[fi] - u - v;
-    if (u < -band || v < -band || w < -band) continue;
-    if (u <= band || v <= band || w <= band) return 2;
+    const float u = fmaf(s.eux[fi], px, fmaf(s.euy[fi], py, s.cu[fi]));
+    const float v = fmaf(s.evx[fi], px, fmaf(s.evy[fi], py, s.cv[fi]));
+    const float w = s.adet[fi] - u - v;
+    const bool valid = (s.flags >> fi) & 1u;
+    const bool out = !valid || u < -band || v < -band || w < -band;
+    const bool in = !out && u > band && v > band && w > band;
+    amb |= !out && !in;
     const int ia = face_vert(fi, 0), ib = face_vert(fi, 1), ic = face_vert(fi, 2);
-    float wa = w * s.iz[ia], wb = u * s.iz[ib], wc = v * s.iz[ic];
-    float D = wa + wb + wc;
-    float rD = 1.0f / D;
-    float zp = s.adet[fi] * rD;
-    float fh = (wa * s.df[ia] + wb * s.df[ib] + wc * s.df[ic]) * rD;
-    if (nh == 0) {
-      zlo = zhi = zp;
-      flo = fhi = fh;
-      lo = hi = fi;
-    } else {
-      if (zp < zlo) { zlo = zp; flo = fh; lo = fi; }
-      if (zp > zhi) { zhi = zp; fhi = fh; hi = fi; }
-    }
-    ++nh;
+    const float wa = w * s.iz[ia], wb = u * s.iz[ib], wc = v * s.iz[ic];
+    const float rD = frcp(wa + wb + wc);
+    const float zp = s.adet[fi] * rD;
+    const float fh = (wa * s.df[ia] + wb * s.df[ib] + wc * s.df[ic]) * rD;
+    const bool first = in && nh == 0;
+    const bool nlo = in && (first || zp < zlo), nhi = in && (first || zp > zhi);
+    zlo = nlo ? zp : zlo;
+    flo = nlo ? fh : flo;
+    lo = nlo ? fi : lo;
+    zhi = nhi ? zp : zhi;
+    fhi = nhi ? fh : fhi;
+    hi = nhi ? fi : hi;
+    nh += in ? 1 : 0;
   }
+  if (amb) return 2;
   if (nh < 2) return 0;
   h.fp = flo;
   h.fn = fhi;
@@ -276,28 +280,67 @@ __device__ __forceinline__ bool tile_rect(const Staged& r, int tx0, int ty0, int
   return true;
 }
 
-// Phase A: codes for every (rectangle pixel, splat) of the chunk; `skip` = pixel mask of
-// finished pixels (bit per pixel).  Warp w takes splats w, w + 8, ...
-__device__ __forceinline__ void phase_codes(const Staged* sh, int n, int tx0, int ty0, int W, int H, float s,
-                                            double s64, const Scene64& S, const uint32_t* skip, float (*code)[TS_TILE_PX],
-                                            unsigned& nrect) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < n; j += kWarps) {
-    const Staged& r = sh[j];
-    int x0, y0, nx, cnt;
-    if (!tile_rect(r, tx0, ty0, x0, y0, nx, cnt)) continue;
-    const float inv = 1.0f / (float)nx;
-    for (int it = lane; it < cnt; it += 32) {
-      const int yy = (int)(((float)it + 0.5f) * inv);
-      const int xi = x0 + (it - yy * nx), yi = y0 + yy;
-      const int pix = (yi - ty0) * TS_TILE + (xi - tx0);
-      if ((skip[pix >> 5] >> (pix & 31)) & 1u) continue;
-      if (xi >= W || yi >= H) continue;
-      ++nrect;
-      Blend b;
-      const bool bl = blend_of(r, (float)(xi - r.rx0) + 0.5f, (float)(yi - r.ry0) + 0.5f, xi, yi, s, s64, S, b);
-      code[j][pix] = encode(bl, b);
+// Per-chunk rectangle table: the (rectangle pixel, splat) pairs of the chunk flattened into
+// one index space so phase A runs on dense lanes (pairs per (tile, splat) are ~16 at
+// config 3, far below a warp).
+struct RectTab {
+  int x0[kCh], y0[kCh], nx[kCh];
+  float inv[kCh];
+  int pre[kCh + 1];  // exclusive prefix of pair counts
+};
+
+// called by thread t < n after staging sh[t]; then warp 0 scans (needs a barrier before)
+__device__ __forceinline__ void rect_entry(const Staged& r, int t, int tx0, int ty0, RectTab& R) {
+  int x0, y0, nx, cnt;
+  if (!tile_rect(r, tx0, ty0, x0, y0, nx, cnt)) {
+    nx = 1;
+    cnt = 0;
+    x0 = y0 = 0;
+  }
+  R.x0[t] = x0;
+  R.y0[t] = y0;
+  R.nx[t] = nx;
+  R.inv[t] = 1.0f / (float)nx;
+  R.pre[t + 1] = cnt;
+}
+
+__device__ __forceinline__ void rect_scan(RectTab& R, int n) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int v = lane < n ? R.pre[lane + 1] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
     }
+    if (lane < n) R.pre[lane + 1] = v;
+    if (lane == 0) R.pre[0] = 0;
+  }
+}
+
+// Phase A: codes for every (rectangle pixel, splat) of the chunk; `skip` = pixel mask of
+// finished pixels (bit per pixel).
+__device__ __forceinline__ void phase_codes(const Staged* sh, const RectTab& R, int n, int tx0, int ty0, int W, int H,
+                                            float s, double s64, const Scene64& S, const uint32_t* skip,
+                                            float (*code)[TS_TILE_PX], unsigned& nrect) {
+  const int total = R.pre[n];
+  for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
+    int j = 0;  // last j with pre[j] <= it (pre is non-decreasing, n <= 32)
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1)
+      if (j + step < n && R.pre[j + step] <= it) j += step;
+    const int local = it - R.pre[j];
+    const int nx = R.nx[j];
+    const int yy = (int)(((float)local + 0.5f) * R.inv[j]);
+    const int xi = R.x0[j] + (local - yy * nx), yi = R.y0[j] + yy;
+    const int pix = (yi - ty0) * TS_TILE + (xi - tx0);
+    if ((skip[pix >> 5] >> (pix & 31)) & 1u) continue;
+    if (xi >= W || yi >= H) continue;
+    ++nrect;
+    const Staged& r = sh[j];
+    Blend b;
+    const bool bl = blend_of(r, (float)(xi - r.rx0) + 0.5f, (float)(yi - r.ry0) + 0.5f, xi, yi, s, s64, S, b);
+    code[j][pix] = encode(bl, b);
   }
 }
 
@@ -312,6 +355,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   __shared__ float code[kCh][TS_TILE_PX];
   __shared__ float shc[COLOR ? kCh : 1][3];
   __shared__ uint32_t skip[TS_TILE_PX / 32];
+  __shared__ RectTab R;
   const int tile = blockIdx.x;
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x;
@@ -332,14 +376,19 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   }
   for (int base = 0; base < L; base += kCh) {
     const int n = min(kCh, L - base);
-    if (threadIdx.x < n) {
-      const int k = list[base + threadIdx.x];
-      stage(recs, k, sh[threadIdx.x]);
-      if (COLOR)
-        for (int c = 0; c < 3; ++c) shc[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
+    if (threadIdx.x < 32) {  // warp 0 stages the chunk and builds its rectangle table
+      if (threadIdx.x < n) {
+        const int k = list[base + threadIdx.x];
+        stage(recs, k, sh[threadIdx.x]);
+        rect_entry(sh[threadIdx.x], threadIdx.x, tx0, ty0, R);
+        if (COLOR)
+          for (int c = 0; c < 3; ++c) shc[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
+      }
+      __syncwarp();
+      rect_scan(R, n);
     }
     __syncthreads();
-    phase_codes(sh, n, tx0, ty0, W, H, s, s64, S64, skip, code, nrect);
+    phase_codes(sh, R, n, tx0, ty0, W, H, s, s64, S64, skip, code, nrect);
     __syncthreads();
     if (!done) {
       for (int j = 0; j < n; ++j) {
@@ -458,6 +507,7 @@ struct BwdSmem {
   int buf[kWarps][64];        // per-warp compacted items (j << 8 | pixel)
   float rows[kWarps][32][kGr];
   uint32_t skip[TS_TILE_PX / 32];
+  RectTab R;
   int maxproc;
 };
 
@@ -569,11 +619,16 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
   unsigned nrect_unused = 0;
   for (int base = 0; base < maxproc; base += kCh) {
     const int n = min(kCh, maxproc - base);
-    if (threadIdx.x < n) {
-      const int k = list[base + threadIdx.x];
-      stage(recs, k, S.sh[threadIdx.x]);
-      if (COLOR)
-        for (int c = 0; c < 3; ++c) S.col[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
+    if (threadIdx.x < 32) {
+      if (threadIdx.x < n) {
+        const int k = list[base + threadIdx.x];
+        stage(recs, k, S.sh[threadIdx.x]);
+        rect_entry(S.sh[threadIdx.x], threadIdx.x, tx0, ty0, S.R);
+        if (COLOR)
+          for (int c = 0; c < 3; ++c) S.col[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
+      }
+      __syncwarp();
+      rect_scan(S.R, n);
     }
     for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
     {
@@ -582,7 +637,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
     }
     __syncthreads();
     // ---- A: codes ---------------------------------------------------------------------
-    phase_codes(S.sh, n, tx0, ty0, W, H, s, s64, S64, S.skip, S.wv, nrect_unused);
+    phase_codes(S.sh, S.R, n, tx0, ty0, W, H, s, s64, S64, S.skip, S.wv, nrect_unused);
     __syncthreads();
     // ---- B: pixel-serial prefix walk -> w, G ----------------------------------------------
     for (int j = 0; j < n; ++j) {
