@@ -170,20 +170,24 @@ struct Blend {
 };
 
 // Exact replica of the reference decision chain in FP64 (_core.pyx:67-95, 35-36, 190-196).
-__device__ __noinline__ bool blend_exact(const Scene64& S, int k, int xi, int yi, double s, Blend& b) {
+// Returned by value (registers) so the caller's Blend never lives in local memory.
+struct ExactOut {
+  float fp, fn, d;
+  int faces;  // fip | fin << 4 | clipped << 8 | blended << 9
+};
+__device__ __noinline__ ExactOut blend_exact(const Scene64& S, int k, int xi, int yi, double s) {
+  ExactOut o{0.f, 0.f, 0.f, 0};
   double fp, fn;
   int i0, i1;
-  if (!splat_hits_exact(S, k, xi + 0.5, yi + 0.5, fp, fn, i0, i1)) return false;
+  if (!splat_hits_exact(S, k, xi + 0.5, yi + 0.5, fp, fn, i0, i1)) return o;
   double d = dsub(softplus_d(dmul(-s, fp)), softplus_d(dmul(-s, fn)));
   double a = dsub(1.0, exp(d));
-  if (a <= 0.0) return false;
-  b.fp = (float)fp;
-  b.fn = (float)fn;
-  b.fip = i0;
-  b.fin = i1;
-  b.clipped = a > 1.0 - 1e-4;
-  b.d = (float)d;
-  return true;
+  if (a <= 0.0) return o;
+  o.fp = (float)fp;
+  o.fn = (float)fn;
+  o.d = (float)d;
+  o.faces = i0 | (i1 << 4) | ((a > 1.0 - 1e-4) ? 256 : 0) | 512;
+  return o;
 }
 
 // FP32 fast path with error-bounded decisions; anything within the bounds of a decision
@@ -222,26 +226,32 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
   } else {
     atomicAdd(&g_ts_counters[0], 1ull);
   }
-  return blend_exact(S, r.k, xi, yi, s64, b);
+  const ExactOut o = blend_exact(S, r.k, xi, yi, s64);
+  b.fp = o.fp;
+  b.fn = o.fn;
+  b.d = o.d;
+  b.fip = o.faces & 15;
+  b.fin = (o.faces >> 4) & 15;
+  b.clipped = (o.faces & 256) != 0;
+  return (o.faces & 512) != 0;
 }
 
-// 4-byte code of a pair: +0 no blend, +1 clipped, d = log(1-alpha) <= -0 otherwise
-__device__ __forceinline__ float encode(bool blended, const Blend& b) {
-  if (!blended) return 0.f;
-  if (b.clipped) return 1.f;
-  return b.d > 0.f ? -0.f : (b.d == 0.f ? -0.f : b.d);
-}
-__device__ __forceinline__ bool code_blends(float c) { return __float_as_uint(c) != 0u; }
-__device__ __forceinline__ void decode(float c, float& a, float& om, bool& clipped) {
-  clipped = c > 0.f;
-  if (clipped) {
+// Per-pair code in two shared-memory words: alpha (+0 bits = no blend, -0 = blend with
+// alpha below FP32 range) and 1 - alpha (negative = clipped at ALPHA_CLIP).
+__device__ __forceinline__ void encode(bool blended, const Blend& b, float& a, float& om) {
+  if (!blended) {
+    a = 0.f;
+    om = 1.f;
+  } else if (b.clipped) {
     a = kAlphaClipF;
-    om = kOneMinusClipF;
+    om = -kOneMinusClipF;
   } else {
-    a = -expm1f(c);
-    om = expf(c);
+    const float av = -expm1f(b.d);
+    a = av > 0.f ? av : -0.f;
+    om = expf(b.d);
   }
 }
+__device__ __forceinline__ bool code_blends(float a) { return __float_as_uint(a) != 0u; }
 
 __device__ __forceinline__ float sigmoidf_stable(float x) {
   if (x >= 0.f) return 1.0f / (1.0f + expf(-x));
@@ -322,7 +332,8 @@ __device__ __forceinline__ void rect_scan(RectTab& R, int n) {
 // finished pixels (bit per pixel).
 __device__ __forceinline__ void phase_codes(const Staged* sh, const RectTab& R, int n, int tx0, int ty0, int W, int H,
                                             float s, double s64, const Scene64& S, const uint32_t* skip,
-                                            float (*code)[TS_TILE_PX], unsigned& nrect) {
+                                            float (*code_a)[TS_TILE_PX], float (*code_om)[TS_TILE_PX],
+                                            unsigned& nrect) {
   const int total = R.pre[n];
   for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
     int j = 0;  // last j with pre[j] <= it (pre is non-decreasing, n <= 32)
@@ -340,9 +351,21 @@ __device__ __forceinline__ void phase_codes(const Staged* sh, const RectTab& R, 
     const Staged& r = sh[j];
     Blend b;
     const bool bl = blend_of(r, (float)(xi - r.rx0) + 0.5f, (float)(yi - r.ry0) + 0.5f, xi, yi, s, s64, S, b);
-    code[j][pix] = encode(bl, b);
+    float a, om;
+    encode(bl, b, a, om);
+    code_a[j][pix] = a;
+    code_om[j][pix] = om;
   }
 }
+
+struct FwdSmem {
+  Staged sh[kCh];
+  float a[kCh][TS_TILE_PX];   // alpha per (splat, pixel) (+0 bits: no blend)
+  float om[kCh][TS_TILE_PX];  // 1 - alpha (negative: clipped)
+  float col[kCh][3];
+  uint32_t skip[TS_TILE_PX / 32];
+  RectTab R;
+};
 
 template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
@@ -351,11 +374,14 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, float* __restrict__ normal_map,
     float* __restrict__ depth_map, float* __restrict__ opacity_map, float* __restrict__ color_map,
     int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
-  __shared__ Staged sh[kCh];
-  __shared__ float code[kCh][TS_TILE_PX];
-  __shared__ float shc[COLOR ? kCh : 1][3];
-  __shared__ uint32_t skip[TS_TILE_PX / 32];
-  __shared__ RectTab R;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FwdSmem& FS = *reinterpret_cast<FwdSmem*>(smem_raw);
+  Staged* sh = FS.sh;
+  float (*code_a)[TS_TILE_PX] = FS.a;
+  float (*code_om)[TS_TILE_PX] = FS.om;
+  float (*shc)[3] = FS.col;
+  uint32_t* skip = FS.skip;
+  RectTab& R = FS.R;
   const int tile = blockIdx.x;
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x;
@@ -388,17 +414,15 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
       rect_scan(R, n);
     }
     __syncthreads();
-    phase_codes(sh, R, n, tx0, ty0, W, H, s, s64, S64, skip, code, nrect);
+    phase_codes(sh, R, n, tx0, ty0, W, H, s, s64, S64, skip, code_a, code_om, nrect);
     __syncthreads();
     if (!done) {
       for (int j = 0; j < n; ++j) {
         const int4 rr = *reinterpret_cast<const int4*>(&sh[j].rx0);
         if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
-        const float c = code[j][pix];
-        if (!code_blends(c)) continue;
-        float a, om;
-        bool cl;
-        decode(c, a, om, cl);
+        const float a = code_a[j][pix];
+        if (!code_blends(a)) continue;
+        const float om = fabsf(code_om[j][pix]);
         acc.add(__fmul_rn(T, a), sh[j], COLOR ? shc[j] : nullptr);
         T = __fmul_rn(T, om);
         ++nb;
@@ -637,7 +661,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
     }
     __syncthreads();
     // ---- A: codes ---------------------------------------------------------------------
-    phase_codes(S.sh, S.R, n, tx0, ty0, W, H, s, s64, S64, S.skip, S.wv, nrect_unused);
+    phase_codes(S.sh, S.R, n, tx0, ty0, W, H, s, s64, S64, S.skip, S.wv, S.Gv, nrect_unused);
     __syncthreads();
     // ---- B: pixel-serial prefix walk -> w, G ----------------------------------------------
     for (int j = 0; j < n; ++j) {
@@ -647,11 +671,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
         S.wv[j][pix] = 0.f;
         continue;
       }
-      const float c = S.wv[j][pix];
-      if (!code_blends(c)) continue;
-      float a, om;
-      bool cl;
-      decode(c, a, om, cl);
+      const float a = S.wv[j][pix];
+      if (!code_blends(a)) continue;
+      const float omc = S.Gv[j][pix];
+      const bool cl = omc < 0.f;
+      const float om = fabsf(omc);
       const Staged& r = S.sh[j];
       const float* col = COLOR ? S.col[j] : nullptr;
       const float w = __fmul_rn(T, a);
@@ -820,12 +844,20 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
                      const Scene64& S64, int W, int H, double s, float t_stop, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
+  static bool attr = false;
+  const int smem = (int)sizeof(FwdSmem);
+  if (!attr) {
+    cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
   if (colors && cmap)
-    k_forward<true><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x, W,
-                                             H, (float)s, s, t_stop, nmap, dmap, omap, cmap, n_proc, n_blend);
+    k_forward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
+                                                W, H, (float)s, s, t_stop, nmap, dmap, omap, cmap, n_proc, n_blend);
   else
-    k_forward<false><<<T, TS_TILE_PX, 0, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64, tiles_x,
-                                              W, H, (float)s, s, t_stop, nmap, dmap, omap, nullptr, n_proc, n_blend);
+    k_forward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
+                                                 tiles_x, W, H, (float)s, s, t_stop, nmap, dmap, omap, nullptr, n_proc,
+                                                 n_blend);
 }
 
 void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, int64_t K, const SplatRec* rec,
