@@ -165,7 +165,7 @@ __device__ __forceinline__ float softplus_tail(float x) { return log1pf(expf(-fa
 struct Blend {
   float fp, fn;  // SDF at entry / exit
   int fip, fin;  // entry / exit faces
-  float d;       // log(1 - alpha_unclipped)
+  float a, om;   // unclipped alpha and 1 - alpha
   bool clipped;  // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
 };
 
@@ -203,22 +203,26 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
     const float ftol = r.fband / fminf(r.adet[h.fip], r.adet[h.fin]) + r.ftol0;
     if (dfl < -ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
     if (dfl > ftol) {
+      // alpha = 1 - exp(sp(x) - sp(y)) = 1 - (1 + e^x) / (1 + e^y), x = -s fp, y = -s fn:
+      //   alpha = sigmoid(y) (1 - e^{x-y}),  1 - alpha = sigmoid(-y) + sigmoid(y) e^{x-y}
+      // (no logarithms, no cancellation: x - y = -s (fp - fn) from the exact-ish deltas)
       const float fp = r.f0 + h.fp, fn = r.f0 + h.fn;
-      const float x = -s * fp, y = -s * fn;
-      float d;
-      if (x > 0.f && y > 0.f)
-        d = -s * dfl + (softplus_tail(x) - softplus_tail(y));
-      else
-        d = (fmaxf(x, 0.f) + softplus_tail(x)) - (fmaxf(y, 0.f) + softplus_tail(y));
-      const float a_un = -expm1f(d);
+      const float y = -s * fn, t = s * dfl;
+      const float ey = expf(-fabsf(y));
+      const float ry = frcp(1.0f + ey);
+      const float sy = y >= 0.f ? ry : ey * ry;   // sigmoid(y)
+      const float sny = y >= 0.f ? ey * ry : ry;  // sigmoid(-y)
+      const float q = expf(-t);
+      const float a_un = sy * (t < 0.25f ? -expm1f(-t) : 1.0f - q);
       // alpha > 1e-10 and not at the clip threshold: the FP64 reference decides the same
-      if (d < -1e-10f && fabsf(a_un - kAlphaClipF) > 2e-6f) {
+      if (a_un > 1e-10f && fabsf(a_un - kAlphaClipF) > 2e-6f) {
         b.fp = fp;
         b.fn = fn;
         b.fip = h.fip;
         b.fin = h.fin;
         b.clipped = a_un > kAlphaClipF;
-        b.d = d;
+        b.a = a_un;
+        b.om = fmaf(sy, q, sny);
         return true;
       }
     }
@@ -229,7 +233,8 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
   const ExactOut o = blend_exact(S, r.k, xi, yi, s64);
   b.fp = o.fp;
   b.fn = o.fn;
-  b.d = o.d;
+  b.a = -expm1f(o.d);
+  b.om = expf(o.d);
   b.fip = o.faces & 15;
   b.fin = (o.faces >> 4) & 15;
   b.clipped = (o.faces & 256) != 0;
@@ -246,9 +251,8 @@ __device__ __forceinline__ void encode(bool blended, const Blend& b, float& a, f
     a = kAlphaClipF;
     om = -kOneMinusClipF;
   } else {
-    const float av = -expm1f(b.d);
-    a = av > 0.f ? av : -0.f;
-    om = expf(b.d);
+    a = b.a > 0.f ? b.a : -0.f;
+    om = b.om;
   }
 }
 __device__ __forceinline__ bool code_blends(float a) { return __float_as_uint(a) != 0u; }
