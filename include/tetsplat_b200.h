@@ -128,6 +128,10 @@ int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution
  * last reset).  [sync] */
 int ts_debug_counters(uint64_t* out4, int reset);
 
+/* Diagnostics for timing experiments only: bit 0 skips the exact FP64 re-decisions
+ * (results then no longer match the reference).  Default 0. */
+int ts_debug_set_flags(int flags);
+
 #ifdef __cplusplus
 }
 #endif

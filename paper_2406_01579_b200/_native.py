@@ -64,6 +64,7 @@ def lib():
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),
         "ts_marching_tets": ([P, P, I32, P, P, PI64, P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
+        "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

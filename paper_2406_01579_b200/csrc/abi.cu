@@ -251,4 +251,9 @@ int ts_debug_counters(uint64_t* out4, int reset) {
   return check_cuda("ts_debug_counters");
 }
 
+int ts_debug_set_flags(int flags) {
+  ts_impl_debug_flags(flags);
+  return check_cuda("ts_debug_set_flags");
+}
+
 }  // extern "C"

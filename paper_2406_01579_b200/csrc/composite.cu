@@ -63,6 +63,8 @@ static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 // diagnostics: [0] pairs re-decided in FP64 at a face edge / degenerate face,
 // [1] pairs re-decided in FP64 at an alpha threshold, [2] forward rectangle-pass pairs
 __device__ unsigned long long g_ts_counters[4];
+// diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity)
+__device__ int g_ts_debug_flags;
 
 __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, Staged& s) {
   const float4* p = reinterpret_cast<const float4*>(recs + k);
@@ -230,6 +232,7 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
   } else {
     atomicAdd(&g_ts_counters[0], 1ull);
   }
+  if (g_ts_debug_flags & 1) return false;
   const ExactOut o = blend_exact(S, r.k, xi, yi, s64);
   b.fp = o.fp;
   b.fn = o.fn;
@@ -908,3 +911,5 @@ void ts_impl_counters(unsigned long long out[4], int reset) {
     cudaMemcpyToSymbol(g_ts_counters, z, sizeof(z));
   }
 }
+
+void ts_impl_debug_flags(int flags) { cudaMemcpyToSymbol(g_ts_debug_flags, &flags, sizeof(int)); }

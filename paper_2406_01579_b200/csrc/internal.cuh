@@ -72,3 +72,4 @@ int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
 void ts_impl_counters(unsigned long long out[4], int reset);
+void ts_impl_debug_flags(int flags);
