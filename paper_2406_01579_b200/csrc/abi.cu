@@ -175,28 +175,43 @@ static BinsView bv_of(const ts_bins* b) {
   return BinsView{b->starts, b->splat_off, b->items, b->pos_of, b->nonmono, b->witems};
 }
 
-int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
-                      const ts_camera* cam, int32_t n_w, double s, double t_stop, float* nmap, float* dmap,
-                      float* omap, float* cmap, int32_t* n_proc, int32_t* n_blend, void* stream) {
+int ts_forward_prepare(const ts_scene* sc, int64_t K, const ts_bins* b, int64_t M, const ts_camera* cam, int32_t n_w,
+                       int64_t* item_off, int64_t* out_pairs, void* stream) {
   if (n_w < 1) return fail(TS_EINVAL, "resorting window must be >= 1");
-  if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0)
+  if (!sc || !b || !cam || !item_off || !out_pairs || K < 0 || M < 0)
+    return fail(TS_EINVAL, "ts_forward_prepare: bad arguments");
+  int tx, ty;
+  if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  keep_pool_warm();
+  *out_pairs = ts_impl_forward_prepare(tx, ty, bv_of(b), M, sc->mean_depth, n_w,
+                                       reinterpret_cast<const SplatRec*>(sc->records), item_off, ST(stream));
+  return check_cuda("ts_forward_prepare");
+}
+
+int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
+                      const ts_camera* cam, double s, double t_stop, const int64_t* item_off, void* pair_code,
+                      void* pair_sig, uint8_t* pair_faces, float* nmap, float* dmap, float* omap, float* cmap,
+                      int32_t* n_proc, int32_t* n_blend, void* stream) {
+  if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0 ||
+      (M > 0 && (!item_off || !pair_code || !pair_sig || !pair_faces)))
     return fail(TS_EINVAL, "ts_render_forward: bad arguments");
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
-  cudaStream_t st = ST(stream);
   keep_pool_warm();
-  BinsView bv = bv_of(b);
-  ts_impl_window(tx * ty, bv, M, sc->mean_depth, n_w, st);
-  ts_impl_forward(tx, ty, bv, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
-                  cam->height, s, (float)t_stop, nmap, dmap, omap, cmap, n_proc, n_blend, st);
+  ts_impl_forward(tx, ty, bv_of(b), reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
+                  cam->height, s, (float)t_stop, item_off, reinterpret_cast<float2*>(pair_code),
+                  reinterpret_cast<float2*>(pair_sig), pair_faces, nmap, dmap, omap, cmap, n_proc, n_blend,
+                  ST(stream));
   return check_cuda("ts_render_forward");
 }
 
 int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
-                       const ts_camera* cam, double s, const float* const maps[4], const float* const dmaps[4],
+                       const ts_camera* cam, const int64_t* item_off, const void* pair_code, const void* pair_sig,
+                       const uint8_t* pair_faces, const float* const maps[4], const float* const dmaps[4],
                        const int32_t* n_proc, const double* deform, int32_t R, float* d_vert, float* d_color,
                        void* stream) {
-  if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert || R < 1 || K < 0 || M < 0)
+  if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert || R < 1 || K < 0 || M < 0 ||
+      (M > 0 && (!item_off || !pair_code || !pair_sig || !pair_faces)))
     return fail(TS_EINVAL, "ts_render_backward: bad arguments");
   for (int i = 0; i < 3; ++i)
     if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward: missing map");
@@ -205,9 +220,10 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
   keep_pool_warm();
   const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
-  ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc),
-                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), s, m4, d4, n_proc, d_vert, d_color,
-                   ST(stream));
+  ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, sc->f,
+                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), item_off,
+                   reinterpret_cast<const float2*>(pair_code), reinterpret_cast<const float2*>(pair_sig), pair_faces,
+                   m4, d4, n_proc, d_vert, d_color, ST(stream));
   return check_cuda("ts_render_backward");
 }
 

@@ -1,51 +1,54 @@
 // composite.cu — K6 forward compositing, K7 backward + vertex chain, N_w window.
 //
-// One 256-thread CTA per 16x16 tile.  The tile's list is staged through shared memory in
-// chunks of kCh records.  Each chunk runs in phases that keep all 32 lanes busy:
+// One 256-thread CTA per 16x16 tile; the tile's list is processed in chunks of up to kCh
+// splats whose (pixel, splat) PAIRS — the pixels of each splat's pixel rectangle inside the
+// tile (the reference's inclusive bbox test, _core.pyx:80, made exact at setup) — are
+// flattened into one index space of at most kCap pairs.  Every pair of the view has a
+// global index: item_off[list position] + local index in the rectangle (k_item_counts).
 //
-//  A (splat-parallel): each warp walks the pixels of its splats' pixel rectangles (the
-//    reference's inclusive bbox test, _core.pyx:80, made exact in FP64 at setup) and decides
-//    hit + opacity for every (pixel, splat) pair, writing a 4-byte code per pair to shared
-//    memory: no blend / clipped / d = log(1 - alpha).  The decision is FP32 on sign-normalised
-//    edge functions in splat-anchored coordinates; any pair within a rigorous FP32 error band
-//    of a decision threshold (face edge, alpha = 0, alpha = ALPHA_CLIP) is re-decided with the
-//    reference's exact FP64 arithmetic (records.cuh: splat_hits_exact), so the set of blended
-//    pairs matches the FP64 reference.
-//  B (pixel-serial): each thread blends its pixel's codes front to back (Eq. 2,
-//    _core.pyx:189-213) with early stop at T < t_stop; the CTA leaves when all pixels stopped.
-//
-// The per-pixel loop of the reference (_core.pyx:158-229) touches every list entry of the
-// tile; here the expensive hit test runs only on rectangle pixels (dense lanes) and the
-// per-pixel walk is a 16-byte shared-memory rectangle test plus a 4-byte code read.
+// Forward (forward_tiles, _core.pyx:98-229):
+//  A (pair-parallel, dense lanes): hit + opacity of every pair.  FP32 on sign-normalised
+//    edge functions in splat-anchored coordinates; any pair within a rigorous FP32 error
+//    band of a decision threshold (face edge, alpha = 0, alpha = ALPHA_CLIP, tiny alpha)
+//    is re-decided with the reference's exact FP64 arithmetic (records.cuh:
+//    splat_hits_exact), so the blended set matches the FP64 reference.  The pair's
+//    (alpha, 1-alpha) goes to shared memory for phase B and, with s*sigmoid(-s f) of the
+//    entry/exit points and the two face ids, to the global pair records the backward
+//    reads — the backward never re-evaluates a hit.
+//  B (pixel-serial): each thread blends its pixel's pairs front to back (Eq. 2,
+//    _core.pyx:189-213) with early stop at T < t_stop; a finished pixel's later pairs are
+//    skipped by phase A; the CTA leaves when all its pixels stopped.
 //
 // The N_w resorting window (_core.pyx:171-187) pops the same sequence for every pixel of a
 // tile — it depends only on the list.  When mean depth is non-decreasing along the list
 // (bin.cu flags it) the window is the identity; otherwise k_window replays it per tile.
 //
 // Backward (backward_tiles _core.pyx:344-471 + splat_grads_to_vertices raster.py:253-306):
-//  A as above;
+//  load: the chunk's pair records (contiguous in global memory) into shared memory;
 //  B (pixel-serial, FRONT to back): w = T a and the d_alpha chain
 //      G = sum_ch g_ch (T x_ch (1-a) - S_ch),  S_ch = C_final,ch - prefix_ch (inclusive)
-//    which is the reference's d_alpha * (1 - a) with the suffix sums taken from the forward
-//    maps — no division by 1-a, no reverse walk, no per-pixel record lists;
-//  C (item-parallel): each warp compacts the blended (pixel, splat) items of its splats
-//    (ballot) and processes them 32 at a time — face-hit backward (_core.pyx:295-341) into
-//    a 24-float row per item — then a segmented sum over the item rows into the per-(tile,
-//    splat) gradient row.  Rows are written per list position; k_chain gathers each splat's
-//    rows in a fixed order (deterministic, atomic-free), applies the normal and camera chains
-//    in FP64 and scatters to vertices with one red.global.add.v4.f32 per (splat, vertex).
+//    = the reference's d_alpha * (1 - a) with the suffix sums taken from the forward maps —
+//    no division by 1-a, no reverse walk, no per-pixel record lists;
+//  C (item-parallel): each warp compacts the blended pairs of its splats (ballot) and
+//    processes them 32 at a time — face-hit backward (_core.pyx:295-341) into a 24-float
+//    row per item — then a segmented sum into the per-(tile, splat) gradient row, written
+//    per list position.  k_chain gathers each splat's rows in a fixed order (deterministic,
+//    atomic-free), applies the normal and camera chains in FP64 and scatters to vertices
+//    with one red.global.add.v4.f32 per (splat, vertex).
 #include "internal.cuh"
+#include "scan.cuh"
 
 namespace ts {
 
 constexpr float kAlphaClipF = 0.9999f;  // splat.py:14
 constexpr float kOneMinusClipF = 1e-4f;
-constexpr int kCh = 32;   // records per shared-memory stage
-constexpr int kGr = 24;   // floats per (tile, splat) gradient row
+constexpr int kCh = 32;      // max splats per chunk
+constexpr int kCap = 2048;   // max (pixel, splat) pairs per chunk
+constexpr int kGr = 24;      // floats per (tile, splat) gradient row
 constexpr int kWarps = TS_TILE_PX / 32;
 
 struct __align__(16) Staged {
-  int rx0, rx1, ry0, ry1;  // pixel rectangle (inclusive)
+  int rx0, rx1, ry0, ry1;  // pixel rectangle (inclusive, clipped to the image)
   float band;
   uint32_t flags;
   int k;
@@ -53,7 +56,7 @@ struct __align__(16) Staged {
   float iz[4], df[4];  // 1/z; f_i - f_0
   float eux[4], euy[4], cu[4], evx[4], evy[4], cv[4], adet[4];
   float n[3];
-  float fband;  // 0.75 band (z_max/z_min) spread(f): FP32 (f_hit - f0) error <= fband / |det_face|
+  float fband;  // FP32 (f_hit - f0) error <= fband / |det_face| (see stage())
   float ftol0;  // rounding of the stored f deltas
   float f0;
   float pad[2];
@@ -61,10 +64,12 @@ struct __align__(16) Staged {
 static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 
 // diagnostics: [0] pairs re-decided in FP64 at a face edge / degenerate face,
-// [1] pairs re-decided in FP64 at an alpha threshold, [2] forward rectangle-pass pairs
+// [1] pairs re-decided in FP64 at an alpha threshold, [2] forward pairs evaluated
 __device__ unsigned long long g_ts_counters[4];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity)
 __device__ int g_ts_debug_flags;
+
+__device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
 
 __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, Staged& s) {
   const float4* p = reinterpret_cast<const float4*>(recs + k);
@@ -107,6 +112,9 @@ __device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, 
     s.cv[fi] = -(evx * vx[ia] + evy * vy[ia]);
     s.adet[fi] = fabsf(det);
   }
+  // f_hit - f0 = sum(lambda_i df_i): with edge-function errors E <= band/16 the barycentric
+  // error is <= 4 E (z_max/z_min) / |det|, i.e. 0.25 band zr spread / |det| per face and
+  // 0.5 band zr spread / |det| for f_prev - f_next; 0.75 keeps a 1.5x margin.
   float fmax = fmaxf(fabsf(s.df[1]), fmaxf(fabsf(s.df[2]), fabsf(s.df[3])));
   float izmin = fminf(fminf(s.iz[0], s.iz[1]), fminf(s.iz[2], s.iz[3]));
   float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
@@ -118,8 +126,6 @@ struct Hit {
   float fp, fn;  // f - f0 at entry / exit
   int fip, fin;
 };
-
-__device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
 
 // 0: no hit, 1: hit, 2: undecided in FP32 (caller takes the exact FP64 path).
 // Branch-free over the four faces so a warp of different pixels never diverges here.
@@ -161,14 +167,18 @@ __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hi
   return 1;
 }
 
-__device__ __forceinline__ float softplus_tail(float x) { return log1pf(expf(-fabsf(x))); }
+__device__ __forceinline__ float sigmoidf_stable(float x) {
+  if (x >= 0.f) return 1.0f / (1.0f + expf(-x));
+  float e = expf(x);
+  return e / (1.0f + e);
+}
 
-// Outcome of one (pixel, splat) pair: whether it blends, and the values the blend uses.
+// Outcome of one (pixel, splat) pair.
 struct Blend {
-  float fp, fn;  // SDF at entry / exit
-  int fip, fin;  // entry / exit faces
-  float a, om;   // unclipped alpha and 1 - alpha
-  bool clipped;  // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
+  float a, om;    // unclipped alpha and 1 - alpha
+  float sp, sn;   // s * sigmoid(-s f_prev), s * sigmoid(-s f_next): d alpha / d f factors
+  int fip, fin;   // entry / exit faces
+  bool clipped;   // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
 };
 
 // Exact replica of the reference decision chain in FP64 (_core.pyx:67-95, 35-36, 190-196).
@@ -193,8 +203,7 @@ __device__ __noinline__ ExactOut blend_exact(const Scene64& S, int k, int xi, in
 }
 
 // FP32 fast path with error-bounded decisions; anything within the bounds of a decision
-// threshold (face edges, alpha == 0, alpha == ALPHA_CLIP, tiny alpha) is re-decided by
-// blend_exact so the blended set matches the FP64 reference.
+// threshold is re-decided by blend_exact so the blended set matches the FP64 reference.
 __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, int xi, int yi, float s, double s64,
                                          const Scene64& S, Blend& b) {
   Hit h;
@@ -207,24 +216,25 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
     if (dfl > ftol) {
       // alpha = 1 - exp(sp(x) - sp(y)) = 1 - (1 + e^x) / (1 + e^y), x = -s fp, y = -s fn:
       //   alpha = sigmoid(y) (1 - e^{x-y}),  1 - alpha = sigmoid(-y) + sigmoid(y) e^{x-y}
-      // (no logarithms, no cancellation: x - y = -s (fp - fn) from the exact-ish deltas)
-      const float fp = r.f0 + h.fp, fn = r.f0 + h.fn;
+      // (no logarithms, no cancellation: x - y = -s (fp - fn) from the delta samples)
+      const float fn = r.f0 + h.fn;
       const float y = -s * fn, t = s * dfl;
       const float ey = expf(-fabsf(y));
       const float ry = frcp(1.0f + ey);
       const float sy = y >= 0.f ? ry : ey * ry;   // sigmoid(y)
       const float sny = y >= 0.f ? ey * ry : ry;  // sigmoid(-y)
-      const float q = expf(-t);
+      const float q = expf(-t);                    // e^{x-y}
       const float a_un = sy * (t < 0.25f ? -expm1f(-t) : 1.0f - q);
       // alpha > 1e-10 and not at the clip threshold: the FP64 reference decides the same
       if (a_un > 1e-10f && fabsf(a_un - kAlphaClipF) > 2e-6f) {
-        b.fp = fp;
-        b.fn = fn;
+        b.a = a_un;
+        b.om = fmaf(sy, q, sny);
+        b.sn = s * sy;
+        // sigmoid(x) = 1 / (1 + e^{-x}), e^{-x} = e^{-y} / q
+        b.sp = s * (y >= 0.f ? q * frcp(q + ey) : ey * q * frcp(ey * q + 1.0f));
         b.fip = h.fip;
         b.fin = h.fin;
         b.clipped = a_un > kAlphaClipF;
-        b.a = a_un;
-        b.om = fmaf(sy, q, sny);
         return true;
       }
     }
@@ -234,37 +244,24 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
   }
   if (g_ts_debug_flags & 1) return false;
   const ExactOut o = blend_exact(S, r.k, xi, yi, s64);
-  b.fp = o.fp;
-  b.fn = o.fn;
   b.a = -expm1f(o.d);
   b.om = expf(o.d);
+  b.sp = s * sigmoidf_stable(-s * o.fp);
+  b.sn = s * sigmoidf_stable(-s * o.fn);
   b.fip = o.faces & 15;
   b.fin = (o.faces >> 4) & 15;
   b.clipped = (o.faces & 256) != 0;
   return (o.faces & 512) != 0;
 }
 
-// Per-pair code in two shared-memory words: alpha (+0 bits = no blend, -0 = blend with
-// alpha below FP32 range) and 1 - alpha (negative = clipped at ALPHA_CLIP).
-__device__ __forceinline__ void encode(bool blended, const Blend& b, float& a, float& om) {
-  if (!blended) {
-    a = 0.f;
-    om = 1.f;
-  } else if (b.clipped) {
-    a = kAlphaClipF;
-    om = -kOneMinusClipF;
-  } else {
-    a = b.a > 0.f ? b.a : -0.f;
-    om = b.om;
-  }
+// Pair code: alpha (+0 bits = no blend, -0 = blended with alpha below FP32 range) and
+// 1 - alpha (negative = clipped at ALPHA_CLIP).
+__device__ __forceinline__ float2 encode(bool blended, const Blend& b) {
+  if (!blended) return make_float2(0.f, 1.f);
+  if (b.clipped) return make_float2(kAlphaClipF, -kOneMinusClipF);
+  return make_float2(b.a > 0.f ? b.a : -0.f, b.om);
 }
 __device__ __forceinline__ bool code_blends(float a) { return __float_as_uint(a) != 0u; }
-
-__device__ __forceinline__ float sigmoidf_stable(float x) {
-  if (x >= 0.f) return 1.0f / (1.0f + expf(-x));
-  float e = expf(x);
-  return e / (1.0f + e);
-}
 
 template <int NC>
 struct Accum {
@@ -286,89 +283,85 @@ struct Accum {
   }
 };
 
-// rectangle of splat r inside the tile; false when empty
-__device__ __forceinline__ bool tile_rect(const Staged& r, int tx0, int ty0, int& x0, int& y0, int& nx, int& cnt) {
-  x0 = max(r.rx0, tx0);
-  y0 = max(r.ry0, ty0);
-  const int x1 = min(r.rx1, tx0 + TS_TILE - 1), y1 = min(r.ry1, ty0 + TS_TILE - 1);
+// rectangle of a splat (packed int16 record rect) inside the tile; false when empty
+__device__ __forceinline__ bool tile_rect(int rx0, int rx1, int ry0, int ry1, int tx0, int ty0, int& x0, int& y0,
+                                          int& nx, int& cnt) {
+  x0 = max(rx0, tx0);
+  y0 = max(ry0, ty0);
+  const int x1 = min(rx1, tx0 + TS_TILE - 1), y1 = min(ry1, ty0 + TS_TILE - 1);
   if (x0 > x1 || y0 > y1) return false;
   nx = x1 - x0 + 1;
   cnt = nx * (y1 - y0 + 1);
   return true;
 }
 
-// Per-chunk rectangle table: the (rectangle pixel, splat) pairs of the chunk flattened into
-// one index space so phase A runs on dense lanes (pairs per (tile, splat) are ~16 at
-// config 3, far below a warp).
+// Per-chunk pair table.
 struct RectTab {
   int x0[kCh], y0[kCh], nx[kCh];
   float inv[kCh];
   int pre[kCh + 1];  // exclusive prefix of pair counts
+  int n;             // splats in this chunk
+  int64_t ib0;       // global index of the chunk's first pair
 };
 
-// called by thread t < n after staging sh[t]; then warp 0 scans (needs a barrier before)
-__device__ __forceinline__ void rect_entry(const Staged& r, int t, int tx0, int ty0, RectTab& R) {
-  int x0, y0, nx, cnt;
-  if (!tile_rect(r, tx0, ty0, x0, y0, nx, cnt)) {
-    nx = 1;
-    cnt = 0;
-    x0 = y0 = 0;
-  }
-  R.x0[t] = x0;
-  R.y0[t] = y0;
-  R.nx[t] = nx;
-  R.inv[t] = 1.0f / (float)nx;
-  R.pre[t + 1] = cnt;
-}
-
-__device__ __forceinline__ void rect_scan(RectTab& R, int n) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int v = lane < n ? R.pre[lane + 1] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
+// Warp 0 only: stage up to kCh records from list position `base` (at most `avail`) and cut
+// the chunk so it holds at most kCap pairs.
+__device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, int base, int avail,
+                                            const SplatRec* __restrict__ recs, const float* __restrict__ colors,
+                                            bool color, Staged* sh, float (*col)[3], RectTab& R, int tx0, int ty0,
+                                            const int64_t* __restrict__ item_off_tile) {
+  const int lane = threadIdx.x;
+  const int m = min(kCh, avail);
+  int cnt = 0;
+  if (lane < m) {
+    const int k = list[base + lane];
+    stage(recs, k, sh[lane]);
+    const Staged& r = sh[lane];
+    int x0, y0, nx;
+    if (!tile_rect(r.rx0, r.rx1, r.ry0, r.ry1, tx0, ty0, x0, y0, nx, cnt)) {
+      nx = 1;
+      cnt = 0;
+      x0 = y0 = 0;
     }
-    if (lane < n) R.pre[lane + 1] = v;
-    if (lane == 0) R.pre[0] = 0;
+    R.x0[lane] = x0;
+    R.y0[lane] = y0;
+    R.nx[lane] = nx;
+    R.inv[lane] = 1.0f / (float)nx;
+    if (color)
+      for (int c = 0; c < 3; ++c) col[lane][c] = colors[(int64_t)k * 3 + c];
+  }
+  int v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane < m) R.pre[lane + 1] = v;
+  // cut: the largest prefix with at most kCap pairs (one splat has <= 256 pairs)
+  const unsigned ok = __ballot_sync(0xffffffffu, lane < m && v <= kCap);
+  if (lane == 0) {
+    R.pre[0] = 0;
+    R.n = __popc(ok);
+    R.ib0 = item_off_tile[base];
   }
 }
 
-// Phase A: codes for every (rectangle pixel, splat) of the chunk; `skip` = pixel mask of
-// finished pixels (bit per pixel).
-__device__ __forceinline__ void phase_codes(const Staged* sh, const RectTab& R, int n, int tx0, int ty0, int W, int H,
-                                            float s, double s64, const Scene64& S, const uint32_t* skip,
-                                            float (*code_a)[TS_TILE_PX], float (*code_om)[TS_TILE_PX],
-                                            unsigned& nrect) {
-  const int total = R.pre[n];
-  for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
-    int j = 0;  // last j with pre[j] <= it (pre is non-decreasing, n <= 32)
+// last j with pre[j] <= it (pre is non-decreasing, n <= 32)
+__device__ __forceinline__ int pair_splat(const RectTab& R, int n, int it) {
+  int j = 0;
 #pragma unroll
-    for (int step = 16; step >= 1; step >>= 1)
-      if (j + step < n && R.pre[j + step] <= it) j += step;
-    const int local = it - R.pre[j];
-    const int nx = R.nx[j];
-    const int yy = (int)(((float)local + 0.5f) * R.inv[j]);
-    const int xi = R.x0[j] + (local - yy * nx), yi = R.y0[j] + yy;
-    const int pix = (yi - ty0) * TS_TILE + (xi - tx0);
-    if ((skip[pix >> 5] >> (pix & 31)) & 1u) continue;
-    if (xi >= W || yi >= H) continue;
-    ++nrect;
-    const Staged& r = sh[j];
-    Blend b;
-    const bool bl = blend_of(r, (float)(xi - r.rx0) + 0.5f, (float)(yi - r.ry0) + 0.5f, xi, yi, s, s64, S, b);
-    float a, om;
-    encode(bl, b, a, om);
-    code_a[j][pix] = a;
-    code_om[j][pix] = om;
-  }
+  for (int step = 16; step >= 1; step >>= 1)
+    if (j + step < n && R.pre[j + step] <= it) j += step;
+  return j;
+}
+
+__device__ __forceinline__ int pair_index(const RectTab& R, int j, int xi, int yi) {
+  return R.pre[j] + (yi - R.y0[j]) * R.nx[j] + (xi - R.x0[j]);
 }
 
 struct FwdSmem {
   Staged sh[kCh];
-  float a[kCh][TS_TILE_PX];   // alpha per (splat, pixel) (+0 bits: no blend)
-  float om[kCh][TS_TILE_PX];  // 1 - alpha (negative: clipped)
+  float2 code[kCap];  // (alpha, 1 - alpha) per pair of the chunk
   float col[kCh][3];
   uint32_t skip[TS_TILE_PX / 32];
   RectTab R;
@@ -378,17 +371,12 @@ template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-    Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, float* __restrict__ normal_map,
-    float* __restrict__ depth_map, float* __restrict__ opacity_map, float* __restrict__ color_map,
-    int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
+    Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, const int64_t* __restrict__ item_off,
+    float2* __restrict__ pair_code, float2* __restrict__ pair_sig, uint8_t* __restrict__ pair_faces,
+    float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
+    float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FwdSmem& FS = *reinterpret_cast<FwdSmem*>(smem_raw);
-  Staged* sh = FS.sh;
-  float (*code_a)[TS_TILE_PX] = FS.a;
-  float (*code_om)[TS_TILE_PX] = FS.om;
-  float (*shc)[3] = FS.col;
-  uint32_t* skip = FS.skip;
-  RectTab& R = FS.R;
+  FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
   const int tile = blockIdx.x;
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x;
@@ -400,38 +388,51 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   float T = 1.f;
   Accum<COLOR> acc;
   acc.zero();
-  unsigned nrect = 0;
+  unsigned npairs = 0;
   bool done = !inside;
   int nproc = inside ? L : 0, nb = 0;
   {
     const unsigned m = __ballot_sync(0xffffffffu, done);
-    if ((threadIdx.x & 31) == 0) skip[threadIdx.x >> 5] = m;
+    if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
   }
-  for (int base = 0; base < L; base += kCh) {
-    const int n = min(kCh, L - base);
-    if (threadIdx.x < 32) {  // warp 0 stages the chunk and builds its rectangle table
-      if (threadIdx.x < n) {
-        const int k = list[base + threadIdx.x];
-        stage(recs, k, sh[threadIdx.x]);
-        rect_entry(sh[threadIdx.x], threadIdx.x, tx0, ty0, R);
-        if (COLOR)
-          for (int c = 0; c < 3; ++c) shc[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
+  for (int base = 0; base < L;) {
+    if (threadIdx.x < 32)
+      stage_chunk(list, base, L - base, recs, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
+    __syncthreads();
+    const int n = F.R.n, total = F.R.pre[n];
+    const int64_t ib0 = F.R.ib0;
+    // ---- A: pair-parallel hit + opacity ----------------------------------------------------
+    for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
+      const int j = pair_splat(F.R, n, it);
+      const int local = it - F.R.pre[j];
+      const int nx = F.R.nx[j];
+      const int yy = (int)(((float)local + 0.5f) * F.R.inv[j]);
+      const int px_ = F.R.x0[j] + (local - yy * nx), py_ = F.R.y0[j] + yy;
+      const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
+      if ((F.skip[q >> 5] >> (q & 31)) & 1u) continue;
+      ++npairs;
+      const Staged& r = F.sh[j];
+      Blend b;
+      const bool bl =
+          blend_of(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, px_, py_, s, s64, S64, b);
+      const float2 c = encode(bl, b);
+      F.code[it] = c;
+      pair_code[ib0 + it] = c;
+      if (bl) {
+        pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
+        pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
       }
-      __syncwarp();
-      rect_scan(R, n);
     }
     __syncthreads();
-    phase_codes(sh, R, n, tx0, ty0, W, H, s, s64, S64, skip, code_a, code_om, nrect);
-    __syncthreads();
+    // ---- B: pixel-serial blend ------------------------------------------------------------
     if (!done) {
       for (int j = 0; j < n; ++j) {
-        const int4 rr = *reinterpret_cast<const int4*>(&sh[j].rx0);
+        const int4 rr = *reinterpret_cast<const int4*>(&F.sh[j].rx0);
         if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
-        const float a = code_a[j][pix];
-        if (!code_blends(a)) continue;
-        const float om = fabsf(code_om[j][pix]);
-        acc.add(__fmul_rn(T, a), sh[j], COLOR ? shc[j] : nullptr);
-        T = __fmul_rn(T, om);
+        const float2 c = F.code[pair_index(F.R, j, xi, yi)];
+        if (!code_blends(c.x)) continue;
+        acc.add(__fmul_rn(T, c.x), F.sh[j], COLOR ? F.col[j] : nullptr);
+        T = __fmul_rn(T, fabsf(c.y));
         ++nb;
         if (T < t_stop) {
           done = true;
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, done);
-    if ((threadIdx.x & 31) == 0) skip[threadIdx.x >> 5] = m;
+    if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
+    base += n;
     if (__syncthreads_and(done)) break;
   }
   if (inside) {
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
     n_proc[p] = nproc;
     n_blend[p] = nb;
   }
-  const unsigned wb = warp_sum(nrect);
+  const unsigned wb = warp_sum(npairs);
   if ((threadIdx.x & 31) == 0 && wb) atomicAdd(&g_ts_counters[2], (unsigned long long)wb);
 }
 
@@ -495,11 +497,30 @@ __global__ void k_window(int T, const int64_t* __restrict__ starts, const int32_
   }
 }
 
+// pairs per list position: |pixel rectangle of the splat  ∩  tile|
+__global__ void k_item_counts(int T, int tiles_x, const int64_t* __restrict__ starts,
+                              const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
+                              const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs,
+                              int32_t* __restrict__ cnt) {
+  const int t = blockIdx.x;
+  if (t >= T) return;
+  const int tx0 = (t % tiles_x) * TS_TILE, ty0 = (t / tiles_x) * TS_TILE;
+  const int64_t lo = starts[t], hi = starts[t + 1];
+  const int32_t* list = nonmono[t] ? witems : items;
+  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
+    const int2 rr = *reinterpret_cast<const int2*>(recs + list[p]);
+    int x0, y0, nx, c = 0;
+    tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0, y0, nx,
+              c);
+    cnt[p] = c;
+  }
+}
+
 // backward of one face hit (_core.pyx:295-341) accumulated into an item row (shared memory,
 // per-vertex slots: [0,4) d_f, [4,8) d_depth, [8,12) d_px, [12,16) d_py)
 __device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, float px, float py, float g) {
   const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
-  const float inv_ad = 1.0f / r.adet[fi];
+  const float inv_ad = frcp(r.adet[fi]);
   const float eux = r.eux[fi], euy = r.euy[fi], evx = r.evx[fi], evy = r.evy[fi];
   const float u = fmaf(eux, px, fmaf(euy, py, r.cu[fi])) * inv_ad;
   const float v = fmaf(evx, px, fmaf(evy, py, r.cv[fi])) * inv_ad;
@@ -507,7 +528,7 @@ __device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, fl
   const float iza = r.iz[ia], izb = r.iz[ib], izc = r.iz[ic];
   const float fa = r.df[ia], fb = r.df[ib], fc = r.df[ic];
   const float w0 = wbar * iza, w1 = u * izb, w2 = v * izc;
-  const float iS = 1.0f / (w0 + w1 + w2);
+  const float iS = frcp(w0 + w1 + w2);
   const float fh = (w0 * fa + w1 * fb + w2 * fc) * iS;
   row[ia] += g * w0 * iS;
   row[ib] += g * w1 * iS;
@@ -530,30 +551,33 @@ __device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, fl
 
 struct BwdSmem {
   Staged sh[kCh];
-  float wv[kCh][TS_TILE_PX];  // phase A: codes; phase B: w = T a (-0 = blended with w == 0)
-  float Gv[kCh][TS_TILE_PX];  // phase B: G (0 when clipped)
-  float acc[kCh][kGr];        // per-(tile, splat) gradient rows of the chunk
-  float gpx[TS_TILE_PX][8];   // per-pixel upstream gradients: g_d, g_n[3], g_c[3]
+  float2 wg[kCap];           // load: (alpha, 1-alpha); phase B: (w = T a, G)
+  float acc[kCh][kGr];       // per-(tile, splat) gradient rows of the chunk
+  float gpx[TS_TILE_PX][8];  // per-pixel upstream gradients: g_d, g_n[3], g_c[3]
   float col[kCh][3];
-  int buf[kWarps][64];        // per-warp compacted items (j << 8 | pixel)
+  int buf[kWarps][64];       // per-warp compacted items (j << 16 | pair)
   float rows[kWarps][32][kGr];
-  uint32_t skip[TS_TILE_PX / 32];
   RectTab R;
   int maxproc;
 };
 
 template <bool COLOR>
-__device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty0, float s, double s64,
-                                              const Scene64& S64) {
+__device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty0,
+                                              const float2* __restrict__ pair_sig,
+                                              const uint8_t* __restrict__ pair_faces, int64_t ib0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* row = S.rows[warp][lane];
   if (lane < m) {
     const int item = S.buf[warp][lane];
-    const int j = item >> 8, pix = item & 255;
+    const int j = item >> 16, it = item & 0xffff;
     const Staged& r = S.sh[j];
-    const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
-    const float w = S.wv[j][pix];
-    const float G = S.Gv[j][pix];
+    const int local = it - S.R.pre[j];
+    const int nx = S.R.nx[j];
+    const int yy = (int)(((float)local + 0.5f) * S.R.inv[j]);
+    const int xi = S.R.x0[j] + (local - yy * nx), yi = S.R.y0[j] + yy;
+    const int pix = (yi - ty0) * TS_TILE + (xi - tx0);
+    const float2 wg = S.wg[it];
+    const float w = wg.x, G = wg.y;
     const float* gp = S.gpx[pix];
 #pragma unroll
     for (int i = 0; i < 16; ++i) row[i] = 0.f;
@@ -567,14 +591,11 @@ __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty
       row[22] = gp[6] * w;
     }
     if (G != 0.f) {
+      const float2 sg = pair_sig[ib0 + it];
+      const int faces = pair_faces[ib0 + it];
       const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-      Blend b;
-      if (blend_of(r, px, py, xi, yi, s, s64, S64, b)) {  // same deterministic decision as phase A
-        const float dfp = G * s * sigmoidf_stable(-s * b.fp);
-        const float dfn = -G * s * sigmoidf_stable(-s * b.fn);
-        face_bwd(row, r, b.fip, px, py, dfp);
-        face_bwd(row, r, b.fin, px, py, dfn);
-      }
+      face_bwd(row, r, faces & 3, px, py, G * sg.x);
+      face_bwd(row, r, faces >> 2, px, py, -G * sg.y);
     }
   }
   __syncwarp();
@@ -583,7 +604,7 @@ __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty
     int cur = -1;
     float sum = 0.f;
     for (int i = 0; i < m; ++i) {
-      const int jj = S.buf[warp][i] >> 8;
+      const int jj = S.buf[warp][i] >> 16;
       if (jj != cur) {
         if (cur >= 0) S.acc[cur][lane] += sum;
         cur = jj;
@@ -600,7 +621,8 @@ template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-    Scene64 S64, int tiles_x, int W, int H, float s, double s64, const float* __restrict__ normal_map,
+    int tiles_x, int W, int H, const int64_t* __restrict__ item_off, const float2* __restrict__ pair_code,
+    const float2* __restrict__ pair_sig, const uint8_t* __restrict__ pair_faces, const float* __restrict__ normal_map,
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
@@ -647,42 +669,32 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
   float T = 1.f;
   Accum<COLOR> P;
   P.zero();
-  unsigned nrect_unused = 0;
-  for (int base = 0; base < maxproc; base += kCh) {
-    const int n = min(kCh, maxproc - base);
-    if (threadIdx.x < 32) {
-      if (threadIdx.x < n) {
-        const int k = list[base + threadIdx.x];
-        stage(recs, k, S.sh[threadIdx.x]);
-        rect_entry(S.sh[threadIdx.x], threadIdx.x, tx0, ty0, S.R);
-        if (COLOR)
-          for (int c = 0; c < 3; ++c) S.col[threadIdx.x][c] = colors[(int64_t)k * 3 + c];
-      }
-      __syncwarp();
-      rect_scan(S.R, n);
-    }
+  for (int base = 0; base < maxproc;) {
+    if (threadIdx.x < 32)
+      stage_chunk(list, base, maxproc - base, recs, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
+    __syncthreads();
+    const int n = S.R.n, total = S.R.pre[n];
+    const int64_t ib0 = S.R.ib0;
+    // ---- load the chunk's pair codes (contiguous) and clear its gradient rows -------------
+    for (int it = threadIdx.x; it < total; it += TS_TILE_PX) S.wg[it] = pair_code[ib0 + it];
     for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
-    {
-      const unsigned m = __ballot_sync(0xffffffffu, nproc <= base);
-      if (lane == 0) S.skip[warp] = m;
-    }
     __syncthreads();
-    // ---- A: codes ---------------------------------------------------------------------
-    phase_codes(S.sh, S.R, n, tx0, ty0, W, H, s, s64, S64, S.skip, S.wv, S.Gv, nrect_unused);
-    __syncthreads();
-    // ---- B: pixel-serial prefix walk -> w, G ----------------------------------------------
+    // ---- B: pixel-serial prefix walk -> (w, G) ---------------------------------------------
     for (int j = 0; j < n; ++j) {
       const int4 rr = *reinterpret_cast<const int4*>(&S.sh[j].rx0);
       if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
-      if (base + j >= nproc) {  // past this pixel's early stop: no contribution
-        S.wv[j][pix] = 0.f;
+      const int it = pair_index(S.R, j, xi, yi);
+      if (base + j >= nproc) {  // past this pixel's early stop (code may be stale): none
+        S.wg[it] = make_float2(0.f, 0.f);
         continue;
       }
-      const float a = S.wv[j][pix];
-      if (!code_blends(a)) continue;
-      const float omc = S.Gv[j][pix];
-      const bool cl = omc < 0.f;
-      const float om = fabsf(omc);
+      const float2 c = S.wg[it];
+      if (!code_blends(c.x)) {
+        S.wg[it] = make_float2(0.f, 0.f);
+        continue;
+      }
+      const float a = c.x, om = fabsf(c.y);
+      const bool cl = c.y < 0.f;
       const Staged& r = S.sh[j];
       const float* col = COLOR ? S.col[j] : nullptr;
       const float w = __fmul_rn(T, a);
@@ -697,36 +709,26 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
 #pragma unroll
           for (int i = 0; i < 3; ++i) G += g_c[i] * (Tom * col[i] - (C_c[i] - P.c[i]));
       }
-      S.wv[j][pix] = w == 0.f ? -0.f : w;
-      S.Gv[j][pix] = G;
+      S.wg[it] = make_float2(w == 0.f ? -0.f : w, G);
       T = __fmul_rn(T, om);
     }
     __syncthreads();
-    // ---- C: compacted blended items per warp, 32 at a time ------------------------------
+    // ---- C: compacted blended items per warp, 32 at a time --------------------------------
     {
       const int per = (n + kWarps - 1) / kWarps;
       const int j0 = warp * per, j1 = min(n, j0 + per);
       int cnt = 0;
       for (int j = j0; j < j1; ++j) {
-        int x0, y0, nx, tot;
-        if (!tile_rect(S.sh[j], tx0, ty0, x0, y0, nx, tot)) continue;
-        const float inv = 1.0f / (float)nx;
-        for (int it0 = 0; it0 < tot; it0 += 32) {
+        const int b0 = S.R.pre[j], b1 = S.R.pre[j + 1];
+        for (int it0 = b0; it0 < b1; it0 += 32) {
           const int it = it0 + lane;
-          int q = 0;
-          bool has = false;
-          if (it < tot) {
-            const int yy = (int)(((float)it + 0.5f) * inv);
-            const int xx = x0 + (it - yy * nx), yv = y0 + yy;
-            q = (yv - ty0) * TS_TILE + (xx - tx0);
-            has = xx < W && yv < H && code_blends(S.wv[j][q]);
-          }
+          const bool has = it < b1 && code_blends(S.wg[it].x);
           const unsigned m = __ballot_sync(0xffffffffu, has);
-          if (has) S.buf[warp][cnt + __popc(m & ((1u << lane) - 1u))] = (j << 8) | q;
+          if (has) S.buf[warp][cnt + __popc(m & ((1u << lane) - 1u))] = (j << 16) | it;
           cnt += __popc(m);
           __syncwarp();
           if (cnt >= 32) {
-            process_items<COLOR>(S, 32, tx0, ty0, s, s64, S64);
+            process_items<COLOR>(S, 32, tx0, ty0, pair_sig, pair_faces, ib0);
             const int rest = cnt - 32;
             const int moved = lane < rest ? S.buf[warp][32 + lane] : 0;
             __syncwarp();
@@ -736,7 +738,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
           }
         }
       }
-      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, s, s64, S64);
+      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_sig, pair_faces, ib0);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += TS_TILE_PX) {
@@ -745,6 +747,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
 #pragma unroll
       for (int i = 0; i < kGr / 4; ++i) dst[i] = src[i];
     }
+    base += n;
     __syncthreads();
   }
   // positions no pixel reached: zero rows so the gather sees every pair
@@ -836,19 +839,38 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
 
 using namespace ts;
 
-void ts_impl_window(int T, const BinsView& b, int64_t M, const double* md, int n_w, cudaStream_t st) {
-  if (M <= 0) return;
+// window-resorted lists + pair offsets of the view: item_off[M+1]; returns the pair count
+int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int64_t M, const double* md, int n_w,
+                                const SplatRec* rec, int64_t* item_off, cudaStream_t st) {
+  const int T = tiles_x * tiles_y;
+  if (M <= 0) {
+    cudaMemsetAsync(item_off, 0, sizeof(int64_t), st);
+    return 0;
+  }
   int32_t* widx = nullptr;
   double* wz = nullptr;
+  int32_t* cnt = nullptr;
+  int64_t* scratch = nullptr;
   cudaMallocAsync(&widx, sizeof(int32_t) * M, st);
   cudaMallocAsync(&wz, sizeof(double) * M, st);
+  cudaMallocAsync(&cnt, sizeof(int32_t) * M, st);
+  cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(M), st);
   k_window<<<(T + 63) / 64, 64, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, b.witems, widx, wz);
+  k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
+  scan_counts(cnt, M, item_off, scratch, st);
+  int64_t total = 0;
+  cudaMemcpyAsync(&total, item_off + M, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(widx, st);
   cudaFreeAsync(wz, st);
+  cudaFreeAsync(cnt, st);
+  cudaFreeAsync(scratch, st);
+  cudaStreamSynchronize(st);
+  return total;
 }
 
 void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec* rec, const float* colors,
-                     const Scene64& S64, int W, int H, double s, float t_stop, float* nmap, float* dmap, float* omap,
+                     const Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
+                     float2* pair_code, float2* pair_sig, uint8_t* pair_faces, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
   static bool attr = false;
@@ -860,18 +882,19 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
   }
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
-                                                W, H, (float)s, s, t_stop, nmap, dmap, omap, cmap, n_proc, n_blend);
+                                                W, H, (float)s, s, t_stop, item_off, pair_code, pair_sig,
+                                                pair_faces, nmap, dmap, omap, cmap, n_proc, n_blend);
   else
     k_forward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
-                                                 tiles_x, W, H, (float)s, s, t_stop, nmap, dmap, omap, nullptr, n_proc,
-                                                 n_blend);
+                                                 tiles_x, W, H, (float)s, s, t_stop, item_off, pair_code, pair_sig,
+                                                 pair_faces, nmap, dmap, omap, nullptr, n_proc, n_blend);
 }
 
 void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, int64_t K, const SplatRec* rec,
-                      const float* colors, const Scene64& S64, const int32_t* vert_ids, const int32_t* tet_ids,
-                      const double* deform, int R, const Camera& cam, double s, const float* maps[4],
-                      const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color,
-                      cudaStream_t st) {
+                      const float* colors, const double* fsc, const int32_t* vert_ids, const int32_t* tet_ids,
+                      const double* deform, int R, const Camera& cam, const int64_t* item_off,
+                      const float2* pair_code, const float2* pair_sig, const uint8_t* pair_faces, const float* maps[4],
+                      const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
   static bool attr = false;
@@ -885,21 +908,22 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   cudaMallocAsync(&rows, sizeof(float) * kGr * (size_t)M, st);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
-    k_backward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
-                                                 cam.width, cam.height, (float)s, s, maps[0], maps[1], maps[2],
-                                                 maps[3], dmaps[0], dmaps[1], dmaps[2], dmaps[3], n_proc, rows);
+    k_backward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
+                                                 cam.width, cam.height, item_off, pair_code, pair_sig, pair_faces,
+                                                 maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
+                                                 dmaps[3], n_proc, rows);
   else
-    k_backward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
-                                                  tiles_x, cam.width, cam.height, (float)s, s, maps[0], maps[1],
-                                                  maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2], nullptr, n_proc,
-                                                  rows);
+    k_backward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
+                                                  cam.width, cam.height, item_off, pair_code, pair_sig, pair_faces,
+                                                  maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
+                                                  nullptr, n_proc, rows);
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (color)
-    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform,
+    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
                                           make_grid(R), cam, d_vert, d_color);
   else
-    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, S64.f, deform,
+    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
                                            make_grid(R), cam, d_vert, nullptr);
   cudaFreeAsync(rows, st);
 }

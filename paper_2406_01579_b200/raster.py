@@ -137,6 +137,10 @@ class SavedState:
     maps: RenderMaps
     n_proc: torch.Tensor   # (H,W) int32
     n_blend: torch.Tensor  # (H,W) int32 — the reference's per-pixel record counts
+    item_off: torch.Tensor | None = None    # (M+1,) int64: first pair of each list position
+    pair_code: torch.Tensor | None = None   # (P,2) f32: alpha, 1-alpha (negative: clipped)
+    pair_sig: torch.Tensor | None = None    # (P,2) f32: s*sigmoid(-s f_prev), s*sigmoid(-s f_next)
+    pair_faces: torch.Tensor | None = None  # (P,) u8: entry | exit << 2
 
 
 def bin_and_sort(scene: SplatScene, camera, tile_size: int = TILE_SIZE, stream=None) -> TileBins:
@@ -183,17 +187,30 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
     n_proc = torch.empty((H, W), dtype=torch.int32, device=dev)
     n_blend = torch.empty((H, W), dtype=torch.int32, device=dev)
     K = len(scene)
-    if K == 0 or bins.num_pairs == 0:
+    M = bins.num_pairs
+    item_off = pair_code = pair_sig = pair_faces = None
+    if K == 0 or M == 0:
         for t in (maps.normal, maps.depth, maps.opacity, maps.color, n_proc, n_blend):
             if t is not None:
                 t.zero_()
     else:
-        _native.check(L.ts_render_forward(scene.abi(), K, _native.ptr(scene.colors), bins.abi(), bins.num_pairs,
-                                          camera.abi(), int(n_w), float(scene.steepness), float(t_stop),
+        sp = _native.stream_ptr(stream)
+        sc_abi, b_abi, cam = scene.abi(), bins.abi(), camera.abi()
+        item_off = torch.empty(M + 1, dtype=torch.int64, device=dev)
+        npairs = _native.i64()
+        _native.check(L.ts_forward_prepare(sc_abi, K, b_abi, M, cam, int(n_w), _native.ptr(item_off), npairs, sp))
+        P = max(npairs.value, 1)
+        pair_code = torch.empty((P, 2), dtype=torch.float32, device=dev)
+        pair_sig = torch.empty((P, 2), dtype=torch.float32, device=dev)
+        pair_faces = torch.empty(P, dtype=torch.uint8, device=dev)
+        _native.check(L.ts_render_forward(sc_abi, K, _native.ptr(scene.colors), b_abi, M, cam,
+                                          float(scene.steepness), float(t_stop), _native.ptr(item_off),
+                                          _native.ptr(pair_code), _native.ptr(pair_sig), _native.ptr(pair_faces),
                                           _native.ptr(maps.normal), _native.ptr(maps.depth),
                                           _native.ptr(maps.opacity), _native.ptr(maps.color),
-                                          _native.ptr(n_proc), _native.ptr(n_blend), _native.stream_ptr(stream)))
-    saved = SavedState(bins, n_w, t_stop, maps, n_proc, n_blend) if save_state else None
+                                          _native.ptr(n_proc), _native.ptr(n_blend), sp))
+    saved = SavedState(bins, n_w, t_stop, maps, n_proc, n_blend, item_off, pair_code, pair_sig,
+                       pair_faces) if save_state else None
     return maps, saved
 
 
@@ -226,7 +243,9 @@ def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d
                                  saved.maps.color.data_ptr() if with_color else None)
     dmaps = (ctypes.c_void_p * 4)(dn.data_ptr(), dd.data_ptr(), do.data_ptr(), dc.data_ptr() if with_color else None)
     _native.check(L.ts_render_backward(scene.abi(), K, _native.ptr(scene.colors), saved.bins.abi(),
-                                       saved.bins.num_pairs, camera.abi(), float(scene.steepness),
+                                       saved.bins.num_pairs, camera.abi(), _native.ptr(saved.item_off),
+                                       _native.ptr(saved.pair_code), _native.ptr(saved.pair_sig),
+                                       _native.ptr(saved.pair_faces),
                                        ctypes.cast(maps, ctypes.POINTER(ctypes.c_void_p)),
                                        ctypes.cast(dmaps, ctypes.POINTER(ctypes.c_void_p)),
                                        _native.ptr(saved.n_proc), _native.ptr(field.deformation), grid.resolution,
