@@ -142,6 +142,10 @@ int ts_debug_counters(uint64_t* out4, int reset);
  * (results then no longer match the reference).  Default 0. */
 int ts_debug_set_flags(int flags);
 
+/* Diagnostics: with flag bit 1 set, the forward records per-tile start/end %globaltimer
+ * (ns) and SM id of its last launch; copies the first n tiles.  [sync] */
+int ts_debug_tile_times(uint64_t* t2, uint32_t* sm, int n);
+
 #ifdef __cplusplus
 }
 #endif

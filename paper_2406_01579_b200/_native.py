@@ -66,6 +66,8 @@ def lib():
         "ts_marching_tets": ([P, P, I32, P, P, PI64, P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
+        "ts_debug_tile_times": ([ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int],
+                                ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -267,6 +267,12 @@ int ts_debug_counters(uint64_t* out4, int reset) {
   return check_cuda("ts_debug_counters");
 }
 
+int ts_debug_tile_times(uint64_t* t2, uint32_t* sm, int n) {
+  if (!t2 || !sm || n < 0 || n > 65536) return fail(TS_EINVAL, "ts_debug_tile_times: bad arguments");
+  ts_impl_tile_times(reinterpret_cast<unsigned long long*>(t2), sm, n);
+  return check_cuda("ts_debug_tile_times");
+}
+
 int ts_debug_set_flags(int flags) {
   ts_impl_debug_flags(flags);
   return check_cuda("ts_debug_set_flags");

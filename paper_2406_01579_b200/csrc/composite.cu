@@ -68,6 +68,20 @@ static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 __device__ unsigned long long g_ts_counters[4];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity)
 __device__ int g_ts_debug_flags;
+// diagnostics only (flag bit 1): per-tile forward start/end globaltimer, SM id
+__device__ unsigned long long g_ts_tile_time[2 * 65536];
+__device__ unsigned int g_ts_tile_sm[65536];
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 __device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
 
@@ -378,6 +392,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
   const int tile = blockIdx.x;
+  const bool timing = (g_ts_debug_flags & 2) && tile < 65536;
+  if (timing && threadIdx.x == 0) {
+    g_ts_tile_time[2 * tile] = gtimer();
+    g_ts_tile_sm[tile] = smid();
+  }
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x;
   const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
@@ -463,6 +482,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   }
   const unsigned wb = warp_sum(npairs);
   if ((threadIdx.x & 31) == 0 && wb) atomicAdd(&g_ts_counters[2], (unsigned long long)wb);
+  if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
 }
 
 // per-tile replay of the reference window (_core.pyx:171-187) for tiles whose list is
@@ -937,3 +957,8 @@ void ts_impl_counters(unsigned long long out[4], int reset) {
 }
 
 void ts_impl_debug_flags(int flags) { cudaMemcpyToSymbol(g_ts_debug_flags, &flags, sizeof(int)); }
+
+void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n) {
+  cudaMemcpyFromSymbol(t2, g_ts_tile_time, sizeof(unsigned long long) * 2 * n);
+  cudaMemcpyFromSymbol(sm, g_ts_tile_sm, sizeof(unsigned int) * n);
+}

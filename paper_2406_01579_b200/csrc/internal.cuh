@@ -55,6 +55,7 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
 void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const ts::BinWork& w,
                       const int64_t* starts, const int64_t* splat_off, int64_t maxL, uint64_t* keys,
                       uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st);
+void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n);
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, const double* md,
                                 int n_w, const ts::SplatRec* rec, int64_t* item_off, cudaStream_t st);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
