@@ -316,6 +316,7 @@ struct RectTab {
   int pre[kCh + 1];  // exclusive prefix of pair counts
   int n;             // splats in this chunk
   int64_t ib0;       // global index of the chunk's first pair
+  uint8_t jtab[kCap];  // splat of each pair
 };
 
 // Warp 0 only: stage up to kCh records from list position `base` (at most `avail`) and cut
@@ -353,20 +354,25 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
   if (lane < m) R.pre[lane + 1] = v;
   // cut: the largest prefix with at most kCap pairs (one splat has <= 256 pairs)
   const unsigned ok = __ballot_sync(0xffffffffu, lane < m && v <= kCap);
+  const int n = __popc(ok);
+  if (lane < n)
+    for (int it = v - cnt; it < v; ++it) R.jtab[it] = (uint8_t)lane;
   if (lane == 0) {
     R.pre[0] = 0;
-    R.n = __popc(ok);
+    R.n = n;
     R.ib0 = item_off_tile[base];
   }
 }
 
-// last j with pre[j] <= it (pre is non-decreasing, n <= 32)
-__device__ __forceinline__ int pair_splat(const RectTab& R, int n, int it) {
-  int j = 0;
-#pragma unroll
-  for (int step = 16; step >= 1; step >>= 1)
-    if (j + step < n && R.pre[j + step] <= it) j += step;
-  return j;
+__device__ __forceinline__ int pair_splat(const RectTab& R, int it) { return R.jtab[it]; }
+
+// pixel (tile-local index) of pair `it` of splat j
+__device__ __forceinline__ void pair_pixel(const RectTab& R, int j, int it, int& xi, int& yi) {
+  const int local = it - R.pre[j];
+  const int nx = R.nx[j];
+  const int yy = (int)(((float)local + 0.5f) * R.inv[j]);
+  xi = R.x0[j] + (local - yy * nx);
+  yi = R.y0[j] + yy;
 }
 
 __device__ __forceinline__ int pair_index(const RectTab& R, int j, int xi, int yi) {
@@ -376,6 +382,7 @@ __device__ __forceinline__ int pair_index(const RectTab& R, int j, int xi, int y
 struct FwdSmem {
   Staged sh[kCh];
   float2 code[kCap];  // (alpha, 1 - alpha) per pair of the chunk
+  uint32_t bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   float col[kCh][3];
   uint32_t skip[TS_TILE_PX / 32];
   RectTab R;
@@ -417,16 +424,15 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   for (int base = 0; base < L;) {
     if (threadIdx.x < 32)
       stage_chunk(list, base, L - base, recs, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
+    F.bmask[pix] = 0u;
     __syncthreads();
     const int n = F.R.n, total = F.R.pre[n];
     const int64_t ib0 = F.R.ib0;
     // ---- A: pair-parallel hit + opacity ----------------------------------------------------
     for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
-      const int j = pair_splat(F.R, n, it);
-      const int local = it - F.R.pre[j];
-      const int nx = F.R.nx[j];
-      const int yy = (int)(((float)local + 0.5f) * F.R.inv[j]);
-      const int px_ = F.R.x0[j] + (local - yy * nx), py_ = F.R.y0[j] + yy;
+      const int j = pair_splat(F.R, it);
+      int px_, py_;
+      pair_pixel(F.R, j, it, px_, py_);
       const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
       if ((F.skip[q >> 5] >> (q & 31)) & 1u) continue;
       ++npairs;
@@ -435,21 +441,22 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
       const bool bl =
           blend_of(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, px_, py_, s, s64, S64, b);
       const float2 c = encode(bl, b);
-      F.code[it] = c;
       pair_code[ib0 + it] = c;
       if (bl) {
+        F.code[it] = c;
+        atomicOr(&F.bmask[q], 1u << j);
         pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
         pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
       }
     }
     __syncthreads();
-    // ---- B: pixel-serial blend ------------------------------------------------------------
+    // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
     if (!done) {
-      for (int j = 0; j < n; ++j) {
-        const int4 rr = *reinterpret_cast<const int4*>(&F.sh[j].rx0);
-        if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
+      unsigned m = F.bmask[pix];
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1u;
         const float2 c = F.code[pair_index(F.R, j, xi, yi)];
-        if (!code_blends(c.x)) continue;
         acc.add(__fmul_rn(T, c.x), F.sh[j], COLOR ? F.col[j] : nullptr);
         T = __fmul_rn(T, fabsf(c.y));
         ++nb;
@@ -577,6 +584,7 @@ struct BwdSmem {
   float col[kCh][3];
   int buf[kWarps][64];       // per-warp compacted items (j << 16 | pair)
   float rows[kWarps][32][kGr];
+  uint32_t bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   RectTab R;
   int maxproc;
 };
@@ -692,27 +700,34 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
   for (int base = 0; base < maxproc;) {
     if (threadIdx.x < 32)
       stage_chunk(list, base, maxproc - base, recs, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
+    S.bmask[pix] = 0u;
     __syncthreads();
     const int n = S.R.n, total = S.R.pre[n];
     const int64_t ib0 = S.R.ib0;
-    // ---- load the chunk's pair codes (contiguous) and clear its gradient rows -------------
-    for (int it = threadIdx.x; it < total; it += TS_TILE_PX) S.wg[it] = pair_code[ib0 + it];
+    // ---- load the chunk's pair codes (contiguous), per-pixel blend masks, clear rows --------
+    for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
+      const float2 c = pair_code[ib0 + it];
+      S.wg[it] = c;
+      if (code_blends(c.x)) {
+        const int j = pair_splat(S.R, it);
+        int px_, py_;
+        pair_pixel(S.R, j, it, px_, py_);
+        atomicOr(&S.bmask[(py_ - ty0) * TS_TILE + (px_ - tx0)], 1u << j);
+      }
+    }
     for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
     __syncthreads();
-    // ---- B: pixel-serial prefix walk -> (w, G) ---------------------------------------------
-    for (int j = 0; j < n; ++j) {
-      const int4 rr = *reinterpret_cast<const int4*>(&S.sh[j].rx0);
-      if (xi < rr.x || xi > rr.y || yi < rr.z || yi > rr.w) continue;
+    // ---- B: pixel-serial prefix walk over this pixel's blended splats -> (w, G) --------------
+    const int lim = nproc - base;  // splats j >= lim lie past this pixel's early stop
+    for (unsigned m = S.bmask[pix]; m;) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1u;
       const int it = pair_index(S.R, j, xi, yi);
-      if (base + j >= nproc) {  // past this pixel's early stop (code may be stale): none
+      if (j >= lim) {  // code may be stale (pixel skipped by the forward): no contribution
         S.wg[it] = make_float2(0.f, 0.f);
         continue;
       }
       const float2 c = S.wg[it];
-      if (!code_blends(c.x)) {
-        S.wg[it] = make_float2(0.f, 0.f);
-        continue;
-      }
       const float a = c.x, om = fabsf(c.y);
       const bool cl = c.y < 0.f;
       const Staged& r = S.sh[j];
