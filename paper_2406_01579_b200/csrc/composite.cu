@@ -195,38 +195,87 @@ struct Blend {
   bool clipped;   // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
 };
 
-// Exact replica of the reference decision chain in FP64 (_core.pyx:67-95, 35-36, 190-196).
-// Returned by value (registers) so the caller's Blend never lives in local memory.
-struct ExactOut {
-  float fp, fn, d;
-  int faces;  // fip | fin << 4 | clipped << 8 | blended << 9
-};
-__device__ __noinline__ ExactOut blend_exact(const Scene64& S, int k, int xi, int yi, double s) {
-  ExactOut o{0.f, 0.f, 0.f, 0};
-  double fp, fn;
-  int i0, i1;
-  if (!splat_hits_exact(S, k, xi + 0.5, yi + 0.5, fp, fn, i0, i1)) return o;
-  double d = dsub(softplus_d(dmul(-s, fp)), softplus_d(dmul(-s, fn)));
-  double a = dsub(1.0, exp(d));
-  if (a <= 0.0) return o;
-  o.fp = (float)fp;
-  o.fn = (float)fn;
-  o.d = (float)d;
-  o.faces = i0 | (i1 << 4) | ((a > 1.0 - 1e-4) ? 256 : 0) | 512;
-  return o;
+// One face of the reference's _face_hit (_core.pyx:39-64) in exact FP64 (no contraction).
+__device__ __forceinline__ bool exact_face(const Scene64& S, int64_t k, int fi, double px, double py, double& zp,
+                                          double& fh) {
+  const double* P = S.proj + k * 8;
+  const double* Z = S.depths + k * 4;
+  const double* F = S.f + k * 4;
+  const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
+  const double ax = P[2 * ia], ay = P[2 * ia + 1];
+  const double m00 = dsub(P[2 * ib], ax), m10 = dsub(P[2 * ib + 1], ay);
+  const double m01 = dsub(P[2 * ic], ax), m11 = dsub(P[2 * ic + 1], ay);
+  const double det = dsub(dmul(m00, m11), dmul(m01, m10));
+  if (fabs(det) < kEpsDet) return false;
+  const double rx = dsub(px, ax), ry = dsub(py, ay);
+  const double u = ddiv(dsub(dmul(m11, rx), dmul(m01, ry)), det);
+  const double v = ddiv(dadd(dmul(-m10, rx), dmul(m00, ry)), det);
+  if (u < 0.0 || v < 0.0 || dadd(u, v) > 1.0) return false;
+  const double za = Z[ia], zb = Z[ib], zc = Z[ic];
+  const double w0 = ddiv(dsub(dsub(1.0, u), v), za), w1 = ddiv(u, zb), w2 = ddiv(v, zc);
+  const double Ss = dadd(dadd(w0, w1), w2);
+  fh = ddiv(dadd(dadd(dmul(w0, F[ia]), dmul(w1, F[ib])), dmul(w2, F[ic])), Ss);
+  zp = ddiv(1.0, Ss);
+  return true;
 }
 
-// FP32 fast path with error-bounded decisions; anything within the bounds of a decision
-// threshold is re-decided by blend_exact so the blended set matches the FP64 reference.
-__device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, int xi, int yi, float s, double s64,
-                                         const Scene64& S, Blend& b) {
+// Warp-cooperative exact re-decision (the reference's decision chain, _core.pyx:67-95,
+// 35-36, 190-196, in FP64): 4 lanes per queued pair, one face each; the group leader
+// combines the faces in face order (first hit seeds, strict < / > updates) and decides
+// alpha.  Returns true on the leader when the pair blends.
+__device__ __forceinline__ bool exact_group(const Scene64& S, bool act, int64_t k, int xi, int yi, double s, Blend& b) {
+  const int lane = threadIdx.x & 31, fi = lane & 3, lead = lane & ~3;
+  const double px = xi + 0.5, py = yi + 0.5;
+  double zp = 0.0, fh = 0.0;
+  bool hit = false;
+  if (act) {
+    const double* B = S.bbox + k * 4;
+    const bool inb = !(px < B[0] || px > B[2] || py < B[1] || py > B[3]);
+    hit = inb && exact_face(S, k, fi, px, py, zp, fh);
+  }
+  double zlo = 0, zhi = 0, flo = 0, fhi = 0;
+  int n = 0, lo = -1, hi = -1;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const bool h = __shfl_sync(0xffffffffu, hit, lead + f);
+    const double z = __shfl_sync(0xffffffffu, zp, lead + f);
+    const double v = __shfl_sync(0xffffffffu, fh, lead + f);
+    if (!h) continue;
+    if (n == 0) {
+      zlo = zhi = z;
+      flo = fhi = v;
+      lo = hi = f;
+    } else {
+      if (z < zlo) { zlo = z; flo = v; lo = f; }
+      if (z > zhi) { zhi = z; fhi = v; hi = f; }
+    }
+    ++n;
+  }
+  if (!act || fi != 0 || n < 2) return false;
+  const double d = dsub(softplus_d(dmul(-s, flo)), softplus_d(dmul(-s, fhi)));
+  const double a = dsub(1.0, exp(d));
+  if (a <= 0.0) return false;
+  const float sf = (float)s;
+  b.a = (float)a;
+  b.om = (float)exp(d);
+  b.sp = sf * sigmoidf_stable(-sf * (float)flo);
+  b.sn = sf * sigmoidf_stable(-sf * (float)fhi);
+  b.fip = lo;
+  b.fin = hi;
+  b.clipped = a > 1.0 - 1e-4;
+  return true;
+}
+
+// FP32 fast path with error-bounded decisions: 0 no blend, 1 blend (b filled), 2 the pair
+// lies within the error bound of a decision threshold and needs the exact re-decision.
+__device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, float s, Blend& b) {
   Hit h;
   const int e = eval_hits(r, px, py, h);
-  if (e == 0) return false;
+  if (e == 0) return 0;
   if (e == 1) {
     const float dfl = h.fp - h.fn;  // f_prev - f_next, f0 cancels exactly
     const float ftol = r.fband / fminf(r.adet[h.fip], r.adet[h.fin]) + r.ftol0;
-    if (dfl < -ftol) return false;  // f_prev < f_next: alpha <= 0 exactly
+    if (dfl < -ftol) return 0;  // f_prev < f_next: alpha <= 0 exactly
     if (dfl > ftol) {
       // alpha = 1 - exp(sp(x) - sp(y)) = 1 - (1 + e^x) / (1 + e^y), x = -s fp, y = -s fn:
       //   alpha = sigmoid(y) (1 - e^{x-y}),  1 - alpha = sigmoid(-y) + sigmoid(y) e^{x-y}
@@ -249,23 +298,14 @@ __device__ __forceinline__ bool blend_of(const Staged& r, float px, float py, in
         b.fip = h.fip;
         b.fin = h.fin;
         b.clipped = a_un > kAlphaClipF;
-        return true;
+        return 1;
       }
     }
     atomicAdd(&g_ts_counters[1], 1ull);
   } else {
     atomicAdd(&g_ts_counters[0], 1ull);
   }
-  if (g_ts_debug_flags & 1) return false;
-  const ExactOut o = blend_exact(S, r.k, xi, yi, s64);
-  b.a = -expm1f(o.d);
-  b.om = expf(o.d);
-  b.sp = s * sigmoidf_stable(-s * o.fp);
-  b.sn = s * sigmoidf_stable(-s * o.fn);
-  b.fip = o.faces & 15;
-  b.fin = (o.faces >> 4) & 15;
-  b.clipped = (o.faces & 256) != 0;
-  return (o.faces & 512) != 0;
+  return (g_ts_debug_flags & 1) ? 0 : 2;
 }
 
 // Pair code: alpha (+0 bits = no blend, -0 = blended with alpha below FP32 range) and
@@ -385,8 +425,24 @@ struct FwdSmem {
   uint32_t bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   float col[kCh][3];
   uint32_t skip[TS_TILE_PX / 32];
+  uint16_t exq[kCap];  // pairs queued for the exact FP64 re-decision
+  int nex;
   RectTab R;
 };
+
+// record one decided pair: shared code + blend bit (forward phase B), global pair record (backward)
+__device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, bool bl, const Blend& b, int64_t ib0,
+                                         float2* __restrict__ pair_code, float2* __restrict__ pair_sig,
+                                         uint8_t* __restrict__ pair_faces) {
+  const float2 c = encode(bl, b);
+  pair_code[ib0 + it] = c;
+  if (bl) {
+    F.code[it] = c;
+    atomicOr(&F.bmask[q], 1u << j);
+    pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
+    pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
+  }
+}
 
 template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
@@ -425,10 +481,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
     if (threadIdx.x < 32)
       stage_chunk(list, base, L - base, recs, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
     F.bmask[pix] = 0u;
+    if (threadIdx.x == 0) F.nex = 0;
     __syncthreads();
     const int n = F.R.n, total = F.R.pre[n];
     const int64_t ib0 = F.R.ib0;
-    // ---- A: pair-parallel hit + opacity ----------------------------------------------------
+    // ---- A: pair-parallel hit + opacity (FP32, error-bounded) ------------------------------
     for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
       const int j = pair_splat(F.R, it);
       int px_, py_;
@@ -438,16 +495,25 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
       ++npairs;
       const Staged& r = F.sh[j];
       Blend b;
-      const bool bl =
-          blend_of(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, px_, py_, s, s64, S64, b);
-      const float2 c = encode(bl, b);
-      pair_code[ib0 + it] = c;
-      if (bl) {
-        F.code[it] = c;
-        atomicOr(&F.bmask[q], 1u << j);
-        pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
-        pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
-      }
+      const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, b);
+      if (e == 2)
+        F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)it;
+      else
+        put_pair(F, it, j, q, e == 1, b, ib0, pair_code, pair_sig, pair_faces);
+    }
+    __syncthreads();
+    // ---- A': exact FP64 re-decisions, 8 pairs per warp, one face per lane ------------------
+    for (int q0 = (threadIdx.x >> 5) * 8; q0 < F.nex; q0 += kWarps * 8) {
+      const int qi = q0 + ((threadIdx.x & 31) >> 2);
+      const bool act = qi < F.nex;
+      const int it = act ? F.exq[qi] : 0;
+      const int j = pair_splat(F.R, it);
+      int px_, py_;
+      pair_pixel(F.R, j, it, px_, py_);
+      Blend b;
+      const bool bl = exact_group(S64, act, F.sh[j].k, px_, py_, s64, b);
+      if (act && (threadIdx.x & 3) == 0)
+        put_pair(F, it, j, (py_ - ty0) * TS_TILE + (px_ - tx0), bl, b, ib0, pair_code, pair_sig, pair_faces);
     }
     __syncthreads();
     // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
