@@ -128,10 +128,11 @@ int ts_normal_consistency(const double* sdf, const double* deform, int32_t resol
 int ts_marching_tets_count(const double* sdf, const double* deform, int32_t resolution, int64_t* out_num_verts,
                            int64_t* out_num_tris, void* stream);
 
-/* K9 phase 2: vertices f64[V,3] (lexicographic, welded) and triangles i64[F,3]
- * (degenerates removed; out_num_tris receives the final F).  [sync] */
+/* K9 phase 2: vertices f64[V,3] (welded, lexicographic (x, y, z)) and triangles i64[F,3]
+ * (group order of grid.py:192-214, oriented, degenerates removed); capacities = the
+ * counts of phase 1.  out_counts[0] = final F, out_counts[1] = welded V (host).  [sync] */
 int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
-                     int64_t* triangles, int64_t* out_num_tris, void* stream);
+                     int64_t* triangles, int64_t* out_counts, void* stream);
 
 /* Diagnostics: out4[0] = (pixel, splat) pairs re-decided in FP64 at a face edge or a
  * degenerate face, out4[1] = pairs re-decided in FP64 at an alpha threshold (since the

@@ -63,7 +63,7 @@ def lib():
         "ts_eikonal": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency": ([P, P, I32, D, P, P, P], ctypes.c_int),
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),
-        "ts_marching_tets": ([P, P, I32, P, P, PI64, P], ctypes.c_int),
+        "ts_marching_tets": ([P, P, I32, P, P, ctypes.POINTER(ctypes.c_int64), P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
         "ts_debug_tile_times": ([ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int],

@@ -6,6 +6,7 @@ arrays are available on demand for interop/tests only.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -113,9 +114,11 @@ def marching_tetrahedra(grid: TetrahedralGrid, field, stream=None) -> TriangleMe
     sp = _native.stream_ptr(stream)
     nv, nt = _native.i64(), _native.i64()
     _native.check(L.ts_marching_tets_count(_native.ptr(field.sdf), _native.ptr(field.deformation), R, nv, nt, sp))
-    V = torch.empty((max(nv.value, 1), 3), dtype=torch.float64, device=field.sdf.device)
-    F = torch.empty((max(nt.value, 1), 3), dtype=torch.int64, device=field.sdf.device)
-    nf = _native.i64()
+    if nv.value == 0 or nt.value == 0:
+        return TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64))
+    V = torch.empty((nv.value, 3), dtype=torch.float64, device=field.sdf.device)
+    F = torch.empty((nt.value, 3), dtype=torch.int64, device=field.sdf.device)
+    counts = (ctypes.c_int64 * 2)()
     _native.check(L.ts_marching_tets(_native.ptr(field.sdf), _native.ptr(field.deformation), R, _native.ptr(V),
-                                     _native.ptr(F), nf, sp))
-    return TriangleMesh(V[:nv.value].cpu().numpy(), F[:nf.value].cpu().numpy())
+                                     _native.ptr(F), counts, sp))
+    return TriangleMesh(V[:counts[1]].cpu().numpy(), F[:counts[0]].cpu().numpy())

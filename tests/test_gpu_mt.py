@@ -1,0 +1,49 @@
+"""Marching Tetrahedra on the GPU against the reference fixtures (grid.py:136-239):
+bit-exact vertex positions (welded, lexicographic) and triangle indices."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ts():
+    import paper_2406_01579_b200 as ts
+    from paper_2406_01579_b200 import _native
+    _native.lib()
+    return ts
+
+
+def _mt(ts, R, sdf, deform):
+    g = ts.build_grid(R)
+    fs = ts.FieldState.from_numpy(sdf, deform, ts.deform_limit_for(g))
+    return ts.marching_tetrahedra(g, fs)
+
+
+@pytest.mark.parametrize("tag", ["one_neg", "two_neg"])
+def test_single_tet_examples(ts, tag):
+    G = load_golden("mt.npz")
+    sdf = G[f"{tag}_sdf"]
+    m = _mt(ts, 1, sdf, np.zeros((len(sdf), 3)))
+    assert np.array_equal(m.vertices, G[f"{tag}_V"])
+    assert np.array_equal(m.triangles, G[f"{tag}_F"])
+
+
+@pytest.mark.parametrize("tag,R", [("r16", 16), ("r16_noisy", 16), ("r24", 24)])
+def test_grids_bitexact(ts, tag, R):
+    G = load_golden("mt.npz")
+    m = _mt(ts, R, G[f"{tag}_sdf"], G[f"{tag}_deform"])
+    assert m.vertices.shape == G[f"{tag}_V"].shape
+    assert np.array_equal(m.vertices, G[f"{tag}_V"])
+    assert np.array_equal(m.triangles, G[f"{tag}_F"])
+
+
+def test_sphere_watertight_and_empty(ts):
+    g = ts.build_grid(32)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.41,)))
+    m = ts.marching_tetrahedra(g, f)
+    assert m.euler_characteristic() == 2 and m.is_watertight()
+    e = ts.FieldState.from_numpy(np.ones(g.num_vertices), np.zeros((g.num_vertices, 3)), ts.deform_limit_for(g))
+    assert ts.marching_tetrahedra(g, e).is_empty
