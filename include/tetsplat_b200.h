@@ -115,6 +115,22 @@ int ts_render_backward(const ts_scene* scene, int64_t K, const float* colors, co
                        const int32_t* n_proc, const double* deform, int32_t resolution, float* d_vert,
                        float* d_color, void* stream);
 
+/* Fused per-view pipeline over a persistent, grow-only device workspace (one view in flight
+ * per workspace).  ts_view_forward = build_scene + bin_and_sort + window + render_forward;
+ * out_counts = {K visible splats, M tile pairs, P pixel pairs} (host).  [sync]
+ * ts_view_backward = render_backward of the workspace's last forward, accumulated into d_vert
+ * (and d_color when the forward had colors_tet f32[6R^3,3]). */
+typedef struct ts_workspace ts_workspace;
+ts_workspace* ts_workspace_create(void);
+void ts_workspace_destroy(ts_workspace* ws);
+int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, int32_t resolution,
+                    const ts_camera* cam, double s, const int32_t* active, int64_t n_active, int32_t n_w,
+                    double t_stop, const float* colors_tet, float* normal_map, float* depth_map, float* opacity_map,
+                    float* color_map, int64_t* out_counts, void* stream);
+int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4],
+                     const float* const d_maps[4], float* d_vert, float* d_color, void* stream);
+const int32_t* ts_view_n_blend(ts_workspace* ws);
+
 /* K8 eikonal_loss (losses.py:25-36): loss (device f64[1], overwritten) and
  * scale * gradients accumulated into d_vert. */
 int ts_eikonal(const double* sdf, const double* deform, int32_t resolution, const int32_t* tet_set, int64_t n,

@@ -66,6 +66,12 @@ def lib():
         "ts_marching_tets": ([P, P, I32, P, P, ctypes.POINTER(ctypes.c_int64), P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
+        "ts_workspace_create": ([], P),
+        "ts_workspace_destroy": ([P], None),
+        "ts_view_forward": ([P, P, P, I32, pc, D, P, I64, I32, D, P, P, P, P, P, ctypes.POINTER(ctypes.c_int64), P],
+                            ctypes.c_int),
+        "ts_view_backward": ([P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, P], ctypes.c_int),
+        "ts_view_n_blend": ([P], P),
         "ts_debug_tile_times": ([ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int],
                                 ctypes.c_int),
     }

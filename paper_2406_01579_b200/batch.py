@@ -16,8 +16,9 @@ import torch
 import torch.distributed as dist
 
 from .losses import eikonal_loss_async, normal_consistency_loss_async
-from .raster import GradientBuffers, RenderMaps, bin_and_sort, render_backward, render_forward
-from .splat import EmptySceneError, build_scene, prefilter
+from .raster import GradientBuffers
+from .splat import EmptySceneError, prefilter
+from .view import ViewRenderer
 
 
 def shard_views(n_views: int, rank: int, world: int) -> list[int]:
@@ -91,6 +92,7 @@ class FitStep:
         self.nc_loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.opt = Adam([field.sdf, field.deformation], [self.cfg.lr_sdf, self.cfg.lr_deform], self.cfg.betas) \
             if self.cfg.optimizer else None
+        self.view = ViewRenderer(dev)
 
     def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None):
         g, f, cfg = self.grid, self.field, self.cfg
@@ -102,16 +104,15 @@ class FitStep:
             stats.active = int(active.numel())
         for vi in views:
             cam = self.cameras[vi]
-            scene = build_scene(g, f, cam, s, active=active)
-            if len(scene) == 0:
+            maps = self.view.forward(g, f, cam, s, active, n_w=cfg.n_w)
+            K, M, _ = self.view.counts
+            if K == 0:
                 continue
-            bins = bin_and_sort(scene, cam)
-            maps, saved = render_forward(scene, bins, cam, n_w=cfg.n_w, save_state=True)
-            render_backward(saved, scene, g, f, cam, d_maps_fn(vi, maps), out=self.grads)
+            self.view.backward(f, d_maps_fn(vi, maps), self.grads)
             if stats is not None:
                 stats.views += 1
-                stats.splats.append(len(scene))
-                stats.pairs.append(bins.num_pairs)
+                stats.splats.append(K)
+                stats.pairs.append(M)
         # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce)
         rank0 = not (dist.is_available() and dist.is_initialized()) or dist.get_rank(self.group) == 0
         if rank0:

@@ -19,6 +19,8 @@ static int fail(int code, const char* msg) {
   return code;
 }
 
+void ts_set_error_msg(const char* msg) { g_err = msg; }
+
 static int check_cuda(const char* where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

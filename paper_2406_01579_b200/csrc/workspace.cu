@@ -1,0 +1,226 @@
+// workspace.cu — fused per-view pipeline over a persistent device workspace.
+//
+// ts_view_forward  = build_scene (K2) -> bin_and_sort (K3-K5) -> window + pair numbering ->
+//                    render_forward (K6), with every intermediate in a workspace whose
+//                    buffers only grow.  The three host syncs that size outputs happen inside
+//                    C++ (microseconds), not between Python calls.
+// ts_view_backward = render_backward (K7) + vertex chain into the shared gradient buffer,
+//                    reading the saved state the last ts_view_forward left in the workspace.
+// The fine-grained entry points in abi.cu stay for reference-style use (and tests).
+#include <cstring>
+
+#include "../../include/tetsplat_b200.h"
+#include "internal.cuh"
+#include "scan.cuh"
+
+using namespace ts;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n) {
+    const size_t bytes = (n ? n : 1) * sizeof(T);
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      size_t c = bytes + bytes / 4;  // grow with headroom
+      if (cudaMalloc(&p, c) != cudaSuccess) {
+        p = nullptr;
+        cap = 0;
+        return nullptr;
+      }
+      cap = c;
+    }
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct ts_workspace {
+  // scene
+  Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors;
+  // bins
+  Buf starts, splat_off, items, pos_of, nonmono, witems, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
+  // forward state
+  Buf item_off, pair_code, pair_sig, pair_faces, n_proc, n_blend;
+  // view description of the last forward
+  int64_t K = 0, M = 0, P = 0, maxL = 0;
+  int tiles_x = 0, tiles_y = 0, R = 0;
+  Camera cam{};
+  double s = 0.0;
+  bool color = false;
+  bool valid = false;
+};
+
+void ts_set_error_msg(const char* msg);  // abi.cu (ts_last_error)
+
+static int ws_fail(int code, const char* msg) {
+  ts_set_error_msg(msg);
+  return code;
+}
+
+static Camera cam_of(const ts_camera* c) {
+  Camera k;
+  memcpy(k.R, c->R, sizeof(k.R));
+  memcpy(k.t, c->t, sizeof(k.t));
+  k.fx = c->fx; k.fy = c->fy; k.cx = c->cx; k.cy = c->cy;
+  k.near_ = c->near_; k.far_ = c->far_;
+  k.width = c->width; k.height = c->height;
+  return k;
+}
+
+__global__ void k_gather_colors(int64_t K, const int32_t* __restrict__ tet_ids, const float* __restrict__ ctet,
+                                float* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < 3; ++c) out[k * 3 + c] = ctet[(int64_t)tet_ids[k] * 3 + c];
+}
+
+extern "C" {
+
+ts_workspace* ts_workspace_create(void) { return new ts_workspace(); }
+
+void ts_workspace_destroy(ts_workspace* ws) {
+  if (!ws) return;
+  Buf* all[] = {&ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
+                &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
+                &ws->nonmono, &ws->witems, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
+                &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_code, &ws->pair_sig,
+                &ws->pair_faces, &ws->n_proc, &ws->n_blend};
+  cudaDeviceSynchronize();
+  for (Buf* b : all)
+    if (b->p) cudaFree(b->p);
+  delete ws;
+}
+
+int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, int32_t R, const ts_camera* camp,
+                    double s, const int32_t* active, int64_t n_active, int32_t n_w, double t_stop,
+                    const float* colors_tet, float* nmap, float* dmap, float* omap, float* cmap,
+                    int64_t* out_counts, void* stream) {
+  if (!ws || !sdf || !deform || !camp || R < 1 || n_active < 0 || (n_active > 0 && !active) || !nmap || !dmap ||
+      !omap || !out_counts)
+    return ws_fail(TS_EINVAL, "ts_view_forward: bad arguments");
+  if (n_w < 1) return ws_fail(TS_EINVAL, "resorting window must be >= 1");
+  if (camp->width < 1 || camp->height < 1 || camp->width > 32767 || camp->height > 32767)
+    return ws_fail(TS_EINVAL, "image size must be in [1, 32767]");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Camera cam = cam_of(camp);
+  const int tx = (cam.width + TS_TILE - 1) / TS_TILE, ty = (cam.height + TS_TILE - 1) / TS_TILE;
+  const int64_t T = (int64_t)tx * ty, HW = (int64_t)cam.width * cam.height;
+  ws->valid = false;
+  // ---- K2 build_scene ----------------------------------------------------------------------
+  const int64_t cap = n_active > 0 ? n_active : 1;
+  SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), ws->proj.get<double>(cap * 8),
+              ws->depths.get<double>(cap * 4), ws->f.get<double>(cap * 4), ws->normals.get<double>(cap * 3),
+              ws->md.get<double>(cap), ws->amax.get<double>(cap), ws->bbox.get<double>(cap * 4),
+              ws->rec.get<SplatRec>(cap)};
+  int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1));
+  if (!so.tet_ids || !so.rec || !scratch) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  const int64_t K = n_active > 0 ? ts_impl_build_scene(sdf, deform, R, cam, s, active, n_active, so, scratch, st) : 0;
+  // ---- K3-K5 bins ----------------------------------------------------------------------------
+  BinWork w;
+  w.br = reinterpret_cast<BinRec*>(ws->br.get<int4>(cap));
+  w.q = ws->q.get<uint32_t>(cap);
+  w.splat_cnt = ws->splat_cnt.get<int32_t>(cap);
+  w.tile_cnt = ws->tile_cnt.get<int32_t>(T);
+  w.scratch = scratch;
+  w.dev_i64 = ws->dev_i64.get<int64_t>(2);
+  int64_t* starts = ws->starts.get<int64_t>(T + 1);
+  int64_t* splat_off = ws->splat_off.get<int64_t>(cap + 1);
+  uint8_t* nonmono = ws->nonmono.get<uint8_t>(T);
+  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !splat_off || !nonmono)
+    return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  int64_t M = 0, maxL = 0;
+  ts_impl_bin_count(K, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, &M, &maxL, st);
+  int32_t* items = ws->items.get<int32_t>(M);
+  int32_t* pos_of = ws->pos_of.get<int32_t>(M);
+  int32_t* witems = ws->witems.get<int32_t>(M);
+  uint64_t* keys = ws->keys.get<uint64_t>(M);
+  uint64_t* gs = maxL > 16384 ? ws->gsort.get<uint64_t>(2 * M) : nullptr;
+  if (!items || !pos_of || !witems || !keys || (maxL > 16384 && !gs))
+    return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  if (M > 0) ts_impl_bin_sort(K, tx, ty, so.md, w, starts, splat_off, maxL, keys, gs, items, pos_of, nonmono, st);
+  else cudaMemsetAsync(nonmono, 0, T, st);
+  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems};
+  // ---- colors of the visible splats ------------------------------------------------------
+  const float* colors = nullptr;
+  if (colors_tet && cmap && K > 0) {
+    float* c = ws->colors.get<float>(K * 3);
+    if (!c) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+    k_gather_colors<<<(int)((K + 255) / 256 < 4096 ? (K + 255) / 256 : 4096), 256, 0, st>>>(K, so.tet_ids, colors_tet,
+                                                                                            c);
+    colors = c;
+  }
+  // ---- K6 forward ------------------------------------------------------------------------------
+  int32_t* n_proc = ws->n_proc.get<int32_t>(HW);
+  int32_t* n_blend = ws->n_blend.get<int32_t>(HW);
+  int64_t* item_off = ws->item_off.get<int64_t>(M + 1);
+  if (!n_proc || !n_blend || !item_off) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  int64_t P = 0;
+  if (K > 0 && M > 0) P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, so.rec, item_off, st);
+  float2* pc = ws->pair_code.get<float2>(P);
+  float2* psg = ws->pair_sig.get<float2>(P);
+  uint8_t* pf = ws->pair_faces.get<uint8_t>(P);
+  if (!pc || !psg || !pf) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  if (K > 0 && M > 0) {
+    ts_impl_forward(tx, ty, bv, so.rec, colors, Scene64{so.proj, so.depths, so.f, so.bbox}, cam.width, cam.height, s,
+                    (float)t_stop, item_off, pc, psg, pf, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
+                    st);
+  } else {
+    cudaMemsetAsync(nmap, 0, sizeof(float) * 3 * HW, st);
+    cudaMemsetAsync(dmap, 0, sizeof(float) * HW, st);
+    cudaMemsetAsync(omap, 0, sizeof(float) * HW, st);
+    if (cmap) cudaMemsetAsync(cmap, 0, sizeof(float) * 3 * HW, st);
+    cudaMemsetAsync(n_proc, 0, sizeof(int32_t) * HW, st);
+    cudaMemsetAsync(n_blend, 0, sizeof(int32_t) * HW, st);
+  }
+  ws->K = K;
+  ws->M = M;
+  ws->P = P;
+  ws->maxL = maxL;
+  ws->tiles_x = tx;
+  ws->tiles_y = ty;
+  ws->R = R;
+  ws->cam = cam;
+  ws->s = s;
+  ws->color = colors != nullptr;
+  ws->valid = true;
+  out_counts[0] = K;
+  out_counts[1] = M;
+  out_counts[2] = P;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
+  return TS_OK;
+}
+
+int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4], const float* const dmaps[4],
+                     float* d_vert, float* d_color, void* stream) {
+  if (!ws || !ws->valid) return ws_fail(TS_EINVAL, "ts_view_backward: no forward state in the workspace");
+  if (!deform || !maps || !dmaps || !d_vert || !maps[0] || !maps[1] || !maps[2] || !dmaps[0] || !dmaps[1] ||
+      !dmaps[2])
+    return ws_fail(TS_EINVAL, "ts_view_backward: bad arguments");
+  if (ws->K == 0 || ws->M == 0) return TS_OK;
+  const float* m4[4] = {maps[0], maps[1], maps[2], ws->color ? maps[3] : nullptr};
+  const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], ws->color ? dmaps[3] : nullptr};
+  BinsView bv{reinterpret_cast<int64_t*>(ws->starts.p), reinterpret_cast<int64_t*>(ws->splat_off.p),
+              reinterpret_cast<int32_t*>(ws->items.p), reinterpret_cast<int32_t*>(ws->pos_of.p),
+              reinterpret_cast<uint8_t*>(ws->nonmono.p), reinterpret_cast<int32_t*>(ws->witems.p)};
+  ts_impl_backward(ws->tiles_x, ws->tiles_y, bv, ws->M, ws->K, reinterpret_cast<SplatRec*>(ws->rec.p),
+                   ws->color ? reinterpret_cast<float*>(ws->colors.p) : nullptr,
+                   reinterpret_cast<double*>(ws->f.p), reinterpret_cast<int32_t*>(ws->vert_ids.p),
+                   reinterpret_cast<int32_t*>(ws->tet_ids.p), deform, ws->R, ws->cam,
+                   reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<float2*>(ws->pair_code.p),
+                   reinterpret_cast<float2*>(ws->pair_sig.p), reinterpret_cast<uint8_t*>(ws->pair_faces.p), m4, d4,
+                   reinterpret_cast<int32_t*>(ws->n_proc.p), d_vert, ws->color ? d_color : nullptr,
+                   reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
+  return TS_OK;
+}
+
+// n_blend of the last forward (H*W int32, device) — for parity checks
+const int32_t* ts_view_n_blend(ts_workspace* ws) { return ws ? reinterpret_cast<int32_t*>(ws->n_blend.p) : nullptr; }
+
+}  // extern "C"

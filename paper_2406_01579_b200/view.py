@@ -1,0 +1,73 @@
+"""Fused per-view forward/backward over a persistent device workspace (csrc/workspace.cu).
+
+`ViewRenderer.forward` runs build_scene -> bin_and_sort -> window -> render_forward in one C++
+call (the host syncs that size the outputs happen inside C++), `ViewRenderer.backward` runs
+render_backward + the vertex chain on the state the last forward left behind.  Same math
+and kernels as the fine-grained API in splat.py / raster.py (which stays for reference-style
+use); this is what the multi-view fit step uses.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native
+from .raster import GradientBuffers, RenderMaps, DEFAULT_WINDOW
+from .splat import T_STOP
+
+
+class ViewRenderer:
+    def __init__(self, device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._L = _native.lib()
+        self._ws = ctypes.c_void_p(self._L.ts_workspace_create())
+        self._maps = {}
+        self.counts = (0, 0, 0)
+
+    def __del__(self):
+        try:
+            if self._ws and self._L is not None:
+                self._L.ts_workspace_destroy(self._ws)
+        except Exception:
+            pass
+
+    def _maps_for(self, H, W, color):
+        key = (H, W, color)
+        if key not in self._maps:
+            self._maps[key] = RenderMaps.empty(H, W, color, self.device)
+        return self._maps[key]
+
+    def forward(self, grid, field, camera, s: float, active: torch.Tensor, n_w: int = DEFAULT_WINDOW,
+                t_stop: float = T_STOP, colors: torch.Tensor | None = None, out: RenderMaps | None = None,
+                stream=None) -> RenderMaps:
+        """Render one view; `active` = int32 prefilter output.  Returns maps (reused buffers
+        unless `out` is given)."""
+        if n_w < 1:
+            raise ValueError("resorting window must be >= 1")
+        maps = out if out is not None else self._maps_for(camera.height, camera.width, colors is not None)
+        counts = (ctypes.c_int64 * 3)()
+        col = None if colors is None else colors.to(device=self.device, dtype=torch.float32).contiguous()
+        _native.check(self._L.ts_view_forward(
+            self._ws, _native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution, camera.abi(),
+            float(s), _native.ptr(active), int(active.numel()), int(n_w), float(t_stop), _native.ptr(col),
+            _native.ptr(maps.normal), _native.ptr(maps.depth), _native.ptr(maps.opacity), _native.ptr(maps.color),
+            counts, _native.stream_ptr(stream)))
+        self.counts = (counts[0], counts[1], counts[2])
+        self._last = maps
+        return maps
+
+    def backward(self, field, d_maps: RenderMaps, out: GradientBuffers, maps: RenderMaps | None = None,
+                 stream=None) -> GradientBuffers:
+        """Accumulate the last view's dL/d(sdf, deform) (and dL/dcolor) into `out`."""
+        maps = maps if maps is not None else self._last
+        P = ctypes.c_void_p
+        m = (P * 4)(maps.normal.data_ptr(), maps.depth.data_ptr(), maps.opacity.data_ptr(),
+                    maps.color.data_ptr() if maps.color is not None else None)
+        d = (P * 4)(d_maps.normal.data_ptr(), d_maps.depth.data_ptr(), d_maps.opacity.data_ptr(),
+                    d_maps.color.data_ptr() if d_maps.color is not None else None)
+        _native.check(self._L.ts_view_backward(self._ws, _native.ptr(field.deformation),
+                                               ctypes.cast(m, ctypes.POINTER(P)), ctypes.cast(d, ctypes.POINTER(P)),
+                                               _native.ptr(out.d_vert), _native.ptr(out.d_color),
+                                               _native.stream_ptr(stream)))
+        return out

@@ -169,3 +169,29 @@ def test_window_sizes_agree_on_monotone_lists(ts):
     assert torch.equal(m1.normal, m9.normal)
     with pytest.raises(ValueError):
         ts.render_forward(sc, b, cam, n_w=0)
+
+
+@pytest.mark.parametrize("case", RENDER_CASES)
+def test_fused_view_pipeline_matches_api(ts, case):
+    """ViewRenderer (one C++ call per direction over a persistent workspace) == the
+    fine-grained reference-style API, bit for bit."""
+    from paper_2406_01579_b200.view import ViewRenderer
+    G = load_golden(f"render_{case}.npz")
+    g, fs, cam = _setup(ts, G)
+    s = float(G["s"])
+    active = ts.prefilter(g, fs, s)
+    sc = ts.build_scene(g, fs, cam, s, active=active)
+    b = ts.bin_and_sort(sc, cam)
+    maps, saved = ts.render_forward(sc, b, cam, save_state=True)
+    S = int(G["S"])
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    dm = ts.RenderMaps(torch.randn((S, S, 3), device="cuda", generator=gen),
+                       torch.randn((S, S), device="cuda", generator=gen), torch.randn((S, S), device="cuda", generator=gen))
+    gb = ts.render_backward(saved, sc, g, fs, cam, dm)
+    vr = ViewRenderer()
+    m2 = vr.forward(g, fs, cam, s, active)
+    assert vr.counts[0] == len(sc) and vr.counts[1] == b.num_pairs
+    assert torch.equal(m2.normal, maps.normal) and torch.equal(m2.depth, maps.depth)
+    assert torch.equal(m2.opacity, maps.opacity)
+    gb2 = vr.backward(fs, dm, ts.GradientBuffers.zeros(g.num_vertices))
+    assert torch.allclose(gb2.d_vert, gb.d_vert, rtol=1e-6, atol=1e-6 * float(gb.d_vert.abs().max()))
