@@ -558,14 +558,51 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
 }
 
-// per-tile replay of the reference window (_core.pyx:171-187) for tiles whose list is
-// not mean-depth monotone; one thread per flagged tile, window state in global scratch
-__global__ void k_window(int T, const int64_t* __restrict__ starts, const int32_t* __restrict__ items,
-                         const uint8_t* __restrict__ nonmono, const double* __restrict__ md, int n_w,
-                         int32_t* __restrict__ witems, int32_t* __restrict__ widx_s, double* __restrict__ wz_s) {
-  int t = blockIdx.x * blockDim.x + threadIdx.x;
+// per-tile replay of the reference window (_core.pyx:171-187) for tiles whose list is not
+// mean-depth monotone.  One CTA per flagged tile: the list and its mean depths are staged
+// into shared memory (coalesced), then one thread replays the window over shared memory
+// (a global-memory replay is latency-bound: one dependent L2 round trip per pop).
+constexpr int kWinCap = 8192;  // list entries staged in shared memory (12 B each)
+constexpr int kWinW = 64;      // window slots kept in shared memory
+
+__global__ void __launch_bounds__(128) k_window(int T, const int64_t* __restrict__ starts,
+                                                const int32_t* __restrict__ items,
+                                                const uint8_t* __restrict__ nonmono, const double* __restrict__ md,
+                                                int n_w, int32_t* __restrict__ witems, int32_t* __restrict__ widx_s,
+                                                double* __restrict__ wz_s) {
+  const int t = blockIdx.x;
   if (t >= T || !nonmono[t]) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
+  if (L <= kWinCap && n_w <= kWinW) {
+    extern __shared__ __align__(16) unsigned char wsm[];
+    double* smd = reinterpret_cast<double*>(wsm);
+    int32_t* sit = reinterpret_cast<int32_t*>(smd + kWinCap);
+    int32_t* win = sit + kWinCap;  // window = stream positions, in stream order
+    for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+      const int32_t k = items[lo + i];
+      sit[i] = k;
+      smd[i] = md[k];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    int wc = 0;
+    int64_t pos = 0, out = 0;
+    for (;;) {
+      while (wc < n_w && pos < L) win[wc++] = (int32_t)pos++;
+      if (wc == 0) break;
+      int m = 0;
+      double zm = smd[win[0]];
+      for (int i = 1; i < wc; ++i) {
+        const double z = smd[win[i]];
+        if (z < zm) { zm = z; m = i; }
+      }
+      witems[lo + out++] = sit[win[m]];
+      for (int i = m; i < wc - 1; ++i) win[i] = win[i + 1];
+      --wc;
+    }
+    return;
+  }
+  if (threadIdx.x != 0) return;
   int32_t* widx = widx_s + lo;
   double* wz = wz_s + lo;
   int64_t wcount = 0, pos = 0, out = 0;
@@ -956,7 +993,13 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   cudaMallocAsync(&wz, sizeof(double) * M, st);
   cudaMallocAsync(&cnt, sizeof(int32_t) * M, st);
   cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(M), st);
-  k_window<<<(T + 63) / 64, 64, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, b.witems, widx, wz);
+  static bool wattr = false;
+  const int wsmem = kWinCap * 12 + kWinW * 4;
+  if (!wattr) {
+    cudaFuncSetAttribute(k_window, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem);
+    wattr = true;
+  }
+  k_window<<<T, 128, wsmem, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, b.witems, widx, wz);
   k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
   scan_counts(cnt, M, item_off, scratch, st);
   int64_t total = 0;
