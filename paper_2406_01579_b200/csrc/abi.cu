@@ -185,7 +185,7 @@ int ts_forward_prepare(const ts_scene* sc, int64_t K, const ts_bins* b, int64_t 
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   keep_pool_warm();
-  *out_pairs = ts_impl_forward_prepare(tx, ty, bv_of(b), M, sc->mean_depth, n_w,
+  *out_pairs = ts_impl_forward_prepare(tx, ty, bv_of(b), M, sc->mean_depth, n_w, cam->near_, cam->far_,
                                        reinterpret_cast<const SplatRec*>(sc->records), item_off, ST(stream));
   return check_cuda("ts_forward_prepare");
 }

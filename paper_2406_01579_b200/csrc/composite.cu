@@ -558,72 +558,68 @@ __global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
   if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
 }
 
-// per-tile replay of the reference window (_core.pyx:171-187) for tiles whose list is not
-// mean-depth monotone.  One CTA per flagged tile: the list and its mean depths are staged
-// into shared memory (coalesced), then one thread replays the window over shared memory
-// (a global-memory replay is latency-bound: one dependent L2 round trip per pop).
-constexpr int kWinCap = 8192;  // list entries staged in shared memory (12 B each)
-constexpr int kWinW = 64;      // window slots kept in shared memory
+// N_w resorting window (_core.pyx:171-187) for tiles whose list is not mean-depth monotone.
+// The list is sorted by (q, splat) with q = 32-bit quantised mean depth, so entries with
+// different q are already in strict mean-depth order and every q change is a clean boundary:
+// all entries before it are <= all entries after it, so the window pops the whole prefix
+// first (ties go to the earlier position) and then restarts with a fresh window.  The
+// window therefore acts independently on each run of equal q; runs are short, so one
+// thread per run replays the window on it (identity when the run is monotone).
+__device__ __forceinline__ uint32_t qkey(double md, double near_, double far_) {
+  double qq = ddiv(dsub(md, near_), dsub(far_, near_));
+  qq = qq < 0.0 ? 0.0 : qq;
+  qq = qq > 1.0 ? 1.0 : qq;
+  return (uint32_t)(unsigned long long)dmul(qq, 4294967295.0);  // raster.py:132-134
+}
 
 __global__ void __launch_bounds__(128) k_window(int T, const int64_t* __restrict__ starts,
                                                 const int32_t* __restrict__ items,
                                                 const uint8_t* __restrict__ nonmono, const double* __restrict__ md,
-                                                int n_w, int32_t* __restrict__ witems, int32_t* __restrict__ widx_s,
-                                                double* __restrict__ wz_s) {
+                                                int n_w, double near_, double far_, int32_t* __restrict__ witems,
+                                                int32_t* __restrict__ widx_s, double* __restrict__ wz_s) {
   const int t = blockIdx.x;
   if (t >= T || !nonmono[t]) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
-  if (L <= kWinCap && n_w <= kWinW) {
-    extern __shared__ __align__(16) unsigned char wsm[];
-    double* smd = reinterpret_cast<double*>(wsm);
-    int32_t* sit = reinterpret_cast<int32_t*>(smd + kWinCap);
-    int32_t* win = sit + kWinCap;  // window = stream positions, in stream order
-    for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
-      const int32_t k = items[lo + i];
-      sit[i] = k;
-      smd[i] = md[k];
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
+    const double mi = md[items[lo + i]];
+    const uint32_t qi = qkey(mi, near_, far_);
+    if (i > 0 && qkey(md[items[lo + i - 1]], near_, far_) == qi) continue;  // not a run start
+    int64_t e = i + 1;
+    bool mono = true;
+    double prev = mi;
+    while (e < L) {
+      const double me = md[items[lo + e]];
+      if (qkey(me, near_, far_) != qi) break;
+      mono &= !(me < prev);
+      prev = me;
+      ++e;
     }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    int wc = 0;
-    int64_t pos = 0, out = 0;
+    if (mono) {
+      for (int64_t k = i; k < e; ++k) witems[lo + k] = items[lo + k];
+      continue;
+    }
+    int32_t* widx = widx_s + lo + i;
+    double* wz = wz_s + lo + i;
+    int64_t wcount = 0, pos = i, out = i;
     for (;;) {
-      while (wc < n_w && pos < L) win[wc++] = (int32_t)pos++;
-      if (wc == 0) break;
-      int m = 0;
-      double zm = smd[win[0]];
-      for (int i = 1; i < wc; ++i) {
-        const double z = smd[win[i]];
-        if (z < zm) { zm = z; m = i; }
+      while (wcount < n_w && pos < e) {
+        const int32_t k = items[lo + pos];
+        widx[wcount] = k;
+        wz[wcount] = md[k];
+        ++wcount;
+        ++pos;
       }
-      witems[lo + out++] = sit[win[m]];
-      for (int i = m; i < wc - 1; ++i) win[i] = win[i + 1];
-      --wc;
+      if (wcount == 0) break;
+      int64_t m = 0;
+      for (int64_t k = 1; k < wcount; ++k)
+        if (wz[k] < wz[m]) m = k;
+      witems[lo + out++] = widx[m];
+      for (int64_t k = m; k < wcount - 1; ++k) {
+        widx[k] = widx[k + 1];
+        wz[k] = wz[k + 1];
+      }
+      --wcount;
     }
-    return;
-  }
-  if (threadIdx.x != 0) return;
-  int32_t* widx = widx_s + lo;
-  double* wz = wz_s + lo;
-  int64_t wcount = 0, pos = 0, out = 0;
-  for (;;) {
-    while (wcount < n_w && pos < L) {
-      int32_t k = items[lo + pos];
-      widx[wcount] = k;
-      wz[wcount] = md[k];
-      ++wcount;
-      ++pos;
-    }
-    if (wcount == 0) break;
-    int64_t m = 0;
-    for (int64_t i = 1; i < wcount; ++i)
-      if (wz[i] < wz[m]) m = i;
-    witems[lo + out++] = widx[m];
-    for (int64_t i = m; i < wcount - 1; ++i) {
-      widx[i] = widx[i + 1];
-      wz[i] = wz[i + 1];
-    }
-    --wcount;
   }
 }
 
@@ -979,7 +975,7 @@ using namespace ts;
 
 // window-resorted lists + pair offsets of the view: item_off[M+1]; returns the pair count
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int64_t M, const double* md, int n_w,
-                                const SplatRec* rec, int64_t* item_off, cudaStream_t st) {
+                                double near_, double far_, const SplatRec* rec, int64_t* item_off, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
   if (M <= 0) {
     cudaMemsetAsync(item_off, 0, sizeof(int64_t), st);
@@ -993,13 +989,7 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   cudaMallocAsync(&wz, sizeof(double) * M, st);
   cudaMallocAsync(&cnt, sizeof(int32_t) * M, st);
   cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(M), st);
-  static bool wattr = false;
-  const int wsmem = kWinCap * 12 + kWinW * 4;
-  if (!wattr) {
-    cudaFuncSetAttribute(k_window, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem);
-    wattr = true;
-  }
-  k_window<<<T, 128, wsmem, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, b.witems, widx, wz);
+  k_window<<<T, 128, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, widx, wz);
   k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
   scan_counts(cnt, M, item_off, scratch, st);
   int64_t total = 0;

@@ -57,7 +57,8 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
                       uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st);
 void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n);
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, const double* md,
-                                int n_w, const ts::SplatRec* rec, int64_t* item_off, cudaStream_t st);
+                                int n_w, double near_, double far_, const ts::SplatRec* rec, int64_t* item_off,
+                                cudaStream_t st);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
                      const ts::Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
                      float2* pair_code, float2* pair_sig, uint8_t* pair_faces, float* nmap, float* dmap, float* omap,

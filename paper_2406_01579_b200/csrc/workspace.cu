@@ -159,7 +159,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   int64_t* item_off = ws->item_off.get<int64_t>(M + 1);
   if (!n_proc || !n_blend || !item_off) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   int64_t P = 0;
-  if (K > 0 && M > 0) P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, so.rec, item_off, st);
+  if (K > 0 && M > 0) P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st);
   float2* pc = ws->pair_code.get<float2>(P);
   float2* psg = ws->pair_sig.get<float2>(P);
   uint8_t* pf = ws->pair_faces.get<uint8_t>(P);
