@@ -445,7 +445,7 @@ __device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, bool 
 }
 
 template <bool COLOR>
-__global__ void __launch_bounds__(TS_TILE_PX, 2) k_forward(
+__global__ void __launch_bounds__(TS_TILE_PX, 3) k_forward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, const int64_t* __restrict__ item_off,
@@ -745,7 +745,7 @@ __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty
 }
 
 template <bool COLOR>
-__global__ void __launch_bounds__(TS_TILE_PX, 2) k_backward(
+__global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     int tiles_x, int W, int H, const int64_t* __restrict__ item_off, const float2* __restrict__ pair_code,
