@@ -42,8 +42,9 @@ namespace ts {
 
 constexpr float kAlphaClipF = 0.9999f;  // splat.py:14
 constexpr float kOneMinusClipF = 1e-4f;
-constexpr int kCh = 32;      // max splats per chunk
+constexpr int kCh = 64;      // max splats per chunk (one bit each in the per-pixel masks)
 constexpr int kCap = 2048;   // max (pixel, splat) pairs per chunk
+typedef unsigned long long ChunkMask;
 constexpr int kGr = 24;      // floats per (tile, splat) gradient row
 constexpr int kWarps = TS_TILE_PX / 32;
 
@@ -354,36 +355,38 @@ struct RectTab {
   int x0[kCh], y0[kCh], nx[kCh];
   float inv[kCh];
   int pre[kCh + 1];  // exclusive prefix of pair counts
+  int wtot[kCh / 32], wok[kCh / 32];  // staging scan exchange
   int n;             // splats in this chunk
   int64_t ib0;       // global index of the chunk's first pair
   uint8_t jtab[kCap];  // splat of each pair
 };
 
-// Warp 0 only: stage up to kCh records from list position `base` (at most `avail`) and cut
-// the chunk so it holds at most kCap pairs.
+// Threads [0, kCh) only: stage up to kCh records from list position `base` (at most
+// `avail`) and cut the chunk so it holds at most kCap pairs.  The warps exchange their scan
+// totals through `wtot` behind a named barrier over the kCh staging threads.
 __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, int base, int avail,
                                             const SplatRec* __restrict__ recs, const float* __restrict__ colors,
                                             bool color, Staged* sh, float (*col)[3], RectTab& R, int tx0, int ty0,
                                             const int64_t* __restrict__ item_off_tile) {
-  const int lane = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int m = min(kCh, avail);
   int cnt = 0;
-  if (lane < m) {
-    const int k = list[base + lane];
-    stage(recs, k, sh[lane]);
-    const Staged& r = sh[lane];
+  if (t < m) {
+    const int k = list[base + t];
+    stage(recs, k, sh[t]);
+    const Staged& r = sh[t];
     int x0, y0, nx;
     if (!tile_rect(r.rx0, r.rx1, r.ry0, r.ry1, tx0, ty0, x0, y0, nx, cnt)) {
       nx = 1;
       cnt = 0;
       x0 = y0 = 0;
     }
-    R.x0[lane] = x0;
-    R.y0[lane] = y0;
-    R.nx[lane] = nx;
-    R.inv[lane] = 1.0f / (float)nx;
+    R.x0[t] = x0;
+    R.y0[t] = y0;
+    R.nx[t] = nx;
+    R.inv[t] = 1.0f / (float)nx;
     if (color)
-      for (int c = 0; c < 3; ++c) col[lane][c] = colors[(int64_t)k * 3 + c];
+      for (int c = 0; c < 3; ++c) col[t][c] = colors[(int64_t)k * 3 + c];
   }
   int v = cnt;
 #pragma unroll
@@ -391,18 +394,25 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
     int y = __shfl_up_sync(0xffffffffu, v, o);
     if (lane >= o) v += y;
   }
-  if (lane < m) R.pre[lane + 1] = v;
+  if (lane == 31) R.wtot[wid] = v;
+  asm volatile("bar.sync 1, %0;" ::"n"(kCh));
+  for (int w = 0; w < wid; ++w) v += R.wtot[w];
+  if (t < m) R.pre[t + 1] = v;
   // cut: the largest prefix with at most kCap pairs (one splat has <= 256 pairs)
-  const unsigned ok = __ballot_sync(0xffffffffu, lane < m && v <= kCap);
-  const int n = __popc(ok);
-  if (lane < n)
-    for (int it = v - cnt; it < v; ++it) R.jtab[it] = (uint8_t)lane;
-  if (lane == 0) {
+  const unsigned ok = __ballot_sync(0xffffffffu, t < m && v <= kCap);
+  if (lane == 0) R.wok[wid] = __popc(ok);
+  asm volatile("bar.sync 1, %0;" ::"n"(kCh));
+  int n = 0;
+  for (int w = 0; w < kCh / 32; ++w) n += R.wok[w];
+  if (t < n)
+    for (int it = v - cnt; it < v; ++it) R.jtab[it] = (uint8_t)t;
+  if (t == 0) {
     R.pre[0] = 0;
     R.n = n;
     R.ib0 = item_off_tile[base];
   }
 }
+
 
 __device__ __forceinline__ int pair_splat(const RectTab& R, int it) { return R.jtab[it]; }
 
@@ -422,7 +432,7 @@ __device__ __forceinline__ int pair_index(const RectTab& R, int j, int xi, int y
 struct FwdSmem {
   Staged sh[kCh];
   float2 code[kCap];  // (alpha, 1 - alpha) per pair of the chunk
-  uint32_t bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
+  ChunkMask bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   float col[kCh][3];
   uint32_t skip[TS_TILE_PX / 32];
   uint16_t exq[kCap];  // pairs queued for the exact FP64 re-decision
@@ -438,14 +448,14 @@ __device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, bool 
   pair_code[ib0 + it] = c;
   if (bl) {
     F.code[it] = c;
-    atomicOr(&F.bmask[q], 1u << j);
+    atomicOr(&F.bmask[q], 1ull << j);
     pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
     pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
   }
 }
 
 template <bool COLOR>
-__global__ void __launch_bounds__(TS_TILE_PX, 3) k_forward(
+__global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, const int64_t* __restrict__ item_off,
@@ -478,9 +488,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_forward(
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
   }
   for (int base = 0; base < L;) {
-    if (threadIdx.x < 32)
+    if (threadIdx.x < kCh)
       stage_chunk(list, base, L - base, recs, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
-    F.bmask[pix] = 0u;
+    F.bmask[pix] = 0ull;
     if (threadIdx.x == 0) F.nex = 0;
     __syncthreads();
     const int n = F.R.n, total = F.R.pre[n];
@@ -518,10 +528,10 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_forward(
     __syncthreads();
     // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
     if (!done) {
-      unsigned m = F.bmask[pix];
+      ChunkMask m = F.bmask[pix];
       while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1u;
+        const int j = __ffsll(m) - 1;
+        m &= m - 1ull;
         const float2 c = F.code[pair_index(F.R, j, xi, yi)];
         acc.add(__fmul_rn(T, c.x), F.sh[j], COLOR ? F.col[j] : nullptr);
         T = __fmul_rn(T, fabsf(c.y));
@@ -683,7 +693,7 @@ struct BwdSmem {
   float col[kCh][3];
   int buf[kWarps][64];       // per-warp compacted items (j << 16 | pair)
   float rows[kWarps][32][kGr];
-  uint32_t bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
+  ChunkMask bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   RectTab R;
   int maxproc;
 };
@@ -797,9 +807,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   Accum<COLOR> P;
   P.zero();
   for (int base = 0; base < maxproc;) {
-    if (threadIdx.x < 32)
+    if (threadIdx.x < kCh)
       stage_chunk(list, base, maxproc - base, recs, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
-    S.bmask[pix] = 0u;
+    S.bmask[pix] = 0ull;
     __syncthreads();
     const int n = S.R.n, total = S.R.pre[n];
     const int64_t ib0 = S.R.ib0;
@@ -811,16 +821,16 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         const int j = pair_splat(S.R, it);
         int px_, py_;
         pair_pixel(S.R, j, it, px_, py_);
-        atomicOr(&S.bmask[(py_ - ty0) * TS_TILE + (px_ - tx0)], 1u << j);
+        atomicOr(&S.bmask[(py_ - ty0) * TS_TILE + (px_ - tx0)], 1ull << j);
       }
     }
     for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
     __syncthreads();
     // ---- B: pixel-serial prefix walk over this pixel's blended splats -> (w, G) --------------
     const int lim = nproc - base;  // splats j >= lim lie past this pixel's early stop
-    for (unsigned m = S.bmask[pix]; m;) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1u;
+    for (ChunkMask m = S.bmask[pix]; m;) {
+      const int j = __ffsll(m) - 1;
+      m &= m - 1ull;
       const int it = pair_index(S.R, j, xi, yi);
       if (j >= lim) {  // code may be stale (pixel skipped by the forward): no contribution
         S.wg[it] = make_float2(0.f, 0.f);
