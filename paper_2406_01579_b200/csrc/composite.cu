@@ -689,7 +689,6 @@ struct BwdSmem {
   Staged sh[kCh];
   float2 wg[kCap];           // load: (alpha, 1-alpha); phase B: (w = T a, G)
   float acc[kCh][kGr];       // per-(tile, splat) gradient rows of the chunk
-  float gpx[TS_TILE_PX][8];  // per-pixel upstream gradients: g_d, g_n[3], g_c[3]
   float col[kCh][3];
   int buf[kWarps][64];       // per-warp compacted items (j << 16 | pair)
   float rows[kWarps][32][kGr];
@@ -701,7 +700,9 @@ struct BwdSmem {
 template <bool COLOR>
 __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty0,
                                               const float2* __restrict__ pair_sig,
-                                              const uint8_t* __restrict__ pair_faces, int64_t ib0) {
+                                              const uint8_t* __restrict__ pair_faces, int64_t ib0, int W,
+                                              const float* __restrict__ d_normal, const float* __restrict__ d_depth,
+                                              const float* __restrict__ d_color) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* row = S.rows[warp][lane];
   if (lane < m) {
@@ -712,20 +713,19 @@ __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty
     const int nx = S.R.nx[j];
     const int yy = (int)(((float)local + 0.5f) * S.R.inv[j]);
     const int xi = S.R.x0[j] + (local - yy * nx), yi = S.R.y0[j] + yy;
-    const int pix = (yi - ty0) * TS_TILE + (xi - tx0);
+    const int64_t p = (int64_t)yi * W + xi;
     const float2 wg = S.wg[it];
     const float w = wg.x, G = wg.y;
-    const float* gp = S.gpx[pix];
 #pragma unroll
     for (int i = 0; i < 16; ++i) row[i] = 0.f;
-    row[16] = gp[1] * w;
-    row[17] = gp[2] * w;
-    row[18] = gp[3] * w;
-    row[19] = gp[0] * w;
+    row[16] = __ldg(d_normal + p * 3) * w;
+    row[17] = __ldg(d_normal + p * 3 + 1) * w;
+    row[18] = __ldg(d_normal + p * 3 + 2) * w;
+    row[19] = __ldg(d_depth + p) * w;
     if (COLOR) {
-      row[20] = gp[4] * w;
-      row[21] = gp[5] * w;
-      row[22] = gp[6] * w;
+      row[20] = __ldg(d_color + p * 3) * w;
+      row[21] = __ldg(d_color + p * 3 + 1) * w;
+      row[22] = __ldg(d_color + p * 3 + 2) * w;
     }
     if (G != 0.f) {
       const float2 sg = pair_sig[ib0 + it];
@@ -794,13 +794,6 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
       }
     }
   }
-  S.gpx[pix][0] = g_d;
-  S.gpx[pix][1] = g_n[0];
-  S.gpx[pix][2] = g_n[1];
-  S.gpx[pix][3] = g_n[2];
-  S.gpx[pix][4] = g_c[0];
-  S.gpx[pix][5] = g_c[1];
-  S.gpx[pix][6] = g_c[2];
   __syncthreads();
   const int maxproc = S.maxproc;
   float T = 1.f;
@@ -872,7 +865,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
           cnt += __popc(m);
           __syncwarp();
           if (cnt >= 32) {
-            process_items<COLOR>(S, 32, tx0, ty0, pair_sig, pair_faces, ib0);
+            process_items<COLOR>(S, 32, tx0, ty0, pair_sig, pair_faces, ib0, W, d_normal, d_depth, d_color);
             const int rest = cnt - 32;
             const int moved = lane < rest ? S.buf[warp][32 + lane] : 0;
             __syncwarp();
@@ -882,7 +875,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
           }
         }
       }
-      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_sig, pair_faces, ib0);
+      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_sig, pair_faces, ib0, W, d_normal, d_depth, d_color);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += TS_TILE_PX) {
