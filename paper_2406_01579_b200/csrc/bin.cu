@@ -41,33 +41,59 @@ __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const do
                             int tiles_y, double near_, double far_, BinRec* __restrict__ br,
                             uint32_t* __restrict__ qout, int32_t* __restrict__ splat_cnt,
                             int32_t* __restrict__ tile_cnt) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
-    int tx0, tx1, ty0, ty1;
-    uint32_t q;
-    tile_rect_q(bbox + k * 4, md[k], tiles_x, tiles_y, near_, far_, tx0, tx1, ty0, ty1, q);
-    int nx = tx1 - tx0 + 1, ny = ty1 - ty0 + 1;
-    if (nx < 0) nx = 0;
-    if (ny < 0) ny = 0;
-    br[k] = BinRec{tx0, ty0, nx, ny};
-    qout[k] = q;
-    splat_cnt[k] = nx * ny;
-    for (int y = 0; y < ny; ++y)
-      for (int x = 0; x < nx; ++x) atomicAdd(&tile_cnt[(ty0 + y) * tiles_x + tx0 + x], 1);
+  // warp-uniform loop so the per-tile counter updates can be aggregated per warp: splats
+  // with nearby tet ids are nearby in space and mostly share tiles (one atomic per
+  // distinct tile per warp instead of one per (splat, tile) pair)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x; k0 < K; k0 += stride) {
+    const int64_t k = k0 + threadIdx.x;
+    int tx0 = 0, ty0 = 0, nx = 0, ny = 0;
+    if (k < K) {
+      int tx1, ty1;
+      uint32_t q;
+      tile_rect_q(bbox + k * 4, md[k], tiles_x, tiles_y, near_, far_, tx0, tx1, ty0, ty1, q);
+      nx = tx1 - tx0 + 1;
+      ny = ty1 - ty0 + 1;
+      if (nx < 0) nx = 0;
+      if (ny < 0) ny = 0;
+      br[k] = BinRec{tx0, ty0, nx, ny};
+      qout[k] = q;
+      splat_cnt[k] = nx * ny;
+    }
+    const int cnt = nx * ny;
+    const int wmax = __reduce_max_sync(0xffffffffu, cnt);
+    for (int i = 0; i < wmax; ++i) {
+      const int t = i < cnt ? (ty0 + i / nx) * tiles_x + tx0 + i % nx : -1;
+      const unsigned same = __match_any_sync(0xffffffffu, t);
+      if (t >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&tile_cnt[t], __popc(same));
+    }
   }
 }
 
 __global__ void k_bin_scatter(int64_t K, const BinRec* __restrict__ br, const uint32_t* __restrict__ q, int tiles_x,
                               const int64_t* __restrict__ starts, int32_t* __restrict__ cursor,
                               uint64_t* __restrict__ keys) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
-    BinRec b = br[k];
-    uint64_t key = ((uint64_t)q[k] << 32) | (uint64_t)(uint32_t)k;
-    for (int y = 0; y < b.ny; ++y)
-      for (int x = 0; x < b.nx; ++x) {
-        int t = (b.ty0 + y) * tiles_x + b.tx0 + x;
-        int slot = atomicAdd(&cursor[t], 1);
-        keys[starts[t] + slot] = key;
-      }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const unsigned lane = threadIdx.x & 31;
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x; k0 < K; k0 += stride) {
+    const int64_t k = k0 + threadIdx.x;
+    BinRec b{0, 0, 0, 0};
+    uint64_t key = 0;
+    if (k < K) {
+      b = br[k];
+      key = ((uint64_t)q[k] << 32) | (uint64_t)(uint32_t)k;
+    }
+    const int cnt = b.nx * b.ny;
+    const int wmax = __reduce_max_sync(0xffffffffu, cnt);
+    for (int i = 0; i < wmax; ++i) {
+      const int t = i < cnt ? (b.ty0 + i / b.nx) * tiles_x + b.tx0 + i % b.nx : -1;
+      const unsigned same = __match_any_sync(0xffffffffu, t);
+      const int leader = __ffs(same) - 1;
+      int base = 0;
+      if (t >= 0 && (int)lane == leader) base = atomicAdd(&cursor[t], __popc(same));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (t >= 0) keys[starts[t] + base + __popc(same & ((1u << lane) - 1u))] = key;
+    }
   }
 }
 
@@ -236,13 +262,15 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
     if (maxL > 2048) {
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(k_tile_sort_smem<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_tile_sort_smem<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              16384 * (int)sizeof(uint64_t));
         attr = true;
       }
-      k_tile_sort_smem<1024><<<T, 1024, 16384 * sizeof(uint64_t), st>>>(T, 2048, 16384, starts, keys, tiles_x,
-                                                                         w.br, splat_off, md, items, pos_of,
-                                                                         nonmono);
+      // shared memory sized to the longest list (not the 16384 cap) so several CTAs fit per SM
+      int64_t P = 4096;
+      while (P < maxL && P < 16384) P <<= 1;
+      k_tile_sort_smem<512><<<T, 512, P * sizeof(uint64_t), st>>>(T, 2048, 16384, starts, keys, tiles_x, w.br,
+                                                                  splat_off, md, items, pos_of, nonmono);
     }
     if (maxL > 16384)
       k_tile_sort_global<<<T, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,

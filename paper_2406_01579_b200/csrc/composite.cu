@@ -917,53 +917,71 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
         a[4 * i + 3] += q.w;
       }
     }
-    double dF[4], dZ[4], dPx[4], dPy[4], dPos[4][3];
-    const double dMd = a[19];
+    // FP32 chain math (the gradients are FP32); only the tet edge vectors and the camera-space
+    // positions are formed in FP64 (differences of O(1) coordinates) before rounding.
+    float dF[4], dZ[4], dPx[4], dPy[4], dPos[4][3];
+    const float dMd = a[19];
     for (int v = 0; v < 4; ++v) {
       dF[v] = a[v];
-      dZ[v] = (double)a[4 + v] + dMd / 4.0;
+      dZ[v] = a[4 + v] + 0.25f * dMd;
       dPx[v] = a[8 + v];
       dPy[v] = a[12 + v];
-      dPos[v][0] = dPos[v][1] = dPos[v][2] = 0.0;
+      dPos[v][0] = dPos[v][1] = dPos[v][2] = 0.f;
     }
     uint32_t vid[4];
-    double P[4][3], f[4];
+    double P[4][3], f64[4];
     for (int v = 0; v < 4; ++v) {
       vid[v] = (uint32_t)vert_ids[k * 4 + v];
       vertex_position(vid[v], G, deform, P[v]);
-      f[v] = fsc[k * 4 + v];
+      f64[v] = fsc[k * 4 + v];
     }
     // normal chain: n = g/|g|, dL/dg = (I - n n^T) dL/dn / |g|, dL/df = B^-T [dL/dg, 0]
-    double g[3], c1[3], c2[3], c3[3];
-    double det = tet_gradient(P, f, g, c1, c2, c3);
-    double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-    if (gn >= 1e-8 && det != 0.0) {
-      double nn[3] = {g[0] / gn, g[1] / gn, g[2] / gn};
-      double dn[3] = {a[16], a[17], a[18]};
-      double dot = nn[0] * dn[0] + nn[1] * dn[1] + nn[2] * dn[2];
-      double dg[3];
-      for (int i = 0; i < 3; ++i) dg[i] = (dn[i] - nn[i] * dot) / gn;
-      double d1 = (c1[0] * dg[0] + c1[1] * dg[1] + c1[2] * dg[2]) / det;
-      double d2 = (c2[0] * dg[0] + c2[1] * dg[1] + c2[2] * dg[2]) / det;
-      double d3 = (c3[0] * dg[0] + c3[1] * dg[1] + c3[2] * dg[2]) / det;
-      double dfn[4] = {-(d1 + d2 + d3), d1, d2, d3};
-      for (int v = 0; v < 4; ++v) {
-        dF[v] += dfn[v];
-        for (int i = 0; i < 3; ++i) dPos[v][i] -= dfn[v] * g[i];
+    // (B^-T [dL/dg, 0] in the cross-product form of _core.pyx:517-541)
+    float e1[3], e2[3], e3[3];
+    for (int i = 0; i < 3; ++i) {
+      e1[i] = (float)(P[1][i] - P[0][i]);
+      e2[i] = (float)(P[2][i] - P[0][i]);
+      e3[i] = (float)(P[3][i] - P[0][i]);
+    }
+    const float df1 = (float)(f64[1] - f64[0]), df2 = (float)(f64[2] - f64[0]), df3 = (float)(f64[3] - f64[0]);
+    const float c1[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2], e2[0] * e3[1] - e2[1] * e3[0]};
+    const float c2[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2], e3[0] * e1[1] - e3[1] * e1[0]};
+    const float c3[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const float det = e1[0] * c1[0] + e1[1] * c1[1] + e1[2] * c1[2];
+    if (det != 0.f) {
+      const float idet = 1.0f / det;
+      float g[3];
+      for (int i = 0; i < 3; ++i) g[i] = (df1 * c1[i] + df2 * c2[i] + df3 * c3[i]) * idet;
+      const float gn = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+      if (gn >= 1e-8f) {
+        const float ign = 1.0f / gn;
+        const float nn[3] = {g[0] * ign, g[1] * ign, g[2] * ign};
+        const float dn[3] = {a[16], a[17], a[18]};
+        const float dot = nn[0] * dn[0] + nn[1] * dn[1] + nn[2] * dn[2];
+        float dg[3];
+        for (int i = 0; i < 3; ++i) dg[i] = (dn[i] - nn[i] * dot) * ign;
+        const float d1 = (c1[0] * dg[0] + c1[1] * dg[1] + c1[2] * dg[2]) * idet;
+        const float d2 = (c2[0] * dg[0] + c2[1] * dg[1] + c2[2] * dg[2]) * idet;
+        const float d3 = (c3[0] * dg[0] + c3[1] * dg[1] + c3[2] * dg[2]) * idet;
+        const float dfn[4] = {-(d1 + d2 + d3), d1, d2, d3};
+        for (int v = 0; v < 4; ++v) {
+          dF[v] += dfn[v];
+          for (int i = 0; i < 3; ++i) dPos[v][i] -= dfn[v] * g[i];
+        }
       }
     }
     // camera chain: pixel = (fx X/Z + cx, fy Y/Z + cy), depth = Z
+    const float fx = (float)cam.fx, fy = (float)cam.fy;
     for (int v = 0; v < 4; ++v) {
-      double pc[3];
+      float pc[3];
       for (int r = 0; r < 3; ++r)
-        pc[r] = P[v][0] * cam.R[r * 3] + P[v][1] * cam.R[r * 3 + 1] + P[v][2] * cam.R[r * 3 + 2] + cam.t[r];
-      const double X = pc[0], Y = pc[1], Z = pc[2];
-      const double dpc[3] = {dPx[v] * cam.fx / Z, dPy[v] * cam.fy / Z,
-                             -dPx[v] * cam.fx * X / (Z * Z) - dPy[v] * cam.fy * Y / (Z * Z) + dZ[v]};
+        pc[r] = (float)(P[v][0] * cam.R[r * 3] + P[v][1] * cam.R[r * 3 + 1] + P[v][2] * cam.R[r * 3 + 2] + cam.t[r]);
+      const float iZ = 1.0f / pc[2];
+      const float dpc[3] = {dPx[v] * fx * iZ, dPy[v] * fy * iZ,
+                            (-dPx[v] * fx * pc[0] - dPy[v] * fy * pc[1]) * iZ * iZ + dZ[v]};
       for (int j = 0; j < 3; ++j)
-        dPos[v][j] += dpc[0] * cam.R[j] + dpc[1] * cam.R[3 + j] + dpc[2] * cam.R[6 + j];
-      red_add_v4(d_vert + (size_t)vid[v] * 4, (float)dF[v], (float)dPos[v][0], (float)dPos[v][1],
-                 (float)dPos[v][2]);
+        dPos[v][j] += dpc[0] * (float)cam.R[j] + dpc[1] * (float)cam.R[3 + j] + dpc[2] * (float)cam.R[6 + j];
+      red_add_v4(d_vert + (size_t)vid[v] * 4, dF[v], dPos[v][0], dPos[v][1], dPos[v][2]);
     }
     if (COLOR) {
       const int64_t t = tet_ids[k];
