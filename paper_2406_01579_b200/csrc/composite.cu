@@ -45,6 +45,12 @@ constexpr float kOneMinusClipF = 1e-4f;
 constexpr int kCh = 64;      // max splats per chunk (one bit each in the per-pixel masks)
 constexpr int kCap = 2048;   // max (pixel, splat) pairs per chunk
 typedef unsigned long long ChunkMask;
+
+// set bit j of a 64-bit shared mask with a native 32-bit atomic (64-bit shared atomicOr is
+// a CAS loop on sm_100)
+__device__ __forceinline__ void mask_set(ChunkMask* m, int j) {
+  atomicOr(reinterpret_cast<unsigned*>(m) + (j >> 5), 1u << (j & 31));
+}
 constexpr int kGr = 24;      // floats per (tile, splat) gradient row
 constexpr int kWarps = TS_TILE_PX / 32;
 
@@ -448,7 +454,7 @@ __device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, bool 
   pair_code[ib0 + it] = c;
   if (bl) {
     F.code[it] = c;
-    atomicOr(&F.bmask[q], 1ull << j);
+    mask_set(&F.bmask[q], j);
     pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
     pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
   }
@@ -814,7 +820,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         const int j = pair_splat(S.R, it);
         int px_, py_;
         pair_pixel(S.R, j, it, px_, py_);
-        atomicOr(&S.bmask[(py_ - ty0) * TS_TILE + (px_ - tx0)], 1ull << j);
+        mask_set(&S.bmask[(py_ - ty0) * TS_TILE + (px_ - tx0)], j);
       }
     }
     for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
