@@ -37,7 +37,7 @@ LAMBDA = 1000.0
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -169,7 +169,7 @@ class ClockSampler:
             return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -330,6 +330,7 @@ def run_gpu(args):
     roof, kernels = roofline_probe(ts, _native, g, field, cams[views[0]], dmaps[views[0]], s, sdf0, def0)
 
     launches_per_step, other_launches, per_kernel = count_my_kernels(lambda: one_step())
+    ktab = kernel_table(lambda: one_step())
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -342,7 +343,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches_per_step * args.steps),
             "gpu_launches_per_step": {"libtetsplat_b200": launches_per_step, "torch_other": other_launches},
-            "clocks": clk.result, "roofline": roof, "kernels": kernels,
+            "clocks": clk.result, "roofline": roof, "kernels": kernels, "kernel_ms_per_step": ktab,
             "workload_counts": {"active_tets": stats.active, "splats_view0": stats.splats[:1],
                                 "pairs_view0": stats.pairs[:1]}}
     if not args.no_cpu_baseline:
@@ -354,89 +355,79 @@ def run_gpu(args):
 
 
 def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
-    """Average device time of each stage's kernels (CUDA events on the launching stream) and
-    the roofline of the dominant kernel.  Work models: SURVEY.md §8d; DESIGN.md §Roofline."""
+    """Roofline of the two compositing launches, timed with CUDA events recorded on the
+    launching stream immediately around each launch (render_forward = the compositing
+    kernel; render_backward = compositing backward + vertex chain), averaged over reps.
+    Algorithmic work (the reference's own per-pair / per-record operation counts, SURVEY.md
+    §8d): forward 8 P_pop + 120 P_bbox + 19 B flops, backward 300 B + 300 K_v flops."""
     import torch
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if \
         os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     fp32_peak = n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s (FMA = 2)
     field.sdf.copy_(sdf0)
     field.deformation.copy_(def0)
-    st = torch.cuda.current_stream()
     reps = 5
-    acc = {k: 0.0 for k in ("prefilter", "build_scene", "bin_and_sort", "render_forward", "render_backward",
-                            "eikonal", "normal_consistency")}
-    cnt = None
+    tf = tb = 0.0
     for r in range(reps + 1):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
-        ev[0].record(st)
         act = ts.prefilter(g, field, s)
-        ev[1].record(st)
         sc = ts.build_scene(g, field, cam, s, active=act)
-        ev[2].record(st)
         b = ts.bin_and_sort(sc, cam)
-        ev[3].record(st)
         _native.debug_counters(True)
-        ev[3].synchronize()
-        e_f0 = torch.cuda.Event(enable_timing=True)
-        e_f0.record(st)
-        maps, sv = ts.render_forward(sc, b, cam, save_state=True)
-        ev[4].record(st)
-        gb = ts.render_backward(sv, sc, g, field, cam, dm)
-        ev[5].record(st)
-        ts.eikonal_loss(g, field, act, out=gb, scale=LAMBDA)
-        ev[6].record(st)
-        ts.normal_consistency_loss(g, field, out=gb, scale=LAMBDA)
-        ev[7].record(st)
+        ef = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        eb = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        maps, sv = ts.render_forward(sc, b, cam, save_state=True, timing=ef)
+        ts.render_backward(sv, sc, g, field, cam, dm, timing=eb)
         torch.cuda.synchronize()
         if r == 0:
             cnt = _native.debug_counters(True)
             P_pop = int(sv.n_proc.sum())
             B = int(sv.n_blend.sum())
             K_a, K_v, M = int(act.numel()), len(sc), b.num_pairs
+            P_pairs = int(sv.item_off[-1].item())
             continue
-        names = list(acc)
-        for i, n in enumerate(names):
-            a0 = e_f0 if n == "render_forward" else ev[i]
-            acc[n] += a0.elapsed_time(ev[i + 1])
-    ms = {k: v / reps for k, v in acc.items()}
+        tf += ef[0].elapsed_time(ef[1])
+        tb += eb[0].elapsed_time(eb[1])
+    tf /= reps
+    tb /= reps
     P_bbox = cnt[2]
-    N = g.num_vertices
-    # algorithmic work per launch
     fwd_flop = 8 * P_pop + 120 * P_bbox + 19 * B
-    bwd_flop = fwd_flop + 300 * B
-    kern = {
-        "prefilter": {"ms": ms["prefilter"], "bytes": 8 * N + 4 * K_a, "bound": "hbm"},
-        "build_scene": {"ms": ms["build_scene"], "bytes": 32 * N + 4 * K_a + 336 * K_v, "bound": "hbm"},
-        "bin_and_sort": {"ms": ms["bin_and_sort"], "bytes": 40 * K_v + 24 * M + 16 * M, "bound": "hbm"},
-        "render_forward": {"ms": ms["render_forward"], "flop": fwd_flop, "bound": "fp32"},
-        "render_backward": {"ms": ms["render_backward"], "flop": bwd_flop, "bound": "fp32"},
-        "eikonal": {"ms": ms["eikonal"], "bytes": 32 * N + 4 * K_a + 64 * K_a, "bound": "hbm"},
-        "normal_consistency": {"ms": ms["normal_consistency"], "bytes": 32 * N * 3 + 16 * N, "bound": "hbm"},
-    }
-    for k, d in kern.items():
-        if d["bound"] == "hbm":
-            d["achieved_GBs"] = d["bytes"] / (d["ms"] * 1e-3) / 1e9
-            d["frac_of_hbm"] = d["achieved_GBs"] / hbm
-        else:
-            d["achieved_TFLOPs"] = d["flop"] / (d["ms"] * 1e-3) / 1e12
-            d["frac_of_fp32"] = d["achieved_TFLOPs"] / fp32_peak
+    bwd_flop = 300 * B + 300 * K_v
+    kern = {"render_forward": {"ms": tf, "flop": fwd_flop}, "render_backward": {"ms": tb, "flop": bwd_flop}}
+    for d in kern.values():
+        d["achieved_TFLOPs"] = d["flop"] / (d["ms"] * 1e-3) / 1e12
+        d["frac_of_fp32"] = d["achieved_TFLOPs"] / fp32_peak
     top = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[top]
-    if d["bound"] == "hbm":
-        roof = {"kernel": top, "bound": "hbm", "achieved": d["achieved_GBs"], "peak": hbm, "unit": "GB/s",
-                "frac": d["frac_of_hbm"], "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    else:
-        roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_TFLOPs"], "peak": fp32_peak,
-                "unit": "TFLOP/s", "frac": d["frac_of_fp32"], "traffic": None,
-                "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no tensor cores: not a "
-                               f"dense contraction)"}
-    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M,
-             "fp64_fallbacks_edge": cnt[0], "fp64_fallbacks_alpha": cnt[1]}
-    return roof, {"per_view_ms": {k: round(v["ms"], 4) for k, v in kern.items()}, "detail": kern, "counts": extra}
+    roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_TFLOPs"], "peak": fp32_peak,
+            "unit": "TFLOP/s", "frac": d["frac_of_fp32"], "traffic": None,
+            "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (FP32 issue; no tensor "
+                           f"cores: not a dense contraction)"}
+    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M, "pixel_pairs": P_pairs,
+             "fp64_redecisions_edge": cnt[0], "fp64_redecisions_alpha": cnt[1]}
+    return roof, {"compositing": kern, "counts": extra}
+
+
+def kernel_table(fn):
+    """Per-kernel device time of one step (CUPTI through torch.profiler), our kernels only,
+    plus HBM-roofline fractions for the stream kernels (algorithmic bytes in DESIGN.md §3)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    tab = {}
+    for ev in prof.events():
+        if ev.device_type is None or not str(ev.device_type).endswith("CUDA"):
+            continue
+        name = ev.name.split("(")[0].replace("void ", "")
+        if not name.startswith("ts::"):
+            continue
+        t = tab.setdefault(name, [0, 0.0])
+        t[0] += 1
+        t[1] += (ev.time_range.end - ev.time_range.start) / 1e3
+    return {k: {"launches": v[0], "ms_per_step": round(v[1], 4)} for k, v in sorted(tab.items(), key=lambda x: -x[1][1])}
 
 
 def cpu_baseline(args, world):

@@ -175,8 +175,9 @@ def bin_and_sort(scene: SplatScene, camera, tile_size: int = TILE_SIZE, stream=N
 
 
 def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT_WINDOW, t_stop: float = T_STOP,
-                   save_state: bool = False, stream=None):
-    """Tile-based forward pass (raster.py:149-177).  Returns (RenderMaps, SavedState | None)."""
+                   save_state: bool = False, stream=None, timing=None):
+    """Tile-based forward pass (raster.py:149-177).  Returns (RenderMaps, SavedState | None).
+    `timing` = (start, end) CUDA events recorded around the compositing kernel launch."""
     if n_w < 1:
         raise ValueError("resorting window must be >= 1")
     L = _native.lib()
@@ -203,12 +204,16 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
         pair_code = torch.empty((P, 2), dtype=torch.float32, device=dev)
         pair_sig = torch.empty((P, 2), dtype=torch.float32, device=dev)
         pair_faces = torch.empty(P, dtype=torch.uint8, device=dev)
+        if timing is not None:
+            timing[0].record(stream if stream is not None else torch.cuda.current_stream())
         _native.check(L.ts_render_forward(sc_abi, K, _native.ptr(scene.colors), b_abi, M, cam,
                                           float(scene.steepness), float(t_stop), _native.ptr(item_off),
                                           _native.ptr(pair_code), _native.ptr(pair_sig), _native.ptr(pair_faces),
                                           _native.ptr(maps.normal), _native.ptr(maps.depth),
                                           _native.ptr(maps.opacity), _native.ptr(maps.color),
                                           _native.ptr(n_proc), _native.ptr(n_blend), sp))
+        if timing is not None:
+            timing[1].record(stream if stream is not None else torch.cuda.current_stream())
     saved = SavedState(bins, n_w, t_stop, maps, n_proc, n_blend, item_off, pair_code, pair_sig,
                        pair_faces) if save_state else None
     return maps, saved
@@ -221,7 +226,7 @@ def _as_f32(t, dev):
 
 
 def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d_maps: RenderMaps,
-                    out: GradientBuffers | None = None, stream=None) -> GradientBuffers:
+                    out: GradientBuffers | None = None, stream=None, timing=None) -> GradientBuffers:
     """Exact reverse-mode pass: map gradients -> per-vertex SDF/deformation gradients
     (raster.py:206-306).  With `out`, gradients are accumulated into it (fused batch)."""
     dev = scene.mean_depth.device
@@ -242,6 +247,8 @@ def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d
                                  saved.maps.opacity.data_ptr(),
                                  saved.maps.color.data_ptr() if with_color else None)
     dmaps = (ctypes.c_void_p * 4)(dn.data_ptr(), dd.data_ptr(), do.data_ptr(), dc.data_ptr() if with_color else None)
+    if timing is not None:
+        timing[0].record(stream if stream is not None else torch.cuda.current_stream())
     _native.check(L.ts_render_backward(scene.abi(), K, _native.ptr(scene.colors), saved.bins.abi(),
                                        saved.bins.num_pairs, camera.abi(), _native.ptr(saved.item_off),
                                        _native.ptr(saved.pair_code), _native.ptr(saved.pair_sig),
@@ -251,4 +258,6 @@ def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d
                                        _native.ptr(saved.n_proc), _native.ptr(field.deformation), grid.resolution,
                                        _native.ptr(out.d_vert), _native.ptr(out.d_color) if with_color else None,
                                        _native.stream_ptr(stream)))
+    if timing is not None:
+        timing[1].record(stream if stream is not None else torch.cuda.current_stream())
     return out
