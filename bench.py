@@ -400,8 +400,18 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
         d["frac_of_fp32"] = d["achieved_TFLOPs"] / fp32_peak
     top = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[top]
+    # DRAM traffic per launch of the same kernel from the committed ncu --set full capture
+    traffic, tsrc = None, None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile))
+        key = {"render_forward": "void k_forward<0>", "render_backward": "void k_backward<0>"}[top]
+        if key in tj:
+            traffic = tj[key]["dram_bytes_per_launch"]
+            tsrc = f"profiles/{tj[key]['source']} ({key}, dram__bytes_read.sum + dram__bytes_write.sum)"
     roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_TFLOPs"], "peak": fp32_peak,
-            "unit": "TFLOP/s", "frac": d["frac_of_fp32"], "traffic": None,
+            "unit": "TFLOP/s", "frac": d["frac_of_fp32"], "traffic": traffic, "traffic_unit": "bytes/launch",
+            "traffic_source": tsrc,
             "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (FP32 issue; no tensor "
                            f"cores: not a dense contraction)"}
     extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M, "pixel_pairs": P_pairs,
