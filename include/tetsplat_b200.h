@@ -96,22 +96,28 @@ int ts_bin_sort(const double* bbox, const double* mean_depth, int64_t K, const t
 int ts_forward_prepare(const ts_scene* scene, int64_t K, const ts_bins* bins, int64_t M, const ts_camera* cam,
                        int32_t n_w, int64_t* item_off, int64_t* out_pairs, void* stream);
 
+/* Words of the pair blend-bit array for P pair records (one spare word for unaligned ORs). */
+#define TS_PAIR_BIT_WORDS(n_pairs) (((n_pairs) + 31) / 32 + 1)
+
 /* K6 render_forward, step 2 (forward_tiles _core.pyx:98-229).  colors f32[K,3] / color_map
- * may be NULL.  Pair records (saved state for the backward, sized out_pairs):
- * pair_code f32[P,2] (alpha, 1-alpha), pair_sig f32[P,2] (s sigmoid(-s f_prev),
- * s sigmoid(-s f_next)), pair_faces u8[P] (entry | exit << 2).  n_proc[H,W]: list entries
- * consumed per pixel; n_blend[H,W]: blended records per pixel (_core.pyx:227-228). */
+ * may be NULL.  Pair records (saved state for the backward; P = n_pairs = out_pairs of
+ * ts_forward_prepare): pair_bits u32[TS_PAIR_BIT_WORDS(P)] — bit g set when pair g blends
+ * (cleared here first) — and pair_rec f32[P,4] written for blending pairs only:
+ * (alpha, 1-alpha (negative: clipped at ALPHA_CLIP), s sigmoid(-s f_prev) with the entry
+ * face in its two low mantissa bits, s sigmoid(-s f_next) with the exit face likewise).
+ * n_proc[H,W]: list entries consumed per pixel; n_blend[H,W]: blended records per pixel
+ * (_core.pyx:227-228). */
 int ts_render_forward(const ts_scene* scene, int64_t K, const float* colors, const ts_bins* bins, int64_t M,
-                      const ts_camera* cam, double s, double t_stop, const int64_t* item_off, void* pair_code,
-                      void* pair_sig, uint8_t* pair_faces, float* normal_map, float* depth_map,
+                      const ts_camera* cam, double s, double t_stop, const int64_t* item_off, int64_t n_pairs,
+                      uint32_t* pair_bits, void* pair_rec, float* normal_map, float* depth_map,
                       float* opacity_map, float* color_map, int32_t* n_proc, int32_t* n_blend, void* stream);
 
 /* K7 render_backward (raster.py:206-306 + backward_tiles _core.pyx:344-471): accumulates
  * dL/d(sdf, deform) into d_vert f32[N,4] and dL/dcolor into d_color f32[6R^3,3] (nullable).
  * maps = forward outputs {normal, depth, opacity, color|NULL}; d_maps likewise. */
 int ts_render_backward(const ts_scene* scene, int64_t K, const float* colors, const ts_bins* bins, int64_t M,
-                       const ts_camera* cam, const int64_t* item_off, const void* pair_code, const void* pair_sig,
-                       const uint8_t* pair_faces, const float* const maps[4], const float* const d_maps[4],
+                       const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits,
+                       const void* pair_rec, const float* const maps[4], const float* const d_maps[4],
                        const int32_t* n_proc, const double* deform, int32_t resolution, float* d_vert,
                        float* d_color, void* stream);
 

@@ -57,8 +57,8 @@ def lib():
         "ts_bin_count": ([P, P, I64, pc, I32, P, P, PI64, PI64, P], ctypes.c_int),
         "ts_bin_sort": ([P, P, I64, pc, I32, pb, I64, I64, P], ctypes.c_int),
         "ts_forward_prepare": ([ps, I64, pb, I64, pc, I32, P, PI64, P], ctypes.c_int),
-        "ts_render_forward": ([ps, I64, P, pb, I64, pc, D, D, P, P, P, P, P, P, P, P, P, P, P], ctypes.c_int),
-        "ts_render_backward": ([ps, I64, P, pb, I64, pc, P, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, I32,
+        "ts_render_forward": ([ps, I64, P, pb, I64, pc, D, D, P, I64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
+        "ts_render_backward": ([ps, I64, P, pb, I64, pc, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, I32,
                                 P, P, P], ctypes.c_int),
         "ts_eikonal": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency": ([P, P, I32, D, P, P, P], ctypes.c_int),

@@ -191,29 +191,27 @@ int ts_forward_prepare(const ts_scene* sc, int64_t K, const ts_bins* b, int64_t 
 }
 
 int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
-                      const ts_camera* cam, double s, double t_stop, const int64_t* item_off, void* pair_code,
-                      void* pair_sig, uint8_t* pair_faces, float* nmap, float* dmap, float* omap, float* cmap,
+                      const ts_camera* cam, double s, double t_stop, const int64_t* item_off, int64_t n_pairs,
+                      uint32_t* pair_bits, void* pair_rec, float* nmap, float* dmap, float* omap, float* cmap,
                       int32_t* n_proc, int32_t* n_blend, void* stream) {
-  if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0 ||
-      (M > 0 && (!item_off || !pair_code || !pair_sig || !pair_faces)))
+  if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0 || n_pairs < 0 ||
+      (M > 0 && (!item_off || !pair_bits || (n_pairs > 0 && !pair_rec))))
     return fail(TS_EINVAL, "ts_render_forward: bad arguments");
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   keep_pool_warm();
   ts_impl_forward(tx, ty, bv_of(b), reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
-                  cam->height, s, (float)t_stop, item_off, reinterpret_cast<float2*>(pair_code),
-                  reinterpret_cast<float2*>(pair_sig), pair_faces, nmap, dmap, omap, cmap, n_proc, n_blend,
-                  ST(stream));
+                  cam->height, s, (float)t_stop, item_off, n_pairs, pair_bits, reinterpret_cast<float4*>(pair_rec),
+                  nmap, dmap, omap, cmap, n_proc, n_blend, ST(stream));
   return check_cuda("ts_render_forward");
 }
 
 int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
-                       const ts_camera* cam, const int64_t* item_off, const void* pair_code, const void* pair_sig,
-                       const uint8_t* pair_faces, const float* const maps[4], const float* const dmaps[4],
-                       const int32_t* n_proc, const double* deform, int32_t R, float* d_vert, float* d_color,
-                       void* stream) {
+                       const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits, const void* pair_rec,
+                       const float* const maps[4], const float* const dmaps[4], const int32_t* n_proc,
+                       const double* deform, int32_t R, float* d_vert, float* d_color, void* stream) {
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert || R < 1 || K < 0 || M < 0 ||
-      (M > 0 && (!item_off || !pair_code || !pair_sig || !pair_faces)))
+      (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_render_backward: bad arguments");
   for (int i = 0; i < 3; ++i)
     if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward: missing map");
@@ -223,9 +221,8 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
   const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
   ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, sc->f,
-                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), item_off,
-                   reinterpret_cast<const float2*>(pair_code), reinterpret_cast<const float2*>(pair_sig), pair_faces,
-                   m4, d4, n_proc, d_vert, d_color, ST(stream));
+                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), item_off, pair_bits,
+                   reinterpret_cast<const float4*>(pair_rec), m4, d4, n_proc, d_vert, d_color, ST(stream));
   return check_cuda("ts_render_backward");
 }
 

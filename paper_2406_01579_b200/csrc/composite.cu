@@ -35,6 +35,7 @@
 //    per list position.  k_chain gathers each splat's rows in a fixed order (deterministic,
 //    atomic-free), applies the normal and camera chains in FP64 and scatters to vertices
 //    with one red.global.add.v4.f32 per (splat, vertex).
+#include "../../include/tetsplat_b200.h"
 #include "internal.cuh"
 #include "scan.cuh"
 
@@ -324,6 +325,25 @@ __device__ __forceinline__ float2 encode(bool blended, const Blend& b) {
 }
 __device__ __forceinline__ bool code_blends(float a) { return __float_as_uint(a) != 0u; }
 
+// Pair records of the view (item space, written by the forward, read by the backward):
+//   pair_bits[g >> 5] bit (g & 31): pair g blends (cleared before the forward);
+//   pair_rec[g] = (alpha code, 1 - alpha code, s sigmoid(-s f_prev) | entry face,
+//                  s sigmoid(-s f_next) | exit face) for blending pairs only — the face ids
+//   ride in the two low mantissa bits (2^-22 relative, far below FP32 gradient noise).
+__device__ __forceinline__ float pack_face(float v, int f) {
+  return __uint_as_float((__float_as_uint(v) & ~3u) | (unsigned)f);
+}
+__device__ __forceinline__ int face_of(float v) { return (int)(__float_as_uint(v) & 3u); }
+__device__ __forceinline__ bool pair_bit(const uint32_t* __restrict__ bits, int64_t g) {
+  return (__ldg(bits + (g >> 5)) >> (g & 31)) & 1u;
+}
+// OR a warp's 32-pair ballot into the (unaligned) bit range starting at pair g
+__device__ __forceinline__ void set_bits(uint32_t* bits, int64_t g, unsigned m) {
+  const int sh = (int)(g & 31);
+  atomicOr(bits + (g >> 5), m << sh);
+  if (sh && (m >> (32 - sh))) atomicOr(bits + (g >> 5) + 1, m >> (32 - sh));
+}
+
 template <int NC>
 struct Accum {
   float o, d, n[3], c[3];
@@ -446,18 +466,14 @@ struct FwdSmem {
   RectTab R;
 };
 
-// record one decided pair: shared code + blend bit (forward phase B), global pair record (backward)
-__device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, bool bl, const Blend& b, int64_t ib0,
-                                         float2* __restrict__ pair_code, float2* __restrict__ pair_sig,
-                                         uint8_t* __restrict__ pair_faces) {
-  const float2 c = encode(bl, b);
-  pair_code[ib0 + it] = c;
-  if (bl) {
-    F.code[it] = c;
-    mask_set(&F.bmask[q], j);
-    pair_sig[ib0 + it] = make_float2(b.sp, b.sn);
-    pair_faces[ib0 + it] = (uint8_t)(b.fip | (b.fin << 2));
-  }
+// record one blending pair: shared code + blend bit (forward phase B), global pair record
+// (backward); the caller sets the pair's bit in pair_bits
+__device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, const Blend& b, int64_t ib0,
+                                         float4* __restrict__ pair_rec) {
+  const float2 c = encode(true, b);
+  F.code[it] = c;
+  mask_set(&F.bmask[q], j);
+  pair_rec[ib0 + it] = make_float4(c.x, c.y, pack_face(b.sp, b.fip), pack_face(b.sn, b.fin));
 }
 
 template <bool COLOR>
@@ -465,8 +481,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, const int64_t* __restrict__ item_off,
-    float2* __restrict__ pair_code, float2* __restrict__ pair_sig, uint8_t* __restrict__ pair_faces,
-    float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
+    uint32_t* __restrict__ pair_bits, float4* __restrict__ pair_rec, float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
     float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
@@ -502,20 +517,29 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     const int n = F.R.n, total = F.R.pre[n];
     const int64_t ib0 = F.R.ib0;
     // ---- A: pair-parallel hit + opacity (FP32, error-bounded) ------------------------------
-    for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
-      const int j = pair_splat(F.R, it);
-      int px_, py_;
-      pair_pixel(F.R, j, it, px_, py_);
-      const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
-      if ((F.skip[q >> 5] >> (q & 31)) & 1u) continue;
-      ++npairs;
-      const Staged& r = F.sh[j];
-      Blend b;
-      const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, b);
-      if (e == 2)
-        F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)it;
-      else
-        put_pair(F, it, j, q, e == 1, b, ib0, pair_code, pair_sig, pair_faces);
+    for (int it0 = threadIdx.x & ~31; it0 < total; it0 += TS_TILE_PX) {
+      const int it = it0 + (threadIdx.x & 31);
+      bool bl = false;
+      if (it < total) {
+        const int j = pair_splat(F.R, it);
+        int px_, py_;
+        pair_pixel(F.R, j, it, px_, py_);
+        const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
+        if (!((F.skip[q >> 5] >> (q & 31)) & 1u)) {
+          ++npairs;
+          const Staged& r = F.sh[j];
+          Blend b;
+          const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, b);
+          if (e == 2) {
+            F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)it;
+          } else if (e == 1) {
+            put_pair(F, it, j, q, b, ib0, pair_rec);
+            bl = true;
+          }
+        }
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, bl);
+      if ((threadIdx.x & 31) == 0 && bm) set_bits(pair_bits, ib0 + it0, bm);
     }
     __syncthreads();
     // ---- A': exact FP64 re-decisions, 8 pairs per warp, one face per lane ------------------
@@ -528,8 +552,10 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       pair_pixel(F.R, j, it, px_, py_);
       Blend b;
       const bool bl = exact_group(S64, act, F.sh[j].k, px_, py_, s64, b);
-      if (act && (threadIdx.x & 3) == 0)
-        put_pair(F, it, j, (py_ - ty0) * TS_TILE + (px_ - tx0), bl, b, ib0, pair_code, pair_sig, pair_faces);
+      if (act && bl && (threadIdx.x & 3) == 0) {
+        put_pair(F, it, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
+        atomicOr(pair_bits + ((ib0 + it) >> 5), 1u << ((ib0 + it) & 31));
+      }
     }
     __syncthreads();
     // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
@@ -705,8 +731,7 @@ struct BwdSmem {
 
 template <bool COLOR>
 __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty0,
-                                              const float2* __restrict__ pair_sig,
-                                              const uint8_t* __restrict__ pair_faces, int64_t ib0, int W,
+                                              const float4* __restrict__ pair_rec, int64_t ib0, int W,
                                               const float* __restrict__ d_normal, const float* __restrict__ d_depth,
                                               const float* __restrict__ d_color) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -734,11 +759,10 @@ __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty
       row[22] = __ldg(d_color + p * 3 + 2) * w;
     }
     if (G != 0.f) {
-      const float2 sg = pair_sig[ib0 + it];
-      const int faces = pair_faces[ib0 + it];
+      const float2 sg = __ldg(reinterpret_cast<const float2*>(pair_rec + ib0 + it) + 1);
       const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-      face_bwd(row, r, faces & 3, px, py, G * sg.x);
-      face_bwd(row, r, faces >> 2, px, py, -G * sg.y);
+      face_bwd(row, r, face_of(sg.x), px, py, G * sg.x);
+      face_bwd(row, r, face_of(sg.y), px, py, -G * sg.y);
     }
   }
   __syncwarp();
@@ -764,8 +788,8 @@ template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-    int tiles_x, int W, int H, const int64_t* __restrict__ item_off, const float2* __restrict__ pair_code,
-    const float2* __restrict__ pair_sig, const uint8_t* __restrict__ pair_faces, const float* __restrict__ normal_map,
+    int tiles_x, int W, int H, const int64_t* __restrict__ item_off, const uint32_t* __restrict__ pair_bits,
+    const float4* __restrict__ pair_rec, const float* __restrict__ normal_map,
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
@@ -812,11 +836,13 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     __syncthreads();
     const int n = S.R.n, total = S.R.pre[n];
     const int64_t ib0 = S.R.ib0;
-    // ---- load the chunk's pair codes (contiguous), per-pixel blend masks, clear rows --------
+    // ---- load the chunk's blend bits + blending pair codes, per-pixel masks, clear rows -----
     for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
-      const float2 c = pair_code[ib0 + it];
+      float2 c = make_float2(0.f, 0.f);
+      const bool bl = pair_bit(pair_bits, ib0 + it);
+      if (bl) c = __ldg(reinterpret_cast<const float2*>(pair_rec + ib0 + it));
       S.wg[it] = c;
-      if (code_blends(c.x)) {
+      if (bl) {
         const int j = pair_splat(S.R, it);
         int px_, py_;
         pair_pixel(S.R, j, it, px_, py_);
@@ -871,7 +897,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
           cnt += __popc(m);
           __syncwarp();
           if (cnt >= 32) {
-            process_items<COLOR>(S, 32, tx0, ty0, pair_sig, pair_faces, ib0, W, d_normal, d_depth, d_color);
+            process_items<COLOR>(S, 32, tx0, ty0, pair_rec, ib0, W, d_normal, d_depth, d_color);
             const int rest = cnt - 32;
             const int moved = lane < rest ? S.buf[warp][32 + lane] : 0;
             __syncwarp();
@@ -881,7 +907,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
           }
         }
       }
-      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_sig, pair_faces, ib0, W, d_normal, d_depth, d_color);
+      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_rec, ib0, W, d_normal, d_depth, d_color);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n; t += TS_TILE_PX) {
@@ -1031,9 +1057,10 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
 
 void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec* rec, const float* colors,
                      const Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
-                     float2* pair_code, float2* pair_sig, uint8_t* pair_faces, float* nmap, float* dmap, float* omap,
+                     int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
+  cudaMemsetAsync(pair_bits, 0, sizeof(uint32_t) * (size_t)TS_PAIR_BIT_WORDS(n_pairs), st);
   static bool attr = false;
   const int smem = (int)sizeof(FwdSmem);
   if (!attr) {
@@ -1043,18 +1070,18 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
   }
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
-                                                W, H, (float)s, s, t_stop, item_off, pair_code, pair_sig,
-                                                pair_faces, nmap, dmap, omap, cmap, n_proc, n_blend);
+                                                W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
+                                                nmap, dmap, omap, cmap, n_proc, n_blend);
   else
     k_forward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
-                                                 tiles_x, W, H, (float)s, s, t_stop, item_off, pair_code, pair_sig,
-                                                 pair_faces, nmap, dmap, omap, nullptr, n_proc, n_blend);
+                                                 tiles_x, W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
+                                                 nmap, dmap, omap, nullptr, n_proc, n_blend);
 }
 
 void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, int64_t K, const SplatRec* rec,
                       const float* colors, const double* fsc, const int32_t* vert_ids, const int32_t* tet_ids,
                       const double* deform, int R, const Camera& cam, const int64_t* item_off,
-                      const float2* pair_code, const float2* pair_sig, const uint8_t* pair_faces, const float* maps[4],
+                      const uint32_t* pair_bits, const float4* pair_rec, const float* maps[4],
                       const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st) {
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
@@ -1070,12 +1097,12 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
     k_backward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
-                                                 cam.width, cam.height, item_off, pair_code, pair_sig, pair_faces,
+                                                 cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                  maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
                                                  dmaps[3], n_proc, rows);
   else
     k_backward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
-                                                  cam.width, cam.height, item_off, pair_code, pair_sig, pair_faces,
+                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                   maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
                                                   nullptr, n_proc, rows);
   int blocks = (int)((K + 127) / 128);

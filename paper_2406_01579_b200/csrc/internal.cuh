@@ -61,13 +61,13 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b,
                                 cudaStream_t st);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
                      const ts::Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
-                     float2* pair_code, float2* pair_sig, uint8_t* pair_faces, float* nmap, float* dmap, float* omap,
+                     int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st);
 void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, int64_t K,
                       const ts::SplatRec* rec, const float* colors, const double* fsc, const int32_t* vert_ids,
                       const int32_t* tet_ids, const double* deform, int R, const ts::Camera& cam,
-                      const int64_t* item_off, const float2* pair_code, const float2* pair_sig,
-                      const uint8_t* pair_faces, const float* maps[4], const float* dmaps[4],
+                      const int64_t* item_off, const uint32_t* pair_bits, const float4* pair_rec,
+                      const float* maps[4], const float* dmaps[4],
                       const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st);
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
                      float* d_vert, double* loss, cudaStream_t st);

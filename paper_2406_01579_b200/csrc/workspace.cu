@@ -45,7 +45,7 @@ struct ts_workspace {
   // bins
   Buf starts, splat_off, items, pos_of, nonmono, witems, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
   // forward state
-  Buf item_off, pair_code, pair_sig, pair_faces, n_proc, n_blend;
+  Buf item_off, pair_bits, pair_rec, n_proc, n_blend;
   // view description of the last forward
   int64_t K = 0, M = 0, P = 0, maxL = 0;
   int tiles_x = 0, tiles_y = 0, R = 0;
@@ -87,8 +87,8 @@ void ts_workspace_destroy(ts_workspace* ws) {
   Buf* all[] = {&ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
                 &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
                 &ws->nonmono, &ws->witems, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
-                &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_code, &ws->pair_sig,
-                &ws->pair_faces, &ws->n_proc, &ws->n_blend};
+                &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
+                &ws->n_proc, &ws->n_blend};
   cudaDeviceSynchronize();
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
@@ -160,13 +160,12 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   if (!n_proc || !n_blend || !item_off) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   int64_t P = 0;
   if (K > 0 && M > 0) P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st);
-  float2* pc = ws->pair_code.get<float2>(P);
-  float2* psg = ws->pair_sig.get<float2>(P);
-  uint8_t* pf = ws->pair_faces.get<uint8_t>(P);
-  if (!pc || !psg || !pf) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(P));
+  float4* prec = ws->pair_rec.get<float4>(P);
+  if (!pbits || !prec) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0) {
     ts_impl_forward(tx, ty, bv, so.rec, colors, Scene64{so.proj, so.depths, so.f, so.bbox}, cam.width, cam.height, s,
-                    (float)t_stop, item_off, pc, psg, pf, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
+                    (float)t_stop, item_off, P, pbits, prec, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
                     st);
   } else {
     cudaMemsetAsync(nmap, 0, sizeof(float) * 3 * HW, st);
@@ -211,8 +210,8 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
                    ws->color ? reinterpret_cast<float*>(ws->colors.p) : nullptr,
                    reinterpret_cast<double*>(ws->f.p), reinterpret_cast<int32_t*>(ws->vert_ids.p),
                    reinterpret_cast<int32_t*>(ws->tet_ids.p), deform, ws->R, ws->cam,
-                   reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<float2*>(ws->pair_code.p),
-                   reinterpret_cast<float2*>(ws->pair_sig.p), reinterpret_cast<uint8_t*>(ws->pair_faces.p), m4, d4,
+                   reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<uint32_t*>(ws->pair_bits.p),
+                   reinterpret_cast<float4*>(ws->pair_rec.p), m4, d4,
                    reinterpret_cast<int32_t*>(ws->n_proc.p), d_vert, ws->color ? d_color : nullptr,
                    reinterpret_cast<cudaStream_t>(stream));
   cudaError_t e = cudaGetLastError();

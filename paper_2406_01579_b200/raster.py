@@ -138,9 +138,9 @@ class SavedState:
     n_proc: torch.Tensor   # (H,W) int32
     n_blend: torch.Tensor  # (H,W) int32 — the reference's per-pixel record counts
     item_off: torch.Tensor | None = None    # (M+1,) int64: first pair of each list position
-    pair_code: torch.Tensor | None = None   # (P,2) f32: alpha, 1-alpha (negative: clipped)
-    pair_sig: torch.Tensor | None = None    # (P,2) f32: s*sigmoid(-s f_prev), s*sigmoid(-s f_next)
-    pair_faces: torch.Tensor | None = None  # (P,) u8: entry | exit << 2
+    pair_bits: torch.Tensor | None = None   # (ceil(P/32)+1,) int32: blend bit per pair
+    pair_rec: torch.Tensor | None = None    # (P,4) f32 (blending pairs): alpha, 1-alpha (negative:
+    #   clipped), s*sigmoid(-s f_prev) | entry face, s*sigmoid(-s f_next) | exit face (low mantissa bits)
 
 
 def bin_and_sort(scene: SplatScene, camera, tile_size: int = TILE_SIZE, stream=None) -> TileBins:
@@ -189,7 +189,7 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
     n_blend = torch.empty((H, W), dtype=torch.int32, device=dev)
     K = len(scene)
     M = bins.num_pairs
-    item_off = pair_code = pair_sig = pair_faces = None
+    item_off = pair_bits = pair_rec = None
     if K == 0 or M == 0:
         for t in (maps.normal, maps.depth, maps.opacity, maps.color, n_proc, n_blend):
             if t is not None:
@@ -201,21 +201,20 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
         npairs = _native.i64()
         _native.check(L.ts_forward_prepare(sc_abi, K, b_abi, M, cam, int(n_w), _native.ptr(item_off), npairs, sp))
         P = max(npairs.value, 1)
-        pair_code = torch.empty((P, 2), dtype=torch.float32, device=dev)
-        pair_sig = torch.empty((P, 2), dtype=torch.float32, device=dev)
-        pair_faces = torch.empty(P, dtype=torch.uint8, device=dev)
+        pair_bits = torch.empty((P + 31) // 32 + 1, dtype=torch.int32, device=dev)
+        pair_rec = torch.empty((P, 4), dtype=torch.float32, device=dev)
         if timing is not None:
             timing[0].record(stream if stream is not None else torch.cuda.current_stream())
         _native.check(L.ts_render_forward(sc_abi, K, _native.ptr(scene.colors), b_abi, M, cam,
                                           float(scene.steepness), float(t_stop), _native.ptr(item_off),
-                                          _native.ptr(pair_code), _native.ptr(pair_sig), _native.ptr(pair_faces),
+                                          npairs.value, _native.ptr(pair_bits), _native.ptr(pair_rec),
                                           _native.ptr(maps.normal), _native.ptr(maps.depth),
                                           _native.ptr(maps.opacity), _native.ptr(maps.color),
                                           _native.ptr(n_proc), _native.ptr(n_blend), sp))
         if timing is not None:
             timing[1].record(stream if stream is not None else torch.cuda.current_stream())
-    saved = SavedState(bins, n_w, t_stop, maps, n_proc, n_blend, item_off, pair_code, pair_sig,
-                       pair_faces) if save_state else None
+    saved = SavedState(bins, n_w, t_stop, maps, n_proc, n_blend, item_off, pair_bits,
+                       pair_rec) if save_state else None
     return maps, saved
 
 
@@ -251,8 +250,7 @@ def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d
         timing[0].record(stream if stream is not None else torch.cuda.current_stream())
     _native.check(L.ts_render_backward(scene.abi(), K, _native.ptr(scene.colors), saved.bins.abi(),
                                        saved.bins.num_pairs, camera.abi(), _native.ptr(saved.item_off),
-                                       _native.ptr(saved.pair_code), _native.ptr(saved.pair_sig),
-                                       _native.ptr(saved.pair_faces),
+                                       _native.ptr(saved.pair_bits), _native.ptr(saved.pair_rec),
                                        ctypes.cast(maps, ctypes.POINTER(ctypes.c_void_p)),
                                        ctypes.cast(dmaps, ctypes.POINTER(ctypes.c_void_p)),
                                        _native.ptr(saved.n_proc), _native.ptr(field.deformation), grid.resolution,
