@@ -169,6 +169,11 @@ int ts_debug_set_flags(int flags);
  * (ns) and SM id of its last launch; copies the first n tiles.  [sync] */
 int ts_debug_tile_times(uint64_t* t2, uint32_t* sm, int n);
 
+/* Diagnostics: with flag bit 2 set, thread 0 of every compositing CTA sums clock64 cycles
+ * between the CTA barriers per phase: out16[0..3] forward stage / A / A' / B,
+ * out16[8..12] backward stage / load / B / C / row write (since the last reset).  [sync] */
+int ts_debug_phases(uint64_t* out16, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,7 @@ def lib():
         "ts_marching_tets": ([P, P, I32, P, P, ctypes.POINTER(ctypes.c_int64), P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
+        "ts_debug_phases": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_workspace_create": ([], P),
         "ts_workspace_destroy": ([P], None),
         "ts_view_forward": ([P, P, P, I32, pc, D, P, I64, I32, D, P, P, P, P, P, ctypes.POINTER(ctypes.c_int64), P],
@@ -112,4 +113,11 @@ def debug_counters(reset: bool = True):
     """(edge FP64 re-decisions, alpha FP64 re-decisions, forward rect-pass pairs, 0) since last reset."""
     out = (ctypes.c_uint64 * 4)()
     check(lib().ts_debug_counters(out, int(reset)))
+    return tuple(int(v) for v in out)
+
+
+def debug_phases(reset: bool = True):
+    """Per-phase barrier-to-barrier cycles of the compositing kernels (flag bit 2; see the header)."""
+    out = (ctypes.c_uint64 * 16)()
+    check(lib().ts_debug_phases(out, int(reset)))
     return tuple(int(v) for v in out)

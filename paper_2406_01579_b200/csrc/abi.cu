@@ -272,6 +272,14 @@ int ts_debug_tile_times(uint64_t* t2, uint32_t* sm, int n) {
   return check_cuda("ts_debug_tile_times");
 }
 
+int ts_debug_phases(uint64_t* out16, int reset) {
+  if (!out16) return fail(TS_EINVAL, "ts_debug_phases: null output");
+  unsigned long long c[16];
+  ts_impl_phases(c, reset);
+  for (int i = 0; i < 16; ++i) out16[i] = c[i];
+  return check_cuda("ts_debug_phases");
+}
+
 int ts_debug_set_flags(int flags) {
   ts_impl_debug_flags(flags);
   return check_cuda("ts_debug_set_flags");

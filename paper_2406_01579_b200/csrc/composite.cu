@@ -80,6 +80,16 @@ __device__ int g_ts_debug_flags;
 __device__ unsigned long long g_ts_tile_time[2 * 65536];
 __device__ unsigned int g_ts_tile_sm[65536];
 
+// diagnostics only (flag bit 2): clock64 cycles between the CTA barriers, thread 0 of every
+// CTA, summed per phase: [0,4) forward stage/A/A'/B, [8,13) backward stage/load/B/C/write
+__device__ unsigned long long g_ts_phase[16];
+#define TS_PHASE(k)                   \
+  if (ptime) {                        \
+    const long long t_ = clock64();   \
+    pacc[k] += t_ - plast;            \
+    plast = t_;                       \
+  }
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -93,10 +103,10 @@ __device__ __forceinline__ unsigned smid() {
 
 __device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
 
-__device__ __forceinline__ void stage(const SplatRec* __restrict__ recs, int k, Staged& s) {
-  const float4* p = reinterpret_cast<const float4*>(recs + k);
-  float4 q0 = __ldg(p + 0), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3), q4 = __ldg(p + 4),
-         q5 = __ldg(p + 5);
+// decode one record (prefetched into shared memory) into the chunk's staged form
+__device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
+  const float4* p = reinterpret_cast<const float4*>(&rec);
+  float4 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3], q4 = p[4], q5 = p[5];
   int rx = __float_as_int(q0.x), ry = __float_as_int(q0.y);
   s.rx0 = (int)(short)(rx & 0xffff);
   s.rx1 = rx >> 16;
@@ -387,19 +397,60 @@ struct RectTab {
   uint8_t jtab[kCap];  // splat of each pair
 };
 
-// Threads [0, kCh) only: stage up to kCh records from list position `base` (at most
-// `avail`) and cut the chunk so it holds at most kCap pairs.  The warps exchange their scan
-// totals through `wtot` behind a named barrier over the kCh staging threads.
-__device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, int base, int avail,
-                                            const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-                                            bool color, Staged* sh, float (*col)[3], RectTab& R, int tx0, int ty0,
+// Next-chunk prefetch (threads [0, kCh)): the list entries of the next chunk are copied
+// into shared memory with cp.async at the end of the current chunk's staging, their
+// records at the end of the chunk's first phase — both land while the chunk is composited,
+// so staging never waits on a dependent global load.  Each thread copies and later consumes
+// its own slot.
+struct Prefetch {
+  SplatRec raw[kCh];
+  int32_t idx[kCh];
+};
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// list entries [pos, pos + min(kCh, avail)) -> P.idx
+__device__ __forceinline__ void prefetch_idx(Prefetch& P, const int32_t* __restrict__ list, int pos, int avail) {
+  const int t = threadIdx.x;
+  if (t < min(kCh, avail)) cp_async4(&P.idx[t], list + pos + t);
+  cp_async_commit();
+}
+// records of the prefetched list entries -> P.raw
+__device__ __forceinline__ void prefetch_rec(Prefetch& P, const SplatRec* __restrict__ recs, int avail) {
+  const int t = threadIdx.x;
+  cp_async_wait_all();
+  if (t < min(kCh, avail)) {
+    const float4* src = reinterpret_cast<const float4*>(recs + P.idx[t]);
+    float4* dst = reinterpret_cast<float4*>(&P.raw[t]);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) cp_async16(dst + i, src + i);
+  }
+  cp_async_commit();
+}
+
+// Threads [0, kCh) only: stage up to kCh prefetched records from list position `base` (at
+// most `avail`), cut the chunk so it holds at most kCap pairs, and start the prefetch of the
+// next chunk's list entries.  The warps exchange their scan totals through `wtot` behind a
+// named barrier over the kCh staging threads.
+__device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, int base, int avail, Prefetch& P,
+                                            const float* __restrict__ colors, bool color, Staged* sh,
+                                            float (*col)[3], RectTab& R, int tx0, int ty0,
                                             const int64_t* __restrict__ item_off_tile) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int m = min(kCh, avail);
   int cnt = 0;
+  cp_async_wait_all();
   if (t < m) {
-    const int k = list[base + t];
-    stage(recs, k, sh[t]);
+    const int k = P.idx[t];
+    stage(P.raw[t], k, sh[t]);
     const Staged& r = sh[t];
     int x0, y0, nx;
     if (!tile_rect(r.rx0, r.rx1, r.ry0, r.ry1, tx0, ty0, x0, y0, nx, cnt)) {
@@ -437,6 +488,7 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
     R.n = n;
     R.ib0 = item_off_tile[base];
   }
+  prefetch_idx(P, list, base + n, avail - n);
 }
 
 
@@ -464,6 +516,7 @@ struct FwdSmem {
   uint16_t exq[kCap];  // pairs queued for the exact FP64 re-decision
   int nex;
   RectTab R;
+  Prefetch pf;
 };
 
 // record one blending pair: shared code + blend bit (forward phase B), global pair record
@@ -485,6 +538,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
+  const bool ptime = (g_ts_debug_flags & 4) && threadIdx.x == 0;
+  long long pacc[4] = {0, 0, 0, 0}, plast = ptime ? clock64() : 0;
   const int tile = blockIdx.x;
   const bool timing = (g_ts_debug_flags & 2) && tile < 65536;
   if (timing && threadIdx.x == 0) {
@@ -508,12 +563,17 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
   }
+  if (threadIdx.x < kCh) {
+    prefetch_idx(F.pf, list, 0, L);
+    prefetch_rec(F.pf, recs, L);
+  }
   for (int base = 0; base < L;) {
     if (threadIdx.x < kCh)
-      stage_chunk(list, base, L - base, recs, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
+      stage_chunk(list, base, L - base, F.pf, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
     F.bmask[pix] = 0ull;
     if (threadIdx.x == 0) F.nex = 0;
     __syncthreads();
+    TS_PHASE(0);
     const int n = F.R.n, total = F.R.pre[n];
     const int64_t ib0 = F.R.ib0;
     // ---- A: pair-parallel hit + opacity (FP32, error-bounded) ------------------------------
@@ -541,7 +601,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       const unsigned bm = __ballot_sync(0xffffffffu, bl);
       if ((threadIdx.x & 31) == 0 && bm) set_bits(pair_bits, ib0 + it0, bm);
     }
+    if (threadIdx.x < kCh) prefetch_rec(F.pf, recs, L - base - n);
     __syncthreads();
+    TS_PHASE(1);
     // ---- A': exact FP64 re-decisions, 8 pairs per warp, one face per lane ------------------
     for (int q0 = (threadIdx.x >> 5) * 8; q0 < F.nex; q0 += kWarps * 8) {
       const int qi = q0 + ((threadIdx.x & 31) >> 2);
@@ -558,6 +620,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       }
     }
     __syncthreads();
+    TS_PHASE(2);
     // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
     if (!done) {
       ChunkMask m = F.bmask[pix];
@@ -578,7 +641,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
     base += n;
-    if (__syncthreads_and(done)) break;
+    const bool all_done = __syncthreads_and(done);
+    TS_PHASE(3);
+    if (all_done) break;
   }
   if (inside) {
     const int64_t p = (int64_t)yi * W + xi;
@@ -598,6 +663,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   const unsigned wb = warp_sum(npairs);
   if ((threadIdx.x & 31) == 0 && wb) atomicAdd(&g_ts_counters[2], (unsigned long long)wb);
   if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
+  if (ptime)
+    for (int k = 0; k < 4; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
 }
 
 // N_w resorting window (_core.pyx:171-187) for tiles whose list is not mean-depth monotone.
@@ -723,9 +790,10 @@ struct BwdSmem {
   float acc[kCh][kGr];       // per-(tile, splat) gradient rows of the chunk
   float col[kCh][3];
   int buf[kWarps][64];       // per-warp compacted items (j << 16 | pair)
-  float rows[kWarps][32][kGr];
+  float rows[kWarps][32][kGr + 1];  // odd stride: conflict-free per-lane rows
   ChunkMask bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   RectTab R;
+  Prefetch pf;
   int maxproc;
 };
 
@@ -795,6 +863,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
+  const bool ptime = (g_ts_debug_flags & 4) && threadIdx.x == 0;
+  long long pacc[5] = {0, 0, 0, 0, 0}, plast = 0;
   const int tile = blockIdx.x;
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -829,11 +899,17 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   float T = 1.f;
   Accum<COLOR> P;
   P.zero();
+  if (ptime) plast = clock64();
+  if (threadIdx.x < kCh) {
+    prefetch_idx(S.pf, list, 0, maxproc);
+    prefetch_rec(S.pf, recs, maxproc);
+  }
   for (int base = 0; base < maxproc;) {
     if (threadIdx.x < kCh)
-      stage_chunk(list, base, maxproc - base, recs, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
+      stage_chunk(list, base, maxproc - base, S.pf, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
     S.bmask[pix] = 0ull;
     __syncthreads();
+    TS_PHASE(0);
     const int n = S.R.n, total = S.R.pre[n];
     const int64_t ib0 = S.R.ib0;
     // ---- load the chunk's blend bits + blending pair codes, per-pixel masks, clear rows -----
@@ -850,7 +926,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
       }
     }
     for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
+    if (threadIdx.x < kCh) prefetch_rec(S.pf, recs, maxproc - base - n);
     __syncthreads();
+    TS_PHASE(1);
     // ---- B: pixel-serial prefix walk over this pixel's blended splats -> (w, G) --------------
     const int lim = nproc - base;  // splats j >= lim lie past this pixel's early stop
     for (ChunkMask m = S.bmask[pix]; m;) {
@@ -882,6 +960,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
       T = __fmul_rn(T, om);
     }
     __syncthreads();
+    TS_PHASE(2);
     // ---- C: compacted blended items per warp, 32 at a time --------------------------------
     {
       const int per = (n + kWarps - 1) / kWarps;
@@ -908,17 +987,18 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         }
       }
       if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_rec, ib0, W, d_normal, d_depth, d_color);
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n; t += TS_TILE_PX) {
-      float4* dst = reinterpret_cast<float4*>(rows + (lo + base + t) * kGr);
-      const float4* src = reinterpret_cast<const float4*>(&S.acc[t][0]);
-#pragma unroll
-      for (int i = 0; i < kGr / 4; ++i) dst[i] = src[i];
+      // this warp's splats are complete: write their per-(tile, splat) rows
+      for (int i = lane; i < (j1 - j0) * (kGr / 4); i += 32) {
+        const int j = j0 + i / (kGr / 4), c = i % (kGr / 4);
+        reinterpret_cast<float4*>(rows + (lo + base + j) * kGr)[c] = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
+      }
     }
     base += n;
     __syncthreads();
+    TS_PHASE(3);
   }
+  if (ptime)
+    for (int k = 0; k < 5; ++k) atomicAdd(&g_ts_phase[8 + k], (unsigned long long)pacc[k]);
   // positions no pixel reached: zero rows so the gather sees every pair
   for (int64_t q = maxproc + threadIdx.x; q < L; q += TS_TILE_PX) {
     float4* dst = reinterpret_cast<float4*>(rows + (lo + q) * kGr);
@@ -1121,6 +1201,14 @@ void ts_impl_counters(unsigned long long out[4], int reset) {
   if (reset) {
     unsigned long long z[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbol(g_ts_counters, z, sizeof(z));
+  }
+}
+
+void ts_impl_phases(unsigned long long out[16], int reset) {
+  cudaMemcpyFromSymbol(out, g_ts_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_ts_phase, z, sizeof(z));
   }
 }
 

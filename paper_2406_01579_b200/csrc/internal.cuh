@@ -78,3 +78,4 @@ int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, in
                cudaStream_t st);
 void ts_impl_counters(unsigned long long out[4], int reset);
 void ts_impl_debug_flags(int flags);
+void ts_impl_phases(unsigned long long out[16], int reset);
