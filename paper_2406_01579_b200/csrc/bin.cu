@@ -99,17 +99,16 @@ __global__ void k_bin_scatter(int64_t K, const BinRec* __restrict__ br, const ui
 
 template <typename Ptr>
 __device__ __forceinline__ void bitonic_sort(Ptr s, int P, int nthreads) {
+  // every thread owns compare-exchange pairs (not elements): no idle half per stage
   for (int k = 2; k <= P; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < P; i += nthreads) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          uint64_t a = s[i], b = s[ixj];
-          bool asc = (i & k) == 0;
-          if ((a > b) == asc) {
-            s[i] = b;
-            s[ixj] = a;
-          }
+      for (int c = threadIdx.x; c < (P >> 1); c += nthreads) {
+        const int i = ((c & ~(j - 1)) << 1) | (c & (j - 1)), ixj = i | j;
+        const uint64_t a = s[i], b = s[ixj];
+        const bool asc = (i & k) == 0;
+        if ((a > b) == asc) {
+          s[i] = b;
+          s[ixj] = a;
         }
       }
       __syncthreads();
@@ -127,22 +126,14 @@ __device__ __forceinline__ void emit_sorted(uint64_t key, int64_t p, int tile, i
   pos_of[splat_off[k] + local] = (int32_t)p;
 }
 
-// one CTA per tile; handles tiles with lo_len < L <= cap in (dynamic) shared memory
+// sort one tile's list in (dynamic) shared memory and emit items / pos_of / nonmono
 template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t lo_len, int64_t cap,
-                                                            const int64_t* __restrict__ starts,
-                                                            const uint64_t* __restrict__ keys, int tiles_x,
-                                                            const BinRec* __restrict__ br,
-                                                            const int64_t* __restrict__ splat_off,
-                                                            const double* __restrict__ md,
-                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                            uint8_t* __restrict__ nonmono) {
-  extern __shared__ uint64_t s[];
-  __shared__ int bad;
-  const int t = blockIdx.x;
-  if (t >= T) return;
+__device__ __forceinline__ void sort_tile(uint64_t* s, int& bad, int t, const int64_t* __restrict__ starts,
+                                          const uint64_t* __restrict__ keys, int tiles_x,
+                                          const BinRec* __restrict__ br, const int64_t* __restrict__ splat_off,
+                                          const double* __restrict__ md, int32_t* __restrict__ items,
+                                          int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono) {
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
-  if (L <= lo_len || L > cap) return;
   int P = 1;
   while (P < L) P <<= 1;
   for (int i = threadIdx.x; i < P; i += THREADS) s[i] = i < L ? keys[lo + i] : ~0ull;
@@ -157,6 +148,52 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t lo_le
   if (mybad) bad = 1;
   __syncthreads();
   if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
+}
+
+// one CTA per tile; handles the tiles with 0 < L <= cap
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, const int64_t* __restrict__ starts,
+                                                            const uint64_t* __restrict__ keys, int tiles_x,
+                                                            const BinRec* __restrict__ br,
+                                                            const int64_t* __restrict__ splat_off,
+                                                            const double* __restrict__ md,
+                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
+                                                            uint8_t* __restrict__ nonmono) {
+  extern __shared__ uint64_t s[];
+  __shared__ int bad;
+  const int t = blockIdx.x;
+  if (t >= T) return;
+  const int64_t L = starts[t + 1] - starts[t];
+  if (L <= 0 || L > cap) return;
+  sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
+}
+
+// long tiles (lo_len < L <= cap), listed by k_long_tiles: persistent CTAs walk the list, so
+// the large shared-memory footprint is only paid where there is work
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_tile_sort_long(const int32_t* __restrict__ tlist,
+                                                            const int64_t* __restrict__ tcount,
+                                                            const int64_t* __restrict__ starts,
+                                                            const uint64_t* __restrict__ keys, int tiles_x,
+                                                            const BinRec* __restrict__ br,
+                                                            const int64_t* __restrict__ splat_off,
+                                                            const double* __restrict__ md,
+                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
+                                                            uint8_t* __restrict__ nonmono) {
+  extern __shared__ uint64_t s[];
+  __shared__ int bad;
+  const int64_t n = *tcount;
+  for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x)
+    sort_tile<THREADS>(s, bad, tlist[idx], starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
+}
+
+// tiles with lo_len < L <= cap -> tlist[0, *tcount)
+__global__ void k_long_tiles(int T, int64_t lo_len, int64_t cap, const int64_t* __restrict__ starts,
+                             int32_t* __restrict__ tlist, int64_t* __restrict__ tcount) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    const int64_t L = starts[t + 1] - starts[t];
+    if (L > lo_len && L <= cap) tlist[atomicAdd((unsigned long long*)tcount, 1ull)] = t;
+  }
 }
 
 // oversize tiles: bitonic over a padded copy in global scratch (offset 2*lo, size <= 2L)
@@ -181,13 +218,11 @@ __global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, co
   __syncthreads();
   for (int64_t k = 2; k <= P; k <<= 1)
     for (int64_t j = k >> 1; j > 0; j >>= 1) {
-      for (int64_t i = threadIdx.x; i < P; i += 1024) {
-        int64_t ixj = i ^ j;
-        if (ixj > i) {
-          uint64_t a = s[i], b = s[ixj];
-          bool asc = (i & k) == 0;
-          if ((a > b) == asc) { s[i] = b; s[ixj] = a; }
-        }
+      for (int64_t c = threadIdx.x; c < (P >> 1); c += 1024) {
+        const int64_t i = ((c & ~(j - 1)) << 1) | (c & (j - 1)), ixj = i | j;
+        const uint64_t a = s[i], b = s[ixj];
+        const bool asc = (i & k) == 0;
+        if ((a > b) == asc) { s[i] = b; s[ixj] = a; }
       }
       __threadfence_block();
       __syncthreads();
@@ -257,20 +292,24 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
     k_bin_scatter<<<blocks, 256, 0, st>>>(K, w.br, w.q, tiles_x, starts, w.tile_cnt, keys);
   }
   if (maxL >= 1) {
-    k_tile_sort_smem<256><<<T, 256, 2048 * sizeof(uint64_t), st>>>(T, 0, 2048, starts, keys, tiles_x, w.br,
-                                                                   splat_off, md, items, pos_of, nonmono);
+    k_tile_sort_smem<256><<<T, 256, 2048 * sizeof(uint64_t), st>>>(T, 2048, starts, keys, tiles_x, w.br, splat_off,
+                                                                   md, items, pos_of, nonmono);
     if (maxL > 2048) {
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(k_tile_sort_smem<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_tile_sort_long<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              16384 * (int)sizeof(uint64_t));
         attr = true;
       }
+      // the scatter cursor is free again: reuse it as the long-tile list
+      cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
+      k_long_tiles<<<(T + 255) / 256, 256, 0, st>>>(T, 2048, 16384, starts, w.tile_cnt, w.dev_i64);
       // shared memory sized to the longest list (not the 16384 cap) so several CTAs fit per SM
       int64_t P = 4096;
       while (P < maxL && P < 16384) P <<= 1;
-      k_tile_sort_smem<512><<<T, 512, P * sizeof(uint64_t), st>>>(T, 2048, 16384, starts, keys, tiles_x, w.br,
-                                                                  splat_off, md, items, pos_of, nonmono);
+      const int per_sm = P <= 8192 ? 2 : 1;  // 2048 threads / SM
+      k_tile_sort_long<1024><<<148 * per_sm, 1024, P * sizeof(uint64_t), st>>>(
+          w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br, splat_off, md, items, pos_of, nonmono);
     }
     if (maxL > 16384)
       k_tile_sort_global<<<T, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,

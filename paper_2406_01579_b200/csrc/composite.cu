@@ -72,7 +72,8 @@ struct __align__(16) Staged {
 static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 
 // diagnostics: [0] pairs re-decided in FP64 at a face edge / degenerate face,
-// [1] pairs re-decided in FP64 at an alpha threshold, [2] forward pairs evaluated
+// [1] pairs re-decided in FP64 at an alpha threshold ([3]: of those, tiny alpha), [2] forward
+// pairs evaluated
 __device__ unsigned long long g_ts_counters[4];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity)
 __device__ int g_ts_debug_flags;
@@ -83,11 +84,12 @@ __device__ unsigned int g_ts_tile_sm[65536];
 // diagnostics only (flag bit 2): clock64 cycles between the CTA barriers, thread 0 of every
 // CTA, summed per phase: [0,4) forward stage/A/A'/B, [8,13) backward stage/load/B/C/write
 __device__ unsigned long long g_ts_phase[16];
+// (accumulated in shared memory, slot 7 = last stamp, so the hot loop keeps its registers)
 #define TS_PHASE(k)                   \
   if (ptime) {                        \
     const long long t_ = clock64();   \
-    pacc[k] += t_ - plast;            \
-    plast = t_;                       \
+    pacc[k] += t_ - pacc[7];          \
+    pacc[7] = t_;                     \
   }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -237,6 +239,15 @@ __device__ __forceinline__ bool exact_face(const Scene64& S, int64_t k, int fi, 
   return true;
 }
 
+// pull a splat's FP64 scene rows into L1 when one of its pairs is queued for re-decision
+__device__ __forceinline__ void prefetch_exact(const Scene64& S, int64_t k) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.proj + k * 8));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.proj + k * 8 + 7));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.depths + k * 4));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.f + k * 4));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.bbox + k * 4));
+}
+
 // Warp-cooperative exact re-decision (the reference's decision chain, _core.pyx:67-95,
 // 35-36, 190-196, in FP64): 4 lanes per queued pair, one face each; the group leader
 // combines the faces in face order (first hit seeds, strict < / > updates) and decides
@@ -269,13 +280,18 @@ __device__ __forceinline__ bool exact_group(const Scene64& S, bool act, int64_t 
     }
     ++n;
   }
-  if (!act || fi != 0 || n < 2) return false;
-  const double d = dsub(softplus_d(dmul(-s, flo)), softplus_d(dmul(-s, fhi)));
-  const double a = dsub(1.0, exp(d));
+  // the two softplus terms on lanes 1 and 2 of the group, concurrently
+  const bool ok = act && n >= 2;
+  double spv = 0.0;
+  if (ok && (fi == 1 || fi == 2)) spv = softplus_d(dmul(-s, fi == 1 ? flo : fhi));
+  const double spx = __shfl_sync(0xffffffffu, spv, lead + 1), spy = __shfl_sync(0xffffffffu, spv, lead + 2);
+  if (!ok || fi != 0) return false;
+  const double ed = exp(dsub(spx, spy));
+  const double a = dsub(1.0, ed);
   if (a <= 0.0) return false;
   const float sf = (float)s;
   b.a = (float)a;
-  b.om = (float)exp(d);
+  b.om = (float)ed;
   b.sp = sf * sigmoidf_stable(-sf * (float)flo);
   b.sn = sf * sigmoidf_stable(-sf * (float)fhi);
   b.fip = lo;
@@ -318,6 +334,7 @@ __device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, f
         b.clipped = a_un > kAlphaClipF;
         return 1;
       }
+      if (!(a_un > 1e-10f)) atomicAdd(&g_ts_counters[3], 1ull);
     }
     atomicAdd(&g_ts_counters[1], 1ull);
   } else {
@@ -515,8 +532,10 @@ struct FwdSmem {
   uint32_t skip[TS_TILE_PX / 32];
   uint16_t exq[kCap];  // pairs queued for the exact FP64 re-decision
   int nex;
+  unsigned npairs;  // diagnostics: pairs evaluated by phase A
   RectTab R;
   Prefetch pf;
+  long long phase[8];  // diagnostics (flag bit 2)
 };
 
 // record one blending pair: shared code + blend bit (forward phase B), global pair record
@@ -538,8 +557,13 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
+  if (threadIdx.x == 0) F.npairs = 0;
   const bool ptime = (g_ts_debug_flags & 4) && threadIdx.x == 0;
-  long long pacc[4] = {0, 0, 0, 0}, plast = ptime ? clock64() : 0;
+  long long* pacc = F.phase;
+  if (ptime) {
+    for (int k = 0; k < 7; ++k) pacc[k] = 0;
+    pacc[7] = clock64();
+  }
   const int tile = blockIdx.x;
   const bool timing = (g_ts_debug_flags & 2) && tile < 65536;
   if (timing && threadIdx.x == 0) {
@@ -556,7 +580,6 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   float T = 1.f;
   Accum<COLOR> acc;
   acc.zero();
-  unsigned npairs = 0;
   bool done = !inside;
   int nproc = inside ? L : 0, nb = 0;
   {
@@ -579,27 +602,31 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     // ---- A: pair-parallel hit + opacity (FP32, error-bounded) ------------------------------
     for (int it0 = threadIdx.x & ~31; it0 < total; it0 += TS_TILE_PX) {
       const int it = it0 + (threadIdx.x & 31);
-      bool bl = false;
+      bool bl = false, ev = false;
       if (it < total) {
         const int j = pair_splat(F.R, it);
         int px_, py_;
         pair_pixel(F.R, j, it, px_, py_);
         const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
         if (!((F.skip[q >> 5] >> (q & 31)) & 1u)) {
-          ++npairs;
+          ev = true;
           const Staged& r = F.sh[j];
           Blend b;
           const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, b);
           if (e == 2) {
             F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)it;
+            prefetch_exact(S64, r.k);
           } else if (e == 1) {
             put_pair(F, it, j, q, b, ib0, pair_rec);
             bl = true;
           }
         }
       }
-      const unsigned bm = __ballot_sync(0xffffffffu, bl);
-      if ((threadIdx.x & 31) == 0 && bm) set_bits(pair_bits, ib0 + it0, bm);
+      const unsigned bm = __ballot_sync(0xffffffffu, bl), em = __ballot_sync(0xffffffffu, ev);
+      if ((threadIdx.x & 31) == 0) {
+        if (bm) set_bits(pair_bits, ib0 + it0, bm);
+        atomicAdd(&F.npairs, __popc(em));
+      }
     }
     if (threadIdx.x < kCh) prefetch_rec(F.pf, recs, L - base - n);
     __syncthreads();
@@ -660,8 +687,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     n_proc[p] = nproc;
     n_blend[p] = nb;
   }
-  const unsigned wb = warp_sum(npairs);
-  if ((threadIdx.x & 31) == 0 && wb) atomicAdd(&g_ts_counters[2], (unsigned long long)wb);
+  if (threadIdx.x == 0) atomicAdd(&g_ts_counters[2], (unsigned long long)F.npairs);
   if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
   if (ptime)
     for (int k = 0; k < 4; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
@@ -794,6 +820,7 @@ struct BwdSmem {
   ChunkMask bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   RectTab R;
   Prefetch pf;
+  long long phase[8];  // diagnostics (flag bit 2)
   int maxproc;
 };
 
@@ -864,7 +891,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
   const bool ptime = (g_ts_debug_flags & 4) && threadIdx.x == 0;
-  long long pacc[5] = {0, 0, 0, 0, 0}, plast = 0;
+  long long* pacc = S.phase;
+  if (ptime)
+    for (int k = 0; k < 7; ++k) pacc[k] = 0;
   const int tile = blockIdx.x;
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -899,7 +928,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   float T = 1.f;
   Accum<COLOR> P;
   P.zero();
-  if (ptime) plast = clock64();
+  if (ptime) pacc[7] = clock64();
   if (threadIdx.x < kCh) {
     prefetch_idx(S.pf, list, 0, maxproc);
     prefetch_rec(S.pf, recs, maxproc);
