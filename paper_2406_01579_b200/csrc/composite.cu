@@ -810,30 +810,49 @@ __device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, fl
   row[12 + ic] -= qy * v;
 }
 
+template <bool COLOR>
 struct BwdSmem {
+  static constexpr int NC = COLOR ? 23 : 20;  // gradient components per item / (tile, splat) row
+  static constexpr int RS = COLOR ? 25 : 21;  // odd item-row stride: conflict-free per-lane rows
+  static constexpr int AS = COLOR ? 24 : 20;  // accumulator row stride (whole float4s)
   Staged sh[kCh];
-  float2 wg[kCap];           // load: (alpha, 1-alpha); phase B: (w = T a, G)
-  float acc[kCh][kGr];       // per-(tile, splat) gradient rows of the chunk
+  float2 wg[kCap];      // load: (alpha, 1-alpha); phase B: (w = T a, G); +0 bits = not an item
+  float acc[kCh][AS];   // per-(tile, splat) gradient rows of the chunk
   float col[kCh][3];
-  int buf[kWarps][64];       // per-warp compacted items (j << 16 | pair)
-  float rows[kWarps][32][kGr + 1];  // odd stride: conflict-free per-lane rows
-  ChunkMask bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
+  union {
+    ChunkMask bmask[TS_TILE_PX];  // load + B: per pixel, chunk splats that blend (bit j)
+    float rows[kWarps][32][RS];   // C: per-item rows of each warp's batch
+  } u;
+  uint32_t items[kCap];  // C: the chunk's items (j << 16 | pair) in pair order
+  int wcnt[kCap / 32];   // items per 32-pair block -> exclusive offsets
+  int lim[TS_TILE_PX];   // per pixel: list entries the forward consumed (n_proc)
   RectTab R;
   Prefetch pf;
   long long phase[8];  // diagnostics (flag bit 2)
-  int maxproc;
+  int maxproc, nitems;
 };
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// One warp, items [b0, b0 + m) of the chunk: face-hit backward of every item into its row,
+// then per run of equal splat (items are in pair order, i.e. grouped by splat) one lane per
+// component sums the run and adds it to the splat's row (shared atomics: a run may continue
+// in the neighbouring batch of another warp).
 template <bool COLOR>
-__device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty0,
-                                              const float4* __restrict__ pair_rec, int64_t ib0, int W,
-                                              const float* __restrict__ d_normal, const float* __restrict__ d_depth,
+__device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, const float4* __restrict__ pair_rec,
+                                              int64_t ib0, int W, const float* __restrict__ d_normal,
+                                              const float* __restrict__ d_depth,
                                               const float* __restrict__ d_color) {
+  using SM = BwdSmem<COLOR>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* row = S.rows[warp][lane];
+  float* row = S.u.rows[warp][lane];
+  const int item = lane < m ? (int)S.items[b0 + lane] : -1;
+  const int jl = item >> 16;
   if (lane < m) {
-    const int item = S.buf[warp][lane];
-    const int j = item >> 16, it = item & 0xffff;
+    const int j = jl, it = item & 0xffff;
     const Staged& r = S.sh[j];
     const int local = it - S.R.pre[j];
     const int nx = S.R.nx[j];
@@ -860,21 +879,19 @@ __device__ __forceinline__ void process_items(BwdSmem& S, int m, int tx0, int ty
       face_bwd(row, r, face_of(sg.y), px, py, -G * sg.y);
     }
   }
+  const int jprev = __shfl_up_sync(0xffffffffu, jl, 1);
+  unsigned heads = __ballot_sync(0xffffffffu, lane < m && (lane == 0 || jl != jprev));
   __syncwarp();
-  // segmented sum of the item rows into the per-splat rows (items sorted by splat)
-  if (lane < (COLOR ? 23 : 20)) {
-    int cur = -1;
-    float sum = 0.f;
-    for (int i = 0; i < m; ++i) {
-      const int jj = S.buf[warp][i] >> 16;
-      if (jj != cur) {
-        if (cur >= 0) S.acc[cur][lane] += sum;
-        cur = jj;
-        sum = 0.f;
-      }
-      sum += S.rows[warp][i][lane];
+  while (heads) {
+    const int s0 = __ffs(heads) - 1;
+    heads &= heads - 1u;
+    const int e0 = heads ? __ffs(heads) - 1 : m;
+    const int jj = __shfl_sync(0xffffffffu, jl, s0);
+    if (lane < SM::NC) {
+      float sum = 0.f;
+      for (int i = s0; i < e0; ++i) sum += S.u.rows[warp][i][lane];
+      atomicAdd(&S.acc[jj][lane], sum);
     }
-    if (cur >= 0) S.acc[cur][lane] += sum;
   }
   __syncwarp();
 }
@@ -888,8 +905,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
+  using SM = BwdSmem<COLOR>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  BwdSmem& S = *reinterpret_cast<BwdSmem*>(smem_raw);
+  SM& S = *reinterpret_cast<SM*>(smem_raw);
   const bool ptime = (g_ts_debug_flags & 4) && threadIdx.x == 0;
   long long* pacc = S.phase;
   if (ptime)
@@ -905,6 +923,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   const int64_t p = inside ? (int64_t)yi * W + xi : 0;
   const int nproc = inside ? n_proc[p] : 0;
   if (threadIdx.x == 0) S.maxproc = 0;
+  S.lim[pix] = nproc;
   __syncthreads();
   if (nproc > 0) atomicMax(&S.maxproc, nproc);
   float g_o = 0.f, g_d = 0.f, g_n[3] = {0.f, 0.f, 0.f}, g_c[3] = {0.f, 0.f, 0.f};
@@ -936,38 +955,67 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   for (int base = 0; base < maxproc;) {
     if (threadIdx.x < kCh)
       stage_chunk(list, base, maxproc - base, S.pf, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
-    S.bmask[pix] = 0ull;
+    S.u.bmask[pix] = 0ull;
     __syncthreads();
     TS_PHASE(0);
     const int n = S.R.n, total = S.R.pre[n];
+    const int nblk = (total + TS_TILE_PX - 1) / TS_TILE_PX;  // <= kCap / 256
     const int64_t ib0 = S.R.ib0;
-    // ---- load the chunk's blend bits + blending pair codes, per-pixel masks, clear rows -----
-    for (int it = threadIdx.x; it < total; it += TS_TILE_PX) {
-      float2 c = make_float2(0.f, 0.f);
-      const bool bl = pair_bit(pair_bits, ib0 + it);
-      if (bl) c = __ldg(reinterpret_cast<const float2*>(pair_rec + ib0 + it));
-      S.wg[it] = c;
-      if (bl) {
-        const int j = pair_splat(S.R, it);
-        int px_, py_;
-        pair_pixel(S.R, j, it, px_, py_);
-        mask_set(&S.bmask[(py_ - ty0) * TS_TILE + (px_ - tx0)], j);
+    // ---- load: blend bits (all words first), then the blending, not early-stopped pairs'
+    //      codes by cp.async; per-pixel masks; per-32-pair item counts -------------------------
+    {
+      uint32_t wv[kCap / TS_TILE_PX];
+#pragma unroll
+      for (int k = 0; k < kCap / TS_TILE_PX; ++k) {
+        const int it = threadIdx.x + k * TS_TILE_PX;
+        wv[k] = (k < nblk && it < total) ? __ldg(pair_bits + ((ib0 + it) >> 5)) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kCap / TS_TILE_PX; ++k) {
+        if (k < nblk) {
+          const int it = threadIdx.x + k * TS_TILE_PX;
+          bool bl = false;
+          if (it < total && ((wv[k] >> ((ib0 + it) & 31)) & 1u)) {
+            const int j = pair_splat(S.R, it);
+            int px_, py_;
+            pair_pixel(S.R, j, it, px_, py_);
+            const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
+            if (base + j < S.lim[q]) {  // past the pixel's early stop: not composited
+              cp_async8(&S.wg[it], pair_rec + ib0 + it);
+              mask_set(&S.u.bmask[q], j);
+              bl = true;
+            }
+          }
+          if (!bl && it < total) S.wg[it] = make_float2(0.f, 0.f);
+          const unsigned bm = __ballot_sync(0xffffffffu, bl);
+          if (lane == 0) S.wcnt[k * kWarps + warp] = __popc(bm);
+        }
       }
     }
-    for (int i = threadIdx.x; i < n * kGr; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
+    for (int i = threadIdx.x; i < n * SM::AS; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
+    cp_async_wait_all();
     if (threadIdx.x < kCh) prefetch_rec(S.pf, recs, maxproc - base - n);
     __syncthreads();
     TS_PHASE(1);
     // ---- B: pixel-serial prefix walk over this pixel's blended splats -> (w, G) --------------
-    const int lim = nproc - base;  // splats j >= lim lie past this pixel's early stop
-    for (ChunkMask m = S.bmask[pix]; m;) {
+    //      (warp 0 first turns the item counts into offsets)
+    if (warp == 0) {
+      const int nb = nblk * kWarps;  // <= 64 blocks, two per lane
+      const int c0 = 2 * lane < nb ? S.wcnt[2 * lane] : 0, c1 = 2 * lane + 1 < nb ? S.wcnt[2 * lane + 1] : 0;
+      int v = c0 + c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (2 * lane < nb) S.wcnt[2 * lane] = v - c0 - c1;
+      if (2 * lane + 1 < nb) S.wcnt[2 * lane + 1] = v - c1;
+      if (lane == 31) S.nitems = v;
+    }
+    for (ChunkMask m = S.u.bmask[pix]; m;) {
       const int j = __ffsll(m) - 1;
       m &= m - 1ull;
       const int it = pair_index(S.R, j, xi, yi);
-      if (j >= lim) {  // code may be stale (pixel skipped by the forward): no contribution
-        S.wg[it] = make_float2(0.f, 0.f);
-        continue;
-      }
       const float2 c = S.wg[it];
       const float a = c.x, om = fabsf(c.y);
       const bool cl = c.y < 0.f;
@@ -990,41 +1038,31 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     }
     __syncthreads();
     TS_PHASE(2);
-    // ---- C: compacted blended items per warp, 32 at a time --------------------------------
-    {
-      const int per = (n + kWarps - 1) / kWarps;
-      const int j0 = warp * per, j1 = min(n, j0 + per);
-      int cnt = 0;
-      for (int j = j0; j < j1; ++j) {
-        const int b0 = S.R.pre[j], b1 = S.R.pre[j + 1];
-        for (int it0 = b0; it0 < b1; it0 += 32) {
-          const int it = it0 + lane;
-          const bool has = it < b1 && code_blends(S.wg[it].x);
-          const unsigned m = __ballot_sync(0xffffffffu, has);
-          if (has) S.buf[warp][cnt + __popc(m & ((1u << lane) - 1u))] = (j << 16) | it;
-          cnt += __popc(m);
-          __syncwarp();
-          if (cnt >= 32) {
-            process_items<COLOR>(S, 32, tx0, ty0, pair_rec, ib0, W, d_normal, d_depth, d_color);
-            const int rest = cnt - 32;
-            const int moved = lane < rest ? S.buf[warp][32 + lane] : 0;
-            __syncwarp();
-            if (lane < rest) S.buf[warp][lane] = moved;
-            cnt = rest;
-            __syncwarp();
-          }
-        }
-      }
-      if (cnt > 0) process_items<COLOR>(S, cnt, tx0, ty0, pair_rec, ib0, W, d_normal, d_depth, d_color);
-      // this warp's splats are complete: write their per-(tile, splat) rows
-      for (int i = lane; i < (j1 - j0) * (kGr / 4); i += 32) {
-        const int j = j0 + i / (kGr / 4), c = i % (kGr / 4);
-        reinterpret_cast<float4*>(rows + (lo + base + j) * kGr)[c] = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
+    // ---- C: the chunk's items in pair order, 32 per warp-batch, batches round-robin ---------
+#pragma unroll
+    for (int k = 0; k < kCap / TS_TILE_PX; ++k) {
+      if (k < nblk) {
+        const int it = threadIdx.x + k * TS_TILE_PX;
+        const bool has = it < total && code_blends(S.wg[it].x);
+        const unsigned bm = __ballot_sync(0xffffffffu, has);
+        if (has)
+          S.items[S.wcnt[k * kWarps + warp] + __popc(bm & ((1u << lane) - 1u))] =
+              ((uint32_t)pair_splat(S.R, it) << 16) | (uint32_t)it;
       }
     }
-    base += n;
+    __syncthreads();
+    const int nitems = S.nitems;
+    for (int b0 = warp * 32; b0 < nitems; b0 += TS_TILE_PX)
+      process_batch<COLOR>(S, b0, min(32, nitems - b0), pair_rec, ib0, W, d_normal, d_depth, d_color);
     __syncthreads();
     TS_PHASE(3);
+    // ---- the chunk's per-(tile, splat) rows -------------------------------------------------
+    for (int i = threadIdx.x; i < n * (SM::AS / 4); i += TS_TILE_PX) {
+      const int j = i / (SM::AS / 4), c = i % (SM::AS / 4);
+      reinterpret_cast<float4*>(rows + (lo + base + j) * kGr)[c] = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
+    }
+    base += n;
+    TS_PHASE(4);
   }
   if (ptime)
     for (int k = 0; k < 5; ++k) atomicAdd(&g_ts_phase[8 + k], (unsigned long long)pacc[k]);
@@ -1195,9 +1233,9 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
   static bool attr = false;
-  const int smem = (int)sizeof(BwdSmem);
+  const int smem_c = (int)sizeof(BwdSmem<true>), smem = (int)sizeof(BwdSmem<false>);
   if (!attr) {
-    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
     cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
@@ -1205,7 +1243,7 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   cudaMallocAsync(&rows, sizeof(float) * kGr * (size_t)M, st);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
-    k_backward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
+    k_backward<true><<<T, TS_TILE_PX, smem_c, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                  maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
                                                  dmaps[3], n_proc, rows);
