@@ -10,7 +10,8 @@ normal consistency (lambda 1000 each) + NCCL all-reduce of the vertex gradients 
 
 Prints ONE JSON line (rank 0).  `value` = views/s with inputs resident in HBM; `e2e` = the
 same through the public API with host inputs copied in (pinned H2D of the field and the
-map gradients, D2H of the gradients) inside the timed region.  `--impl reference` times the
+map gradients — the latter on a copy stream overlapping the compute of earlier views — and
+D2H of the gradients) inside the timed region.  `--impl reference` times the
 reference's CPU implementation (oracle/: the reference's own Cython kernels built from
 /root/reference into oracle/_ref when present, else the plain-C restatement) on the host.
 """
@@ -299,14 +300,28 @@ def run_gpu(args):
     h2d = h_sdf.numel() * 8 + h_def.numel() * 8 + sum(sum(t.numel() * 4 for t in v) for v in h_maps.values())
     d2h = h_grad.numel() * 4
 
+    # The field is copied on the compute stream (the first kernel needs it); the per-view map
+    # gradients stream in on a copy stream, one event per view, so view i's copy overlaps the
+    # compute of the views before it.  The copy stream first waits for the previous step's
+    # consumers of the buffers it overwrites.
+    copy_stream = torch.cuda.Stream(device=dev)
+    view_ready = {vi: torch.cuda.Event() for vi in views}
+
+    def maps_for(vi, m):
+        torch.cuda.current_stream().wait_event(view_ready[vi])
+        return d_maps[vi]
+
     def e2e_step():
         field.sdf.copy_(h_sdf, non_blocking=True)
         field.deformation.copy_(h_def, non_blocking=True)
-        for vi in views:
-            d_maps[vi].normal.copy_(h_maps[vi][0], non_blocking=True)
-            d_maps[vi].depth.copy_(h_maps[vi][1], non_blocking=True)
-            d_maps[vi].opacity.copy_(h_maps[vi][2], non_blocking=True)
-        grads = step(s, views, lambda vi, m: d_maps[vi])
+        copy_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(copy_stream):
+            for vi in views:
+                d_maps[vi].normal.copy_(h_maps[vi][0], non_blocking=True)
+                d_maps[vi].depth.copy_(h_maps[vi][1], non_blocking=True)
+                d_maps[vi].opacity.copy_(h_maps[vi][2], non_blocking=True)
+                view_ready[vi].record(copy_stream)
+        grads = step(s, views, maps_for)
         h_grad.copy_(grads.d_vert, non_blocking=True)
 
     e2e_step()

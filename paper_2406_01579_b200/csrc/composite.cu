@@ -72,8 +72,8 @@ struct __align__(16) Staged {
 static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 
 // diagnostics: [0] pairs re-decided in FP64 at a face edge / degenerate face,
-// [1] pairs re-decided in FP64 at an alpha threshold ([3]: of those, tiny alpha), [2] forward
-// pairs evaluated
+// [1] pairs re-decided in FP64 at an alpha threshold, [2] forward pairs evaluated, [3] of [0],
+// pairs of splats with a sign-uncertain FP32 face determinant
 __device__ unsigned long long g_ts_counters[4];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity)
 __device__ int g_ts_debug_flags;
@@ -103,7 +103,12 @@ __device__ __forceinline__ unsigned smid() {
   return r;
 }
 
-__device__ __forceinline__ float frcp(float x) { return __fdividef(1.0f, x); }
+// single-MUFU reciprocal (max 1 ulp error; the FP32 error bands budget for it)
+__device__ __forceinline__ float frcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 
 // decode one record (prefetched into shared memory) into the chunk's staged form
 __device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
@@ -308,7 +313,7 @@ __device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, f
   if (e == 0) return 0;
   if (e == 1) {
     const float dfl = h.fp - h.fn;  // f_prev - f_next, f0 cancels exactly
-    const float ftol = r.fband / fminf(r.adet[h.fip], r.adet[h.fin]) + r.ftol0;
+    const float ftol = r.fband * frcp(fminf(r.adet[h.fip], r.adet[h.fin])) + r.ftol0;
     if (dfl < -ftol) return 0;  // f_prev < f_next: alpha <= 0 exactly
     if (dfl > ftol) {
       // alpha = 1 - exp(sp(x) - sp(y)) = 1 - (1 + e^x) / (1 + e^y), x = -s fp, y = -s fn:
@@ -334,11 +339,11 @@ __device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, f
         b.clipped = a_un > kAlphaClipF;
         return 1;
       }
-      if (!(a_un > 1e-10f)) atomicAdd(&g_ts_counters[3], 1ull);
     }
     atomicAdd(&g_ts_counters[1], 1ull);
   } else {
     atomicAdd(&g_ts_counters[0], 1ull);
+    if (r.flags & 16u) atomicAdd(&g_ts_counters[3], 1ull);
   }
   return (g_ts_debug_flags & 1) ? 0 : 2;
 }
@@ -498,8 +503,13 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
   asm volatile("bar.sync 1, %0;" ::"n"(kCh));
   int n = 0;
   for (int w = 0; w < kCh / 32; ++w) n += R.wok[w];
-  if (t < n)
-    for (int it = v - cnt; it < v; ++it) R.jtab[it] = (uint8_t)t;
+  if (t < n) {  // this splat's pair range of the pair -> splat table, word stores in the middle
+    int a = v - cnt;
+    for (; a < v && (a & 3); ++a) R.jtab[a] = (uint8_t)t;
+    const uint32_t pat = (uint32_t)t * 0x01010101u;
+    for (; a + 4 <= v; a += 4) *reinterpret_cast<uint32_t*>(&R.jtab[a]) = pat;
+    for (; a < v; ++a) R.jtab[a] = (uint8_t)t;
+  }
   if (t == 0) {
     R.pre[0] = 0;
     R.n = n;
@@ -648,6 +658,12 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     }
     __syncthreads();
     TS_PHASE(2);
+    if (ptime) {  // chunks, chunks with re-decisions, re-decided pairs, max per chunk
+      pacc[4] += 1;
+      pacc[5] += F.nex > 0;
+      pacc[6] += F.nex;
+      if (F.nex > (int)g_ts_phase[7]) atomicMax(&g_ts_phase[7], (unsigned long long)F.nex);
+    }
     // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
     if (!done) {
       ChunkMask m = F.bmask[pix];
@@ -690,7 +706,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   if (threadIdx.x == 0) atomicAdd(&g_ts_counters[2], (unsigned long long)F.npairs);
   if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
   if (ptime)
-    for (int k = 0; k < 4; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
 }
 
 // N_w resorting window (_core.pyx:171-187) for tiles whose list is not mean-depth monotone.

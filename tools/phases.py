@@ -22,9 +22,10 @@ for flags in (0, 4):
     gb = ts.render_backward(sv, sc, g, f, cam, dm, timing=(e[2], e[3]))
     torch.cuda.synchronize()
     ph = _native.debug_phases(reset=True)
-    print("counters (edge, alpha, evaluated, tiny-alpha):", _native.debug_counters(reset=True))
+    print("counters (edge, alpha, evaluated, edge-from-uncertain-det):", _native.debug_counters(reset=True))
     print(f"flags={flags}: forward {e[0].elapsed_time(e[1]):.3f} ms  backward {e[2].elapsed_time(e[3]):.3f} ms")
 fw, bw = ph[0:4], ph[8:13]
+print(f"forward chunks {ph[4]}, with FP64 re-decisions {ph[5]}, re-decided pairs {ph[6]}, max per chunk {ph[7]}")
 print("forward  stage/A/A'/B  :", " ".join(f"{100 * x / max(sum(fw), 1):.1f}%" for x in fw), f"(sum {sum(fw):.3e} cyc)")
 print("backward stage/load/B/C/write:", " ".join(f"{100 * x / max(sum(bw), 1):.1f}%" for x in bw), f"(sum {sum(bw):.3e} cyc)")
 _native.check(_native.lib().ts_debug_set_flags(0))
