@@ -5,16 +5,18 @@
 // red.global.add.v4.f32 per (tet, vertex) into the shared FP32 [N,4] gradient buffer
 // (scaled by lambda: the fit loop's weighting, fit.py:196-207, fused here).
 //
-// normal consistency (_core.pyx:571-668, losses.py:39-52) is rebuilt as three vertex-
-// centric GATHER passes over the implicit Kuhn grid (no atomics, deterministic):
-//   A: vertex mean of incident unit tet normals -> unit vertex normal (+ count, |mean|)
-//   B: per-vertex edge term  d_n(v) = -sum_{edge neighbours} n(b), projected back
-//      through the normalisation; per-vertex share of sum_edges (1 - n_a.n_b)
-//   C: per-vertex sum over incident tets of the chain through the tet normal
-// Incident tets are visited in increasing tet id and edge neighbours in increasing
-// vertex id, which is the reference's accumulation order, so every per-vertex FP64
-// value is bit-identical to the Cython kernel's (only the scalar loss is summed in a
-// different order).
+// normal consistency (_core.pyx:571-668, losses.py:39-52): two per-tet passes and three
+// vertex-centric GATHER passes over the implicit Kuhn grid (no atomics, deterministic):
+//   T1: per tet, unit normal g/|g| (or "undefined")                        [6R^3 threads]
+//   A : vertex mean of incident unit tet normals -> unit vertex normal (+ count, |mean|)
+//   B : per-vertex edge term  d_n(v) = -sum_{edge neighbours} n(b), projected back
+//       through the normalisation; per-vertex share of sum_edges (1 - n_a.n_b)
+//   T2: per tet, the chain through the tet normal: dL/df (4) and g            [6R^3 threads]
+//   C : per-vertex sum over incident tets of dL/df_slot and -dL/df_slot * g
+// Each tet's FP64 work is done once (not once per incident vertex), and incident tets are
+// visited in increasing tet id and edge neighbours in increasing vertex id — the
+// reference's accumulation order — so every per-vertex FP64 value is bit-identical to the
+// Cython kernel's (only the scalar loss is summed in a different order).
 #include "internal.cuh"
 
 namespace ts {
@@ -74,7 +76,8 @@ __global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __res
   block_add_to(local, loss);
 }
 
-// Incident tets of vertex (x,y,z) in increasing tet id.  Calls fn(tet_id, local_slot).
+// Incident tets of vertex (x,y,z) in increasing tet id.  Calls fn(buffer index, local slot),
+// buffer index = x-fastest cell index * 6 + p (see nc_tet_id).
 template <class Fn>
 __device__ __forceinline__ void for_incident_tets(uint32_t vid, const Grid& G, Fn&& fn) {
   const int R = G.R;
@@ -86,35 +89,59 @@ __device__ __forceinline__ void for_incident_tets(uint32_t vid, const Grid& G, F
         const int cx = x - dx, cy = y - dy, cz = z - dz;
         if (cx < 0 || cy < 0 || cz < 0 || cx >= R || cy >= R || cz >= R) continue;
         const int lc = dx | (dy << 1) | (dz << 2);
-        const uint32_t cell = ((uint32_t)cx * (uint32_t)R + (uint32_t)cy) * (uint32_t)R + (uint32_t)cz;
+        // per-tet NC buffers are laid out x-fastest (like vertex ids), not in tet-id order, so
+        // neighbouring vertices read neighbouring cells
+        const uint32_t cell = ((uint32_t)cz * (uint32_t)R + (uint32_t)cy) * (uint32_t)R + (uint32_t)cx;
         for (int p = 0; p < 6; ++p) {
           const int k1 = 1 << perm_a0(p), k2 = k1 | (1 << perm_a1(p));
-          if (lc == 0 || lc == 7 || lc == k1 || lc == k2) fn(cell * 6u + (uint32_t)p);
+          if (lc == 0 || lc == 7 || lc == k1 || lc == k2) {
+            // local slot of the vertex in the tet (tet_corners: odd permutations swap 2 and 3)
+            const bool odd = (p == 1 || p == 2 || p == 5);
+            const int slot = lc == 0 ? 0 : (lc == k1 ? 1 : ((lc == k2) != odd ? 2 : 3));
+            fn(cell * 6u + (uint32_t)p, slot);
+          }
         }
       }
 }
 
-__device__ __forceinline__ int local_slot(const uint32_t v[4], uint32_t vid) {
-  return v[0] == vid ? 0 : (v[1] == vid ? 1 : (v[2] == vid ? 2 : 3));
+// tet id of per-tet NC buffer index i (cells x-fastest there, z-fastest in tet ids)
+__device__ __forceinline__ uint32_t nc_tet_id(int64_t i, const Grid& G) {
+  const uint32_t cell = (uint32_t)(i / 6), p = (uint32_t)(i - (int64_t)cell * 6);
+  const uint32_t q = G.dR.div(cell);  // cy + R cz
+  const uint32_t cx = cell - q * (uint32_t)G.R;
+  const uint32_t cz = G.dR.div(q);
+  const uint32_t cy = q - cz * (uint32_t)G.R;
+  return ((cx * (uint32_t)G.R + cy) * (uint32_t)G.R + cz) * 6u + p;
+}
+
+// pass T1: per-tet unit normal (w = 1) or undefined (all 0)
+__global__ void __launch_bounds__(256) k_nc_tet_normals(int64_t T, Grid G, const double* __restrict__ sdf,
+                                                        const double* __restrict__ deform, double4* __restrict__ tn) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v[4];
+    double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+    load_tet(nc_tet_id(t, G), G, sdf, deform, v, P, f);
+    tet_gradient(P, f, g, c1, c2, c3);
+    const double nrm = gnorm3(g);
+    tn[t] = nrm < kEpsNormal ? make_double4(0.0, 0.0, 0.0, 0.0)
+                             : make_double4(ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm), 1.0);
+  }
 }
 
 // pass A: nv = normalized mean of incident unit normals; cnt; an (0 = undefined)
-__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, const double* __restrict__ sdf,
-                                                           const double* __restrict__ deform,
+__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, const double4* __restrict__ tn,
                                                            double* __restrict__ nv, double* __restrict__ cnt,
                                                            double* __restrict__ an) {
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double s[3] = {0.0, 0.0, 0.0}, c = 0.0;
-    for_incident_tets((uint32_t)vid, G, [&](uint32_t t) {
-      uint32_t v[4];
-      double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
-      load_tet(t, G, sdf, deform, v, P, f);
-      tet_gradient(P, f, g, c1, c2, c3);
-      double nrm = gnorm3(g);
-      if (nrm < kEpsNormal) return;
+    for_incident_tets((uint32_t)vid, G, [&](uint32_t t, int) {
+      const double4 q = tn[t];
+      if (q.w == 0.0) return;
       c = dadd(c, 1.0);
-      for (int i = 0; i < 3; ++i) s[i] = dadd(s[i], ddiv(g[i], nrm));
+      s[0] = dadd(s[0], q.x);
+      s[1] = dadd(s[1], q.y);
+      s[2] = dadd(s[2], q.z);
     });
     double a = 0.0;
     if (c != 0.0) {
@@ -176,21 +203,20 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const doubl
   block_add_to(local, loss);
 }
 
-// pass C: per-vertex gather of the tet-normal chain (_core.pyx:651-667)
-__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double* __restrict__ sdf,
-                                                 const double* __restrict__ deform, const double* __restrict__ cnt,
-                                                 const double* __restrict__ dm, float scale,
-                                                 float* __restrict__ d_vert) {
-  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
-       vid += (int64_t)gridDim.x * blockDim.x) {
-    double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
-    for_incident_tets((uint32_t)vid, G, [&](uint32_t t) {
-      uint32_t v[4];
-      double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
-      load_tet(t, G, sdf, deform, v, P, f);
-      double det = tet_gradient(P, f, g, c1, c2, c3);
-      double nrm = gnorm3(g);
-      if (nrm < kEpsNormal) return;
+// pass T2: per-tet chain through the tet normal (_core.pyx:651-667): dL/df per slot and g
+// (zeros where the reference skips the tet)
+__global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t T, Grid G, const double* __restrict__ sdf,
+                                                      const double* __restrict__ deform,
+                                                      const double* __restrict__ cnt, const double* __restrict__ dm,
+                                                      double4* __restrict__ tdf, double4* __restrict__ tg) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t v[4];
+    double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+    load_tet(nc_tet_id(t, G), G, sdf, deform, v, P, f);
+    const double det = tet_gradient(P, f, g, c1, c2, c3);
+    const double nrm = gnorm3(g);
+    double4 o = make_double4(0.0, 0.0, 0.0, 0.0), og = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (!(nrm < kEpsNormal) && det != 0.0) {
       double nt[3] = {ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm)};
       double dnt[3] = {0.0, 0.0, 0.0};
       for (int c = 0; c < 4; ++c) {
@@ -200,12 +226,32 @@ __global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double
       double dot = dadd(dadd(dmul(nt[0], dnt[0]), dmul(nt[1], dnt[1])), dmul(nt[2], dnt[2]));
       double dg[3];
       for (int i = 0; i < 3; ++i) dg[i] = ddiv(dsub(dnt[i], dmul(nt[i], dot)), nrm);
-      if (det == 0.0) return;
       double dfs[4];
       chain_coeffs(det, c1, c2, c3, dg, dfs);
-      const int c = local_slot(v, (uint32_t)vid);
-      ds = dadd(ds, dfs[c]);
-      for (int i = 0; i < 3; ++i) dp[i] = dsub(dp[i], dmul(dfs[c], g[i]));
+      o = make_double4(dfs[0], dfs[1], dfs[2], dfs[3]);
+      og = make_double4(g[0], g[1], g[2], 1.0);
+    }
+    tdf[t] = o;
+    tg[t] = og;
+  }
+}
+
+// pass C: per-vertex gather of the per-tet chain terms
+__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double4* __restrict__ tdf,
+                                                 const double4* __restrict__ tg, float scale,
+                                                 float* __restrict__ d_vert) {
+  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+       vid += (int64_t)gridDim.x * blockDim.x) {
+    double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
+    for_incident_tets((uint32_t)vid, G, [&](uint32_t t, int slot) {
+      const double4 gq = tg[t];
+      if (gq.w == 0.0) return;  // skipped by the reference (undefined normal or det == 0)
+      const double4 dq = tdf[t];
+      const double d = slot == 0 ? dq.x : (slot == 1 ? dq.y : (slot == 2 ? dq.z : dq.w));
+      ds = dadd(ds, d);
+      dp[0] = dsub(dp[0], dmul(d, gq.x));
+      dp[1] = dsub(dp[1], dmul(d, gq.y));
+      dp[2] = dsub(dp[2], dmul(d, gq.z));
     });
     float4* o = reinterpret_cast<float4*>(d_vert + vid * 4);
     float4 cur = *o;
@@ -232,20 +278,28 @@ void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32
 
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
                                 double* loss, cudaStream_t st) {
-  const int64_t n = R + 1, N = n * n * n;
+  const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
   cudaMemsetAsync(loss, 0, sizeof(double), st);
   double *nv, *cnt, *an, *dm;
+  double4 *tdf, *tg;  // T1 writes the unit normals into tdf; T2 overwrites it
   cudaMallocAsync(&nv, sizeof(double) * 3 * N, st);
   cudaMallocAsync(&dm, sizeof(double) * 3 * N, st);
   cudaMallocAsync(&cnt, sizeof(double) * N, st);
   cudaMallocAsync(&an, sizeof(double) * N, st);
-  int blocks = (int)((N + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  k_nc_vertex_normals<<<blocks, 256, 0, st>>>(N, make_grid(R), sdf, deform, nv, cnt, an);
-  k_nc_edges<<<blocks, 256, 0, st>>>(N, make_grid(R), nv, an, dm, loss);
-  k_nc_grad<<<blocks, 256, 0, st>>>(N, make_grid(R), sdf, deform, cnt, dm, scale, d_vert);
+  cudaMallocAsync(&tdf, sizeof(double4) * T, st);
+  cudaMallocAsync(&tg, sizeof(double4) * T, st);
+  const Grid G = make_grid(R);
+  const int vblocks = (int)((N + 255) / 256 < 148 * 8 ? (N + 255) / 256 : 148 * 8);
+  const int tblocks = (int)((T + 255) / 256 < 148 * 16 ? (T + 255) / 256 : 148 * 16);
+  k_nc_tet_normals<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, tdf);
+  k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tdf, nv, cnt, an);
+  k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, an, dm, loss);
+  k_nc_tet_chain<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, cnt, dm, tdf, tg);
+  k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert);
   cudaFreeAsync(nv, st);
   cudaFreeAsync(dm, st);
   cudaFreeAsync(cnt, st);
   cudaFreeAsync(an, st);
+  cudaFreeAsync(tdf, st);
+  cudaFreeAsync(tg, st);
 }
