@@ -92,7 +92,11 @@ class FitStep:
         self.nc_loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.opt = Adam([field.sdf, field.deformation], [self.cfg.lr_sdf, self.cfg.lr_deform], self.cfg.betas) \
             if self.cfg.optimizer else None
-        self.view = ViewRenderer(dev)
+        # two views in flight: each renderer owns a workspace and a stream, so one view's
+        # kernels run while the host waits on the other's sizing syncs (and kernel tails overlap)
+        self.renderers = [ViewRenderer(dev), ViewRenderer(dev)]
+        self.streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+        self.view = self.renderers[0]
 
     def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None):
         g, f, cfg = self.grid, self.field, self.cfg
@@ -102,17 +106,24 @@ class FitStep:
             raise EmptySceneError("pre-filtering removed every tetrahedron")
         if stats is not None:
             stats.active = int(active.numel())
-        for vi in views:
-            cam = self.cameras[vi]
-            maps = self.view.forward(g, f, cam, s, active, n_w=cfg.n_w)
-            K, M, _ = self.view.counts
-            if K == 0:
-                continue
-            self.view.backward(f, d_maps_fn(vi, maps), self.grads)
+        main = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(main)  # zeroed gradients, prefilter output
+            active.record_stream(st)
+        for j, vi in enumerate(views):
+            r, st = self.renderers[j % 2], self.streams[j % 2]
+            with torch.cuda.stream(st):
+                maps = r.forward(g, f, self.cameras[vi], s, active, n_w=cfg.n_w, stream=st)
+                K, M, _ = r.counts
+                if K == 0:
+                    continue
+                r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st)
             if stats is not None:
                 stats.views += 1
                 stats.splats.append(K)
                 stats.pairs.append(M)
+        for st in self.streams:
+            main.wait_stream(st)
         # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce)
         rank0 = not (dist.is_available() and dist.is_initialized()) or dist.get_rank(self.group) == 0
         if rank0:

@@ -10,9 +10,9 @@ struct SceneOut {
   double* proj;       // [K,4,2]
   double* depths;     // [K,4]
   double* f;          // [K,4]
-  double* normals;    // [K,3]
+  double* normals;    // [K,3] (nullable)
   double* md;         // [K]
-  double* amax;       // [K]
+  double* amax;       // [K] (nullable)
   double* bbox;       // [K,4]
   SplatRec* rec;      // [K]
 };

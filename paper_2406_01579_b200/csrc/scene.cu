@@ -105,12 +105,15 @@ struct CullF {
     double gn = sqrt(dadd(dadd(dmul(g[0], g[0]), dmul(g[1], g[1])), dmul(g[2], g[2])));
     if (gn >= 1e-8)
       for (int c = 0; c < 3; ++c) nrm[c] = ddiv(g[c], gn);
-    for (int c = 0; c < 3; ++c) out.normals[k * 3 + c] = nrm[c];
+    if (out.normals)  // optional FP64 outputs (the fused view pipeline needs neither)
+      for (int c = 0; c < 3; ++c) out.normals[k * 3 + c] = nrm[c];
     double md = ddiv(dadd(dadd(dadd(z[0], z[1]), z[2]), z[3]), 4.0);
     out.md[k] = md;
-    double am;
-    alpha_max_pass(f, s, 0.0, &am);
-    out.amax[k] = am;
+    if (out.amax) {
+      double am;
+      alpha_max_pass(f, s, 0.0, &am);
+      out.amax[k] = am;
+    }
     out.rec[k] = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height);
   }
 };

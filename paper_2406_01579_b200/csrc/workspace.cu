@@ -113,8 +113,8 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   // ---- K2 build_scene ----------------------------------------------------------------------
   const int64_t cap = n_active > 0 ? n_active : 1;
   SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), ws->proj.get<double>(cap * 8),
-              ws->depths.get<double>(cap * 4), ws->f.get<double>(cap * 4), ws->normals.get<double>(cap * 3),
-              ws->md.get<double>(cap), ws->amax.get<double>(cap), ws->bbox.get<double>(cap * 4),
+              ws->depths.get<double>(cap * 4), ws->f.get<double>(cap * 4), nullptr,
+              ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
               ws->rec.get<SplatRec>(cap)};
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1));
   if (!so.tet_ids || !so.rec || !scratch) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
