@@ -69,6 +69,7 @@ class StepConfig:
     lr_deform: float = 1e-3
     betas: tuple = (0.9, 0.99)
     optimizer: bool = True
+    inflight: int = 2  # views in flight (renderer + workspace + stream each)
 
 
 @dataclass
@@ -94,8 +95,9 @@ class FitStep:
             if self.cfg.optimizer else None
         # two views in flight: each renderer owns a workspace and a stream, so one view's
         # kernels run while the host waits on the other's sizing syncs (and kernel tails overlap)
-        self.renderers = [ViewRenderer(dev), ViewRenderer(dev)]
-        self.streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+        n = max(1, int(self.cfg.inflight))
+        self.renderers = [ViewRenderer(dev) for _ in range(n)]
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
         self.view = self.renderers[0]
 
     def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None):
@@ -111,7 +113,7 @@ class FitStep:
             st.wait_stream(main)  # zeroed gradients, prefilter output
             active.record_stream(st)
         for j, vi in enumerate(views):
-            r, st = self.renderers[j % 2], self.streams[j % 2]
+            r, st = self.renderers[j % len(self.renderers)], self.streams[j % len(self.streams)]
             with torch.cuda.stream(st):
                 maps = r.forward(g, f, self.cameras[vi], s, active, n_w=cfg.n_w, stream=st)
                 K, M, _ = r.counts
