@@ -285,23 +285,42 @@ __device__ __forceinline__ bool exact_group(const Scene64& S, bool act, int64_t 
     }
     ++n;
   }
-  // the two softplus terms on lanes 1 and 2 of the group, concurrently
   const bool ok = act && n >= 2;
+  // The reference blends iff a = 1 - exp(sp(x) - sp(y)) > 0 in FP64, x = -s f_prev,
+  // y = -s f_next (these products are bit-identical here).  With alpha = sigmoid(y)(1 - e^{x-y})
+  // evaluated in FP32 from the FP64 difference x - y (relative error ~1e-6), the rounded
+  // reference outcome is certain once |alpha| clears the rounding of its softplus terms
+  // (<= ~4 ulp of max(1, |x|, |y|)) by a wide margin, and alpha is away from ALPHA_CLIP;
+  // only the remaining pairs evaluate the FP64 softplus chain (on lanes 1 and 2 at once).
+  const double x = dmul(-s, flo), y = dmul(-s, fhi), dxy = dsub(x, y);
+  const float yf = (float)y;
+  const float ey = expf(-fabsf(yf)), ry = 1.0f / (1.0f + ey);
+  const float sy = yf >= 0.f ? ry : ey * ry, sny = yf >= 0.f ? ey * ry : ry;  // sigmoid(+-y)
+  const float a_est = sy * -expm1f((float)dxy);
+  const float margin = 1e-13f * fmaxf(1.0f, fmaxf(fabsf((float)x), fabsf(yf)));
+  const bool certain = fabsf(a_est) > margin && fabsf(a_est - kAlphaClipF) > 1e-5f;
   double spv = 0.0;
-  if (ok && (fi == 1 || fi == 2)) spv = softplus_d(dmul(-s, fi == 1 ? flo : fhi));
+  if (ok && !certain && (fi == 1 || fi == 2)) spv = softplus_d(fi == 1 ? x : y);
   const double spx = __shfl_sync(0xffffffffu, spv, lead + 1), spy = __shfl_sync(0xffffffffu, spv, lead + 2);
   if (!ok || fi != 0) return false;
-  const double ed = exp(dsub(spx, spy));
-  const double a = dsub(1.0, ed);
-  if (a <= 0.0) return false;
   const float sf = (float)s;
-  b.a = (float)a;
-  b.om = (float)ed;
+  if (certain) {
+    if (a_est < 0.f) return false;
+    b.a = a_est;
+    b.om = fmaf(sy, expf((float)dxy), sny);
+    b.clipped = a_est > kAlphaClipF;
+  } else {
+    const double ed = exp(dsub(spx, spy));
+    const double a = dsub(1.0, ed);
+    if (a <= 0.0) return false;
+    b.a = (float)a;
+    b.om = (float)ed;
+    b.clipped = a > 1.0 - 1e-4;
+  }
   b.sp = sf * sigmoidf_stable(-sf * (float)flo);
   b.sn = sf * sigmoidf_stable(-sf * (float)fhi);
   b.fip = lo;
   b.fin = hi;
-  b.clipped = a > 1.0 - 1e-4;
   return true;
 }
 
