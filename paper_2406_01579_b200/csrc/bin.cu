@@ -168,23 +168,128 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
 }
 
-// long tiles (lo_len < L <= cap), listed by k_long_tiles: persistent CTAs walk the list, so
-// the large shared-memory footprint is only paid where there is work
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_tile_sort_long(const int32_t* __restrict__ tlist,
-                                                            const int64_t* __restrict__ tcount,
-                                                            const int64_t* __restrict__ starts,
-                                                            const uint64_t* __restrict__ keys, int tiles_x,
-                                                            const BinRec* __restrict__ br,
-                                                            const int64_t* __restrict__ splat_off,
-                                                            const double* __restrict__ md,
-                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                            uint8_t* __restrict__ nonmono) {
-  extern __shared__ uint64_t s[];
+// Long tiles (2048 < L <= 16384), listed by k_long_tiles: persistent 1024-thread CTAs walk the
+// list and sort each tile with a shared-memory LSD radix sort (8-bit digits) on the key
+// (q, splat): ceil(splat bits / 8) passes over the splat index, then four over q.  Each
+// warp owns a striped slab of E * 32 elements (slot e of lane l at w*32E + e*32 + l, so warp
+// order is (e, lane) = position order and the sort is stable); ranks inside a warp come from
+// __match_any_sync peers and per-warp digit counters, offsets from a digit-major scan of the
+// counters.  O(passes * L) instead of the bitonic O(L log^2 L).
+constexpr int kRadixThreads = 1024;
+constexpr int kRadixWarps = kRadixThreads / 32;
+
+template <int E>
+__device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint32_t* H, uint32_t* dbase,
+                                                int passes_lo) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int base = w * 32 * E + lane;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int pass = 0; pass < passes_lo + 4; ++pass) {
+    const bool hi = pass >= passes_lo;
+    const int shift = (hi ? pass - passes_lo : pass) * 8;
+    for (int i = threadIdx.x; i < kRadixWarps * 256; i += kRadixThreads) H[i] = 0u;
+    uint32_t q[E], v[E], rk[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      q[e] = kq[base + e * 32];
+      v[e] = kv[base + e * 32];
+    }
+    __syncthreads();
+    uint32_t* Hw = H + w * 256;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t d = ((hi ? q[e] : v[e]) >> shift) & 255u;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t cur = Hw[d];
+      rk[e] = cur + __popc(peers & lt);
+      __syncwarp();
+      if ((peers & lt) == 0u) Hw[d] = cur + __popc(peers);  // lowest peer updates
+      __syncwarp();
+    }
+    __syncthreads();
+    // digit-major exclusive scan of the per-warp counters
+    if (threadIdx.x < 256) {
+      const int d = threadIdx.x;
+      uint32_t run = 0;
+      for (int ww = 0; ww < kRadixWarps; ++ww) {
+        const uint32_t c = H[ww * 256 + d];
+        H[ww * 256 + d] = run;
+        run += c;
+      }
+      dbase[d] = run;
+    }
+    __syncthreads();
+    if (w == 0) {
+      uint32_t t8[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        t8[k] = dbase[lane * 8 + k];
+        sum += t8[k];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        dbase[lane * 8 + k] = run;
+        run += t8[k];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t d = ((hi ? q[e] : v[e]) >> shift) & 255u;
+      const uint32_t dst = dbase[d] + Hw[d] + rk[e];
+      kq[dst] = q[e];
+      kv[dst] = v[e];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
+    const int32_t* __restrict__ tlist, const int64_t* __restrict__ tcount, const int64_t* __restrict__ starts,
+    const uint64_t* __restrict__ keys, int tiles_x, const BinRec* __restrict__ br,
+    const int64_t* __restrict__ splat_off, const double* __restrict__ md, int32_t* __restrict__ items,
+    int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono, int cap, int passes_lo) {
+  extern __shared__ uint32_t sm32[];
+  uint32_t* kq = sm32;
+  uint32_t* kv = sm32 + cap;
+  uint32_t* H = sm32 + 2 * cap;
+  uint32_t* dbase = H + kRadixWarps * 256;
   __shared__ int bad;
   const int64_t n = *tcount;
-  for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x)
-    sort_tile<THREADS>(s, bad, tlist[idx], starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
+  for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
+    const int t = tlist[idx];
+    const int64_t lo = starts[t];
+    const int L = (int)(starts[t + 1] - lo);
+    const int P = L <= 4096 ? 4096 : (L <= 8192 ? 8192 : 16384);
+    for (int i = threadIdx.x; i < P; i += kRadixThreads) {
+      const uint64_t k = i < L ? keys[lo + i] : ~0ull;  // padding sorts last
+      kq[i] = (uint32_t)(k >> 32);
+      kv[i] = (uint32_t)k;
+    }
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    if (P == 4096)
+      radix_sort_tile<4>(kq, kv, H, dbase, passes_lo);
+    else if (P == 8192)
+      radix_sort_tile<8>(kq, kv, H, dbase, passes_lo);
+    else
+      radix_sort_tile<16>(kq, kv, H, dbase, passes_lo);
+    int mybad = 0;
+    for (int i = threadIdx.x; i < L; i += kRadixThreads) {
+      emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+      if (i + 1 < L && md[kv[i]] > md[kv[i + 1]]) mybad = 1;
+    }
+    if (mybad) bad = 1;
+    __syncthreads();
+    if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
+  }
 }
 
 // tiles with lo_len < L <= cap -> tlist[0, *tcount)
@@ -295,21 +400,24 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
     k_tile_sort_smem<256><<<T, 256, 2048 * sizeof(uint64_t), st>>>(T, 2048, starts, keys, tiles_x, w.br, splat_off,
                                                                    md, items, pos_of, nonmono);
     if (maxL > 2048) {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_tile_sort_long<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             16384 * (int)sizeof(uint64_t));
-        attr = true;
-      }
       // the scatter cursor is free again: reuse it as the long-tile list
       cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
       k_long_tiles<<<(T + 255) / 256, 256, 0, st>>>(T, 2048, 16384, starts, w.tile_cnt, w.dev_i64);
-      // shared memory sized to the longest list (not the 16384 cap) so several CTAs fit per SM
-      int64_t P = 4096;
-      while (P < maxL && P < 16384) P <<= 1;
-      const int per_sm = P <= 8192 ? 2 : 1;  // 2048 threads / SM
-      k_tile_sort_long<1024><<<148 * per_sm, 1024, P * sizeof(uint64_t), st>>>(
-          w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br, splat_off, md, items, pos_of, nonmono);
+      // shared memory sized to the longest list (not the 16384 cap) so two CTAs fit per SM
+      // where they can; digit passes over the splat index: ceil(bits(K - 1) / 8)
+      const int cap = maxL <= 4096 ? 4096 : (maxL <= 8192 ? 8192 : 16384);
+      const size_t smem = sizeof(uint32_t) * (2 * (size_t)cap + kRadixWarps * 256 + 256);
+      static size_t attr = 0;
+      if (smem > attr) {
+        cudaFuncSetAttribute(k_tile_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+      }
+      int kbits = 1;
+      while (kbits < 32 && ((int64_t)1 << kbits) < K) ++kbits;
+      const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+      k_tile_sort_long<<<148 * per_sm, kRadixThreads, smem, st>>>(w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br,
+                                                                 splat_off, md, items, pos_of, nonmono, cap,
+                                                                 (kbits + 7) / 8);
     }
     if (maxL > 16384)
       k_tile_sort_global<<<T, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,

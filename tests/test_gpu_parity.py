@@ -195,3 +195,31 @@ def test_fused_view_pipeline_matches_api(ts, case):
     assert torch.equal(m2.opacity, maps.opacity)
     gb2 = vr.backward(fs, dm, ts.GradientBuffers.zeros(g.num_vertices))
     assert torch.allclose(gb2.d_vert, gb.d_vert, rtol=1e-6, atol=1e-6 * float(gb.d_vert.abs().max()))
+
+
+@pytest.mark.parametrize("R,S", [(48, 128), (64, 96)])
+def test_bins_long_tiles_match_stable_sort(ts, R, S):
+    """Tiles longer than 2048 entries take the shared-memory radix sort: the lists must equal
+    the reference's stable (tile, q) sort (raster.py:104-141, restated in the oracle)."""
+    from types import SimpleNamespace
+    from oracle import ts_oracle as O
+    g = ts.build_grid(R)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    cam = ts.orbit_camera(1, 8, width=S, height=S)
+    sc = ts.build_scene(g, f, cam, 100.0)
+    b = ts.bin_and_sort(sc, cam)
+    starts = b.starts.cpu().numpy()
+    assert np.diff(starts).max() > 2048  # the long-tile path is exercised
+    osc = SimpleNamespace(bbox=sc.bbox.cpu().numpy(), mean_depth=sc.mean_depth.cpu().numpy())
+    ob = O.bin_and_sort(_Len(osc, len(sc)), SimpleNamespace(width=S, height=S, near=cam.near, far=cam.far))
+    assert np.array_equal(starts, ob.starts)
+    assert np.array_equal(b.items.cpu().numpy().astype(np.int64), ob.items)
+
+
+class _Len:
+    def __init__(self, ns, n):
+        self.__dict__.update(ns.__dict__)
+        self._n = n
+
+    def __len__(self):
+        return self._n
