@@ -88,7 +88,7 @@ int ts_build_scene(const double* sdf, const double* deform, int32_t R, const ts_
   if (!sdf || !deform || !cam || !out || !count || R < 1 || n_active < 0 || (n_active > 0 && !active))
     return fail(TS_EINVAL, "ts_build_scene: bad arguments");
   cudaStream_t st = ST(stream);
-  int64_t* scratch = dalloc<int64_t>(compact_blocks(n_active), st);
+  int64_t* scratch = dalloc<int64_t>(compact_blocks(n_active, 1), st);
   if (!scratch) return fail(TS_ENOMEM, "ts_build_scene: out of device memory");
   SceneOut o{out->tet_ids, out->vert_ids, out->proj, out->depths, out->f, out->normals, out->mean_depth,
              out->alpha_max, out->bbox, reinterpret_cast<SplatRec*>(out->records)};

@@ -16,12 +16,13 @@ constexpr int kScanThreads = 256;
 constexpr int kItemsPerThread = 8;
 constexpr int kChunk = kScanThreads * kItemsPerThread;  // 2048 items per CTA
 
-template <class F>
+// IPT items per thread: 8 for light predicates, 1 for latency-bound ones (more CTAs in flight)
+template <class F, int IPT>
 __global__ void __launch_bounds__(kScanThreads) k_count(int64_t n, F f, int64_t* __restrict__ counts) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int64_t base = (int64_t)blockIdx.x * (kScanThreads * IPT);
   int c = 0;
 #pragma unroll 4
-  for (int k = 0; k < kItemsPerThread; ++k) {
+  for (int k = 0; k < IPT; ++k) {
     int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
     if (i < n && f.pred(i)) ++c;
   }
@@ -74,13 +75,13 @@ static __global__ void __launch_bounds__(1024) k_scan_i64(int64_t* __restrict__ 
   if (threadIdx.x == 0) a[n] = carry_s;
 }
 
-template <class F>
+template <class F, int IPT>
 __global__ void __launch_bounds__(kScanThreads) k_emit(int64_t n, F f, const int64_t* __restrict__ offs) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int64_t base = (int64_t)blockIdx.x * (kScanThreads * IPT);
   int64_t run = offs[blockIdx.x];
   __shared__ int wcnt[kScanThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int k = 0; k < kItemsPerThread; ++k) {
+  for (int k = 0; k < IPT; ++k) {
     int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
     bool p = i < n && f.pred(i);
     unsigned m = __ballot_sync(0xffffffffu, p);
@@ -100,18 +101,20 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(int64_t n, F f, const int
 }
 
 // host-side driver: returns the device pointer holding the survivor total (offs[nb])
-template <class F>
+template <class F, int IPT = kItemsPerThread>
 inline int64_t* compact(int64_t n, const F& f, int64_t* offs_scratch, cudaStream_t st) {
-  int64_t nb = (n + kChunk - 1) / kChunk;
+  const int64_t chunk = kScanThreads * IPT, nb = (n + chunk - 1) / chunk;
   if (nb > 0) {
-    k_count<F><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
+    k_count<F, IPT><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
   }
   k_scan_i64<<<1, 1024, 0, st>>>(offs_scratch, nb);
-  if (nb > 0) k_emit<F><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
+  if (nb > 0) k_emit<F, IPT><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
   return offs_scratch + nb;
 }
 
-inline int64_t compact_blocks(int64_t n) { return (n + kChunk - 1) / kChunk + 1; }
+inline int64_t compact_blocks(int64_t n, int ipt = kItemsPerThread) {
+  return (n + kScanThreads * ipt - 1) / (kScanThreads * ipt) + 1;
+}
 
 // ---- exclusive scan of int32 counts into int64 offsets (out[n] = total) --------------
 static __global__ void __launch_bounds__(kScanThreads) k_chunk_sums(const int32_t* __restrict__ in, int64_t n,

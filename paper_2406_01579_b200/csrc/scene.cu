@@ -152,7 +152,7 @@ int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, cons
                             const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
                             cudaStream_t st) {
   CullF f{active, sdf, deform, make_grid(R), cam, s, out};
-  int64_t* d_total = compact(n_active, f, scratch, st);
+  int64_t* d_total = compact<CullF, 1>(n_active, f, scratch, st);  // scratch: compact_blocks(n, 1)
   int64_t h = 0;
   cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);

@@ -116,7 +116,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
               ws->depths.get<double>(cap * 4), ws->f.get<double>(cap * 4), nullptr,
               ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
               ws->rec.get<SplatRec>(cap)};
-  int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1));
+  int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1, 1));
   if (!so.tet_ids || !so.rec || !scratch) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   const int64_t K = n_active > 0 ? ts_impl_build_scene(sdf, deform, R, cam, s, active, n_active, so, scratch, st) : 0;
   // ---- K3-K5 bins ----------------------------------------------------------------------------
