@@ -1109,55 +1109,67 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   }
 }
 
-// per-splat gather + normal chain + camera chain (raster.py:253-306), FP64 math
+// per-splat gather + normal chain + camera chain (raster.py:253-306).  FP32 chain math (the
+// gradients are FP32); vertex positions are formed in FP64 (grid coordinate + deformation)
+// and only their differences / camera-space coordinates are rounded, one vertex at a time.
 template <bool COLOR>
-__global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const int32_t* __restrict__ pos_of,
-                        const float* __restrict__ rows, const int32_t* __restrict__ vert_ids,
-                        const int32_t* __restrict__ tet_ids, const double* __restrict__ fsc,
-                        const double* __restrict__ deform, Grid G, Camera cam, float* __restrict__ d_vert,
-                        float* __restrict__ d_color) {
+__global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const int64_t* __restrict__ splat_off,
+                                               const int32_t* __restrict__ pos_of, const float* __restrict__ rows,
+                                               const int32_t* __restrict__ vert_ids,
+                                               const int32_t* __restrict__ tet_ids, const double* __restrict__ fsc,
+                                               const double* __restrict__ deform, Grid G, Camera cam,
+                                               float* __restrict__ d_vert, float* __restrict__ d_color) {
+  constexpr int NQ = COLOR ? 6 : 5;  // float4s of a row that carry data
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
-    float a[kGr];
+    float a[4 * NQ];
 #pragma unroll
-    for (int i = 0; i < kGr; ++i) a[i] = 0.f;
-    for (int64_t r = splat_off[k]; r < splat_off[k + 1]; ++r) {
-      const float4* src = reinterpret_cast<const float4*>(rows + (int64_t)pos_of[r] * kGr);
+    for (int i = 0; i < 4 * NQ; ++i) a[i] = 0.f;
+    const int64_t r0 = splat_off[k], r1 = splat_off[k + 1];
+    for (int64_t r = r0; r < r1; ++r) {
+      const float4* src = reinterpret_cast<const float4*>(rows + (int64_t)__ldg(pos_of + r) * kGr);
 #pragma unroll
-      for (int i = 0; i < kGr / 4; ++i) {
-        float4 q = __ldg(src + i);
+      for (int i = 0; i < NQ; ++i) {
+        const float4 q = __ldg(src + i);
         a[4 * i] += q.x;
         a[4 * i + 1] += q.y;
         a[4 * i + 2] += q.z;
         a[4 * i + 3] += q.w;
       }
     }
-    // FP32 chain math (the gradients are FP32); only the tet edge vectors and the camera-space
-    // positions are formed in FP64 (differences of O(1) coordinates) before rounding.
-    float dF[4], dZ[4], dPx[4], dPy[4], dPos[4][3];
+    const int4 vv = __ldg(reinterpret_cast<const int4*>(vert_ids) + k);
+    const uint32_t vid[4] = {(uint32_t)vv.x, (uint32_t)vv.y, (uint32_t)vv.z, (uint32_t)vv.w};
+    const double2 fa = __ldg(reinterpret_cast<const double2*>(fsc) + 2 * k);
+    const double2 fb = __ldg(reinterpret_cast<const double2*>(fsc) + 2 * k + 1);
+    float e[3][3], pcs[4][3];
+    {
+      double P0[3];
+      vertex_position(vid[0], G, deform, P0);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        double P[3];
+        if (v == 0) {
+          P[0] = P0[0]; P[1] = P0[1]; P[2] = P0[2];
+        } else {
+          vertex_position(vid[v], G, deform, P);
+          for (int i = 0; i < 3; ++i) e[v - 1][i] = (float)(P[i] - P0[i]);
+        }
+        for (int r = 0; r < 3; ++r)
+          pcs[v][r] = (float)(P[0] * cam.R[r * 3] + P[1] * cam.R[r * 3 + 1] + P[2] * cam.R[r * 3 + 2] + cam.t[r]);
+      }
+    }
+    float dF[4], dPos[4][3];
     const float dMd = a[19];
+#pragma unroll
     for (int v = 0; v < 4; ++v) {
       dF[v] = a[v];
-      dZ[v] = a[4 + v] + 0.25f * dMd;
-      dPx[v] = a[8 + v];
-      dPy[v] = a[12 + v];
       dPos[v][0] = dPos[v][1] = dPos[v][2] = 0.f;
-    }
-    uint32_t vid[4];
-    double P[4][3], f64[4];
-    for (int v = 0; v < 4; ++v) {
-      vid[v] = (uint32_t)vert_ids[k * 4 + v];
-      vertex_position(vid[v], G, deform, P[v]);
-      f64[v] = fsc[k * 4 + v];
     }
     // normal chain: n = g/|g|, dL/dg = (I - n n^T) dL/dn / |g|, dL/df = B^-T [dL/dg, 0]
     // (B^-T [dL/dg, 0] in the cross-product form of _core.pyx:517-541)
-    float e1[3], e2[3], e3[3];
-    for (int i = 0; i < 3; ++i) {
-      e1[i] = (float)(P[1][i] - P[0][i]);
-      e2[i] = (float)(P[2][i] - P[0][i]);
-      e3[i] = (float)(P[3][i] - P[0][i]);
-    }
-    const float df1 = (float)(f64[1] - f64[0]), df2 = (float)(f64[2] - f64[0]), df3 = (float)(f64[3] - f64[0]);
+    const float df1 = (float)(fa.y - fa.x), df2 = (float)(fb.x - fa.x), df3 = (float)(fb.y - fa.x);
+    const float* e1 = e[0];
+    const float* e2 = e[1];
+    const float* e3 = e[2];
     const float c1[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2], e2[0] * e3[1] - e2[1] * e3[0]};
     const float c2[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2], e3[0] * e1[1] - e3[1] * e1[0]};
     const float c3[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
@@ -1186,13 +1198,12 @@ __global__ void k_chain(int64_t K, const int64_t* __restrict__ splat_off, const 
     }
     // camera chain: pixel = (fx X/Z + cx, fy Y/Z + cy), depth = Z
     const float fx = (float)cam.fx, fy = (float)cam.fy;
+#pragma unroll
     for (int v = 0; v < 4; ++v) {
-      float pc[3];
-      for (int r = 0; r < 3; ++r)
-        pc[r] = (float)(P[v][0] * cam.R[r * 3] + P[v][1] * cam.R[r * 3 + 1] + P[v][2] * cam.R[r * 3 + 2] + cam.t[r]);
+      const float* pc = pcs[v];
+      const float dPx = a[8 + v], dPy = a[12 + v], dZ = a[4 + v] + 0.25f * dMd;
       const float iZ = 1.0f / pc[2];
-      const float dpc[3] = {dPx[v] * fx * iZ, dPy[v] * fy * iZ,
-                            (-dPx[v] * fx * pc[0] - dPy[v] * fy * pc[1]) * iZ * iZ + dZ[v]};
+      const float dpc[3] = {dPx * fx * iZ, dPy * fy * iZ, (-dPx * fx * pc[0] - dPy * fy * pc[1]) * iZ * iZ + dZ};
       for (int j = 0; j < 3; ++j)
         dPos[v][j] += dpc[0] * (float)cam.R[j] + dpc[1] * (float)cam.R[3 + j] + dpc[2] * (float)cam.R[6 + j];
       red_add_v4(d_vert + (size_t)vid[v] * 4, dF[v], dPos[v][0], dPos[v][1], dPos[v][2]);
@@ -1288,7 +1299,7 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
                                                   maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
                                                   nullptr, n_proc, rows);
   int blocks = (int)((K + 127) / 128);
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * 64) blocks = 148 * 64;
   if (color)
     k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
                                           make_grid(R), cam, d_vert, d_color);
