@@ -742,24 +742,32 @@ __device__ __forceinline__ uint32_t qkey(double md, double near_, double far_) {
   return (uint32_t)(unsigned long long)dmul(qq, 4294967295.0);  // raster.py:132-134
 }
 
-__global__ void __launch_bounds__(128) k_window(int T, const int64_t* __restrict__ starts,
+__global__ void __launch_bounds__(256) k_window(int T, const int64_t* __restrict__ starts,
                                                 const int32_t* __restrict__ items,
                                                 const uint8_t* __restrict__ nonmono, const double* __restrict__ md,
                                                 int n_w, double near_, double far_, int32_t* __restrict__ witems,
-                                                int32_t* __restrict__ widx_s, double* __restrict__ wz_s) {
+                                                uint32_t* __restrict__ qpos, int32_t* __restrict__ widx_s,
+                                                double* __restrict__ wz_s) {
   const int t = blockIdx.x;
   if (t >= T || !nonmono[t]) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
+  // the tile's depth keys, once per position
+  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) qpos[lo + i] = qkey(md[items[lo + i]], near_, far_);
+  __syncthreads();
+  const uint32_t* qs = qpos + lo;
   for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
-    const double mi = md[items[lo + i]];
-    const uint32_t qi = qkey(mi, near_, far_);
-    if (i > 0 && qkey(md[items[lo + i - 1]], near_, far_) == qi) continue;  // not a run start
+    const uint32_t qi = qs[i];
+    const bool starts_run = i == 0 || qs[i - 1] != qi;
+    if (!starts_run) continue;
+    if (i + 1 >= L || qs[i + 1] != qi) {  // run of one
+      witems[lo + i] = items[lo + i];
+      continue;
+    }
     int64_t e = i + 1;
     bool mono = true;
-    double prev = mi;
-    while (e < L) {
+    double prev = md[items[lo + i]];
+    while (e < L && qs[e] == qi) {
       const double me = md[items[lo + e]];
-      if (qkey(me, near_, far_) != qi) break;
       mono &= !(me < prev);
       prev = me;
       ++e;
@@ -1235,7 +1243,8 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   cudaMallocAsync(&wz, sizeof(double) * M, st);
   cudaMallocAsync(&cnt, sizeof(int32_t) * M, st);
   cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(M), st);
-  k_window<<<T, 128, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, widx, wz);
+  uint32_t* qpos = reinterpret_cast<uint32_t*>(cnt);  // dead before k_item_counts writes cnt
+  k_window<<<T, 256, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, qpos, widx, wz);
   k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
   scan_counts(cnt, M, item_off, scratch, st);
   int64_t total = 0;
