@@ -10,6 +10,7 @@ rank (fit.py:70-90), followed by the deformation clamp (field.py:40-42).
 from __future__ import annotations
 
 import math
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field as dc_field
 
 import torch
@@ -99,6 +100,8 @@ class FitStep:
         self.renderers = [ViewRenderer(dev) for _ in range(n)]
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
         self.view = self.renderers[0]
+        self.reg_stream = torch.cuda.Stream(device=dev)
+        self._pool = ThreadPoolExecutor(max_workers=n) if n > 1 else None
 
     def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None):
         g, f, cfg = self.grid, self.field, self.cfg
@@ -109,30 +112,51 @@ class FitStep:
         if stats is not None:
             stats.active = int(active.numel())
         main = torch.cuda.current_stream()
-        for st in self.streams:
+        for st in self.streams + [self.reg_stream]:
             st.wait_stream(main)  # zeroed gradients, prefilter output
             active.record_stream(st)
-        for j, vi in enumerate(views):
-            r, st = self.renderers[j % len(self.renderers)], self.streams[j % len(self.streams)]
-            with torch.cuda.stream(st):
-                maps = r.forward(g, f, self.cameras[vi], s, active, n_w=cfg.n_w, stream=st)
-                K, M, _ = r.counts
-                if K == 0:
-                    continue
-                r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st)
-            if stats is not None:
-                stats.views += 1
-                stats.splats.append(K)
-                stats.pairs.append(M)
-        for st in self.streams:
-            main.wait_stream(st)
-        # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce)
+        # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce);
+        # they depend only on the field, so they run on their own stream beside the views
+        # (every gradient kernel accumulates atomically)
         rank0 = not (dist.is_available() and dist.is_initialized()) or dist.get_rank(self.group) == 0
         if rank0:
-            if cfg.lambda_eik > 0:
-                eikonal_loss_async(g, f, active, self.grads, cfg.lambda_eik, self.eik_loss)
-            if cfg.lambda_nc > 0:
-                normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss)
+            with torch.cuda.stream(self.reg_stream):
+                if cfg.lambda_eik > 0:
+                    eikonal_loss_async(g, f, active, self.grads, cfg.lambda_eik, self.eik_loss, self.reg_stream)
+                if cfg.lambda_nc > 0:
+                    normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss, self.reg_stream)
+        # views: one host thread per renderer/stream, so one view's sizing syncs never stall the
+        # other stream's launches
+        lanes = len(self.renderers)
+        work = [list(views)[j::lanes] for j in range(lanes)]
+
+        def run_lane(j):
+            r, st = self.renderers[j], self.streams[j]
+            torch.cuda.set_device(st.device)  # worker threads start on device 0
+            done = []
+            with torch.cuda.stream(st):
+                for vi in work[j]:
+                    maps = r.forward(g, f, self.cameras[vi], s, active, n_w=cfg.n_w, stream=st)
+                    K, M, _ = r.counts
+                    if K == 0:
+                        continue
+                    r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st)
+                    done.append((K, M))
+            return done
+
+        if lanes == 1:
+            results = [run_lane(0)]
+        else:
+            futs = [self._pool.submit(run_lane, j) for j in range(lanes)]
+            results = [fu.result() for fu in futs]
+        if stats is not None:
+            for done in results:
+                for K, M in done:
+                    stats.views += 1
+                    stats.splats.append(K)
+                    stats.pairs.append(M)
+        for st in self.streams + [self.reg_stream]:
+            main.wait_stream(st)
         allreduce_gradients(self.grads, self.group)
         if self.opt is not None:
             self.opt.step([f.sdf, f.deformation], [self.grads.d_sdf, self.grads.d_deform])

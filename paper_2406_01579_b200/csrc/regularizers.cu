@@ -253,13 +253,9 @@ __global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double
       dp[1] = dsub(dp[1], dmul(d, gq.y));
       dp[2] = dsub(dp[2], dmul(d, gq.z));
     });
-    float4* o = reinterpret_cast<float4*>(d_vert + vid * 4);
-    float4 cur = *o;
-    cur.x += (float)(scale * ds);
-    cur.y += (float)(scale * dp[0]);
-    cur.z += (float)(scale * dp[1]);
-    cur.w += (float)(scale * dp[2]);
-    *o = cur;
+    // atomic add: the fit step runs the regularizers concurrently with the views' chains
+    red_add_v4(d_vert + vid * 4, (float)(scale * ds), (float)(scale * dp[0]), (float)(scale * dp[1]),
+               (float)(scale * dp[2]));
   }
 }
 

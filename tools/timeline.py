@@ -44,3 +44,25 @@ for a, b, n in ks:
     tot[k] = tot.get(k, 0.0) + (b - a)
 for k, v in sorted(tot.items(), key=lambda x: -x[1])[:20]:
     print(f"  {v/1e3:8.3f} ms  {k}")
+
+# concurrency sweep: time with 0 / 1 / 2+ kernels running, and per kernel the time it ran alone
+pts = []
+for a, b, n in ks:
+    pts.append((a, 1, n))
+    pts.append((b, -1, n))
+pts.sort(key=lambda x: (x[0], x[1]))
+active, last, lvl = {}, pts[0][0], {0: 0.0, 1: 0.0, 2: 0.0}
+alone = {}
+for tt, d, n in pts:
+    c = sum(active.values())
+    dt = tt - last
+    lvl[min(c, 2)] += dt
+    if c == 1:
+        only = next(k for k, v in active.items() if v > 0)
+        alone[only] = alone.get(only, 0.0) + dt
+    k = n.split("(")[0][:60]
+    active[k] = active.get(k, 0) + d
+    last = tt
+print(f"time with 0 / 1 / 2+ kernels: {lvl[0]/1e3:.2f} / {lvl[1]/1e3:.2f} / {lvl[2]/1e3:.2f} ms")
+for k, v in sorted(alone.items(), key=lambda x: -x[1])[:12]:
+    print(f"  alone {v/1e3:8.3f} ms  {k}")
