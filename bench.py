@@ -374,14 +374,15 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     """Roofline of the two compositing launches, timed with CUDA events recorded on the
     launching stream immediately around each launch (render_forward = the compositing
     kernel; render_backward = compositing backward + vertex chain), averaged over reps.
-    Algorithmic work (the reference's own per-pair / per-record operation counts, SURVEY.md
-    §8d): forward 8 P_pop + 120 P_bbox + 19 B flops, backward 300 B + 300 K_v flops."""
+    Algorithmic work in FP32 lane-ops (the reference's own per-pair /
+    per-record operation counts): forward 8 P_pop + 120 P_bbox + 19 B, backward 300 B + 300 K_v;
+    peak = FP32 issue, 148 SMs x 128 lanes x max SM clock (§8d: 37.2 T lane-ops/s)."""
     import torch
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if \
         os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
-    fp32_peak = n_sm * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s (FMA = 2)
+    fp32_peak = n_sm * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s (SURVEY §8d)
     field.sdf.copy_(sdf0)
     field.deformation.copy_(def0)
     reps = 5
@@ -410,10 +411,10 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     P_bbox = cnt[2]
     fwd_flop = 8 * P_pop + 120 * P_bbox + 19 * B
     bwd_flop = 300 * B + 300 * K_v
-    kern = {"render_forward": {"ms": tf, "flop": fwd_flop}, "render_backward": {"ms": tb, "flop": bwd_flop}}
+    kern = {"render_forward": {"ms": tf, "lane_ops": fwd_flop}, "render_backward": {"ms": tb, "lane_ops": bwd_flop}}
     for d in kern.values():
-        d["achieved_TFLOPs"] = d["flop"] / (d["ms"] * 1e-3) / 1e12
-        d["frac_of_fp32"] = d["achieved_TFLOPs"] / fp32_peak
+        d["achieved_Tlaneops"] = d["lane_ops"] / (d["ms"] * 1e-3) / 1e12
+        d["frac_of_fp32_issue"] = d["achieved_Tlaneops"] / fp32_peak
     top = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[top]
     # DRAM traffic per launch of the same kernel from the committed ncu --set full capture
@@ -425,11 +426,11 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
         if key in tj:
             traffic = tj[key]["dram_bytes_per_launch"]
             tsrc = f"profiles/{tj[key]['source']} ({key}, dram__bytes_read.sum + dram__bytes_write.sum)"
-    roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_TFLOPs"], "peak": fp32_peak,
-            "unit": "TFLOP/s", "frac": d["frac_of_fp32"], "traffic": traffic, "traffic_unit": "bytes/launch",
+    roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_Tlaneops"], "peak": fp32_peak,
+            "unit": "T lane-op/s", "frac": d["frac_of_fp32_issue"], "traffic": traffic, "traffic_unit": "bytes/launch",
             "traffic_source": tsrc,
-            "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (FP32 issue; no tensor "
-                           f"cores: not a dense contraction)"}
+            "peak_source": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FP32 issue, SURVEY 8d; no tensor "
+                           f"cores: not a dense contraction; DRAM traffic well under HBM bandwidth)"}
     extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M, "pixel_pairs": P_pairs,
              "fp64_redecisions_edge": cnt[0], "fp64_redecisions_alpha": cnt[1]}
     return roof, {"compositing": kern, "counts": extra}
