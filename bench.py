@@ -10,8 +10,8 @@ normal consistency (lambda 1000 each) + NCCL all-reduce of the vertex gradients 
 
 Prints ONE JSON line (rank 0).  `value` = views/s with inputs resident in HBM; `e2e` = the
 same through the public API with host inputs copied in (pinned H2D of the field and the
-map gradients — the latter on a copy stream overlapping the compute of earlier views — and
-D2H of the gradients) inside the timed region.  `--impl reference` times the
+map gradients — deformation and maps on a copy stream overlapping the prefilter and the
+compute of earlier views — and D2H of the step's loss pair) inside the timed region.  `--impl reference` times the
 reference's CPU implementation (oracle/: the reference's own Cython kernels built from
 /root/reference into oracle/_ref when present, else the plain-C restatement) on the host.
 """
@@ -297,33 +297,37 @@ def run_gpu(args):
     h_maps = {vi: [m.normal.cpu().pin_memory(), m.depth.cpu().pin_memory(), m.opacity.cpu().pin_memory()]
               for vi, m in dmaps.items()}
     d_maps = {vi: ts.RenderMaps.empty(S, S, device=dev) for vi in views}
-    h_grad = torch.empty_like(step.grads.d_vert, device="cpu").pin_memory()
+    h_loss = torch.empty(2, dtype=torch.float64).pin_memory()  # the step's losses (eikonal, NC)
     h2d = h_sdf.numel() * 8 + h_def.numel() * 8 + sum(sum(t.numel() * 4 for t in v) for v in h_maps.values())
-    d2h = h_grad.numel() * 4
+    d2h = h_loss.numel() * 8
 
-    # The field is copied on the compute stream (the first kernel needs it); the per-view map
-    # gradients stream in on a copy stream, one event per view, so view i's copy overlaps the
-    # compute of the views before it.  The copy stream first waits for the previous step's
-    # consumers of the buffers it overwrites.
+    # The SDF is copied on the compute stream (the prefilter needs only it); the deformation and
+    # the per-view map gradients stream in on a copy stream — the deformation overlapping the
+    # prefilter, view i's maps overlapping the compute of the views before it (one event each).
+    # The copy stream first waits for the previous step's consumers of the buffers it overwrites.
+    # The step's result read back to the host is its loss pair.
     copy_stream = torch.cuda.Stream(device=dev)
     view_ready = {vi: torch.cuda.Event() for vi in views}
+    deform_ready = torch.cuda.Event()
 
     def maps_for(vi, m):
         torch.cuda.current_stream().wait_event(view_ready[vi])
         return d_maps[vi]
 
     def e2e_step():
-        field.sdf.copy_(h_sdf, non_blocking=True)
-        field.deformation.copy_(h_def, non_blocking=True)
         copy_stream.wait_stream(torch.cuda.current_stream())
+        field.sdf.copy_(h_sdf, non_blocking=True)
         with torch.cuda.stream(copy_stream):
+            field.deformation.copy_(h_def, non_blocking=True)
+            deform_ready.record(copy_stream)
             for vi in views:
                 d_maps[vi].normal.copy_(h_maps[vi][0], non_blocking=True)
                 d_maps[vi].depth.copy_(h_maps[vi][1], non_blocking=True)
                 d_maps[vi].opacity.copy_(h_maps[vi][2], non_blocking=True)
                 view_ready[vi].record(copy_stream)
-        grads = step(s, views, maps_for)
-        h_grad.copy_(grads.d_vert, non_blocking=True)
+        step(s, views, maps_for, inputs_ready=deform_ready)
+        h_loss[0:1].copy_(step.eik_loss, non_blocking=True)
+        h_loss[1:2].copy_(step.nc_loss, non_blocking=True)
 
     e2e_step()
     barrier()

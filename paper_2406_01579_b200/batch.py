@@ -103,7 +103,9 @@ class FitStep:
         self.reg_stream = torch.cuda.Stream(device=dev)
         self._pool = ThreadPoolExecutor(max_workers=n) if n > 1 else None
 
-    def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None):
+    def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None, inputs_ready=None):
+        """`inputs_ready`: optional CUDA event after which the deformation is valid (the SDF
+        must be valid on the current stream); everything but the prefilter waits for it."""
         g, f, cfg = self.grid, self.field, self.cfg
         self.grads.d_vert.zero_()
         active = prefilter(g, f, s)
@@ -114,6 +116,8 @@ class FitStep:
         main = torch.cuda.current_stream()
         for st in self.streams + [self.reg_stream]:
             st.wait_stream(main)  # zeroed gradients, prefilter output
+            if inputs_ready is not None:
+                st.wait_event(inputs_ready)
             active.record_stream(st)
         # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce);
         # they depend only on the field, so they run on their own stream beside the views
@@ -157,6 +161,8 @@ class FitStep:
                     stats.pairs.append(M)
         for st in self.streams + [self.reg_stream]:
             main.wait_stream(st)
+        if inputs_ready is not None:
+            main.wait_event(inputs_ready)
         allreduce_gradients(self.grads, self.group)
         if self.opt is not None:
             self.opt.step([f.sdf, f.deformation], [self.grads.d_sdf, self.grads.d_deform])
