@@ -446,9 +446,14 @@ struct RectTab {
 struct Prefetch {
   SplatRec raw[kCh];
   int32_t idx[kCh];
+  int64_t ib0;  // item_off of the next chunk's first list position
 };
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -458,10 +463,12 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// list entries [pos, pos + min(kCh, avail)) -> P.idx
-__device__ __forceinline__ void prefetch_idx(Prefetch& P, const int32_t* __restrict__ list, int pos, int avail) {
+// list entries [pos, pos + min(kCh, avail)) -> P.idx, item_off_tile[pos] -> P.ib0
+__device__ __forceinline__ void prefetch_idx(Prefetch& P, const int32_t* __restrict__ list,
+                                             const int64_t* __restrict__ item_off_tile, int pos, int avail) {
   const int t = threadIdx.x;
   if (t < min(kCh, avail)) cp_async4(&P.idx[t], list + pos + t);
+  if (t == 0 && avail > 0) cp_async8(&P.ib0, item_off_tile + pos);
   cp_async_commit();
 }
 // records of the prefetched list entries -> P.raw
@@ -532,9 +539,9 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
   if (t == 0) {
     R.pre[0] = 0;
     R.n = n;
-    R.ib0 = item_off_tile[base];
+    R.ib0 = P.ib0;
   }
-  prefetch_idx(P, list, base + n, avail - n);
+  prefetch_idx(P, list, item_off_tile, base + n, avail - n);
 }
 
 
@@ -616,7 +623,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
   }
   if (threadIdx.x < kCh) {
-    prefetch_idx(F.pf, list, 0, L);
+    prefetch_idx(F.pf, list, item_off + lo, 0, L);
     prefetch_rec(F.pf, recs, L);
   }
   for (int base = 0; base < L;) {
@@ -875,10 +882,6 @@ struct BwdSmem {
   int maxproc, nitems;
 };
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
 
 // One warp, items [b0, b0 + m) of the chunk: face-hit backward of every item into its row,
 // then per run of equal splat (items are in pair order, i.e. grouped by splat) one lane per
@@ -992,7 +995,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   P.zero();
   if (ptime) pacc[7] = clock64();
   if (threadIdx.x < kCh) {
-    prefetch_idx(S.pf, list, 0, maxproc);
+    prefetch_idx(S.pf, list, item_off + lo, 0, maxproc);
     prefetch_rec(S.pf, recs, maxproc);
   }
   for (int base = 0; base < maxproc;) {
