@@ -166,13 +166,11 @@ struct Hit {
   int fip, fin;
 };
 
-// 0: no hit, 1: hit, 2: undecided in FP32 (caller takes the exact FP64 path).
-// Branch-free over the four faces so a warp of different pixels never diverges here.
-__device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hit& h) {
+// Phase A1: the faces that certainly contain the pixel (bits 0-3); bit 4 = undecided (within
+// the band of a face edge, or a splat with a sign-uncertain face).  Same tests as eval_hits.
+__device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float py) {
   const float band = s.band;
-  bool amb = (s.flags & 16u) != 0;
-  int nh = 0, lo = -1, hi = -1;
-  float zlo = 0.f, zhi = 0.f, flo = 0.f, fhi = 0.f;
+  uint32_t m = s.flags & 16u;
 #pragma unroll
   for (int fi = 0; fi < 4; ++fi) {
     const float u = fmaf(s.eux[fi], px, fmaf(s.euy[fi], py, s.cu[fi]));
@@ -181,29 +179,35 @@ __device__ __forceinline__ int eval_hits(const Staged& s, float px, float py, Hi
     const bool valid = (s.flags >> fi) & 1u;
     const bool out = !valid || u < -band || v < -band || w < -band;
     const bool in = !out && u > band && v > band && w > band;
-    amb |= !out && !in;
-    const int ia = face_vert(fi, 0), ib = face_vert(fi, 1), ic = face_vert(fi, 2);
+    m |= in ? (1u << fi) : 0u;
+    m |= (!out && !in) ? 16u : 0u;
+  }
+  return m;
+}
+
+// Phase A2: entry / exit among the in-faces of mask m (face order, first hit seeds, strict
+// < / > updates — eval_hits' rule), recomputing each in-face's values bit-identically.
+__device__ __forceinline__ void hit_faces(const Staged& s, float px, float py, uint32_t m, Hit& h) {
+  int nh = 0, lo = -1, hi = -1;
+  float zlo = 0.f, zhi = 0.f, flo = 0.f, fhi = 0.f;
+  for (uint32_t mm = m & 15u; mm; mm &= mm - 1u) {
+    const int fi = __ffs(mm) - 1;
+    const float u = fmaf(s.eux[fi], px, fmaf(s.euy[fi], py, s.cu[fi]));
+    const float v = fmaf(s.evx[fi], px, fmaf(s.evy[fi], py, s.cv[fi]));
+    const float w = s.adet[fi] - u - v;
+    const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
     const float wa = w * s.iz[ia], wb = u * s.iz[ib], wc = v * s.iz[ic];
     const float rD = frcp(wa + wb + wc);
     const float zp = s.adet[fi] * rD;
     const float fh = (wa * s.df[ia] + wb * s.df[ib] + wc * s.df[ic]) * rD;
-    const bool first = in && nh == 0;
-    const bool nlo = in && (first || zp < zlo), nhi = in && (first || zp > zhi);
-    zlo = nlo ? zp : zlo;
-    flo = nlo ? fh : flo;
-    lo = nlo ? fi : lo;
-    zhi = nhi ? zp : zhi;
-    fhi = nhi ? fh : fhi;
-    hi = nhi ? fi : hi;
-    nh += in ? 1 : 0;
+    if (nh == 0 || zp < zlo) { zlo = zp; flo = fh; lo = fi; }
+    if (nh == 0 || zp > zhi) { zhi = zp; fhi = fh; hi = fi; }
+    ++nh;
   }
-  if (amb) return 2;
-  if (nh < 2) return 0;
   h.fp = flo;
   h.fn = fhi;
   h.fip = lo;
   h.fin = hi;
-  return 1;
 }
 
 __device__ __forceinline__ float sigmoidf_stable(float x) {
@@ -326,10 +330,11 @@ __device__ __forceinline__ bool exact_group(const Scene64& S, bool act, int64_t 
 
 // FP32 fast path with error-bounded decisions: 0 no blend, 1 blend (b filled), 2 the pair
 // lies within the error bound of a decision threshold and needs the exact re-decision.
-__device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, float s, Blend& b) {
+__device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, float s, uint32_t m, Blend& b) {
   Hit h;
-  const int e = eval_hits(r, px, py, h);
+  const int e = (m & 16u) ? 2 : (__popc(m) < 2 ? 0 : 1);
   if (e == 0) return 0;
+  if (e == 1) hit_faces(r, px, py, m, h);
   if (e == 1) {
     const float dfl = h.fp - h.fn;  // f_prev - f_next, f0 cancels exactly
     const float ftol = r.fband * frcp(fminf(r.adet[h.fip], r.adet[h.fin])) + r.ftol0;
@@ -567,6 +572,8 @@ struct FwdSmem {
   float col[kCh][3];
   uint32_t skip[TS_TILE_PX / 32];
   uint16_t exq[kCap];  // pairs queued for the exact FP64 re-decision
+  uint16_t cand[kWarps][64];  // per warp: candidate pairs (it | face mask << 11) of phase A1
+  uint32_t cbits[kCap / 32];  // the chunk's blend bits (pair index within the chunk)
   int nex;
   unsigned npairs;  // diagnostics: pairs evaluated by phase A
   RectTab R;
@@ -574,14 +581,38 @@ struct FwdSmem {
   long long phase[8];  // diagnostics (flag bit 2)
 };
 
-// record one blending pair: shared code + blend bit (forward phase B), global pair record
-// (backward); the caller sets the pair's bit in pair_bits
+// record one blending pair: shared code + blend bit (forward phase B), the chunk's blend-bit
+// word (flushed to pair_bits after the exact re-decisions), global pair record (backward)
 __device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, const Blend& b, int64_t ib0,
                                          float4* __restrict__ pair_rec) {
   const float2 c = encode(true, b);
   F.code[it] = c;
   mask_set(&F.bmask[q], j);
+  atomicOr(&F.cbits[it >> 5], 1u << (it & 31));
   pair_rec[ib0 + it] = make_float4(c.x, c.y, pack_face(b.sp, b.fip), pack_face(b.sn, b.fin));
+}
+
+// Phase A2 for one warp: candidates cq[0, m) (pair | face mask << 11), one per lane.
+__device__ __forceinline__ void a2_candidates(FwdSmem& F, const uint16_t* cq, int m, const Scene64& S64, float s,
+                                              int ty0, int tx0, int64_t ib0, float4* __restrict__ pair_rec) {
+  const int lane = threadIdx.x & 31;
+  if (lane < m) {
+    const uint32_t c = cq[lane];
+    const int itc = (int)(c & 2047u);
+    const int j = pair_splat(F.R, itc);
+    int px_, py_;
+    pair_pixel(F.R, j, itc, px_, py_);
+    const Staged& r = F.sh[j];
+    Blend b;
+    const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, c >> 11, b);
+    if (e == 2) {
+      F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)itc;
+      prefetch_exact(S64, r.k);
+    } else if (e == 1) {
+      put_pair(F, itc, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
+    }
+  }
+  __syncwarp();
 }
 
 template <bool COLOR>
@@ -630,39 +661,52 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     if (threadIdx.x < kCh)
       stage_chunk(list, base, L - base, F.pf, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
     F.bmask[pix] = 0ull;
+    if (threadIdx.x < kCap / 32) F.cbits[threadIdx.x] = 0u;
     if (threadIdx.x == 0) F.nex = 0;
     __syncthreads();
     TS_PHASE(0);
     const int n = F.R.n, total = F.R.pre[n];
     const int64_t ib0 = F.R.ib0;
     // ---- A: pair-parallel hit + opacity (FP32, error-bounded) ------------------------------
-    for (int it0 = threadIdx.x & ~31; it0 < total; it0 += TS_TILE_PX) {
-      const int it = it0 + (threadIdx.x & 31);
-      bool bl = false, ev = false;
-      if (it < total) {
-        const int j = pair_splat(F.R, it);
-        int px_, py_;
-        pair_pixel(F.R, j, it, px_, py_);
-        const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
-        if (!((F.skip[q >> 5] >> (q & 31)) & 1u)) {
-          ev = true;
-          const Staged& r = F.sh[j];
-          Blend b;
-          const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, b);
-          if (e == 2) {
-            F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)it;
-            prefetch_exact(S64, r.k);
-          } else if (e == 1) {
-            put_pair(F, it, j, q, b, ib0, pair_rec);
-            bl = true;
+    //  A1: face containment of every pair (dense lanes); the pairs inside >= 2 faces or within
+    //      a band are compacted per warp;  A2: 32 candidates at a time, all lanes busy: entry /
+    //      exit interpolation and opacity.  About half of the rectangle pairs miss the splat.
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      uint16_t* cq = F.cand[warp];
+      int cnt = 0;
+      for (int it0 = warp * 32; it0 < total; it0 += TS_TILE_PX) {
+        const int it = it0 + lane;
+        bool ev = false, cand = false;
+        uint32_t fm = 0;
+        if (it < total) {
+          const int j = pair_splat(F.R, it);
+          int px_, py_;
+          pair_pixel(F.R, j, it, px_, py_);
+          const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
+          if (!((F.skip[q >> 5] >> (q & 31)) & 1u)) {
+            ev = true;
+            const Staged& r = F.sh[j];
+            fm = face_mask(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f);
+            cand = (fm & 16u) || __popc(fm) >= 2;
           }
         }
+        const unsigned cm = __ballot_sync(0xffffffffu, cand), em = __ballot_sync(0xffffffffu, ev);
+        if (lane == 0) atomicAdd(&F.npairs, __popc(em));
+        if (cand) cq[cnt + __popc(cm & ((1u << lane) - 1u))] = (uint16_t)(it | (fm << 11));
+        cnt += __popc(cm);
+        __syncwarp();
+        if (cnt >= 32) {
+          a2_candidates(F, cq, 32, S64, s, ty0, tx0, ib0, pair_rec);
+          const int rest = cnt - 32;
+          const uint16_t moved = lane < rest ? cq[32 + lane] : 0;
+          __syncwarp();
+          if (lane < rest) cq[lane] = moved;
+          cnt = rest;
+          __syncwarp();
+        }
       }
-      const unsigned bm = __ballot_sync(0xffffffffu, bl), em = __ballot_sync(0xffffffffu, ev);
-      if ((threadIdx.x & 31) == 0) {
-        if (bm) set_bits(pair_bits, ib0 + it0, bm);
-        atomicAdd(&F.npairs, __popc(em));
-      }
+      if (cnt > 0) a2_candidates(F, cq, cnt, S64, s, ty0, tx0, ib0, pair_rec);
     }
     if (threadIdx.x < kCh) prefetch_rec(F.pf, recs, L - base - n);
     __syncthreads();
@@ -677,13 +721,16 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       pair_pixel(F.R, j, it, px_, py_);
       Blend b;
       const bool bl = exact_group(S64, act, F.sh[j].k, px_, py_, s64, b);
-      if (act && bl && (threadIdx.x & 3) == 0) {
+      if (act && bl && (threadIdx.x & 3) == 0)
         put_pair(F, it, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
-        atomicOr(pair_bits + ((ib0 + it) >> 5), 1u << ((ib0 + it) & 31));
-      }
     }
     __syncthreads();
     TS_PHASE(2);
+    // the chunk's blend bits into the view's bit array (words at the chunk ends are shared)
+    if (threadIdx.x < (total + 31) / 32) {
+      const uint32_t wbits = F.cbits[threadIdx.x];
+      if (wbits) set_bits(pair_bits, ib0 + 32 * threadIdx.x, wbits);
+    }
     if (ptime) {  // chunks, chunks with re-decisions, re-decided pairs, max per chunk
       pacc[4] += 1;
       pacc[5] += F.nex > 0;
