@@ -617,7 +617,7 @@ __device__ __forceinline__ void a2_candidates(FwdSmem& F, const uint16_t* cq, in
 
 template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
-    const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
+    const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, const int64_t* __restrict__ item_off,
     uint32_t* __restrict__ pair_bits, float4* __restrict__ pair_rec, float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     for (int k = 0; k < 7; ++k) pacc[k] = 0;
     pacc[7] = clock64();
   }
-  const int tile = blockIdx.x;
+  const int tile = torder[blockIdx.x];  // longest lists first (k_tile_order)
   const bool timing = (g_ts_debug_flags & 2) && tile < 65536;
   if (timing && threadIdx.x == 0) {
     g_ts_tile_time[2 * tile] = gtimer();
@@ -855,6 +855,39 @@ __global__ void __launch_bounds__(256) k_window(int T, const int64_t* __restrict
   }
 }
 
+// Launch order of the compositing CTAs: tiles by decreasing list length (16-entry buckets),
+// so the long tiles start first and the short ones fill the tail (results do not depend on
+// the order).  One CTA, shared-memory counting sort.
+__global__ void __launch_bounds__(1024) k_tile_order(int T, const int64_t* __restrict__ starts,
+                                                    int32_t* __restrict__ order) {
+  __shared__ int cnt[1024];
+  __shared__ int wsum[32];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  auto bucket = [&](int t) {
+    const int64_t L = starts[t + 1] - starts[t];
+    return 1023 - (int)(L >> 4 < 1023 ? L >> 4 : 1023);
+  };
+  for (int t = threadIdx.x; t < T; t += 1024) atomicAdd(&cnt[bucket(t)], 1);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = cnt[threadIdx.x];
+  int v = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) wsum[w] = v;
+  __syncthreads();
+  int off = 0;
+  for (int k = 0; k < w; ++k) off += wsum[k];
+  __syncthreads();
+  cnt[threadIdx.x] = off + v - c;  // exclusive offset of the bucket
+  __syncthreads();
+  for (int t = threadIdx.x; t < T; t += 1024) order[atomicAdd(&cnt[bucket(t)], 1)] = t;
+}
+
 // pairs per list position: |pixel rectangle of the splat  ∩  tile|
 __global__ void k_item_counts(int T, int tiles_x, const int64_t* __restrict__ starts,
                               const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
@@ -991,7 +1024,7 @@ __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, 
 
 template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
-    const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
+    const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     int tiles_x, int W, int H, const int64_t* __restrict__ item_off, const uint32_t* __restrict__ pair_bits,
     const float4* __restrict__ pair_rec, const float* __restrict__ normal_map,
@@ -1005,7 +1038,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   long long* pacc = S.phase;
   if (ptime)
     for (int k = 0; k < 7; ++k) pacc[k] = 0;
-  const int tile = blockIdx.x;
+  const int tile = torder[blockIdx.x];  // longest lists first (k_tile_order)
   const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
   const int pix = threadIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
@@ -1320,14 +1353,18 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
     cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
+  int32_t* torder = nullptr;
+  cudaMallocAsync(&torder, sizeof(int32_t) * T, st);
+  k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   if (colors && cmap)
-    k_forward<true><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
+    k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
                                                 W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
                                                 nmap, dmap, omap, cmap, n_proc, n_blend);
   else
-    k_forward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
+    k_forward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
                                                  tiles_x, W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
                                                  nmap, dmap, omap, nullptr, n_proc, n_blend);
+  cudaFreeAsync(torder, st);
 }
 
 void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, int64_t K, const SplatRec* rec,
@@ -1345,15 +1382,18 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
     attr = true;
   }
   float* rows = nullptr;
+  int32_t* torder = nullptr;
   cudaMallocAsync(&rows, sizeof(float) * kGr * (size_t)M, st);
+  cudaMallocAsync(&torder, sizeof(int32_t) * T, st);
+  k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
-    k_backward<true><<<T, TS_TILE_PX, smem_c, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
+    k_backward<true><<<T, TS_TILE_PX, smem_c, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                  maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
                                                  dmaps[3], n_proc, rows);
   else
-    k_backward<false><<<T, TS_TILE_PX, smem, st>>>(b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
+    k_backward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
                                                   cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                   maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
                                                   nullptr, n_proc, rows);
@@ -1366,6 +1406,7 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
     k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
                                            make_grid(R), cam, d_vert, nullptr);
   cudaFreeAsync(rows, st);
+  cudaFreeAsync(torder, st);
 }
 
 void ts_impl_counters(unsigned long long out[4], int reset) {
