@@ -948,7 +948,7 @@ struct BwdSmem {
   Staged sh[kCh];
   float2 wg[kCap];      // load: (alpha, 1-alpha); phase B: (w = T a, G); +0 bits = not an item
   float acc[kCh][AS];   // per-(tile, splat) gradient rows of the chunk
-  float col[kCh][3];
+  float col[COLOR ? kCh : 1][3];  // colour variant only
   union {
     ChunkMask bmask[TS_TILE_PX];  // load + B: per pixel, chunk splats that blend (bit j)
     float rows[kWarps][32][RS];   // C: per-item rows of each warp's batch
@@ -961,6 +961,12 @@ struct BwdSmem {
   long long phase[8];  // diagnostics (flag bit 2)
   int maxproc, nitems;
 };
+
+// occupancy the launch bounds assume (228 KB shared memory per SM, 1 KB reserved per CTA)
+static_assert(4 * (sizeof(FwdSmem) + 1024) <= 228 * 1024, "forward: 4 CTAs per SM");
+static_assert(3 * (sizeof(BwdSmem<false>) + 1024) <= 228 * 1024, "backward: 3 CTAs per SM");
+
+
 
 
 // One warp, items [b0, b0 + m) of the chunk: face-hit backward of every item into its row,
