@@ -909,7 +909,7 @@ __global__ void k_item_counts(int T, int tiles_x, const int64_t* __restrict__ st
 
 // backward of one face hit (_core.pyx:295-341) accumulated into an item row (shared memory,
 // per-vertex slots: [0,4) d_f, [4,8) d_depth, [8,12) d_px, [12,16) d_py)
-__device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, float px, float py, float g) {
+__device__ __forceinline__ void face_bwd(float (&acc)[16], const Staged& r, int fi, float px, float py, float g) {
   const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
   const float inv_ad = frcp(r.adet[fi]);
   const float eux = r.eux[fi], euy = r.euy[fi], evx = r.evx[fi], evy = r.evy[fi];
@@ -921,23 +921,25 @@ __device__ __forceinline__ void face_bwd(float* row, const Staged& r, int fi, fl
   const float w0 = wbar * iza, w1 = u * izb, w2 = v * izc;
   const float iS = frcp(w0 + w1 + w2);
   const float fh = (w0 * fa + w1 * fb + w2 * fc) * iS;
-  row[ia] += g * w0 * iS;
-  row[ib] += g * w1 * iS;
-  row[ic] += g * w2 * iS;
   const float dw0 = g * (fa - fh) * iS, dw1 = g * (fb - fh) * iS, dw2 = g * (fc - fh) * iS;
-  row[4 + ia] += dw0 * (-w0 * iza);
-  row[4 + ib] += dw1 * (-w1 * izb);
-  row[4 + ic] += dw2 * (-w2 * izc);
   const float gu = -dw0 * iza + dw1 * izb;
   const float gv = -dw0 * iza + dw2 * izc;
   const float qx = (eux * gu + evx * gv) * inv_ad;
   const float qy = (euy * gu + evy * gv) * inv_ad;
-  row[8 + ia] -= qx * wbar;
-  row[12 + ia] -= qy * wbar;
-  row[8 + ib] -= qx * u;
-  row[12 + ib] -= qy * u;
-  row[8 + ic] -= qx * v;
-  row[12 + ic] -= qy * v;
+  // per face vertex (a, b, c): d f, d depth, d px, d py
+  const float c[4][3] = {{g * w0 * iS, g * w1 * iS, g * w2 * iS},
+                         {dw0 * (-w0 * iza), dw1 * (-w1 * izb), dw2 * (-w2 * izc)},
+                         {-qx * wbar, -qx * u, -qx * v},
+                         {-qy * wbar, -qy * u, -qy * v}};
+  // scatter to the tet's vertex slots (face fi omits vertex fi) with selects, so the
+  // accumulators stay in registers
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    acc[4 * q + 0] += fi == 0 ? 0.f : c[q][0];
+    acc[4 * q + 1] += fi == 0 ? c[q][0] : (fi == 1 ? 0.f : c[q][1]);
+    acc[4 * q + 2] += fi <= 1 ? c[q][1] : (fi == 2 ? 0.f : c[q][2]);
+    acc[4 * q + 3] += fi == 3 ? 0.f : c[q][2];
+  }
 }
 
 template <bool COLOR>
@@ -993,8 +995,6 @@ __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, 
     const int64_t p = (int64_t)yi * W + xi;
     const float2 wg = S.wg[it];
     const float w = wg.x, G = wg.y;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) row[i] = 0.f;
     row[16] = __ldg(d_normal + p * 3) * w;
     row[17] = __ldg(d_normal + p * 3 + 1) * w;
     row[18] = __ldg(d_normal + p * 3 + 2) * w;
@@ -1004,12 +1004,17 @@ __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, 
       row[21] = __ldg(d_color + p * 3 + 1) * w;
       row[22] = __ldg(d_color + p * 3 + 2) * w;
     }
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
     if (G != 0.f) {
       const float2 sg = __ldg(reinterpret_cast<const float2*>(pair_rec + ib0 + it) + 1);
       const float px = (float)(xi - r.rx0) + 0.5f, py = (float)(yi - r.ry0) + 0.5f;
-      face_bwd(row, r, face_of(sg.x), px, py, G * sg.x);
-      face_bwd(row, r, face_of(sg.y), px, py, -G * sg.y);
+      face_bwd(acc, r, face_of(sg.x), px, py, G * sg.x);
+      face_bwd(acc, r, face_of(sg.y), px, py, -G * sg.y);
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) row[i] = acc[i];
   }
   const int jprev = __shfl_up_sync(0xffffffffu, jl, 1);
   unsigned heads = __ballot_sync(0xffffffffu, lane < m && (lane == 0 || jl != jprev));
