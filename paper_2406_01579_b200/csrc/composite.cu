@@ -379,7 +379,6 @@ __device__ __forceinline__ float2 encode(bool blended, const Blend& b) {
   if (b.clipped) return make_float2(kAlphaClipF, -kOneMinusClipF);
   return make_float2(b.a > 0.f ? b.a : -0.f, b.om);
 }
-__device__ __forceinline__ bool code_blends(float a) { return __float_as_uint(a) != 0u; }
 
 // Pair records of the view (item space, written by the forward, read by the backward):
 //   pair_bits[g >> 5] bit (g & 31): pair g blends (cleared before the forward);
@@ -948,7 +947,7 @@ struct BwdSmem {
   static constexpr int RS = COLOR ? 25 : 21;  // odd item-row stride: conflict-free per-lane rows
   static constexpr int AS = COLOR ? 24 : 20;  // accumulator row stride (whole float4s)
   Staged sh[kCh];
-  float2 wg[kCap];      // load: (alpha, 1-alpha); phase B: (w = T a, G); +0 bits = not an item
+  float2 wg[kCap];      // items only — load: (alpha, 1-alpha); phase B: (w = T a, G)
   float acc[kCh][AS];   // per-(tile, splat) gradient rows of the chunk
   float col[COLOR ? kCh : 1][3];  // colour variant only
   union {
@@ -957,6 +956,7 @@ struct BwdSmem {
   } u;
   uint32_t items[kCap];  // C: the chunk's items (j << 16 | pair) in pair order
   int wcnt[kCap / 32];   // items per 32-pair block -> exclusive offsets
+  uint32_t lbits[kCap / 32];  // loaded (blending, not early-stopped) pairs, block k*8+warp
   int lim[TS_TILE_PX];   // per pixel: list entries the forward consumed (n_proc)
   RectTab R;
   Prefetch pf;
@@ -1123,9 +1123,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
               bl = true;
             }
           }
-          if (!bl && it < total) S.wg[it] = make_float2(0.f, 0.f);
           const unsigned bm = __ballot_sync(0xffffffffu, bl);
-          if (lane == 0) S.wcnt[k * kWarps + warp] = __popc(bm);
+          if (lane == 0) {
+            S.wcnt[k * kWarps + warp] = __popc(bm);
+            S.lbits[k * kWarps + warp] = bm;
+          }
         }
       }
     }
@@ -1180,8 +1182,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     for (int k = 0; k < kCap / TS_TILE_PX; ++k) {
       if (k < nblk) {
         const int it = threadIdx.x + k * TS_TILE_PX;
-        const bool has = it < total && code_blends(S.wg[it].x);
-        const unsigned bm = __ballot_sync(0xffffffffu, has);
+        const unsigned bm = S.lbits[k * kWarps + warp];
+        const bool has = (bm >> lane) & 1u;
         if (has)
           S.items[S.wcnt[k * kWarps + warp] + __popc(bm & ((1u << lane) - 1u))] =
               ((uint32_t)pair_splat(S.R, it) << 16) | (uint32_t)it;
