@@ -169,8 +169,10 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
 }
 
 // Long tiles (2048 < L <= 16384), listed by k_long_tiles: persistent 1024-thread CTAs walk the
-// list and sort each tile with a shared-memory LSD radix sort (8-bit digits) on the key
-// (q, splat): ceil(splat bits / 8) passes over the splat index, then four over q.  Each
+// list and sort each tile with a shared-memory LSD radix sort (8-bit digits) on q (four
+// passes), then order each run of equal q by splat index in place (runs are short; a tile
+// with a run longer than 64 is re-sorted on the full key: ceil(splat bits / 8) passes over
+// the splat index, then four over q).  Each
 // warp owns a striped slab of E * 32 elements (slot e of lane l at w*32E + e*32 + l, so warp
 // order is (e, lane) = position order and the sort is stable); ranks inside a warp come from
 // __match_any_sync peers and per-warp digit counters, offsets from a digit-major scan of the
@@ -257,6 +259,8 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     const int64_t* __restrict__ splat_off, const double* __restrict__ md, int32_t* __restrict__ items,
     int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono, int cap, int passes_lo) {
   extern __shared__ uint32_t sm32[];
+  constexpr int kMaxRun = 64;
+  __shared__ int longrun;
   uint32_t* kq = sm32;
   uint32_t* kv = sm32 + cap;
   uint32_t* H = sm32 + 2 * cap;
@@ -273,14 +277,43 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
       kq[i] = (uint32_t)(k >> 32);
       kv[i] = (uint32_t)k;
     }
-    if (threadIdx.x == 0) bad = 0;
+    if (threadIdx.x == 0) {
+      bad = 0;
+      longrun = 0;
+    }
     __syncthreads();
-    if (P == 4096)
-      radix_sort_tile<4>(kq, kv, H, dbase, passes_lo);
-    else if (P == 8192)
-      radix_sort_tile<8>(kq, kv, H, dbase, passes_lo);
-    else
-      radix_sort_tile<16>(kq, kv, H, dbase, passes_lo);
+    // the four q digits only; equal-q runs (rare, short) are then ordered by splat index
+    // in place, and a tile with a run longer than kMaxRun is re-sorted on the full key
+    for (int full = 0; full < 2; ++full) {
+      const int plo = full ? passes_lo : 0;
+      if (P == 4096)
+        radix_sort_tile<4>(kq, kv, H, dbase, plo);
+      else if (P == 8192)
+        radix_sort_tile<8>(kq, kv, H, dbase, plo);
+      else
+        radix_sort_tile<16>(kq, kv, H, dbase, plo);
+      if (full) break;
+      for (int i = threadIdx.x; i < L; i += kRadixThreads) {
+        if (i > 0 && kq[i - 1] == kq[i]) continue;  // not a run start
+        int e = i + 1;
+        while (e < L && kq[e] == kq[i] && e - i <= kMaxRun) ++e;
+        if (e - i > kMaxRun) {
+          longrun = 1;
+          continue;
+        }
+        for (int a = i + 1; a < e; ++a) {  // insertion sort of the run by splat index
+          const uint32_t x = kv[a];
+          int b = a - 1;
+          while (b >= i && kv[b] > x) {
+            kv[b + 1] = kv[b];
+            --b;
+          }
+          kv[b + 1] = x;
+        }
+      }
+      __syncthreads();
+      if (!longrun) break;
+    }
     int mybad = 0;
     for (int i = threadIdx.x; i < L; i += kRadixThreads) {
       emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
