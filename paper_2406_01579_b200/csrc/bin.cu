@@ -150,24 +150,6 @@ __device__ __forceinline__ void sort_tile(uint64_t* s, int& bad, int t, const in
   if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
 }
 
-// one CTA per tile; handles the tiles with 0 < L <= cap
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, const int64_t* __restrict__ starts,
-                                                            const uint64_t* __restrict__ keys, int tiles_x,
-                                                            const BinRec* __restrict__ br,
-                                                            const int64_t* __restrict__ splat_off,
-                                                            const double* __restrict__ md,
-                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                            uint8_t* __restrict__ nonmono) {
-  extern __shared__ uint64_t s[];
-  __shared__ int bad;
-  const int t = blockIdx.x;
-  if (t >= T) return;
-  const int64_t L = starts[t + 1] - starts[t];
-  if (L <= 0 || L > cap) return;
-  sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
-}
-
 // Long tiles (2048 < L <= 16384), listed by k_long_tiles: persistent 1024-thread CTAs walk the
 // list and sort each tile with a shared-memory LSD radix sort (8-bit digits) on q (four
 // passes), then order each run of equal q by splat index in place (runs are short; a tile
@@ -180,16 +162,17 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
 constexpr int kRadixThreads = 1024;
 constexpr int kRadixWarps = kRadixThreads / 32;
 
-template <int E>
+template <int NT, int E>
 __device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint32_t* H, uint32_t* dbase,
                                                 int passes_lo) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int base = w * 32 * E + lane;
   const unsigned lt = (1u << lane) - 1u;
   for (int pass = 0; pass < passes_lo + 4; ++pass) {
     const bool hi = pass >= passes_lo;
     const int shift = (hi ? pass - passes_lo : pass) * 8;
-    for (int i = threadIdx.x; i < kRadixWarps * 256; i += kRadixThreads) H[i] = 0u;
+    for (int i = threadIdx.x; i < NW * 256; i += NT) H[i] = 0u;
     uint32_t q[E], v[E], rk[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -213,7 +196,7 @@ __device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint
     if (threadIdx.x < 256) {
       const int d = threadIdx.x;
       uint32_t run = 0;
-      for (int ww = 0; ww < kRadixWarps; ++ww) {
+      for (int ww = 0; ww < NW; ++ww) {
         const uint32_t c = H[ww * 256 + d];
         H[ww * 256 + d] = run;
         run += c;
@@ -253,13 +236,97 @@ __device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint
   }
 }
 
+// Sort P = NT * E keys (q, splat) held as kq / kv in shared memory (L valid, the rest padded
+// with ~0): four radix passes on q, then each run of equal q is ordered by splat index in
+// place; a run longer than kMaxRun triggers a re-sort on the full key.  `flag` is a shared
+// scratch int.
+template <int NT, int MAXE>
+__device__ __forceinline__ void radix_sort_keys(uint32_t* kq, uint32_t* kv, uint32_t* H, uint32_t* dbase, int P,
+                                                int L, int passes_lo, int& flag) {
+  constexpr int kMaxRun = 64;
+  if (threadIdx.x == 0) flag = 0;
+  for (int full = 0; full < 2; ++full) {
+    const int plo = full ? passes_lo : 0;
+    if (P == 4 * NT)
+      radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo);
+    else if (MAXE == 8 || P == 8 * NT)
+      radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo);
+    else
+      radix_sort_tile<NT, MAXE>(kq, kv, H, dbase, plo);
+    if (full) break;
+    for (int i = threadIdx.x; i < L; i += NT) {
+      if (i > 0 && kq[i - 1] == kq[i]) continue;  // not a run start
+      int e = i + 1;
+      while (e < L && kq[e] == kq[i] && e - i <= kMaxRun) ++e;
+      if (e - i > kMaxRun) {
+        flag = 1;
+        continue;
+      }
+      for (int a = i + 1; a < e; ++a) {  // insertion sort of the run by splat index
+        const uint32_t x = kv[a];
+        int b = a - 1;
+        while (b >= i && kv[b] > x) {
+          kv[b + 1] = kv[b];
+          --b;
+        }
+        kv[b + 1] = x;
+      }
+    }
+    __syncthreads();
+    if (!flag) break;
+  }
+}
+
+// one CTA per tile for the tiles with 0 < L <= cap (bitonic up to 512 entries, radix above)
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, int passes_lo,
+                                                            const int64_t* __restrict__ starts,
+                                                            const uint64_t* __restrict__ keys, int tiles_x,
+                                                            const BinRec* __restrict__ br,
+                                                            const int64_t* __restrict__ splat_off,
+                                                            const double* __restrict__ md,
+                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
+                                                            uint8_t* __restrict__ nonmono) {
+  extern __shared__ uint64_t s[];
+  __shared__ int bad, longrun;
+  const int t = blockIdx.x;
+  if (t >= T) return;
+  const int64_t lo = starts[t], L = starts[t + 1] - lo;
+  if (L <= 0 || L > cap) return;
+  if (L <= 512 || cap > 8 * THREADS) {  // short lists: bitonic
+    sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
+    return;
+  }
+  // longer lists: the radix sort of k_tile_sort_long at THREADS threads (kq / kv alias s)
+  uint32_t* kq = reinterpret_cast<uint32_t*>(s);
+  uint32_t* kv = kq + cap;
+  uint32_t* H = kq + 2 * cap;
+  uint32_t* dbase = H + (THREADS / 32) * 256;
+  const int P = L <= 4 * THREADS ? 4 * THREADS : 8 * THREADS;  // cap <= 8 * THREADS
+  for (int i = threadIdx.x; i < P; i += THREADS) {
+    const uint64_t k = i < L ? keys[lo + i] : ~0ull;
+    kq[i] = (uint32_t)(k >> 32);
+    kv[i] = (uint32_t)k;
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  radix_sort_keys<THREADS, 8>(kq, kv, H, dbase, P, (int)L, passes_lo, longrun);
+  int mybad = 0;
+  for (int i = threadIdx.x; i < L; i += THREADS) {
+    emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+    if (i + 1 < L && md[kv[i]] > md[kv[i + 1]]) mybad = 1;
+  }
+  if (mybad) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
+}
+
 __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     const int32_t* __restrict__ tlist, const int64_t* __restrict__ tcount, const int64_t* __restrict__ starts,
     const uint64_t* __restrict__ keys, int tiles_x, const BinRec* __restrict__ br,
     const int64_t* __restrict__ splat_off, const double* __restrict__ md, int32_t* __restrict__ items,
     int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono, int cap, int passes_lo) {
   extern __shared__ uint32_t sm32[];
-  constexpr int kMaxRun = 64;
   __shared__ int longrun;
   uint32_t* kq = sm32;
   uint32_t* kv = sm32 + cap;
@@ -277,43 +344,9 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
       kq[i] = (uint32_t)(k >> 32);
       kv[i] = (uint32_t)k;
     }
-    if (threadIdx.x == 0) {
-      bad = 0;
-      longrun = 0;
-    }
+    if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    // the four q digits only; equal-q runs (rare, short) are then ordered by splat index
-    // in place, and a tile with a run longer than kMaxRun is re-sorted on the full key
-    for (int full = 0; full < 2; ++full) {
-      const int plo = full ? passes_lo : 0;
-      if (P == 4096)
-        radix_sort_tile<4>(kq, kv, H, dbase, plo);
-      else if (P == 8192)
-        radix_sort_tile<8>(kq, kv, H, dbase, plo);
-      else
-        radix_sort_tile<16>(kq, kv, H, dbase, plo);
-      if (full) break;
-      for (int i = threadIdx.x; i < L; i += kRadixThreads) {
-        if (i > 0 && kq[i - 1] == kq[i]) continue;  // not a run start
-        int e = i + 1;
-        while (e < L && kq[e] == kq[i] && e - i <= kMaxRun) ++e;
-        if (e - i > kMaxRun) {
-          longrun = 1;
-          continue;
-        }
-        for (int a = i + 1; a < e; ++a) {  // insertion sort of the run by splat index
-          const uint32_t x = kv[a];
-          int b = a - 1;
-          while (b >= i && kv[b] > x) {
-            kv[b + 1] = kv[b];
-            --b;
-          }
-          kv[b + 1] = x;
-        }
-      }
-      __syncthreads();
-      if (!longrun) break;
-    }
+    radix_sort_keys<kRadixThreads, 16>(kq, kv, H, dbase, P, L, passes_lo, longrun);
     int mybad = 0;
     for (int i = threadIdx.x; i < L; i += kRadixThreads) {
       emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
@@ -430,8 +463,11 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
     k_bin_scatter<<<blocks, 256, 0, st>>>(K, w.br, w.q, tiles_x, starts, w.tile_cnt, keys);
   }
   if (maxL >= 1) {
-    k_tile_sort_smem<256><<<T, 256, 2048 * sizeof(uint64_t), st>>>(T, 2048, starts, keys, tiles_x, w.br, splat_off,
-                                                                   md, items, pos_of, nonmono);
+    int kbits = 1;  // digit passes over the splat index of a full-key sort: ceil(bits(K - 1) / 8)
+    while (kbits < 32 && ((int64_t)1 << kbits) < K) ++kbits;
+    const size_t smem_s = sizeof(uint32_t) * (2 * 2048 + 8 * 256 + 256);  // kq, kv | bitonic u64; H; dbase
+    k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, 2048, (kbits + 7) / 8, starts, keys, tiles_x, w.br, splat_off,
+                                                  md, items, pos_of, nonmono);
     if (maxL > 2048) {
       // the scatter cursor is free again: reuse it as the long-tile list
       cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
@@ -445,8 +481,6 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
         cudaFuncSetAttribute(k_tile_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = smem;
       }
-      int kbits = 1;
-      while (kbits < 32 && ((int64_t)1 << kbits) < K) ++kbits;
       const int per_sm = smem <= 110 * 1024 ? 2 : 1;
       k_tile_sort_long<<<148 * per_sm, kRadixThreads, smem, st>>>(w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br,
                                                                  splat_off, md, items, pos_of, nonmono, cap,
