@@ -112,6 +112,33 @@ inline int64_t* compact(int64_t n, const F& f, int64_t* offs_scratch, cudaStream
   return offs_scratch + nb;
 }
 
+// One item per thread, for functors whose predicate computes state the emission reuses
+// (F::State, pred(i, State&), emit(i, pos, const State&)): the emit pass evaluates once.
+template <class F>
+__global__ void __launch_bounds__(kScanThreads) k_emit_state(int64_t n, F f, const int64_t* __restrict__ offs) {
+  __shared__ int wcnt[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * kScanThreads + threadIdx.x;
+  typename F::State st;
+  const bool p = i < n && f.pred(i, st);
+  const unsigned m = __ballot_sync(0xffffffffu, p);
+  if (lane == 0) wcnt[wid] = __popc(m);
+  __syncthreads();
+  int before = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) before += (w < wid) ? wcnt[w] : 0;
+  if (p) f.emit(i, offs[blockIdx.x] + before + __popc(m & ((1u << lane) - 1u)), st);
+}
+
+template <class F>
+inline int64_t* compact_state(int64_t n, const F& f, int64_t* offs_scratch, cudaStream_t st) {
+  const int64_t nb = (n + kScanThreads - 1) / kScanThreads;
+  if (nb > 0) k_count<F, 1><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
+  k_scan_i64<<<1, 1024, 0, st>>>(offs_scratch, nb);
+  if (nb > 0) k_emit_state<F><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
+  return offs_scratch + nb;
+}
+
 inline int64_t compact_blocks(int64_t n, int ipt = kItemsPerThread) {
   return (n + kScanThreads * ipt - 1) / (kScanThreads * ipt) + 1;
 }

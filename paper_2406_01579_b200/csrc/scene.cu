@@ -72,33 +72,50 @@ struct CullF {
       ymax = py[c] > ymax ? py[c] : ymax;
     }
   }
-  __device__ bool pred(int64_t i) const {
+  // projected tet, kept between the visibility test and the emission (k_emit_state)
+  struct State {
     uint32_t v[4];
     double P[4][3], px[4], py[4], z[4];
-    project4(i, v, P, px, py, z);
+  };
+  __device__ bool visible(const double px[4], const double py[4], const double z[4]) const {
     double dmin, xmin, xmax, ymin, ymax;
     bounds(px, py, z, dmin, xmin, xmax, ymin, ymax);
     return (dmin > cam.near_) && (dmin <= cam.far_) && (xmax >= 0.0) && (xmin <= (double)cam.width) &&
            (ymax >= 0.0) && (ymin <= (double)cam.height);
   }
-  __device__ void emit(int64_t i, int64_t k) const {
-    uint32_t v[4];
-    double P[4][3], px[4], py[4], z[4];
-    project4(i, v, P, px, py, z);
+  __device__ bool pred(int64_t i) const {
+    State st;
+    return pred(i, st);
+  }
+  __device__ bool pred(int64_t i, State& st) const {
+    project4(i, st.v, st.P, st.px, st.py, st.z);
+    return visible(st.px, st.py, st.z);
+  }
+  __device__ void emit(int64_t i, int64_t k, const State& st) const {
+    const uint32_t* v = st.v;
+    const double(*P)[3] = st.P;
+    const double *px = st.px, *py = st.py, *z = st.z;
     double dmin, xmin, xmax, ymin, ymax;
     bounds(px, py, z, dmin, xmin, xmax, ymin, ymax);
     double f[4], proj[8], bb[4] = {xmin, ymin, xmax, ymax};
     for (int c = 0; c < 4; ++c) {
-      f[c] = sdf[v[c]];
+      f[c] = __ldg(sdf + v[c]);
       proj[2 * c] = px[c];
       proj[2 * c + 1] = py[c];
-      out.vert_ids[k * 4 + c] = (int32_t)v[c];
-      out.proj[k * 8 + 2 * c] = px[c];
-      out.proj[k * 8 + 2 * c + 1] = py[c];
-      out.depths[k * 4 + c] = z[c];
-      out.f[k * 4 + c] = f[c];
-      out.bbox[k * 4 + c] = bb[c];
     }
+    // 16-byte stores (the arrays are 16-byte aligned per splat)
+    reinterpret_cast<int4*>(out.vert_ids)[k] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
+    double2* pj = reinterpret_cast<double2*>(out.proj + k * 8);
+    for (int c = 0; c < 4; ++c) pj[c] = make_double2(px[c], py[c]);
+    double2* dz = reinterpret_cast<double2*>(out.depths + k * 4);
+    double2* ff = reinterpret_cast<double2*>(out.f + k * 4);
+    double2* bx = reinterpret_cast<double2*>(out.bbox + k * 4);
+    dz[0] = make_double2(z[0], z[1]);
+    dz[1] = make_double2(z[2], z[3]);
+    ff[0] = make_double2(f[0], f[1]);
+    ff[1] = make_double2(f[2], f[3]);
+    bx[0] = make_double2(bb[0], bb[1]);
+    bx[1] = make_double2(bb[2], bb[3]);
     out.tet_ids[k] = active[i];
     double g[3], c1[3], c2[3], c3[3], nrm[3] = {0.0, 0.0, 0.0};
     tet_gradient(P, f, g, c1, c2, c3);
@@ -152,7 +169,7 @@ int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, cons
                             const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
                             cudaStream_t st) {
   CullF f{active, sdf, deform, make_grid(R), cam, s, out};
-  int64_t* d_total = compact<CullF, 1>(n_active, f, scratch, st);  // scratch: compact_blocks(n, 1)
+  int64_t* d_total = compact_state<CullF>(n_active, f, scratch, st);  // scratch: compact_blocks(n, 1)
   int64_t h = 0;
   cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
