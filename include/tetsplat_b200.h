@@ -156,6 +156,13 @@ int ts_marching_tets_count(const double* sdf, const double* deform, int32_t reso
 int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
                      int64_t* triangles, int64_t* out_counts, void* stream);
 
+/* Adam step of the fit loop (fit.py:70-90) from the interleaved gradient buffer d_vert f32[N,4]:
+ * FP64 moments m_sdf, v_sdf [N] and m_def, v_def [N,3], step t >= 1 (bias corrections
+ * 1 - beta^t), deformation clamped to +-deform_limit (field.py:40-42) afterwards. */
+int ts_adam_step(int32_t resolution, const float* d_vert, double* sdf, double* deform, double* m_sdf,
+                 double* v_sdf, double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1,
+                 double beta2, int64_t t, double eps, double deform_limit, void* stream);
+
 /* Diagnostics: out4[0] = (pixel, splat) pairs re-decided in FP64 at a face edge or a
  * degenerate face, out4[1] = pairs re-decided in FP64 at an alpha threshold (since the
  * last reset).  [sync] */

@@ -60,6 +60,18 @@ class Adam:
             v.mul_(self.b2).addcmul_(g, g, value=1 - self.b2)
             p.addcdiv_(m / c1, (v / c2).sqrt_().add_(self.eps), value=-lr)
 
+    @torch.no_grad()
+    def step_field(self, field, grads: GradientBuffers, resolution: int, stream=None):
+        """The same update for (sdf, deformation) in one fused kernel straight from the
+        interleaved gradient buffer, deformation clamped to its limit (ts_adam_step)."""
+        from . import _native
+        self.t += 1
+        _native.check(_native.lib().ts_adam_step(
+            int(resolution), _native.ptr(grads.d_vert), _native.ptr(field.sdf), _native.ptr(field.deformation),
+            _native.ptr(self.m[0]), _native.ptr(self.v[0]), _native.ptr(self.m[1]), _native.ptr(self.v[1]),
+            float(self.lrs[0]), float(self.lrs[1]), float(self.b1), float(self.b2), int(self.t), float(self.eps),
+            float(field.deform_limit), _native.stream_ptr(stream)))
+
 
 @dataclass
 class StepConfig:
@@ -165,6 +177,5 @@ class FitStep:
             main.wait_event(inputs_ready)
         allreduce_gradients(self.grads, self.group)
         if self.opt is not None:
-            self.opt.step([f.sdf, f.deformation], [self.grads.d_sdf, self.grads.d_deform])
-            f.clamp_deformation()
+            self.opt.step_field(f, self.grads, g.resolution)
         return self.grads

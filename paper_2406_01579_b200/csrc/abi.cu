@@ -242,6 +242,17 @@ int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, do
   return check_cuda("ts_normal_consistency");
 }
 
+int ts_adam_step(int32_t R, const float* d_vert, double* sdf, double* deform, double* m_sdf, double* v_sdf,
+                 double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1, double beta2, int64_t t,
+                 double eps, double deform_limit, void* stream) {
+  if (!d_vert || !sdf || !deform || !m_sdf || !v_sdf || !m_def || !v_def || R < 1 || t < 1)
+    return fail(TS_EINVAL, "ts_adam_step: bad arguments");
+  const int64_t n = (int64_t)R + 1;
+  ts_impl_adam(n * n * n, d_vert, sdf, deform, m_sdf, v_sdf, m_def, v_def, lr_sdf, lr_def, beta1, beta2, t, eps,
+               deform_limit, ST(stream));
+  return check_cuda("ts_adam_step");
+}
+
 int ts_marching_tets_count(const double* sdf, const double* deform, int32_t R, int64_t* nv, int64_t* nt,
                            void* stream) {
   if (!sdf || !deform || !nv || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets_count: bad arguments");

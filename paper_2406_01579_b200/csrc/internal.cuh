@@ -77,5 +77,8 @@ int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
 void ts_impl_counters(unsigned long long out[4], int reset);
+void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,
+                  double* m_def, double* v_def, double lr_sdf, double lr_def, double b1, double b2, int64_t t,
+                  double eps, double limit, cudaStream_t st);
 void ts_impl_debug_flags(int flags);
 void ts_impl_phases(unsigned long long out[16], int reset);

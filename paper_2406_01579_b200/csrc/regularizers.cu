@@ -259,9 +259,48 @@ __global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double
   }
 }
 
+// Adam (fit.py:70-90) on the interleaved FP32 gradient buffer: FP64 moments and parameters,
+// torch's operation order (m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+// p -= lr (m/c1) / (sqrt(v/c2) + eps)), deformation clamped to +-limit afterwards.
+__global__ void __launch_bounds__(256) k_adam(int64_t N, const float4* __restrict__ g4, double* __restrict__ sdf,
+                                              double* __restrict__ deform, double* __restrict__ m_sdf,
+                                              double* __restrict__ v_sdf, double* __restrict__ m_def,
+                                              double* __restrict__ v_def, double lr_sdf, double lr_def, double b1,
+                                              double b2, double c1, double c2, double eps, double limit) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 g = g4[i];
+    const double gs[4] = {(double)g.x, (double)g.y, (double)g.z, (double)g.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double* p = c == 0 ? sdf + i : deform + 3 * i + (c - 1);
+      double* m = c == 0 ? m_sdf + i : m_def + 3 * i + (c - 1);
+      double* v = c == 0 ? v_sdf + i : v_def + 3 * i + (c - 1);
+      const double lr = c == 0 ? lr_sdf : lr_def;
+      const double mm = dadd(dmul(*m, b1), dmul(gs[c], 1.0 - b1));
+      const double vv = dadd(dmul(*v, b2), dmul(dmul(gs[c], gs[c]), 1.0 - b2));
+      *m = mm;
+      *v = vv;
+      double np = dsub(*p, dmul(lr, ddiv(ddiv(mm, c1), dadd(sqrt(ddiv(vv, c2)), eps))));
+      if (c > 0) np = fmin(fmax(np, -limit), limit);
+      *p = np;
+    }
+  }
+}
+
 }  // namespace ts
 
 using namespace ts;
+
+void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,
+                  double* m_def, double* v_def, double lr_sdf, double lr_def, double b1, double b2, int64_t t,
+                  double eps, double limit, cudaStream_t st) {
+  if (N <= 0) return;
+  const double c1 = 1.0 - pow(b1, (double)t), c2 = 1.0 - pow(b2, (double)t);
+  int blocks = (int)((N + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_adam<<<blocks, 256, 0, st>>>(N, reinterpret_cast<const float4*>(g4), sdf, deform, m_sdf, v_sdf, m_def, v_def,
+                                 lr_sdf, lr_def, b1, b2, c1, c2, eps, limit);
+}
 
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
                      float* d_vert, double* loss, cudaStream_t st) {

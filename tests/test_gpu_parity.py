@@ -223,3 +223,29 @@ class _Len:
 
     def __len__(self):
         return self._n
+
+
+def test_fused_adam_matches_torch_adam(ts):
+    """ts_adam_step == batch.Adam.step (fit.py:70-90) + clamp_deformation, three steps."""
+    import torch
+    from paper_2406_01579_b200.batch import Adam
+    from paper_2406_01579_b200.raster import GradientBuffers
+    g = ts.build_grid(8)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    f1 = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    f1.deformation.copy_(torch.randn(f1.deformation.shape, dtype=torch.float64, device="cuda",
+                                     generator=gen) * f1.deform_limit)
+    f1.clamp_deformation()  # (FieldState construction clamps too)
+    f2 = f1.copy()
+    o1 = Adam([f1.sdf, f1.deformation], [1e-2, 1e-3])
+    o2 = Adam([f2.sdf, f2.deformation], [1e-2, 1e-3])
+    for _ in range(3):
+        gb = GradientBuffers.zeros(g.num_vertices, "cuda")
+        gb.d_vert.copy_(torch.randn(gb.d_vert.shape, device="cuda", generator=gen))
+        o1.step([f1.sdf, f1.deformation], [gb.d_sdf, gb.d_deform])
+        f1.clamp_deformation()
+        o2.step_field(f2, gb, g.resolution)
+    torch.cuda.synchronize()
+    assert torch.allclose(f1.sdf, f2.sdf, rtol=1e-12, atol=1e-15)
+    assert torch.allclose(f1.deformation, f2.deformation, rtol=1e-12, atol=1e-15)
+    assert float(f2.deformation.abs().max()) <= f2.deform_limit
