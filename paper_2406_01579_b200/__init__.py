@@ -10,7 +10,7 @@ from .field import (FieldState, AnalyticShape, analytic_sdf, init_sphere, init_f
 from .splat import (T_FILTER, ALPHA_CLIP, T_STOP, EmptySceneError, SplatScene, prefilter, build_scene,
                     coarse_to_fine_filter, scene_from_arrays)
 from .raster import (TILE_SIZE, DEFAULT_WINDOW, RenderMaps, TileBins, GradientBuffers, SavedState, bin_and_sort,
-                     render_forward, render_backward)
+                     render_forward, render_reference, render_backward)
 from .losses import eikonal_loss, normal_consistency_loss, map_mse_loss
 
 BACKEND_NAME = "b200"

@@ -218,6 +218,25 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
     return maps, saved
 
 
+# A window at least as long as any list turns the N_w resorting into the exact mean-depth
+# order (ties by splat index) — the order render_reference's global lexsort gives.
+REFERENCE_WINDOW = 1 << 30
+
+
+def render_reference(scene: SplatScene, camera, stream=None) -> RenderMaps:
+    """Oracle renderer: exact per-pixel depth ordering, no early stop (raster.py:180-199,
+    _core.reference_render _core.pyx:232-292).
+
+    Every splat whose bbox holds a pixel is in that pixel's tile list, so the reference's
+    per-pixel walk over the globally (mean depth, index)-sorted splats equals a walk over the
+    tile list in that order: the tile lists sorted by (depth key, index) with an unbounded
+    resorting window (which sorts each equal-key run by mean depth, ties by position) and
+    compositing without early stop (t_stop = 0)."""
+    bins = bin_and_sort(scene, camera, stream=stream)
+    maps, _ = render_forward(scene, bins, camera, n_w=REFERENCE_WINDOW, t_stop=0.0, stream=stream)
+    return maps
+
+
 def _as_f32(t, dev):
     if t is None:
         return None

@@ -249,3 +249,17 @@ def test_fused_adam_matches_torch_adam(ts):
     assert torch.allclose(f1.sdf, f2.sdf, rtol=1e-12, atol=1e-15)
     assert torch.allclose(f1.deformation, f2.deformation, rtol=1e-12, atol=1e-15)
     assert float(f2.deformation.abs().max()) <= f2.deform_limit
+
+
+@pytest.mark.parametrize("case", [c for c in RENDER_CASES if "cfg1" not in c])
+def test_render_reference_matches_reference(ts, case):
+    """render_reference (raster.py:180-199): exact mean-depth order, no early stop."""
+    G = load_golden(f"render_{case}.npz")
+    if "ref_opacity" not in G:
+        pytest.skip("no reference_render fixture")
+    g, fs, cam = _setup(ts, G)
+    sc = _golden_scene(ts, G, cam, None if "proj" in G else _oracle_scene(G))
+    n, d, o, _ = ts.render_reference(sc, cam).numpy()
+    assert rel_err(n, G["ref_normal"]) < MAP_TOL
+    assert rel_err(d, G["ref_depth"]) < MAP_TOL
+    assert rel_err(o, G["ref_opacity"]) < MAP_TOL
