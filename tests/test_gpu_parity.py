@@ -263,3 +263,13 @@ def test_render_reference_matches_reference(ts, case):
     assert rel_err(n, G["ref_normal"]) < MAP_TOL
     assert rel_err(d, G["ref_depth"]) < MAP_TOL
     assert rel_err(o, G["ref_opacity"]) < MAP_TOL
+
+
+def test_bench_sort_windows_track_reference(ts):
+    """bench-sort (cli.py:194-225): every window stays within the reference's measured
+    distance of render_reference (max_abs ~3e-4 at R=16/32, 128^2)."""
+    from paper_2406_01579_b200.bench_sort import bench_sort
+    rows = [l.split(",") for l in bench_sort((16,), (1, 5, 1 << 20)).strip().split("\n")[1:]]
+    assert len(rows) == 3
+    for r, w, mx, mean, ms in rows:
+        assert float(mx) < 1e-3 and float(mean) < 1e-4
