@@ -83,6 +83,7 @@ class StepConfig:
     betas: tuple = (0.9, 0.99)
     optimizer: bool = True
     inflight: int = 2  # views in flight (renderer + workspace + stream each)
+    eik_all: bool = False  # eikonal over every tet (fit.py eikonal_scope="all") instead of the active set
 
 
 @dataclass
@@ -113,6 +114,8 @@ class FitStep:
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
         self.view = self.renderers[0]
         self.reg_stream = torch.cuda.Stream(device=dev)
+        self._all_tets = None
+        self.last_active = 0
         self._pool = ThreadPoolExecutor(max_workers=n) if n > 1 else None
 
     def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None, inputs_ready=None):
@@ -123,8 +126,9 @@ class FitStep:
         active = prefilter(g, f, s)
         if active.numel() == 0:
             raise EmptySceneError("pre-filtering removed every tetrahedron")
+        self.last_active = int(active.numel())
         if stats is not None:
-            stats.active = int(active.numel())
+            stats.active = self.last_active
         main = torch.cuda.current_stream()
         for st in self.streams + [self.reg_stream]:
             st.wait_stream(main)  # zeroed gradients, prefilter output
@@ -138,7 +142,10 @@ class FitStep:
         if rank0:
             with torch.cuda.stream(self.reg_stream):
                 if cfg.lambda_eik > 0:
-                    eikonal_loss_async(g, f, active, self.grads, cfg.lambda_eik, self.eik_loss, self.reg_stream)
+                    if cfg.eik_all and self._all_tets is None:
+                        self._all_tets = torch.arange(g.num_tets, dtype=torch.int32, device=active.device)
+                    tets = self._all_tets if cfg.eik_all else active
+                    eikonal_loss_async(g, f, tets, self.grads, cfg.lambda_eik, self.eik_loss, self.reg_stream)
                 if cfg.lambda_nc > 0:
                     normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss, self.reg_stream)
         # views: one host thread per renderer/stream, so one view's sizing syncs never stall the

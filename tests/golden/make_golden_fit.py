@@ -1,0 +1,44 @@
+"""Golden fixtures for the fit-loop layer from the UNMODIFIED reference.
+
+    python tests/golden/make_golden_fit.py /tmp/tsref/src      (see make_golden.py)
+
+Writes fit.npz: sphere-traced target maps (fit.py:93-133) for two shapes / cameras, and the
+trace of a 3-iteration fit_field run on a tiny configuration (fit.py:144-231).
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def main(ref_src: str):
+    sys.path.insert(0, ref_src)
+    import tetsplat
+    from tetsplat import camera, field, fit, grid
+    assert tetsplat.BACKEND_NAME == "compiled", "build the reference's Cython kernels first"
+    out = {}
+    shapes = {"sphere": field.AnalyticShape("sphere", (0.6,)), "torus": field.AnalyticShape("torus", (0.45, 0.15))}
+    for i, (name, shp) in enumerate(shapes.items()):
+        cam = camera.orbit_camera(1 + i, 8, width=48, height=48)
+        t = fit.render_target(shp, cam)
+        out[f"target_{name}_normal"], out[f"target_{name}_depth"] = t.normal, t.depth
+        out[f"target_{name}_opacity"] = t.opacity
+    cfg = fit.FitConfig(resolution=8, image_size=32, n_views=4, batch_size=2, iterations=3, trace_every=1)
+    g = grid.build_grid(cfg.resolution)
+    f = field.init_from_shape(g, field.AnalyticShape("sphere", (0.5,)))
+    cams, targets = fit.make_targets(field.AnalyticShape("sphere", (0.6,)), cfg)
+    tr = fit.fit_field(g, f, cams, targets, cfg)
+    out["fit_trace"] = np.array(json.dumps(tr.iterations))
+    out["fit_final_sdf"] = f.sdf
+    out["fit_final_deform"] = f.deformation
+    np.savez_compressed(os.path.join(HERE, "fit.npz"), **out)
+    print(json.dumps(tr.iterations, indent=1)[:2000])
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "/tmp/tsref/src")
