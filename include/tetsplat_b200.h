@@ -156,6 +156,13 @@ int ts_marching_tets_count(const double* sdf, const double* deform, int32_t reso
 int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
                      int64_t* triangles, int64_t* out_counts, void* stream);
 
+/* Z-buffered flat-shaded rasterization of a triangle mesh (mesh.py:98-147), the surface-limit
+ * reference: vertices f64[V,3], triangles i64[F,3] -> mask u8[H,W], depth f64[H,W] (camera z of
+ * the nearest triangle, 0 where uncovered), normal f64[H,W,3] (its unit world face normal).
+ * Ties in depth go to the lowest triangle index, like the reference's ordered loop. */
+int ts_rasterize_mesh(const double* vertices, int64_t V, const int64_t* triangles, int64_t F, const ts_camera* cam,
+                      uint8_t* mask, double* depth, double* normal, void* stream);
+
 /* Adam step of the fit loop (fit.py:70-90) from the interleaved gradient buffer d_vert f32[N,4]:
  * FP64 moments m_sdf, v_sdf [N] and m_def, v_def [N,3], step t >= 1 (bias corrections
  * 1 - beta^t), deformation clamped to +-deform_limit (field.py:40-42) afterwards. */

@@ -12,6 +12,7 @@ from .splat import (T_FILTER, ALPHA_CLIP, T_STOP, EmptySceneError, SplatScene, p
 from .raster import (TILE_SIZE, DEFAULT_WINDOW, RenderMaps, TileBins, GradientBuffers, SavedState, bin_and_sort,
                      render_forward, render_reference, render_backward)
 from .losses import eikonal_loss, normal_consistency_loss, map_mse_loss
+from .mesh import rasterize_mesh, export_obj, load_obj
 from .fit import FitConfig, FitTrace, fit_field, make_targets, render_target, run_fit, s_schedule
 
 BACKEND_NAME = "b200"

@@ -63,6 +63,7 @@ def lib():
         "ts_eikonal": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency": ([P, P, I32, D, P, P, P], ctypes.c_int),
         "ts_adam_step": ([I32, P, P, P, P, P, P, P, D, D, D, D, I64, D, D, P], ctypes.c_int),
+        "ts_rasterize_mesh": ([P, I64, P, I64, pc, P, P, P, P], ctypes.c_int),
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),
         "ts_marching_tets": ([P, P, I32, P, P, ctypes.POINTER(ctypes.c_int64), P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),

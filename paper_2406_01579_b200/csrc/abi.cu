@@ -269,6 +269,16 @@ int ts_marching_tets(const double* sdf, const double* deform, int32_t R, double*
   return check_cuda("ts_marching_tets");
 }
 
+int ts_rasterize_mesh(const double* vertices, int64_t V, const int64_t* triangles, int64_t F, const ts_camera* cam,
+                      uint8_t* mask, double* depth, double* normal, void* stream) {
+  if (!cam || !mask || !depth || !normal || V < 0 || F < 0 || (V > 0 && !vertices) || (F > 0 && !triangles))
+    return fail(TS_EINVAL, "ts_rasterize_mesh: bad arguments");
+  if (cam->width < 1 || cam->height < 1) return fail(TS_EINVAL, "ts_rasterize_mesh: bad image size");
+  keep_pool_warm();
+  ts_impl_rasterize_mesh(vertices, V, triangles, F, to_cam(cam), mask, depth, normal, ST(stream));
+  return check_cuda("ts_rasterize_mesh");
+}
+
 int ts_debug_counters(uint64_t* out4, int reset) {
   if (!out4) return fail(TS_EINVAL, "ts_debug_counters: null output");
   unsigned long long c[4];

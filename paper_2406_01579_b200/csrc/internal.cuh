@@ -77,6 +77,8 @@ int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
 void ts_impl_counters(unsigned long long out[4], int reset);
+int ts_impl_rasterize_mesh(const double* verts, int64_t V, const int64_t* tris, int64_t F, const ts::Camera& cam,
+                           uint8_t* mask, double* depth, double* normal, cudaStream_t st);
 void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,
                   double* m_def, double* v_def, double lr_sdf, double lr_def, double b1, double b2, int64_t t,
                   double eps, double limit, cudaStream_t st);

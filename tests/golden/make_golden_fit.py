@@ -2,8 +2,9 @@
 
     python tests/golden/make_golden_fit.py /tmp/tsref/src      (see make_golden.py)
 
-Writes fit.npz: sphere-traced target maps (fit.py:93-133) for two shapes / cameras, and the
-trace of a 3-iteration fit_field run on a tiny configuration (fit.py:144-231).
+Writes fit.npz (sphere-traced target maps (fit.py:93-133) for two shapes / cameras, and the
+trace of a 3-iteration fit_field run on a tiny configuration, fit.py:144-231) and
+meshraster.npz (rasterize_mesh of a Marching-Tetrahedra torus, mesh.py:98-147).
 """
 from __future__ import annotations
 
@@ -37,6 +38,17 @@ def main(ref_src: str):
     out["fit_final_sdf"] = f.sdf
     out["fit_final_deform"] = f.deformation
     np.savez_compressed(os.path.join(HERE, "fit.npz"), **out)
+
+    # z-buffered mesh rasterization (mesh.py:98-147) of a Marching-Tetrahedra mesh
+    from tetsplat import mesh as rmesh
+    g = grid.build_grid(12)
+    f = field.init_from_shape(g, field.AnalyticShape("torus", (0.45, 0.2)))
+    m = grid.marching_tetrahedra(g, f)
+    cam = camera.orbit_camera(2, 8, width=64, height=64)
+    mask, depth, normal = rmesh.rasterize_mesh(m, cam)
+    np.savez_compressed(os.path.join(HERE, "meshraster.npz"), vertices=m.vertices, triangles=m.triangles,
+                        cam_index=2, cam_count=8, size=64, mask=mask, depth=depth, normal=normal)
+    print("mesh", m.vertices.shape, m.triangles.shape, int(mask.sum()))
     print(json.dumps(tr.iterations, indent=1)[:2000])
 
 
