@@ -13,6 +13,7 @@ from .raster import (TILE_SIZE, DEFAULT_WINDOW, RenderMaps, TileBins, GradientBu
                      render_forward, render_reference, render_backward)
 from .losses import eikonal_loss, normal_consistency_loss, map_mse_loss
 from .mesh import rasterize_mesh, export_obj, load_obj
+from .imgio import write_pfm, read_pfm, write_png, save_maps, save_checkpoint, load_checkpoint
 from .fit import FitConfig, FitTrace, fit_field, make_targets, render_target, run_fit, s_schedule
 
 BACKEND_NAME = "b200"

@@ -4,7 +4,8 @@
 
 Writes fit.npz (sphere-traced target maps (fit.py:93-133) for two shapes / cameras, and the
 trace of a 3-iteration fit_field run on a tiny configuration, fit.py:144-231) and
-meshraster.npz (rasterize_mesh of a Marching-Tetrahedra torus, mesh.py:98-147).
+meshraster.npz (rasterize_mesh of a Marching-Tetrahedra torus, mesh.py:98-147) and
+formats.npz (PFM / TSPF bytes written by the reference).
 """
 from __future__ import annotations
 
@@ -49,6 +50,21 @@ def main(ref_src: str):
     np.savez_compressed(os.path.join(HERE, "meshraster.npz"), vertices=m.vertices, triangles=m.triangles,
                         cam_index=2, cam_count=8, size=64, mask=mask, depth=depth, normal=normal)
     print("mesh", m.vertices.shape, m.triangles.shape, int(mask.sum()))
+
+    # byte formats (imgio.py:18-48, field.py:180-203)
+    import tempfile
+    from tetsplat import imgio
+    rng = np.random.default_rng(7)
+    a1, a3 = rng.standard_normal((3, 5)), rng.standard_normal((3, 5, 3))
+    st = field.FieldState(rng.standard_normal(6), 0.01 * rng.standard_normal((6, 3)), 0.05, 42.5)
+    blobs = {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, fn in (("pfm1", lambda p: imgio.write_pfm(p, a1)), ("pfm3", lambda p: imgio.write_pfm(p, a3)),
+                         ("tspf", lambda p: field.save_checkpoint(st, p))):
+            fn(os.path.join(d, name))
+            blobs[name] = np.frombuffer(open(os.path.join(d, name), "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "formats.npz"), a1=a1, a3=a3, sdf=st.sdf, deform=st.deformation,
+                        s=st.steepness, limit=0.05, **blobs)
     print(json.dumps(tr.iterations, indent=1)[:2000])
 
 
