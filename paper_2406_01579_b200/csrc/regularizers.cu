@@ -12,11 +12,12 @@
 //   B : per-vertex edge term  d_n(v) = -sum_{edge neighbours} n(b), projected back
 //       through the normalisation; per-vertex share of sum_edges (1 - n_a.n_b)
 //   T2: per tet, the chain through the tet normal: dL/df (4) and g            [6R^3 threads]
-//   C : per-vertex sum over incident tets of dL/df_slot and -dL/df_slot * g
+//   C : per-vertex sum over incident tets of dL/df_slot and -dL/df_slot * g (the per-tet chain
+//       terms are stored in FP32 — they only feed the FP32 gradient buffer; sums in FP64)
 // Each tet's FP64 work is done once (not once per incident vertex), and incident tets are
 // visited in increasing tet id and edge neighbours in increasing vertex id — the
-// reference's accumulation order — so every per-vertex FP64 value is bit-identical to the
-// Cython kernel's (only the scalar loss is summed in a different order).
+// reference's accumulation order — so the vertex normals and edge terms are bit-identical to
+// the Cython kernel's FP64 values (only the scalar loss is summed in a different order).
 #include "internal.cuh"
 
 namespace ts {
@@ -208,14 +209,14 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const doubl
 __global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t T, Grid G, const double* __restrict__ sdf,
                                                       const double* __restrict__ deform,
                                                       const double* __restrict__ cnt, const double* __restrict__ dm,
-                                                      double4* __restrict__ tdf, double4* __restrict__ tg) {
+                                                      float4* __restrict__ tdf, float4* __restrict__ tg) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
     uint32_t v[4];
     double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
     load_tet(nc_tet_id(t, G), G, sdf, deform, v, P, f);
     const double det = tet_gradient(P, f, g, c1, c2, c3);
     const double nrm = gnorm3(g);
-    double4 o = make_double4(0.0, 0.0, 0.0, 0.0), og = make_double4(0.0, 0.0, 0.0, 0.0);
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f), og = make_float4(0.f, 0.f, 0.f, 0.f);
     if (!(nrm < kEpsNormal) && det != 0.0) {
       double nt[3] = {ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm)};
       double dnt[3] = {0.0, 0.0, 0.0};
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t T, Grid G, const d
       for (int i = 0; i < 3; ++i) dg[i] = ddiv(dsub(dnt[i], dmul(nt[i], dot)), nrm);
       double dfs[4];
       chain_coeffs(det, c1, c2, c3, dg, dfs);
-      o = make_double4(dfs[0], dfs[1], dfs[2], dfs[3]);
-      og = make_double4(g[0], g[1], g[2], 1.0);
+      o = make_float4((float)dfs[0], (float)dfs[1], (float)dfs[2], (float)dfs[3]);
+      og = make_float4((float)g[0], (float)g[1], (float)g[2], 1.f);
     }
     tdf[t] = o;
     tg[t] = og;
@@ -237,16 +238,16 @@ __global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t T, Grid G, const d
 }
 
 // pass C: per-vertex gather of the per-tet chain terms
-__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const double4* __restrict__ tdf,
-                                                 const double4* __restrict__ tg, float scale,
+__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const float4* __restrict__ tdf,
+                                                 const float4* __restrict__ tg, float scale,
                                                  float* __restrict__ d_vert) {
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
     for_incident_tets((uint32_t)vid, G, [&](uint32_t t, int slot) {
-      const double4 gq = tg[t];
-      if (gq.w == 0.0) return;  // skipped by the reference (undefined normal or det == 0)
-      const double4 dq = tdf[t];
+      const float4 gq = tg[t];
+      if (gq.w == 0.f) return;  // skipped by the reference (undefined normal or det == 0)
+      const float4 dq = tdf[t];
       const double d = slot == 0 ? dq.x : (slot == 1 ? dq.y : (slot == 2 ? dq.z : dq.w));
       ds = dadd(ds, d);
       dp[0] = dsub(dp[0], dmul(d, gq.x));
@@ -316,18 +317,20 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
   cudaMemsetAsync(loss, 0, sizeof(double), st);
   double *nv, *cnt, *an, *dm;
-  double4 *tdf, *tg;  // T1 writes the unit normals into tdf; T2 overwrites it
+  double4* tn;         // T1: unit tet normals (FP64: they feed the loss)
+  float4 *tdf, *tg;    // T2: per-tet chain terms (FP32: they only feed the FP32 gradient)
   cudaMallocAsync(&nv, sizeof(double) * 3 * N, st);
   cudaMallocAsync(&dm, sizeof(double) * 3 * N, st);
   cudaMallocAsync(&cnt, sizeof(double) * N, st);
   cudaMallocAsync(&an, sizeof(double) * N, st);
-  cudaMallocAsync(&tdf, sizeof(double4) * T, st);
-  cudaMallocAsync(&tg, sizeof(double4) * T, st);
+  cudaMallocAsync(&tn, sizeof(double4) * T, st);
+  cudaMallocAsync(&tdf, sizeof(float4) * T, st);
+  cudaMallocAsync(&tg, sizeof(float4) * T, st);
   const Grid G = make_grid(R);
   const int vblocks = (int)((N + 255) / 256 < 148 * 8 ? (N + 255) / 256 : 148 * 8);
   const int tblocks = (int)((T + 255) / 256 < 148 * 16 ? (T + 255) / 256 : 148 * 16);
-  k_nc_tet_normals<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, tdf);
-  k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tdf, nv, cnt, an);
+  k_nc_tet_normals<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, tn);
+  k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tn, nv, cnt, an);
   k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, an, dm, loss);
   k_nc_tet_chain<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, cnt, dm, tdf, tg);
   k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert);
@@ -335,6 +338,7 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   cudaFreeAsync(dm, st);
   cudaFreeAsync(cnt, st);
   cudaFreeAsync(an, st);
+  cudaFreeAsync(tn, st);
   cudaFreeAsync(tdf, st);
   cudaFreeAsync(tg, st);
 }
