@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, co
       }
     }
     for (int i = 0; i < 3; ++i) nv[vid * 3 + i] = s[i];
-    cnt[vid] = c;
+    cnt[vid] = c != 0.0 ? ddiv(1.0, c) : 0.0;  // stored as the reciprocal the chain pass uses
     an[vid] = a;
   }
 }
@@ -208,29 +208,54 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const doubl
 // (zeros where the reference skips the tet)
 __global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t T, Grid G, const double* __restrict__ sdf,
                                                       const double* __restrict__ deform,
-                                                      const double* __restrict__ cnt, const double* __restrict__ dm,
+                                                      const double* __restrict__ icnt, const double* __restrict__ dm,
                                                       float4* __restrict__ tdf, float4* __restrict__ tg) {
+  // FP64 throughout, but with reciprocals instead of the reference's repeated divisions: the
+  // results are rounded to FP32 for the gradient buffer anyway (the skip tests are unchanged)
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
     uint32_t v[4];
-    double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+    double P[4][3], f[4];
     load_tet(nc_tet_id(t, G), G, sdf, deform, v, P, f);
-    const double det = tet_gradient(P, f, g, c1, c2, c3);
-    const double nrm = gnorm3(g);
+    double e1[3], e2[3], e3[3], c1[3], c2[3], c3[3];
+    for (int i = 0; i < 3; ++i) {
+      e1[i] = P[1][i] - P[0][i];
+      e2[i] = P[2][i] - P[0][i];
+      e3[i] = P[3][i] - P[0][i];
+    }
+    c1[0] = e2[1] * e3[2] - e2[2] * e3[1];
+    c1[1] = e2[2] * e3[0] - e2[0] * e3[2];
+    c1[2] = e2[0] * e3[1] - e2[1] * e3[0];
+    c2[0] = e3[1] * e1[2] - e3[2] * e1[1];
+    c2[1] = e3[2] * e1[0] - e3[0] * e1[2];
+    c2[2] = e3[0] * e1[1] - e3[1] * e1[0];
+    c3[0] = e1[1] * e2[2] - e1[2] * e2[1];
+    c3[1] = e1[2] * e2[0] - e1[0] * e2[2];
+    c3[2] = e1[0] * e2[1] - e1[1] * e2[0];
+    const double det = e1[0] * c1[0] + e1[1] * c1[1] + e1[2] * c1[2];
     float4 o = make_float4(0.f, 0.f, 0.f, 0.f), og = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!(nrm < kEpsNormal) && det != 0.0) {
-      double nt[3] = {ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm)};
-      double dnt[3] = {0.0, 0.0, 0.0};
-      for (int c = 0; c < 4; ++c) {
-        double inv = ddiv(1.0, cnt[v[c]]);
-        for (int i = 0; i < 3; ++i) dnt[i] = dadd(dnt[i], dmul(dm[v[c] * 3 + i], inv));
+    if (det != 0.0) {
+      const double idet = 1.0 / det;
+      const double d1 = f[1] - f[0], d2 = f[2] - f[0], d3 = f[3] - f[0];
+      double g[3];
+      for (int i = 0; i < 3; ++i) g[i] = (d1 * c1[i] + d2 * c2[i] + d3 * c3[i]) * idet;
+      const double nrm = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+      if (!(nrm < kEpsNormal)) {
+        const double inrm = 1.0 / nrm;
+        const double nt[3] = {g[0] * inrm, g[1] * inrm, g[2] * inrm};
+        double dnt[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < 4; ++c) {
+          const double inv = icnt[v[c]];
+          for (int i = 0; i < 3; ++i) dnt[i] += dm[v[c] * 3 + i] * inv;
+        }
+        const double dot = nt[0] * dnt[0] + nt[1] * dnt[1] + nt[2] * dnt[2];
+        double dg[3];
+        for (int i = 0; i < 3; ++i) dg[i] = (dnt[i] - nt[i] * dot) * inrm;
+        const double k1 = (c1[0] * dg[0] + c1[1] * dg[1] + c1[2] * dg[2]) * idet;
+        const double k2 = (c2[0] * dg[0] + c2[1] * dg[1] + c2[2] * dg[2]) * idet;
+        const double k3 = (c3[0] * dg[0] + c3[1] * dg[1] + c3[2] * dg[2]) * idet;
+        o = make_float4((float)(-(k1 + k2 + k3)), (float)k1, (float)k2, (float)k3);
+        og = make_float4((float)g[0], (float)g[1], (float)g[2], 1.f);
       }
-      double dot = dadd(dadd(dmul(nt[0], dnt[0]), dmul(nt[1], dnt[1])), dmul(nt[2], dnt[2]));
-      double dg[3];
-      for (int i = 0; i < 3; ++i) dg[i] = ddiv(dsub(dnt[i], dmul(nt[i], dot)), nrm);
-      double dfs[4];
-      chain_coeffs(det, c1, c2, c3, dg, dfs);
-      o = make_float4((float)dfs[0], (float)dfs[1], (float)dfs[2], (float)dfs[3]);
-      og = make_float4((float)g[0], (float)g[1], (float)g[2], 1.f);
     }
     tdf[t] = o;
     tg[t] = og;
