@@ -36,6 +36,22 @@ struct PrefilterF {
     uint32_t v[4];
     tet_vertices((uint32_t)t, G, v);
     double f[4] = {sdf[v[0]], sdf[v[1]], sdf[v[2]], sdf[v[3]]};
+    // alpha_max = sigmoid(-b) (1 - e^{-(a-b)}), a = s fmax >= b = s fmin, estimated in FP32
+    // from the FP64 difference (relative error ~1e-6); the reference's FP64 evaluation errs
+    // by < 1e-13 absolute, so outside a 2e-6 relative band around the threshold the decision
+    // is certain and only the pairs inside it take the FP64 softplus path
+    double fmx = f[0], fmn = f[0];
+    for (int i = 1; i < 4; ++i) {
+      fmx = f[i] > fmx ? f[i] : fmx;
+      fmn = f[i] < fmn ? f[i] : fmn;
+    }
+    const double a = dmul(s, fmx), b = dmul(s, fmn);
+    const float y = (float)(-b), d = (float)dsub(a, b);
+    const float ey = expf(-fabsf(y)), r = 1.0f / (1.0f + ey);
+    const float sig = y >= 0.f ? r : ey * r;  // sigmoid(-b)
+    const float est = sig * -expm1f(-d);
+    const float tf = (float)thr;
+    if (fabsf(est - tf) > 2e-6f * tf + 1e-12f) return est > tf;
     return alpha_max_pass(f, s, thr, nullptr);
   }
   __device__ void emit(int64_t t, int64_t pos) const { out[pos] = (int32_t)t; }
