@@ -157,7 +157,7 @@ __device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
   float fmax = fmaxf(fabsf(s.df[1]), fmaxf(fabsf(s.df[2]), fabsf(s.df[3])));
   float izmin = fminf(fminf(s.iz[0], s.iz[1]), fminf(s.iz[2], s.iz[3]));
   float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
-  s.fband = 0.75f * s.band * (izmax / izmin) * fmax;
+  s.fband = 0.75f * s.band * (izmax * frcp(izmin)) * fmax;
   s.ftol0 = 1e-6f * fmax;
 }
 
@@ -513,7 +513,7 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
     R.x0[t] = x0;
     R.y0[t] = y0;
     R.nx[t] = nx;
-    R.inv[t] = 1.0f / (float)nx;
+    R.inv[t] = frcp((float)nx);
     if (color)
       for (int c = 0; c < 3; ++c) col[t][c] = colors[(int64_t)k * 3 + c];
   }
