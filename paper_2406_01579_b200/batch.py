@@ -82,7 +82,7 @@ class StepConfig:
     lr_deform: float = 1e-3
     betas: tuple = (0.9, 0.99)
     optimizer: bool = True
-    inflight: int = 2  # views in flight (renderer + workspace + stream each)
+    inflight: int = 3  # views in flight (renderer + workspace + stream + host thread each)
     eik_all: bool = False  # eikonal over every tet (fit.py eikonal_scope="all") instead of the active set
 
 
