@@ -249,7 +249,8 @@ def run_gpu(args):
                                torch.randn((S, S), device=dev, generator=gen),
                                torch.randn((S, S), device=dev, generator=gen)) for vi in views}
     step = FitStep(g, field, cams, StepConfig(lambda_eik=LAMBDA, lambda_nc=LAMBDA,
-                                              inflight=int(os.environ.get("TS_INFLIGHT", "3"))))
+                                              inflight=int(os.environ["TS_INFLIGHT"]) if "TS_INFLIGHT" in os.environ
+                                              else None))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 

@@ -38,6 +38,18 @@ def allreduce_gradients(grads: GradientBuffers, group=None) -> None:
             dist.all_reduce(grads.d_color, op=dist.ReduceOp.SUM, group=group)
 
 
+def default_inflight() -> int:
+    """Three views in flight, fewer when the ranks of this node share few host CPUs (each lane
+    has a host thread that waits on its stream)."""
+    import os
+    try:
+        cpus = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cpus = os.cpu_count() or 1
+    per_rank = cpus // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(1, min(3, per_rank - 1))
+
+
 class Adam:
     """fit.py:70-90 on the device (FP64 moments, like the reference)."""
 
@@ -82,7 +94,8 @@ class StepConfig:
     lr_deform: float = 1e-3
     betas: tuple = (0.9, 0.99)
     optimizer: bool = True
-    inflight: int = 3  # views in flight (renderer + workspace + stream + host thread each)
+    inflight: int | None = None  # views in flight (renderer + workspace + stream + host thread
+    #                              each); None = 3, fewer when the rank has < 4 host CPUs
     eik_all: bool = False  # eikonal over every tet (fit.py eikonal_scope="all") instead of the active set
 
 
@@ -109,7 +122,8 @@ class FitStep:
             if self.cfg.optimizer else None
         # two views in flight: each renderer owns a workspace and a stream, so one view's
         # kernels run while the host waits on the other's sizing syncs (and kernel tails overlap)
-        n = max(1, int(self.cfg.inflight))
+        n = self.cfg.inflight if self.cfg.inflight is not None else default_inflight()
+        n = max(1, int(n))
         self.renderers = [ViewRenderer(dev) for _ in range(n)]
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(n)]
         self.view = self.renderers[0]

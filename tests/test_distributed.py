@@ -74,3 +74,15 @@ def test_gloo_allreduce_matches_single_process():
     # every rank applies the identical optimizer update
     assert np.array_equal(out[0][1], out[1][1])
     assert sorted(out[0][2] + out[1][2]) == list(range(NV))
+
+
+def test_default_inflight_respects_host_cpus(monkeypatch):
+    import os
+    from paper_2406_01579_b200 import batch
+    monkeypatch.setattr(os, "sched_getaffinity", lambda pid: set(range(16)))
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
+    assert batch.default_inflight() == 3
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    assert batch.default_inflight() == 1
+    monkeypatch.setattr(os, "sched_getaffinity", lambda pid: set(range(64)))
+    assert batch.default_inflight() == 3
