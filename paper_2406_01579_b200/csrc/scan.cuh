@@ -1,12 +1,14 @@
 // scan.cuh — order-preserving stream compaction and exclusive scans.
 //
-// Compaction is two passes over a predicate functor F:
-//   k_count : each CTA owns a contiguous chunk of kChunk items and writes its survivor count
-//   k_scan  : one CTA turns the counts into exclusive offsets (+ total at [nb])
-//   k_emit  : each CTA re-evaluates F on its chunk, ranks survivors with warp ballots and
-//             calls F.emit(i, pos) so output order == input order (np.nonzero semantics)
-// Recomputing the predicate is cheaper than materialising flags for the HBM-bound
-// predicates used here (prefilter, cull, MT classification).
+// Compaction of a predicate functor F (np.nonzero semantics: output order == input order):
+//   compact<F>       : k_count (per-CTA survivor counts) -> k_scan_i64 (one CTA) -> k_emit
+//                      (re-evaluates F, ranks survivors with warp ballots) — for cheap
+//                      predicates over many items (prefilter, MT classification);
+//   compact_state<F> : one pass, one item per thread — the predicate's state feeds the
+//                      emission and the output offsets come from a decoupled look-back over
+//                      the CTA tiles (scene cull / setup).
+// scan_counts (int32 counts -> int64 exclusive offsets, total at [n]) is a single decoupled
+// look-back pass.
 #pragma once
 #include "common.cuh"
 
@@ -17,6 +19,45 @@ constexpr int kItemsPerThread = 8;
 constexpr int kChunk = kScanThreads * kItemsPerThread;  // 2048 items per CTA
 
 // IPT items per thread: 8 for light predicates, 1 for latency-bound ones (more CTAs in flight)
+// ---- decoupled look-back (single-pass scans): per tile one status word, flag << 62 | value --
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbPre = 2ull << 62, kLbMask = (1ull << 62) - 1;
+
+// logical tile of this CTA in start order (so every predecessor is resident or done)
+__device__ __forceinline__ int lb_tile(unsigned long long* ticket) {
+  __shared__ int tile;
+  if (threadIdx.x == 0) tile = (int)atomicAdd(ticket, 1ull);
+  __syncthreads();
+  return tile;
+}
+// warp 0 (all lanes): publish this tile's aggregate, walk back 32 tiles at a time to the
+// nearest inclusive prefix, publish ours; returns the exclusive prefix on every lane
+__device__ __forceinline__ long long lb_exclusive(unsigned long long* status, int tile, long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) atomicExch(status, kLbPre | (unsigned long long)agg);
+    return 0;
+  }
+  if (lane == 0) atomicExch(status + tile, kLbAgg | (unsigned long long)agg);
+  long long prefix = 0;
+  for (int hi = tile - 1;;) {
+    const int p = hi - lane;  // lane 0 = nearest predecessor
+    const unsigned long long w =
+        p >= 0 ? *reinterpret_cast<volatile unsigned long long*>(status + p) : (unsigned long long)(2ull << 62);
+    const unsigned long long f = w & ~kLbMask;
+    if (__any_sync(0xffffffffu, f == 0)) continue;  // a predecessor has not published yet
+    const unsigned pm = __ballot_sync(0xffffffffu, f == kLbPre);
+    const int k = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix in the window
+    long long v = lane <= k ? (long long)(w & kLbMask) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (pm) break;
+    hi -= 32;
+  }
+  if (lane == 0) atomicExch(status + tile, kLbPre | (unsigned long long)(prefix + agg));
+  return prefix;
+}
+
 template <class F, int IPT>
 __global__ void __launch_bounds__(kScanThreads) k_count(int64_t n, F f, int64_t* __restrict__ counts) {
   const int64_t base = (int64_t)blockIdx.x * (kScanThreads * IPT);
@@ -113,30 +154,48 @@ inline int64_t* compact(int64_t n, const F& f, int64_t* offs_scratch, cudaStream
 }
 
 // One item per thread, for functors whose predicate computes state the emission reuses
-// (F::State, pred(i, State&), emit(i, pos, const State&)): the emit pass evaluates once.
+// (F::State, pred(i, State&), emit(i, pos, const State&)): a single pass — the predicate is
+// evaluated once and the output offsets come from a decoupled look-back over the tiles.
 template <class F>
-__global__ void __launch_bounds__(kScanThreads) k_emit_state(int64_t n, F f, const int64_t* __restrict__ offs) {
+__global__ void __launch_bounds__(kScanThreads) k_compact_lb(int64_t n, F f, unsigned long long* __restrict__ status,
+                                                             unsigned long long* __restrict__ ticket, int64_t nb) {
   __shared__ int wcnt[kScanThreads / 32];
+  __shared__ long long pre_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * kScanThreads + threadIdx.x;
+  const int tile = lb_tile(ticket);
+  const int64_t i = (int64_t)tile * kScanThreads + threadIdx.x;
   typename F::State st;
   const bool p = i < n && f.pred(i, st);
   const unsigned m = __ballot_sync(0xffffffffu, p);
   if (lane == 0) wcnt[wid] = __popc(m);
   __syncthreads();
-  int before = 0;
+  int before = 0, agg = 0;
 #pragma unroll
-  for (int w = 0; w < kScanThreads / 32; ++w) before += (w < wid) ? wcnt[w] : 0;
-  if (p) f.emit(i, offs[blockIdx.x] + before + __popc(m & ((1u << lane) - 1u)), st);
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    before += (w < wid) ? wcnt[w] : 0;
+    agg += wcnt[w];
+  }
+  if (wid == 0) {
+    const long long pr = lb_exclusive(status, tile, agg);
+    if (lane == 0) pre_s = pr;
+  }
+  __syncthreads();
+  const long long pre = pre_s;
+  if (p) f.emit(i, pre + before + __popc(m & ((1u << lane) - 1u)), st);
+  // the last tile is the last ticket taken: its slot can carry the total
+  if (tile == nb - 1 && threadIdx.x == 0) *reinterpret_cast<long long*>(ticket) = pre + agg;
 }
 
+// returns the device pointer holding the survivor total (scratch[nb]); scratch needs
+// compact_blocks(n, 1) int64 entries
 template <class F>
-inline int64_t* compact_state(int64_t n, const F& f, int64_t* offs_scratch, cudaStream_t st) {
+inline int64_t* compact_state(int64_t n, const F& f, int64_t* scratch, cudaStream_t st) {
   const int64_t nb = (n + kScanThreads - 1) / kScanThreads;
-  if (nb > 0) k_count<F, 1><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
-  k_scan_i64<<<1, 1024, 0, st>>>(offs_scratch, nb);
-  if (nb > 0) k_emit_state<F><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, offs_scratch);
-  return offs_scratch + nb;
+  cudaMemsetAsync(scratch, 0, sizeof(int64_t) * (nb + 1), st);
+  if (nb > 0)
+    k_compact_lb<F><<<(unsigned)nb, kScanThreads, 0, st>>>(n, f, reinterpret_cast<unsigned long long*>(scratch),
+                                                           reinterpret_cast<unsigned long long*>(scratch + nb), nb);
+  return scratch + nb;
 }
 
 inline int64_t compact_blocks(int64_t n, int ipt = kItemsPerThread) {
@@ -144,31 +203,16 @@ inline int64_t compact_blocks(int64_t n, int ipt = kItemsPerThread) {
 }
 
 // ---- exclusive scan of int32 counts into int64 offsets (out[n] = total) --------------
-static __global__ void __launch_bounds__(kScanThreads) k_chunk_sums(const int32_t* __restrict__ in, int64_t n,
-                                                                  int64_t* __restrict__ sums) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  int64_t c = 0;
-  for (int k = 0; k < kItemsPerThread; ++k) {
-    int64_t i = base + (int64_t)k * kScanThreads + threadIdx.x;
-    if (i < n) c += in[i];
-  }
-  c = warp_sum(c);
+// single pass: each CTA scans kChunk counts (kItemsPerThread consecutive per thread) and gets
+// its offset from a decoupled look-back
+static __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int32_t* __restrict__ in, int64_t n,
+                                                               int64_t* __restrict__ out,
+                                                               unsigned long long* __restrict__ status,
+                                                               unsigned long long* __restrict__ ticket, int64_t nb) {
   __shared__ int64_t ws[kScanThreads / 32];
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t t = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
-    sums[blockIdx.x] = t;
-  }
-}
-
-static __global__ void __launch_bounds__(kScanThreads) k_chunk_scan(const int32_t* __restrict__ in, int64_t n,
-                                                                  const int64_t* __restrict__ sums,
-                                                                  int64_t* __restrict__ out) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  // each thread owns kItemsPerThread consecutive items
-  const int64_t my = base + (int64_t)threadIdx.x * kItemsPerThread;
+  __shared__ long long pre_s;
+  const int tile = lb_tile(ticket);
+  const int64_t my = (int64_t)tile * kChunk + (int64_t)threadIdx.x * kItemsPerThread;
   int32_t v[kItemsPerThread];
   int64_t loc = 0;
 #pragma unroll
@@ -180,33 +224,41 @@ static __global__ void __launch_bounds__(kScanThreads) k_chunk_scan(const int32_
   int64_t incl = loc;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  __shared__ int64_t ws[kScanThreads / 32];
   if (lane == 31) ws[wid] = incl;
   __syncthreads();
-  int64_t wbase = 0;
-  for (int w = 0; w < wid; ++w) wbase += ws[w];
-  int64_t run = sums[blockIdx.x] + wbase + incl - loc;
+  int64_t wbase = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    wbase += (w < wid) ? ws[w] : 0;
+    agg += ws[w];
+  }
+  if (wid == 0) {
+    const long long pr = lb_exclusive(status, tile, agg);
+    if (lane == 0) pre_s = pr;
+  }
+  __syncthreads();
+  int64_t run = pre_s + wbase + incl - loc;
 #pragma unroll
   for (int k = 0; k < kItemsPerThread; ++k) {
     if (my + k < n) out[my + k] = run;
     run += v[k];
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
+  if (tile == nb - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
 }
 
 // scratch needs compact_blocks(n) int64 entries
 inline void scan_counts(const int32_t* in, int64_t n, int64_t* out, int64_t* scratch, cudaStream_t st) {
-  int64_t nb = (n + kChunk - 1) / kChunk;
+  const int64_t nb = (n + kChunk - 1) / kChunk;
   if (nb == 0) {
     cudaMemsetAsync(out, 0, sizeof(int64_t), st);
     return;
   }
-  k_chunk_sums<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch);
-  k_scan_i64<<<1, 1024, 0, st>>>(scratch, nb);
-  k_chunk_scan<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, scratch, out);
+  cudaMemsetAsync(scratch, 0, sizeof(int64_t) * (nb + 1), st);
+  k_scan_lb<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, out, reinterpret_cast<unsigned long long*>(scratch),
+                                                   reinterpret_cast<unsigned long long*>(scratch + nb), nb);
 }
 
 }  // namespace ts

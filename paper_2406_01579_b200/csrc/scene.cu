@@ -88,7 +88,7 @@ struct CullF {
       ymax = py[c] > ymax ? py[c] : ymax;
     }
   }
-  // projected tet, kept between the visibility test and the emission (k_emit_state)
+  // projected tet, kept between the visibility test and the emission (k_compact_lb)
   struct State {
     uint32_t v[4];
     double P[4][3], px[4], py[4], z[4];
