@@ -197,10 +197,11 @@ def test_fused_view_pipeline_matches_api(ts, case):
     assert torch.allclose(gb2.d_vert, gb.d_vert, rtol=1e-6, atol=1e-6 * float(gb.d_vert.abs().max()))
 
 
-@pytest.mark.parametrize("R,S", [(48, 128), (64, 96)])
+@pytest.mark.parametrize("R,S", [(48, 128), (64, 96), (48, 16)])
 def test_bins_long_tiles_match_stable_sort(ts, R, S):
-    """Tiles longer than 2048 entries take the shared-memory radix sort: the lists must equal
-    the reference's stable (tile, q) sort (raster.py:104-141, restated in the oracle)."""
+    """Tiles longer than 2048 entries take the shared-memory radix sort (longer than 16384:
+    the global-memory bitonic; S=16 is a single tile holding every splat): the lists must
+    equal the reference's stable (tile, q) sort (raster.py:104-141, restated in the oracle)."""
     from types import SimpleNamespace
     from oracle import ts_oracle as O
     g = ts.build_grid(R)
