@@ -156,6 +156,13 @@ int ts_marching_tets_count(const double* sdf, const double* deform, int32_t reso
 int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
                      int64_t* triangles, int64_t* out_counts, void* stream);
 
+/* ts_normal_consistency with caller-owned scratch (ts_normal_consistency_scratch_bytes(R)
+ * bytes of device memory) instead of stream-ordered allocations — for callers that run it
+ * beside other streams every step. */
+int64_t ts_normal_consistency_scratch_bytes(int32_t resolution);
+int ts_normal_consistency_ws(const double* sdf, const double* deform, int32_t resolution, double scale, float* d_vert,
+                             double* loss, void* scratch, void* stream);
+
 /* Z-buffered flat-shaded rasterization of a triangle mesh (mesh.py:98-147), the surface-limit
  * reference: vertices f64[V,3], triangles i64[F,3] -> mask u8[H,W], depth f64[H,W] (camera z of
  * the nearest triangle, 0 where uncovered), normal f64[H,W,3] (its unit world face normal).

@@ -62,6 +62,8 @@ def lib():
                                 P, P, P], ctypes.c_int),
         "ts_eikonal": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency": ([P, P, I32, D, P, P, P], ctypes.c_int),
+        "ts_normal_consistency_scratch_bytes": ([I32], ctypes.c_int64),
+        "ts_normal_consistency_ws": ([P, P, I32, D, P, P, P, P], ctypes.c_int),
         "ts_adam_step": ([I32, P, P, P, P, P, P, P, D, D, D, D, I64, D, D, P], ctypes.c_int),
         "ts_rasterize_mesh": ([P, I64, P, I64, pc, P, P, P, P], ctypes.c_int),
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),

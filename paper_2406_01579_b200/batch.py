@@ -16,7 +16,7 @@ from dataclasses import dataclass, field as dc_field
 import torch
 import torch.distributed as dist
 
-from .losses import eikonal_loss_async, normal_consistency_loss_async
+from .losses import eikonal_loss_async, nc_scratch_bytes, normal_consistency_loss_async
 from .raster import GradientBuffers
 from .splat import EmptySceneError, prefilter
 from .view import ViewRenderer
@@ -129,6 +129,7 @@ class FitStep:
         self.view = self.renderers[0]
         self.reg_stream = torch.cuda.Stream(device=dev)
         self._all_tets = None
+        self._nc_scratch = None  # normal-consistency scratch, allocated once
         self.last_active = 0
         self._pool = ThreadPoolExecutor(max_workers=n) if n > 1 else None
 
@@ -161,7 +162,10 @@ class FitStep:
                     tets = self._all_tets if cfg.eik_all else active
                     eikonal_loss_async(g, f, tets, self.grads, cfg.lambda_eik, self.eik_loss, self.reg_stream)
                 if cfg.lambda_nc > 0:
-                    normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss, self.reg_stream)
+                    if self._nc_scratch is None:
+                        self._nc_scratch = torch.empty(nc_scratch_bytes(g), dtype=torch.uint8, device=f.sdf.device)
+                    normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss, self.reg_stream,
+                                                  self._nc_scratch)
         # views: one host thread per renderer/stream, so one view's sizing syncs never stall the
         # other stream's launches
         lanes = len(self.renderers)

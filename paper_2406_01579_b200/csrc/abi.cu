@@ -52,6 +52,10 @@ static void keep_pool_warm() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // no hidden cross-stream waits: a stream never reuses another stream's freed block by
+    // waiting on it (the views in flight run on separate streams)
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   dev_done = dev;
 }
@@ -251,6 +255,16 @@ int ts_adam_step(int32_t R, const float* d_vert, double* sdf, double* deform, do
   ts_impl_adam(n * n * n, d_vert, sdf, deform, m_sdf, v_sdf, m_def, v_def, lr_sdf, lr_def, beta1, beta2, t, eps,
                deform_limit, ST(stream));
   return check_cuda("ts_adam_step");
+}
+
+int64_t ts_normal_consistency_scratch_bytes(int32_t R) { return R < 1 ? 0 : ts_impl_nc_scratch_bytes(R); }
+
+int ts_normal_consistency_ws(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
+                             double* loss, void* scratch, void* stream) {
+  if (!sdf || !deform || !d_vert || !loss || !scratch || R < 1)
+    return fail(TS_EINVAL, "ts_normal_consistency_ws: bad arguments");
+  ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream), scratch);
+  return check_cuda("ts_normal_consistency_ws");
 }
 
 int ts_marching_tets_count(const double* sdf, const double* deform, int32_t R, int64_t* nv, int64_t* nt,

@@ -1324,31 +1324,43 @@ __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const int64_t* __re
 using namespace ts;
 
 // window-resorted lists + pair offsets of the view: item_off[M+1]; returns the pair count
+// a caller-owned temporary when given, else one from the stream-ordered pool (freed by put_tmp)
+template <class T>
+static T* take_tmp(T* given, size_t n, cudaStream_t st) {
+  if (given) return given;
+  T* p = nullptr;
+  cudaMallocAsync(&p, sizeof(T) * (n ? n : 1), st);
+  return p;
+}
+template <class T>
+static void put_tmp(T* p, const T* given, cudaStream_t st) {
+  if (p && p != given) cudaFreeAsync(p, st);
+}
+
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int64_t M, const double* md, int n_w,
-                                double near_, double far_, const SplatRec* rec, int64_t* item_off, cudaStream_t st) {
+                                double near_, double far_, const SplatRec* rec, int64_t* item_off, cudaStream_t st,
+                                const ViewScratch* scr) {
+  const ViewScratch none{};
+  const ViewScratch& sc = scr ? *scr : none;
   const int T = tiles_x * tiles_y;
   if (M <= 0) {
     cudaMemsetAsync(item_off, 0, sizeof(int64_t), st);
     return 0;
   }
-  int32_t* widx = nullptr;
-  double* wz = nullptr;
-  int32_t* cnt = nullptr;
-  int64_t* scratch = nullptr;
-  cudaMallocAsync(&widx, sizeof(int32_t) * M, st);
-  cudaMallocAsync(&wz, sizeof(double) * M, st);
-  cudaMallocAsync(&cnt, sizeof(int32_t) * M, st);
-  cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(M), st);
+  int32_t* widx = take_tmp(sc.widx, M, st);
+  double* wz = take_tmp(sc.wz, M, st);
+  int32_t* cnt = take_tmp(sc.cnt, M, st);
+  int64_t* scratch = take_tmp(sc.scan, compact_blocks(M), st);
   uint32_t* qpos = reinterpret_cast<uint32_t*>(cnt);  // dead before k_item_counts writes cnt
   k_window<<<T, 256, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, qpos, widx, wz);
   k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
   scan_counts(cnt, M, item_off, scratch, st);
   int64_t total = 0;
   cudaMemcpyAsync(&total, item_off + M, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaFreeAsync(widx, st);
-  cudaFreeAsync(wz, st);
-  cudaFreeAsync(cnt, st);
-  cudaFreeAsync(scratch, st);
+  put_tmp(widx, sc.widx, st);
+  put_tmp(wz, sc.wz, st);
+  put_tmp(cnt, sc.cnt, st);
+  put_tmp(scratch, sc.scan, st);
   cudaStreamSynchronize(st);
   return total;
 }
@@ -1356,8 +1368,9 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
 void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec* rec, const float* colors,
                      const Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
-                     float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st) {
+                     float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st, const ViewScratch* scr) {
   const int T = tiles_x * tiles_y;
+  int32_t* const given_order = scr ? scr->torder : nullptr;
   cudaMemsetAsync(pair_bits, 0, sizeof(uint32_t) * (size_t)TS_PAIR_BIT_WORDS(n_pairs), st);
   static bool attr = false;
   const int smem = (int)sizeof(FwdSmem);
@@ -1366,8 +1379,7 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
     cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  int32_t* torder = nullptr;
-  cudaMallocAsync(&torder, sizeof(int32_t) * T, st);
+  int32_t* torder = take_tmp(given_order, T, st);
   k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
@@ -1377,14 +1389,15 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
     k_forward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
                                                  tiles_x, W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
                                                  nmap, dmap, omap, nullptr, n_proc, n_blend);
-  cudaFreeAsync(torder, st);
+  put_tmp(torder, given_order, st);
 }
 
 void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, int64_t K, const SplatRec* rec,
                       const float* colors, const double* fsc, const int32_t* vert_ids, const int32_t* tet_ids,
                       const double* deform, int R, const Camera& cam, const int64_t* item_off,
                       const uint32_t* pair_bits, const float4* pair_rec, const float* maps[4],
-                      const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st) {
+                      const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
+                      const ViewScratch* scr) {
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
   static bool attr = false;
@@ -1394,10 +1407,10 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
     cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  float* rows = nullptr;
-  int32_t* torder = nullptr;
-  cudaMallocAsync(&rows, sizeof(float) * kGr * (size_t)M, st);
-  cudaMallocAsync(&torder, sizeof(int32_t) * T, st);
+  float* const given_rows = scr ? scr->rows : nullptr;
+  int32_t* const given_order = scr ? scr->torder : nullptr;
+  float* rows = take_tmp(given_rows, kGr * (size_t)M, st);
+  int32_t* torder = take_tmp(given_order, T, st);
   k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   if (color)
@@ -1418,8 +1431,8 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   else
     k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
                                            make_grid(R), cam, d_vert, nullptr);
-  cudaFreeAsync(rows, st);
-  cudaFreeAsync(torder, st);
+  put_tmp(rows, given_rows, st);
+  put_tmp(torder, given_order, st);
 }
 
 void ts_impl_counters(unsigned long long out[4], int reset) {

@@ -30,6 +30,18 @@ struct BinWork {
   int64_t* dev_i64;    // [2]
 };
 
+// Caller-owned temporaries of the per-view path (the fused workspace passes its own grow-only
+// buffers so no view in flight allocates from the shared stream-ordered pool; nullptr
+// members are taken from the pool).
+struct ViewScratch {
+  int32_t* widx = nullptr;   // [M]   window indices
+  double* wz = nullptr;      // [M]   window depths
+  int32_t* cnt = nullptr;    // [M]   pairs per list position
+  int64_t* scan = nullptr;   // [compact_blocks(M)]
+  int32_t* torder = nullptr; // [T]   CTA launch order
+  float* rows = nullptr;     // [kGr * M] per-(tile, splat) gradient rows
+};
+
 struct BinsView {
   const int64_t* starts;
   const int64_t* splat_off;
@@ -58,21 +70,24 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
 void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n);
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, const double* md,
                                 int n_w, double near_, double far_, const ts::SplatRec* rec, int64_t* item_off,
-                                cudaStream_t st);
+                                cudaStream_t st, const ts::ViewScratch* scr = nullptr);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
                      const ts::Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
-                     float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st);
+                     float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st,
+                     const ts::ViewScratch* scr = nullptr);
 void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, int64_t K,
                       const ts::SplatRec* rec, const float* colors, const double* fsc, const int32_t* vert_ids,
                       const int32_t* tet_ids, const double* deform, int R, const ts::Camera& cam,
                       const int64_t* item_off, const uint32_t* pair_bits, const float4* pair_rec,
                       const float* maps[4], const float* dmaps[4],
-                      const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st);
+                      const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
+                      const ts::ViewScratch* scr = nullptr);
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
                      float* d_vert, double* loss, cudaStream_t st);
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
-                                double* loss, cudaStream_t st);
+                                double* loss, cudaStream_t st, void* scratch = nullptr);
+int64_t ts_impl_nc_scratch_bytes(int R);
 int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);

@@ -337,20 +337,36 @@ void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32
   k_eikonal<<<blocks, 256, 0, st>>>(n, tet_set, make_grid(R), sdf, deform, scale, d_vert, loss);
 }
 
+// scratch layout of the normal-consistency passes (16-byte aligned pieces)
+static void nc_layout(int R, int64_t off[8]) {
+  const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
+  const int64_t sz[7] = {24 * N, 24 * N, 8 * N, 8 * N, 32 * T, 16 * T, 16 * T};  // nv dm cnt an tn tdf tg
+  off[0] = 0;
+  for (int i = 0; i < 7; ++i) off[i + 1] = off[i] + ((sz[i] + 255) & ~255ll);
+}
+
+int64_t ts_impl_nc_scratch_bytes(int R) {
+  int64_t off[8];
+  nc_layout(R, off);
+  return off[7];
+}
+
+// scratch: ts_impl_nc_scratch_bytes(R) bytes of device memory, or nullptr (stream-ordered pool)
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
-                                double* loss, cudaStream_t st) {
+                                double* loss, cudaStream_t st, void* scratch) {
   const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
   cudaMemsetAsync(loss, 0, sizeof(double), st);
-  double *nv, *cnt, *an, *dm;
-  double4* tn;         // T1: unit tet normals (FP64: they feed the loss)
-  float4 *tdf, *tg;    // T2: per-tet chain terms (FP32: they only feed the FP32 gradient)
-  cudaMallocAsync(&nv, sizeof(double) * 3 * N, st);
-  cudaMallocAsync(&dm, sizeof(double) * 3 * N, st);
-  cudaMallocAsync(&cnt, sizeof(double) * N, st);
-  cudaMallocAsync(&an, sizeof(double) * N, st);
-  cudaMallocAsync(&tn, sizeof(double4) * T, st);
-  cudaMallocAsync(&tdf, sizeof(float4) * T, st);
-  cudaMallocAsync(&tg, sizeof(float4) * T, st);
+  int64_t off[8];
+  nc_layout(R, off);
+  char* base = static_cast<char*>(scratch);
+  if (!base) cudaMallocAsync(reinterpret_cast<void**>(&base), off[7], st);
+  double* nv = reinterpret_cast<double*>(base + off[0]);
+  double* dm = reinterpret_cast<double*>(base + off[1]);
+  double* cnt = reinterpret_cast<double*>(base + off[2]);
+  double* an = reinterpret_cast<double*>(base + off[3]);
+  double4* tn = reinterpret_cast<double4*>(base + off[4]);  // T1: unit tet normals (FP64: they feed the loss)
+  float4* tdf = reinterpret_cast<float4*>(base + off[5]);   // T2: per-tet chain terms (FP32: gradient only)
+  float4* tg = reinterpret_cast<float4*>(base + off[6]);
   const Grid G = make_grid(R);
   const int vblocks = (int)((N + 255) / 256 < 148 * 8 ? (N + 255) / 256 : 148 * 8);
   const int tblocks = (int)((T + 255) / 256 < 148 * 16 ? (T + 255) / 256 : 148 * 16);
@@ -359,11 +375,5 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, an, dm, loss);
   k_nc_tet_chain<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, cnt, dm, tdf, tg);
   k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert);
-  cudaFreeAsync(nv, st);
-  cudaFreeAsync(dm, st);
-  cudaFreeAsync(cnt, st);
-  cudaFreeAsync(an, st);
-  cudaFreeAsync(tn, st);
-  cudaFreeAsync(tdf, st);
-  cudaFreeAsync(tg, st);
+  if (!scratch) cudaFreeAsync(base, st);
 }

@@ -46,6 +46,8 @@ struct ts_workspace {
   Buf starts, splat_off, items, pos_of, nonmono, witems, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
   // forward state
   Buf item_off, pair_bits, pair_rec, n_proc, n_blend;
+  // per-view temporaries (kept so no view in flight allocates from the shared pool)
+  Buf widx, wz, pcnt, pscan, torder, rows;
   // view description of the last forward
   int64_t K = 0, M = 0, P = 0, maxL = 0;
   int tiles_x = 0, tiles_y = 0, R = 0;
@@ -88,7 +90,7 @@ void ts_workspace_destroy(ts_workspace* ws) {
                 &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
                 &ws->nonmono, &ws->witems, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
                 &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
-                &ws->n_proc, &ws->n_blend};
+                &ws->n_proc, &ws->widx, &ws->wz, &ws->pcnt, &ws->pscan, &ws->torder, &ws->rows, &ws->n_blend};
   cudaDeviceSynchronize();
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
@@ -159,14 +161,24 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   int64_t* item_off = ws->item_off.get<int64_t>(M + 1);
   if (!n_proc || !n_blend || !item_off) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   int64_t P = 0;
-  if (K > 0 && M > 0) P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st);
+  ViewScratch scr;
+  scr.widx = ws->widx.get<int32_t>(M);
+  scr.wz = ws->wz.get<double>(M);
+  scr.cnt = ws->pcnt.get<int32_t>(M);
+  scr.scan = ws->pscan.get<int64_t>(compact_blocks(M));
+  scr.torder = ws->torder.get<int32_t>(T);
+  scr.rows = ws->rows.get<float>(24 * (M > 0 ? M : 1));  // kGr floats per list position
+  if (!scr.widx || !scr.wz || !scr.cnt || !scr.scan || !scr.torder || !scr.rows)
+    return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  if (K > 0 && M > 0)
+    P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr);
   uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(P));
   float4* prec = ws->pair_rec.get<float4>(P);
   if (!pbits || !prec) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0) {
     ts_impl_forward(tx, ty, bv, so.rec, colors, Scene64{so.proj, so.depths, so.f, so.bbox}, cam.width, cam.height, s,
                     (float)t_stop, item_off, P, pbits, prec, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
-                    st);
+                    st, &scr);
   } else {
     cudaMemsetAsync(nmap, 0, sizeof(float) * 3 * HW, st);
     cudaMemsetAsync(dmap, 0, sizeof(float) * HW, st);
@@ -201,6 +213,9 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
       !dmaps[2])
     return ws_fail(TS_EINVAL, "ts_view_backward: bad arguments");
   if (ws->K == 0 || ws->M == 0) return TS_OK;
+  ViewScratch scr;  // sized by the forward of this view
+  scr.torder = reinterpret_cast<int32_t*>(ws->torder.p);
+  scr.rows = reinterpret_cast<float*>(ws->rows.p);
   const float* m4[4] = {maps[0], maps[1], maps[2], ws->color ? maps[3] : nullptr};
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], ws->color ? dmaps[3] : nullptr};
   BinsView bv{reinterpret_cast<int64_t*>(ws->starts.p), reinterpret_cast<int64_t*>(ws->splat_off.p),
@@ -213,7 +228,7 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
                    reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<uint32_t*>(ws->pair_bits.p),
                    reinterpret_cast<float4*>(ws->pair_rec.p), m4, d4,
                    reinterpret_cast<int32_t*>(ws->n_proc.p), d_vert, ws->color ? d_color : nullptr,
-                   reinterpret_cast<cudaStream_t>(stream));
+                   reinterpret_cast<cudaStream_t>(stream), &scr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
   return TS_OK;

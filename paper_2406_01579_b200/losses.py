@@ -40,10 +40,22 @@ def normal_consistency_loss(grid, field, out: GradientBuffers | None = None, sca
     return float(loss.item()), out
 
 
-def normal_consistency_loss_async(grid, field, out, scale, loss, stream=None):
-    _native.check(_native.lib().ts_normal_consistency(_native.ptr(field.sdf), _native.ptr(field.deformation),
-                                                      grid.resolution, float(scale), _native.ptr(out.d_vert),
-                                                      _native.ptr(loss), _native.stream_ptr(stream)))
+def normal_consistency_loss_async(grid, field, out, scale, loss, stream=None, scratch=None):
+    """Sync-free variant; `scratch` (uint8 device tensor of nc_scratch_bytes(grid) bytes)
+    avoids per-call stream-ordered allocations."""
+    L = _native.lib()
+    if scratch is not None:
+        _native.check(L.ts_normal_consistency_ws(_native.ptr(field.sdf), _native.ptr(field.deformation),
+                                                 grid.resolution, float(scale), _native.ptr(out.d_vert),
+                                                 _native.ptr(loss), _native.ptr(scratch), _native.stream_ptr(stream)))
+        return
+    _native.check(L.ts_normal_consistency(_native.ptr(field.sdf), _native.ptr(field.deformation),
+                                          grid.resolution, float(scale), _native.ptr(out.d_vert),
+                                          _native.ptr(loss), _native.stream_ptr(stream)))
+
+
+def nc_scratch_bytes(grid) -> int:
+    return int(_native.lib().ts_normal_consistency_scratch_bytes(grid.resolution))
 
 
 def map_mse_loss(rendered: RenderMaps, target: RenderMaps, weights: dict):
