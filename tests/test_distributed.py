@@ -81,8 +81,8 @@ def test_default_inflight_respects_host_cpus(monkeypatch):
     from paper_2406_01579_b200 import batch
     monkeypatch.setattr(os, "sched_getaffinity", lambda pid: set(range(16)))
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
-    assert batch.default_inflight() == 3
+    assert batch.default_inflight() == 4
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
     assert batch.default_inflight() == 1
     monkeypatch.setattr(os, "sched_getaffinity", lambda pid: set(range(64)))
-    assert batch.default_inflight() == 3
+    assert batch.default_inflight() == 4
