@@ -147,9 +147,11 @@ def grid_axis(R):
     return np.linspace(-1.0, 1.0, R + 1)
 
 
-def build_grid(R: int) -> TetrahedralGrid:
+def build_grid(R: int, with_edges: bool = True) -> TetrahedralGrid:
     """Kuhn 6-tet grid (grid.py:64-117).  Vertex id x + n*y + n^2*z; tet id
-    cell*6 + p with cell = ix*R^2 + iy*R + iz; negative-volume tets swap v2/v3."""
+    cell*6 + p with cell = ix*R^2 + iy*R + iz; negative-volume tets swap v2/v3.
+    `with_edges=False` skips the sorted edge list (only normal consistency reads it; at
+    R=256 its lexsort is most of the 130 s build)."""
     if R < 1:
         raise ValueError("resolution must be >= 1")
     n = R + 1
@@ -173,6 +175,8 @@ def build_grid(R: int) -> TetrahedralGrid:
                     pos[tets[:, 3]] - a)
     flip = vol < 0
     tets[flip] = tets[flip][:, [0, 1, 3, 2]]
+    if not with_edges:
+        return TetrahedralGrid(pos, tets, np.zeros((0, 2), np.int64), R)
     g = np.arange(n)
     gx, gy, gz = np.meshgrid(g, g, g, indexing="ij")
     el = []

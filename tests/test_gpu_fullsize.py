@@ -1,0 +1,234 @@
+"""GPU parity at BASELINE.json's full configurations (configs[1], [2], [4]) against the CPU
+oracle on identical inputs — the sizes the bench runs, not just the small golden cases.
+
+* config 2 — 64^3 grid, 512^2, 4 views, fwd+bwd with eikonal + normal-consistency gradients
+  (lambda 1000 each) through `batch.FitStep`, the exact multi-view path `bench.py` times:
+  per-view maps <= 1e-4, the summed vertex gradient <= 1e-3, regularizer losses <= 1e-9.
+* config 3 — 128^3 grid, 1024^2, one view at s = 100 (headline) and s = 20 (worst case):
+  bit-exact active set and tile lists (stage level, on the GPU's FP64 scene), maps <= 1e-4,
+  vertex gradients <= 1e-3, regularizers at 128^3.
+* config 5 — 256^3 grid: Marching Tetrahedra bit-exact (vertices and triangles); 2048^2
+  forward: tile lists bit-exact, and the maps of a sample of tiles (the longest lists plus a
+  seeded random set) against the oracle compositing exactly those tiles.
+
+Relative error = max|gpu - ref| / max|ref| (gradcheck.py:136-137).  The oracle (oracle/,
+test infrastructure) is the checker only; every GPU value comes through the C ABI.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+MAP_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def ts():
+    import paper_2406_01579_b200 as ts
+    from paper_2406_01579_b200 import _native
+    _native.lib()  # fail loudly when the CUDA library or the device is missing
+    return ts
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import ts_oracle as O
+    return O
+
+
+def _gpu_field(ts, g, of):
+    return ts.FieldState.from_numpy(of.sdf, of.deformation, ts.deform_limit_for(g))
+
+
+def _dmaps_torch(ts, O, S, seed):
+    w = O.synthetic_dmaps(S, S, seed=seed)
+    t = lambda a: torch.as_tensor(a, dtype=torch.float32, device="cuda")
+    return ts.RenderMaps(t(w.normal), t(w.depth), t(w.opacity)), w
+
+
+def _maps_np(maps):
+    return [m.detach().cpu().numpy() for m in (maps.normal, maps.depth, maps.opacity)]
+
+
+def _check_maps(gpu, ref):
+    for a, b in zip(gpu, (ref.normal, ref.depth, ref.opacity)):
+        assert rel_err(a, b) < MAP_TOL
+
+
+def _restrict_bins(O, bins, tiles):
+    """The oracle's TileBins with every tile but `tiles` emptied (starts stay monotone), so
+    its compositing kernel renders exactly those tiles."""
+    T = bins.tiles_x * bins.tiles_y
+    keep = np.zeros(T, bool)
+    keep[tiles] = True
+    lens = np.where(keep, np.diff(bins.starts), 0)
+    starts = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    items = np.concatenate([bins.items[bins.starts[t]:bins.starts[t + 1]] for t in np.nonzero(keep)[0]])
+    return O.TileBins(bins.tile_size, bins.tiles_x, bins.tiles_y, starts, items.astype(np.int64))
+
+
+def _oracle_scene_on(O, sc, cam):
+    """The GPU's FP64 scene as an oracle SplatScene (stage-level parity of bins/compositing)."""
+    n = lambda t: t.detach().cpu().numpy()
+    return O.SplatScene(n(sc.tet_ids).astype(np.int64), n(sc.vert_ids).astype(np.int64), n(sc.proj),
+                        n(sc.depths), n(sc.f), n(sc.normals), n(sc.mean_depth), n(sc.alpha_max), n(sc.bbox),
+                        float(sc.steepness), None)
+
+
+# --- config 2: 64^3, 512^2, 4 views, fwd+bwd + regularizers through FitStep ----------------
+
+def test_config2_fitstep_matches_oracle(ts, O):
+    from paper_2406_01579_b200.batch import FitStep, StepConfig
+    R, S, V, s, lam = 64, 512, 4, 100.0, 1000.0
+    og = O.build_grid(R)
+    of = O.noisy_field(og, seed=0)
+    g = ts.build_grid(R)
+    cams = [ts.orbit_camera(i, V, width=S, height=S) for i in range(V)]
+    dms = [_dmaps_torch(ts, O, S, seed=1 + i) for i in range(V)]
+    got_maps = {}
+
+    def dfn(vi, maps):
+        got_maps[vi] = _maps_np(maps)
+        return dms[vi][0]
+
+    for lam_reg in (0.0, lam):  # render-only first (regularizers would dominate the scale)
+        f = _gpu_field(ts, g, of)
+        step = FitStep(g, f, cams, StepConfig(lambda_eik=lam_reg, lambda_nc=lam_reg, optimizer=False))
+        gb = step(s, range(V), dfn)
+        torch.cuda.synchronize()
+        gpu = gb.d_vert.cpu().numpy().astype(np.float64)
+        if lam_reg == 0.0:
+            render_grad = gpu
+        else:
+            eik, nc = float(step.eik_loss.item()), float(step.nc_loss.item())
+
+    active = O.prefilter(og, of, s)
+    ref_sdf, ref_def = np.zeros(og.num_vertices), np.zeros((og.num_vertices, 3))
+    for i in range(V):
+        ocam = O.orbit_camera(i, V, width=S, height=S)
+        sc = O.build_scene(og, of, ocam, s, active=active)
+        b = O.bin_and_sort(sc, ocam)
+        maps, saved = O.render_forward(sc, b, ocam, save_state=True)
+        _check_maps(got_maps[i], maps)
+        gr = O.render_backward(saved, sc, og, of, ocam, dms[i][1])
+        ref_sdf += gr.d_sdf
+        ref_def += gr.d_deform
+    assert rel_err(render_grad[:, 0], ref_sdf) < GRAD_TOL
+    assert rel_err(render_grad[:, 1:], ref_def) < GRAD_TOL
+
+    le, ge = O.eikonal_loss(og, of, active)
+    ln, gn = O.normal_consistency_loss(og, of)
+    assert abs(eik - le) <= 1e-9 * max(1.0, abs(le))
+    assert abs(nc - ln) <= 1e-9 * max(1.0, abs(ln))
+    tot_sdf = ref_sdf + lam * (ge.d_sdf + gn.d_sdf)
+    tot_def = ref_def + lam * (ge.d_deform + gn.d_deform)
+    assert rel_err(gpu[:, 0], tot_sdf) < GRAD_TOL
+    assert rel_err(gpu[:, 1:], tot_def) < GRAD_TOL
+
+
+# --- config 3: 128^3, 1024^2 (the bench workload), one view ------------------------------
+
+@pytest.fixture(scope="module")
+def cfg3(O):
+    og = O.build_grid(128)
+    return og, O.init_sphere_field(og)
+
+
+@pytest.mark.parametrize("s", [100.0, 20.0])
+def test_config3_view_matches_oracle(ts, O, cfg3, s):
+    og, of = cfg3
+    S = 1024
+    g = ts.build_grid(128)
+    f = _gpu_field(ts, g, of)
+    cam = ts.orbit_camera(0, 8, width=S, height=S)
+    ocam = O.orbit_camera(0, 8, width=S, height=S)
+    active = ts.prefilter(g, f, s)
+    oactive = O.prefilter(og, of, s)
+    assert np.array_equal(active.cpu().numpy().astype(np.int64), oactive)
+    sc = ts.build_scene(g, f, cam, s, active=active)
+    b = ts.bin_and_sort(sc, cam)
+    maps, saved = ts.render_forward(sc, b, cam, save_state=True)
+    dm, dm_np = _dmaps_torch(ts, O, S, seed=1)
+    gb = ts.render_backward(saved, sc, g, f, cam, dm)
+    torch.cuda.synchronize()
+
+    osc = O.build_scene(og, of, ocam, s, active=oactive)
+    assert np.array_equal(sc.tet_ids.cpu().numpy().astype(np.int64), osc.tet_ids)
+    assert rel_err(sc.proj.cpu().numpy(), osc.proj) < 1e-12
+    # tile lists bit-exact on the same FP64 scene (the sort/binning stage)
+    sb = O.bin_and_sort(_oracle_scene_on(O, sc, ocam), ocam)
+    assert np.array_equal(b.starts.cpu().numpy(), sb.starts)
+    assert np.array_equal(b.items.cpu().numpy().astype(np.int64), sb.items)
+    # maps and gradients end to end against the oracle's own scene
+    ob = O.bin_and_sort(osc, ocam)
+    omaps, osaved = O.render_forward(osc, ob, ocam, save_state=True)
+    _check_maps(_maps_np(maps), omaps)
+    ogr = O.render_backward(osaved, osc, og, of, ocam, dm_np)
+    assert rel_err(gb.d_sdf.cpu().numpy(), ogr.d_sdf) < GRAD_TOL
+    assert rel_err(gb.d_deform.cpu().numpy(), ogr.d_deform) < GRAD_TOL
+
+
+def test_config3_regularizers(ts, O, cfg3):
+    og, of = cfg3
+    g = ts.build_grid(128)
+    f = _gpu_field(ts, g, of)
+    oactive = O.prefilter(og, of, 100.0)
+    le, ge = ts.eikonal_loss(g, f, torch.as_tensor(oactive.astype(np.int32), device="cuda"))
+    ln, gn = ts.normal_consistency_loss(g, f)
+    ole, oge = O.eikonal_loss(og, of, oactive)
+    oln, ogn = O.normal_consistency_loss(og, of)
+    assert abs(le - ole) <= 1e-9 * max(1.0, abs(ole))
+    assert abs(ln - oln) <= 1e-9 * max(1.0, abs(oln))
+    assert rel_err(ge.d_sdf.cpu().numpy(), oge.d_sdf) < 1e-6
+    assert rel_err(ge.d_deform.cpu().numpy(), oge.d_deform) < 1e-6
+    assert rel_err(gn.d_sdf.cpu().numpy(), ogn.d_sdf) < 1e-6
+    assert rel_err(gn.d_deform.cpu().numpy(), ogn.d_deform) < 1e-6
+
+
+# --- config 5: 256^3 Marching Tetrahedra + 2048^2 forward ----------------------------------
+
+def test_config5_marching_tets_bitexact(ts, O):
+    R = 256
+    og = O.build_grid(R, with_edges=False)
+    of = O.noisy_field(og, noise=0.002, seed=5)
+    g = ts.build_grid(R)
+    m = ts.marching_tetrahedra(g, _gpu_field(ts, g, of))
+    V, F = O.marching_tetrahedra(og, of)
+    del og
+    assert m.vertices.shape == V.shape and m.triangles.shape == F.shape
+    assert np.array_equal(m.vertices, V)
+    assert np.array_equal(m.triangles, F)
+
+
+def test_config5_forward_2048(ts, O):
+    R, S, s = 256, 2048, 100.0
+    g = ts.build_grid(R)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    cam = ts.orbit_camera(0, 8, width=S, height=S)
+    ocam = O.orbit_camera(0, 8, width=S, height=S)
+    sc = ts.build_scene(g, f, cam, s)
+    b = ts.bin_and_sort(sc, cam)
+    maps, _ = ts.render_forward(sc, b, cam)
+    torch.cuda.synchronize()
+    osc = _oracle_scene_on(O, sc, ocam)
+    ob = O.bin_and_sort(osc, ocam)
+    starts = b.starts.cpu().numpy()
+    assert np.array_equal(starts, ob.starts)
+    assert np.array_equal(b.items.cpu().numpy().astype(np.int64), ob.items)
+    lens = np.diff(starts)
+    touched = np.nonzero(lens)[0]
+    rng = np.random.default_rng(5)
+    tiles = np.union1d(np.argsort(lens, kind="stable")[-16:], rng.choice(touched, 48, replace=False))
+    omaps, _ = O.render_forward(osc, _restrict_bins(O, ob, tiles), ocam)
+    ts_ = ob.tile_size
+    gpu = _maps_np(maps)
+    for t in tiles:
+        y0, x0 = (t // ob.tiles_x) * ts_, (t % ob.tiles_x) * ts_
+        sl = (slice(y0, y0 + ts_), slice(x0, x0 + ts_))
+        for a, r in zip(gpu, (omaps.normal, omaps.depth, omaps.opacity)):
+            den = max(np.abs(r).max(), 1e-30)
+            assert np.abs(a[sl] - r[sl]).max() / den < MAP_TOL, t
