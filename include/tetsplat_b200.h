@@ -177,10 +177,13 @@ int ts_adam_step(int32_t resolution, const float* d_vert, double* sdf, double* d
                  double* v_sdf, double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1,
                  double beta2, int64_t t, double eps, double deform_limit, void* stream);
 
-/* Diagnostics: out4[0] = (pixel, splat) pairs re-decided in FP64 at a face edge or a
- * degenerate face, out4[1] = pairs re-decided in FP64 at an alpha threshold (since the
- * last reset).  [sync] */
-int ts_debug_counters(uint64_t* out4, int reset);
+/* Diagnostics (since the last reset): out8[0] = (pixel, splat) pairs re-decided in FP64 at
+ * a face edge or a degenerate face, out8[1] = pairs re-decided in FP64 at an alpha
+ * threshold, out8[2] = forward pairs evaluated, out8[3] = of [0], pairs of splats with a
+ * sign-uncertain face determinant; with debug flag 8: out8[4] / out8[5] = of [1], pairs
+ * within the f_prev - f_next error bound / near the tiny-alpha or clip bounds, out8[7] =
+ * re-decided pairs whose alpha needed the FP64 softplus chain.  [sync] */
+int ts_debug_counters(uint64_t* out8, int reset);
 
 /* Diagnostics for timing experiments only: bit 0 skips the exact FP64 re-decisions
  * (results then no longer match the reference).  Default 0. */

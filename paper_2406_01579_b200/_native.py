@@ -11,7 +11,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtetsplat_b200.so")
+LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(HERE, "libtetsplat_b200.so")  # override: A/B timing only
 
 TS_EINVAL = -1
 
@@ -114,8 +114,10 @@ def i64():
 
 
 def debug_counters(reset: bool = True):
-    """(edge FP64 re-decisions, alpha FP64 re-decisions, forward rect-pass pairs, 0) since last reset."""
-    out = (ctypes.c_uint64 * 4)()
+    """(edge FP64 re-decisions, alpha FP64 re-decisions, forward rect-pass pairs, uncertain-det
+    edge re-decisions, alpha re-decisions by reason [flag 8]: f band / tiny-or-clip, 0,
+    softplus-chain re-decisions [flag 8]) since last reset."""
+    out = (ctypes.c_uint64 * 8)()
     check(lib().ts_debug_counters(out, int(reset)))
     return tuple(int(v) for v in out)
 

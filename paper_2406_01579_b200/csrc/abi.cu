@@ -293,11 +293,11 @@ int ts_rasterize_mesh(const double* vertices, int64_t V, const int64_t* triangle
   return check_cuda("ts_rasterize_mesh");
 }
 
-int ts_debug_counters(uint64_t* out4, int reset) {
-  if (!out4) return fail(TS_EINVAL, "ts_debug_counters: null output");
-  unsigned long long c[4];
+int ts_debug_counters(uint64_t* out8, int reset) {
+  if (!out8) return fail(TS_EINVAL, "ts_debug_counters: null output");
+  unsigned long long c[8];
   ts_impl_counters(c, reset);
-  for (int i = 0; i < 4; ++i) out4[i] = c[i];
+  for (int i = 0; i < 8; ++i) out8[i] = c[i];
   return check_cuda("ts_debug_counters");
 }
 

@@ -91,7 +91,7 @@ int64_t ts_impl_nc_scratch_bytes(int R);
 int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
-void ts_impl_counters(unsigned long long out[4], int reset);
+void ts_impl_counters(unsigned long long out[8], int reset);
 int ts_impl_rasterize_mesh(const double* verts, int64_t V, const int64_t* tris, int64_t F, const ts::Camera& cam,
                            uint8_t* mask, double* depth, double* normal, cudaStream_t st);
 void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,

@@ -7,11 +7,14 @@
 //
 // normal consistency (_core.pyx:571-668, losses.py:39-52): two per-tet passes and three
 // vertex-centric GATHER passes over the implicit Kuhn grid (no atomics, deterministic):
-//   T1: per tet, unit normal g/|g| (or "undefined")                        [6R^3 threads]
+//   T1: per tet, unit normal g/|g| (or "undefined")   [one thread per cell: its 8 corners
+//       are loaded once for the cell's 6 tets]
 //   A : vertex mean of incident unit tet normals -> unit vertex normal (+ count, |mean|)
 //   B : per-vertex edge term  d_n(v) = -sum_{edge neighbours} n(b), projected back
 //       through the normalisation; per-vertex share of sum_edges (1 - n_a.n_b)
-//   T2: per tet, the chain through the tet normal: dL/df (4) and g            [6R^3 threads]
+//   T2: per tet, the chain through the tet normal: dL/df (4) and g   [one thread per cell]
+// Per-tet buffers are p-major (index p R^3 + x-fastest cell): T1/T2 store coalesced per
+// permutation and the vertex gathers read one contiguous run per (cell offset, p).
 //   C : per-vertex sum over incident tets of dL/df_slot and -dL/df_slot * g (the per-tet chain
 //       terms are stored in FP32 — they only feed the FP32 gradient buffer; sums in FP64)
 // Each tet's FP64 work is done once (not once per incident vertex), and incident tets are
@@ -78,61 +81,109 @@ __global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __res
 }
 
 // Incident tets of vertex (x,y,z) in increasing tet id.  Calls fn(buffer index, local slot),
-// buffer index = x-fastest cell index * 6 + p (see nc_tet_id).
+// buffer index = p * R^3 + x-fastest cell index (see nc_tet_id).
 template <class Fn>
 __device__ __forceinline__ void for_incident_tets(uint32_t vid, const Grid& G, Fn&& fn) {
   const int R = G.R;
   int x, y, z;
   vertex_xyz(vid, G, x, y, z);
+#pragma unroll
   for (int dx = 1; dx >= 0; --dx)
+#pragma unroll
     for (int dy = 1; dy >= 0; --dy)
+#pragma unroll
       for (int dz = 1; dz >= 0; --dz) {
         const int cx = x - dx, cy = y - dy, cz = z - dz;
         if (cx < 0 || cy < 0 || cz < 0 || cx >= R || cy >= R || cz >= R) continue;
         const int lc = dx | (dy << 1) | (dz << 2);
-        // per-tet NC buffers are laid out x-fastest (like vertex ids), not in tet-id order, so
-        // neighbouring vertices read neighbouring cells
+        // per-tet NC buffers are p-major with cells x-fastest (like vertex ids), not in tet-id
+        // order: a warp of neighbouring vertices reads one contiguous run per (cell offset, p)
         const uint32_t cell = ((uint32_t)cz * (uint32_t)R + (uint32_t)cy) * (uint32_t)R + (uint32_t)cx;
+        const uint32_t C = (uint32_t)R * (uint32_t)R * (uint32_t)R;
+#pragma unroll
         for (int p = 0; p < 6; ++p) {
           const int k1 = 1 << perm_a0(p), k2 = k1 | (1 << perm_a1(p));
           if (lc == 0 || lc == 7 || lc == k1 || lc == k2) {
             // local slot of the vertex in the tet (tet_corners: odd permutations swap 2 and 3)
             const bool odd = (p == 1 || p == 2 || p == 5);
             const int slot = lc == 0 ? 0 : (lc == k1 ? 1 : ((lc == k2) != odd ? 2 : 3));
-            fn(cell * 6u + (uint32_t)p, slot);
+            fn((uint32_t)p * C + cell, slot);
           }
         }
       }
 }
 
-// tet id of per-tet NC buffer index i (cells x-fastest there, z-fastest in tet ids)
-__device__ __forceinline__ uint32_t nc_tet_id(int64_t i, const Grid& G) {
-  const uint32_t cell = (uint32_t)(i / 6), p = (uint32_t)(i - (int64_t)cell * 6);
-  const uint32_t q = G.dR.div(cell);  // cy + R cz
-  const uint32_t cx = cell - q * (uint32_t)G.R;
-  const uint32_t cz = G.dR.div(q);
-  const uint32_t cy = q - cz * (uint32_t)G.R;
-  return ((cx * (uint32_t)G.R + cy) * (uint32_t)G.R + cz) * 6u + p;
-}
-
-// pass T1: per-tet unit normal (w = 1) or undefined (all 0)
-__global__ void __launch_bounds__(256) k_nc_tet_normals(int64_t T, Grid G, const double* __restrict__ sdf,
-                                                        const double* __restrict__ deform, double4* __restrict__ tn) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t v[4];
-    double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
-    load_tet(nc_tet_id(t, G), G, sdf, deform, v, P, f);
-    tet_gradient(P, f, g, c1, c2, c3);
-    const double nrm = gnorm3(g);
-    tn[t] = nrm < kEpsNormal ? make_double4(0.0, 0.0, 0.0, 0.0)
-                             : make_double4(ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm), 1.0);
+// The 8 corners of cell (cx, cy, cz) — deformed positions and SDF (corner bit 0 = +x,
+// bit 1 = +y, bit 2 = +z), loaded once for the cell's 6 tets.
+struct CellCorners {
+  double P[8][3], f[8];
+  uint32_t v[8];
+};
+__device__ __forceinline__ void load_cell(uint32_t c, const Grid& G, const double* __restrict__ sdf,
+                                          const double* __restrict__ deform, CellCorners& K) {
+  const uint32_t q = G.dR.div(c);  // cy + R cz
+  const int cx = (int)(c - q * (uint32_t)G.R);
+  const uint32_t czu = G.dR.div(q);
+  const int cy = (int)(q - czu * (uint32_t)G.R), cz = (int)czu;
+#pragma unroll
+  for (int lc = 0; lc < 8; ++lc) {
+    const int xyz[3] = {cx + (lc & 1), cy + ((lc >> 1) & 1), cz + ((lc >> 2) & 1)};
+    K.v[lc] = (uint32_t)xyz[0] + (uint32_t)G.n * ((uint32_t)xyz[1] + (uint32_t)G.n * (uint32_t)xyz[2]);
+    vertex_pos_xyz(xyz, K.v[lc], G, deform, K.P[lc]);
+    K.f[lc] = __ldg(sdf + K.v[lc]);
   }
 }
 
-// pass A: nv = normalized mean of incident unit normals; cnt; an (0 = undefined)
+// corner of local slot `slot` of permutation p (tet_corners: odd permutations swap 2 and 3)
+__host__ __device__ constexpr int perm_corner(int p, int slot) {
+  return slot == 0 ? 0
+                   : (slot == 1 ? (1 << perm_a0(p))
+                                : (((slot == 2) != (p == 1 || p == 2 || p == 5)) ? ((1 << perm_a0(p)) | (1 << perm_a1(p)))
+                                                                                 : 7));
+}
+
+template <int p>
+__device__ __forceinline__ void cell_tet(const CellCorners& K, uint32_t v[4], double P[4][3], double f[4]) {
+#pragma unroll
+  for (int sl = 0; sl < 4; ++sl) {
+    const int lc = perm_corner(p, sl);
+    v[sl] = K.v[lc];
+    f[sl] = K.f[lc];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) P[sl][i] = K.P[lc][i];
+  }
+}
+
+// pass T1: per-tet unit normal (w = 1) or undefined (all 0); one thread per cell, 6 tets
+template <int p>
+__device__ __forceinline__ void t1_tet(const CellCorners& K, double4* __restrict__ out) {
+  uint32_t v[4];
+  double P[4][3], f[4], g[3], c1[3], c2[3], c3[3];
+  cell_tet<p>(K, v, P, f);
+  tet_gradient(P, f, g, c1, c2, c3);
+  const double nrm = gnorm3(g);
+  *out = nrm < kEpsNormal ? make_double4(0.0, 0.0, 0.0, 0.0)
+                          : make_double4(ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm), 1.0);
+}
+
+__global__ void __launch_bounds__(256) k_nc_tet_normals(int64_t C, Grid G, const double* __restrict__ sdf,
+                                                        const double* __restrict__ deform, double4* __restrict__ tn) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+    CellCorners K;
+    load_cell((uint32_t)c, G, sdf, deform, K);
+    t1_tet<0>(K, tn + c);
+    t1_tet<1>(K, tn + C + c);
+    t1_tet<2>(K, tn + 2 * C + c);
+    t1_tet<3>(K, tn + 3 * C + c);
+    t1_tet<4>(K, tn + 4 * C + c);
+    t1_tet<5>(K, tn + 5 * C + c);
+  }
+}
+
+// pass A: nv = normalized mean of incident unit normals, .w = |mean| (0 = undefined);
+// icnt = 1 / count (0 without a defined incident tet)
 __global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, const double4* __restrict__ tn,
-                                                           double* __restrict__ nv, double* __restrict__ cnt,
-                                                           double* __restrict__ an) {
+                                                           double4* __restrict__ nv, double* __restrict__ icnt) {
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double s[3] = {0.0, 0.0, 0.0}, c = 0.0;
@@ -153,15 +204,15 @@ __global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, co
         for (int i = 0; i < 3; ++i) s[i] = ddiv(s[i], m);
       }
     }
-    for (int i = 0; i < 3; ++i) nv[vid * 3 + i] = s[i];
-    cnt[vid] = c != 0.0 ? ddiv(1.0, c) : 0.0;  // stored as the reciprocal the chain pass uses
-    an[vid] = a;
+    nv[vid] = make_double4(s[0], s[1], s[2], a);
+    icnt[vid] = c != 0.0 ? ddiv(1.0, c) : 0.0;  // the reciprocal the chain pass uses
   }
 }
 
-// pass B: edge penalty and its gradient, pushed back through the vertex normalisation
-__global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const double* __restrict__ nv,
-                                                  const double* __restrict__ an, double* __restrict__ dm,
+// pass B: edge penalty and its gradient, pushed back through the vertex normalisation; the
+// result is stored pre-multiplied by 1/count (the factor the tet chain applies per vertex)
+__global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const double4* __restrict__ nv,
+                                                  const double* __restrict__ icnt, double4* __restrict__ dmi,
                                                   double* __restrict__ loss) {
   const int64_t n = G.n;
   // Kuhn edge offsets (grid.py:106-107) as vertex-id deltas, ascending
@@ -173,92 +224,117 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const doubl
     int x, y, z;
     vertex_xyz((uint32_t)vid, G, x, y, z);
     double d[3] = {0.0, 0.0, 0.0};
-    const bool def = an[vid] != 0.0;
-    const double a0 = nv[vid * 3], a1 = nv[vid * 3 + 1], a2 = nv[vid * 3 + 2];
-    // lower neighbours (ascending id = descending delta), then upper ones
+    const double4 A = nv[vid];
+    const bool def = A.w != 0.0;
+    // neighbour records loaded up front, 7 at a time (independent loads), then the FP64
+    // sums in order: lower neighbours (ascending id = descending delta), then upper ones
+    double4 nb[7];
+#pragma unroll
+    for (int e = 0; e < 7; ++e)
+      nb[e] = def && x - ox[e] >= 0 && y - oy[e] >= 0 && z - oz[e] >= 0 ? nv[vid - off[e]]
+                                                                        : make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
     for (int e = 6; e >= 0; --e) {
-      if (x - ox[e] < 0 || y - oy[e] < 0 || z - oz[e] < 0) continue;
-      const int64_t b = vid - off[e];
-      if (!def || an[b] == 0.0) continue;
-      for (int i = 0; i < 3; ++i) d[i] = dsub(d[i], nv[b * 3 + i]);
+      if (nb[e].w == 0.0) continue;
+      d[0] = dsub(d[0], nb[e].x);
+      d[1] = dsub(d[1], nb[e].y);
+      d[2] = dsub(d[2], nb[e].z);
     }
+#pragma unroll
+    for (int e = 0; e < 7; ++e)
+      nb[e] = def && x + ox[e] < n && y + oy[e] < n && z + oz[e] < n ? nv[vid + off[e]]
+                                                                     : make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
     for (int e = 0; e < 7; ++e) {
-      if (x + ox[e] >= n || y + oy[e] >= n || z + oz[e] >= n) continue;
-      const int64_t b = vid + off[e];
-      if (!def || an[b] == 0.0) continue;
-      const double b0 = nv[b * 3], b1 = nv[b * 3 + 1], b2 = nv[b * 3 + 2];
-      local += dsub(1.0, dadd(dadd(dmul(a0, b0), dmul(a1, b1)), dmul(a2, b2)));
-      d[0] = dsub(d[0], b0);
-      d[1] = dsub(d[1], b1);
-      d[2] = dsub(d[2], b2);
+      const double4 B = nb[e];
+      if (B.w == 0.0) continue;
+      local += dsub(1.0, dadd(dadd(dmul(A.x, B.x), dmul(A.y, B.y)), dmul(A.z, B.z)));
+      d[0] = dsub(d[0], B.x);
+      d[1] = dsub(d[1], B.y);
+      d[2] = dsub(d[2], B.z);
     }
     if (def) {
-      double dot = dadd(dadd(dmul(a0, d[0]), dmul(a1, d[1])), dmul(a2, d[2]));
-      const double av = an[vid];
-      d[0] = ddiv(dsub(d[0], dmul(a0, dot)), av);
-      d[1] = ddiv(dsub(d[1], dmul(a1, dot)), av);
-      d[2] = ddiv(dsub(d[2], dmul(a2, dot)), av);
+      double dot = dadd(dadd(dmul(A.x, d[0]), dmul(A.y, d[1])), dmul(A.z, d[2]));
+      d[0] = ddiv(dsub(d[0], dmul(A.x, dot)), A.w);
+      d[1] = ddiv(dsub(d[1], dmul(A.y, dot)), A.w);
+      d[2] = ddiv(dsub(d[2], dmul(A.z, dot)), A.w);
     }
-    for (int i = 0; i < 3; ++i) dm[vid * 3 + i] = d[i];
+    const double ic = icnt[vid];
+    dmi[vid] = make_double4(d[0] * ic, d[1] * ic, d[2] * ic, 0.0);
   }
   block_add_to(local, loss);
 }
 
 // pass T2: per-tet chain through the tet normal (_core.pyx:651-667): dL/df per slot and g
-// (zeros where the reference skips the tet)
-__global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t T, Grid G, const double* __restrict__ sdf,
-                                                      const double* __restrict__ deform,
-                                                      const double* __restrict__ icnt, const double* __restrict__ dm,
-                                                      float4* __restrict__ tdf, float4* __restrict__ tg) {
+// (zeros where the reference skips the tet); one thread per cell, 6 tets
+template <int p>
+__device__ __forceinline__ void t2_tet(const CellCorners& K, const double4* __restrict__ dmi, float4* __restrict__ tdf,
+                                       float4* __restrict__ tg) {
   // FP64 throughout, but with reciprocals instead of the reference's repeated divisions: the
   // results are rounded to FP32 for the gradient buffer anyway (the skip tests are unchanged)
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t v[4];
-    double P[4][3], f[4];
-    load_tet(nc_tet_id(t, G), G, sdf, deform, v, P, f);
-    double e1[3], e2[3], e3[3], c1[3], c2[3], c3[3];
-    for (int i = 0; i < 3; ++i) {
-      e1[i] = P[1][i] - P[0][i];
-      e2[i] = P[2][i] - P[0][i];
-      e3[i] = P[3][i] - P[0][i];
-    }
-    c1[0] = e2[1] * e3[2] - e2[2] * e3[1];
-    c1[1] = e2[2] * e3[0] - e2[0] * e3[2];
-    c1[2] = e2[0] * e3[1] - e2[1] * e3[0];
-    c2[0] = e3[1] * e1[2] - e3[2] * e1[1];
-    c2[1] = e3[2] * e1[0] - e3[0] * e1[2];
-    c2[2] = e3[0] * e1[1] - e3[1] * e1[0];
-    c3[0] = e1[1] * e2[2] - e1[2] * e2[1];
-    c3[1] = e1[2] * e2[0] - e1[0] * e2[2];
-    c3[2] = e1[0] * e2[1] - e1[1] * e2[0];
-    const double det = e1[0] * c1[0] + e1[1] * c1[1] + e1[2] * c1[2];
-    float4 o = make_float4(0.f, 0.f, 0.f, 0.f), og = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (det != 0.0) {
-      const double idet = 1.0 / det;
-      const double d1 = f[1] - f[0], d2 = f[2] - f[0], d3 = f[3] - f[0];
-      double g[3];
-      for (int i = 0; i < 3; ++i) g[i] = (d1 * c1[i] + d2 * c2[i] + d3 * c3[i]) * idet;
-      const double nrm = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-      if (!(nrm < kEpsNormal)) {
-        const double inrm = 1.0 / nrm;
-        const double nt[3] = {g[0] * inrm, g[1] * inrm, g[2] * inrm};
-        double dnt[3] = {0.0, 0.0, 0.0};
-        for (int c = 0; c < 4; ++c) {
-          const double inv = icnt[v[c]];
-          for (int i = 0; i < 3; ++i) dnt[i] += dm[v[c] * 3 + i] * inv;
-        }
-        const double dot = nt[0] * dnt[0] + nt[1] * dnt[1] + nt[2] * dnt[2];
-        double dg[3];
-        for (int i = 0; i < 3; ++i) dg[i] = (dnt[i] - nt[i] * dot) * inrm;
-        const double k1 = (c1[0] * dg[0] + c1[1] * dg[1] + c1[2] * dg[2]) * idet;
-        const double k2 = (c2[0] * dg[0] + c2[1] * dg[1] + c2[2] * dg[2]) * idet;
-        const double k3 = (c3[0] * dg[0] + c3[1] * dg[1] + c3[2] * dg[2]) * idet;
-        o = make_float4((float)(-(k1 + k2 + k3)), (float)k1, (float)k2, (float)k3);
-        og = make_float4((float)g[0], (float)g[1], (float)g[2], 1.f);
+  uint32_t v[4];
+  double P[4][3], f[4];
+  cell_tet<p>(K, v, P, f);
+  double e1[3], e2[3], e3[3], c1[3], c2[3], c3[3];
+  for (int i = 0; i < 3; ++i) {
+    e1[i] = P[1][i] - P[0][i];
+    e2[i] = P[2][i] - P[0][i];
+    e3[i] = P[3][i] - P[0][i];
+  }
+  c1[0] = e2[1] * e3[2] - e2[2] * e3[1];
+  c1[1] = e2[2] * e3[0] - e2[0] * e3[2];
+  c1[2] = e2[0] * e3[1] - e2[1] * e3[0];
+  c2[0] = e3[1] * e1[2] - e3[2] * e1[1];
+  c2[1] = e3[2] * e1[0] - e3[0] * e1[2];
+  c2[2] = e3[0] * e1[1] - e3[1] * e1[0];
+  c3[0] = e1[1] * e2[2] - e1[2] * e2[1];
+  c3[1] = e1[2] * e2[0] - e1[0] * e2[2];
+  c3[2] = e1[0] * e2[1] - e1[1] * e2[0];
+  const double det = e1[0] * c1[0] + e1[1] * c1[1] + e1[2] * c1[2];
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f), og = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (det != 0.0) {
+    const double idet = 1.0 / det;
+    const double d1 = f[1] - f[0], d2 = f[2] - f[0], d3 = f[3] - f[0];
+    double g[3];
+    for (int i = 0; i < 3; ++i) g[i] = (d1 * c1[i] + d2 * c2[i] + d3 * c3[i]) * idet;
+    const double nrm = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (!(nrm < kEpsNormal)) {
+      const double inrm = 1.0 / nrm;
+      const double nt[3] = {g[0] * inrm, g[1] * inrm, g[2] * inrm};
+      double dnt[3] = {0.0, 0.0, 0.0};
+      for (int c = 0; c < 4; ++c) {
+        const double4 m = dmi[v[c]];
+        dnt[0] += m.x;
+        dnt[1] += m.y;
+        dnt[2] += m.z;
       }
+      const double dot = nt[0] * dnt[0] + nt[1] * dnt[1] + nt[2] * dnt[2];
+      double dg[3];
+      for (int i = 0; i < 3; ++i) dg[i] = (dnt[i] - nt[i] * dot) * inrm;
+      const double k1 = (c1[0] * dg[0] + c1[1] * dg[1] + c1[2] * dg[2]) * idet;
+      const double k2 = (c2[0] * dg[0] + c2[1] * dg[1] + c2[2] * dg[2]) * idet;
+      const double k3 = (c3[0] * dg[0] + c3[1] * dg[1] + c3[2] * dg[2]) * idet;
+      o = make_float4((float)(-(k1 + k2 + k3)), (float)k1, (float)k2, (float)k3);
+      og = make_float4((float)g[0], (float)g[1], (float)g[2], 1.f);
     }
-    tdf[t] = o;
-    tg[t] = og;
+  }
+  *tdf = o;
+  *tg = og;
+}
+
+__global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t C, Grid G, const double* __restrict__ sdf,
+                                                      const double* __restrict__ deform,
+                                                      const double4* __restrict__ dmi, float4* __restrict__ tdf,
+                                                      float4* __restrict__ tg) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+    CellCorners K;
+    load_cell((uint32_t)c, G, sdf, deform, K);
+    t2_tet<0>(K, dmi, tdf + c, tg + c);
+    t2_tet<1>(K, dmi, tdf + C + c, tg + C + c);
+    t2_tet<2>(K, dmi, tdf + 2 * C + c, tg + 2 * C + c);
+    t2_tet<3>(K, dmi, tdf + 3 * C + c, tg + 3 * C + c);
+    t2_tet<4>(K, dmi, tdf + 4 * C + c, tg + 4 * C + c);
+    t2_tet<5>(K, dmi, tdf + 5 * C + c, tg + 5 * C + c);
   }
 }
 
@@ -340,7 +416,7 @@ void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32
 // scratch layout of the normal-consistency passes (16-byte aligned pieces)
 static void nc_layout(int R, int64_t off[8]) {
   const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
-  const int64_t sz[7] = {24 * N, 24 * N, 8 * N, 8 * N, 32 * T, 16 * T, 16 * T};  // nv dm cnt an tn tdf tg
+  const int64_t sz[7] = {32 * N, 32 * N, 8 * N, 0, 32 * T, 16 * T, 16 * T};  // nv dmi icnt - tn tdf tg
   off[0] = 0;
   for (int i = 0; i < 7; ++i) off[i + 1] = off[i] + ((sz[i] + 255) & ~255ll);
 }
@@ -360,20 +436,20 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   nc_layout(R, off);
   char* base = static_cast<char*>(scratch);
   if (!base) cudaMallocAsync(reinterpret_cast<void**>(&base), off[7], st);
-  double* nv = reinterpret_cast<double*>(base + off[0]);
-  double* dm = reinterpret_cast<double*>(base + off[1]);
-  double* cnt = reinterpret_cast<double*>(base + off[2]);
-  double* an = reinterpret_cast<double*>(base + off[3]);
-  double4* tn = reinterpret_cast<double4*>(base + off[4]);  // T1: unit tet normals (FP64: they feed the loss)
-  float4* tdf = reinterpret_cast<float4*>(base + off[5]);   // T2: per-tet chain terms (FP32: gradient only)
+  double4* nv = reinterpret_cast<double4*>(base + off[0]);   // A: unit vertex normals, .w = |mean|
+  double4* dmi = reinterpret_cast<double4*>(base + off[1]);  // B: edge terms / count
+  double* icnt = reinterpret_cast<double*>(base + off[2]);
+  double4* tn = reinterpret_cast<double4*>(base + off[4]);   // T1: unit tet normals (FP64: they feed the loss)
+  float4* tdf = reinterpret_cast<float4*>(base + off[5]);    // T2: per-tet chain terms (FP32: gradient only)
   float4* tg = reinterpret_cast<float4*>(base + off[6]);
   const Grid G = make_grid(R);
+  const int64_t C = T / 6;
   const int vblocks = (int)((N + 255) / 256 < 148 * 8 ? (N + 255) / 256 : 148 * 8);
-  const int tblocks = (int)((T + 255) / 256 < 148 * 16 ? (T + 255) / 256 : 148 * 16);
-  k_nc_tet_normals<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, tn);
-  k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tn, nv, cnt, an);
-  k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, an, dm, loss);
-  k_nc_tet_chain<<<tblocks, 256, 0, st>>>(T, G, sdf, deform, cnt, dm, tdf, tg);
+  const int cblocks = (int)((C + 255) / 256 < 148 * 8 ? (C + 255) / 256 : 148 * 8);
+  k_nc_tet_normals<<<cblocks, 256, 0, st>>>(C, G, sdf, deform, tn);
+  k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tn, nv, icnt);
+  k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, icnt, dmi, loss);
+  k_nc_tet_chain<<<cblocks, 256, 0, st>>>(C, G, sdf, deform, dmi, tdf, tg);
   k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert);
   if (!scratch) cudaFreeAsync(base, st);
 }

@@ -14,7 +14,7 @@ dm = ts.RenderMaps(torch.randn((S, S, 3), device="cuda", generator=gen), torch.r
 act = ts.prefilter(g, f, s)
 sc = ts.build_scene(g, f, cam, s, active=act)
 b = ts.bin_and_sort(sc, cam)
-for flags in (0, 4):
+for flags in (0, 8, 4):
     _native.check(_native.lib().ts_debug_set_flags(flags))
     _native.debug_phases(reset=True)
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
