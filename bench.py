@@ -396,6 +396,7 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
         act = ts.prefilter(g, field, s)
         sc = ts.build_scene(g, field, cam, s, active=act)
         b = ts.bin_and_sort(sc, cam)
+        _native.check(_native.lib().ts_debug_set_flags(16 if r == 0 else 0))  # count evaluated pairs once
         _native.debug_counters(True)
         ef = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         eb = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -404,6 +405,7 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
         torch.cuda.synchronize()
         if r == 0:
             cnt = _native.debug_counters(True)
+            _native.check(_native.lib().ts_debug_set_flags(0))
             P_pop = int(sv.n_proc.sum())
             B = int(sv.n_blend.sum())
             K_a, K_v, M = int(act.numel()), len(sc), b.num_pairs

@@ -73,9 +73,12 @@ static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 
 // diagnostics: [0] pairs re-decided in FP64 at a face edge / degenerate face,
 // [1] pairs re-decided in FP64 at an alpha threshold, [2] forward pairs evaluated, [3] of [0],
-// pairs of splats with a sign-uncertain FP32 face determinant
-__device__ unsigned long long g_ts_counters[4];
-// diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity)
+// pairs of splats with a sign-uncertain FP32 face determinant; [4..6] of [1], by reason:
+// |f_prev - f_next| within the FP32 f error bound, alpha below the tiny-alpha bound or near
+// ALPHA_CLIP; [7] re-decided pairs whose alpha needed the FP64 softplus chain
+__device__ unsigned long long g_ts_counters[8];
+// diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity),
+// bit 4 = count the pairs phase A evaluates (g_ts_counters[2])
 __device__ int g_ts_debug_flags;
 // diagnostics only (flag bit 1): per-tile forward start/end globaltimer, SM id
 __device__ unsigned long long g_ts_tile_time[2 * 65536];
@@ -307,6 +310,7 @@ __device__ __forceinline__ bool exact_group(const Scene64& S, bool act, int64_t 
   if (ok && !certain && (fi == 1 || fi == 2)) spv = softplus_d(fi == 1 ? x : y);
   const double spx = __shfl_sync(0xffffffffu, spv, lead + 1), spy = __shfl_sync(0xffffffffu, spv, lead + 2);
   if (!ok || fi != 0) return false;
+  if ((g_ts_debug_flags & 8) && !certain) atomicAdd(&g_ts_counters[7], 1ull);
   const float sf = (float)s;
   if (certain) {
     if (a_est < 0.f) return false;
@@ -365,6 +369,11 @@ __device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, f
       }
     }
     atomicAdd(&g_ts_counters[1], 1ull);
+    if (g_ts_debug_flags & 8) {
+      const float dfl = h.fp - h.fn;
+      const float ftol = r.fband * frcp(fminf(r.adet[h.fip], r.adet[h.fin])) + r.ftol0;
+      atomicAdd(&g_ts_counters[fabsf(dfl) <= ftol ? 4 : 5], 1ull);
+    }
   } else {
     atomicAdd(&g_ts_counters[0], 1ull);
     if (r.flags & 16u) atomicAdd(&g_ts_counters[3], 1ull);
@@ -574,7 +583,7 @@ struct FwdSmem {
   uint16_t cand[kWarps][64];  // per warp: candidate pairs (it | face mask << 11) of phase A1
   uint32_t cbits[kCap / 32];  // the chunk's blend bits (pair index within the chunk)
   int nex;
-  unsigned npairs;  // diagnostics: pairs evaluated by phase A
+  unsigned npairs;  // diagnostics (flag bit 4): pairs evaluated by phase A
   RectTab R;
   Prefetch pf;
   long long phase[8];  // diagnostics (flag bit 2)
@@ -624,6 +633,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
   if (threadIdx.x == 0) F.npairs = 0;
+  const bool count_pairs = g_ts_debug_flags & 16;
   const bool ptime = (g_ts_debug_flags & 4) && threadIdx.x == 0;
   long long* pacc = F.phase;
   if (ptime) {
@@ -690,8 +700,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
             cand = (fm & 16u) || __popc(fm) >= 2;
           }
         }
-        const unsigned cm = __ballot_sync(0xffffffffu, cand), em = __ballot_sync(0xffffffffu, ev);
-        if (lane == 0) atomicAdd(&F.npairs, __popc(em));
+        const unsigned cm = __ballot_sync(0xffffffffu, cand);
+        if (count_pairs) {
+          const unsigned em = __ballot_sync(0xffffffffu, ev);
+          if (lane == 0) atomicAdd(&F.npairs, __popc(em));
+        }
         if (cand) cq[cnt + __popc(cm & ((1u << lane) - 1u))] = (uint16_t)(it | (fm << 11));
         cnt += __popc(cm);
         __syncwarp();
@@ -775,7 +788,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     n_proc[p] = nproc;
     n_blend[p] = nb;
   }
-  if (threadIdx.x == 0) atomicAdd(&g_ts_counters[2], (unsigned long long)F.npairs);
+  if (count_pairs && threadIdx.x == 0) atomicAdd(&g_ts_counters[2], (unsigned long long)F.npairs);
   if (timing && threadIdx.x == 0) g_ts_tile_time[2 * tile + 1] = gtimer();
   if (ptime)
     for (int k = 0; k < 7; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
@@ -1435,10 +1448,10 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   put_tmp(torder, given_order, st);
 }
 
-void ts_impl_counters(unsigned long long out[4], int reset) {
-  cudaMemcpyFromSymbol(out, g_ts_counters, sizeof(unsigned long long) * 4);
+void ts_impl_counters(unsigned long long out[8], int reset) {
+  cudaMemcpyFromSymbol(out, g_ts_counters, sizeof(unsigned long long) * 8);
   if (reset) {
-    unsigned long long z[4] = {0, 0, 0, 0};
+    unsigned long long z[8] = {};
     cudaMemcpyToSymbol(g_ts_counters, z, sizeof(z));
   }
 }

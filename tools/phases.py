@@ -15,7 +15,7 @@ act = ts.prefilter(g, f, s)
 sc = ts.build_scene(g, f, cam, s, active=act)
 b = ts.bin_and_sort(sc, cam)
 for flags in (0, 8, 4):
-    _native.check(_native.lib().ts_debug_set_flags(flags))
+    _native.check(_native.lib().ts_debug_set_flags(flags | 16))
     _native.debug_phases(reset=True)
     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     maps, sv = ts.render_forward(sc, b, cam, save_state=True, timing=(e[0], e[1]))
