@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-stress", action="store_true", help="skip the config-5 (256^3, 2048^2) stress figures")
     p.add_argument("--resolution", type=int, default=R_GRID)
     p.add_argument("--image", type=int, default=IMG)
     p.add_argument("--s", type=float, default=STEEP)
@@ -367,12 +368,52 @@ def run_gpu(args):
             "clocks": clk.result, "roofline": roof, "kernels": kernels, "kernel_ms_per_step": ktab,
             "workload_counts": {"active_tets": stats.active, "splats_view0": stats.splats[:1],
                                 "pairs_view0": stats.pairs[:1]}}
+    if world == 1 and not args.no_stress:
+        line["stress"] = stress_probe(ts)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, world)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def stress_probe(ts, R=256, S=2048, s=STEEP, reps=3):
+    """BASELINE.json configs[4] (large-grid stress): Marching Tetrahedra of the 256^3 sphere
+    field and a 2048^2 forward render (prefilter + scene + bins + compositing) of orbit view
+    0 — reported beside the headline, not part of it.  Device time with CUDA events; MT's
+    host readback of the mesh is included (its API returns host arrays)."""
+    import torch
+    g = ts.build_grid(R)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    cam = ts.orbit_camera(0, 8, width=S, height=S)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    mt_ms, fw_ms, comp_ms = [], [], []
+    for r in range(reps + 1):
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        mesh = ts.marching_tetrahedra(g, f)
+        e1.record()
+        e1.synchronize()
+        e2, e3, c0, c1 = ev(), ev(), ev(), ev()
+        e2.record()
+        act = ts.prefilter(g, f, s)
+        sc = ts.build_scene(g, f, cam, s, active=act)
+        b = ts.bin_and_sort(sc, cam)
+        maps, _ = ts.render_forward(sc, b, cam, timing=(c0, c1))
+        e3.record()
+        e3.synchronize()
+        if r:
+            mt_ms.append(e0.elapsed_time(e1))
+            fw_ms.append(e2.elapsed_time(e3))
+            comp_ms.append(c0.elapsed_time(c1))
+    med = lambda v: sorted(v)[len(v) // 2]
+    return {"config": f"configs[4]: {R}^3 grid (sphere r=0.5), MT + {S}x{S} forward render, s={s:g}",
+            "mt_ms": med(mt_ms), "mt_vertices": int(mesh.vertices.shape[0]),
+            "mt_triangles": int(mesh.triangles.shape[0]),
+            "forward_ms": med(fw_ms), "forward_renders_per_s": 1e3 / med(fw_ms), "compositing_ms": med(comp_ms),
+            "splats": len(sc), "pairs": int(b.num_pairs), "timing": f"CUDA events, median of {reps}"}
 
 
 def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
