@@ -146,13 +146,29 @@ int ts_eikonal(const double* sdf, const double* deform, int32_t resolution, cons
 int ts_normal_consistency(const double* sdf, const double* deform, int32_t resolution, double scale, float* d_vert,
                           double* loss, void* stream);
 
-/* K9 marching_tetrahedra (grid.py:136-239), phase 1: counts.  [sync] */
+/* K9 marching_tetrahedra (grid.py:136-239) in one pass: the welded mesh is built into
+ * device buffers owned by *out_handle; *out_num_verts / *out_num_tris are its final sizes.
+ * Replaces the reference's grid.marching_tetrahedra (grid.py:136) call.  [sync] */
+int ts_marching_tets_run(const double* sdf, const double* deform, int32_t resolution, void** out_handle,
+                         int64_t* out_num_verts, int64_t* out_num_tris, void* stream);
+
+/* Copy a ts_marching_tets_run result into caller buffers — host or device memory —
+ * vertices f64[V,3] (lexicographic (x, y, z)), triangles i64[F,3] (group order of
+ * grid.py:192-214, oriented, degenerates removed).  [sync] */
+int ts_marching_tets_fetch(void* handle, double* vertices, int64_t* triangles);
+
+/* Free a ts_marching_tets_run result (after any number of fetches). */
+int ts_marching_tets_release(void* handle);
+
+/* K9 counts only: the final vertex / triangle counts (capacities for ts_marching_tets).
+ * [sync] */
 int ts_marching_tets_count(const double* sdf, const double* deform, int32_t resolution, int64_t* out_num_verts,
                            int64_t* out_num_tris, void* stream);
 
-/* K9 phase 2: vertices f64[V,3] (welded, lexicographic (x, y, z)) and triangles i64[F,3]
- * (group order of grid.py:192-214, oriented, degenerates removed); capacities = the
- * counts of phase 1.  out_counts[0] = final F, out_counts[1] = welded V (host).  [sync] */
+/* K9 into caller device buffers: vertices f64[V,3] (welded, lexicographic (x, y, z)) and
+ * triangles i64[F,3] (group order of grid.py:192-214, oriented, degenerates removed);
+ * capacities >= ts_marching_tets_count's.  out_counts[0] = F, out_counts[1] = V (host).
+ * [sync] */
 int ts_marching_tets(const double* sdf, const double* deform, int32_t resolution, double* vertices,
                      int64_t* triangles, int64_t* out_counts, void* stream);
 

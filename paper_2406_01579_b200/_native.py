@@ -68,6 +68,9 @@ def lib():
         "ts_rasterize_mesh": ([P, I64, P, I64, pc, P, P, P, P], ctypes.c_int),
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),
         "ts_marching_tets": ([P, P, I32, P, P, ctypes.POINTER(ctypes.c_int64), P], ctypes.c_int),
+        "ts_marching_tets_run": ([P, P, I32, ctypes.POINTER(P), PI64, PI64, P], ctypes.c_int),
+        "ts_marching_tets_fetch": ([P, P, P], ctypes.c_int),
+        "ts_marching_tets_release": ([P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
         "ts_debug_phases": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),

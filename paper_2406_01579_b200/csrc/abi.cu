@@ -269,14 +269,38 @@ int ts_normal_consistency_ws(const double* sdf, const double* deform, int32_t R,
 
 int ts_marching_tets_count(const double* sdf, const double* deform, int32_t R, int64_t* nv, int64_t* nt,
                            void* stream) {
+  keep_pool_warm();
   if (!sdf || !deform || !nv || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets_count: bad arguments");
   int rc = ts_impl_mt_count(sdf, deform, R, nv, nt, ST(stream));
   if (rc) return fail(rc, "ts_marching_tets_count failed");
   return check_cuda("ts_marching_tets_count");
 }
 
+int ts_marching_tets_run(const double* sdf, const double* deform, int32_t R, void** handle, int64_t* nv,
+                         int64_t* nt, void* stream) {
+  keep_pool_warm();
+  if (!sdf || !deform || !handle || !nv || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets_run: bad arguments");
+  *handle = nullptr;
+  int rc = ts_impl_mt_run(sdf, deform, R, handle, nv, nt, ST(stream));
+  if (rc) return fail(rc, "ts_marching_tets_run failed");
+  return check_cuda("ts_marching_tets_run");
+}
+
+int ts_marching_tets_fetch(void* handle, double* vertices, int64_t* triangles) {
+  if (!handle) return fail(TS_EINVAL, "ts_marching_tets_fetch: null handle");
+  int rc = ts_impl_mt_fetch(handle, vertices, triangles);
+  if (rc) return fail(rc, "ts_marching_tets_fetch failed");
+  return check_cuda("ts_marching_tets_fetch");
+}
+
+int ts_marching_tets_release(void* handle) {
+  ts_impl_mt_release(handle);
+  return check_cuda("ts_marching_tets_release");
+}
+
 int ts_marching_tets(const double* sdf, const double* deform, int32_t R, double* verts, int64_t* tris,
                      int64_t* nt, void* stream) {
+  keep_pool_warm();
   if (!sdf || !deform || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets: bad arguments");
   int rc = ts_impl_mt(sdf, deform, R, verts, tris, nt, ST(stream));
   if (rc) return fail(rc, "ts_marching_tets failed");

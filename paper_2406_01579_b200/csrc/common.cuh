@@ -77,6 +77,14 @@ __host__ __device__ __forceinline__ int perm_a0(int p) { return (p < 2) ? 0 : (p
 __host__ __device__ __forceinline__ int perm_a1(int p) {
   return (p == 0 || p == 5) ? 1 : ((p == 1 || p == 3) ? 2 : 0);
 }
+// cell corner (bit 0 = +x, bit 1 = +y, bit 2 = +z) of local slot `slot` of permutation p
+// (tet_corners: slot 1 = +a0, slot 2 = +a0+a1, slot 3 = +xyz; odd permutations swap 2 and 3)
+__host__ __device__ constexpr int perm_corner(int p, int slot) {
+  return slot == 0 ? 0
+                   : (slot == 1 ? (1 << perm_a0(p))
+                                : (((slot == 2) != (p == 1 || p == 2 || p == 5)) ? ((1 << perm_a0(p)) | (1 << perm_a1(p)))
+                                                                                 : 7));
+}
 
 // integer vertex coordinates + ids of tet t (local order of grid.py, orientation fixed)
 __device__ __forceinline__ void tet_corners(uint32_t t, const Grid& G, int xyz[4][3], uint32_t vid[4]) {

@@ -89,6 +89,10 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
                                 double* loss, cudaStream_t st, void* scratch = nullptr);
 int64_t ts_impl_nc_scratch_bytes(int R);
 int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);
+int ts_impl_mt_run(const double* sdf, const double* deform, int R, void** handle, int64_t* nv, int64_t* nt,
+                   cudaStream_t st);
+int ts_impl_mt_fetch(void* handle, double* verts, int64_t* tris);
+void ts_impl_mt_release(void* handle);
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
 void ts_impl_counters(unsigned long long out[8], int reset);

@@ -22,6 +22,8 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+#include <initializer_list>
+
 namespace ts {
 
 __device__ __forceinline__ int64_t edge_delta(int s, int64_t n) {
@@ -34,23 +36,31 @@ __device__ __forceinline__ void edge_off(int s, int& ox, int& oy, int& oz) {
   oz = (s >= 3);
 }
 
-// E1: per-vertex crossing flags (bit s) and counts
+// E1: per-vertex crossing flags (bit s) and counts; negbits = one "f < 0" bit per vertex
+// (2 MB at 256^3: the per-cell classification reads it from L2 instead of the FP64 field)
 __global__ void k_mt_vflags(int64_t N, Grid G, const double* __restrict__ sdf, uint8_t* __restrict__ flags,
-                            int32_t* __restrict__ cnt) {
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < N; a += (int64_t)gridDim.x * blockDim.x) {
-    int x, y, z;
-    vertex_xyz((uint32_t)a, G, x, y, z);
-    const bool na = sdf[a] < 0.0;
-    uint32_t fl = 0;
-    for (int s = 0; s < 7; ++s) {
-      int ox, oy, oz;
-      edge_off(s, ox, oy, oz);
-      if (x + ox > G.R || y + oy > G.R || z + oz > G.R) continue;
-      const int64_t b = a + edge_delta(s, G.n);
-      if ((sdf[b] < 0.0) != na) fl |= 1u << s;
+                            int32_t* __restrict__ cnt, uint32_t* __restrict__ negbits) {
+  for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); a0 < N;
+       a0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = a0 + (threadIdx.x & 31);
+    bool na = false;
+    if (a < N) {
+      int x, y, z;
+      vertex_xyz((uint32_t)a, G, x, y, z);
+      na = sdf[a] < 0.0;
+      uint32_t fl = 0;
+      for (int s = 0; s < 7; ++s) {
+        int ox, oy, oz;
+        edge_off(s, ox, oy, oz);
+        if (x + ox > G.R || y + oy > G.R || z + oz > G.R) continue;
+        const int64_t b = a + edge_delta(s, G.n);
+        if ((sdf[b] < 0.0) != na) fl |= 1u << s;
+      }
+      flags[a] = (uint8_t)fl;
+      cnt[a] = __popc(fl);
     }
-    flags[a] = (uint8_t)fl;
-    cnt[a] = __popc(fl);
+    const unsigned w = __ballot_sync(0xffffffffu, na);
+    if ((threadIdx.x & 31) == 0) negbits[a0 >> 5] = w;
   }
 }
 
@@ -99,31 +109,56 @@ __global__ void k_mt_verts(int64_t N, Grid G, const double* __restrict__ sdf, co
   }
 }
 
-__device__ __forceinline__ int tet_class(uint32_t t, const Grid& G, const double* __restrict__ sdf) {
-  uint32_t v[4];
-  tet_vertices(t, G, v);
-  int c = 0;
-  for (int i = 0; i < 4; ++i) c += sdf[v[i]] < 0.0;
-  return c;  // 1, 3: one triangle; 2: two
+// Crossing tets are classified per CELL: the 8 corner signs form a mask, each tet's class is
+// the popcount of (mask & its corner mask) — 1 / 3: one triangle, 2: two.  Cells are taken in
+// tet-id order (cell = ix R^2 + iy R + iz; tet = cell * 6 + p), so per-thread cell ranges
+// plus block scans give the reference's group-ordered output slots.
+constexpr int kCellsPerThread = 8;
+constexpr int kCellChunk = kScanThreads * kCellsPerThread;  // cells per CTA
+
+__device__ __forceinline__ uint32_t tet_cmask(int p) {
+  return (1u << perm_corner(p, 0)) | (1u << perm_corner(p, 1)) | (1u << perm_corner(p, 2)) | (1u << perm_corner(p, 3));
+}
+
+// negative-corner mask of cell c (f < 0 inside, f = 0 counts as outside) from the vertex bits
+__device__ __forceinline__ uint32_t cell_negmask(uint32_t c, const Grid& G, const uint32_t* __restrict__ negbits) {
+  const uint32_t q = G.dR.div(c);  // ix*R + iy
+  const uint32_t iz = c - q * (uint32_t)G.R;
+  const uint32_t ix = G.dR.div(q);
+  const uint32_t iy = q - ix * (uint32_t)G.R;
+  const uint32_t n = (uint32_t)G.n;
+  const uint32_t v0 = ix + n * (iy + n * iz);
+  uint32_t m = 0;
+#pragma unroll
+  for (int lc = 0; lc < 8; ++lc) {
+    const uint32_t v = v0 + (lc & 1) + n * (((lc >> 1) & 1) + n * ((lc >> 2) & 1));
+    m |= ((__ldg(negbits + (v >> 5)) >> (v & 31)) & 1u) << lc;
+  }
+  return m;
+}
+
+// class counts of a cell's 6 tets, packed n1 | n3 << 8 | n2 << 16
+__device__ __forceinline__ uint32_t cell_counts(uint32_t m) {
+  if (m == 0u || m == 0xffu) return 0u;
+  uint32_t r = 0;
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    const int c = __popc(m & tet_cmask(p));
+    r += c == 1 ? 1u : (c == 3 ? (1u << 8) : (c == 2 ? (1u << 16) : 0u));
+  }
+  return r;
 }
 
 // T1: per-chunk counts of the three groups
-__global__ void __launch_bounds__(kScanThreads) k_mt_tcount(int64_t K, Grid G, const double* __restrict__ sdf,
+__global__ void __launch_bounds__(kScanThreads) k_mt_ccount(int64_t C, Grid G, const uint32_t* __restrict__ negbits,
                                                            int64_t* __restrict__ c1, int64_t* __restrict__ c3,
                                                            int64_t* __restrict__ c2) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  int n1 = 0, n3 = 0, n2 = 0;
-  for (int k = 0; k < kItemsPerThread; ++k) {
-    const int64_t t = base + (int64_t)k * kScanThreads + threadIdx.x;
-    if (t >= K) break;
-    const int c = tet_class((uint32_t)t, G, sdf);
-    n1 += c == 1;
-    n3 += c == 3;
-    n2 += c == 2;
-  }
-  n1 = warp_sum(n1);
-  n3 = warp_sum(n3);
-  n2 = warp_sum(n2);
+  const int64_t c0 = (int64_t)blockIdx.x * kCellChunk + (int64_t)threadIdx.x * kCellsPerThread;
+  uint32_t acc = 0;  // <= 8 cells x 6 tets per field
+#pragma unroll
+  for (int k = 0; k < kCellsPerThread; ++k)
+    if (c0 + k < C) acc += cell_counts(cell_negmask((uint32_t)(c0 + k), G, negbits));
+  int n1 = warp_sum((int)(acc & 0xffu)), n3 = warp_sum((int)((acc >> 8) & 0xffu)), n2 = warp_sum((int)(acc >> 16));
   __shared__ int s[3][kScanThreads / 32];
   if ((threadIdx.x & 31) == 0) {
     s[0][threadIdx.x >> 5] = n1;
@@ -140,156 +175,175 @@ __global__ void __launch_bounds__(kScanThreads) k_mt_tcount(int64_t K, Grid G, c
   }
 }
 
-// T2: triangles of the crossing tets at their group-ordered slots
-__global__ void __launch_bounds__(kScanThreads) k_mt_temit(int64_t K, Grid G, const double* __restrict__ sdf,
-                                                          const double* __restrict__ deform,
-                                                          const uint8_t* __restrict__ flags,
-                                                          const int64_t* __restrict__ ebase,
-                                                          const double* __restrict__ verts,
+// orient triangle tri against the tet gradient g (grid.py:219-225) and store it at `slot`
+__device__ __forceinline__ void put_tri(int64_t tri[3], const double g[3], const double* __restrict__ verts,
+                                       int64_t slot, int64_t* __restrict__ tris) {
+  const double* a0 = verts + tri[0] * 3;
+  const double* a1 = verts + tri[1] * 3;
+  const double* a2 = verts + tri[2] * 3;
+  double u[3], w[3];
+  for (int i = 0; i < 3; ++i) {
+    u[i] = dsub(a1[i], a0[i]);
+    w[i] = dsub(a2[i], a0[i]);
+  }
+  const double nx_ = dsub(dmul(u[1], w[2]), dmul(u[2], w[1]));
+  const double ny_ = dsub(dmul(u[2], w[0]), dmul(u[0], w[2]));
+  const double nz_ = dsub(dmul(u[0], w[1]), dmul(u[1], w[0]));
+  const double dot = dadd(dadd(dmul(nx_, g[0]), dmul(ny_, g[1])), dmul(nz_, g[2]));
+  if (dot < 0.0) {
+    const int64_t tmp = tri[1];
+    tri[1] = tri[2];
+    tri[2] = tmp;
+  }
+  for (int i = 0; i < 3; ++i) tris[slot * 3 + i] = tri[i];
+}
+
+__device__ __forceinline__ void tet_grad_of(uint32_t t, const Grid& G, const double* __restrict__ sdf,
+                                            const double* __restrict__ deform, double g[3]) {
+  double P[4][3], f[4], cc1[3], cc2[3], cc3[3];
+  uint32_t vv[4];
+  load_tet(t, G, sdf, deform, vv, P, f);
+  tet_gradient(P, f, g, cc1, cc2, cc3);
+}
+
+// one triangle of a 1- or 3-negative tet at `slot`
+__device__ void emit_single(uint32_t t, int c, int64_t slot, const Grid& G, const double* __restrict__ sdf,
+                            const double* __restrict__ deform, const uint8_t* __restrict__ flags,
+                            const int64_t* __restrict__ ebase, const double* __restrict__ verts,
+                            int64_t* __restrict__ tris) {
+  uint32_t v[4];
+  tet_vertices(t, G, v);
+  bool neg[4];
+  for (int i = 0; i < 4; ++i) neg[i] = sdf[v[i]] < 0.0;
+  // lone vertex = first vertex of the minority sign; the others in local order
+  const bool lone_neg = c == 1;
+  int m = 0;
+  for (int i = 3; i >= 0; --i)
+    if (neg[i] == lone_neg) m = i;
+  int64_t tri[3];
+  int q = 0;
+  for (int i = 0; i < 4; ++i)
+    if (i != m) tri[q++] = edge_index(flags, ebase, v[m], v[i], G.n);
+  double g[3];
+  tet_grad_of(t, G, sdf, deform, g);
+  put_tri(tri, g, verts, slot, tris);
+}
+
+// the two triangles of a 2-2 tet (quad split by the reference's diagonal rule)
+__device__ void emit_quad(uint32_t t, int64_t s1, int64_t s2, const Grid& G, const double* __restrict__ sdf,
+                          const double* __restrict__ deform, const uint8_t* __restrict__ flags,
+                          const int64_t* __restrict__ ebase, const double* __restrict__ verts,
+                          int64_t* __restrict__ tris) {
+  const int64_t n = G.n;
+  uint32_t v[4];
+  tet_vertices(t, G, v);
+  bool neg[4];
+  for (int i = 0; i < 4; ++i) neg[i] = sdf[v[i]] < 0.0;
+  int ord[4], q = 0;
+  for (int i = 0; i < 4; ++i)
+    if (neg[i]) ord[q++] = i;
+  for (int i = 0; i < 4; ++i)
+    if (!neg[i]) ord[q++] = i;
+  const int64_t I = v[ord[0]], J = v[ord[1]], Kv = v[ord[2]], Lv = v[ord[3]];
+  const int64_t ik = edge_index(flags, ebase, I, Kv, n), il = edge_index(flags, ebase, I, Lv, n);
+  const int64_t jl = edge_index(flags, ebase, J, Lv, n), jk = edge_index(flags, ebase, J, Kv, n);
+  auto dist = [&](int64_t p, int64_t q2) {
+    const double* A = verts + p * 3;
+    const double* B = verts + q2 * 3;
+    double s = 0.0;
+    for (int i = 0; i < 3; ++i) {
+      const double d = dsub(A[i], B[i]);
+      s = dadd(s, dmul(d, d));
+    }
+    return sqrt(s);
+  };
+  const double d1 = dist(ik, jl), d2 = dist(il, jk);
+  const int64_t key1 = min(min(I, Kv), min(J, Lv)), key2 = min(min(I, Lv), min(J, Kv));
+  const bool close = fabs(dsub(d1, d2)) <= dadd(1e-8, dmul(1e-5, fabs(d2)));  // np.isclose
+  const bool use1 = close ? (key1 <= key2) : (d1 < d2);
+  int64_t T1[3], T2[3];
+  if (use1) {
+    T1[0] = ik; T1[1] = il; T1[2] = jl;
+    T2[0] = ik; T2[1] = jl; T2[2] = jk;
+  } else {
+    T1[0] = ik; T1[1] = il; T1[2] = jk;
+    T2[0] = il; T2[1] = jl; T2[2] = jk;
+  }
+  double g[3];
+  tet_grad_of(t, G, sdf, deform, g);
+  put_tri(T1, g, verts, s1, tris);
+  put_tri(T2, g, verts, s2, tris);
+}
+
+// T2a: the crossing tets in the reference's group order: tlist[pos] = tet id, pos = r1
+// (1-negative), n1 + r3 (3-negative), n1 + n3 + r2 (2-2); o1/o3/o2 = exclusive per-chunk
+// offsets of the three groups (k_mt_ccount + scans)
+__global__ void __launch_bounds__(kScanThreads) k_mt_clist(int64_t C, Grid G, const uint32_t* __restrict__ negbits,
                                                           const int64_t* __restrict__ o1, const int64_t* __restrict__ o3,
                                                           const int64_t* __restrict__ o2, int64_t n1, int64_t n3,
-                                                          int64_t n2, int64_t* __restrict__ tris) {
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  int64_t r1 = o1[blockIdx.x], r3 = o3[blockIdx.x], r2 = o2[blockIdx.x];
-  __shared__ int wc[3][kScanThreads / 32];
+                                                          uint32_t* __restrict__ tlist) {
+  const int64_t c0 = (int64_t)blockIdx.x * kCellChunk + (int64_t)threadIdx.x * kCellsPerThread;
+  uint32_t masks[kCellsPerThread];
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < kCellsPerThread; ++k) {
+    masks[k] = c0 + k < C ? cell_negmask((uint32_t)(c0 + k), G, negbits) : 0u;
+    acc += cell_counts(masks[k]);
+  }
+  // block exclusive scan of the three counts (16-bit fields: <= 12288 per CTA, no carries)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t n = G.n;
-  for (int kk = 0; kk < kItemsPerThread; ++kk) {
-    const int64_t t = base + (int64_t)kk * kScanThreads + threadIdx.x;
-    uint32_t v[4] = {0, 0, 0, 0};
-    bool neg[4] = {false, false, false, false};
-    int c = 0;
-    if (t < K) {
-      tet_vertices((uint32_t)t, G, v);
-      for (int i = 0; i < 4; ++i) {
-        neg[i] = sdf[v[i]] < 0.0;
-        c += neg[i];
-      }
+  const uint32_t x = (acc & 0xffu) | (((acc >> 8) & 0xffu) << 16), y = acc >> 16;
+  uint32_t ix = x, iy = y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t tx = __shfl_up_sync(0xffffffffu, ix, o), ty = __shfl_up_sync(0xffffffffu, iy, o);
+    if (lane >= o) {
+      ix += tx;
+      iy += ty;
     }
-    const unsigned m1 = __ballot_sync(0xffffffffu, t < K && c == 1);
-    const unsigned m3 = __ballot_sync(0xffffffffu, t < K && c == 3);
-    const unsigned m2 = __ballot_sync(0xffffffffu, t < K && c == 2);
-    if (lane == 0) {
-      wc[0][wid] = __popc(m1);
-      wc[1][wid] = __popc(m3);
-      wc[2][wid] = __popc(m2);
+  }
+  __shared__ uint32_t wx[kScanThreads / 32], wy[kScanThreads / 32];
+  if (lane == 31) {
+    wx[wid] = ix;
+    wy[wid] = iy;
+  }
+  __syncthreads();
+  uint32_t bx = 0, by = 0;
+  for (int w = 0; w < wid; ++w) bx += wx[w], by += wy[w];
+  if (acc == 0u) return;
+  const uint32_t ex = bx + ix - x, ey = by + iy - y;
+  int64_t p1 = o1[blockIdx.x] + (ex & 0xffffu), p3 = n1 + o3[blockIdx.x] + (ex >> 16),
+          p2 = n1 + n3 + o2[blockIdx.x] + ey;
+#pragma unroll
+  for (int k = 0; k < kCellsPerThread; ++k) {
+    const uint32_t m = masks[k];
+    if (m == 0u || m == 0xffu) continue;
+    const uint32_t t0 = (uint32_t)(c0 + k) * 6u;
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const int cl = __popc(m & tet_cmask(p));
+      if (cl == 1) tlist[p1++] = t0 + p;
+      else if (cl == 3) tlist[p3++] = t0 + p;
+      else if (cl == 2) tlist[p2++] = t0 + p;
     }
-    __syncthreads();
-    int b1 = 0, b3 = 0, b2 = 0, t1 = 0, t3 = 0, t2 = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) {
-      if (w < wid) b1 += wc[0][w], b3 += wc[1][w], b2 += wc[2][w];
-      t1 += wc[0][w], t3 += wc[1][w], t2 += wc[2][w];
+  }
+}
+
+// T2b: one thread per crossing tet of the list: its triangle(s) at the group-ordered slots
+__global__ void __launch_bounds__(256) k_mt_emit(int64_t ncross, Grid G, const double* __restrict__ sdf,
+                                                 const double* __restrict__ deform, const uint8_t* __restrict__ flags,
+                                                 const int64_t* __restrict__ ebase, const double* __restrict__ verts,
+                                                 const uint32_t* __restrict__ tlist, int64_t n1, int64_t n3,
+                                                 int64_t n2, int64_t* __restrict__ tris) {
+  for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < ncross;
+       pos += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = tlist[pos];
+    if (pos < n1 + n3) {
+      emit_single(t, pos < n1 ? 1 : 3, pos, G, sdf, deform, flags, ebase, verts, tris);
+    } else {
+      const int64_t rank = pos - n1 - n3;
+      emit_quad(t, n1 + n3 + rank, n1 + n3 + n2 + rank, G, sdf, deform, flags, ebase, verts, tris);
     }
-    const unsigned lt = (1u << lane) - 1u;
-    if (t < K && (c == 1 || c == 3)) {
-      // lone vertex = first vertex of the minority sign; the others in local order
-      const bool lone_neg = c == 1;
-      int m = 0;
-      for (int i = 3; i >= 0; --i)
-        if (neg[i] == lone_neg) m = i;
-      int64_t e[3];
-      int q = 0;
-      for (int i = 0; i < 4; ++i)
-        if (i != m) e[q++] = edge_index(flags, ebase, v[m], v[i], n);
-      const int64_t slot = c == 1 ? (r1 + b1 + __popc(m1 & lt)) : (n1 + r3 + b3 + __popc(m3 & lt));
-      int64_t tri[3] = {e[0], e[1], e[2]};
-      // orientation against the tet gradient (grid.py:219-225)
-      double P[4][3], f[4], g[3], cc1[3], cc2[3], cc3[3];
-      int xyz[4][3];
-      uint32_t vv[4];
-      tet_corners((uint32_t)t, G, xyz, vv);
-      for (int i = 0; i < 4; ++i) {
-        vertex_pos_xyz(xyz[i], vv[i], G, deform, P[i]);
-        f[i] = sdf[vv[i]];
-      }
-      tet_gradient(P, f, g, cc1, cc2, cc3);
-      const double* a0 = verts + tri[0] * 3;
-      const double* a1 = verts + tri[1] * 3;
-      const double* a2 = verts + tri[2] * 3;
-      double u[3], w[3];
-      for (int i = 0; i < 3; ++i) {
-        u[i] = dsub(a1[i], a0[i]);
-        w[i] = dsub(a2[i], a0[i]);
-      }
-      const double nx_ = dsub(dmul(u[1], w[2]), dmul(u[2], w[1]));
-      const double ny_ = dsub(dmul(u[2], w[0]), dmul(u[0], w[2]));
-      const double nz_ = dsub(dmul(u[0], w[1]), dmul(u[1], w[0]));
-      const double dot = dadd(dadd(dmul(nx_, g[0]), dmul(ny_, g[1])), dmul(nz_, g[2]));
-      if (dot < 0.0) {
-        const int64_t tmp = tri[1];
-        tri[1] = tri[2];
-        tri[2] = tmp;
-      }
-      for (int i = 0; i < 3; ++i) tris[slot * 3 + i] = tri[i];
-    } else if (t < K && c == 2) {
-      int ord[4], q = 0;
-      for (int i = 0; i < 4; ++i)
-        if (neg[i]) ord[q++] = i;
-      for (int i = 0; i < 4; ++i)
-        if (!neg[i]) ord[q++] = i;
-      const int64_t I = v[ord[0]], J = v[ord[1]], Kv = v[ord[2]], Lv = v[ord[3]];
-      const int64_t ik = edge_index(flags, ebase, I, Kv, n), il = edge_index(flags, ebase, I, Lv, n);
-      const int64_t jl = edge_index(flags, ebase, J, Lv, n), jk = edge_index(flags, ebase, J, Kv, n);
-      auto dist = [&](int64_t p, int64_t q2) {
-        const double* A = verts + p * 3;
-        const double* B = verts + q2 * 3;
-        double s = 0.0;
-        for (int i = 0; i < 3; ++i) {
-          const double d = dsub(A[i], B[i]);
-          s = dadd(s, dmul(d, d));
-        }
-        return sqrt(s);
-      };
-      const double d1 = dist(ik, jl), d2 = dist(il, jk);
-      const int64_t key1 = min(min(I, Kv), min(J, Lv)), key2 = min(min(I, Lv), min(J, Kv));
-      const bool close = fabs(dsub(d1, d2)) <= dadd(1e-8, dmul(1e-5, fabs(d2)));
-      const bool use1 = close ? (key1 <= key2) : (d1 < d2);
-      int64_t T1[3], T2[3];
-      if (use1) {
-        T1[0] = ik; T1[1] = il; T1[2] = jl;
-        T2[0] = ik; T2[1] = jl; T2[2] = jk;
-      } else {
-        T1[0] = ik; T1[1] = il; T1[2] = jk;
-        T2[0] = il; T2[1] = jl; T2[2] = jk;
-      }
-      const int64_t rank = r2 + b2 + __popc(m2 & lt);
-      const int64_t s1 = n1 + n3 + rank, s2 = n1 + n3 + n2 + rank;
-      double P[4][3], f[4], g[3], cc1[3], cc2[3], cc3[3];
-      int xyz[4][3];
-      uint32_t vv[4];
-      tet_corners((uint32_t)t, G, xyz, vv);
-      for (int i = 0; i < 4; ++i) {
-        vertex_pos_xyz(xyz[i], vv[i], G, deform, P[i]);
-        f[i] = sdf[vv[i]];
-      }
-      tet_gradient(P, f, g, cc1, cc2, cc3);
-      for (int h = 0; h < 2; ++h) {
-        int64_t* tri = h == 0 ? T1 : T2;
-        const double* a0 = verts + tri[0] * 3;
-        const double* a1 = verts + tri[1] * 3;
-        const double* a2 = verts + tri[2] * 3;
-        double u[3], w[3];
-        for (int i = 0; i < 3; ++i) {
-          u[i] = dsub(a1[i], a0[i]);
-          w[i] = dsub(a2[i], a0[i]);
-        }
-        const double nx_ = dsub(dmul(u[1], w[2]), dmul(u[2], w[1]));
-        const double ny_ = dsub(dmul(u[2], w[0]), dmul(u[0], w[2]));
-        const double nz_ = dsub(dmul(u[0], w[1]), dmul(u[1], w[0]));
-        const double dot = dadd(dadd(dmul(nx_, g[0]), dmul(ny_, g[1])), dmul(nz_, g[2]));
-        if (dot < 0.0) {
-          const int64_t tmp = tri[1];
-          tri[1] = tri[2];
-          tri[2] = tmp;
-        }
-        const int64_t slot = h == 0 ? s1 : s2;
-        for (int i = 0; i < 3; ++i) tris[slot * 3 + i] = tri[i];
-      }
-    }
-    r1 += t1;
-    r3 += t3;
-    r2 += t2;
-    __syncthreads();
   }
 }
 
@@ -341,6 +395,32 @@ __global__ void k_mt_bitonic(int64_t P, int64_t kk, int64_t jj, VKey* __restrict
   }
 }
 
+// all bitonic steps with stride < kLocalSort of merge size kk (kk_lo <= kk <= kk_hi, powers of
+// two), on kLocalSort-key blocks in shared memory (one launch instead of log2 steps each)
+constexpr int kLocalSort = 1024;
+__global__ void __launch_bounds__(kLocalSort / 2) k_mt_bitonic_local(int64_t P, int64_t kk_lo, int64_t kk_hi,
+                                                                    VKey* __restrict__ keys) {
+  __shared__ VKey sk[kLocalSort];
+  const int64_t b0 = (int64_t)blockIdx.x * kLocalSort;
+  for (int i = threadIdx.x; i < kLocalSort; i += blockDim.x) sk[i] = keys[b0 + i];
+  __syncthreads();
+  for (int64_t kk = kk_lo; kk <= kk_hi; kk <<= 1) {
+    for (int jj = (int)min(kk >> 1, (int64_t)kLocalSort / 2); jj > 0; jj >>= 1) {
+      const int t = threadIdx.x;
+      const int i = 2 * t - (t & (jj - 1));  // lower index of this thread's pair
+      const int l = i + jj;
+      const bool asc = ((b0 + i) & kk) == 0;
+      const VKey a = sk[i], b = sk[l];
+      if (vless(b, a) == asc) {
+        sk[i] = b;
+        sk[l] = a;
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < kLocalSort; i += blockDim.x) keys[b0 + i] = sk[i];
+}
+
 __global__ void k_mt_newgroup(int64_t V, const VKey* __restrict__ keys, int32_t* __restrict__ first) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
     first[i] = (i == 0 || !vsame(keys[i], keys[i - 1])) ? 1 : 0;
@@ -390,40 +470,105 @@ inline int grid_blocks(int64_t n) {
   return (int)(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
 }
 
-struct MtCounts {
-  int64_t V, n1, n3, n2;
+// ---- host pipeline ------------------------------------------------------------------------
+struct MtResult {
+  double* verts = nullptr;  // welded vertices f64[nv, 3] (device)
+  int64_t* tris = nullptr;  // triangles i64[nt, 3] (device)
+  int64_t nv = 0, nt = 0;
+  cudaStream_t st = nullptr;
 };
 
-// shared first half: vertex flags + edge bases + triangle group counts
-static int mt_counts(const double* sdf, int R, uint8_t** flags, int64_t** ebase, MtCounts& mc, int64_t** o1,
-                     int64_t** o3, int64_t** o2, int64_t& nb, cudaStream_t st) {
+static void bitonic_sort(VKey* keys, int64_t P, cudaStream_t st) {
+  // P is a power of two >= kLocalSort
+  k_mt_bitonic_local<<<(unsigned)(P / kLocalSort), kLocalSort / 2, 0, st>>>(P, 2, kLocalSort, keys);
+  for (int64_t kk = 2 * kLocalSort; kk <= P; kk <<= 1) {
+    for (int64_t jj = kk >> 1; jj >= kLocalSort; jj >>= 1) k_mt_bitonic<<<grid_blocks(P), 256, 0, st>>>(P, kk, jj, keys);
+    k_mt_bitonic_local<<<(unsigned)(P / kLocalSort), kLocalSort / 2, 0, st>>>(P, kk, kk, keys);
+  }
+}
+
+static void free_all(std::initializer_list<void*> ps, cudaStream_t st) {
+  for (void* p : ps)
+    if (p) cudaFreeAsync(p, st);
+}
+
+// The whole extraction into device buffers owned by `out` (two host syncs: the sizes, the
+// final counts).
+static int mt_run(const double* sdf, const double* deform, int R, MtResult& out, cudaStream_t st) {
   const Grid G = make_grid(R);
-  const int64_t n = R + 1, N = n * n * n, K = 6ll * R * R * R;
+  const int64_t n = R + 1, N = n * n * n, C = (int64_t)R * R * R;
+  out.st = st;
+  // E1: crossing edges per vertex -> edge index bases
+  uint8_t* flags = nullptr;
   int32_t* cnt = nullptr;
-  int64_t* scratch = nullptr;
-  cudaMallocAsync(flags, N, st);
+  int64_t *ebase = nullptr, *scratch = nullptr;
+  cudaMallocAsync(&flags, N, st);
   cudaMallocAsync(&cnt, sizeof(int32_t) * N, st);
-  cudaMallocAsync(ebase, sizeof(int64_t) * (N + 1), st);
+  cudaMallocAsync(&ebase, sizeof(int64_t) * (N + 1), st);
   cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(N), st);
-  k_mt_vflags<<<grid_blocks(N), 256, 0, st>>>(N, G, sdf, *flags, cnt);
-  scan_counts(cnt, N, *ebase, scratch, st);
-  nb = (K + kChunk - 1) / kChunk;
-  cudaMallocAsync(o1, sizeof(int64_t) * (nb + 1), st);
-  cudaMallocAsync(o3, sizeof(int64_t) * (nb + 1), st);
-  cudaMallocAsync(o2, sizeof(int64_t) * (nb + 1), st);
-  k_mt_tcount<<<(unsigned)nb, kScanThreads, 0, st>>>(K, G, sdf, *o1, *o3, *o2);
-  k_scan_i64<<<1, 1024, 0, st>>>(*o1, nb);
-  k_scan_i64<<<1, 1024, 0, st>>>(*o3, nb);
-  k_scan_i64<<<1, 1024, 0, st>>>(*o2, nb);
+  uint32_t* negbits = nullptr;
+  cudaMallocAsync(&negbits, sizeof(uint32_t) * ((N + 31) / 32 + 8), st);
+  k_mt_vflags<<<grid_blocks(N), 256, 0, st>>>(N, G, sdf, flags, cnt, negbits);
+  scan_counts(cnt, N, ebase, scratch, st);
+  // T1: per-chunk group counts over cells, exclusive scans
+  const int64_t nb = (C + kCellChunk - 1) / kCellChunk;
+  int64_t* off = nullptr;  // o1 | o3 | o2, nb + 1 each
+  cudaMallocAsync(&off, sizeof(int64_t) * 3 * (nb + 1), st);
+  int64_t *o1 = off, *o3 = off + (nb + 1), *o2 = off + 2 * (nb + 1);
+  k_mt_ccount<<<(unsigned)nb, kScanThreads, 0, st>>>(C, G, negbits, o1, o3, o2);
+  k_scan_i64<<<1, 1024, 0, st>>>(o1, nb);
+  k_scan_i64<<<1, 1024, 0, st>>>(o3, nb);
+  k_scan_i64<<<1, 1024, 0, st>>>(o2, nb);
   int64_t h[4];
-  cudaMemcpyAsync(&h[0], *ebase + N, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&h[1], *o1 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&h[2], *o3 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&h[3], *o2 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[0], ebase + N, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[1], o1 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[2], o3 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[3], o2 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(cnt, st);
-  cudaFreeAsync(scratch, st);
   cudaStreamSynchronize(st);
-  mc = MtCounts{h[0], h[1], h[2], h[3]};
+  const int64_t V = h[0], n1 = h[1], n3 = h[2], n2 = h[3], F = n1 + n3 + 2 * n2;
+  if (V == 0 || F == 0) {
+    free_all({flags, ebase, scratch, off, negbits}, st);
+    cudaStreamSynchronize(st);
+    return 0;
+  }
+  // E2 + T2: crossing positions, group-ordered oriented triangles
+  double* verts = nullptr;
+  int64_t* tris = nullptr;
+  cudaMallocAsync(&verts, sizeof(double) * 3 * V, st);
+  cudaMallocAsync(&tris, sizeof(int64_t) * 3 * F, st);
+  k_mt_verts<<<grid_blocks(N), 256, 0, st>>>(N, G, sdf, deform, flags, ebase, verts);
+  uint32_t* tlist = nullptr;
+  const int64_t ncross = n1 + n3 + n2;
+  cudaMallocAsync(&tlist, sizeof(uint32_t) * ncross, st);
+  k_mt_clist<<<(unsigned)nb, kScanThreads, 0, st>>>(C, G, negbits, o1, o3, o2, n1, n3, tlist);
+  k_mt_emit<<<grid_blocks(ncross), 256, 0, st>>>(ncross, G, sdf, deform, flags, ebase, verts, tlist, n1, n3, n2, tris);
+  // W: weld equal positions (np.unique over rows: lexicographic), remap, drop degenerates
+  int64_t P = kLocalSort;
+  while (P < V) P <<= 1;
+  VKey* keys = nullptr;
+  cudaMallocAsync(&keys, sizeof(VKey) * P, st);
+  k_mt_keys<<<grid_blocks(P), 256, 0, st>>>(V, P, verts, keys);
+  bitonic_sort(keys, P, st);
+  int32_t* first = nullptr;
+  int64_t *excl = nullptr, *remap = nullptr, *scratch2 = nullptr;
+  cudaMallocAsync(&first, sizeof(int32_t) * V, st);
+  cudaMallocAsync(&excl, sizeof(int64_t) * (V + 1), st);
+  cudaMallocAsync(&remap, sizeof(int64_t) * V, st);
+  cudaMallocAsync(&scratch2, sizeof(int64_t) * compact_blocks(V > F ? V : F), st);
+  cudaMallocAsync(&out.verts, sizeof(double) * 3 * V, st);
+  cudaMallocAsync(&out.tris, sizeof(int64_t) * 3 * F, st);
+  k_mt_newgroup<<<grid_blocks(V), 256, 0, st>>>(V, keys, first);
+  scan_counts(first, V, excl, scratch2, st);
+  k_mt_remap<<<grid_blocks(V), 256, 0, st>>>(V, keys, first, excl, verts, remap, out.verts);
+  TriKeep tk{tris, remap, out.verts, out.tris};
+  int64_t* d_total = compact(F, tk, scratch2, st);
+  cudaMemcpyAsync(&h[0], d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[1], excl + V, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  free_all({flags, ebase, scratch, off, negbits, tlist, verts, tris, keys, first, excl, remap, scratch2}, st);
+  cudaStreamSynchronize(st);
+  out.nt = h[0];
+  out.nv = h[1];
   return 0;
 }
 
@@ -431,80 +576,51 @@ static int mt_counts(const double* sdf, int R, uint8_t** flags, int64_t** ebase,
 
 using namespace ts;
 
-int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st) {
-  (void)deform;
-  uint8_t* flags;
-  int64_t *ebase, *o1, *o3, *o2, nb;
-  MtCounts mc;
-  mt_counts(sdf, R, &flags, &ebase, mc, &o1, &o3, &o2, nb, st);
-  *nv = mc.V;
-  *nt = mc.n1 + mc.n3 + 2 * mc.n2;
-  cudaFreeAsync(flags, st);
-  cudaFreeAsync(ebase, st);
-  cudaFreeAsync(o1, st);
-  cudaFreeAsync(o3, st);
-  cudaFreeAsync(o2, st);
+int ts_impl_mt_run(const double* sdf, const double* deform, int R, void** handle, int64_t* nv, int64_t* nt,
+                   cudaStream_t st) {
+  MtResult* r = new MtResult();
+  const int rc = mt_run(sdf, deform, R, *r, st);
+  *nv = r->nv;
+  *nt = r->nt;
+  *handle = r;
+  return rc;
+}
+
+// copy the result into caller buffers (host or device: cudaMemcpyDefault)
+int ts_impl_mt_fetch(void* handle, double* verts, int64_t* tris) {
+  MtResult* r = static_cast<MtResult*>(handle);
+  if (r->nv && verts)
+    cudaMemcpyAsync(verts, r->verts, sizeof(double) * 3 * r->nv, cudaMemcpyDefault, r->st);
+  if (r->nt && tris)
+    cudaMemcpyAsync(tris, r->tris, sizeof(int64_t) * 3 * r->nt, cudaMemcpyDefault, r->st);
+  cudaStreamSynchronize(r->st);
   return 0;
 }
 
-// vertices: capacity >= count's nv (welded count returned through the first row count);
-// triangles: capacity >= count's nt.  *out_nt = final triangle count; the welded vertex
-// count is returned as the return value's companion via out_nt[1] when non-null.
+void ts_impl_mt_release(void* handle) {
+  MtResult* r = static_cast<MtResult*>(handle);
+  if (!r) return;
+  free_all({r->verts, r->tris}, r->st);
+  delete r;
+}
+
+int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st) {
+  void* h = nullptr;
+  const int rc = ts_impl_mt_run(sdf, deform, R, &h, nv, nt, st);
+  ts_impl_mt_release(h);
+  return rc;
+}
+
+// vertices / triangles: capacities >= the counts of ts_impl_mt_count.  out_n[0] = final
+// triangle count, out_n[1] = welded vertex count.
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* out_verts, int64_t* out_tris, int64_t* out_n,
                cudaStream_t st) {
-  const Grid G = make_grid(R);
-  const int64_t n = R + 1, N = n * n * n, K = 6ll * R * R * R;
-  uint8_t* flags;
-  int64_t *ebase, *o1, *o3, *o2, nb;
-  MtCounts mc;
-  mt_counts(sdf, R, &flags, &ebase, mc, &o1, &o3, &o2, nb, st);
-  const int64_t V = mc.V, F = mc.n1 + mc.n3 + 2 * mc.n2;
-  if (V == 0 || F == 0) {
-    out_n[0] = 0;
-    out_n[1] = 0;
-    cudaFreeAsync(flags, st);
-    cudaFreeAsync(ebase, st);
-    cudaFreeAsync(o1, st);
-    cudaFreeAsync(o3, st);
-    cudaFreeAsync(o2, st);
-    cudaStreamSynchronize(st);
-    return 0;
-  }
-  double* verts;
-  int64_t* tris;
-  cudaMallocAsync(&verts, sizeof(double) * 3 * V, st);
-  cudaMallocAsync(&tris, sizeof(int64_t) * 3 * F, st);
-  k_mt_verts<<<grid_blocks(N), 256, 0, st>>>(N, G, sdf, deform, flags, ebase, verts);
-  k_mt_temit<<<(unsigned)nb, kScanThreads, 0, st>>>(K, G, sdf, deform, flags, ebase, verts, o1, o3, o2, mc.n1, mc.n3,
-                                                    mc.n2, tris);
-  // weld
-  int64_t P = 1;
-  while (P < V) P <<= 1;
-  VKey* keys;
-  cudaMallocAsync(&keys, sizeof(VKey) * P, st);
-  k_mt_keys<<<grid_blocks(P), 256, 0, st>>>(V, P, verts, keys);
-  for (int64_t kk = 2; kk <= P; kk <<= 1)
-    for (int64_t jj = kk >> 1; jj > 0; jj >>= 1) k_mt_bitonic<<<grid_blocks(P), 256, 0, st>>>(P, kk, jj, keys);
-  int32_t* first;
-  int64_t *excl, *remap, *scratch;
-  cudaMallocAsync(&first, sizeof(int32_t) * V, st);
-  cudaMallocAsync(&excl, sizeof(int64_t) * (V + 1), st);
-  cudaMallocAsync(&remap, sizeof(int64_t) * V, st);
-  cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(V > F ? V : F), st);
-  k_mt_newgroup<<<grid_blocks(V), 256, 0, st>>>(V, keys, first);
-  scan_counts(first, V, excl, scratch, st);
-  k_mt_remap<<<grid_blocks(V), 256, 0, st>>>(V, keys, first, excl, verts, remap, out_verts);
-  TriKeep tk{tris, remap, out_verts, out_tris};
-  int64_t* d_total = compact(F, tk, scratch, st);
-  int64_t h[2];
-  cudaMemcpyAsync(&h[0], d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&h[1], excl + V, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaStreamSynchronize(st);
-  out_n[0] = h[0];
-  out_n[1] = h[1];
-  for (void* p : {(void*)flags, (void*)ebase, (void*)o1, (void*)o3, (void*)o2, (void*)verts, (void*)tris,
-                  (void*)keys, (void*)first, (void*)excl, (void*)remap, (void*)scratch})
-    cudaFreeAsync(p, st);
-  cudaStreamSynchronize(st);
-  return 0;
+  void* h = nullptr;
+  int64_t nv = 0, nt = 0;
+  int rc = ts_impl_mt_run(sdf, deform, R, &h, &nv, &nt, st);
+  if (!rc) rc = ts_impl_mt_fetch(h, out_verts, out_tris);
+  ts_impl_mt_release(h);
+  out_n[0] = nt;
+  out_n[1] = nv;
+  return rc;
 }

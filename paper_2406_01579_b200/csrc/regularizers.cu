@@ -134,14 +134,6 @@ __device__ __forceinline__ void load_cell(uint32_t c, const Grid& G, const doubl
   }
 }
 
-// corner of local slot `slot` of permutation p (tet_corners: odd permutations swap 2 and 3)
-__host__ __device__ constexpr int perm_corner(int p, int slot) {
-  return slot == 0 ? 0
-                   : (slot == 1 ? (1 << perm_a0(p))
-                                : (((slot == 2) != (p == 1 || p == 2 || p == 5)) ? ((1 << perm_a0(p)) | (1 << perm_a1(p)))
-                                                                                 : 7));
-}
-
 template <int p>
 __device__ __forceinline__ void cell_tet(const CellCorners& K, uint32_t v[4], double P[4][3], double f[4]) {
 #pragma unroll

@@ -113,12 +113,18 @@ def marching_tetrahedra(grid: TetrahedralGrid, field, stream=None) -> TriangleMe
     R = grid.resolution
     sp = _native.stream_ptr(stream)
     nv, nt = _native.i64(), _native.i64()
-    _native.check(L.ts_marching_tets_count(_native.ptr(field.sdf), _native.ptr(field.deformation), R, nv, nt, sp))
+    h = ctypes.c_void_p()
+    _native.check(L.ts_marching_tets_run(_native.ptr(field.sdf), _native.ptr(field.deformation), R,
+                                         ctypes.byref(h), nv, nt, sp))
+    try:
+        # pinned host buffers (torch's caching host allocator): the D2H is a DMA copy, and the
+        # returned numpy arrays share their memory
+        V = torch.empty((nv.value, 3), dtype=torch.float64, pin_memory=True)
+        F = torch.empty((nt.value, 3), dtype=torch.int64, pin_memory=True)
+        if nv.value and nt.value:
+            _native.check(L.ts_marching_tets_fetch(h, V.data_ptr(), F.data_ptr()))
+    finally:
+        _native.check(L.ts_marching_tets_release(h))
     if nv.value == 0 or nt.value == 0:
         return TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64))
-    V = torch.empty((nv.value, 3), dtype=torch.float64, device=field.sdf.device)
-    F = torch.empty((nt.value, 3), dtype=torch.int64, device=field.sdf.device)
-    counts = (ctypes.c_int64 * 2)()
-    _native.check(L.ts_marching_tets(_native.ptr(field.sdf), _native.ptr(field.deformation), R, _native.ptr(V),
-                                     _native.ptr(F), counts, sp))
-    return TriangleMesh(V[:counts[1]].cpu().numpy(), F[:counts[0]].cpu().numpy())
+    return TriangleMesh(V.numpy(), F.numpy())
