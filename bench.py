@@ -354,6 +354,34 @@ def run_gpu(args):
     launches_per_step, other_launches, per_kernel = count_my_kernels(lambda: one_step())
     ktab = kernel_table(lambda: one_step())
 
+    # ---- worst case of SURVEY 8d: s = 20 (fit.py S_START), same views, value only -----------
+    worst = None
+    if not args.no_stress and args.s != 20.0:
+        def step20():
+            field.sdf.copy_(sdf0)
+            field.deformation.copy_(def0)
+            step(20.0, views, lambda vi, m: dmaps[vi])
+        for _ in range(2):
+            step20()
+        barrier()
+        w_ms, w_steps = 0.0, max(3, args.steps // 4)
+        for k in range(w_steps):
+            flush.fill_(float(k))
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step20()
+            e1.record(stream)
+            e1.synchronize()
+            w_ms += e0.elapsed_time(e1)
+        t = torch.tensor([w_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        w_ms = float(t.item())
+        worst = {"steepness": 20.0, "value": n_views * w_steps / (w_ms / 1e3), "unit": "views/s",
+                 "ms_per_step": w_ms / w_steps, "steps": w_steps,
+                 "note": "SURVEY 8d worst case (fit.py S_START): same views and step, device-resident inputs"}
+
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return 0
@@ -368,6 +396,8 @@ def run_gpu(args):
             "clocks": clk.result, "roofline": roof, "kernels": kernels, "kernel_ms_per_step": ktab,
             "workload_counts": {"active_tets": stats.active, "splats_view0": stats.splats[:1],
                                 "pairs_view0": stats.pairs[:1]}}
+    if worst is not None:
+        line["worst_case_s20"] = worst
     if world == 1 and not args.no_stress:
         line["stress"] = stress_probe(ts)
     if not args.no_cpu_baseline:

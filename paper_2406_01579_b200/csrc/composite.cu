@@ -114,6 +114,9 @@ __device__ __forceinline__ float frcp(float x) {
 }
 
 // decode one record (prefetched into shared memory) into the chunk's staged form
+// FOLD (forward): faces the reference rejects as degenerate get edge functions that are always
+// out, so phase A1 needs no validity test
+template <bool FOLD>
 __device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
   const float4* p = reinterpret_cast<const float4*>(&rec);
   float4 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3], q4 = p[4], q5 = p[5];
@@ -153,6 +156,10 @@ __device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
     s.cu[fi] = -(eux * vx[ia] + euy * vy[ia]);
     s.cv[fi] = -(evx * vx[ia] + evy * vy[ia]);
     s.adet[fi] = fabsf(det);
+    if (FOLD && !((s.flags >> fi) & 1u)) {  // degenerate in the reference: never contains a pixel
+      s.eux[fi] = s.euy[fi] = s.evx[fi] = s.evy[fi] = 0.f;
+      s.cu[fi] = s.cv[fi] = -1e30f;
+    }
   }
   // f_hit - f0 = sum(lambda_i df_i): with edge-function errors E <= band/16 the barycentric
   // error is <= 4 E (z_max/z_min) / |det|, i.e. 0.25 band zr spread / |det| per face and
@@ -170,7 +177,9 @@ struct Hit {
 };
 
 // Phase A1: the faces that certainly contain the pixel (bits 0-3); bit 4 = undecided (within
-// the band of a face edge, or a splat with a sign-uncertain face).  Same tests as eval_hits.
+// the band of a face edge, or a splat with a sign-uncertain face).  Same tests as eval_hits:
+// a face is out iff min(u, v, w) < -band, in iff min(u, v, w) > band (faces the reference
+// rejects as degenerate were given edge functions that are always out, see stage()).
 __device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float py) {
   const float band = s.band;
   uint32_t m = s.flags & 16u;
@@ -179,11 +188,9 @@ __device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float p
     const float u = fmaf(s.eux[fi], px, fmaf(s.euy[fi], py, s.cu[fi]));
     const float v = fmaf(s.evx[fi], px, fmaf(s.evy[fi], py, s.cv[fi]));
     const float w = s.adet[fi] - u - v;
-    const bool valid = (s.flags >> fi) & 1u;
-    const bool out = !valid || u < -band || v < -band || w < -band;
-    const bool in = !out && u > band && v > band && w > band;
-    m |= in ? (1u << fi) : 0u;
-    m |= (!out && !in) ? 16u : 0u;
+    const float mn = fminf(fminf(u, v), w);
+    m |= mn > band ? (1u << fi) : 0u;
+    m |= (mn >= -band && !(mn > band)) ? 16u : 0u;
   }
   return m;
 }
@@ -501,6 +508,7 @@ __device__ __forceinline__ void prefetch_rec(Prefetch& P, const SplatRec* __rest
 // most `avail`), cut the chunk so it holds at most kCap pairs, and start the prefetch of the
 // next chunk's list entries.  The warps exchange their scan totals through `wtot` behind a
 // named barrier over the kCh staging threads.
+template <bool FOLD>
 __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, int base, int avail, Prefetch& P,
                                             const float* __restrict__ colors, bool color, Staged* sh,
                                             float (*col)[3], RectTab& R, int tx0, int ty0,
@@ -511,7 +519,7 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
   cp_async_wait_all();
   if (t < m) {
     const int k = P.idx[t];
-    stage(P.raw[t], k, sh[t]);
+    stage<FOLD>(P.raw[t], k, sh[t]);
     const Staged& r = sh[t];
     int x0, y0, nx;
     if (!tile_rect(r.rx0, r.rx1, r.ry0, r.ry1, tx0, ty0, x0, y0, nx, cnt)) {
@@ -668,7 +676,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   }
   for (int base = 0; base < L;) {
     if (threadIdx.x < kCh)
-      stage_chunk(list, base, L - base, F.pf, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
+      stage_chunk<true>(list, base, L - base, F.pf, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
     F.bmask[pix] = 0ull;
     if (threadIdx.x < kCap / 32) F.cbits[threadIdx.x] = 0u;
     if (threadIdx.x == 0) F.nex = 0;
@@ -1104,7 +1112,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   }
   for (int base = 0; base < maxproc;) {
     if (threadIdx.x < kCh)
-      stage_chunk(list, base, maxproc - base, S.pf, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
+      stage_chunk<false>(list, base, maxproc - base, S.pf, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
     S.u.bmask[pix] = 0ull;
     __syncthreads();
     TS_PHASE(0);
