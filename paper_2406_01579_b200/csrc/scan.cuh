@@ -157,7 +157,7 @@ inline int64_t* compact(int64_t n, const F& f, int64_t* offs_scratch, cudaStream
 // (F::State, pred(i, State&), emit(i, pos, const State&)): a single pass — the predicate is
 // evaluated once and the output offsets come from a decoupled look-back over the tiles.
 template <class F>
-__global__ void __launch_bounds__(kScanThreads) k_compact_lb(int64_t n, F f, unsigned long long* __restrict__ status,
+__global__ void __launch_bounds__(kScanThreads, 3) k_compact_lb(int64_t n, F f, unsigned long long* __restrict__ status,
                                                              unsigned long long* __restrict__ ticket, int64_t nb) {
   __shared__ int wcnt[kScanThreads / 32];
   __shared__ long long pre_s;

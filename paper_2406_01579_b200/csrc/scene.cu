@@ -88,10 +88,11 @@ struct CullF {
       ymax = py[c] > ymax ? py[c] : ymax;
     }
   }
-  // projected tet, kept between the visibility test and the emission (k_compact_lb)
+  // projected tet, kept between the visibility test and the emission (k_compact_lb); the
+  // positions are re-formed at emission (an L1 hit) instead of living across the look-back
   struct State {
     uint32_t v[4];
-    double P[4][3], px[4], py[4], z[4];
+    double px[4], py[4], z[4];
   };
   __device__ bool visible(const double px[4], const double py[4], const double z[4]) const {
     double dmin, xmin, xmax, ymin, ymax;
@@ -104,12 +105,19 @@ struct CullF {
     return pred(i, st);
   }
   __device__ bool pred(int64_t i, State& st) const {
-    project4(i, st.v, st.P, st.px, st.py, st.z);
+    double P[4][3];
+    project4(i, st.v, P, st.px, st.py, st.z);
     return visible(st.px, st.py, st.z);
   }
   __device__ void emit(int64_t i, int64_t k, const State& st) const {
     const uint32_t* v = st.v;
-    const double(*P)[3] = st.P;
+    double P[4][3];
+    {
+      int xyz[4][3];
+      uint32_t vv[4];
+      tet_corners((uint32_t)active[i], G, xyz, vv);
+      for (int c = 0; c < 4; ++c) vertex_pos_xyz(xyz[c], vv[c], G, deform, P[c]);
+    }
     const double *px = st.px, *py = st.py, *z = st.z;
     double dmin, xmin, xmax, ymin, ymax;
     bounds(px, py, z, dmin, xmin, xmax, ymin, ymax);
@@ -140,7 +148,7 @@ struct CullF {
       for (int c = 0; c < 3; ++c) nrm[c] = ddiv(g[c], gn);
     if (out.normals)  // optional FP64 outputs (the fused view pipeline needs neither)
       for (int c = 0; c < 3; ++c) out.normals[k * 3 + c] = nrm[c];
-    double md = ddiv(dadd(dadd(dadd(z[0], z[1]), z[2]), z[3]), 4.0);
+    double md = dmul(dadd(dadd(dadd(z[0], z[1]), z[2]), z[3]), 0.25);  // == the division by 4, exactly
     out.md[k] = md;
     if (out.amax) {
       double am;
