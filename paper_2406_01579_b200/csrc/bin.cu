@@ -247,12 +247,23 @@ __device__ __forceinline__ void radix_sort_keys(uint32_t* kq, uint32_t* kv, uint
   if (threadIdx.x == 0) flag = 0;
   for (int full = 0; full < 2; ++full) {
     const int plo = full ? passes_lo : 0;
-    if (P == 4 * NT)
-      radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo);
-    else if (MAXE == 8 || P == 8 * NT)
-      radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo);
-    else
-      radix_sort_tile<NT, MAXE>(kq, kv, H, dbase, plo);
+    if (MAXE == 8) {
+      if (P == 4 * NT)
+        radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo);
+      else
+        radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo);
+    } else {  // P = NT * E with E = ceil(L / NT) (>= 3): no power-of-two padding
+      switch (P / NT) {
+        case 3: radix_sort_tile<NT, 3>(kq, kv, H, dbase, plo); break;
+        case 4: radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo); break;
+        case 5: radix_sort_tile<NT, 5>(kq, kv, H, dbase, plo); break;
+        case 6: radix_sort_tile<NT, 6>(kq, kv, H, dbase, plo); break;
+        case 7: radix_sort_tile<NT, 7>(kq, kv, H, dbase, plo); break;
+        case 8: radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo); break;
+        case 12: radix_sort_tile<NT, 12>(kq, kv, H, dbase, plo); break;
+        default: radix_sort_tile<NT, MAXE>(kq, kv, H, dbase, plo); break;
+      }
+    }
     if (full) break;
     for (int i = threadIdx.x; i < L; i += NT) {
       if (i > 0 && kq[i - 1] == kq[i]) continue;  // not a run start
@@ -338,7 +349,10 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     const int t = tlist[idx];
     const int64_t lo = starts[t];
     const int L = (int)(starts[t + 1] - lo);
-    const int P = L <= 4096 ? 4096 : (L <= 8192 ? 8192 : 16384);
+    // keys per thread: E = ceil(L / 1024) (>= 3), rounded up to 12 / 16 above 8
+    int E = (L + kRadixThreads - 1) / kRadixThreads;
+    E = E < 3 ? 3 : (E <= 8 ? E : (E <= 12 ? 12 : 16));
+    const int P = E * kRadixThreads;
     for (int i = threadIdx.x; i < P; i += kRadixThreads) {
       const uint64_t k = i < L ? keys[lo + i] : ~0ull;  // padding sorts last
       kq[i] = (uint32_t)(k >> 32);
