@@ -32,8 +32,8 @@
 //  C (item-parallel): each warp compacts the blended pairs of its splats (ballot) and
 //    processes them 32 at a time — face-hit backward (_core.pyx:295-341) into a 24-float
 //    row per item — then a segmented sum into the per-(tile, splat) gradient row, written
-//    per list position.  k_chain gathers each splat's rows in a fixed order (deterministic,
-//    atomic-free), applies the normal and camera chains in FP64 and scatters to vertices
+//    added (red.global.add.v4.f32) into the splat's row.  k_chain reads each splat's row
+//    (coalesced), applies the normal and camera chains and scatters to vertices
 //    with one red.global.add.v4.f32 per (splat, vertex).
 #include "../../include/tetsplat_b200.h"
 #include "internal.cuh"
@@ -1216,30 +1216,27 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
       process_batch<COLOR>(S, b0, min(32, nitems - b0), pair_rec, ib0, W, d_normal, d_depth, d_color);
     __syncthreads();
     TS_PHASE(3);
-    // ---- the chunk's per-(tile, splat) rows -------------------------------------------------
+    // ---- the chunk's per-(tile, splat) rows, added into the splats' rows (zeroed per view;
+    //      a splat's tiles add in any order: FP32 rounding-level nondeterminism only) ----------
     for (int i = threadIdx.x; i < n * (SM::AS / 4); i += TS_TILE_PX) {
       const int j = i / (SM::AS / 4), c = i % (SM::AS / 4);
-      reinterpret_cast<float4*>(rows + (lo + base + j) * kGr)[c] = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
+      const float4 v = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
+      // the splat index from the list (S.sh may already hold the next chunk: staging threads
+      // do not wait for this loop)
+      red_add_v4(rows + (int64_t)__ldg(list + base + j) * SM::AS + 4 * c, v.x, v.y, v.z, v.w);
     }
     base += n;
     TS_PHASE(4);
   }
   if (ptime)
     for (int k = 0; k < 5; ++k) atomicAdd(&g_ts_phase[8 + k], (unsigned long long)pacc[k]);
-  // positions no pixel reached: zero rows so the gather sees every pair
-  for (int64_t q = maxproc + threadIdx.x; q < L; q += TS_TILE_PX) {
-    float4* dst = reinterpret_cast<float4*>(rows + (lo + q) * kGr);
-#pragma unroll
-    for (int i = 0; i < kGr / 4; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
 }
 
 // per-splat gather + normal chain + camera chain (raster.py:253-306).  FP32 chain math (the
 // gradients are FP32); vertex positions are formed in FP64 (grid coordinate + deformation)
 // and only their differences / camera-space coordinates are rounded, one vertex at a time.
 template <bool COLOR>
-__global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const int64_t* __restrict__ splat_off,
-                                               const int32_t* __restrict__ pos_of, const float* __restrict__ rows,
+__global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const float* __restrict__ rows,
                                                const int32_t* __restrict__ vert_ids,
                                                const int32_t* __restrict__ tet_ids, const double* __restrict__ fsc,
                                                const double* __restrict__ deform, Grid G, Camera cam,
@@ -1247,18 +1244,15 @@ __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const int64_t* __re
   constexpr int NQ = COLOR ? 6 : 5;  // float4s of a row that carry data
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
     float a[4 * NQ];
-#pragma unroll
-    for (int i = 0; i < 4 * NQ; ++i) a[i] = 0.f;
-    const int64_t r0 = splat_off[k], r1 = splat_off[k + 1];
-    for (int64_t r = r0; r < r1; ++r) {
-      const float4* src = reinterpret_cast<const float4*>(rows + (int64_t)__ldg(pos_of + r) * kGr);
+    {
+      const float4* src = reinterpret_cast<const float4*>(rows + k * (4 * NQ));
 #pragma unroll
       for (int i = 0; i < NQ; ++i) {
         const float4 q = __ldg(src + i);
-        a[4 * i] += q.x;
-        a[4 * i + 1] += q.y;
-        a[4 * i + 2] += q.z;
-        a[4 * i + 3] += q.w;
+        a[4 * i] = q.x;
+        a[4 * i + 1] = q.y;
+        a[4 * i + 2] = q.z;
+        a[4 * i + 3] = q.w;
       }
     }
     const int4 vv = __ldg(reinterpret_cast<const int4*>(vert_ids) + k);
@@ -1430,10 +1424,11 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   }
   float* const given_rows = scr ? scr->rows : nullptr;
   int32_t* const given_order = scr ? scr->torder : nullptr;
-  float* rows = take_tmp(given_rows, kGr * (size_t)M, st);
+  float* rows = take_tmp(given_rows, kGr * (size_t)M, st);  // per-splat rows: K <= M
   int32_t* torder = take_tmp(given_order, T, st);
   k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
+  cudaMemsetAsync(rows, 0, sizeof(float) * (color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
   if (color)
     k_backward<true><<<T, TS_TILE_PX, smem_c, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
@@ -1447,10 +1442,10 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (color)
-    k_chain<true><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
+    k_chain<true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform,
                                           make_grid(R), cam, d_vert, d_color);
   else
-    k_chain<false><<<blocks, 128, 0, st>>>(K, b.splat_off, b.pos_of, rows, vert_ids, tet_ids, fsc, deform,
+    k_chain<false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform,
                                            make_grid(R), cam, d_vert, nullptr);
   put_tmp(rows, given_rows, st);
   put_tmp(torder, given_order, st);

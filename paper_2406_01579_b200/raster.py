@@ -58,7 +58,7 @@ class TileBins:
     """Per-tile splat lists sorted by (tile id, quantized mean depth) (raster.py:53-71).
 
     starts/items equal the reference's bit for bit; pos_of, splat_off, nonmono and witems
-    are the B200 extras (deterministic gradient gather, resorting window)."""
+    are the B200 extras (pair positions, resorting window)."""
 
     tile_size: int
     tiles_x: int
