@@ -27,36 +27,86 @@ __device__ __forceinline__ bool alpha_max_pass(const double f[4], double s, doub
   return am >= thr;
 }
 
-struct PrefilterF {
-  const double* sdf;
-  Grid G;
-  double s, thr;
-  int32_t* out;
-  __device__ bool pred(int64_t t) const {
-    uint32_t v[4];
-    tet_vertices((uint32_t)t, G, v);
-    double f[4] = {sdf[v[0]], sdf[v[1]], sdf[v[2]], sdf[v[3]]};
-    // alpha_max = sigmoid(-b) (1 - e^{-(a-b)}), a = s fmax >= b = s fmin, estimated in FP32
-    // from the FP64 difference (relative error ~1e-6); the reference's FP64 evaluation errs
-    // by < 1e-13 absolute, so outside a 2e-6 relative band around the threshold the decision
-    // is certain and only the pairs inside it take the FP64 softplus path
-    double fmx = f[0], fmn = f[0];
-    for (int i = 1; i < 4; ++i) {
-      fmx = f[i] > fmx ? f[i] : fmx;
-      fmn = f[i] < fmn ? f[i] : fmn;
-    }
-    const double a = dmul(s, fmx), b = dmul(s, fmn);
-    const float y = (float)(-b), d = (float)dsub(a, b);
-    const float ey = expf(-fabsf(y)), r = 1.0f / (1.0f + ey);
-    const float sig = y >= 0.f ? r : ey * r;  // sigmoid(-b)
-    const float est = sig * -expm1f(-d);
-    const float tf = (float)thr;
-    if (fabsf(est - tf) > 2e-6f * tf + 1e-12f) return est > tf;
-    return alpha_max_pass(f, s, thr, nullptr);
+// alpha_max >= thr for a tet with corner SDF values f: alpha_max = sigmoid(-b) (1 - e^{-(a-b)}),
+// a = s fmax >= b = s fmin, estimated in FP32 from the FP64 difference (relative error ~1e-6);
+// the reference's FP64 evaluation errs by < 1e-13 absolute, so outside a 2e-6 relative band
+// around the threshold the decision is certain and only the tets inside it take the FP64
+// softplus path
+__device__ __forceinline__ bool prefilter_pass(const double f[4], double s, double thr) {
+  double fmx = f[0], fmn = f[0];
+  for (int i = 1; i < 4; ++i) {
+    fmx = f[i] > fmx ? f[i] : fmx;
+    fmn = f[i] < fmn ? f[i] : fmn;
   }
-  __device__ void emit(int64_t t, int64_t pos) const { out[pos] = (int32_t)t; }
-};
+  const double a = dmul(s, fmx), b = dmul(s, fmn);
+  const float y = (float)(-b), d = (float)dsub(a, b);
+  const float ey = expf(-fabsf(y)), r = 1.0f / (1.0f + ey);
+  const float sig = y >= 0.f ? r : ey * r;
+  const float est = sig * -expm1f(-d);
+  const float tf = (float)thr;
+  if (fabsf(est - tf) > 2e-6f * tf + 1e-12f) return est > tf;
+  return alpha_max_pass(f, s, thr, nullptr);
+}
 
+// K1 per cell: the 8 corner samples of a cell are loaded once for its 6 tets (tet id = cell * 6
+// + p, cells z-fastest = tet-id order), two consecutive cells per thread; survivors compacted
+// in increasing id with a decoupled look-back (single pass).
+constexpr int kPfCells = 2;
+__global__ void __launch_bounds__(256) k_prefilter_cells(int64_t C, Grid G, const double* __restrict__ sdf, double s,
+                                                         double thr, int32_t* __restrict__ out,
+                                                         unsigned long long* __restrict__ status,
+                                                         unsigned long long* __restrict__ ticket, int64_t nb) {
+  __shared__ int wcnt[8];
+  __shared__ long long pre_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int tile = lb_tile(ticket);
+  const int64_t c0 = (int64_t)tile * (256 * kPfCells) + (int64_t)threadIdx.x * kPfCells;
+  uint32_t mask = 0;  // bit k * 6 + p: tet p of cell c0 + k passes
+#pragma unroll
+  for (int k = 0; k < kPfCells; ++k) {
+    const int64_t c = c0 + k;
+    if (c >= C) break;
+    const uint32_t q = G.dR.div((uint32_t)c);  // ix*R + iy
+    const uint32_t iz = (uint32_t)c - q * (uint32_t)G.R;
+    const uint32_t ix = G.dR.div(q);
+    const uint32_t iy = q - ix * (uint32_t)G.R;
+    const uint32_t n = (uint32_t)G.n, v0 = ix + n * (iy + n * iz);
+    double fc[8];
+#pragma unroll
+    for (int lc = 0; lc < 8; ++lc) fc[lc] = __ldg(sdf + v0 + (lc & 1) + n * (((lc >> 1) & 1) + n * ((lc >> 2) & 1)));
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const double f[4] = {fc[perm_corner(p, 0)], fc[perm_corner(p, 1)], fc[perm_corner(p, 2)], fc[perm_corner(p, 3)]};
+      if (prefilter_pass(f, s, thr)) mask |= 1u << (k * 6 + p);
+    }
+  }
+  const int cnt = __popc(mask);
+  int v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) wcnt[wid] = v;
+  __syncthreads();
+  int before = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    before += (w < wid) ? wcnt[w] : 0;
+    agg += wcnt[w];
+  }
+  if (wid == 0) {
+    const long long pr = lb_exclusive(status, tile, agg);
+    if (lane == 0) pre_s = pr;
+  }
+  __syncthreads();
+  long long pos = pre_s + before + v - cnt;
+  for (uint32_t m = mask; m; m &= m - 1u) {
+    const int b = __ffs(m) - 1;
+    out[pos++] = (int32_t)((c0 + b / 6) * 6 + b % 6);
+  }
+  if (tile == nb - 1 && threadIdx.x == 0) *reinterpret_cast<long long*>(ticket) = pre_s + agg;
+}
 
 struct CullF {
   const int32_t* active;
@@ -180,11 +230,15 @@ using namespace ts;
 // host entry points used by abi.cu
 int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_t* out_active,
                           int64_t* scratch, cudaStream_t st) {
-  const int64_t K = 6ll * R * R * R;
-  PrefilterF f{sdf, make_grid(R), s, thr, out_active};
-  int64_t* d_total = compact(K, f, scratch, st);
+  // scratch: compact_blocks(6 R^3) >= nb + 1 entries (a tile = 512 cells = 3072 tets)
+  const int64_t C = (int64_t)R * R * R;
+  const int64_t nb = (C + 256 * kPfCells - 1) / (256 * kPfCells);
+  cudaMemsetAsync(scratch, 0, sizeof(int64_t) * (nb + 1), st);
+  k_prefilter_cells<<<(unsigned)nb, 256, 0, st>>>(C, make_grid(R), sdf, s, thr, out_active,
+                                                  reinterpret_cast<unsigned long long*>(scratch),
+                                                  reinterpret_cast<unsigned long long*>(scratch + nb), nb);
   int64_t h = 0;
-  cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h, scratch + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   return h;
 }

@@ -47,3 +47,28 @@ def test_sphere_watertight_and_empty(ts):
     assert m.euler_characteristic() == 2 and m.is_watertight()
     e = ts.FieldState.from_numpy(np.ones(g.num_vertices), np.zeros((g.num_vertices, 3)), ts.deform_limit_for(g))
     assert ts.marching_tetrahedra(g, e).is_empty
+
+
+def test_two_phase_abi_matches_one_pass(ts):
+    """ts_marching_tets_count + ts_marching_tets (caller-owned device outputs) == the one-pass
+    run/fetch/release path behind marching_tetrahedra."""
+    import ctypes
+    import torch
+    from paper_2406_01579_b200 import _native
+    G = load_golden("mt.npz")
+    R = 24
+    g = ts.build_grid(R)
+    fs = ts.FieldState.from_numpy(G["r24_sdf"], G["r24_deform"], ts.deform_limit_for(g))
+    ref = ts.marching_tetrahedra(g, fs)
+    L = _native.lib()
+    nv, nt = _native.i64(), _native.i64()
+    _native.check(L.ts_marching_tets_count(_native.ptr(fs.sdf), _native.ptr(fs.deformation), R, nv, nt, None))
+    assert nv.value == ref.vertices.shape[0] and nt.value == ref.triangles.shape[0]
+    V = torch.empty((nv.value, 3), dtype=torch.float64, device="cuda")
+    F = torch.empty((nt.value, 3), dtype=torch.int64, device="cuda")
+    counts = (ctypes.c_int64 * 2)()
+    _native.check(L.ts_marching_tets(_native.ptr(fs.sdf), _native.ptr(fs.deformation), R, _native.ptr(V),
+                                     _native.ptr(F), counts, None))
+    assert counts[0] == nt.value and counts[1] == nv.value
+    assert np.array_equal(V.cpu().numpy(), ref.vertices)
+    assert np.array_equal(F.cpu().numpy(), ref.triangles)
