@@ -234,23 +234,20 @@ struct Blend {
   bool clipped;   // alpha_un > ALPHA_CLIP (no d_alpha/d_f, _core.pyx:462)
 };
 
-// One face of the reference's _face_hit (_core.pyx:39-64) in exact FP64 (no contraction).
-__device__ __forceinline__ bool exact_face(const Scene64& S, int64_t k, int fi, double px, double py, double& zp,
-                                          double& fh) {
-  const double* P = S.proj + k * 8;
-  const double* Z = S.depths + k * 4;
-  const double* F = S.f + k * 4;
+// One face of the reference's _face_hit (_core.pyx:39-64) in exact FP64 (no contraction); the
+// face's vertices a, b, c (projected x, y and depth) are given, F = the splat's SDF samples.
+__device__ __forceinline__ bool exact_face(const double* F, int fi, double ax, double ay, double bx, double by,
+                                          double cx, double cy, double za, double zb, double zc, double px, double py,
+                                          double& zp, double& fh) {
   const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
-  const double ax = P[2 * ia], ay = P[2 * ia + 1];
-  const double m00 = dsub(P[2 * ib], ax), m10 = dsub(P[2 * ib + 1], ay);
-  const double m01 = dsub(P[2 * ic], ax), m11 = dsub(P[2 * ic + 1], ay);
+  const double m00 = dsub(bx, ax), m10 = dsub(by, ay);
+  const double m01 = dsub(cx, ax), m11 = dsub(cy, ay);
   const double det = dsub(dmul(m00, m11), dmul(m01, m10));
   if (fabs(det) < kEpsDet) return false;
   const double rx = dsub(px, ax), ry = dsub(py, ay);
   const double u = ddiv(dsub(dmul(m11, rx), dmul(m01, ry)), det);
   const double v = ddiv(dadd(dmul(-m10, rx), dmul(m00, ry)), det);
   if (u < 0.0 || v < 0.0 || dadd(u, v) > 1.0) return false;
-  const double za = Z[ia], zb = Z[ib], zc = Z[ic];
   const double w0 = ddiv(dsub(dsub(1.0, u), v), za), w1 = ddiv(u, zb), w2 = ddiv(v, zc);
   const double Ss = dadd(dadd(w0, w1), w2);
   fh = ddiv(dadd(dadd(dmul(w0, F[ia]), dmul(w1, F[ib])), dmul(w2, F[ic])), Ss);
@@ -260,9 +257,13 @@ __device__ __forceinline__ bool exact_face(const Scene64& S, int64_t k, int fi, 
 
 // pull a splat's FP64 scene rows into L1 when one of its pairs is queued for re-decision
 __device__ __forceinline__ void prefetch_exact(const Scene64& S, int64_t k) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.proj + k * 8));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.proj + k * 8 + 7));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(S.depths + k * 4));
+  if (S.proj) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.proj + k * 8));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.proj + k * 8 + 7));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.depths + k * 4));
+  } else {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(S.vert_ids + k * 4));
+  }
   asm volatile("prefetch.global.L1 [%0];" ::"l"(S.f + k * 4));
   asm volatile("prefetch.global.L1 [%0];" ::"l"(S.bbox + k * 4));
 }
@@ -276,10 +277,29 @@ __device__ __forceinline__ bool exact_group(const Scene64& S, bool act, int64_t 
   const double px = xi + 0.5, py = yi + 0.5;
   double zp = 0.0, fh = 0.0;
   bool hit = false;
+  const int ia = fi == 0 ? 1 : 0, ib = fi <= 1 ? 2 : 1, ic = fi <= 2 ? 3 : 2;
+  double ax, ay, bx, by, cx, cy, za, zb, zc;
+  if (S.proj) {
+    const double* P = S.proj + k * 8;
+    const double* Z = S.depths + k * 4;
+    ax = P[2 * ia]; ay = P[2 * ia + 1]; bx = P[2 * ib]; by = P[2 * ib + 1]; cx = P[2 * ic]; cy = P[2 * ic + 1];
+    za = Z[ia]; zb = Z[ib]; zc = Z[ic];
+  } else {
+    // lane fi projects vertex fi of the splat (camera.py:56-67, as the scene build did); the
+    // four lanes of the group exchange the three vertices of their faces
+    double Pw[3], pc[3], vx, vy, vz;
+    vertex_position((uint32_t)S.vert_ids[k * 4 + fi], S.G, S.deform, Pw);
+    project_point(S.cam, Pw, vx, vy, vz, pc);
+    ax = __shfl_sync(0xffffffffu, vx, lead + ia); ay = __shfl_sync(0xffffffffu, vy, lead + ia);
+    bx = __shfl_sync(0xffffffffu, vx, lead + ib); by = __shfl_sync(0xffffffffu, vy, lead + ib);
+    cx = __shfl_sync(0xffffffffu, vx, lead + ic); cy = __shfl_sync(0xffffffffu, vy, lead + ic);
+    za = __shfl_sync(0xffffffffu, vz, lead + ia); zb = __shfl_sync(0xffffffffu, vz, lead + ib);
+    zc = __shfl_sync(0xffffffffu, vz, lead + ic);
+  }
   if (act) {
     const double* B = S.bbox + k * 4;
     const bool inb = !(px < B[0] || px > B[2] || py < B[1] || py > B[3]);
-    hit = inb && exact_face(S, k, fi, px, py, zp, fh);
+    hit = inb && exact_face(S.f + k * 4, fi, ax, ay, bx, by, cx, cy, za, zb, zc, px, py, zp, fh);
   }
   double zlo = 0, zhi = 0, flo = 0, fhi = 0;
   int n = 0, lo = -1, hi = -1;

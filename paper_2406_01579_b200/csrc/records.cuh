@@ -95,10 +95,16 @@ __device__ inline SplatRec make_record(const double proj[8], const double depths
 
 // FP64 view of the scene for the exact fallback and the chain kernel
 struct Scene64 {
-  const double* proj;     // [K,4,2]
-  const double* depths;   // [K,4]
+  const double* proj;     // [K,4,2]  (nullptr: re-projected from the vertices, see below)
+  const double* depths;   // [K,4]    (nullptr with proj)
   const double* f;        // [K,4]
   const double* bbox;     // [K,4]
+  // the fused view path stores no proj / depths (96 B per splat of write traffic): the exact
+  // path re-projects the splat's vertices with the same FP64 functions (bit-identical values)
+  const int32_t* vert_ids;  // [K,4]
+  const double* deform;
+  Grid G;
+  Camera cam;
 };
 
 // Exact replica of _splat_hits (_core.pyx:67-95) incl. the bbox test.

@@ -179,13 +179,15 @@ struct CullF {
     }
     // 16-byte stores (the arrays are 16-byte aligned per splat)
     reinterpret_cast<int4*>(out.vert_ids)[k] = make_int4((int)v[0], (int)v[1], (int)v[2], (int)v[3]);
-    double2* pj = reinterpret_cast<double2*>(out.proj + k * 8);
-    for (int c = 0; c < 4; ++c) pj[c] = make_double2(px[c], py[c]);
-    double2* dz = reinterpret_cast<double2*>(out.depths + k * 4);
+    if (out.proj) {  // optional: the fused view path re-projects in its exact path instead
+      double2* pj = reinterpret_cast<double2*>(out.proj + k * 8);
+      for (int c = 0; c < 4; ++c) pj[c] = make_double2(px[c], py[c]);
+      double2* dz = reinterpret_cast<double2*>(out.depths + k * 4);
+      dz[0] = make_double2(z[0], z[1]);
+      dz[1] = make_double2(z[2], z[3]);
+    }
     double2* ff = reinterpret_cast<double2*>(out.f + k * 4);
     double2* bx = reinterpret_cast<double2*>(out.bbox + k * 4);
-    dz[0] = make_double2(z[0], z[1]);
-    dz[1] = make_double2(z[2], z[3]);
     ff[0] = make_double2(f[0], f[1]);
     ff[1] = make_double2(f[2], f[3]);
     bx[0] = make_double2(bb[0], bb[1]);

@@ -114,8 +114,9 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   ws->valid = false;
   // ---- K2 build_scene ----------------------------------------------------------------------
   const int64_t cap = n_active > 0 ? n_active : 1;
-  SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), ws->proj.get<double>(cap * 8),
-              ws->depths.get<double>(cap * 4), ws->f.get<double>(cap * 4), nullptr,
+  // no FP64 proj / depths: the forward's exact path re-projects the few splats it needs
+  SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), nullptr,
+              nullptr, ws->f.get<double>(cap * 4), nullptr,
               ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
               ws->rec.get<SplatRec>(cap)};
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1, 1));
@@ -176,7 +177,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   float4* prec = ws->pair_rec.get<float4>(P);
   if (!pbits || !prec) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0) {
-    ts_impl_forward(tx, ty, bv, so.rec, colors, Scene64{so.proj, so.depths, so.f, so.bbox}, cam.width, cam.height, s,
+    ts_impl_forward(tx, ty, bv, so.rec, colors, Scene64{nullptr, nullptr, so.f, so.bbox, so.vert_ids, deform, make_grid(R), cam}, cam.width, cam.height, s,
                     (float)t_stop, item_off, P, pbits, prec, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
                     st, &scr);
   } else {
