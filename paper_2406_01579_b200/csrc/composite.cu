@@ -10,8 +10,8 @@
 //  A (pair-parallel, dense lanes): hit + opacity of every pair.  FP32 on sign-normalised
 //    edge functions in splat-anchored coordinates; any pair within a rigorous FP32 error
 //    band of a decision threshold (face edge, alpha = 0, alpha = ALPHA_CLIP, tiny alpha)
-//    is re-decided with the reference's exact FP64 arithmetic (records.cuh:
-//    splat_hits_exact), so the blended set matches the FP64 reference.  The pair's
+//    is re-decided with the reference's exact FP64 arithmetic (below:
+//    exact_group / exact_face), so the blended set matches the FP64 reference.  The pair's
 //    (alpha, 1-alpha) goes to shared memory for phase B and, with s*sigmoid(-s f) of the
 //    entry/exit points and the two face ids, to the global pair records the backward
 //    reads — the backward never re-evaluates a hit.
@@ -177,7 +177,7 @@ struct Hit {
 };
 
 // Phase A1: the faces that certainly contain the pixel (bits 0-3); bit 4 = undecided (within
-// the band of a face edge, or a splat with a sign-uncertain face).  Same tests as eval_hits:
+// the band of a face edge, or a splat with a sign-uncertain face).  The reference's face test:
 // a face is out iff min(u, v, w) < -band, in iff min(u, v, w) > band (faces the reference
 // rejects as degenerate were given edge functions that are always out, see stage()).
 __device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float py) {
@@ -196,7 +196,7 @@ __device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float p
 }
 
 // Phase A2: entry / exit among the in-faces of mask m (face order, first hit seeds, strict
-// < / > updates — eval_hits' rule), recomputing each in-face's values bit-identically.
+// < / > updates — _splat_hits' rule, _core.pyx:67-95), recomputing each in-face's values.
 __device__ __forceinline__ void hit_faces(const Staged& s, float px, float py, uint32_t m, Hit& h) {
   int nh = 0, lo = -1, hi = -1;
   float zlo = 0.f, zhi = 0.f, flo = 0.f, fhi = 0.f;

@@ -107,44 +107,4 @@ struct Scene64 {
   Camera cam;
 };
 
-// Exact replica of _splat_hits (_core.pyx:67-95) incl. the bbox test.
-__device__ inline int splat_hits_exact(const Scene64& S, int64_t k, double px, double py, double& f_prev,
-                                       double& f_next, int& fi_prev, int& fi_next) {
-  const double* B = S.bbox + k * 4;
-  if (px < B[0] || px > B[2] || py < B[1] || py > B[3]) return 0;
-  const double* P = S.proj + k * 8;
-  const double* Z = S.depths + k * 4;
-  const double* F = S.f + k * 4;
-  double z_lo = 0, z_hi = 0, f_lo = 0, f_hi = 0;
-  int n = 0, lo_fi = -1, hi_fi = -1;
-#pragma unroll 1
-  for (int fi = 0; fi < 4; ++fi) {
-    const int ia = face_vert(fi, 0), ib = face_vert(fi, 1), ic = face_vert(fi, 2);
-    double ax = P[2 * ia], ay = P[2 * ia + 1];
-    double m00 = dsub(P[2 * ib], ax), m10 = dsub(P[2 * ib + 1], ay);
-    double m01 = dsub(P[2 * ic], ax), m11 = dsub(P[2 * ic + 1], ay);
-    double det = dsub(dmul(m00, m11), dmul(m01, m10));
-    if (fabs(det) < kEpsDet) continue;
-    double rx = dsub(px, ax), ry = dsub(py, ay);
-    double u = ddiv(dsub(dmul(m11, rx), dmul(m01, ry)), det);
-    double v = ddiv(dadd(dmul(-m10, rx), dmul(m00, ry)), det);
-    if (u < 0.0 || v < 0.0 || dadd(u, v) > 1.0) continue;
-    double za = Z[ia], zb = Z[ib], zc = Z[ic];
-    double w0 = ddiv(dsub(dsub(1.0, u), v), za), w1 = ddiv(u, zb), w2 = ddiv(v, zc);
-    double Ss = dadd(dadd(w0, w1), w2);
-    double fh = ddiv(dadd(dadd(dmul(w0, F[ia]), dmul(w1, F[ib])), dmul(w2, F[ic])), Ss);
-    double zp = ddiv(1.0, Ss);
-    if (n == 0) {
-      z_lo = z_hi = zp; f_lo = f_hi = fh; lo_fi = hi_fi = fi;
-    } else {
-      if (zp < z_lo) { z_lo = zp; f_lo = fh; lo_fi = fi; }
-      if (zp > z_hi) { z_hi = zp; f_hi = fh; hi_fi = fi; }
-    }
-    ++n;
-  }
-  if (n < 2) return 0;
-  f_prev = f_lo; f_next = f_hi; fi_prev = lo_fi; fi_next = hi_fi;
-  return 1;
-}
-
 }  // namespace ts
