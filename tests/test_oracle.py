@@ -26,6 +26,9 @@ def test_grid_matches_reference(R):
     assert np.array_equal(g.rest_positions, G["rest"])
     assert np.array_equal(g.tets, G["tets"])
     assert np.array_equal(g.edges, G["edges"])
+    h = O.build_grid(R, with_edges=False)  # the edge-free build used for the 256^3 MT check
+    assert np.array_equal(h.rest_positions, G["rest"]) and np.array_equal(h.tets, G["tets"])
+    assert h.edges.shape == (0, 2)
 
 
 @pytest.mark.parametrize("case", RENDER_CASES)
