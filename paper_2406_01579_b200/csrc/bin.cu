@@ -117,9 +117,11 @@ __device__ __forceinline__ void bitonic_sort(Ptr s, int P, int nthreads) {
 }
 
 __device__ __forceinline__ void emit_sorted(uint64_t key, int64_t p, int tile, int tiles_x, const BinRec* br,
-                                            const int64_t* splat_off, int32_t* items, int32_t* pos_of) {
+                                            const int64_t* splat_off, int32_t* items, int32_t* pos_of,
+                                            uint32_t* qsorted) {
   int k = (int)(uint32_t)key;
   items[p] = k;
+  if (qsorted) qsorted[p] = (uint32_t)(key >> 32);  // the depth key per position (k_window)
   BinRec b = br[k];
   int tx = tile % tiles_x, ty = tile / tiles_x;
   int local = (ty - b.ty0) * b.nx + (tx - b.tx0);
@@ -132,7 +134,8 @@ __device__ __forceinline__ void sort_tile(uint64_t* s, int& bad, int t, const in
                                           const uint64_t* __restrict__ keys, int tiles_x,
                                           const BinRec* __restrict__ br, const int64_t* __restrict__ splat_off,
                                           const double* __restrict__ md, int32_t* __restrict__ items,
-                                          int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono) {
+                                          int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono,
+                                          uint32_t* __restrict__ qsorted) {
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
   int P = 1;
   while (P < L) P <<= 1;
@@ -142,7 +145,7 @@ __device__ __forceinline__ void sort_tile(uint64_t* s, int& bad, int t, const in
   bitonic_sort(s, P, THREADS);
   int mybad = 0;
   for (int i = threadIdx.x; i < L; i += THREADS) {
-    emit_sorted(s[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+    emit_sorted(s[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
     if (i + 1 < L && md[(uint32_t)s[i]] > md[(uint32_t)s[i + 1]]) mybad = 1;
   }
   if (mybad) bad = 1;
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
                                                             const int64_t* __restrict__ splat_off,
                                                             const double* __restrict__ md,
                                                             int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                            uint8_t* __restrict__ nonmono) {
+                                                            uint8_t* __restrict__ nonmono, uint32_t* __restrict__ qsorted) {
   extern __shared__ uint64_t s[];
   __shared__ int bad, longrun;
   const int t = blockIdx.x;
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
   if (L <= 0 || L > cap) return;
   if (L <= 512 || cap > 8 * THREADS) {  // short lists: bitonic
-    sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono);
+    sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono, qsorted);
     return;
   }
   // longer lists: the radix sort of k_tile_sort_long at THREADS threads (kq / kv alias s)
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   radix_sort_keys<THREADS, 8>(kq, kv, H, dbase, P, (int)L, passes_lo, longrun);
   int mybad = 0;
   for (int i = threadIdx.x; i < L; i += THREADS) {
-    emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+    emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
     if (i + 1 < L && md[kv[i]] > md[kv[i + 1]]) mybad = 1;
   }
   if (mybad) bad = 1;
@@ -336,7 +339,8 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     const int32_t* __restrict__ tlist, const int64_t* __restrict__ tcount, const int64_t* __restrict__ starts,
     const uint64_t* __restrict__ keys, int tiles_x, const BinRec* __restrict__ br,
     const int64_t* __restrict__ splat_off, const double* __restrict__ md, int32_t* __restrict__ items,
-    int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono, int cap, int passes_lo) {
+    int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono, int cap, int passes_lo,
+    uint32_t* __restrict__ qsorted) {
   extern __shared__ uint32_t sm32[];
   __shared__ int longrun;
   uint32_t* kq = sm32;
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     radix_sort_keys<kRadixThreads, 16>(kq, kv, H, dbase, P, L, passes_lo, longrun);
     int mybad = 0;
     for (int i = threadIdx.x; i < L; i += kRadixThreads) {
-      emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+      emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
       if (i + 1 < L && md[kv[i]] > md[kv[i + 1]]) mybad = 1;
     }
     if (mybad) bad = 1;
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, co
                                                            const double* __restrict__ md,
                                                            uint64_t* __restrict__ scratch,
                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                           uint8_t* __restrict__ nonmono) {
+                                                           uint8_t* __restrict__ nonmono, uint32_t* __restrict__ qsorted) {
   __shared__ int bad;
   const int t = blockIdx.x;
   if (t >= T) return;
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, co
     }
   int mybad = 0;
   for (int64_t i = threadIdx.x; i < L; i += 1024) {
-    emit_sorted(s[i], lo + i, t, tiles_x, br, splat_off, items, pos_of);
+    emit_sorted(s[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
     if (i + 1 < L && md[(uint32_t)s[i]] > md[(uint32_t)s[i + 1]]) mybad = 1;
   }
   if (mybad) bad = 1;
@@ -467,7 +471,7 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
 // Phase 2: scatter keys + per-tile sort.  keys: [M]; gscratch: [2M] only when maxL > 16384.
 void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const BinWork& w, const int64_t* starts,
                       const int64_t* splat_off, int64_t maxL, uint64_t* keys, uint64_t* gscratch, int32_t* items,
-                      int32_t* pos_of, uint8_t* nonmono, cudaStream_t st) {
+                      int32_t* pos_of, uint8_t* nonmono, cudaStream_t st, uint32_t* qsorted) {
   const int T = tiles_x * tiles_y;
   cudaMemsetAsync(w.tile_cnt, 0, sizeof(int32_t) * T, st);
   cudaMemsetAsync(nonmono, 0, T, st);
@@ -481,7 +485,7 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
     while (kbits < 32 && ((int64_t)1 << kbits) < K) ++kbits;
     const size_t smem_s = sizeof(uint32_t) * (2 * 2048 + 8 * 256 + 256);  // kq, kv | bitonic u64; H; dbase
     k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, 2048, (kbits + 7) / 8, starts, keys, tiles_x, w.br, splat_off,
-                                                  md, items, pos_of, nonmono);
+                                                  md, items, pos_of, nonmono, qsorted);
     if (maxL > 2048) {
       // the scatter cursor is free again: reuse it as the long-tile list
       cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
@@ -498,10 +502,10 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
       const int per_sm = smem <= 110 * 1024 ? 2 : 1;
       k_tile_sort_long<<<148 * per_sm, kRadixThreads, smem, st>>>(w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br,
                                                                  splat_off, md, items, pos_of, nonmono, cap,
-                                                                 (kbits + 7) / 8);
+                                                                 (kbits + 7) / 8, qsorted);
     }
     if (maxL > 16384)
       k_tile_sort_global<<<T, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,
-                                             pos_of, nonmono);
+                                             pos_of, nonmono, qsorted);
   }
 }

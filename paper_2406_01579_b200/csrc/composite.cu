@@ -841,13 +841,15 @@ __global__ void __launch_bounds__(256) k_window(int T, const int64_t* __restrict
                                                 const uint8_t* __restrict__ nonmono, const double* __restrict__ md,
                                                 int n_w, double near_, double far_, int32_t* __restrict__ witems,
                                                 uint32_t* __restrict__ qpos, int32_t* __restrict__ widx_s,
-                                                double* __restrict__ wz_s) {
+                                                double* __restrict__ wz_s, bool q_ready) {
   const int t = blockIdx.x;
   if (t >= T || !nonmono[t]) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
-  // the tile's depth keys, once per position
-  for (int64_t i = threadIdx.x; i < L; i += blockDim.x) qpos[lo + i] = qkey(md[items[lo + i]], near_, far_);
-  __syncthreads();
+  // the tile's depth keys, once per position (q_ready: the sort already wrote them)
+  if (!q_ready) {
+    for (int64_t i = threadIdx.x; i < L; i += blockDim.x) qpos[lo + i] = qkey(md[items[lo + i]], near_, far_);
+    __syncthreads();
+  }
   const uint32_t* qs = qpos + lo;
   for (int64_t i = threadIdx.x; i < L; i += blockDim.x) {
     const uint32_t qi = qs[i];
@@ -1372,9 +1374,10 @@ static void put_tmp(T* p, const T* given, cudaStream_t st) {
   if (p && p != given) cudaFreeAsync(p, st);
 }
 
+// q_ready: scr->cnt already holds each position's depth key (written by the sort)
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int64_t M, const double* md, int n_w,
                                 double near_, double far_, const SplatRec* rec, int64_t* item_off, cudaStream_t st,
-                                const ViewScratch* scr) {
+                                const ViewScratch* scr, bool q_ready) {
   const ViewScratch none{};
   const ViewScratch& sc = scr ? *scr : none;
   const int T = tiles_x * tiles_y;
@@ -1387,7 +1390,8 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   int32_t* cnt = take_tmp(sc.cnt, M, st);
   int64_t* scratch = take_tmp(sc.scan, compact_blocks(M), st);
   uint32_t* qpos = reinterpret_cast<uint32_t*>(cnt);  // dead before k_item_counts writes cnt
-  k_window<<<T, 256, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, qpos, widx, wz);
+  k_window<<<T, 256, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, qpos, widx, wz,
+                              q_ready && sc.cnt);
   k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
   scan_counts(cnt, M, item_off, scratch, st);
   int64_t total = 0;

@@ -66,11 +66,12 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
                        int64_t* maxL_out, cudaStream_t st);
 void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const ts::BinWork& w,
                       const int64_t* starts, const int64_t* splat_off, int64_t maxL, uint64_t* keys,
-                      uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st);
+                      uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st,
+                      uint32_t* qsorted = nullptr);
 void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n);
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, const double* md,
                                 int n_w, double near_, double far_, const ts::SplatRec* rec, int64_t* item_off,
-                                cudaStream_t st, const ts::ViewScratch* scr = nullptr);
+                                cudaStream_t st, const ts::ViewScratch* scr = nullptr, bool q_ready = false);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
                      const ts::Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,

@@ -144,7 +144,13 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   uint64_t* gs = maxL > 16384 ? ws->gsort.get<uint64_t>(2 * M) : nullptr;
   if (!items || !pos_of || !witems || !keys || (maxL > 16384 && !gs))
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
-  if (M > 0) ts_impl_bin_sort(K, tx, ty, so.md, w, starts, splat_off, maxL, keys, gs, items, pos_of, nonmono, st);
+  // the sort also writes each position's depth key into the pair-count scratch, which k_window
+  // reads (before k_item_counts overwrites it with the counts)
+  int32_t* pcnt = ws->pcnt.get<int32_t>(M);
+  if (!pcnt) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  if (M > 0)
+    ts_impl_bin_sort(K, tx, ty, so.md, w, starts, splat_off, maxL, keys, gs, items, pos_of, nonmono, st,
+                     reinterpret_cast<uint32_t*>(pcnt));
   else cudaMemsetAsync(nonmono, 0, T, st);
   BinsView bv{starts, splat_off, items, pos_of, nonmono, witems};
   // ---- colors of the visible splats ------------------------------------------------------
@@ -165,14 +171,14 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   ViewScratch scr;
   scr.widx = ws->widx.get<int32_t>(M);
   scr.wz = ws->wz.get<double>(M);
-  scr.cnt = ws->pcnt.get<int32_t>(M);
+  scr.cnt = pcnt;
   scr.scan = ws->pscan.get<int64_t>(compact_blocks(M));
   scr.torder = ws->torder.get<int32_t>(T);
   scr.rows = ws->rows.get<float>(24 * (M > 0 ? M : 1));  // kGr floats per list position
   if (!scr.widx || !scr.wz || !scr.cnt || !scr.scan || !scr.torder || !scr.rows)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0)
-    P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr);
+    P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr, true);
   uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(P));
   float4* prec = ws->pair_rec.get<float4>(P);
   if (!pbits || !prec) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
