@@ -1,7 +1,9 @@
-"""Reference-side binding: the reference's raster entry points —
-`render_forward` (raster.py:149) and `render_backward` (raster.py:206) — on the reference's
-own host objects (numpy SplatScene / TileBins / Camera / TetrahedralGrid / FieldState /
-RenderMaps), executed by the B200 kernels through the C ABI.
+"""Reference-side binding: the reference's hot-path entry points —
+`render_forward` (raster.py:149), `render_backward` (raster.py:206), `prefilter`
+(splat.py:66), `bin_and_sort` (raster.py:104), `eikonal_loss` / `normal_consistency_loss`
+(losses.py:25,39) and `marching_tetrahedra` (grid.py:136) — on the reference's own host
+objects (numpy SplatScene / TileBins / Camera / TetrahedralGrid / FieldState / RenderMaps),
+executed by the B200 kernels through the C ABI.
 
 Objects are duck-typed on the reference's field names, so `tetsplat.raster` can route its two
 calls here unchanged (tests/test_gpu_refbackend.py drives it with mirror types of the same layout).
@@ -18,9 +20,13 @@ import numpy as np
 from .camera import Camera
 from .field import FieldState
 from .grid import build_grid
+from .grid import marching_tetrahedra as _marching_tetrahedra
+from .losses import eikonal_loss as _eikonal_loss
+from .losses import normal_consistency_loss as _normal_consistency_loss
 from .raster import RenderMaps, bin_and_sort
 from .raster import render_backward as _render_backward
 from .raster import render_forward as _render_forward
+from .splat import prefilter as _prefilter
 from .splat import scene_from_arrays
 
 
@@ -63,9 +69,52 @@ def render_backward(saved: DeviceSaved, scene, grid, field, camera, d_maps, grad
         raise ValueError("render_backward needs the state render_forward(save_state=True) returned")
     del scene, camera  # the device copies in `saved` are the same scene and camera
     g = build_grid(int(grid.resolution))
-    fs = FieldState.from_numpy(field.sdf, field.deformation, float(field.deform_limit))
+    fs = _field(field)
     dm = RenderMaps(d_maps.normal, d_maps.depth, d_maps.opacity, getattr(d_maps, "color", None))
     gb = _render_backward(saved.saved, saved.scene, g, fs, saved.camera, dm)
+    return _grads(gb, grads_type)
+
+
+def _field(field) -> FieldState:
+    return FieldState.from_numpy(field.sdf, field.deformation, float(field.deform_limit))
+
+
+def _grads(gb, grads_type):
     d_sdf = gb.d_sdf.double().cpu().numpy()
     d_def = gb.d_deform.double().cpu().numpy()
     return grads_type(d_sdf, d_def) if grads_type is not None else (d_sdf, d_def)
+
+
+def prefilter(grid, field, s, threshold=1.0 / 255.0):
+    """splat.py:66-69: increasing int64 ids of the tets whose alpha_max reaches `threshold`."""
+    return _prefilter(build_grid(int(grid.resolution)), _field(field), float(s), threshold).cpu().numpy().astype(
+        np.int64)
+
+
+def bin_and_sort_arrays(scene, camera, tile_size=16):
+    """raster.py:104-141 on a host SplatScene: (tile_size, tiles_x, tiles_y, starts i64, items
+    i64) — the fields of the reference's TileBins, bit for bit."""
+    cam = _camera(camera)
+    sc = scene_from_arrays(scene.tet_ids, scene.vert_ids, scene.proj, scene.depths, scene.f, scene.normals,
+                           scene.mean_depth, scene.alpha_max, scene.bbox, scene.steepness, cam)
+    b = bin_and_sort(sc, cam, tile_size)
+    return (b.tile_size, b.tiles_x, b.tiles_y, b.starts.cpu().numpy(), b.items.cpu().numpy().astype(np.int64))
+
+
+def eikonal_loss(grid, field, tet_set, grads_type=None):
+    """losses.py:25-36: (loss, gradients)."""
+    loss, gb = _eikonal_loss(build_grid(int(grid.resolution)), _field(field), np.asarray(tet_set))
+    return loss, _grads(gb, grads_type)
+
+
+def normal_consistency_loss(grid, field, grads_type=None):
+    """losses.py:39-52: (loss, gradients)."""
+    loss, gb = _normal_consistency_loss(build_grid(int(grid.resolution)), _field(field))
+    return loss, _grads(gb, grads_type)
+
+
+def marching_tetrahedra(grid, field, mesh_type=None):
+    """grid.py:136-239: the welded mesh as `mesh_type(vertices, triangles)` (the caller's
+    TriangleMesh class) or a (vertices f64[V,3], triangles i64[F,3]) tuple — bit for bit."""
+    m = _marching_tetrahedra(build_grid(int(grid.resolution)), _field(field))
+    return mesh_type(m.vertices, m.triangles) if mesh_type is not None else (m.vertices, m.triangles)
