@@ -1098,7 +1098,6 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
   const bool inside = xi < W && yi < H;
   const int64_t lo = starts[tile];
-  const int L = (int)(starts[tile + 1] - lo);
   const int32_t* list = (nonmono[tile] ? witems : items) + lo;
   const int64_t p = inside ? (int64_t)yi * W + xi : 0;
   const int nproc = inside ? n_proc[p] : 0;
