@@ -46,15 +46,27 @@ def parse():
     p.add_argument("--resolution", type=int, default=R_GRID)
     p.add_argument("--image", type=int, default=IMG)
     p.add_argument("--s", type=float, default=STEEP)
+    p.add_argument("--views", type=int, default=VIEWS_PER_GPU,
+                   help="views per GPU (8: configs 3/4 — 64 views at 8 GPUs; 4 with --resolution 64 --image 512: config 2)")
     return p.parse_args()
 
 
+def config_name(args, world):
+    """BASELINE.json configs this run measures (configs[2] at 1 GPU, configs[3] = 64 views over
+    8 GPUs at 8 per GPU, configs[1] = 64^3 / 512^2 / 4 views)."""
+    if (args.resolution, args.image, args.views) == (128, 1024, 8):
+        return "config 3" if world == 1 else f"config 4 ({8 * world} views over {world} GPUs)"
+    if (args.resolution, args.image, args.views) == (64, 512, 4):
+        return "config 2"
+    return "custom"
+
+
 def config_dict(args, world):
-    return {"workload": f"config 3: {args.resolution}^3 Kuhn tet grid, {args.image}x{args.image}, s={args.s:g}, "
-                        f"{VIEWS_PER_GPU} orbit views per GPU (fwd+bwd + eikonal + normal consistency + "
+    return {"workload": f"{config_name(args, world)}: {args.resolution}^3 Kuhn tet grid, {args.image}x{args.image}, s={args.s:g}, "
+                        f"{args.views} orbit views per GPU (fwd+bwd + eikonal + normal consistency + "
                         f"allreduce + Adam)",
-            "grid": args.resolution, "image": args.image, "steepness": args.s, "views_per_gpu": VIEWS_PER_GPU,
-            "global_batch_views": VIEWS_PER_GPU * world, "field": "analytic sphere r=0.5 (synthetic)",
+            "grid": args.resolution, "image": args.image, "steepness": args.s, "views_per_gpu": args.views,
+            "global_batch_views": args.views * world, "field": "analytic sphere r=0.5 (synthetic)",
             "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"views sharded x{world}"}
 
 
@@ -109,12 +121,12 @@ def cpu_kind():
     return "reference" if O.default_backend() == "ref" else "port"
 
 
-def cpu_sample_desc(backend):
+def cpu_sample_desc(backend, views=VIEWS_PER_GPU):
     src = ("the reference's own Cython kernels (oracle/_ref, compiled from /root/reference kernels/_core.pyx) "
            "driven by the numpy restatement of raster.py/splat.py") if backend == "ref" else \
         "plain-C restatement of the reference kernels (oracle/liboracle.so, OpenMP) + numpy orchestration"
     return (f"1 view fwd+bwd of config 3 (build_scene, bin_and_sort, render_forward, render_backward incl. "
-            f"vertex chain) + per-batch prefilter/eikonal/normal-consistency amortised over {VIEWS_PER_GPU} "
+            f"vertex chain) + per-batch prefilter/eikonal/normal-consistency amortised over {views} "
             f"views; {src}")
 
 
@@ -127,23 +139,23 @@ def run_reference(args):
     os.environ.setdefault("TETSPLAT_THREADS", str(threads))
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     for _ in range(args.warmup):
-        cpu_reference_sample(args.resolution, args.image, args.s, VIEWS_PER_GPU * world, warm=True)
+        cpu_reference_sample(args.resolution, args.image, args.s, args.views * world, warm=True)
     per_view = []
     tb = None
     for k in range(args.steps):
-        r = cpu_reference_sample(args.resolution, args.image, args.s, VIEWS_PER_GPU * world, view_index=k)
+        r = cpu_reference_sample(args.resolution, args.image, args.s, args.views * world, view_index=k)
         per_view.append(r["t_view"])
         tb = r["t_batch"]
         backend = r["backend"]
     t_view = statistics.mean(per_view)
-    sec_per_view = t_view + tb / VIEWS_PER_GPU
+    sec_per_view = t_view + tb / args.views
     value = 1.0 / sec_per_view
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_view, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, world),
             "cpu_baseline": {"value": value, "unit": "views/s", "cores": int(os.environ["TETSPLAT_THREADS"]),
-                             "kind": "reference" if backend == "ref" else "port", "sample": cpu_sample_desc(backend),
+                             "kind": "reference" if backend == "ref" else "port", "sample": cpu_sample_desc(backend, args.views),
                              "t_view_s": t_view, "t_batch_s": tb},
             "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -240,7 +252,7 @@ def run_gpu(args):
 
     dev = torch.device("cuda", local)
     R, S, s = args.resolution, args.image, args.s
-    n_views = VIEWS_PER_GPU * world
+    n_views = args.views * world
     g = ts.build_grid(R)
     field = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)), device=dev)
     cams = [ts.orbit_camera(i, n_views, width=S, height=S) for i in range(n_views)]
@@ -543,12 +555,12 @@ def cpu_baseline(args, world):
     os.environ.setdefault("TETSPLAT_THREADS", str(threads))
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     try:
-        r = cpu_reference_sample(args.resolution, args.image, args.s, VIEWS_PER_GPU)
+        r = cpu_reference_sample(args.resolution, args.image, args.s, args.views)
     except Exception as e:  # the checker must never break the GPU line
         return {"value": None, "error": str(e)[:200]}
-    v = 1.0 / (r["t_view"] + r["t_batch"] / VIEWS_PER_GPU)
+    v = 1.0 / (r["t_view"] + r["t_batch"] / args.views)
     return {"value": v, "unit": "views/s", "cores": int(os.environ["TETSPLAT_THREADS"]),
-            "kind": "reference" if r["backend"] == "ref" else "port", "sample": cpu_sample_desc(r["backend"]),
+            "kind": "reference" if r["backend"] == "ref" else "port", "sample": cpu_sample_desc(r["backend"], args.views),
             "t_view_s": r["t_view"], "t_batch_s": r["t_batch"]}
 
 
