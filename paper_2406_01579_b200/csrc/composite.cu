@@ -1449,7 +1449,8 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   int32_t* const given_order = scr ? scr->torder : nullptr;
   float* rows = take_tmp(given_rows, kGr * (size_t)M, st);  // per-splat rows: K <= M
   int32_t* torder = take_tmp(given_order, T, st);
-  k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
+  // the fused view path's workspace still holds this view's order from its forward
+  if (!given_order) k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   const bool color = colors && maps[3] && dmaps[3] && d_color;
   cudaMemsetAsync(rows, 0, sizeof(float) * (color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
   if (color)
