@@ -4,7 +4,7 @@
 // splats whose (pixel, splat) PAIRS — the pixels of each splat's pixel rectangle inside the
 // tile (the reference's inclusive bbox test, _core.pyx:80, made exact at setup) — are
 // flattened into one index space of at most kCap pairs.  Every pair of the view has a
-// global index: item_off[list position] + local index in the rectangle (k_item_counts).
+// global index: item_off[list position] + local index in the rectangle (k_window_counts).
 //
 // Forward (forward_tiles, _core.pyx:98-229):
 //  A (pair-parallel, dense lanes): hit + opacity of every pair.  FP32 on sign-normalised
@@ -836,15 +836,45 @@ __device__ __forceinline__ uint32_t qkey(double md, double near_, double far_) {
   return (uint32_t)(unsigned long long)dmul(qq, 4294967295.0);  // raster.py:132-134
 }
 
-__global__ void __launch_bounds__(256) k_window(int T, const int64_t* __restrict__ starts,
-                                                const int32_t* __restrict__ items,
-                                                const uint8_t* __restrict__ nonmono, const double* __restrict__ md,
-                                                int n_w, double near_, double far_, int32_t* __restrict__ witems,
-                                                uint32_t* __restrict__ qpos, int32_t* __restrict__ widx_s,
-                                                double* __restrict__ wz_s, bool q_ready) {
+__device__ void window_tile(int t, int64_t lo, int64_t L, const int32_t* __restrict__ items,
+                            const double* __restrict__ md, int n_w, double near_, double far_,
+                            int32_t* __restrict__ witems, uint32_t* __restrict__ qpos, int32_t* __restrict__ widx_s,
+                            double* __restrict__ wz_s, bool q_ready);
+
+// One CTA per tile: the window (non-monotone tiles only), then the pairs per list position
+// (|pixel rectangle of the splat ∩ tile|, in the order the compositing kernels walk).
+// qpos aliases cnt: each tile's keys are read before its counts overwrite them.
+__global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const int64_t* __restrict__ starts,
+                                                       const int32_t* __restrict__ items,
+                                                       const uint8_t* __restrict__ nonmono,
+                                                       const double* __restrict__ md, int n_w, double near_,
+                                                       double far_, int32_t* __restrict__ witems,
+                                                       const SplatRec* __restrict__ recs, int32_t* __restrict__ cnt,
+                                                       int32_t* __restrict__ widx_s, double* __restrict__ wz_s,
+                                                       bool q_ready) {
   const int t = blockIdx.x;
-  if (t >= T || !nonmono[t]) return;
+  if (t >= T) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
+  const bool nm = nonmono[t];
+  if (nm) window_tile(t, lo, L, items, md, n_w, near_, far_, witems, reinterpret_cast<uint32_t*>(cnt), widx_s, wz_s,
+                      q_ready);
+  const int tx0 = (t % tiles_x) * TS_TILE, ty0 = (t / tiles_x) * TS_TILE;
+  const int32_t* list = nm ? witems : items;
+  for (int64_t p = lo + threadIdx.x; p < lo + L; p += blockDim.x) {
+    const int2 rr = *reinterpret_cast<const int2*>(recs + list[p]);
+    int x0, y0, nx, c = 0;
+    tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0, y0, nx,
+              c);
+    cnt[p] = c;
+  }
+}
+
+// the window of one non-monotone tile (all threads of the CTA; ends with a barrier)
+__device__ void window_tile(int t, int64_t lo, int64_t L, const int32_t* __restrict__ items,
+                            const double* __restrict__ md, int n_w, double near_, double far_,
+                            int32_t* __restrict__ witems, uint32_t* __restrict__ qpos, int32_t* __restrict__ widx_s,
+                            double* __restrict__ wz_s, bool q_ready) {
+  (void)t;
   // the tile's depth keys, once per position (q_ready: the sort already wrote them)
   if (!q_ready) {
     for (int64_t i = threadIdx.x; i < L; i += blockDim.x) qpos[lo + i] = qkey(md[items[lo + i]], near_, far_);
@@ -895,6 +925,7 @@ __global__ void __launch_bounds__(256) k_window(int T, const int64_t* __restrict
       --wcount;
     }
   }
+  __syncthreads();  // witems complete, the keys (aliasing the counts) consumed
 }
 
 // Launch order of the compositing CTAs: tiles by decreasing list length (16-entry buckets),
@@ -930,24 +961,6 @@ __global__ void __launch_bounds__(1024) k_tile_order(int T, const int64_t* __res
   for (int t = threadIdx.x; t < T; t += 1024) order[atomicAdd(&cnt[bucket(t)], 1)] = t;
 }
 
-// pairs per list position: |pixel rectangle of the splat  ∩  tile|
-__global__ void k_item_counts(int T, int tiles_x, const int64_t* __restrict__ starts,
-                              const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
-                              const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs,
-                              int32_t* __restrict__ cnt) {
-  const int t = blockIdx.x;
-  if (t >= T) return;
-  const int tx0 = (t % tiles_x) * TS_TILE, ty0 = (t / tiles_x) * TS_TILE;
-  const int64_t lo = starts[t], hi = starts[t + 1];
-  const int32_t* list = nonmono[t] ? witems : items;
-  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) {
-    const int2 rr = *reinterpret_cast<const int2*>(recs + list[p]);
-    int x0, y0, nx, c = 0;
-    tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0, y0, nx,
-              c);
-    cnt[p] = c;
-  }
-}
 
 // backward of one face hit (_core.pyx:295-341) accumulated into an item row (shared memory,
 // per-vertex slots: [0,4) d_f, [4,8) d_depth, [8,12) d_px, [12,16) d_py)
@@ -1388,10 +1401,8 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   double* wz = take_tmp(sc.wz, M, st);
   int32_t* cnt = take_tmp(sc.cnt, M, st);
   int64_t* scratch = take_tmp(sc.scan, compact_blocks(M), st);
-  uint32_t* qpos = reinterpret_cast<uint32_t*>(cnt);  // dead before k_item_counts writes cnt
-  k_window<<<T, 256, 0, st>>>(T, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, qpos, widx, wz,
-                              q_ready && sc.cnt);
-  k_item_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.witems, b.nonmono, rec, cnt);
+  k_window_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, rec,
+                                     cnt, widx, wz, q_ready && sc.cnt);
   scan_counts(cnt, M, item_off, scratch, st);
   int64_t total = 0;
   cudaMemcpyAsync(&total, item_off + M, sizeof(int64_t), cudaMemcpyDeviceToHost, st);

@@ -145,7 +145,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   if (!items || !pos_of || !witems || !keys || (maxL > 16384 && !gs))
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   // the sort also writes each position's depth key into the pair-count scratch, which k_window
-  // reads (before k_item_counts overwrites it with the counts)
+  // reads (each tile before k_window_counts overwrites it with the tile's pair counts)
   int32_t* pcnt = ws->pcnt.get<int32_t>(M);
   if (!pcnt) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (M > 0)
