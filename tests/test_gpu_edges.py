@@ -86,7 +86,9 @@ def test_far_plane_culls_everything(ts):
     m2 = vr.forward(g, fs, cam, STEEP, active)
     assert vr.counts[0] == 0 and vr.counts[1] == 0
     assert float(m2.opacity.abs().max()) == 0.0
-    gb2 = vr.backward(fs, ts.RenderMaps(w.normal, w.depth, w.opacity), ts.GradientBuffers.zeros(g.num_vertices))
+    dmd = ts.RenderMaps(*(torch.as_tensor(x, dtype=torch.float32, device="cuda").contiguous()
+                          for x in (w.normal, w.depth, w.opacity)))
+    gb2 = vr.backward(fs, dmd, ts.GradientBuffers.zeros(g.num_vertices))
     assert float(gb2.d_vert.abs().max()) == 0.0
 
 
