@@ -95,7 +95,10 @@ def main():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         tj = {k: {"dram_bytes_per_launch": sum(v) / len(v) * scale, "launches_captured": len(v),
                   "source": os.path.basename(a.report)} for k, v in traffic.items()}
-        json.dump(tj, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        merged = json.load(open(tp)) if os.path.exists(tp) else {}
+        merged.update(tj)  # keep the other kernels' captures
+        json.dump(merged, open(tp, "w"), indent=1)
     open(a.out, "w").write("\n\n".join(text) + "\n")
     print(open(a.out).read()[:3000])
 
