@@ -2,7 +2,8 @@
  * tetsplat_b200.h — C ABI of the B200-native TeT-Splatting rasterizer (sm_100a).
  *
  * The drop-in boundary for the reference's kernel plugin (tetsplat.kernels.get_backend(),
- * /root/reference/pkg/src/tetsplat/kernels/__init__.py:91-102) and the per-view
+ * pkg/src/tetsplat/kernels/__init__.py:35-36; the module paper_2406_01579_b200.kernels binds
+ * its five functions) and the per-view
  * orchestration around it (splat.py, raster.py, losses.py, grid.py).  Every pointer
  * argument is a DEVICE pointer unless noted; `stream` is a cudaStream_t (NULL = legacy
  * default stream).  All entry points return 0 on success and a negative TS_E* code on
@@ -121,11 +122,37 @@ int ts_render_backward(const ts_scene* scene, int64_t K, const float* colors, co
                        const int32_t* n_proc, const double* deform, int32_t resolution, float* d_vert,
                        float* d_color, void* stream);
 
+/* ---- kernel plugin contract (tetsplat.kernels.get_backend(), kernels/__init__.py:35-36) ----
+ * Window flags of caller-given tile lists (forward_tiles receives the lists, _core.pyx:98-107):
+ * flags[t] = 0 mean depth non-decreasing, 1 sorted by the 32-bit depth key but not by mean
+ * depth, 2 not sorted by depth key (the window is replayed over the whole list).  near < far. */
+int ts_bins_from_lists(const int64_t* starts, const int32_t* items, int32_t n_tiles, const double* mean_depth,
+                       double near_, double far_, uint8_t* flags, void* stream);
+
+/* SavedState.records (_core.pyx:206-209): for each of n_tiles tiles, per pixel (row major in
+ * the 16x16 tile) the blended splat indices idx[] and clipped alphas alpha[] in blend order,
+ * written from rec_off[i * 256 + pixel] (exclusive scan of the forward's n_blend in that
+ * order).  Inputs are a ts_render_forward's bins / pair records / n_proc. */
+int ts_saved_records(const ts_scene* scene, const ts_bins* bins, const ts_camera* cam, const int64_t* item_off,
+                     const uint32_t* pair_bits, const void* pair_rec, const int32_t* n_proc, const int32_t* tiles,
+                     int32_t n_tiles, const int64_t* rec_off, int64_t* idx, double* alpha, void* stream);
+
+/* backward_tiles (_core.pyx:344-471) for n_tiles tiles of a ts_render_forward: the per-splat
+ * gradients are ADDED to rows f32[K, 20] (24 with colours): [0,4) d_f, [4,8) d_depths,
+ * [8,12) d_proj x, [12,16) d_proj y (per tet vertex), [16,19) d_normals, 19 d_mean_depth,
+ * [20,23) d_colors.  No vertex chain (splat_grads_to_vertices stays with the caller). */
+int ts_backward_tiles(const ts_scene* scene, int64_t K, const float* colors, const ts_bins* bins, int64_t M,
+                      const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits, const void* pair_rec,
+                      const float* const maps[4], const float* const d_maps[4], const int32_t* n_proc,
+                      const int32_t* tiles, int32_t n_tiles, float* rows, void* stream);
+
 /* Fused per-view pipeline over a persistent, grow-only device workspace (one view in flight
  * per workspace).  ts_view_forward = build_scene + bin_and_sort + window + render_forward;
  * out_counts = {K visible splats, M tile pairs, P pixel pairs} (host).  [sync]
  * ts_view_backward = render_backward of the workspace's last forward, accumulated into d_vert
- * (and d_color when the forward had colors_tet f32[6R^3,3]). */
+ * (and d_color when the forward had colors_tet f32[6R^3,3]).  status (nullable, device f32):
+ * incremented when a map gradient is non-finite (raster.py:209-211 raises ValueError; here the
+ * caller raises at its next sync, and ts_adam_step skips the update). */
 typedef struct ts_workspace ts_workspace;
 ts_workspace* ts_workspace_create(void);
 void ts_workspace_destroy(ts_workspace* ws);
@@ -134,7 +161,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
                     double t_stop, const float* colors_tet, float* normal_map, float* depth_map, float* opacity_map,
                     float* color_map, int64_t* out_counts, void* stream);
 int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4],
-                     const float* const d_maps[4], float* d_vert, float* d_color, void* stream);
+                     const float* const d_maps[4], float* d_vert, float* d_color, float* status, void* stream);
 const int32_t* ts_view_n_blend(ts_workspace* ws);
 
 /* K8 eikonal_loss (losses.py:25-36): loss (device f64[1], overwritten) and
@@ -188,10 +215,14 @@ int ts_rasterize_mesh(const double* vertices, int64_t V, const int64_t* triangle
 
 /* Adam step of the fit loop (fit.py:70-90) from the interleaved gradient buffer d_vert f32[N,4]:
  * FP64 moments m_sdf, v_sdf [N] and m_def, v_def [N,3], step t >= 1 (bias corrections
- * 1 - beta^t), deformation clamped to +-deform_limit (field.py:40-42) afterwards. */
+ * 1 - beta^t), deformation clamped to +-deform_limit (field.py:40-42) afterwards.
+ * status (nullable, device f32[2+]): the non-finite entries of d_vert are counted into
+ * status[1] first; when status[0] (non-finite map gradients, ts_view_backward) or status[1] is
+ * non-zero the parameters and moments are left untouched (fit.py:209-212 checks before
+ * opt.step) and the caller raises at its next sync. */
 int ts_adam_step(int32_t resolution, const float* d_vert, double* sdf, double* deform, double* m_sdf,
                  double* v_sdf, double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1,
-                 double beta2, int64_t t, double eps, double deform_limit, void* stream);
+                 double beta2, int64_t t, double eps, double deform_limit, float* status, void* stream);
 
 /* Diagnostics (since the last reset): out8[0] = (pixel, splat) pairs re-decided in FP64 at
  * a face edge or a degenerate face, out8[1] = pairs re-decided in FP64 at an alpha

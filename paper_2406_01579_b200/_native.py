@@ -60,11 +60,15 @@ def lib():
         "ts_render_forward": ([ps, I64, P, pb, I64, pc, D, D, P, I64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
         "ts_render_backward": ([ps, I64, P, pb, I64, pc, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, I32,
                                 P, P, P], ctypes.c_int),
+        "ts_bins_from_lists": ([P, P, I32, P, D, D, P, P], ctypes.c_int),
+        "ts_saved_records": ([ps, pb, pc, P, P, P, P, P, I32, P, P, P, P], ctypes.c_int),
+        "ts_backward_tiles": ([ps, I64, P, pb, I64, pc, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, I32, P,
+                               P], ctypes.c_int),
         "ts_eikonal": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency": ([P, P, I32, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency_scratch_bytes": ([I32], ctypes.c_int64),
         "ts_normal_consistency_ws": ([P, P, I32, D, P, P, P, P], ctypes.c_int),
-        "ts_adam_step": ([I32, P, P, P, P, P, P, P, D, D, D, D, I64, D, D, P], ctypes.c_int),
+        "ts_adam_step": ([I32, P, P, P, P, P, P, P, D, D, D, D, I64, D, D, P, P], ctypes.c_int),
         "ts_rasterize_mesh": ([P, I64, P, I64, pc, P, P, P, P], ctypes.c_int),
         "ts_marching_tets_count": ([P, P, I32, PI64, PI64, P], ctypes.c_int),
         "ts_marching_tets": ([P, P, I32, P, P, ctypes.POINTER(ctypes.c_int64), P], ctypes.c_int),
@@ -78,7 +82,7 @@ def lib():
         "ts_workspace_destroy": ([P], None),
         "ts_view_forward": ([P, P, P, I32, pc, D, P, I64, I32, D, P, P, P, P, P, ctypes.POINTER(ctypes.c_int64), P],
                             ctypes.c_int),
-        "ts_view_backward": ([P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, P], ctypes.c_int),
+        "ts_view_backward": ([P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, P, P], ctypes.c_int),
         "ts_view_n_blend": ([P], P),
         "ts_debug_tile_times": ([ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int],
                                 ctypes.c_int),

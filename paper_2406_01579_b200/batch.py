@@ -48,7 +48,10 @@ def default_inflight() -> int:
     except AttributeError:
         cpus = os.cpu_count() or 1
     per_rank = cpus // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
-    return max(1, min(4, per_rank - 1))
+    # at least two lanes even when 8 ranks share 16 host CPUs: a lane's host thread spends
+    # its time blocked on its stream's sizing syncs, so two fit on one core (1 -> 2 lanes
+    # was +24% on one GPU)
+    return max(2, min(4, per_rank - 1))
 
 
 class Adam:
@@ -74,16 +77,18 @@ class Adam:
             p.addcdiv_(m / c1, (v / c2).sqrt_().add_(self.eps), value=-lr)
 
     @torch.no_grad()
-    def step_field(self, field, grads: GradientBuffers, resolution: int, stream=None):
+    def step_field(self, field, grads: GradientBuffers, resolution: int, stream=None, status=None):
         """The same update for (sdf, deformation) in one fused kernel straight from the
-        interleaved gradient buffer, deformation clamped to its limit (ts_adam_step)."""
+        interleaved gradient buffer, deformation clamped to its limit (ts_adam_step).
+        With `status` (device f32[2+], see FitStep) the update is skipped on the device when
+        a map gradient or a gradient entry is non-finite."""
         from . import _native
         self.t += 1
         _native.check(_native.lib().ts_adam_step(
             int(resolution), _native.ptr(grads.d_vert), _native.ptr(field.sdf), _native.ptr(field.deformation),
             _native.ptr(self.m[0]), _native.ptr(self.v[0]), _native.ptr(self.m[1]), _native.ptr(self.v[1]),
             float(self.lrs[0]), float(self.lrs[1]), float(self.b1), float(self.b2), int(self.t), float(self.eps),
-            float(field.deform_limit), _native.stream_ptr(stream)))
+            float(field.deform_limit), _native.ptr(status), _native.stream_ptr(stream)))
 
 
 @dataclass
@@ -116,7 +121,13 @@ class FitStep:
         self.cfg = cfg or StepConfig()
         self.group = group
         dev = field.sdf.device
-        self.grads = GradientBuffers.zeros(grid.num_vertices, dev)
+        # one flat FP32 buffer: the [N,4] vertex gradients plus a 4-float status tail
+        # ([0] non-finite map gradients, [1] non-finite gradient entries), so the single
+        # all-reduce carries the failure flags too and every rank skips the same update
+        N = grid.num_vertices
+        self._flat = torch.zeros(4 * N + 4, dtype=torch.float32, device=dev)
+        self.grads = GradientBuffers(self._flat[:4 * N].view(N, 4))
+        self.status = self._flat[4 * N:]
         self.eik_loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.nc_loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.opt = Adam([field.sdf, field.deformation], [self.cfg.lr_sdf, self.cfg.lr_deform], self.cfg.betas) \
@@ -134,11 +145,14 @@ class FitStep:
         self.last_active = 0
         self._pool = ThreadPoolExecutor(max_workers=n) if n > 1 else None
 
-    def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None, inputs_ready=None):
+    def __call__(self, s: float, views, d_maps_fn, stats: StepStats | None = None, inputs_ready=None,
+                 update: bool | None = None):
         """`inputs_ready`: optional CUDA event after which the deformation is valid (the SDF
-        must be valid on the current stream); everything but the prefilter waits for it."""
+        must be valid on the current stream); everything but the prefilter waits for it.
+        `update`: run the Adam step at the end (default: when the config has an optimizer);
+        `fit_field` passes False and calls `apply_update` after its host-side checks."""
         g, f, cfg = self.grid, self.field, self.cfg
-        self.grads.d_vert.zero_()
+        self._flat.zero_()
         active = prefilter(g, f, s)
         if active.numel() == 0:
             raise EmptySceneError("pre-filtering removed every tetrahedron")
@@ -182,7 +196,7 @@ class FitStep:
                     K, M, _ = r.counts
                     if K == 0:
                         continue
-                    r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st)
+                    r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st, status=self.status)
                     done.append((K, M))
             return done
 
@@ -201,7 +215,26 @@ class FitStep:
             main.wait_stream(st)
         if inputs_ready is not None:
             main.wait_event(inputs_ready)
-        allreduce_gradients(self.grads, self.group)
-        if self.opt is not None:
-            self.opt.step_field(f, self.grads, g.resolution)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(self._flat, op=dist.ReduceOp.SUM, group=self.group)
+        if update is None:
+            update = self.opt is not None
+        if update:
+            self.apply_update()
         return self.grads
+
+    def apply_update(self):
+        """Adam + clamp on the device from the (all-reduced) gradient buffer; skipped on the
+        device when the status flags a non-finite value (see check_status)."""
+        if self.opt is None:
+            raise RuntimeError("FitStep was built without an optimizer")
+        self.opt.step_field(self.field, self.grads, self.grid.resolution, status=self.status)
+
+    def check_status(self):
+        """Host sync: raise like the reference when the last step saw non-finite values —
+        ValueError for map gradients (raster.py:209-211), RuntimeError for gradients."""
+        bad_maps, bad_grad = (float(v) for v in self.status[:2].tolist())
+        if bad_maps:
+            raise ValueError("non-finite incoming map gradients")
+        if bad_grad:
+            raise RuntimeError("non-finite parameter gradients")

@@ -205,7 +205,7 @@ int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const 
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   keep_pool_warm();
   ts_impl_forward(tx, ty, bv_of(b), reinterpret_cast<const SplatRec*>(sc->records), colors, s64_of(sc), cam->width,
-                  cam->height, s, (float)t_stop, item_off, n_pairs, pair_bits, reinterpret_cast<float4*>(pair_rec),
+                  cam->height, s, t_stop, item_off, n_pairs, pair_bits, reinterpret_cast<float4*>(pair_rec),
                   nmap, dmap, omap, cmap, n_proc, n_blend, ST(stream));
   return check_cuda("ts_render_forward");
 }
@@ -230,6 +230,49 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
   return check_cuda("ts_render_backward");
 }
 
+int ts_bins_from_lists(const int64_t* starts, const int32_t* items, int32_t T, const double* md, double near_,
+                       double far_, uint8_t* flags, void* stream) {
+  if (!starts || !flags || T < 0 || !(far_ > near_) || (T > 0 && (!items || !md)))
+    return fail(TS_EINVAL, "ts_bins_from_lists: bad arguments");
+  ts_impl_list_flags(T, starts, items, md, near_, far_, flags, ST(stream));
+  return check_cuda("ts_bins_from_lists");
+}
+
+int ts_saved_records(const ts_scene* sc, const ts_bins* b, const ts_camera* cam, const int64_t* item_off,
+                     const uint32_t* pair_bits, const void* pair_rec, const int32_t* n_proc, const int32_t* tiles,
+                     int32_t n_tiles, const int64_t* rec_off, int64_t* idx, double* alpha, void* stream) {
+  if (!sc || !b || !cam || !n_proc || n_tiles < 0 || (n_tiles > 0 && (!tiles || !rec_off || !item_off ||
+                                                                       !pair_bits || !pair_rec)))
+    return fail(TS_EINVAL, "ts_saved_records: bad arguments");
+  int tx, ty;
+  if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  ts_impl_saved_records(tiles, n_tiles, tx, cam->width, cam->height, bv_of(b),
+                        reinterpret_cast<const SplatRec*>(sc->records), item_off, pair_bits,
+                        reinterpret_cast<const float4*>(pair_rec), n_proc, rec_off, idx, alpha, ST(stream));
+  return check_cuda("ts_saved_records");
+}
+
+int ts_backward_tiles(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
+                      const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits, const void* pair_rec,
+                      const float* const maps[4], const float* const dmaps[4], const int32_t* n_proc,
+                      const int32_t* tiles, int32_t n_tiles, float* rows, void* stream) {
+  if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !rows || K < 0 || M < 0 || n_tiles < 0 ||
+      (n_tiles > 0 && !tiles) || (M > 0 && (!item_off || !pair_bits)))
+    return fail(TS_EINVAL, "ts_backward_tiles: bad arguments");
+  for (int i = 0; i < 3; ++i)
+    if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_backward_tiles: missing map");
+  int tx, ty;
+  if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  keep_pool_warm();
+  const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
+  const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
+  ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, sc->f,
+                   sc->vert_ids, sc->tet_ids, nullptr, 1, to_cam(cam), item_off, pair_bits,
+                   reinterpret_cast<const float4*>(pair_rec), m4, d4, n_proc, nullptr, nullptr, ST(stream), nullptr,
+                   nullptr, tiles, n_tiles, rows);
+  return check_cuda("ts_backward_tiles");
+}
+
 int ts_eikonal(const double* sdf, const double* deform, int32_t R, const int32_t* tet_set, int64_t n, double scale,
                float* d_vert, double* loss, void* stream) {
   if (!sdf || !deform || !d_vert || !loss || R < 1 || n < 0 || (n > 0 && !tet_set))
@@ -248,12 +291,12 @@ int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, do
 
 int ts_adam_step(int32_t R, const float* d_vert, double* sdf, double* deform, double* m_sdf, double* v_sdf,
                  double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1, double beta2, int64_t t,
-                 double eps, double deform_limit, void* stream) {
+                 double eps, double deform_limit, float* status, void* stream) {
   if (!d_vert || !sdf || !deform || !m_sdf || !v_sdf || !m_def || !v_def || R < 1 || t < 1)
     return fail(TS_EINVAL, "ts_adam_step: bad arguments");
   const int64_t n = (int64_t)R + 1;
   ts_impl_adam(n * n * n, d_vert, sdf, deform, m_sdf, v_sdf, m_def, v_def, lr_sdf, lr_def, beta1, beta2, t, eps,
-               deform_limit, ST(stream));
+               deform_limit, ST(stream), status);
   return check_cuda("ts_adam_step");
 }
 

@@ -494,11 +494,14 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
       // where they can; digit passes over the splat index: ceil(bits(K - 1) / 8)
       const int cap = maxL <= 4096 ? 4096 : (maxL <= 8192 ? 8192 : 16384);
       const size_t smem = sizeof(uint32_t) * (2 * (size_t)cap + kRadixWarps * 256 + 256);
-      static size_t attr = 0;
-      if (smem > attr) {
-        cudaFuncSetAttribute(k_tile_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-      }
+      // the attribute is set once, to the 16384-entry cap (a thread-safe static: views in
+      // flight launch from several host threads); the launch asks for what it needs
+      static const bool attr = [] {
+        const size_t mx = sizeof(uint32_t) * (2 * (size_t)16384 + kRadixWarps * 256 + 256);
+        cudaFuncSetAttribute(k_tile_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+        return true;
+      }();
+      (void)attr;
       const int per_sm = smem <= 110 * 1024 ? 2 : 1;
       k_tile_sort_long<<<148 * per_sm, kRadixThreads, smem, st>>>(w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br,
                                                                  splat_off, md, items, pos_of, nonmono, cap,

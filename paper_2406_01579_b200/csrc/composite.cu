@@ -43,6 +43,7 @@ namespace ts {
 
 constexpr float kAlphaClipF = 0.9999f;  // splat.py:14
 constexpr float kOneMinusClipF = 1e-4f;
+constexpr double kAlphaClipD = 1.0 - 1e-4;  // ALPHA_CLIP in FP64
 constexpr int kCh = 64;      // max splats per chunk (one bit each in the per-pixel masks)
 constexpr int kCap = 2048;   // max (pixel, splat) pairs per chunk
 typedef unsigned long long ChunkMask;
@@ -655,7 +656,8 @@ template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
-    Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, const int64_t* __restrict__ item_off,
+    Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, bool clip_stops,
+    const int64_t* __restrict__ item_off,
     uint32_t* __restrict__ pair_bits, float4* __restrict__ pair_rec, float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
     float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -787,7 +789,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
         acc.add(__fmul_rn(T, c.x), F.sh[j], COLOR ? F.col[j] : nullptr);
         T = __fmul_rn(T, fabsf(c.y));
         ++nb;
-        if (T < t_stop) {
+        // a clipped blend leaves T * (1 - ALPHA_CLIP) < T_STOP in the FP64 reference whenever
+        // 1 - ALPHA_CLIP < t_stop (T <= 1), which FP32 T = 1e-4f would not see at T = 1
+        if (T < t_stop || (c.y < 0.f && clip_stops)) {
           done = true;
           nproc = base + j + 1;
           break;
@@ -841,6 +845,90 @@ __device__ void window_tile(int t, int64_t lo, int64_t L, const int32_t* __restr
                             int32_t* __restrict__ witems, uint32_t* __restrict__ qpos, int32_t* __restrict__ widx_s,
                             double* __restrict__ wz_s, bool q_ready);
 
+// The reference's window (_core.pyx:171-187) replayed over a whole list by one thread (lists
+// handed in by a caller that are not sorted by depth key; ts_bins_from_lists flags them 2).
+__device__ void window_whole(int64_t lo, int64_t L, const int32_t* __restrict__ items, const double* __restrict__ md,
+                             int n_w, int32_t* __restrict__ witems, int32_t* __restrict__ widx_s,
+                             double* __restrict__ wz_s) {
+  if (threadIdx.x == 0) {
+    int32_t* widx = widx_s + lo;
+    double* wz = wz_s + lo;
+    int64_t wcount = 0, pos = 0, out = 0;
+    for (;;) {
+      while (wcount < n_w && pos < L) {
+        const int32_t k = items[lo + pos++];
+        widx[wcount] = k;
+        wz[wcount++] = md[k];
+      }
+      if (wcount == 0) break;
+      int64_t m = 0;
+      for (int64_t k = 1; k < wcount; ++k)
+        if (wz[k] < wz[m]) m = k;
+      witems[lo + out++] = widx[m];
+      for (int64_t k = m; k < wcount - 1; ++k) {
+        widx[k] = widx[k + 1];
+        wz[k] = wz[k + 1];
+      }
+      --wcount;
+    }
+  }
+  __syncthreads();
+}
+
+// Window flags of caller-given tile lists: 0 = mean depth non-decreasing (the window is the
+// identity), 1 = sorted by the 32-bit depth key but not by mean depth (runs replayed by
+// window_tile), 2 = not sorted by depth key (the whole list replayed).  One warp per tile.
+__global__ void k_list_flags(int T, const int64_t* __restrict__ starts, const int32_t* __restrict__ items,
+                             const double* __restrict__ md, double near_, double far_, uint8_t* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int64_t lo = starts[t], hi = starts[t + 1];
+  bool dec = false, qdec = false;
+  for (int64_t i = lo + 1 + lane; i < hi; i += 32) {
+    const double a = md[items[i - 1]], b = md[items[i]];
+    dec |= b < a;
+    qdec |= qkey(b, near_, far_) < qkey(a, near_, far_);
+  }
+  dec = __any_sync(0xffffffffu, dec);
+  qdec = __any_sync(0xffffffffu, qdec);
+  if (lane == 0) flags[t] = qdec ? 2 : (dec ? 1 : 0);
+}
+
+// SavedState.records of the reference (_core.pyx:206-209, raster.py:94-101) materialised from
+// the pair records: per requested tile (CTA) and pixel (thread), the blended splats in blend
+// order with their clipped alpha, at rec_off[tile index * 256 + pixel].
+__global__ void __launch_bounds__(TS_TILE_PX) k_saved_records(
+    const int32_t* __restrict__ tiles, int tiles_x, int W, int H, const int64_t* __restrict__ starts,
+    const int32_t* __restrict__ items, const int32_t* __restrict__ witems, const uint8_t* __restrict__ nonmono,
+    const SplatRec* __restrict__ recs, const int64_t* __restrict__ item_off, const uint32_t* __restrict__ pair_bits,
+    const float4* __restrict__ pair_rec, const int32_t* __restrict__ n_proc, const int64_t* __restrict__ rec_off,
+    int64_t* __restrict__ idx_out, double* __restrict__ alpha_out) {
+  const int tile = tiles[blockIdx.x];
+  const int tx0 = (tile % tiles_x) * TS_TILE, ty0 = (tile / tiles_x) * TS_TILE;
+  const int xi = tx0 + (threadIdx.x & (TS_TILE - 1)), yi = ty0 + (threadIdx.x / TS_TILE);
+  if (xi >= W || yi >= H) return;
+  const int64_t lo = starts[tile];
+  const int32_t* list = (nonmono[tile] ? witems : items) + lo;
+  const int np = n_proc[(int64_t)yi * W + xi];
+  int64_t o = rec_off[(int64_t)blockIdx.x * TS_TILE_PX + threadIdx.x];
+  for (int j = 0; j < np; ++j) {
+    const int k = list[j];
+    const int2 rr = *reinterpret_cast<const int2*>(recs + k);
+    int x0, y0, nx, c;
+    if (!tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0,
+                   y0, nx, c))
+      continue;
+    if (xi < x0 || xi >= x0 + nx || yi < y0 || yi >= y0 + c / nx) continue;
+    const int64_t g = item_off[lo + j] + (int64_t)(yi - y0) * nx + (xi - x0);
+    if (!pair_bit(pair_bits, g)) continue;
+    const float4 r = pair_rec[g];
+    idx_out[o] = k;
+    alpha_out[o] = r.y < 0.f ? kAlphaClipD : (double)fmaxf(r.x, 0.f);
+    ++o;
+  }
+}
+
 // One CTA per tile: the window (non-monotone tiles only), then the pairs per list position
 // (|pixel rectangle of the splat ∩ tile|, in the order the compositing kernels walk).
 // qpos aliases cnt: each tile's keys are read before its counts overwrite them.
@@ -855,9 +943,13 @@ __global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const
   const int t = blockIdx.x;
   if (t >= T) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
-  const bool nm = nonmono[t];
-  if (nm) window_tile(t, lo, L, items, md, n_w, near_, far_, witems, reinterpret_cast<uint32_t*>(cnt), widx_s, wz_s,
-                      q_ready);
+  const uint8_t flag = nonmono[t];
+  const bool nm = flag != 0;
+  if (flag == 2)  // a caller-given list not sorted by depth key: the window over the whole list
+    window_whole(lo, L, items, md, n_w, witems, widx_s, wz_s);
+  else if (nm)
+    window_tile(t, lo, L, items, md, n_w, near_, far_, witems, reinterpret_cast<uint32_t*>(cnt), widx_s, wz_s,
+                q_ready);
   const int tx0 = (t % tiles_x) * TS_TILE, ty0 = (t / tiles_x) * TS_TILE;
   const int32_t* list = nm ? witems : items;
   for (int64_t p = lo + threadIdx.x; p < lo + L; p += blockDim.x) {
@@ -1097,7 +1189,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const float4* __restrict__ pair_rec, const float* __restrict__ normal_map,
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
-    const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows) {
+    const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows,
+    float* __restrict__ status) {
   using SM = BwdSmem<COLOR>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& S = *reinterpret_cast<SM*>(smem_raw);
@@ -1133,6 +1226,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         C_c[i] = color_map[p * 3 + i];
       }
     }
+  }
+  if (status) {  // raster.py:209-211: non-finite incoming map gradients, raised by the caller
+    bool bad = !isfinite(g_o) || !isfinite(g_d) || !isfinite(g_n[0]) || !isfinite(g_n[1]) || !isfinite(g_n[2]);
+    if (COLOR) bad |= !isfinite(g_c[0]) || !isfinite(g_c[1]) || !isfinite(g_c[2]);
+    if (__ballot_sync(0xffffffffu, bad) && lane == 0) atomicAdd(status, 1.0f);
   }
   __syncthreads();
   const int maxproc = S.maxproc;
@@ -1415,28 +1513,29 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
 }
 
 void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec* rec, const float* colors,
-                     const Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
+                     const Scene64& S64, int W, int H, double s, double t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st, const ViewScratch* scr) {
   const int T = tiles_x * tiles_y;
   int32_t* const given_order = scr ? scr->torder : nullptr;
   cudaMemsetAsync(pair_bits, 0, sizeof(uint32_t) * (size_t)TS_PAIR_BIT_WORDS(n_pairs), st);
-  static bool attr = false;
   const int smem = (int)sizeof(FwdSmem);
-  if (!attr) {
+  static const bool attr = [smem] {  // once (thread-safe static: lanes launch from several threads)
     cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   int32_t* torder = take_tmp(given_order, T, st);
   k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
+  const bool clip_stops = (1.0 - kAlphaClipD) < t_stop;  // splat.py:14-15: T (1 - ALPHA_CLIP) < T_STOP
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
-                                                W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
+                                                W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
                                                 nmap, dmap, omap, cmap, n_proc, n_blend);
   else
     k_forward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
-                                                 tiles_x, W, H, (float)s, s, t_stop, item_off, pair_bits, pair_rec,
+                                                 tiles_x, W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
                                                  nmap, dmap, omap, nullptr, n_proc, n_blend);
   put_tmp(torder, given_order, st);
 }
@@ -1446,34 +1545,44 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
                       const double* deform, int R, const Camera& cam, const int64_t* item_off,
                       const uint32_t* pair_bits, const float4* pair_rec, const float* maps[4],
                       const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
-                      const ViewScratch* scr) {
+                      const ViewScratch* scr, float* status, const int32_t* tiles, int n_tiles,
+                      float* rows_out) {
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
-  static bool attr = false;
   const int smem_c = (int)sizeof(BwdSmem<true>), smem = (int)sizeof(BwdSmem<false>);
-  if (!attr) {
+  static const bool attr = [smem_c, smem] {  // once (thread-safe static)
     cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
     cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  float* const given_rows = scr ? scr->rows : nullptr;
-  int32_t* const given_order = scr ? scr->torder : nullptr;
+    return true;
+  }();
+  (void)attr;
+  // rows_out: the plugin contract's per-splat gradients (backward_tiles, _core.pyx:344-471) —
+  // the rows of the requested tiles are ADDED to rows_out and the vertex chain is not run
+  float* const given_rows = rows_out ? rows_out : (scr ? scr->rows : nullptr);
+  int32_t* const given_order = tiles ? const_cast<int32_t*>(tiles) : (scr ? scr->torder : nullptr);
+  const int nblk = tiles ? n_tiles : T;
+  if (nblk <= 0) return;
   float* rows = take_tmp(given_rows, kGr * (size_t)M, st);  // per-splat rows: K <= M
   int32_t* torder = take_tmp(given_order, T, st);
   // the fused view path's workspace still holds this view's order from its forward
   if (!given_order) k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
-  const bool color = colors && maps[3] && dmaps[3] && d_color;
-  cudaMemsetAsync(rows, 0, sizeof(float) * (color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
+  const bool color = colors && maps[3] && dmaps[3] && (d_color || rows_out);
+  if (!rows_out)
+    cudaMemsetAsync(rows, 0, sizeof(float) * (color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
   if (color)
-    k_backward<true><<<T, TS_TILE_PX, smem_c, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
+    k_backward<true><<<nblk, TS_TILE_PX, smem_c, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                  maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
-                                                 dmaps[3], n_proc, rows);
+                                                 dmaps[3], n_proc, rows, status);
   else
-    k_backward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
+    k_backward<false><<<nblk, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
                                                   cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                   maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
-                                                  nullptr, n_proc, rows);
+                                                  nullptr, n_proc, rows, status);
+  if (rows_out) {
+    put_tmp(torder, given_order, st);
+    return;
+  }
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (color)
@@ -1484,6 +1593,21 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
                                            make_grid(R), cam, d_vert, nullptr);
   put_tmp(rows, given_rows, st);
   put_tmp(torder, given_order, st);
+}
+
+void ts_impl_list_flags(int T, const int64_t* starts, const int32_t* items, const double* md, double near_,
+                        double far_, uint8_t* flags, cudaStream_t st) {
+  if (T <= 0) return;
+  k_list_flags<<<(T + 7) / 8, 256, 0, st>>>(T, starts, items, md, near_, far_, flags);
+}
+
+void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W, int H, const BinsView& b,
+                           const SplatRec* rec, const int64_t* item_off, const uint32_t* pair_bits,
+                           const float4* pair_rec, const int32_t* n_proc, const int64_t* rec_off, int64_t* idx,
+                           double* alpha, cudaStream_t st) {
+  if (n_tiles <= 0) return;
+  k_saved_records<<<n_tiles, TS_TILE_PX, 0, st>>>(tiles, tiles_x, W, H, b.starts, b.items, b.witems, b.nonmono, rec,
+                                                  item_off, pair_bits, pair_rec, n_proc, rec_off, idx, alpha);
 }
 
 void ts_impl_counters(unsigned long long out[8], int reset) {

@@ -73,7 +73,7 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b,
                                 int n_w, double near_, double far_, const ts::SplatRec* rec, int64_t* item_off,
                                 cudaStream_t st, const ts::ViewScratch* scr = nullptr, bool q_ready = false);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
-                     const ts::Scene64& S64, int W, int H, double s, float t_stop, const int64_t* item_off,
+                     const ts::Scene64& S64, int W, int H, double s, double t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st,
                      const ts::ViewScratch* scr = nullptr);
@@ -83,7 +83,14 @@ void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M
                       const int64_t* item_off, const uint32_t* pair_bits, const float4* pair_rec,
                       const float* maps[4], const float* dmaps[4],
                       const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
-                      const ts::ViewScratch* scr = nullptr);
+                      const ts::ViewScratch* scr = nullptr, float* status = nullptr,
+                      const int32_t* tiles = nullptr, int n_tiles = 0, float* rows_out = nullptr);
+void ts_impl_list_flags(int T, const int64_t* starts, const int32_t* items, const double* md, double near_,
+                        double far_, uint8_t* flags, cudaStream_t st);
+void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W, int H, const ts::BinsView& b,
+                           const ts::SplatRec* rec, const int64_t* item_off, const uint32_t* pair_bits,
+                           const float4* pair_rec, const int32_t* n_proc, const int64_t* rec_off, int64_t* idx,
+                           double* alpha, cudaStream_t st);
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
                      float* d_vert, double* loss, cudaStream_t st);
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
@@ -101,6 +108,6 @@ int ts_impl_rasterize_mesh(const double* verts, int64_t V, const int64_t* tris, 
                            uint8_t* mask, double* depth, double* normal, cudaStream_t st);
 void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,
                   double* m_def, double* v_def, double lr_sdf, double lr_def, double b1, double b2, int64_t t,
-                  double eps, double limit, cudaStream_t st);
+                  double eps, double limit, cudaStream_t st, float* status = nullptr);
 void ts_impl_debug_flags(int flags);
 void ts_impl_phases(unsigned long long out[16], int reset);

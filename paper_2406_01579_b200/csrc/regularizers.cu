@@ -360,7 +360,12 @@ __global__ void __launch_bounds__(256) k_adam(int64_t N, const float4* __restric
                                               double* __restrict__ deform, double* __restrict__ m_sdf,
                                               double* __restrict__ v_sdf, double* __restrict__ m_def,
                                               double* __restrict__ v_def, double lr_sdf, double lr_def, double b1,
-                                              double b2, double c1, double c2, double eps, double limit) {
+                                              double b2, double c1, double c2, double eps, double limit,
+                                              const float* __restrict__ status) {
+  // status (nullable): [0] non-finite map gradients seen by the backward, [1] non-finite
+  // gradient entries (k_finite_check) — the update is skipped and the caller raises
+  // (raster.py:209-211, fit.py:209-212 check before opt.step)
+  if (status && (status[0] != 0.f || status[1] != 0.f)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 g = g4[i];
     const double gs[4] = {(double)g.x, (double)g.y, (double)g.z, (double)g.w};
@@ -381,19 +386,30 @@ __global__ void __launch_bounds__(256) k_adam(int64_t N, const float4* __restric
   }
 }
 
+// count the non-finite entries of the gradient buffer into *flag (warp-aggregated)
+__global__ void __launch_bounds__(256) k_finite_check(int64_t n4, const float4* __restrict__ g4, float* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 g = g4[i];
+    bad |= !isfinite(g.x) || !isfinite(g.y) || !isfinite(g.z) || !isfinite(g.w);
+  }
+  if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(flag, 1.0f);
+}
+
 }  // namespace ts
 
 using namespace ts;
 
 void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,
                   double* m_def, double* v_def, double lr_sdf, double lr_def, double b1, double b2, int64_t t,
-                  double eps, double limit, cudaStream_t st) {
+                  double eps, double limit, cudaStream_t st, float* status) {
   if (N <= 0) return;
   const double c1 = 1.0 - pow(b1, (double)t), c2 = 1.0 - pow(b2, (double)t);
   int blocks = (int)((N + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
+  if (status) k_finite_check<<<blocks, 256, 0, st>>>(N, reinterpret_cast<const float4*>(g4), status + 1);
   k_adam<<<blocks, 256, 0, st>>>(N, reinterpret_cast<const float4*>(g4), sdf, deform, m_sdf, v_sdf, m_def, v_def,
-                                 lr_sdf, lr_def, b1, b2, c1, c2, eps, limit);
+                                 lr_sdf, lr_def, b1, b2, c1, c2, eps, limit, status);
 }
 
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,

@@ -184,7 +184,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   if (!pbits || !prec) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0) {
     ts_impl_forward(tx, ty, bv, so.rec, colors, Scene64{nullptr, nullptr, so.f, so.bbox, so.vert_ids, deform, make_grid(R), cam}, cam.width, cam.height, s,
-                    (float)t_stop, item_off, P, pbits, prec, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
+                    t_stop, item_off, P, pbits, prec, nmap, dmap, omap, colors ? cmap : nullptr, n_proc, n_blend,
                     st, &scr);
   } else {
     cudaMemsetAsync(nmap, 0, sizeof(float) * 3 * HW, st);
@@ -214,7 +214,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
 }
 
 int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4], const float* const dmaps[4],
-                     float* d_vert, float* d_color, void* stream) {
+                     float* d_vert, float* d_color, float* status, void* stream) {
   if (!ws || !ws->valid) return ws_fail(TS_EINVAL, "ts_view_backward: no forward state in the workspace");
   if (!deform || !maps || !dmaps || !d_vert || !maps[0] || !maps[1] || !maps[2] || !dmaps[0] || !dmaps[1] ||
       !dmaps[2])
@@ -235,7 +235,7 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
                    reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<uint32_t*>(ws->pair_bits.p),
                    reinterpret_cast<float4*>(ws->pair_rec.p), m4, d4,
                    reinterpret_cast<int32_t*>(ws->n_proc.p), d_vert, ws->color ? d_color : nullptr,
-                   reinterpret_cast<cudaStream_t>(stream), &scr);
+                   reinterpret_cast<cudaStream_t>(stream), &scr, status);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
   return TS_OK;

@@ -58,23 +58,30 @@ def nc_scratch_bytes(grid) -> int:
     return int(_native.lib().ts_normal_consistency_scratch_bytes(grid.resolution))
 
 
-def map_mse_loss(rendered: RenderMaps, target: RenderMaps, weights: dict):
-    """losses.py:55-81: weighted per-map MSE and the exact gradient images."""
+def map_mse_loss(rendered: RenderMaps, target: RenderMaps, weights: dict, sync: bool = True):
+    """losses.py:55-81: weighted per-map MSE and the exact gradient images.
+
+    sync=False keeps the loss and its components as FP64 device scalars (no host round trip
+    per view; the fit loop reads them once per iteration)."""
     if rendered.opacity.shape != target.opacity.shape:
         raise ValueError("rendered/target map shapes differ")
     npix = rendered.opacity.numel()
-    comps, total = {}, 0.0
-    grads = RenderMaps.zeros(*rendered.opacity.shape, with_color=rendered.color is not None,
-                             device=rendered.opacity.device)
+    comps = {}
+    total = torch.zeros((), dtype=torch.float64, device=rendered.opacity.device)
+    g = {"color": None}
     pairs = [("normal", rendered.normal, target.normal), ("depth", rendered.depth, target.depth),
              ("opacity", rendered.opacity, target.opacity)]
     if rendered.color is not None and target.color is not None:
         pairs.append(("color", rendered.color, target.color))
     for name, r, t in pairs:
         diff = r - torch.as_tensor(t, device=r.device, dtype=r.dtype)
-        mse = float((diff * diff).sum()) / npix
+        mse = (diff * diff).sum(dtype=torch.float64) / npix
         comps[f"mse_{name}"] = mse
         w = float(weights.get(name, 1.0))
-        total += w * mse
-        setattr(grads, name, (2.0 / npix) * w * diff)
+        total = total + w * mse
+        g[name] = (2.0 / npix) * w * diff
+    grads = RenderMaps(g["normal"], g["depth"], g["opacity"], g["color"])
+    if sync:
+        vals = torch.stack([total, *comps.values()]).tolist()
+        return vals[0], dict(zip(comps.keys(), vals[1:])), grads
     return total, comps, grads

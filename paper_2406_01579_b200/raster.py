@@ -5,6 +5,7 @@ this module owns the device buffers and keeps the reference's call signatures.
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -196,6 +197,9 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
                 t.zero_()
     else:
         sp = _native.stream_ptr(stream)
+        # the window-resorted lists belong to this forward (a later forward on the same bins
+        # with another n_w must not change the order this SavedState's backward walks)
+        bins = dataclasses.replace(bins, witems=torch.empty(M, dtype=torch.int32, device=dev))
         sc_abi, b_abi, cam = scene.abi(), bins.abi(), camera.abi()
         item_off = torch.empty(M + 1, dtype=torch.int64, device=dev)
         npairs = _native.i64()

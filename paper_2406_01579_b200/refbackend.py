@@ -63,8 +63,8 @@ def render_forward(scene, bins, camera, n_w: int = 5, t_stop: float = 1e-4, save
 
 def render_backward(saved: DeviceSaved, scene, grid, field, camera, d_maps, grads_type=None):
     """raster.py:206-306 on host objects: dL/dmaps (numpy) in, vertex gradients out — built
-    with `grads_type(d_sdf, d_deform)` (the caller's GradientBuffers class) when given, else a
-    (d_sdf, d_deform) tuple of FP64 numpy arrays (the device sums are FP32)."""
+    with `grads_type(d_sdf, d_deform[, d_color])` (the caller's GradientBuffers class) when
+    given, else a tuple of FP64 numpy arrays (the device sums are FP32)."""
     if not isinstance(saved, DeviceSaved):
         raise ValueError("render_backward needs the state render_forward(save_state=True) returned")
     del scene, camera  # the device copies in `saved` are the same scene and camera
@@ -80,9 +80,14 @@ def _field(field) -> FieldState:
 
 
 def _grads(gb, grads_type):
+    """(d_sdf, d_deform[, d_color]) — d_color (num_tets, 3) when the scene had colours and
+    the map gradients a colour image (raster.py:303-305), like the reference's GradientBuffers."""
     d_sdf = gb.d_sdf.double().cpu().numpy()
     d_def = gb.d_deform.double().cpu().numpy()
-    return grads_type(d_sdf, d_def) if grads_type is not None else (d_sdf, d_def)
+    if gb.d_color is None:
+        return grads_type(d_sdf, d_def) if grads_type is not None else (d_sdf, d_def)
+    d_col = gb.d_color.double().cpu().numpy()
+    return grads_type(d_sdf, d_def, d_col) if grads_type is not None else (d_sdf, d_def, d_col)
 
 
 def prefilter(grid, field, s, threshold=1.0 / 255.0):

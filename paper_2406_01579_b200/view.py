@@ -58,8 +58,12 @@ class ViewRenderer:
         return maps
 
     def backward(self, field, d_maps: RenderMaps, out: GradientBuffers, maps: RenderMaps | None = None,
-                 stream=None) -> GradientBuffers:
-        """Accumulate the last view's dL/d(sdf, deform) (and dL/dcolor) into `out`."""
+                 stream=None, status: torch.Tensor | None = None) -> GradientBuffers:
+        """Accumulate the last view's dL/d(sdf, deform) (and dL/dcolor) into `out`.
+
+        `status` (device f32, optional): incremented when a map gradient is non-finite — the
+        fused path's form of raster.py:209-211, raised by the caller at its next sync
+        (`batch.FitStep.check_status`)."""
         maps = maps if maps is not None else self._last
         P = ctypes.c_void_p
         m = (P * 4)(maps.normal.data_ptr(), maps.depth.data_ptr(), maps.opacity.data_ptr(),
@@ -69,5 +73,5 @@ class ViewRenderer:
         _native.check(self._L.ts_view_backward(self._ws, _native.ptr(field.deformation),
                                                ctypes.cast(m, ctypes.POINTER(P)), ctypes.cast(d, ctypes.POINTER(P)),
                                                _native.ptr(out.d_vert), _native.ptr(out.d_color),
-                                               _native.stream_ptr(stream)))
+                                               _native.ptr(status), _native.stream_ptr(stream)))
         return out

@@ -122,3 +122,33 @@ def test_partially_visible_grid(ts):
     ogb = O.render_backward(osv, osc, og, ofs, ocam, w)
     assert rel_err(gb.d_sdf.cpu().numpy(), ogb.d_sdf) < 1e-3
     assert rel_err(gb.d_deform.cpu().numpy(), ogb.d_deform) < 1e-3
+
+
+def test_fused_path_rejects_non_finite_map_gradients():
+    """raster.py:209-211 on the fused path: a NaN in dL/dmaps is flagged on the device, the Adam
+    update is skipped (the field stays intact, like the reference, which raises before
+    opt.step), and check_status raises ValueError at the next sync."""
+    import paper_2406_01579_b200 as ts
+    from paper_2406_01579_b200.batch import FitStep, StepConfig
+    g = ts.build_grid(16)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    cams = [ts.orbit_camera(i, 2, width=64, height=64) for i in range(2)]
+    sdf0, def0 = f.sdf.clone(), f.deformation.clone()
+
+    def dfn(vi, maps):
+        d = ts.RenderMaps.zeros(64, 64)
+        if vi == 1:
+            d.depth[10, 20] = float("nan")
+        return d
+
+    step = FitStep(g, f, cams, StepConfig())
+    step(100.0, [0, 1], dfn)
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError):
+        step.check_status()
+    assert torch.equal(f.sdf, sdf0) and torch.equal(f.deformation, def0)
+    # a clean step afterwards runs and updates
+    step(100.0, [0, 1], lambda vi, m: ts.RenderMaps.zeros(64, 64))
+    torch.cuda.synchronize()
+    step.check_status()
+    assert not torch.equal(f.sdf, sdf0)  # the regularizers move the field

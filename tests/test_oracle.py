@@ -108,3 +108,56 @@ def test_spec_known_answers():
     m1, _ = O.render_forward(sc, b, cam, n_w=1, backend=BACKENDS[0])
     m2, _ = O.render_forward(sc, b, cam, n_w=50, backend=BACKENDS[0])
     assert np.array_equal(m1.normal, m2.normal)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_color_path(backend):
+    """Colour compositing and colour gradients (_core.pyx:202-205,219-222,410-413,433-436,
+    raster.py:303-305) against the reference's fixture."""
+    G = load_golden("color_noisy_r12_s100_cam5.npz")
+    g, fs = _field(G)
+    cam = _cam(G)
+    sc = O.build_scene(g, fs, cam, float(G["s"]), active=G["active"], colors=G["colors"])
+    assert np.array_equal(sc.tet_ids, G["tet_ids"])
+    b = O.bin_and_sort(sc, cam)
+    assert np.array_equal(b.items, G["items"])
+    maps, saved = O.render_forward(sc, b, cam, save_state=True, backend=backend, want_counts=True)
+    assert np.array_equal(saved.counts, G["counts"])
+    for k in ("normal", "depth", "opacity", "color"):
+        assert rel_err(getattr(maps, k), G[k]) < 1e-12, k
+    dm = O.RenderMaps(G["d_normal"], G["d_depth"], G["d_opacity"], G["d_color"])
+    gb = O.render_backward(saved, sc, g, fs, cam, dm, backend=backend)
+    assert rel_err(gb.d_sdf, G["d_sdf"]) < 1e-10
+    assert rel_err(gb.d_deform, G["d_deform"]) < 1e-10
+    assert gb.d_color is not None and rel_err(gb.d_color, G["d_color_tet"]) < 1e-10
+
+
+def window_scene(G):
+    """The oracle SplatScene of the window fixture: the reference's FP64 arrays with the
+    fixture's re-keyed mean depths (make_golden.window_depths)."""
+    return O.SplatScene(G["tet_ids"], G["vert_ids"], G["proj"], G["depths"], G["f"], G["normals"],
+                        G["mean_depth"], G["alpha_max"], G["bbox"], float(G["s"]), None)
+
+
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_window_reorders(backend):
+    """The N_w window on lists it actually reorders (_core.pyx:171-187): per-window maps,
+    counts and gradients equal the reference's; the windows give different images."""
+    G = load_golden("window_noisy_r16_s100_cam3.npz")
+    g, fs = _field(G)
+    cam = _cam(G)
+    sc = window_scene(G)
+    b = O.bin_and_sort(sc, cam)
+    assert np.array_equal(b.starts, G["starts"]) and np.array_equal(b.items, G["items"])
+    inv = sum(int((np.diff(G["mean_depth"][b.items[b.starts[t]:b.starts[t + 1]]]) < 0).sum()) for t in range(b.num_tiles))
+    assert inv > 1000
+    dm = O.RenderMaps(G["d_normal"], G["d_depth"], G["d_opacity"])
+    for nw in G["windows"].tolist():
+        maps, saved = O.render_forward(sc, b, cam, n_w=nw, save_state=True, backend=backend, want_counts=True)
+        assert np.array_equal(saved.counts, G[f"counts_w{nw}"]), nw
+        assert rel_err(maps.normal, G[f"normal_w{nw}"]) < 1e-12
+        assert rel_err(maps.opacity, G[f"opacity_w{nw}"]) < 1e-12
+        gb = O.render_backward(saved, sc, g, fs, cam, dm, backend=backend)
+        assert rel_err(gb.d_sdf, G[f"d_sdf_w{nw}"]) < 1e-10
+        assert rel_err(gb.d_deform, G[f"d_deform_w{nw}"]) < 1e-10
+    assert np.abs(G["normal_w1"] - G["normal_w5"]).max() > 0.1
