@@ -81,6 +81,7 @@ __device__ unsigned long long g_ts_counters[8];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity),
 // bit 4 = count the pairs phase A evaluates (g_ts_counters[2])
 __device__ int g_ts_debug_flags;
+static int h_debug_flags = 0;  // host copy (bit 5 = 32: launch the warp-specialised k_forward_ws)
 // diagnostics only (flag bit 1): per-tile forward start/end globaltimer, SM id
 __device__ unsigned long long g_ts_tile_time[2 * 65536];
 __device__ unsigned int g_ts_tile_sm[65536];
@@ -118,9 +119,8 @@ __device__ __forceinline__ float frcp(float x) {
 // FOLD (forward): faces the reference rejects as degenerate get edge functions that are always
 // out, so phase A1 needs no validity test
 template <bool FOLD>
-__device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
-  const float4* p = reinterpret_cast<const float4*>(&rec);
-  float4 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3], q4 = p[4], q5 = p[5];
+__device__ __forceinline__ void stage_q(const float4 q0, const float4 q1, const float4 q2, const float4 q3,
+                                        const float4 q4, const float4 q5, int k, Staged& s) {
   int rx = __float_as_int(q0.x), ry = __float_as_int(q0.y);
   s.rx0 = (int)(short)(rx & 0xffff);
   s.rx1 = rx >> 16;
@@ -170,6 +170,12 @@ __device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
   float izmax = fmaxf(fmaxf(s.iz[0], s.iz[1]), fmaxf(s.iz[2], s.iz[3]));
   s.fband = 0.75f * s.band * (izmax * frcp(izmin)) * fmax;
   s.ftol0 = 1e-6f * fmax;
+}
+
+template <bool FOLD>
+__device__ __forceinline__ void stage(const SplatRec& rec, int k, Staged& s) {
+  const float4* p = reinterpret_cast<const float4*>(&rec);
+  stage_q<FOLD>(p[0], p[1], p[2], p[3], p[4], p[5], k, s);
 }
 
 struct Hit {
@@ -754,19 +760,24 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     __syncthreads();
     TS_PHASE(1);
     // ---- A': exact FP64 re-decisions, 8 pairs per warp, one face per lane ------------------
-    for (int q0 = (threadIdx.x >> 5) * 8; q0 < F.nex; q0 += kWarps * 8) {
-      const int qi = q0 + ((threadIdx.x & 31) >> 2);
-      const bool act = qi < F.nex;
-      const int it = act ? F.exq[qi] : 0;
-      const int j = pair_splat(F.R, it);
-      int px_, py_;
-      pair_pixel(F.R, j, it, px_, py_);
-      Blend b;
-      const bool bl = exact_group(S64, act, F.sh[j].k, px_, py_, s64, b);
-      if (act && bl && (threadIdx.x & 3) == 0)
-        put_pair(F, it, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
+    //      (F.nex is CTA-uniform after the barrier: chunks without queued pairs skip the pass
+    //      and its barrier)
+    const int nex = F.nex;
+    if (nex > 0) {
+      for (int q0 = (threadIdx.x >> 5) * 8; q0 < nex; q0 += kWarps * 8) {
+        const int qi = q0 + ((threadIdx.x & 31) >> 2);
+        const bool act = qi < nex;
+        const int it = act ? F.exq[qi] : 0;
+        const int j = pair_splat(F.R, it);
+        int px_, py_;
+        pair_pixel(F.R, j, it, px_, py_);
+        Blend b;
+        const bool bl = exact_group(S64, act, F.sh[j].k, px_, py_, s64, b);
+        if (act && bl && (threadIdx.x & 3) == 0)
+          put_pair(F, it, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     TS_PHASE(2);
     // the chunk's blend bits into the view's bit array (words at the chunk ends are shared)
     if (threadIdx.x < (total + 31) / 32) {
@@ -825,6 +836,10 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   if (ptime)
     for (int k = 0; k < 7; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
 }
+
+}  // namespace ts
+#include "forward_ws.cuh"
+namespace ts {
 
 // N_w resorting window (_core.pyx:171-187) for tiles whose list is not mean-depth monotone.
 // The list is sorted by (q, splat) with q = 32-bit quantised mean depth, so entries with
@@ -1519,16 +1534,32 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
   const int T = tiles_x * tiles_y;
   int32_t* const given_order = scr ? scr->torder : nullptr;
   cudaMemsetAsync(pair_bits, 0, sizeof(uint32_t) * (size_t)TS_PAIR_BIT_WORDS(n_pairs), st);
-  const int smem = (int)sizeof(FwdSmem);
-  static const bool attr = [smem] {  // once (thread-safe static: lanes launch from several threads)
+  const int smem = (int)sizeof(FwdSmem), smem_ws = (int)sizeof(WsSmem);
+  static const bool attr = [smem, smem_ws] {  // once (thread-safe static: lanes launch from several threads)
     cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_forward_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ws);
+    cudaFuncSetAttribute(k_forward_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ws);
     return true;
   }();
   (void)attr;
   int32_t* torder = take_tmp(given_order, T, st);
   k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   const bool clip_stops = (1.0 - kAlphaClipD) < t_stop;  // splat.py:14-15: T (1 - ALPHA_CLIP) < T_STOP
+  if (h_debug_flags & 32) {  // flag 32: the warp-specialised forward (forward_ws.cuh; measured slower)
+    if (colors && cmap)
+      k_forward_ws<true><<<T, kWsThreads, smem_ws, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors,
+                                                         S64, tiles_x, W, H, (float)s, s, (float)t_stop, clip_stops,
+                                                         item_off, pair_bits, pair_rec, nmap, dmap, omap, cmap, n_proc,
+                                                         n_blend);
+    else
+      k_forward_ws<false><<<T, kWsThreads, smem_ws, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec,
+                                                          nullptr, S64, tiles_x, W, H, (float)s, s, (float)t_stop,
+                                                          clip_stops, item_off, pair_bits, pair_rec, nmap, dmap, omap,
+                                                          nullptr, n_proc, n_blend);
+    put_tmp(torder, given_order, st);
+    return;
+  }
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
                                                 W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
@@ -1626,7 +1657,10 @@ void ts_impl_phases(unsigned long long out[16], int reset) {
   }
 }
 
-void ts_impl_debug_flags(int flags) { cudaMemcpyToSymbol(g_ts_debug_flags, &flags, sizeof(int)); }
+void ts_impl_debug_flags(int flags) {
+  h_debug_flags = flags;
+  cudaMemcpyToSymbol(g_ts_debug_flags, &flags, sizeof(int));
+}
 
 void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n) {
   cudaMemcpyFromSymbol(t2, g_ts_tile_time, sizeof(unsigned long long) * 2 * n);
