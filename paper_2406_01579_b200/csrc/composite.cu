@@ -1109,6 +1109,7 @@ struct BwdSmem {
   static constexpr int NC = COLOR ? 23 : 20;  // gradient components per item / (tile, splat) row
   static constexpr int RS = COLOR ? 25 : 21;  // odd item-row stride: conflict-free per-lane rows
   static constexpr int AS = COLOR ? 24 : 20;  // accumulator row stride (whole float4s)
+  static constexpr int GM = COLOR ? 7 : 4;    // map gradients per pixel (normal, depth, colour)
   Staged sh[kCh];
   float2 wg[kCap];      // items only — load: (alpha, 1-alpha); phase B: (w = T a, G)
   float acc[kCh][AS];   // per-(tile, splat) gradient rows of the chunk
@@ -1117,10 +1118,11 @@ struct BwdSmem {
     ChunkMask bmask[TS_TILE_PX];  // load + B: per pixel, chunk splats that blend (bit j)
     float rows[kWarps][32][RS];   // C: per-item rows of each warp's batch
   } u;
-  uint32_t items[kCap];  // C: the chunk's items (j << 16 | pair) in pair order
+  uint16_t items[kCap];  // C: the chunk's items (pair index) in pair order
   int wcnt[kCap / 32];   // items per 32-pair block -> exclusive offsets
   uint32_t lbits[kCap / 32];  // loaded (blending, not early-stopped) pairs, block k*8+warp
   int lim[TS_TILE_PX];   // per pixel: list entries the forward consumed (n_proc)
+  float gmap[TS_TILE_PX][GM];  // per pixel: dL/d(normal xyz, depth, colour) — read by phase C
   RectTab R;
   Prefetch pf;
   long long phase[8];  // diagnostics (flag bit 2)
@@ -1140,33 +1142,22 @@ static_assert(3 * (sizeof(BwdSmem<false>) + 1024) <= 228 * 1024, "backward: 3 CT
 // in the neighbouring batch of another warp).
 template <bool COLOR>
 __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, const float4* __restrict__ pair_rec,
-                                              int64_t ib0, int W, const float* __restrict__ d_normal,
-                                              const float* __restrict__ d_depth,
-                                              const float* __restrict__ d_color) {
+                                              int64_t ib0) {
   using SM = BwdSmem<COLOR>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* row = S.u.rows[warp][lane];
-  const int item = lane < m ? (int)S.items[b0 + lane] : -1;
-  const int jl = item >> 16;
+  const int it = lane < m ? (int)S.items[b0 + lane] : 0;
+  const int jl = lane < m ? (int)S.R.jtab[it] : -1;
   if (lane < m) {
-    const int j = jl, it = item & 0xffff;
+    const int j = jl;
     const Staged& r = S.sh[j];
-    const int local = it - S.R.pre[j];
-    const int nx = S.R.nx[j];
-    const int yy = (int)(((float)local + 0.5f) * S.R.inv[j]);
-    const int xi = S.R.x0[j] + (local - yy * nx), yi = S.R.y0[j] + yy;
-    const int64_t p = (int64_t)yi * W + xi;
+    int xi, yi;
+    pair_pixel(S.R, j, it, xi, yi);
     const float2 wg = S.wg[it];
     const float w = wg.x, G = wg.y;
-    row[16] = __ldg(d_normal + p * 3) * w;
-    row[17] = __ldg(d_normal + p * 3 + 1) * w;
-    row[18] = __ldg(d_normal + p * 3 + 2) * w;
-    row[19] = __ldg(d_depth + p) * w;
-    if (COLOR) {
-      row[20] = __ldg(d_color + p * 3) * w;
-      row[21] = __ldg(d_color + p * 3 + 1) * w;
-      row[22] = __ldg(d_color + p * 3 + 2) * w;
-    }
+    const float* gm = S.gmap[(yi & (TS_TILE - 1)) * TS_TILE + (xi & (TS_TILE - 1))];
+#pragma unroll
+    for (int i = 0; i < SM::GM; ++i) row[16 + i] = gm[i] * w;
     float acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.f;
@@ -1241,6 +1232,15 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         C_c[i] = color_map[p * 3 + i];
       }
     }
+  }
+  S.gmap[pix][0] = g_n[0];
+  S.gmap[pix][1] = g_n[1];
+  S.gmap[pix][2] = g_n[2];
+  S.gmap[pix][3] = g_d;
+  if (COLOR) {
+    S.gmap[pix][4] = g_c[0];
+    S.gmap[pix][5] = g_c[1];
+    S.gmap[pix][6] = g_c[2];
   }
   if (status) {  // raster.py:209-211: non-finite incoming map gradients, raised by the caller
     bool bad = !isfinite(g_o) || !isfinite(g_d) || !isfinite(g_n[0]) || !isfinite(g_n[1]) || !isfinite(g_n[2]);
@@ -1352,15 +1352,13 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         const int it = threadIdx.x + k * TS_TILE_PX;
         const unsigned bm = S.lbits[k * kWarps + warp];
         const bool has = (bm >> lane) & 1u;
-        if (has)
-          S.items[S.wcnt[k * kWarps + warp] + __popc(bm & ((1u << lane) - 1u))] =
-              ((uint32_t)pair_splat(S.R, it) << 16) | (uint32_t)it;
+        if (has) S.items[S.wcnt[k * kWarps + warp] + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)it;
       }
     }
     __syncthreads();
     const int nitems = S.nitems;
     for (int b0 = warp * 32; b0 < nitems; b0 += TS_TILE_PX)
-      process_batch<COLOR>(S, b0, min(32, nitems - b0), pair_rec, ib0, W, d_normal, d_depth, d_color);
+      process_batch<COLOR>(S, b0, min(32, nitems - b0), pair_rec, ib0);
     __syncthreads();
     TS_PHASE(3);
     // ---- the chunk's per-(tile, splat) rows, added into the splats' rows (zeroed per view;
