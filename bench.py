@@ -263,7 +263,9 @@ def run_gpu(args):
                                torch.randn((S, S), device=dev, generator=gen)) for vi in views}
     step = FitStep(g, field, cams, StepConfig(lambda_eik=LAMBDA, lambda_nc=LAMBDA,
                                               inflight=int(os.environ["TS_INFLIGHT"]) if "TS_INFLIGHT" in os.environ
-                                              else None))
+                                              else None,
+                                              sync_free=None if "TS_SYNC_FREE" not in os.environ
+                                              else os.environ["TS_SYNC_FREE"] != "0"))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 

@@ -148,7 +148,7 @@ int ts_backward_tiles(const ts_scene* scene, int64_t K, const float* colors, con
 
 /* Fused per-view pipeline over a persistent, grow-only device workspace (one view in flight
  * per workspace).  ts_view_forward = build_scene + bin_and_sort + window + render_forward;
- * out_counts = {K visible splats, M tile pairs, P pixel pairs} (host).  [sync]
+ * out_counts = {K visible splats, M tile pairs, P pixel pairs, longest tile list} (host).  [sync]
  * ts_view_backward = render_backward of the workspace's last forward, accumulated into d_vert
  * (and d_color when the forward had colors_tet f32[6R^3,3]).  status (nullable, device f32):
  * incremented when a map gradient is non-finite (raster.py:209-211 raises ValueError; here the
@@ -163,6 +163,24 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
 int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4],
                      const float* const d_maps[4], float* d_vert, float* d_color, float* status, void* stream);
 const int32_t* ts_view_n_blend(ts_workspace* ws);
+
+/* Sync-free per-view path.  With capacities set (cap_M tile pairs, cap_P pixel pairs, cap_L the
+ * longest tile list (0 = unbounded); cap_M or cap_P 0 = off)
+ * ts_view_forward makes no host round trip: buffers are sized by the capacities (visible
+ * splats <= n_active), counts stay on the device and out_counts returns -1.  A view that needs
+ * more raises the workspace's overflow flag, which makes every later kernel of the view (and
+ * its ts_view_backward) exit; ts_view_status [sync] returns {overflow, K, M, P, max list} of the
+ * last forward so the caller can grow the capacities and re-run it; need_out (device int64[5],
+ * nullable) receives the same five values stream-ordered, and ts_view_backward of an
+ * overflowed view adds 1 to its status[2] (ts_adam_step then skips).  ts_view_need /
+ * ts_view_overflow: the device addresses of those counts (int64[4]) and the flag (int32). */
+int ts_workspace_set_caps(ts_workspace* ws, int64_t cap_M, int64_t cap_P, int64_t cap_L, int64_t* need_out);
+/* stream-ordered: out5 (device int64[5]) = {K, M, P, max list, overflow} of the last forward,
+ * and status[2] (device f32, nullable) += 1 when it overflowed (ts_adam_step then skips). */
+int ts_view_collect(ts_workspace* ws, float* status, int64_t* out5, void* stream);
+int ts_view_status(ts_workspace* ws, int64_t* out5, void* stream);
+const int64_t* ts_view_need(ts_workspace* ws);
+const int32_t* ts_view_overflow(ts_workspace* ws);
 
 /* K8 eikonal_loss (losses.py:25-36): loss (device f64[1], overwritten) and
  * scale * gradients accumulated into d_vert. */
@@ -216,10 +234,11 @@ int ts_rasterize_mesh(const double* vertices, int64_t V, const int64_t* triangle
 /* Adam step of the fit loop (fit.py:70-90) from the interleaved gradient buffer d_vert f32[N,4]:
  * FP64 moments m_sdf, v_sdf [N] and m_def, v_def [N,3], step t >= 1 (bias corrections
  * 1 - beta^t), deformation clamped to +-deform_limit (field.py:40-42) afterwards.
- * status (nullable, device f32[2+]): the non-finite entries of d_vert are counted into
- * status[1] first; when status[0] (non-finite map gradients, ts_view_backward) or status[1] is
- * non-zero the parameters and moments are left untouched (fit.py:209-212 checks before
- * opt.step) and the caller raises at its next sync. */
+ * status (nullable, device f32[3+]): the non-finite entries of d_vert are counted into
+ * status[1] first; when status[0] (non-finite map gradients, ts_view_backward), status[1] or
+ * status[2] (a sync-free view overflowed its capacities, ts_view_collect) is non-zero the
+ * parameters and moments are left untouched (fit.py:209-212 checks before opt.step) and the
+ * caller raises / re-runs at its next sync. */
 int ts_adam_step(int32_t resolution, const float* d_vert, double* sdf, double* deform, double* m_sdf,
                  double* v_sdf, double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1,
                  double beta2, int64_t t, double eps, double deform_limit, float* status, void* stream);

@@ -84,6 +84,11 @@ def lib():
                             ctypes.c_int),
         "ts_view_backward": ([P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, P, P], ctypes.c_int),
         "ts_view_n_blend": ([P], P),
+        "ts_workspace_set_caps": ([P, I64, I64, I64, P], ctypes.c_int),
+        "ts_view_collect": ([P, P, P, P], ctypes.c_int),
+        "ts_view_status": ([P, PI64, P], ctypes.c_int),
+        "ts_view_need": ([P], P),
+        "ts_view_overflow": ([P], P),
         "ts_debug_tile_times": ([ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32), ctypes.c_int],
                                 ctypes.c_int),
     }

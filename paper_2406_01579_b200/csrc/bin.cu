@@ -40,7 +40,10 @@ __device__ __forceinline__ void tile_rect_q(const double* bb, double md, int til
 __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const double* __restrict__ md, int tiles_x,
                             int tiles_y, double near_, double far_, BinRec* __restrict__ br,
                             uint32_t* __restrict__ qout, int32_t* __restrict__ splat_cnt,
-                            int32_t* __restrict__ tile_cnt) {
+                            int32_t* __restrict__ tile_cnt, const int64_t* __restrict__ Kdev) {
+  // Kdev (nullable): the visible splats on the device; K is then the capacity and the
+  // counts of [*Kdev, K) are written as 0 (the scans run over the capacity)
+  const int64_t n = Kdev ? min(K, *Kdev) : K;
   // warp-uniform loop so the per-tile counter updates can be aggregated per warp: splats
   // with nearby tet ids are nearby in space and mostly share tiles (one atomic per
   // distinct tile per warp instead of one per (splat, tile) pair)
@@ -48,7 +51,8 @@ __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const do
   for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x; k0 < K; k0 += stride) {
     const int64_t k = k0 + threadIdx.x;
     int tx0 = 0, ty0 = 0, nx = 0, ny = 0;
-    if (k < K) {
+    if (k >= n && k < K) splat_cnt[k] = 0;
+    if (k < n) {
       int tx1, ty1;
       uint32_t q;
       tile_rect_q(bbox + k * 4, md[k], tiles_x, tiles_y, near_, far_, tx0, tx1, ty0, ty1, q);
@@ -72,7 +76,10 @@ __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const do
 
 __global__ void k_bin_scatter(int64_t K, const BinRec* __restrict__ br, const uint32_t* __restrict__ q, int tiles_x,
                               const int64_t* __restrict__ starts, int32_t* __restrict__ cursor,
-                              uint64_t* __restrict__ keys) {
+                              uint64_t* __restrict__ keys, const int64_t* __restrict__ Kdev,
+                              const int* __restrict__ ovf) {
+  if (ovf && *ovf) return;
+  if (Kdev) K = min(K, *Kdev);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const unsigned lane = threadIdx.x & 31;
   for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x; k0 < K; k0 += stride) {
@@ -300,11 +307,12 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
                                                             const int64_t* __restrict__ splat_off,
                                                             const double* __restrict__ md,
                                                             int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                            uint8_t* __restrict__ nonmono, uint32_t* __restrict__ qsorted) {
+                                                            uint8_t* __restrict__ nonmono, uint32_t* __restrict__ qsorted,
+                                                            const int* __restrict__ ovf) {
   extern __shared__ uint64_t s[];
   __shared__ int bad, longrun;
   const int t = blockIdx.x;
-  if (t >= T) return;
+  if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
   if (L <= 0 || L > cap) return;
   if (L <= 512 || cap > 8 * THREADS) {  // short lists: bitonic
@@ -340,7 +348,8 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     const uint64_t* __restrict__ keys, int tiles_x, const BinRec* __restrict__ br,
     const int64_t* __restrict__ splat_off, const double* __restrict__ md, int32_t* __restrict__ items,
     int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono, int cap, int passes_lo,
-    uint32_t* __restrict__ qsorted) {
+    uint32_t* __restrict__ qsorted, const int* __restrict__ ovf) {
+  if (ovf && *ovf) return;
   extern __shared__ uint32_t sm32[];
   __shared__ int longrun;
   uint32_t* kq = sm32;
@@ -378,7 +387,8 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
 
 // tiles with lo_len < L <= cap -> tlist[0, *tcount)
 __global__ void k_long_tiles(int T, int64_t lo_len, int64_t cap, const int64_t* __restrict__ starts,
-                             int32_t* __restrict__ tlist, int64_t* __restrict__ tcount) {
+                             int32_t* __restrict__ tlist, int64_t* __restrict__ tcount, const int* __restrict__ ovf) {
+  if (ovf && *ovf) return;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
     const int64_t L = starts[t + 1] - starts[t];
     if (L > lo_len && L <= cap) tlist[atomicAdd((unsigned long long*)tcount, 1ull)] = t;
@@ -386,6 +396,15 @@ __global__ void k_long_tiles(int T, int64_t lo_len, int64_t cap, const int64_t* 
 }
 
 // oversize tiles: bitonic over a padded copy in global scratch (offset 2*lo, size <= 2L)
+__device__ void sort_tile_global(int t, int lo_len, const int64_t* __restrict__ starts,
+                                 const uint64_t* __restrict__ keys, int tiles_x, const BinRec* __restrict__ br,
+                                 const int64_t* __restrict__ splat_off, const double* __restrict__ md,
+                                 uint64_t* __restrict__ scratch, int32_t* __restrict__ items,
+                                 int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono,
+                                 uint32_t* __restrict__ qsorted);
+
+// tlist / tcount (nullable): the tiles to sort, listed by k_long_tiles (sync-free path, a
+// persistent grid); else CTA t sorts tile t when it is longer than lo_len
 __global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, const int64_t* __restrict__ starts,
                                                            const uint64_t* __restrict__ keys, int tiles_x,
                                                            const BinRec* __restrict__ br,
@@ -393,10 +412,23 @@ __global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, co
                                                            const double* __restrict__ md,
                                                            uint64_t* __restrict__ scratch,
                                                            int32_t* __restrict__ items, int32_t* __restrict__ pos_of,
-                                                           uint8_t* __restrict__ nonmono, uint32_t* __restrict__ qsorted) {
+                                                           uint8_t* __restrict__ nonmono, uint32_t* __restrict__ qsorted,
+                                                           const int* __restrict__ ovf, const int32_t* __restrict__ tlist,
+                                                           const int64_t* __restrict__ tcount) {
+  if (ovf && *ovf) return;
+  const int64_t ntiles = tlist ? *tcount : (int64_t)T;
+  for (int64_t idx = blockIdx.x; idx < ntiles; idx += gridDim.x)
+    sort_tile_global(tlist ? tlist[idx] : (int)idx, lo_len, starts, keys, tiles_x, br, splat_off, md, scratch, items,
+                     pos_of, nonmono, qsorted);
+}
+
+__device__ void sort_tile_global(int t, int lo_len, const int64_t* __restrict__ starts,
+                                 const uint64_t* __restrict__ keys, int tiles_x, const BinRec* __restrict__ br,
+                                 const int64_t* __restrict__ splat_off, const double* __restrict__ md,
+                                 uint64_t* __restrict__ scratch, int32_t* __restrict__ items,
+                                 int32_t* __restrict__ pos_of, uint8_t* __restrict__ nonmono,
+                                 uint32_t* __restrict__ qsorted) {
   __shared__ int bad;
-  const int t = blockIdx.x;
-  if (t >= T) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
   if (L <= lo_len) return;
   int64_t P = 1;
@@ -424,6 +456,7 @@ __global__ void __launch_bounds__(1024) k_tile_sort_global(int T, int lo_len, co
   if (mybad) bad = 1;
   __syncthreads();
   if (threadIdx.x == 0) nonmono[t] = (uint8_t)bad;
+  __syncthreads();  // `bad` is reused by the next tile of a persistent CTA
 }
 
 __global__ void k_max_len(int T, const int64_t* __restrict__ starts, int64_t* __restrict__ out) {
@@ -445,9 +478,11 @@ using namespace ts;
 
 
 // Phase 1: counts, starts[T+1], splat_off[K+1]; returns M and max tile length (host sync).
+// dyn (sync-free): K is the capacity, dyn->K the device count; nothing is copied to the host
+// (M = starts[T] and the longest list dev_i64[1] stay on the device).
 void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tiles_x, int tiles_y, double near_,
                        double far_, const BinWork& w, int64_t* starts, int64_t* splat_off, int64_t* M_out,
-                       int64_t* maxL_out, cudaStream_t st) {
+                       int64_t* maxL_out, cudaStream_t st, const Dyn* dyn) {
   const int T = tiles_x * tiles_y;
   cudaMemsetAsync(w.tile_cnt, 0, sizeof(int32_t) * T, st);
   cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t) * 2, st);
@@ -455,11 +490,12 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
     int blocks = (int)((K + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_bin_count<<<blocks, 256, 0, st>>>(K, bbox, md, tiles_x, tiles_y, near_, far_, w.br, w.q, w.splat_cnt,
-                                        w.tile_cnt);
+                                        w.tile_cnt, dyn ? dyn->K : nullptr);
   }
   scan_counts(w.tile_cnt, T, starts, w.scratch, st);
   scan_counts(w.splat_cnt, K, splat_off, w.scratch, st);
   k_max_len<<<8, 256, 0, st>>>(T, starts, w.dev_i64 + 1);
+  if (dyn) return;
   int64_t h[2];
   cudaMemcpyAsync(&h[0], starts + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&h[1], w.dev_i64 + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
@@ -469,46 +505,65 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
 }
 
 // Phase 2: scatter keys + per-tile sort.  keys: [M]; gscratch: [2M] only when maxL > 16384.
+// dyn (sync-free): maxL is unknown on the host, so every sort launch runs and picks its tiles
+// on the device (bitonic / radix <= 2048 in k_tile_sort_smem, 2048 < L <= 8192 and
+// 8192 < L <= 16384 in k_tile_sort_long at two shared-memory sizes, longer in
+// k_tile_sort_global, which then needs gscratch [2 * M capacity]); dyn->ovf stops them all.
 void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const BinWork& w, const int64_t* starts,
                       const int64_t* splat_off, int64_t maxL, uint64_t* keys, uint64_t* gscratch, int32_t* items,
-                      int32_t* pos_of, uint8_t* nonmono, cudaStream_t st, uint32_t* qsorted) {
+                      int32_t* pos_of, uint8_t* nonmono, cudaStream_t st, uint32_t* qsorted, const Dyn* dyn) {
   const int T = tiles_x * tiles_y;
+  const int* ovf = dyn ? dyn->ovf : nullptr;
   cudaMemsetAsync(w.tile_cnt, 0, sizeof(int32_t) * T, st);
   cudaMemsetAsync(nonmono, 0, T, st);
   if (K > 0) {
     int blocks = (int)((K + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_bin_scatter<<<blocks, 256, 0, st>>>(K, w.br, w.q, tiles_x, starts, w.tile_cnt, keys);
+    k_bin_scatter<<<blocks, 256, 0, st>>>(K, w.br, w.q, tiles_x, starts, w.tile_cnt, keys, dyn ? dyn->K : nullptr,
+                                          ovf);
   }
+  // sync-free: maxL is the capacity of the longest list (the view overflows above it): the
+  // size classes up to it are launched, each picking its tiles on the device
   if (maxL >= 1) {
     int kbits = 1;  // digit passes over the splat index of a full-key sort: ceil(bits(K - 1) / 8)
     while (kbits < 32 && ((int64_t)1 << kbits) < K) ++kbits;
     const size_t smem_s = sizeof(uint32_t) * (2 * 2048 + 8 * 256 + 256);  // kq, kv | bitonic u64; H; dbase
     k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, 2048, (kbits + 7) / 8, starts, keys, tiles_x, w.br, splat_off,
-                                                  md, items, pos_of, nonmono, qsorted);
-    if (maxL > 2048) {
+                                                  md, items, pos_of, nonmono, qsorted, ovf);
+    // the attribute is set once, to the 16384-entry cap (a thread-safe static: views in
+    // flight launch from several host threads); the launch asks for what it needs
+    static const bool attr = [] {
+      const size_t mx = sizeof(uint32_t) * (2 * (size_t)16384 + kRadixWarps * 256 + 256);
+      cudaFuncSetAttribute(k_tile_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+      return true;
+    }();
+    (void)attr;
+    auto long_sort = [&](int64_t lo_len, int cap) {
       // the scatter cursor is free again: reuse it as the long-tile list
       cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
-      k_long_tiles<<<(T + 255) / 256, 256, 0, st>>>(T, 2048, 16384, starts, w.tile_cnt, w.dev_i64);
-      // shared memory sized to the longest list (not the 16384 cap) so two CTAs fit per SM
-      // where they can; digit passes over the splat index: ceil(bits(K - 1) / 8)
-      const int cap = maxL <= 4096 ? 4096 : (maxL <= 8192 ? 8192 : 16384);
+      k_long_tiles<<<(T + 255) / 256, 256, 0, st>>>(T, lo_len, cap, starts, w.tile_cnt, w.dev_i64, ovf);
       const size_t smem = sizeof(uint32_t) * (2 * (size_t)cap + kRadixWarps * 256 + 256);
-      // the attribute is set once, to the 16384-entry cap (a thread-safe static: views in
-      // flight launch from several host threads); the launch asks for what it needs
-      static const bool attr = [] {
-        const size_t mx = sizeof(uint32_t) * (2 * (size_t)16384 + kRadixWarps * 256 + 256);
-        cudaFuncSetAttribute(k_tile_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-        return true;
-      }();
-      (void)attr;
       const int per_sm = smem <= 110 * 1024 ? 2 : 1;
       k_tile_sort_long<<<148 * per_sm, kRadixThreads, smem, st>>>(w.tile_cnt, w.dev_i64, starts, keys, tiles_x, w.br,
                                                                  splat_off, md, items, pos_of, nonmono, cap,
-                                                                 (kbits + 7) / 8, qsorted);
+                                                                 (kbits + 7) / 8, qsorted, ovf);
+    };
+    if (dyn) {
+      if (maxL > 2048) long_sort(2048, 8192);
+      if (maxL > 8192) long_sort(8192, 16384);
+    } else if (maxL > 2048) {
+      // shared memory sized to the longest list (not the 16384 cap) so two CTAs fit per SM
+      // where they can; digit passes over the splat index: ceil(bits(K - 1) / 8)
+      long_sort(2048, maxL <= 4096 ? 4096 : (maxL <= 8192 ? 8192 : 16384));
     }
-    if (maxL > 16384)
+    if (dyn && maxL > 16384) {  // tiles longer than 16384, listed on the device, one persistent CTA per SM
+      cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
+      k_long_tiles<<<(T + 255) / 256, 256, 0, st>>>(T, 16384, (int64_t)1 << 62, starts, w.tile_cnt, w.dev_i64, ovf);
+      k_tile_sort_global<<<148, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,
+                                               pos_of, nonmono, qsorted, ovf, w.tile_cnt, w.dev_i64);
+    } else if (maxL > 16384) {
       k_tile_sort_global<<<T, 1024, 0, st>>>(T, 16384, starts, keys, tiles_x, w.br, splat_off, md, gscratch, items,
-                                             pos_of, nonmono, qsorted);
+                                             pos_of, nonmono, qsorted, ovf, nullptr, nullptr);
+    }
   }
 }

@@ -665,7 +665,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, bool clip_stops,
     const int64_t* __restrict__ item_off,
     uint32_t* __restrict__ pair_bits, float4* __restrict__ pair_rec, float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
-    float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend) {
+    float* __restrict__ color_map, int32_t* __restrict__ n_proc, int32_t* __restrict__ n_blend,
+    const int* __restrict__ ovf) {
+  if (ovf && *ovf) return;  // the view overflowed its capacities (sync-free path): re-run by the caller
   extern __shared__ __align__(16) unsigned char smem_raw[];
   FwdSmem& F = *reinterpret_cast<FwdSmem*>(smem_raw);
   if (threadIdx.x == 0) F.npairs = 0;
@@ -954,9 +956,9 @@ __global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const
                                                        double far_, int32_t* __restrict__ witems,
                                                        const SplatRec* __restrict__ recs, int32_t* __restrict__ cnt,
                                                        int32_t* __restrict__ widx_s, double* __restrict__ wz_s,
-                                                       bool q_ready) {
+                                                       bool q_ready, const int* __restrict__ ovf) {
   const int t = blockIdx.x;
-  if (t >= T) return;
+  if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
   const uint8_t flag = nonmono[t];
   const bool nm = flag != 0;
@@ -1196,7 +1198,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows,
-    float* __restrict__ status) {
+    float* __restrict__ status, const int* __restrict__ ovf) {
+  if (ovf && *ovf) {  // an overflowed sync-free view: flagged for the step's Adam guard
+    if (status && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(status + 2, 1.0f);
+    return;
+  }
   using SM = BwdSmem<COLOR>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& S = *reinterpret_cast<SM*>(smem_raw);
@@ -1385,7 +1391,10 @@ __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const float* __rest
                                                const int32_t* __restrict__ vert_ids,
                                                const int32_t* __restrict__ tet_ids, const double* __restrict__ fsc,
                                                const double* __restrict__ deform, Grid G, Camera cam,
-                                               float* __restrict__ d_vert, float* __restrict__ d_color) {
+                                               float* __restrict__ d_vert, float* __restrict__ d_color,
+                                               const int64_t* __restrict__ Kdev, const int* __restrict__ ovf) {
+  if (ovf && *ovf) return;
+  if (Kdev) K = min(K, *Kdev);
   constexpr int NQ = COLOR ? 6 : 5;  // float4s of a row that carry data
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
     float a[4 * NQ];
@@ -1500,7 +1509,9 @@ static void put_tmp(T* p, const T* given, cudaStream_t st) {
 // q_ready: scr->cnt already holds each position's depth key (written by the sort)
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int64_t M, const double* md, int n_w,
                                 double near_, double far_, const SplatRec* rec, int64_t* item_off, cudaStream_t st,
-                                const ViewScratch* scr, bool q_ready) {
+                                const ViewScratch* scr, bool q_ready, const Dyn* dyn, const int64_t* M_dev) {
+  // dyn (sync-free): M is the capacity, M_dev the device count; item_off[M] (capacity index)
+  // receives the pair total, nothing is read back (returns -1)
   const ViewScratch none{};
   const ViewScratch& sc = scr ? *scr : none;
   const int T = tiles_x * tiles_y;
@@ -1512,9 +1523,17 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   double* wz = take_tmp(sc.wz, M, st);
   int32_t* cnt = take_tmp(sc.cnt, M, st);
   int64_t* scratch = take_tmp(sc.scan, compact_blocks(M), st);
+  const int* ovf = dyn ? dyn->ovf : nullptr;
   k_window_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, rec,
-                                     cnt, widx, wz, q_ready && sc.cnt);
-  scan_counts(cnt, M, item_off, scratch, st);
+                                     cnt, widx, wz, q_ready && sc.cnt, ovf);
+  scan_counts(cnt, M, item_off, scratch, st, dyn ? M_dev : nullptr, ovf);
+  if (dyn) {
+    put_tmp(widx, sc.widx, st);
+    put_tmp(wz, sc.wz, st);
+    put_tmp(cnt, sc.cnt, st);
+    put_tmp(scratch, sc.scan, st);
+    return -1;
+  }
   int64_t total = 0;
   cudaMemcpyAsync(&total, item_off + M, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   put_tmp(widx, sc.widx, st);
@@ -1528,8 +1547,10 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
 void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec* rec, const float* colors,
                      const Scene64& S64, int W, int H, double s, double t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
-                     float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st, const ViewScratch* scr) {
+                     float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st, const ViewScratch* scr,
+                     const Dyn* dyn) {
   const int T = tiles_x * tiles_y;
+  const int* ovf = dyn ? dyn->ovf : nullptr;
   int32_t* const given_order = scr ? scr->torder : nullptr;
   cudaMemsetAsync(pair_bits, 0, sizeof(uint32_t) * (size_t)TS_PAIR_BIT_WORDS(n_pairs), st);
   const int smem = (int)sizeof(FwdSmem), smem_ws = (int)sizeof(WsSmem);
@@ -1549,23 +1570,23 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
       k_forward_ws<true><<<T, kWsThreads, smem_ws, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors,
                                                          S64, tiles_x, W, H, (float)s, s, (float)t_stop, clip_stops,
                                                          item_off, pair_bits, pair_rec, nmap, dmap, omap, cmap, n_proc,
-                                                         n_blend);
+                                                         n_blend, ovf);
     else
       k_forward_ws<false><<<T, kWsThreads, smem_ws, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec,
                                                           nullptr, S64, tiles_x, W, H, (float)s, s, (float)t_stop,
                                                           clip_stops, item_off, pair_bits, pair_rec, nmap, dmap, omap,
-                                                          nullptr, n_proc, n_blend);
+                                                          nullptr, n_proc, n_blend, ovf);
     put_tmp(torder, given_order, st);
     return;
   }
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
                                                 W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
-                                                nmap, dmap, omap, cmap, n_proc, n_blend);
+                                                nmap, dmap, omap, cmap, n_proc, n_blend, ovf);
   else
     k_forward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
                                                  tiles_x, W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
-                                                 nmap, dmap, omap, nullptr, n_proc, n_blend);
+                                                 nmap, dmap, omap, nullptr, n_proc, n_blend, ovf);
   put_tmp(torder, given_order, st);
 }
 
@@ -1575,7 +1596,8 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
                       const uint32_t* pair_bits, const float4* pair_rec, const float* maps[4],
                       const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
                       const ViewScratch* scr, float* status, const int32_t* tiles, int n_tiles,
-                      float* rows_out) {
+                      float* rows_out, const Dyn* dyn) {
+  const int* ovf = dyn ? dyn->ovf : nullptr;
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
   const int smem_c = (int)sizeof(BwdSmem<true>), smem = (int)sizeof(BwdSmem<false>);
@@ -1602,12 +1624,12 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
     k_backward<true><<<nblk, TS_TILE_PX, smem_c, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                  maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
-                                                 dmaps[3], n_proc, rows, status);
+                                                 dmaps[3], n_proc, rows, status, ovf);
   else
     k_backward<false><<<nblk, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
                                                   cam.width, cam.height, item_off, pair_bits, pair_rec,
                                                   maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
-                                                  nullptr, n_proc, rows, status);
+                                                  nullptr, n_proc, rows, status, ovf);
   if (rows_out) {
     put_tmp(torder, given_order, st);
     return;
@@ -1616,10 +1638,10 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (color)
     k_chain<true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform,
-                                          make_grid(R), cam, d_vert, d_color);
+                                          make_grid(R), cam, d_vert, d_color, dyn ? dyn->K : nullptr, ovf);
   else
     k_chain<false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform,
-                                           make_grid(R), cam, d_vert, nullptr);
+                                           make_grid(R), cam, d_vert, nullptr, dyn ? dyn->K : nullptr, ovf);
   put_tmp(rows, given_rows, st);
   put_tmp(torder, given_order, st);
 }

@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(kWsThreads, WS_MINB) k_forward_ws(
     bool clip_stops, const int64_t* __restrict__ item_off, uint32_t* __restrict__ pair_bits,
     float4* __restrict__ pair_rec, float* __restrict__ normal_map, float* __restrict__ depth_map,
     float* __restrict__ opacity_map, float* __restrict__ color_map, int32_t* __restrict__ n_proc,
-    int32_t* __restrict__ n_blend) {
+    int32_t* __restrict__ n_blend, const int* __restrict__ ovf) {
+  if (ovf && *ovf) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WsSmem& S = *reinterpret_cast<WsSmem*>(smem_raw);
   const int tile = torder[blockIdx.x];

@@ -42,6 +42,15 @@ struct ViewScratch {
   float* rows = nullptr;     // [kGr * M] per-(tile, splat) gradient rows
 };
 
+// Sync-free per-view path: device-side counts instead of host round trips.  Buffers are
+// sized by host capacities; K = the visible splats (written by the scene build), ovf = set
+// when the view needs more than the capacities (every later kernel of the view then exits
+// and the caller re-runs the view with larger buffers).
+struct Dyn {
+  const int64_t* K = nullptr;
+  const int* ovf = nullptr;
+};
+
 struct BinsView {
   const int64_t* starts;
   const int64_t* splat_off;
@@ -58,25 +67,29 @@ int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_
 int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, const ts::Camera& cam, double s,
                             const int32_t* active, int64_t n_active, const ts::SceneOut& out, int64_t* scratch,
                             cudaStream_t st);
+int64_t* ts_impl_build_scene_dev(const double* sdf, const double* deform, int R, const ts::Camera& cam, double s,
+                                 const int32_t* active, int64_t n_active, const ts::SceneOut& out, int64_t* scratch,
+                                 cudaStream_t st);
 void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths, const double* f,
                              const double* normals, const double* md, const double* bbox, int width, int height,
                              ts::SplatRec* rec, cudaStream_t st);
 void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tiles_x, int tiles_y, double near_,
                        double far_, const ts::BinWork& w, int64_t* starts, int64_t* splat_off, int64_t* M_out,
-                       int64_t* maxL_out, cudaStream_t st);
+                       int64_t* maxL_out, cudaStream_t st, const ts::Dyn* dyn = nullptr);
 void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const ts::BinWork& w,
                       const int64_t* starts, const int64_t* splat_off, int64_t maxL, uint64_t* keys,
                       uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st,
-                      uint32_t* qsorted = nullptr);
+                      uint32_t* qsorted = nullptr, const ts::Dyn* dyn = nullptr);
 void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n);
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, const double* md,
                                 int n_w, double near_, double far_, const ts::SplatRec* rec, int64_t* item_off,
-                                cudaStream_t st, const ts::ViewScratch* scr = nullptr, bool q_ready = false);
+                                cudaStream_t st, const ts::ViewScratch* scr = nullptr, bool q_ready = false,
+                                const ts::Dyn* dyn = nullptr, const int64_t* M_dev = nullptr);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
                      const ts::Scene64& S64, int W, int H, double s, double t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,
                      float* cmap, int32_t* n_proc, int32_t* n_blend, cudaStream_t st,
-                     const ts::ViewScratch* scr = nullptr);
+                     const ts::ViewScratch* scr = nullptr, const ts::Dyn* dyn = nullptr);
 void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, int64_t K,
                       const ts::SplatRec* rec, const float* colors, const double* fsc, const int32_t* vert_ids,
                       const int32_t* tet_ids, const double* deform, int R, const ts::Camera& cam,
@@ -84,7 +97,8 @@ void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M
                       const float* maps[4], const float* dmaps[4],
                       const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
                       const ts::ViewScratch* scr = nullptr, float* status = nullptr,
-                      const int32_t* tiles = nullptr, int n_tiles = 0, float* rows_out = nullptr);
+                      const int32_t* tiles = nullptr, int n_tiles = 0, float* rows_out = nullptr,
+                      const ts::Dyn* dyn = nullptr);
 void ts_impl_list_flags(int T, const int64_t* starts, const int32_t* items, const double* md, double near_,
                         double far_, uint8_t* flags, cudaStream_t st);
 void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W, int H, const ts::BinsView& b,

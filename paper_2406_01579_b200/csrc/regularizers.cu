@@ -363,9 +363,10 @@ __global__ void __launch_bounds__(256) k_adam(int64_t N, const float4* __restric
                                               double b2, double c1, double c2, double eps, double limit,
                                               const float* __restrict__ status) {
   // status (nullable): [0] non-finite map gradients seen by the backward, [1] non-finite
-  // gradient entries (k_finite_check) — the update is skipped and the caller raises
+  // gradient entries (k_finite_check), [2] overflowed sync-free views — the update is skipped
+  // and the caller raises (or re-runs the step)
   // (raster.py:209-211, fit.py:209-212 check before opt.step)
-  if (status && (status[0] != 0.f || status[1] != 0.f)) return;
+  if (status && (status[0] != 0.f || status[1] != 0.f || status[2] != 0.f)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 g = g4[i];
     const double gs[4] = {(double)g.x, (double)g.y, (double)g.z, (double)g.w};

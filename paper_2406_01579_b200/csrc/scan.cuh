@@ -208,16 +208,21 @@ inline int64_t compact_blocks(int64_t n, int ipt = kItemsPerThread) {
 static __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int32_t* __restrict__ in, int64_t n,
                                                                int64_t* __restrict__ out,
                                                                unsigned long long* __restrict__ status,
-                                                               unsigned long long* __restrict__ ticket, int64_t nb) {
+                                                               unsigned long long* __restrict__ ticket, int64_t nb,
+                                                               const int64_t* __restrict__ n_dev,
+                                                               const int* __restrict__ ovf) {
   __shared__ int64_t ws[kScanThreads / 32];
   __shared__ long long pre_s;
   const int tile = lb_tile(ticket);
+  // n_dev (nullable): the valid count on the device (entries [n_dev, n) count as 0);
+  // ovf (nullable): the view overflowed its capacities — nothing to scan
+  const int64_t nv = ovf && *ovf ? 0 : (n_dev ? min(n, *n_dev) : n);
   const int64_t my = (int64_t)tile * kChunk + (int64_t)threadIdx.x * kItemsPerThread;
   int32_t v[kItemsPerThread];
   int64_t loc = 0;
 #pragma unroll
   for (int k = 0; k < kItemsPerThread; ++k) {
-    v[k] = (my + k < n) ? in[my + k] : 0;
+    v[k] = (my + k < nv) ? in[my + k] : 0;
     loc += v[k];
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -249,8 +254,10 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan_lb(const int32_t* 
   if (tile == nb - 1 && threadIdx.x == kScanThreads - 1) out[n] = run;
 }
 
-// scratch needs compact_blocks(n) int64 entries
-inline void scan_counts(const int32_t* in, int64_t n, int64_t* out, int64_t* scratch, cudaStream_t st) {
+// scratch needs compact_blocks(n) int64 entries.  n_dev / ovf (device, nullable): see k_scan_lb;
+// out[0, n] is written either way (out[n] = the total).
+inline void scan_counts(const int32_t* in, int64_t n, int64_t* out, int64_t* scratch, cudaStream_t st,
+                        const int64_t* n_dev = nullptr, const int* ovf = nullptr) {
   const int64_t nb = (n + kChunk - 1) / kChunk;
   if (nb == 0) {
     cudaMemsetAsync(out, 0, sizeof(int64_t), st);
@@ -258,7 +265,8 @@ inline void scan_counts(const int32_t* in, int64_t n, int64_t* out, int64_t* scr
   }
   cudaMemsetAsync(scratch, 0, sizeof(int64_t) * (nb + 1), st);
   k_scan_lb<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, out, reinterpret_cast<unsigned long long*>(scratch),
-                                                   reinterpret_cast<unsigned long long*>(scratch + nb), nb);
+                                                   reinterpret_cast<unsigned long long*>(scratch + nb), nb, n_dev,
+                                                   ovf);
 }
 
 }  // namespace ts

@@ -256,6 +256,15 @@ int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, cons
   return h;
 }
 
+// sync-free variant: the visible-splat count stays on the device (the returned pointer lives
+// in `scratch`, valid until the next user of the scratch)
+int64_t* ts_impl_build_scene_dev(const double* sdf, const double* deform, int R, const Camera& cam, double s,
+                                 const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
+                                 cudaStream_t st) {
+  CullF f{active, sdf, deform, make_grid(R), cam, s, out};
+  return compact_state<CullF>(n_active, f, scratch, st);
+}
+
 void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths, const double* f,
                              const double* normals, const double* md, const double* bbox, int width, int height,
                              SplatRec* rec, cudaStream_t st) {

@@ -6,6 +6,11 @@
 //                    C++ (microseconds), not between Python calls.
 // ts_view_backward = render_backward (K7) + vertex chain into the shared gradient buffer,
 //                    reading the saved state the last ts_view_forward left in the workspace.
+// With capacities set (ts_workspace_set_caps) the forward is SYNC-FREE: buffers are sized by
+// the capacities (visible splats <= active tets, tile pairs <= cap_M, pixel pairs <= cap_P),
+// every count stays on the device (Dyn), and a view that needs more sets the workspace's
+// overflow flag — all its later kernels exit, the caller reads ts_view_status at its next
+// sync, grows the capacities and re-runs the view.
 // The fine-grained entry points in abi.cu stay for reference-style use (and tests).
 #include <cstring>
 
@@ -48,7 +53,12 @@ struct ts_workspace {
   Buf item_off, pair_bits, pair_rec, n_proc, n_blend;
   // per-view temporaries (kept so no view in flight allocates from the shared pool)
   Buf widx, wz, pcnt, pscan, torder, rows;
-  // view description of the last forward
+  // sync-free path: capacities (0 = sizing syncs), device counts {K, M, P, maxL} + overflow flag
+  Buf need, ovf;
+  int64_t capM = 0, capP = 0, capL = 0;
+  int64_t* need_out = nullptr;  // caller's device int64[5] receiving {K, M, P, max list, overflow}
+  bool dyn = false;
+  // view description of the last forward (capacities on the sync-free path)
   int64_t K = 0, M = 0, P = 0, maxL = 0;
   int tiles_x = 0, tiles_y = 0, R = 0;
   Camera cam{};
@@ -74,19 +84,100 @@ static Camera cam_of(const ts_camera* c) {
   return k;
 }
 
+namespace ts {
 __global__ void k_gather_colors(int64_t K, const int32_t* __restrict__ tet_ids, const float* __restrict__ ctet,
-                                float* __restrict__ out) {
+                                float* __restrict__ out, const int64_t* __restrict__ Kdev) {
+  if (Kdev) K = min(K, *Kdev);
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x)
     for (int c = 0; c < 3; ++c) out[k * 3 + c] = ctet[(int64_t)tet_ids[k] * 3 + c];
 }
+
+// a count the sync-free path produced on the device: recorded, and the overflow flag raised
+// when it exceeds its capacity; the last check also copies {K, M, P, max list, overflow} to
+// the caller's slot (ts_workspace_set_caps) when there is one
+__global__ void k_caps_check(const int64_t* __restrict__ total, int64_t cap, int* __restrict__ ovf,
+                             int64_t* __restrict__ need_slot, const int64_t* __restrict__ extra,
+                             int64_t* __restrict__ extra_slot, int64_t extra_cap, const int64_t* __restrict__ need,
+                             int64_t* __restrict__ out5) {
+  const int64_t v = *total;
+  *need_slot = v;
+  int o = v > cap;
+  if (extra) {
+    *extra_slot = *extra;
+    o |= *extra > extra_cap;
+  }
+  if (o) atomicOr(ovf, 1);
+  if (out5) {
+    for (int i = 0; i < 4; ++i) out5[i] = need[i];
+    out5[4] = *ovf;
+  }
+}
+}  // namespace ts
 
 extern "C" {
 
 ts_workspace* ts_workspace_create(void) { return new ts_workspace(); }
 
+int ts_workspace_set_caps(ts_workspace* ws, int64_t cap_M, int64_t cap_P, int64_t cap_L, int64_t* need_out) {
+  if (!ws || cap_M < 0 || cap_P < 0 || cap_L < 0) return ws_fail(TS_EINVAL, "ts_workspace_set_caps: bad arguments");
+  ws->capM = cap_M;
+  ws->capP = cap_P;
+  ws->capL = cap_L;
+  ws->need_out = need_out;
+  return TS_OK;
+}
+
+int ts_view_status(ts_workspace* ws, int64_t* out5, void* stream) {
+  if (!ws || !out5) return ws_fail(TS_EINVAL, "ts_view_status: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!ws->dyn) {
+    out5[0] = 0;
+    out5[1] = ws->K;
+    out5[2] = ws->M;
+    out5[3] = ws->P;
+    out5[4] = ws->maxL;
+    return TS_OK;
+  }
+  int h = 0;
+  int64_t n[4] = {0, 0, 0, 0};
+  cudaMemcpyAsync(&h, ws->ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(n, ws->need.p, sizeof(n), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(cudaGetLastError()));
+  out5[0] = h;
+  for (int i = 0; i < 4; ++i) out5[1 + i] = n[i];
+  return TS_OK;
+}
+
+__global__ void k_view_collect(const int64_t* __restrict__ need, const int* __restrict__ ovf, float* status,
+                               int64_t* __restrict__ out) {
+  const int o = ovf ? *ovf : 0;
+  if (o && status) atomicAdd(status + 2, 1.0f);
+  for (int i = 0; i < 4; ++i) out[i] = need ? need[i] : 0;
+  out[4] = o;
+}
+
+int ts_view_collect(ts_workspace* ws, float* status, int64_t* out5, void* stream) {
+  if (!ws || !out5) return ws_fail(TS_EINVAL, "ts_view_collect: bad arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (ws->dyn)
+    k_view_collect<<<1, 1, 0, st>>>(reinterpret_cast<int64_t*>(ws->need.p), reinterpret_cast<int*>(ws->ovf.p), status,
+                                    out5);
+  else {
+    const int64_t h[5] = {ws->K, ws->M, ws->P, ws->maxL, 0};
+    cudaMemcpyAsync(out5, h, sizeof(h), cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);  // h is a stack buffer (sizing path: the host already waited)
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TS_OK : ws_fail(TS_ECUDA, cudaGetErrorString(e));
+}
+
+// device pointers of the last forward's {K, M, P, maxL} (int64) and overflow flag (int32)
+const int64_t* ts_view_need(ts_workspace* ws) { return ws ? reinterpret_cast<int64_t*>(ws->need.p) : nullptr; }
+const int32_t* ts_view_overflow(ts_workspace* ws) { return ws ? reinterpret_cast<int32_t*>(ws->ovf.p) : nullptr; }
+
 void ts_workspace_destroy(ts_workspace* ws) {
   if (!ws) return;
-  Buf* all[] = {&ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
+  Buf* all[] = {&ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
                 &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
                 &ws->nonmono, &ws->witems, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
                 &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
@@ -95,6 +186,107 @@ void ts_workspace_destroy(ts_workspace* ws) {
   for (Buf* b : all)
     if (b->p) cudaFree(b->p);
   delete ws;
+}
+
+// the sync-free forward (see the file comment)
+static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* deform, int32_t R, const Camera& cam,
+                            double s, const int32_t* active, int64_t n_active, int32_t n_w, double t_stop,
+                            const float* colors_tet, float* nmap, float* dmap, float* omap, float* cmap,
+                            int64_t* out_counts, cudaStream_t st) {
+  const int tx = (cam.width + TS_TILE - 1) / TS_TILE, ty = (cam.height + TS_TILE - 1) / TS_TILE;
+  const int64_t T = (int64_t)tx * ty, HW = (int64_t)cam.width * cam.height;
+  const int64_t cap = n_active > 0 ? n_active : 1, capM = ws->capM, capP = ws->capP;
+  int64_t* need = ws->need.get<int64_t>(4);
+  int* ovf = ws->ovf.get<int>(1);
+  SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), nullptr,
+              nullptr, ws->f.get<double>(cap * 4), nullptr,
+              ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
+              ws->rec.get<SplatRec>(cap)};
+  const int64_t nmax = cap > T ? (cap > capM ? cap : capM) : (T > capM ? T : capM);
+  int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks(nmax + 1, 1));
+  if (!need || !ovf || !so.tet_ids || !so.rec || !scratch)
+    return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  cudaMemsetAsync(ovf, 0, sizeof(int), st);
+  cudaMemsetAsync(need, 0, 4 * sizeof(int64_t), st);
+  Dyn dyn;
+  dyn.K = need;
+  dyn.ovf = ovf;
+  if (n_active > 0) {
+    const int64_t* dK = ts_impl_build_scene_dev(sdf, deform, R, cam, s, active, n_active, so, scratch, st);
+    cudaMemcpyAsync(need, dK, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);  // the scratch is reused below
+  }
+  // ---- bins (capacity-sized, counts on the device) ----------------------------------------
+  BinWork w;
+  w.br = reinterpret_cast<BinRec*>(ws->br.get<int4>(cap));
+  w.q = ws->q.get<uint32_t>(cap);
+  w.splat_cnt = ws->splat_cnt.get<int32_t>(cap);
+  w.tile_cnt = ws->tile_cnt.get<int32_t>(T);
+  w.scratch = scratch;
+  w.dev_i64 = ws->dev_i64.get<int64_t>(2);
+  int64_t* starts = ws->starts.get<int64_t>(T + 1);
+  int64_t* splat_off = ws->splat_off.get<int64_t>(cap + 1);
+  uint8_t* nonmono = ws->nonmono.get<uint8_t>(T);
+  int32_t* items = ws->items.get<int32_t>(capM);
+  int32_t* pos_of = ws->pos_of.get<int32_t>(capM);
+  int32_t* witems = ws->witems.get<int32_t>(capM);
+  uint64_t* keys = ws->keys.get<uint64_t>(capM);
+  uint64_t* gs = ws->capL > 16384 || ws->capL == 0 ? ws->gsort.get<uint64_t>(2 * capM) : keys;  // unused <= 16384
+  int32_t* pcnt = ws->pcnt.get<int32_t>(capM);
+  int64_t* item_off = ws->item_off.get<int64_t>(capM + 1);
+  int32_t* n_proc = ws->n_proc.get<int32_t>(HW);
+  int32_t* n_blend = ws->n_blend.get<int32_t>(HW);
+  ViewScratch scr;
+  scr.widx = ws->widx.get<int32_t>(capM);
+  scr.wz = ws->wz.get<double>(capM);
+  scr.cnt = pcnt;
+  scr.scan = ws->pscan.get<int64_t>(compact_blocks(capM));
+  scr.torder = ws->torder.get<int32_t>(T);
+  scr.rows = ws->rows.get<float>(24 * cap);
+  uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(capP));
+  float4* prec = ws->pair_rec.get<float4>(capP);
+  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !splat_off || !nonmono || !items ||
+      !pos_of || !witems || !keys || !gs || !pcnt || !item_off || !n_proc || !n_blend || !scr.widx || !scr.wz ||
+      !scr.scan || !scr.torder || !scr.rows || !pbits || !prec)
+    return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  ts_impl_bin_count(cap, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, nullptr, nullptr, st, &dyn);
+  // tile pairs M = starts[T] (and the longest list) recorded; overflow when M > cap_M
+  // (and the longest list: the sort kernels launched are those of lists up to cap_L)
+  const int64_t capL = ws->capL > 0 ? ws->capL : ((int64_t)1 << 40);
+  k_caps_check<<<1, 1, 0, st>>>(starts + T, capM, ovf, need + 1, w.dev_i64 + 1, need + 3, capL, nullptr, nullptr);
+  ts_impl_bin_sort(cap, tx, ty, so.md, w, starts, splat_off, capL, keys, gs, items, pos_of, nonmono, st,
+                   reinterpret_cast<uint32_t*>(pcnt), &dyn);
+  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems};
+  const float* colors = nullptr;
+  if (colors_tet && cmap) {
+    float* c = ws->colors.get<float>(cap * 3);
+    if (!c) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+    k_gather_colors<<<(int)((cap + 255) / 256 < 4096 ? (cap + 255) / 256 : 4096), 256, 0, st>>>(cap, so.tet_ids,
+                                                                                                colors_tet, c, need);
+    colors = c;
+  }
+  // window + pair numbering over the M capacity (the M valid positions scanned)
+  ts_impl_forward_prepare(tx, ty, bv, capM, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr, true, &dyn,
+                          starts + T);
+  k_caps_check<<<1, 1, 0, st>>>(item_off + capM, capP, ovf, need + 2, nullptr, nullptr, 0, need, ws->need_out);
+  ts_impl_forward(tx, ty, bv, so.rec, colors,
+                  Scene64{nullptr, nullptr, so.f, so.bbox, so.vert_ids, deform, make_grid(R), cam}, cam.width,
+                  cam.height, s, t_stop, item_off, capP, pbits, prec, nmap, dmap, omap, colors ? cmap : nullptr,
+                  n_proc, n_blend, st, &scr, &dyn);
+  ws->K = cap;
+  ws->M = capM;
+  ws->P = capP;
+  ws->maxL = -1;
+  ws->tiles_x = tx;
+  ws->tiles_y = ty;
+  ws->R = R;
+  ws->cam = cam;
+  ws->s = s;
+  ws->color = colors != nullptr;
+  ws->valid = true;
+  out_counts[0] = out_counts[1] = out_counts[2] = out_counts[3] = -1;  // on the device: ts_view_collect
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
+  return TS_OK;
 }
 
 int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, int32_t R, const ts_camera* camp,
@@ -112,6 +304,9 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   const int tx = (cam.width + TS_TILE - 1) / TS_TILE, ty = (cam.height + TS_TILE - 1) / TS_TILE;
   const int64_t T = (int64_t)tx * ty, HW = (int64_t)cam.width * cam.height;
   ws->valid = false;
+  ws->dyn = ws->capM > 0 && ws->capP > 0;
+  if (ws->dyn) return view_forward_dyn(ws, sdf, deform, R, cam, s, active, n_active, n_w, t_stop, colors_tet, nmap,
+                                       dmap, omap, cmap, out_counts, st);
   // ---- K2 build_scene ----------------------------------------------------------------------
   const int64_t cap = n_active > 0 ? n_active : 1;
   // no FP64 proj / depths: the forward's exact path re-projects the few splats it needs
@@ -159,7 +354,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
     float* c = ws->colors.get<float>(K * 3);
     if (!c) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
     k_gather_colors<<<(int)((K + 255) / 256 < 4096 ? (K + 255) / 256 : 4096), 256, 0, st>>>(K, so.tet_ids, colors_tet,
-                                                                                            c);
+                                                                                            c, nullptr);
     colors = c;
   }
   // ---- K6 forward ------------------------------------------------------------------------------
@@ -208,6 +403,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   out_counts[0] = K;
   out_counts[1] = M;
   out_counts[2] = P;
+  out_counts[3] = maxL;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
   return TS_OK;
@@ -220,6 +416,9 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
       !dmaps[2])
     return ws_fail(TS_EINVAL, "ts_view_backward: bad arguments");
   if (ws->K == 0 || ws->M == 0) return TS_OK;
+  Dyn dyn;
+  dyn.K = reinterpret_cast<int64_t*>(ws->need.p);
+  dyn.ovf = reinterpret_cast<int*>(ws->ovf.p);
   ViewScratch scr;  // sized by the forward of this view
   scr.torder = reinterpret_cast<int32_t*>(ws->torder.p);
   scr.rows = reinterpret_cast<float*>(ws->rows.p);
@@ -235,7 +434,7 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
                    reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<uint32_t*>(ws->pair_bits.p),
                    reinterpret_cast<float4*>(ws->pair_rec.p), m4, d4,
                    reinterpret_cast<int32_t*>(ws->n_proc.p), d_vert, ws->color ? d_color : nullptr,
-                   reinterpret_cast<cudaStream_t>(stream), &scr, status);
+                   reinterpret_cast<cudaStream_t>(stream), &scr, status, nullptr, 0, nullptr, ws->dyn ? &dyn : nullptr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
   return TS_OK;

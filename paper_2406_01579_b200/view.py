@@ -42,11 +42,12 @@ class ViewRenderer:
                 t_stop: float = T_STOP, colors: torch.Tensor | None = None, out: RenderMaps | None = None,
                 stream=None) -> RenderMaps:
         """Render one view; `active` = int32 prefilter output.  Returns maps (reused buffers
-        unless `out` is given)."""
+        unless `out` is given).  With capacities set (set_caps) no host round trip happens and
+        `counts` is (-1, -1, -1): the counts are on the device (collect)."""
         if n_w < 1:
             raise ValueError("resorting window must be >= 1")
         maps = out if out is not None else self._maps_for(camera.height, camera.width, colors is not None)
-        counts = (ctypes.c_int64 * 3)()
+        counts = (ctypes.c_int64 * 4)()
         col = None if colors is None else colors.to(device=self.device, dtype=torch.float32).contiguous()
         _native.check(self._L.ts_view_forward(
             self._ws, _native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution, camera.abi(),
@@ -54,8 +55,24 @@ class ViewRenderer:
             _native.ptr(maps.normal), _native.ptr(maps.depth), _native.ptr(maps.opacity), _native.ptr(maps.color),
             counts, _native.stream_ptr(stream)))
         self.counts = (counts[0], counts[1], counts[2])
+        self.max_list = counts[3]
         self._last = maps
         return maps
+
+    def set_caps(self, cap_pairs: int = 0, cap_pixel_pairs: int = 0, cap_list: int = 0,
+                 need_out: torch.Tensor | None = None):
+        """Capacities of the sync-free forward (tile pairs M, pixel pairs P, the longest tile
+        list, 0 = unbounded); cap_pairs or cap_pixel_pairs 0 = the sizing path.  need_out
+        (device int64[5]) receives {K, M, P, longest list, overflow} of each later forward."""
+        self._need_out = need_out
+        _native.check(self._L.ts_workspace_set_caps(self._ws, int(cap_pairs), int(cap_pixel_pairs), int(cap_list),
+                                                    _native.ptr(need_out)))
+
+    def collect(self, out5: torch.Tensor, status: torch.Tensor | None = None, stream=None):
+        """Stream-ordered: out5 (device int64[5]) <- {K, M, P, longest list, overflow} of the last
+        forward; status[2] += 1 when it overflowed its capacities."""
+        _native.check(self._L.ts_view_collect(self._ws, _native.ptr(status), _native.ptr(out5),
+                                              _native.stream_ptr(stream)))
 
     def backward(self, field, d_maps: RenderMaps, out: GradientBuffers, maps: RenderMaps | None = None,
                  stream=None, status: torch.Tensor | None = None) -> GradientBuffers:
