@@ -99,7 +99,10 @@ __global__ void k_bin_scatter(int64_t K, const BinRec* __restrict__ br, const ui
       int base = 0;
       if (t >= 0 && (int)lane == leader) base = atomicAdd(&cursor[t], __popc(same));
       base = __shfl_sync(0xffffffffu, base, leader);
-      if (t >= 0) keys[starts[t] + base + __popc(same & ((1u << lane) - 1u))] = key;
+      if (t >= 0) {
+        TS_ASSERT(starts[t] + base + __popc(same & ((1u << lane) - 1u)) < starts[t + 1]);
+        keys[starts[t] + base + __popc(same & ((1u << lane) - 1u))] = key;
+      }
     }
   }
 }
@@ -132,6 +135,7 @@ __device__ __forceinline__ void emit_sorted(uint64_t key, int64_t p, int tile, i
   BinRec b = br[k];
   int tx = tile % tiles_x, ty = tile / tiles_x;
   int local = (ty - b.ty0) * b.nx + (tx - b.tx0);
+  TS_ASSERT(local >= 0 && splat_off[k] + local < splat_off[k + 1]);
   pos_of[splat_off[k] + local] = (int32_t)p;
 }
 

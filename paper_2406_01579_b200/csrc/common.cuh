@@ -12,6 +12,24 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Bounds assertions of the checked build (tools/ab_build.py checked:TS_BOUNDS_CHECKS=1; the
+// pool has no compute-sanitizer): a violated index prints its site and traps the context.
+#ifdef TS_BOUNDS_CHECKS
+#include <cstdio>
+#define TS_ASSERT(cond)                                                                     \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("TS_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                           \
+      asm volatile("trap;");                                                                \
+    }                                                                                       \
+  } while (0)
+#else
+#define TS_ASSERT(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 #define TS_TILE 16
 #define TS_TILE_PX (TS_TILE * TS_TILE)
 

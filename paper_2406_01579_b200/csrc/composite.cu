@@ -619,6 +619,7 @@ struct FwdSmem {
   uint32_t cbits[kCap / 32];  // the chunk's blend bits (pair index within the chunk)
   int nex;
   unsigned npairs;  // diagnostics (flag bit 4): pairs evaluated by phase A
+  int64_t pair_end;  // checked build: end of the tile's pair range
   RectTab R;
   Prefetch pf;
   long long phase[8];  // diagnostics (flag bit 2)
@@ -628,6 +629,8 @@ struct FwdSmem {
 // word (flushed to pair_bits after the exact re-decisions), global pair record (backward)
 __device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, const Blend& b, int64_t ib0,
                                          float4* __restrict__ pair_rec) {
+  TS_ASSERT(it >= 0 && it < F.R.pre[F.R.n] && j >= 0 && j < F.R.n && q >= 0 && q < TS_TILE_PX);
+  TS_ASSERT(ib0 + it < F.pair_end);
   const float2 c = encode(true, b);
   F.code[it] = c;
   mask_set(&F.bmask[q], j);
@@ -649,7 +652,9 @@ __device__ __forceinline__ void a2_candidates(FwdSmem& F, const uint16_t* cq, in
     Blend b;
     const int e = blend_fast(r, (float)(px_ - r.rx0) + 0.5f, (float)(py_ - r.ry0) + 0.5f, s, c >> 11, b);
     if (e == 2) {
-      F.exq[atomicAdd(&F.nex, 1)] = (uint16_t)itc;
+      const int slot = atomicAdd(&F.nex, 1);
+      TS_ASSERT(slot < kCap);
+      F.exq[slot] = (uint16_t)itc;
       prefetch_exact(S64, r.k);
     } else if (e == 1) {
       put_pair(F, itc, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
@@ -691,6 +696,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   const int64_t lo = starts[tile];
   const int L = (int)(starts[tile + 1] - lo);
   const int32_t* list = (nonmono[tile] ? witems : items) + lo;
+#ifdef TS_BOUNDS_CHECKS
+  if (threadIdx.x == 0) F.pair_end = item_off[lo + L];
+#endif
   float T = 1.f;
   Accum<COLOR> acc;
   acc.zero();
@@ -938,6 +946,7 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_saved_records(
       continue;
     if (xi < x0 || xi >= x0 + nx || yi < y0 || yi >= y0 + c / nx) continue;
     const int64_t g = item_off[lo + j] + (int64_t)(yi - y0) * nx + (xi - x0);
+    TS_ASSERT(g < item_off[lo + j + 1]);
     if (!pair_bit(pair_bits, g)) continue;
     const float4 r = pair_rec[g];
     idx_out[o] = k;
@@ -1129,6 +1138,7 @@ struct BwdSmem {
   Prefetch pf;
   long long phase[8];  // diagnostics (flag bit 2)
   int maxproc, nitems;
+  int64_t pair_end;  // checked build: end of the tile's pair range
 };
 
 // occupancy the launch bounds assume (228 KB shared memory per SM, 1 KB reserved per CTA)
@@ -1219,6 +1229,10 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   const int32_t* list = (nonmono[tile] ? witems : items) + lo;
   const int64_t p = inside ? (int64_t)yi * W + xi : 0;
   const int nproc = inside ? n_proc[p] : 0;
+#ifdef TS_BOUNDS_CHECKS
+  if (threadIdx.x == 0) S.pair_end = item_off[starts[tile + 1]];
+  TS_ASSERT(nproc >= 0 && nproc <= starts[tile + 1] - lo);
+#endif
   if (threadIdx.x == 0) S.maxproc = 0;
   S.lim[pix] = nproc;
   __syncthreads();
@@ -1292,6 +1306,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
             pair_pixel(S.R, j, it, px_, py_);
             const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
             if (base + j < S.lim[q]) {  // past the pixel's early stop: not composited
+              TS_ASSERT(ib0 + it < S.pair_end && it < kCap && j < S.R.n);
               cp_async8(&S.wg[it], pair_rec + ib0 + it);
               mask_set(&S.u.bmask[q], j);
               bl = true;
@@ -1411,6 +1426,8 @@ __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const float* __rest
     }
     const int4 vv = __ldg(reinterpret_cast<const int4*>(vert_ids) + k);
     const uint32_t vid[4] = {(uint32_t)vv.x, (uint32_t)vv.y, (uint32_t)vv.z, (uint32_t)vv.w};
+    TS_ASSERT(vid[0] < (uint32_t)(G.n * G.n * G.n) && vid[1] < (uint32_t)(G.n * G.n * G.n) &&
+              vid[2] < (uint32_t)(G.n * G.n * G.n) && vid[3] < (uint32_t)(G.n * G.n * G.n));
     const double2 fa = __ldg(reinterpret_cast<const double2*>(fsc) + 2 * k);
     const double2 fb = __ldg(reinterpret_cast<const double2*>(fsc) + 2 * k + 1);
     float e[3][3], pcs[4][3];

@@ -150,10 +150,12 @@ __device__ __forceinline__ void ws_producer(WsSmem& S, const int32_t* __restrict
 __device__ __forceinline__ void ws_put(WsWarp& Wp, const WsSlot& sl, int it, int j, int q, int px, int py,
                                        const Blend& b, uint32_t* __restrict__ pair_bits,
                                        float4* __restrict__ pair_rec) {
+  TS_ASSERT(it >= 0 && it < kWsCap && j >= 0 && j < sl.n && q >= 0 && q < 32);
   const float2 c = encode(true, b);
   Wp.code[it] = c;
   atomicOr(&Wp.bmask[q], 1u << j);
   const long long g = sl.ib[j] + (long long)(py - sl.ty0[j]) * sl.tnx[j] + (px - sl.tx0[j]);
+  TS_ASSERT(py >= sl.ty0[j] && px >= sl.tx0[j] && px < sl.tx0[j] + sl.tnx[j]);
   pair_rec[g] = make_float4(c.x, c.y, pack_face(b.sp, b.fip), pack_face(b.sn, b.fin));
   atomicOr(pair_bits + (g >> 5), 1u << (g & 31));
 }

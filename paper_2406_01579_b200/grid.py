@@ -73,6 +73,27 @@ class TetrahedralGrid:
         return np.stack(per, axis=1).reshape(-1, 4)
 
 
+def tet_vertex_ids(grid: TetrahedralGrid, tets: torch.Tensor) -> torch.Tensor:
+    """(n,4) int64 vertex ids of the tets `tets` (device), the implicit formula of tets_numpy
+    (grid.py:86-117) evaluated on the device."""
+    R, n = grid.resolution, grid.resolution + 1
+    t = tets.to(torch.int64)
+    cell, p = t // 6, t % 6
+    ix, iy, iz = cell // (R * R), (cell // R) % R, cell % R
+    corners = torch.zeros((6, 4, 3), dtype=torch.int64, device=t.device)
+    for pi, perm in enumerate(AXIS_PERMS):
+        c = corners[pi]
+        c[1, perm[0]] = 1
+        c[2] = c[1]
+        c[2, perm[1]] = 1
+        c[3] = 1
+        if pi in (1, 2, 5):
+            c[[2, 3]] = c[[3, 2]].clone()
+    off = corners[p]  # (n,4,3)
+    x, y, z = ix[:, None] + off[..., 0], iy[:, None] + off[..., 1], iz[:, None] + off[..., 2]
+    return x + n * y + n * n * z
+
+
 def build_grid(resolution: int) -> TetrahedralGrid:
     """grid.py:64-117 (implicit: O(1) instead of the reference's 21-230 s at R=128-256)."""
     return TetrahedralGrid(int(resolution))

@@ -31,16 +31,43 @@ def prefilter(grid, field, s: float, threshold: float = T_FILTER, stream=None) -
     return out[:n.value]
 
 
+def active_aabb(grid, field, active, margin: float = 0.1) -> np.ndarray:
+    """splat.py:70-74: AABB of the active tets' deformed vertices, padded by margin x extent
+    ((2,3) float64, computed on the device)."""
+    from .grid import tet_vertex_ids
+    act = torch.as_tensor(active, device=field.sdf.device)
+    vid = tet_vertex_ids(grid, act).reshape(-1)
+    pos = field.deformed_positions(grid)[vid]
+    lo, hi = pos.min(dim=0).values, pos.max(dim=0).values
+    pad = margin * (hi - lo)
+    return torch.stack([lo - pad, hi + pad]).cpu().numpy()
+
+
+def rescale_grid_to_box(grid, box) -> np.ndarray:
+    """splat.py:77-83: the rest positions of the grid with the canonical cube mapped affinely
+    onto `box` ((N,3) float64, same vertex order).  The device grid stays the canonical Kuhn
+    grid (connectivity is identical); only positional field functions are sampled here."""
+    lo, hi = (np.asarray(b, dtype=np.float64) for b in box)
+    rest = grid.rest_positions("cpu").numpy()
+    return (rest + 1.0) / 2.0 * (hi - lo) + lo
+
+
 def coarse_to_fine_filter(grid, field, s: float, threshold: float = T_FILTER, margin: float = 0.1,
                           field_fn=None, stream=None):
-    """splat.py:88-109 for direct per-vertex parameters (field_fn=None): the second round
-    is inert, so this is the prefilter plus the survivors' AABB."""
-    if field_fn is not None:
-        raise NotImplementedError("positional field resampling (field_fn) is outside the B200 hot path")
+    """splat.py:88-109: full-grid prefilter, AABB of the survivors (plus margin), and — when
+    `field_fn` (a positional SDF callable) is given — a second prefilter of the field resampled
+    on the grid rescaled to that box.  Returns (active ids, box)."""
     active = prefilter(grid, field, s, threshold, stream)
     if active.numel() == 0:
         raise EmptySceneError("pre-filtering removed every tetrahedron")
-    return active, None
+    box = active_aabb(grid, field, active, margin)
+    if field_fn is not None:
+        from .field import FieldState
+        sdf = np.asarray(field_fn(rescale_grid_to_box(grid, box)), dtype=np.float64)
+        fine = FieldState.from_numpy(sdf, np.zeros((grid.num_vertices, 3)), field.deform_limit,
+                                     device=field.sdf.device)
+        active = prefilter(grid, fine, s, threshold, stream)
+    return active, box
 
 
 @dataclass

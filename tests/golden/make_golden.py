@@ -208,10 +208,28 @@ def main_color_window(ref_src: str):
     print("window K=", len(sc), "M=", len(bins.items), "maxL", bins.max_list_length())
 
 
+def main_c2f(ref_src: str):
+    """coarse_to_fine_filter (splat.py:88-109): box of the survivors, and the second round with
+    a positional field function on the rescaled grid."""
+    sys.path.insert(0, ref_src)
+    from tetsplat import field, grid, splat
+    g = grid.build_grid(12)
+    fs = _noisy(field, g)
+    act, box = splat.coarse_to_fine_filter(g, fs, 100.0)
+    fn = lambda p: np.linalg.norm(p - np.array([0.05, -0.02, 0.01]), axis=1) - 0.4
+    act2, box2 = splat.coarse_to_fine_filter(g, fs, 100.0, field_fn=fn)
+    np.savez_compressed(os.path.join(HERE, "c2f_noisy_r12_s100.npz"), sdf=fs.sdf, deform=fs.deformation, R=12,
+                        s=100.0, active=act, box=box, active_fn=act2, box_fn=box2)
+    print("c2f", len(act), len(act2), box)
+
+
 if __name__ == "__main__":
     src = sys.argv[1] if len(sys.argv) > 1 else "/tmp/tsref/src"
     if "--color-window" in sys.argv:
         main_color_window(src)
+    elif "--c2f" in sys.argv:
+        main_c2f(src)
     else:
         main(src)
         main_color_window(src)
+        main_c2f(src)

@@ -64,3 +64,15 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh")):
                 src = open(os.path.join(dp, f)).read()
                 assert "oracle" not in src.replace("# oracle", ""), f
+
+
+def test_tet_vertex_ids_match_explicit_grid():
+    """grid.tet_vertex_ids (the implicit connectivity evaluated by torch) == tets_numpy
+    == the reference's build_grid tets (fixtures)."""
+    import numpy as np
+    import torch
+    from paper_2406_01579_b200.grid import TetrahedralGrid, tet_vertex_ids
+    for R in (1, 2, 3, 5):
+        g = TetrahedralGrid(R)
+        got = tet_vertex_ids(g, torch.arange(g.num_tets)).numpy()
+        assert np.array_equal(got, g.tets_numpy())

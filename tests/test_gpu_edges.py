@@ -152,3 +152,21 @@ def test_fused_path_rejects_non_finite_map_gradients():
     torch.cuda.synchronize()
     step.check_status()
     assert not torch.equal(f.sdf, sdf0)  # the regularizers move the field
+
+
+def test_coarse_to_fine_filter_box_and_second_round():
+    """splat.py:88-109 against the reference's fixture: the survivors' AABB and, with a
+    positional field function, the second prefilter on the rescaled grid."""
+    import numpy as np
+    import paper_2406_01579_b200 as ts
+    from conftest import load_golden
+    G = load_golden("c2f_noisy_r12_s100.npz")
+    g = ts.build_grid(int(G["R"]))
+    fs = ts.FieldState.from_numpy(G["sdf"], G["deform"], ts.deform_limit_for(g))
+    act, box = ts.coarse_to_fine_filter(g, fs, float(G["s"]))
+    assert np.array_equal(act.cpu().numpy().astype(np.int64), G["active"])
+    assert np.abs(box - G["box"]).max() <= 1e-12
+    fn = lambda p: np.linalg.norm(p - np.array([0.05, -0.02, 0.01]), axis=1) - 0.4
+    act2, box2 = ts.coarse_to_fine_filter(g, fs, float(G["s"]), field_fn=fn)
+    assert np.array_equal(act2.cpu().numpy().astype(np.int64), G["active_fn"])
+    assert np.abs(box2 - G["box_fn"]).max() <= 1e-12
