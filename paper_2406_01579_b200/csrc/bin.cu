@@ -173,6 +173,10 @@ __device__ __forceinline__ void sort_tile(uint64_t* s, int& bad, int t, const in
 // order is (e, lane) = position order and the sort is stable); ranks inside a warp come from
 // __match_any_sync peers and per-warp digit counters, offsets from a digit-major scan of the
 // counters.  O(passes * L) instead of the bitonic O(L log^2 L).
+#ifndef TS_SMEM_SORT_CAP
+#define TS_SMEM_SORT_CAP 4096
+#endif
+constexpr int kSmemSortCap = TS_SMEM_SORT_CAP;  // longest list sorted by one 256-thread CTA (<= 16 x 256)
 constexpr int kRadixThreads = 1024;
 constexpr int kRadixWarps = kRadixThreads / 32;
 
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
   if (L <= 0 || L > cap) return;
-  if (L <= 512 || cap > 8 * THREADS) {  // short lists: bitonic
+  if (L <= 512) {  // short lists: bitonic
     sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono, qsorted);
     return;
   }
@@ -328,7 +332,10 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   uint32_t* kv = kq + cap;
   uint32_t* H = kq + 2 * cap;
   uint32_t* dbase = H + (THREADS / 32) * 256;
-  const int P = L <= 4 * THREADS ? 4 * THREADS : 8 * THREADS;  // cap <= 8 * THREADS
+  // keys per thread: E = ceil(L / THREADS) (>= 3), rounded up to 12 / 16 above 8 (cap <= 16 THREADS)
+  int E = (int)((L + THREADS - 1) / THREADS);
+  E = E < 3 ? 3 : (E <= 8 ? E : (E <= 12 ? 12 : 16));
+  const int P = E * THREADS;
   for (int i = threadIdx.x; i < P; i += THREADS) {
     const uint64_t k = i < L ? keys[lo + i] : ~0ull;
     kq[i] = (uint32_t)(k >> 32);
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   }
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
-  radix_sort_keys<THREADS, 8>(kq, kv, H, dbase, P, (int)L, passes_lo, longrun);
+  radix_sort_keys<THREADS, 16>(kq, kv, H, dbase, P, (int)L, passes_lo, longrun);
   int mybad = 0;
   for (int i = threadIdx.x; i < L; i += THREADS) {
     emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
@@ -531,8 +538,16 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
   if (maxL >= 1) {
     int kbits = 1;  // digit passes over the splat index of a full-key sort: ceil(bits(K - 1) / 8)
     while (kbits < 32 && ((int64_t)1 << kbits) < K) ++kbits;
-    const size_t smem_s = sizeof(uint32_t) * (2 * 2048 + 8 * 256 + 256);  // kq, kv | bitonic u64; H; dbase
-    k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, 2048, (kbits + 7) / 8, starts, keys, tiles_x, w.br, splat_off,
+    // lists up to kSmemSortCap: one 256-thread CTA each (bitonic <= 512, radix above; several CTAs
+    // per SM), longer ones by the 1024-thread persistent k_tile_sort_long
+    const size_t smem_s = sizeof(uint32_t) * (2 * kSmemSortCap + 8 * 256 + 256);  // kq, kv | bitonic u64; H; dbase
+    static const bool attr_s = [] {
+      cudaFuncSetAttribute(k_tile_sort_smem<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(uint32_t) * (2 * kSmemSortCap + 8 * 256 + 256)));
+      return true;
+    }();
+    (void)attr_s;
+    k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, kSmemSortCap, (kbits + 7) / 8, starts, keys, tiles_x, w.br, splat_off,
                                                   md, items, pos_of, nonmono, qsorted, ovf);
     // the attribute is set once, to the 16384-entry cap (a thread-safe static: views in
     // flight launch from several host threads); the launch asks for what it needs
@@ -553,12 +568,12 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
                                                                  (kbits + 7) / 8, qsorted, ovf);
     };
     if (dyn) {
-      if (maxL > 2048) long_sort(2048, 8192);
+      if (maxL > kSmemSortCap) long_sort(kSmemSortCap, 8192);
       if (maxL > 8192) long_sort(8192, 16384);
-    } else if (maxL > 2048) {
+    } else if (maxL > kSmemSortCap) {
       // shared memory sized to the longest list (not the 16384 cap) so two CTAs fit per SM
       // where they can; digit passes over the splat index: ceil(bits(K - 1) / 8)
-      long_sort(2048, maxL <= 4096 ? 4096 : (maxL <= 8192 ? 8192 : 16384));
+      long_sort(kSmemSortCap, maxL <= 4096 ? 4096 : (maxL <= 8192 ? 8192 : 16384));
     }
     if (dyn && maxL > 16384) {  // tiles longer than 16384, listed on the device, one persistent CTA per SM
       cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t), st);
