@@ -965,7 +965,8 @@ __global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const
                                                        double far_, int32_t* __restrict__ witems,
                                                        const SplatRec* __restrict__ recs, int32_t* __restrict__ cnt,
                                                        int32_t* __restrict__ widx_s, double* __restrict__ wz_s,
-                                                       bool q_ready, const int* __restrict__ ovf) {
+                                                       bool q_ready, const int* __restrict__ ovf,
+                                                       const int2* __restrict__ prect) {
   const int t = blockIdx.x;
   if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
@@ -979,7 +980,9 @@ __global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const
   const int tx0 = (t % tiles_x) * TS_TILE, ty0 = (t / tiles_x) * TS_TILE;
   const int32_t* list = nm ? witems : items;
   for (int64_t p = lo + threadIdx.x; p < lo + L; p += blockDim.x) {
-    const int2 rr = *reinterpret_cast<const int2*>(recs + list[p]);
+    // the 8-byte rectangle: from the compact array when the scene build wrote one (one 32-byte
+    // sector holds four), else from the 96-byte record
+    const int2 rr = prect ? __ldg(prect + list[p]) : *reinterpret_cast<const int2*>(recs + list[p]);
     int x0, y0, nx, c = 0;
     tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0, y0, nx,
               c);
@@ -1526,7 +1529,8 @@ static void put_tmp(T* p, const T* given, cudaStream_t st) {
 // q_ready: scr->cnt already holds each position's depth key (written by the sort)
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int64_t M, const double* md, int n_w,
                                 double near_, double far_, const SplatRec* rec, int64_t* item_off, cudaStream_t st,
-                                const ViewScratch* scr, bool q_ready, const Dyn* dyn, const int64_t* M_dev) {
+                                const ViewScratch* scr, bool q_ready, const Dyn* dyn, const int64_t* M_dev,
+                                const int2* prect) {
   // dyn (sync-free): M is the capacity, M_dev the device count; item_off[M] (capacity index)
   // receives the pair total, nothing is read back (returns -1)
   const ViewScratch none{};
@@ -1542,7 +1546,7 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   int64_t* scratch = take_tmp(sc.scan, compact_blocks(M), st);
   const int* ovf = dyn ? dyn->ovf : nullptr;
   k_window_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, rec,
-                                     cnt, widx, wz, q_ready && sc.cnt, ovf);
+                                     cnt, widx, wz, q_ready && sc.cnt, ovf, prect);
   scan_counts(cnt, M, item_off, scratch, st, dyn ? M_dev : nullptr, ovf);
   if (dyn) {
     put_tmp(widx, sc.widx, st);

@@ -15,6 +15,7 @@ struct SceneOut {
   double* amax;       // [K] (nullable)
   double* bbox;       // [K,4]
   SplatRec* rec;      // [K]
+  int2* prect = nullptr;  // [K] (nullable): the record's packed pixel rectangle (rx, ry) alone
 };
 
 struct BinRec {  // 16 B per splat: first tile and tile-rect extent
@@ -84,7 +85,8 @@ void ts_impl_tile_times(unsigned long long* t2, unsigned int* sm, int n);
 int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M, const double* md,
                                 int n_w, double near_, double far_, const ts::SplatRec* rec, int64_t* item_off,
                                 cudaStream_t st, const ts::ViewScratch* scr = nullptr, bool q_ready = false,
-                                const ts::Dyn* dyn = nullptr, const int64_t* M_dev = nullptr);
+                                const ts::Dyn* dyn = nullptr, const int64_t* M_dev = nullptr,
+                                const int2* prect = nullptr);
 void ts_impl_forward(int tiles_x, int tiles_y, const ts::BinsView& b, const ts::SplatRec* rec, const float* colors,
                      const ts::Scene64& S64, int W, int H, double s, double t_stop, const int64_t* item_off,
                      int64_t n_pairs, uint32_t* pair_bits, float4* pair_rec, float* nmap, float* dmap, float* omap,

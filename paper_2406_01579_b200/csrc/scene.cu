@@ -208,6 +208,7 @@ struct CullF {
       out.amax[k] = am;
     }
     out.rec[k] = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height);
+    if (out.prect) out.prect[k] = make_int2(out.rec[k].rx, out.rec[k].ry);
   }
 };
 

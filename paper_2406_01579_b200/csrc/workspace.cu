@@ -46,7 +46,7 @@ struct Buf {
 
 struct ts_workspace {
   // scene
-  Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors;
+  Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors, prect;
   // bins
   Buf starts, splat_off, items, pos_of, nonmono, witems, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
   // forward state
@@ -177,7 +177,7 @@ const int32_t* ts_view_overflow(ts_workspace* ws) { return ws ? reinterpret_cast
 
 void ts_workspace_destroy(ts_workspace* ws) {
   if (!ws) return;
-  Buf* all[] = {&ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
+  Buf* all[] = {&ws->prect, &ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
                 &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
                 &ws->nonmono, &ws->witems, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
                 &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
@@ -201,7 +201,7 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), nullptr,
               nullptr, ws->f.get<double>(cap * 4), nullptr,
               ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
-              ws->rec.get<SplatRec>(cap)};
+              ws->rec.get<SplatRec>(cap), ws->prect.get<int2>(cap)};
   const int64_t nmax = cap > T ? (cap > capM ? cap : capM) : (T > capM ? T : capM);
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks(nmax + 1, 1));
   if (!need || !ovf || !so.tet_ids || !so.rec || !scratch)
@@ -266,7 +266,7 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   }
   // window + pair numbering over the M capacity (the M valid positions scanned)
   ts_impl_forward_prepare(tx, ty, bv, capM, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr, true, &dyn,
-                          starts + T);
+                          starts + T, so.prect);
   k_caps_check<<<1, 1, 0, st>>>(item_off + capM, capP, ovf, need + 2, nullptr, nullptr, 0, need, ws->need_out);
   ts_impl_forward(tx, ty, bv, so.rec, colors,
                   Scene64{nullptr, nullptr, so.f, so.bbox, so.vert_ids, deform, make_grid(R), cam}, cam.width,
@@ -313,7 +313,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   SceneOut so{ws->tet_ids.get<int32_t>(cap), ws->vert_ids.get<int32_t>(cap * 4), nullptr,
               nullptr, ws->f.get<double>(cap * 4), nullptr,
               ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
-              ws->rec.get<SplatRec>(cap)};
+              ws->rec.get<SplatRec>(cap), ws->prect.get<int2>(cap)};
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1, 1));
   if (!so.tet_ids || !so.rec || !scratch) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   const int64_t K = n_active > 0 ? ts_impl_build_scene(sdf, deform, R, cam, s, active, n_active, so, scratch, st) : 0;
@@ -373,7 +373,8 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   if (!scr.widx || !scr.wz || !scr.cnt || !scr.scan || !scr.torder || !scr.rows)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0)
-    P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr, true);
+    P = ts_impl_forward_prepare(tx, ty, bv, M, so.md, n_w, cam.near_, cam.far_, so.rec, item_off, st, &scr, true,
+                                nullptr, nullptr, so.prect);
   uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(P));
   float4* prec = ws->pair_rec.get<float4>(P);
   if (!pbits || !prec) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
