@@ -509,18 +509,35 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
         d["frac_of_fp32_issue"] = d["achieved_Tlaneops"] / fp32_peak
     top = max(kern, key=lambda k: kern[k]["ms"])
     d = kern[top]
-    # DRAM traffic per launch of the same kernel from the committed ncu --set full capture
-    traffic, tsrc = None, None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
+    # the work the GPU algorithm actually executes: the N_w window is replayed once per tile (only
+    # where a list is not mean-depth monotone), not popped per pixel, so the 8 P_pop term of the
+    # SURVEY 8d model is not executed
+    kern["render_forward"]["lane_ops_gpu_executed"] = 120 * P_bbox + 19 * B
+    kern["render_forward"]["frac_gpu_executed"] = (kern["render_forward"]["lane_ops_gpu_executed"] / (tf * 1e-3)
+                                                   / 1e12 / fp32_peak)
+    # DRAM traffic, issue and FMA-pipe utilisation of the same kernel from the committed ncu
+    # --set full capture (profiles/r02_ncu_compositing.json, else the round-1 traffic file)
+    traffic, tsrc, ncu = None, None, None
+    key = {"render_forward": "void k_forward<0>", "render_backward": "void k_backward<0>"}[top]
+    for fname in ("r02_ncu_compositing.json", "ncu_traffic.json"):
+        tfile = os.path.join(ROOT, "profiles", fname)
+        if not os.path.exists(tfile):
+            continue
         tj = json.load(open(tfile))
-        key = {"render_forward": "void k_forward<0>", "render_backward": "void k_backward<0>"}[top]
         if key in tj:
             traffic = tj[key]["dram_bytes_per_launch"]
-            tsrc = f"profiles/{tj[key]['source']} ({key}, dram__bytes_read.sum + dram__bytes_write.sum)"
+            tsrc = f"profiles/{fname} <- {tj[key]['source']} ({key}, dram__bytes_read.sum + dram__bytes_write.sum)"
+            ncu = {k: tj[key][k] for k in ("issue_active_pct", "fma_pipe_pct", "warps_active_pct", "top_stalls_pct")
+                   if k in tj[key]} or None
+            break
     roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_Tlaneops"], "peak": fp32_peak,
             "unit": "T lane-op/s", "frac": d["frac_of_fp32_issue"], "traffic": traffic, "traffic_unit": "bytes/launch",
             "traffic_source": tsrc,
+            "work_model": "SURVEY 8d: 8 P_pop + 120 P_bbox + 19 B lane-ops (forward)",
+            "frac_gpu_executed": kern[top].get("frac_gpu_executed"),
+            "gpu_executed_model": "120 P_bbox + 19 B (no per-pixel window pops: the GPU replays the window once per "
+                                  "non-monotone tile)",
+            "ncu": ncu,
             "peak_source": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FP32 issue, SURVEY 8d; no tensor "
                            f"cores: not a dense contraction; DRAM traffic well under HBM bandwidth)"}
     extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M, "pixel_pairs": P_pairs,
