@@ -250,6 +250,9 @@ int ts_adam_step(int32_t resolution, const float* d_vert, double* sdf, double* d
  * within the f_prev - f_next error bound / near the tiny-alpha or clip bounds, out8[7] =
  * re-decided pairs whose alpha needed the FP64 softplus chain.  [sync] */
 int ts_debug_counters(uint64_t* out8, int reset);
+/* Diagnostics (debug flag 64): out32[0..16) = alpha re-decisions by floor(-log2(|f_prev - f_next|
+ * / bound)), out32[16..32) = edge re-decisions by floor(-log2(|edge value| / band)) (15 = clamp). */
+int ts_debug_hist(uint64_t* out32, int reset);
 
 /* Diagnostics for timing experiments only: bit 0 skips the exact FP64 re-decisions
  * (results then no longer match the reference).  Default 0. */

@@ -77,6 +77,7 @@ def lib():
         "ts_marching_tets_release": ([P], ctypes.c_int),
         "ts_debug_counters": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_set_flags": ([ctypes.c_int], ctypes.c_int),
+        "ts_debug_hist": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_debug_phases": ([ctypes.POINTER(ctypes.c_uint64), ctypes.c_int], ctypes.c_int),
         "ts_workspace_create": ([], P),
         "ts_workspace_destroy": ([P], None),

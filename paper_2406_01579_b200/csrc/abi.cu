@@ -368,6 +368,14 @@ int ts_debug_counters(uint64_t* out8, int reset) {
   return check_cuda("ts_debug_counters");
 }
 
+int ts_debug_hist(uint64_t* out32, int reset) {
+  if (!out32) return fail(TS_EINVAL, "ts_debug_hist: null output");
+  unsigned long long c[32];
+  ts_impl_hist(c, reset);
+  for (int i = 0; i < 32; ++i) out32[i] = c[i];
+  return check_cuda("ts_debug_hist");
+}
+
 int ts_debug_tile_times(uint64_t* t2, uint32_t* sm, int n) {
   if (!t2 || !sm || n < 0 || n > 65536) return fail(TS_EINVAL, "ts_debug_tile_times: bad arguments");
   ts_impl_tile_times(reinterpret_cast<unsigned long long*>(t2), sm, n);

@@ -78,6 +78,10 @@ static_assert(sizeof(Staged) == 208, "Staged must be 208 bytes");
 // |f_prev - f_next| within the FP32 f error bound, alpha below the tiny-alpha bound or near
 // ALPHA_CLIP; [7] re-decided pairs whose alpha needed the FP64 softplus chain
 __device__ unsigned long long g_ts_counters[8];
+// diagnostics only (flag bit 64): histograms of how far inside its error bound a re-decided pair
+// lies — [0,16): alpha pairs by floor(-log2(|f_prev - f_next| / ftol)), [16,32): edge pairs by
+// floor(-log2(|min(u, v, w)| / band)) of the nearest face edge (clamped to 15)
+__device__ unsigned long long g_ts_hist[32];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity),
 // bit 4 = count the pairs phase A evaluates (g_ts_counters[2])
 __device__ int g_ts_debug_flags;
@@ -403,6 +407,13 @@ __device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, f
       }
     }
     atomicAdd(&g_ts_counters[1], 1ull);
+    if (g_ts_debug_flags & 64) {
+      const float dfl = h.fp - h.fn;
+      const float ftol = r.fband * frcp(fminf(r.adet[h.fip], r.adet[h.fin])) + r.ftol0;
+      const float q = fabsf(dfl) / ftol;
+      const int b = q <= 0.f ? 15 : min(15, max(0, (int)floorf(-log2f(q))));
+      atomicAdd(&g_ts_hist[b], 1ull);
+    }
     if (g_ts_debug_flags & 8) {
       const float dfl = h.fp - h.fn;
       const float ftol = r.fband * frcp(fminf(r.adet[h.fip], r.adet[h.fin])) + r.ftol0;
@@ -411,6 +422,19 @@ __device__ __forceinline__ int blend_fast(const Staged& r, float px, float py, f
   } else {
     atomicAdd(&g_ts_counters[0], 1ull);
     if (r.flags & 16u) atomicAdd(&g_ts_counters[3], 1ull);
+    if (g_ts_debug_flags & 64) {  // the edge value nearest the band among the faces
+      float best = 1e30f;
+      for (int fi = 0; fi < 4; ++fi) {
+        const float u = fmaf(r.eux[fi], px, fmaf(r.euy[fi], py, r.cu[fi]));
+        const float v = fmaf(r.evx[fi], px, fmaf(r.evy[fi], py, r.cv[fi]));
+        const float w = r.adet[fi] - u - v;
+        const float mn = fminf(fminf(u, v), w);
+        if (fabsf(mn) <= r.band) best = fminf(best, fabsf(mn));
+      }
+      const float q = best / r.band;
+      const int b = q <= 0.f ? 15 : min(15, max(0, (int)floorf(-log2f(q))));
+      atomicAdd(&g_ts_hist[16 + b], 1ull);
+    }
   }
   return (g_ts_debug_flags & 1) ? 0 : 2;
 }
@@ -1680,6 +1704,14 @@ void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W
   if (n_tiles <= 0) return;
   k_saved_records<<<n_tiles, TS_TILE_PX, 0, st>>>(tiles, tiles_x, W, H, b.starts, b.items, b.witems, b.nonmono, rec,
                                                   item_off, pair_bits, pair_rec, n_proc, rec_off, idx, alpha);
+}
+
+void ts_impl_hist(unsigned long long out[32], int reset) {
+  cudaMemcpyFromSymbol(out, g_ts_hist, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(g_ts_hist, z, sizeof(z));
+  }
 }
 
 void ts_impl_counters(unsigned long long out[8], int reset) {

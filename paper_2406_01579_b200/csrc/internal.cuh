@@ -119,6 +119,7 @@ int ts_impl_mt_fetch(void* handle, double* verts, int64_t* tris);
 void ts_impl_mt_release(void* handle);
 int ts_impl_mt(const double* sdf, const double* deform, int R, double* verts, int64_t* tris, int64_t* nt,
                cudaStream_t st);
+void ts_impl_hist(unsigned long long out[32], int reset);
 void ts_impl_counters(unsigned long long out[8], int reset);
 int ts_impl_rasterize_mesh(const double* verts, int64_t V, const int64_t* tris, int64_t F, const ts::Camera& cam,
                            uint8_t* mask, double* depth, double* normal, cudaStream_t st);
