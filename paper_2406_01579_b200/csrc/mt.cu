@@ -14,7 +14,8 @@
 //   T1  per tet class counts in 2048-tet chunks, scans -> group-ordered output slots
 //   T2  per crossing tet: slot edges, quad diagonal rule (np.isclose + min-parent key),
 //       orientation against the cross-product tet gradient
-//   W   weld: bitonic sort of the crossing vertices by (x, y, z) (order-preserving u64 keys,
+//   W   weld: merge sort (1024-key shared-memory block sorts, then merge-path passes) of the
+//       crossing vertices by (x, y, z) (order-preserving u64 keys,
 //       -0 == +0), group ids by adjacent-difference scan, remap, degenerate filter
 //       (distinct indices and |cross| > 1e-14, FP64 numpy order) and order-preserving
 //       compaction.
@@ -382,34 +383,22 @@ __global__ void k_mt_keys(int64_t V, int64_t P, const double* __restrict__ verts
   }
 }
 
-__global__ void k_mt_bitonic(int64_t P, int64_t kk, int64_t jj, VKey* __restrict__ keys) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = i ^ jj;
-    if (l <= i) continue;
-    const VKey a = keys[i], b = keys[l];
-    const bool asc = (i & kk) == 0;
-    if (vless(b, a) == asc) {
-      keys[i] = b;
-      keys[l] = a;
-    }
-  }
-}
+constexpr int kLocalSort = 1024;  // keys per block of the shared-memory block sort
 
-// all bitonic steps with stride < kLocalSort of merge size kk (kk_lo <= kk <= kk_hi, powers of
-// two), on kLocalSort-key blocks in shared memory (one launch instead of log2 steps each)
-constexpr int kLocalSort = 1024;
-__global__ void __launch_bounds__(kLocalSort / 2) k_mt_bitonic_local(int64_t P, int64_t kk_lo, int64_t kk_hi,
-                                                                    VKey* __restrict__ keys) {
+// Merge sort of the weld keys (replaces the global bitonic network: O(n log n) traffic in
+// log2(P / 1024) merge passes instead of O(n log^2 n) compare-exchange launches).
+// Block sort: every 1024-key block ascending in shared memory (bitonic, 512 threads).
+__global__ void __launch_bounds__(kLocalSort / 2) k_mt_block_sort(VKey* __restrict__ keys) {
   __shared__ VKey sk[kLocalSort];
   const int64_t b0 = (int64_t)blockIdx.x * kLocalSort;
   for (int i = threadIdx.x; i < kLocalSort; i += blockDim.x) sk[i] = keys[b0 + i];
   __syncthreads();
-  for (int64_t kk = kk_lo; kk <= kk_hi; kk <<= 1) {
-    for (int jj = (int)min(kk >> 1, (int64_t)kLocalSort / 2); jj > 0; jj >>= 1) {
+  for (int kk = 2; kk <= kLocalSort; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
       const int t = threadIdx.x;
-      const int i = 2 * t - (t & (jj - 1));  // lower index of this thread's pair
+      const int i = 2 * t - (t & (jj - 1));
       const int l = i + jj;
-      const bool asc = ((b0 + i) & kk) == 0;
+      const bool asc = (i & kk) == 0 || kk == kLocalSort;
       const VKey a = sk[i], b = sk[l];
       if (vless(b, a) == asc) {
         sk[i] = b;
@@ -419,6 +408,35 @@ __global__ void __launch_bounds__(kLocalSort / 2) k_mt_bitonic_local(int64_t P, 
     }
   }
   for (int i = threadIdx.x; i < kLocalSort; i += blockDim.x) keys[b0 + i] = sk[i];
+}
+
+// One merge pass: runs of `w` sorted keys merged pairwise into `out` (merge path: every thread
+// finds where its kMergeItems outputs start on the two runs by a binary search on the
+// cross diagonal, then merges them sequentially).  Keys are unique (idx tie-break).
+constexpr int kMergeItems = 4;
+__global__ void __launch_bounds__(256) k_mt_merge(int64_t P, int64_t w, const VKey* __restrict__ in,
+                                                 VKey* __restrict__ out) {
+  const int64_t o0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeItems;
+  if (o0 >= P) return;
+  const int64_t pair0 = o0 / (2 * w) * (2 * w);  // first key of this run pair
+  const VKey* A = in + pair0;
+  const VKey* B = A + w;
+  const int64_t d = o0 - pair0;  // output position inside the pair
+  // merge path: i keys from A and d - i from B precede output d
+  int64_t lo = d > w ? d - w : 0, hi = d < w ? d : w;
+  while (lo < hi) {
+    const int64_t i = (lo + hi) >> 1;
+    if (vless(B[d - 1 - i], A[i])) hi = i;
+    else lo = i + 1;
+  }
+  int64_t i = lo, j = d - lo;
+#pragma unroll
+  for (int k = 0; k < kMergeItems; ++k) {
+    const bool takeA = j >= w || (i < w && vless(A[i], B[j]));
+    out[o0 + k] = takeA ? A[i] : B[j];
+    if (takeA) ++i;
+    else ++j;
+  }
 }
 
 __global__ void k_mt_newgroup(int64_t V, const VKey* __restrict__ keys, int32_t* __restrict__ first) {
@@ -478,12 +496,16 @@ struct MtResult {
   cudaStream_t st = nullptr;
 };
 
-static void bitonic_sort(VKey* keys, int64_t P, cudaStream_t st) {
+// sorted keys end up in *keys (the two buffers are swapped as the passes ping-pong)
+static void merge_sort(VKey*& keys, VKey*& tmp, int64_t P, cudaStream_t st) {
   // P is a power of two >= kLocalSort
-  k_mt_bitonic_local<<<(unsigned)(P / kLocalSort), kLocalSort / 2, 0, st>>>(P, 2, kLocalSort, keys);
-  for (int64_t kk = 2 * kLocalSort; kk <= P; kk <<= 1) {
-    for (int64_t jj = kk >> 1; jj >= kLocalSort; jj >>= 1) k_mt_bitonic<<<grid_blocks(P), 256, 0, st>>>(P, kk, jj, keys);
-    k_mt_bitonic_local<<<(unsigned)(P / kLocalSort), kLocalSort / 2, 0, st>>>(P, kk, kk, keys);
+  k_mt_block_sort<<<(unsigned)(P / kLocalSort), kLocalSort / 2, 0, st>>>(keys);
+  for (int64_t w = kLocalSort; w < P; w <<= 1) {
+    const int64_t threads = P / kMergeItems;
+    k_mt_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(P, w, keys, tmp);
+    VKey* t = keys;
+    keys = tmp;
+    tmp = t;
   }
 }
 
@@ -546,10 +568,11 @@ static int mt_run(const double* sdf, const double* deform, int R, MtResult& out,
   // W: weld equal positions (np.unique over rows: lexicographic), remap, drop degenerates
   int64_t P = kLocalSort;
   while (P < V) P <<= 1;
-  VKey* keys = nullptr;
+  VKey *keys = nullptr, *ktmp = nullptr;
   cudaMallocAsync(&keys, sizeof(VKey) * P, st);
+  cudaMallocAsync(&ktmp, sizeof(VKey) * P, st);
   k_mt_keys<<<grid_blocks(P), 256, 0, st>>>(V, P, verts, keys);
-  bitonic_sort(keys, P, st);
+  merge_sort(keys, ktmp, P, st);
   int32_t* first = nullptr;
   int64_t *excl = nullptr, *remap = nullptr, *scratch2 = nullptr;
   cudaMallocAsync(&first, sizeof(int32_t) * V, st);
@@ -565,7 +588,7 @@ static int mt_run(const double* sdf, const double* deform, int R, MtResult& out,
   int64_t* d_total = compact(F, tk, scratch2, st);
   cudaMemcpyAsync(&h[0], d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&h[1], excl + V, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  free_all({flags, ebase, scratch, off, negbits, tlist, verts, tris, keys, first, excl, remap, scratch2}, st);
+  free_all({flags, ebase, scratch, off, negbits, tlist, verts, tris, keys, ktmp, first, excl, remap, scratch2}, st);
   cudaStreamSynchronize(st);
   out.nt = h[0];
   out.nv = h[1];
