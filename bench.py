@@ -242,9 +242,17 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TS_BENCH_ONE_GPU=1 (test harness only): every rank on cuda:0 over gloo, so the N > 1 code
+    # path (sharding, all-reduce, barriers, max over ranks) runs on a one-GPU box; never a number
+    one_gpu = os.environ.get("TS_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2406_01579_b200 as ts
     from paper_2406_01579_b200 import _native
     from paper_2406_01579_b200.batch import FitStep, StepConfig, StepStats, shard_views
