@@ -85,7 +85,7 @@ __device__ unsigned long long g_ts_hist[32];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity),
 // bit 4 = count the pairs phase A evaluates (g_ts_counters[2])
 __device__ int g_ts_debug_flags;
-static int h_debug_flags = 0;  // host copy (bit 5 = 32: launch the warp-specialised k_forward_ws)
+static int h_debug_flags = 0;  // host copy of the debug flags
 // diagnostics only (flag bit 1): per-tile forward start/end globaltimer, SM id
 __device__ unsigned long long g_ts_tile_time[2 * 65536];
 __device__ unsigned int g_ts_tile_sm[65536];
@@ -871,9 +871,6 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     for (int k = 0; k < 7; ++k) atomicAdd(&g_ts_phase[k], (unsigned long long)pacc[k]);
 }
 
-}  // namespace ts
-#include "forward_ws.cuh"
-namespace ts {
 
 // N_w resorting window (_core.pyx:171-187) for tiles whose list is not mean-depth monotone.
 // The list is sorted by (q, splat) with q = 32-bit quantised mean depth, so entries with
@@ -1598,32 +1595,16 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
   const int* ovf = dyn ? dyn->ovf : nullptr;
   int32_t* const given_order = scr ? scr->torder : nullptr;
   cudaMemsetAsync(pair_bits, 0, sizeof(uint32_t) * (size_t)TS_PAIR_BIT_WORDS(n_pairs), st);
-  const int smem = (int)sizeof(FwdSmem), smem_ws = (int)sizeof(WsSmem);
-  static const bool attr = [smem, smem_ws] {  // once (thread-safe static: lanes launch from several threads)
+  const int smem = (int)sizeof(FwdSmem);
+  static const bool attr = [smem] {  // once (thread-safe static: lanes launch from several threads)
     cudaFuncSetAttribute(k_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(k_forward_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ws);
-    cudaFuncSetAttribute(k_forward_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ws);
     return true;
   }();
   (void)attr;
   int32_t* torder = take_tmp(given_order, T, st);
   k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
   const bool clip_stops = (1.0 - kAlphaClipD) < t_stop;  // splat.py:14-15: T (1 - ALPHA_CLIP) < T_STOP
-  if (h_debug_flags & 32) {  // flag 32: the warp-specialised forward (forward_ws.cuh; measured slower)
-    if (colors && cmap)
-      k_forward_ws<true><<<T, kWsThreads, smem_ws, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors,
-                                                         S64, tiles_x, W, H, (float)s, s, (float)t_stop, clip_stops,
-                                                         item_off, pair_bits, pair_rec, nmap, dmap, omap, cmap, n_proc,
-                                                         n_blend, ovf);
-    else
-      k_forward_ws<false><<<T, kWsThreads, smem_ws, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec,
-                                                          nullptr, S64, tiles_x, W, H, (float)s, s, (float)t_stop,
-                                                          clip_stops, item_off, pair_bits, pair_rec, nmap, dmap, omap,
-                                                          nullptr, n_proc, n_blend, ovf);
-    put_tmp(torder, given_order, st);
-    return;
-  }
   if (colors && cmap)
     k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
                                                 W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,

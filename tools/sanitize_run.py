@@ -27,7 +27,7 @@ dm = ts.RenderMaps(torch.randn((S, S, 3), device="cuda", generator=gen), torch.r
                    torch.randn((S, S), device="cuda", generator=gen), torch.randn((S, S, 3), device="cuda", generator=gen))
 colors = torch.rand((g.num_tets, 3), device="cuda", generator=gen)
 act = ts.prefilter(g, f, s)
-for flags in (0, 32):  # CTA forward, warp-specialised forward
+for flags in (0,):
     _native.check(_native.lib().ts_debug_set_flags(flags))
     for col in (None, colors):
         sc = ts.build_scene(g, f, cams[1], s, active=act, colors=col)
