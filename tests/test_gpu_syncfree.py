@@ -93,3 +93,21 @@ def test_fitstep_sync_free_equals_threaded(ts):
     for x, y in zip(ga, gb):
         assert torch.allclose(x, y, rtol=1e-5, atol=1e-5 * float(x.abs().max()))
     assert float((sa - sb).abs().max()) < 1e-4
+
+
+def test_sync_free_grows_capacities_when_the_workload_grows(ts):
+    """Capacities learned at s = 100 overflow at s = 20 (more splats, pairs and longer lists):
+    the step is re-run transparently with grown capacities and equals the sizing path."""
+    from paper_2406_01579_b200.batch import FitStep, StepConfig
+    res = {}
+    for sf in (False, True):
+        g, f, cams, dms = _problem(ts, R=48, S=384, V=4)
+        step = FitStep(g, f, cams, StepConfig(sync_free=sf, optimizer=False))
+        step(100.0, range(4), lambda vi, m: dms[vi])  # sizes learned at s = 100
+        gr = step(20.0, range(4), lambda vi, m: dms[vi]).d_vert.clone()
+        torch.cuda.synchronize()
+        step.check_status()
+        res[sf] = (gr, dict(step.view_counts))
+    (ga, ca), (gb, cb) = res[False], res[True]
+    assert ca == cb
+    assert torch.allclose(ga, gb, rtol=1e-5, atol=1e-5 * float(ga.abs().max()))
