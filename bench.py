@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-stress", action="store_true", help="skip the config-5 (256^3, 2048^2) stress figures")
+    p.add_argument("--deterministic", action="store_true",
+                   help="bitwise-reproducible fixed-point gradients (StepConfig.deterministic)")
     p.add_argument("--resolution", type=int, default=R_GRID)
     p.add_argument("--image", type=int, default=IMG)
     p.add_argument("--s", type=float, default=STEEP)
@@ -67,7 +69,9 @@ def config_dict(args, world):
                         f"allreduce + Adam)",
             "grid": args.resolution, "image": args.image, "steepness": args.s, "views_per_gpu": args.views,
             "global_batch_views": args.views * world, "field": "analytic sphere r=0.5 (synthetic)",
-            "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"views sharded x{world}"}
+            "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"views sharded x{world}",
+            "gradients": "int64 fixed point (deterministic)" if getattr(args, "deterministic", False)
+            else "fp32 atomics"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -273,7 +277,8 @@ def run_gpu(args):
                                               inflight=int(os.environ["TS_INFLIGHT"]) if "TS_INFLIGHT" in os.environ
                                               else None,
                                               sync_free=None if "TS_SYNC_FREE" not in os.environ
-                                              else os.environ["TS_SYNC_FREE"] != "0"))
+                                              else os.environ["TS_SYNC_FREE"] != "0",
+                                              deterministic=args.deterministic))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 

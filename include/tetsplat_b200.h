@@ -164,6 +164,28 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
                      const float* const d_maps[4], float* d_vert, float* d_color, float* status, void* stream);
 const int32_t* ts_view_n_blend(ts_workspace* ws);
 
+/* Deterministic gradients (the reference's fixed-order chunk merge, raster.py:217-247, makes
+ * its gradients bitwise reproducible).  The _fx variants add every contribution as the 64-bit
+ * integer round(v * 2^36) with integer atomics, so the sums do not depend on the order in
+ * which CTAs, streams or (all-reduced as int64) ranks deliver them: d_vert_fx int64[4N + 1]
+ * (the interleaved [N,4] layout of d_vert; entry 4N counts contributions dropped because they
+ * were non-finite or |v| >= 2^26), d_color_fx int64[3 * 6R^3] (nullable).  Resolution 2^-36.
+ * ts_fx_to_f32 converts n entries to FP32 (out[i] = fx[i] * 2^-36) and, when status is given,
+ * adds the dropped count fx[n] to status[1] (ts_adam_step then skips the step). */
+int ts_view_backward_fx(ts_workspace* ws, const double* deform, const float* const maps[4],
+                        const float* const d_maps[4], int64_t* d_vert_fx, int64_t* d_color_fx, float* status,
+                        void* stream);
+int ts_render_backward_fx(const ts_scene* scene, int64_t K, const float* colors, const ts_bins* bins, int64_t M,
+                          const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits,
+                          const void* pair_rec, const float* const maps[4], const float* const d_maps[4],
+                          const int32_t* n_proc, const double* deform, int32_t resolution, int64_t* d_vert_fx,
+                          int64_t* d_color_fx, void* stream);
+int ts_eikonal_fx(const double* sdf, const double* deform, int32_t resolution, const int32_t* tet_set, int64_t n,
+                  double scale, int64_t* d_vert_fx, double* loss, void* stream);
+int ts_normal_consistency_fx(const double* sdf, const double* deform, int32_t resolution, double scale,
+                             int64_t* d_vert_fx, double* loss, void* scratch, void* stream);
+int ts_fx_to_f32(const int64_t* fx, int64_t n, float* out, float* status, void* stream);
+
 /* Sync-free per-view path.  With capacities set (cap_M tile pairs, cap_P pixel pairs, cap_L the
  * longest tile list (0 = unbounded); cap_M or cap_P 0 = off)
  * ts_view_forward makes no host round trip: buffers are sized by the capacities (visible

@@ -9,8 +9,8 @@ from .field import (FieldState, AnalyticShape, analytic_sdf, init_sphere, init_f
                     EPS_NORMAL)
 from .splat import (T_FILTER, ALPHA_CLIP, T_STOP, EmptySceneError, SplatScene, prefilter, build_scene,
                     coarse_to_fine_filter, scene_from_arrays, active_aabb, rescale_grid_to_box)
-from .raster import (TILE_SIZE, DEFAULT_WINDOW, RenderMaps, TileBins, GradientBuffers, SavedState, bin_and_sort,
-                     render_forward, render_reference, render_backward)
+from .raster import (TILE_SIZE, DEFAULT_WINDOW, RenderMaps, TileBins, GradientBuffers, FixedPointGradients,
+                     SavedState, bin_and_sort, render_forward, render_reference, render_backward)
 from .losses import eikonal_loss, normal_consistency_loss, map_mse_loss
 from .mesh import rasterize_mesh, export_obj, load_obj
 from .imgio import write_pfm, read_pfm, write_png, save_maps, save_checkpoint, load_checkpoint

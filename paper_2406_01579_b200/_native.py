@@ -85,6 +85,12 @@ def lib():
                             ctypes.c_int),
         "ts_view_backward": ([P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, P, P], ctypes.c_int),
         "ts_view_n_blend": ([P], P),
+        "ts_view_backward_fx": ([P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P, P, P], ctypes.c_int),
+        "ts_render_backward_fx": ([ps, I64, P, pb, I64, pc, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P), P, P,
+                                   I32, P, P, P], ctypes.c_int),
+        "ts_eikonal_fx": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
+        "ts_normal_consistency_fx": ([P, P, I32, D, P, P, P, P], ctypes.c_int),
+        "ts_fx_to_f32": ([P, I64, P, P, P], ctypes.c_int),
         "ts_workspace_set_caps": ([P, I64, I64, I64, P], ctypes.c_int),
         "ts_view_collect": ([P, P, P, P], ctypes.c_int),
         "ts_view_status": ([P, PI64, P], ctypes.c_int),

@@ -17,7 +17,7 @@ import torch
 import torch.distributed as dist
 
 from .losses import eikonal_loss_async, nc_scratch_bytes, normal_consistency_loss_async
-from .raster import GradientBuffers
+from .raster import FixedPointGradients, GradientBuffers
 from .splat import EmptySceneError, prefilter
 from .view import ViewRenderer
 
@@ -118,6 +118,11 @@ class StepConfig:
     # None = auto: sync-free when the rank has fewer than 6 host CPUs (8 ranks on a 16-48
     # core host), else one host thread per lane (measured 1.8% faster on one B200 with 16 CPUs)
     sync_free: bool | None = None
+    # bitwise-reproducible gradients: every contribution (views, regularizers) is accumulated
+    # as a 64-bit fixed-point integer (raster.FixedPointGradients) and the all-reduce sums
+    # int64, so the step's gradients — and Adam's update — do not depend on atomic order,
+    # lane scheduling or the number of ranks the views are split over
+    deterministic: bool = False
 
 
 @dataclass
@@ -143,6 +148,8 @@ class FitStep:
         self._flat = torch.zeros(4 * N + 4, dtype=torch.float32, device=dev)  # status: [2] overflowed views
         self.grads = GradientBuffers(self._flat[:4 * N].view(N, 4))
         self.status = self._flat[4 * N:]
+        self._fx = FixedPointGradients.zeros(N, dev) if self.cfg.deterministic else None
+        self._acc = self._fx if self._fx is not None else self.grads  # what the kernels add into
         self.eik_loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.nc_loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.opt = Adam([field.sdf, field.deformation], [self.cfg.lr_sdf, self.cfg.lr_deform], self.cfg.betas) \
@@ -174,6 +181,8 @@ class FitStep:
         `fit_field` passes False and calls `apply_update` after its host-side checks."""
         g, f, cfg = self.grid, self.field, self.cfg
         self._flat.zero_()
+        if self._fx is not None:
+            self._fx.zero_()
         active = prefilter(g, f, s)
         if active.numel() == 0:
             raise EmptySceneError("pre-filtering removed every tetrahedron")
@@ -196,11 +205,11 @@ class FitStep:
                     if cfg.eik_all and self._all_tets is None:
                         self._all_tets = torch.arange(g.num_tets, dtype=torch.int32, device=active.device)
                     tets = self._all_tets if cfg.eik_all else active
-                    eikonal_loss_async(g, f, tets, self.grads, cfg.lambda_eik, self.eik_loss, self.reg_stream)
+                    eikonal_loss_async(g, f, tets, self._acc, cfg.lambda_eik, self.eik_loss, self.reg_stream)
                 if cfg.lambda_nc > 0:
                     if self._nc_scratch is None:
                         self._nc_scratch = torch.empty(nc_scratch_bytes(g), dtype=torch.uint8, device=f.sdf.device)
-                    normal_consistency_loss_async(g, f, self.grads, cfg.lambda_nc, self.nc_loss, self.reg_stream,
+                    normal_consistency_loss_async(g, f, self._acc, cfg.lambda_nc, self.nc_loss, self.reg_stream,
                                                   self._nc_scratch)
         if cfg.sync_free:
             log = self._views_sync_free(s, list(views), d_maps_fn, active)
@@ -210,7 +219,14 @@ class FitStep:
             main.wait_stream(st)
         if inputs_ready is not None:
             main.wait_event(inputs_ready)
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+        if self._fx is not None:
+            # exact integer sums across ranks, then the same FP32 conversion on every rank
+            if multi:
+                dist.all_reduce(self._fx.fx, op=dist.ReduceOp.SUM, group=self.group)
+                dist.all_reduce(self.status, op=dist.ReduceOp.SUM, group=self.group)
+            self._fx.to_float(self.grads, status=self.status)
+        elif multi:
             dist.all_reduce(self._flat, op=dist.ReduceOp.SUM, group=self.group)
         if update is None:
             update = self.opt is not None
@@ -278,7 +294,7 @@ class FitStep:
                     maps = r.forward(g, f, self.cameras[vi], s, active, n_w=cfg.n_w, stream=st)
                     n_dyn += 1
                     log.append((vi, None, None, None))
-                r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st, status=self.status)
+                r.backward(f, d_maps_fn(vi, maps), self._acc, stream=st, status=self.status)
         return log
 
     def _views_threaded(self, s, views, d_maps_fn, active):
@@ -299,7 +315,7 @@ class FitStep:
                     if K == 0:
                         done.append((vi, 0, M, P))
                         continue
-                    r.backward(f, d_maps_fn(vi, maps), self.grads, stream=st, status=self.status)
+                    r.backward(f, d_maps_fn(vi, maps), self._acc, stream=st, status=self.status)
                     done.append((vi, K, M, r.counts[2]))
             return done
 

@@ -230,6 +230,40 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
   return check_cuda("ts_render_backward");
 }
 
+// deterministic (fixed-point) outputs: d_vert_fx int64[4N + 1] (entry 4N counts dropped
+// contributions), d_color_fx int64[3 * num_tets] (nullable)
+static Fx fx_of(int32_t R, int64_t* d_vert_fx, int64_t* d_color_fx) {
+  const int64_t n = (int64_t)R + 1;
+  Fx fx;
+  fx.vert = reinterpret_cast<long long*>(d_vert_fx);
+  fx.color = reinterpret_cast<long long*>(d_color_fx);
+  fx.bad = reinterpret_cast<unsigned long long*>(d_vert_fx + 4 * n * n * n);
+  return fx;
+}
+
+int ts_render_backward_fx(const ts_scene* sc, int64_t K, const float* colors, const ts_bins* b, int64_t M,
+                          const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits,
+                          const void* pair_rec, const float* const maps[4], const float* const dmaps[4],
+                          const int32_t* n_proc, const double* deform, int32_t R, int64_t* d_vert_fx,
+                          int64_t* d_color_fx, void* stream) {
+  if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert_fx || R < 1 || K < 0 || M < 0 ||
+      (M > 0 && (!item_off || !pair_bits)))
+    return fail(TS_EINVAL, "ts_render_backward_fx: bad arguments");
+  for (int i = 0; i < 3; ++i)
+    if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward_fx: missing map");
+  int tx, ty;
+  if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
+  keep_pool_warm();
+  const float* m4[4] = {maps[0], maps[1], maps[2], maps[3]};
+  const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], dmaps[3]};
+  const Fx fx = fx_of(R, d_vert_fx, d_color_fx);
+  ts_impl_backward(tx, ty, bv_of(b), M, K, reinterpret_cast<const SplatRec*>(sc->records), colors, sc->f,
+                   sc->vert_ids, sc->tet_ids, deform, R, to_cam(cam), item_off, pair_bits,
+                   reinterpret_cast<const float4*>(pair_rec), m4, d4, n_proc, nullptr, nullptr, ST(stream), nullptr,
+                   nullptr, nullptr, 0, nullptr, nullptr, &fx);
+  return check_cuda("ts_render_backward_fx");
+}
+
 int ts_bins_from_lists(const int64_t* starts, const int32_t* items, int32_t T, const double* md, double near_,
                        double far_, uint8_t* flags, void* stream) {
   if (!starts || !flags || T < 0 || !(far_ > near_) || (T > 0 && (!items || !md)))
@@ -287,6 +321,30 @@ int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, do
   keep_pool_warm();
   ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream));
   return check_cuda("ts_normal_consistency");
+}
+
+int ts_eikonal_fx(const double* sdf, const double* deform, int32_t R, const int32_t* tet_set, int64_t n,
+                  double scale, int64_t* d_vert_fx, double* loss, void* stream) {
+  if (!sdf || !deform || !d_vert_fx || !loss || R < 1 || n < 0 || (n > 0 && !tet_set))
+    return fail(TS_EINVAL, "ts_eikonal_fx: bad arguments");
+  const Fx fx = fx_of(R, d_vert_fx, nullptr);
+  ts_impl_eikonal(sdf, deform, R, tet_set, n, (float)scale, nullptr, loss, ST(stream), &fx);
+  return check_cuda("ts_eikonal_fx");
+}
+
+int ts_normal_consistency_fx(const double* sdf, const double* deform, int32_t R, double scale, int64_t* d_vert_fx,
+                             double* loss, void* scratch, void* stream) {
+  if (!sdf || !deform || !d_vert_fx || !loss || R < 1) return fail(TS_EINVAL, "ts_normal_consistency_fx: bad arguments");
+  if (!scratch) keep_pool_warm();
+  const Fx fx = fx_of(R, d_vert_fx, nullptr);
+  ts_impl_normal_consistency(sdf, deform, R, (float)scale, nullptr, loss, ST(stream), scratch, &fx);
+  return check_cuda("ts_normal_consistency_fx");
+}
+
+int ts_fx_to_f32(const int64_t* fx, int64_t n, float* out, float* status, void* stream) {
+  if (!fx || !out || n < 0) return fail(TS_EINVAL, "ts_fx_to_f32: bad arguments");
+  ts_impl_fx_to_f32(reinterpret_cast<const long long*>(fx), n, out, status, ST(stream));
+  return check_cuda("ts_fx_to_f32");
 }
 
 int ts_adam_step(int32_t R, const float* d_vert, double* sdf, double* deform, double* m_sdf, double* v_sdf,

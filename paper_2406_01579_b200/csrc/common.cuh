@@ -234,4 +234,34 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
+// ---- deterministic (fixed-point) gradient accumulation ---------------------------------
+// The reference merges per-chunk private buffers in a fixed order (raster.py:217-247), so its
+// gradients are bitwise reproducible.  The deterministic mode adds every contribution as a
+// 64-bit integer v * 2^36 (integer addition is associative: the sum is independent of the
+// order the atomics land in, across CTAs, streams and — all-reduced as int64 — ranks).
+// Resolution 2^-36 ~ 1.5e-11 (three orders below Adam's eps = 1e-8), range per contribution
+// |v| < 2^26; contributions outside it (or non-finite) are counted in `bad` and dropped.
+constexpr double kFxScale = 68719476736.0;           // 2^36
+constexpr double kFxInv = 1.4551915228366852e-11;    // 2^-36
+constexpr double kFxMax = 67108864.0;                // 2^26
+
+__device__ __forceinline__ void fx_add(long long* addr, double v, unsigned long long* bad) {
+  if (v == 0.0) return;
+  if (!(fabs(v) < kFxMax)) {  // also NaN
+    atomicAdd(bad, 1ull);
+    return;
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double2ll_rn(v * kFxScale));
+}
+
+__device__ __forceinline__ void fx_add4(long long* addr, double a, double b, double c, double d,
+                                        unsigned long long* bad) {
+  fx_add(addr, a, bad);
+  fx_add(addr + 1, b, bad);
+  fx_add(addr + 2, c, bad);
+  fx_add(addr + 3, d, bad);
+}
+
+__device__ __forceinline__ float fx_value(long long v) { return (float)((double)v * kFxInv); }
+
 }  // namespace ts

@@ -1176,9 +1176,10 @@ static_assert(3 * (sizeof(BwdSmem<false>) + 1024) <= 228 * 1024, "backward: 3 CT
 // then per run of equal splat (items are in pair order, i.e. grouped by splat) one lane per
 // component sums the run and adds it to the splat's row (shared atomics: a run may continue
 // in the neighbouring batch of another warp).
-template <bool COLOR>
+template <bool COLOR, bool DET>
 __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, const float4* __restrict__ pair_rec,
-                                              int64_t ib0) {
+                                              int64_t ib0, long long* __restrict__ rows_fx,
+                                              unsigned long long* __restrict__ fx_bad) {
   using SM = BwdSmem<COLOR>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* row = S.u.rows[warp][lane];
@@ -1217,13 +1218,16 @@ __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, 
     if (lane < SM::NC) {
       float sum = 0.f;
       for (int i = s0; i < e0; ++i) sum += S.u.rows[warp][i][lane];
-      atomicAdd(&S.acc[jj][lane], sum);
+      if (DET)  // fixed point straight into the splat's row: order-independent
+        fx_add(rows_fx + (int64_t)S.sh[jj].k * SM::AS + lane, sum, fx_bad);
+      else
+        atomicAdd(&S.acc[jj][lane], sum);
     }
   }
   __syncwarp();
 }
 
-template <bool COLOR>
+template <bool COLOR, bool DET>
 __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
     const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
@@ -1232,7 +1236,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
     const float* __restrict__ d_normal, const float* __restrict__ d_depth, const float* __restrict__ d_opacity,
     const float* __restrict__ d_color, const int32_t* __restrict__ n_proc, float* __restrict__ rows,
-    float* __restrict__ status, const int* __restrict__ ovf) {
+    float* __restrict__ status, const int* __restrict__ ovf, unsigned long long* __restrict__ fx_bad) {
   if (ovf && *ovf) {  // an overflowed sync-free view: flagged for the step's Adam guard
     if (status && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(status + 2, 1.0f);
     return;
@@ -1344,7 +1348,8 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         }
       }
     }
-    for (int i = threadIdx.x; i < n * SM::AS; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
+    if (!DET)
+      for (int i = threadIdx.x; i < n * SM::AS; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
     cp_async_wait_all();
     if (threadIdx.x < kCh) prefetch_rec(S.pf, recs, maxproc - base - n);
     __syncthreads();
@@ -1403,12 +1408,14 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     __syncthreads();
     const int nitems = S.nitems;
     for (int b0 = warp * 32; b0 < nitems; b0 += TS_TILE_PX)
-      process_batch<COLOR>(S, b0, min(32, nitems - b0), pair_rec, ib0);
+      process_batch<COLOR, DET>(S, b0, min(32, nitems - b0), pair_rec, ib0, reinterpret_cast<long long*>(rows),
+                                fx_bad);
     __syncthreads();
     TS_PHASE(3);
     // ---- the chunk's per-(tile, splat) rows, added into the splats' rows (zeroed per view;
     //      a splat's tiles add in any order: FP32 rounding-level nondeterminism only) ----------
-    for (int i = threadIdx.x; i < n * (SM::AS / 4); i += TS_TILE_PX) {
+    // (the deterministic variant added its rows in fixed point in process_batch)
+    for (int i = threadIdx.x; !DET && i < n * (SM::AS / 4); i += TS_TILE_PX) {
       const int j = i / (SM::AS / 4), c = i % (SM::AS / 4);
       const float4 v = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
       // the splat index from the list (S.sh may already hold the next chunk: staging threads
@@ -1425,19 +1432,28 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
 // per-splat gather + normal chain + camera chain (raster.py:253-306).  FP32 chain math (the
 // gradients are FP32); vertex positions are formed in FP64 (grid coordinate + deformation)
 // and only their differences / camera-space coordinates are rounded, one vertex at a time.
-template <bool COLOR>
+template <bool COLOR, bool DET>
 __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const float* __restrict__ rows,
                                                const int32_t* __restrict__ vert_ids,
                                                const int32_t* __restrict__ tet_ids, const double* __restrict__ fsc,
                                                const double* __restrict__ deform, Grid G, Camera cam,
                                                float* __restrict__ d_vert, float* __restrict__ d_color,
-                                               const int64_t* __restrict__ Kdev, const int* __restrict__ ovf) {
+                                               const int64_t* __restrict__ Kdev, const int* __restrict__ ovf,
+                                               Fx fxo) {
   if (ovf && *ovf) return;
   if (Kdev) K = min(K, *Kdev);
   constexpr int NQ = COLOR ? 6 : 5;  // float4s of a row that carry data
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
     float a[4 * NQ];
-    {
+    if (DET) {  // fixed-point rows (k_backward<DET>)
+      const longlong2* src = reinterpret_cast<const longlong2*>(rows) + k * (2 * NQ);
+#pragma unroll
+      for (int i = 0; i < 2 * NQ; ++i) {
+        const longlong2 q = src[i];
+        a[2 * i] = fx_value(q.x);
+        a[2 * i + 1] = fx_value(q.y);
+      }
+    } else {
       const float4* src = reinterpret_cast<const float4*>(rows + k * (4 * NQ));
 #pragma unroll
       for (int i = 0; i < NQ; ++i) {
@@ -1520,11 +1536,19 @@ __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const float* __rest
       const float dpc[3] = {dPx * fx * iZ, dPy * fy * iZ, (-dPx * fx * pc[0] - dPy * fy * pc[1]) * iZ * iZ + dZ};
       for (int j = 0; j < 3; ++j)
         dPos[v][j] += dpc[0] * (float)cam.R[j] + dpc[1] * (float)cam.R[3 + j] + dpc[2] * (float)cam.R[6 + j];
-      red_add_v4(d_vert + (size_t)vid[v] * 4, dF[v], dPos[v][0], dPos[v][1], dPos[v][2]);
+      if (DET)
+        fx_add4(fxo.vert + (size_t)vid[v] * 4, dF[v], dPos[v][0], dPos[v][1], dPos[v][2], fxo.bad);
+      else
+        red_add_v4(d_vert + (size_t)vid[v] * 4, dF[v], dPos[v][0], dPos[v][1], dPos[v][2]);
     }
     if (COLOR) {
       const int64_t t = tet_ids[k];
-      for (int c = 0; c < 3; ++c) atomicAdd(d_color + t * 3 + c, a[20 + c]);
+      for (int c = 0; c < 3; ++c) {
+        if (DET)
+          fx_add(fxo.color + t * 3 + c, a[20 + c], fxo.bad);
+        else
+          atomicAdd(d_color + t * 3 + c, a[20 + c]);
+      }
     }
   }
 }
@@ -1622,14 +1646,16 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
                       const uint32_t* pair_bits, const float4* pair_rec, const float* maps[4],
                       const float* dmaps[4], const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
                       const ViewScratch* scr, float* status, const int32_t* tiles, int n_tiles,
-                      float* rows_out, const Dyn* dyn) {
+                      float* rows_out, const Dyn* dyn, const Fx* fx) {
   const int* ovf = dyn ? dyn->ovf : nullptr;
   const int T = tiles_x * tiles_y;
   if (M <= 0 || K <= 0) return;
   const int smem_c = (int)sizeof(BwdSmem<true>), smem = (int)sizeof(BwdSmem<false>);
   static const bool attr = [smem_c, smem] {  // once (thread-safe static)
-    cudaFuncSetAttribute(k_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
-    cudaFuncSetAttribute(k_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_backward<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
+    cudaFuncSetAttribute(k_backward<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_backward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_c);
+    cudaFuncSetAttribute(k_backward<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return true;
   }();
   (void)attr;
@@ -1639,35 +1665,50 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   int32_t* const given_order = tiles ? const_cast<int32_t*>(tiles) : (scr ? scr->torder : nullptr);
   const int nblk = tiles ? n_tiles : T;
   if (nblk <= 0) return;
-  float* rows = take_tmp(given_rows, kGr * (size_t)M, st);  // per-splat rows: K <= M
+  const bool det = fx && fx->vert && !rows_out;  // fixed-point rows and outputs
+  // per-splat rows: K <= M (fixed point: int64, twice the floats)
+  float* rows = take_tmp(given_rows, (det ? 2 : 1) * kGr * (size_t)M, st);
   int32_t* torder = take_tmp(given_order, T, st);
   // the fused view path's workspace still holds this view's order from its forward
   if (!given_order) k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
-  const bool color = colors && maps[3] && dmaps[3] && (d_color || rows_out);
+  const bool color = colors && maps[3] && dmaps[3] && (det ? fx->color != nullptr : (d_color || rows_out));
   if (!rows_out)
-    cudaMemsetAsync(rows, 0, sizeof(float) * (color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
-  if (color)
-    k_backward<true><<<nblk, TS_TILE_PX, smem_c, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, tiles_x,
-                                                 cam.width, cam.height, item_off, pair_bits, pair_rec,
-                                                 maps[0], maps[1], maps[2], maps[3], dmaps[0], dmaps[1], dmaps[2],
-                                                 dmaps[3], n_proc, rows, status, ovf);
+    cudaMemsetAsync(rows, 0,
+                    (det ? 8 : 4) * (size_t)(color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
+  unsigned long long* bad = det ? fx->bad : nullptr;
+#define TS_BWD_ARGS(C)                                                                                              \
+  torder, b.starts, b.items, b.witems, b.nonmono, rec, C ? colors : nullptr, tiles_x, cam.width, cam.height,         \
+      item_off, pair_bits, pair_rec, maps[0], maps[1], maps[2], C ? maps[3] : nullptr, dmaps[0], dmaps[1], dmaps[2], \
+      C ? dmaps[3] : nullptr, n_proc, rows, status, ovf, bad
+  if (color && det)
+    k_backward<true, true><<<nblk, TS_TILE_PX, smem_c, st>>>(TS_BWD_ARGS(true));
+  else if (color)
+    k_backward<true, false><<<nblk, TS_TILE_PX, smem_c, st>>>(TS_BWD_ARGS(true));
+  else if (det)
+    k_backward<false, true><<<nblk, TS_TILE_PX, smem, st>>>(TS_BWD_ARGS(false));
   else
-    k_backward<false><<<nblk, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, tiles_x,
-                                                  cam.width, cam.height, item_off, pair_bits, pair_rec,
-                                                  maps[0], maps[1], maps[2], nullptr, dmaps[0], dmaps[1], dmaps[2],
-                                                  nullptr, n_proc, rows, status, ovf);
+    k_backward<false, false><<<nblk, TS_TILE_PX, smem, st>>>(TS_BWD_ARGS(false));
+#undef TS_BWD_ARGS
   if (rows_out) {
     put_tmp(torder, given_order, st);
     return;
   }
   int blocks = (int)((K + 127) / 128);
   if (blocks > 148 * 64) blocks = 148 * 64;
-  if (color)
-    k_chain<true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform,
-                                          make_grid(R), cam, d_vert, d_color, dyn ? dyn->K : nullptr, ovf);
+  const Fx fxa = det ? *fx : Fx{};
+  const int64_t* Kd = dyn ? dyn->K : nullptr;
+  if (color && det)
+    k_chain<true, true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, nullptr,
+                                                nullptr, Kd, ovf, fxa);
+  else if (color)
+    k_chain<true, false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, d_vert,
+                                                 d_color, Kd, ovf, fxa);
+  else if (det)
+    k_chain<false, true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, nullptr,
+                                                 nullptr, Kd, ovf, fxa);
   else
-    k_chain<false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform,
-                                           make_grid(R), cam, d_vert, nullptr, dyn ? dyn->K : nullptr, ovf);
+    k_chain<false, false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, d_vert,
+                                                  nullptr, Kd, ovf, fxa);
   put_tmp(rows, given_rows, st);
   put_tmp(torder, given_order, st);
 }

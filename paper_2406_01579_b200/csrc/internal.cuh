@@ -52,6 +52,14 @@ struct Dyn {
   const int* ovf = nullptr;
 };
 
+// Deterministic gradient output (fixed point, common.cuh fx_add): when given, the backward
+// chain and the regularizers add into these int64 buffers instead of the FP32 d_vert / d_color.
+struct Fx {
+  long long* vert = nullptr;          // [4 N] (d_sdf, d_deform xyz) * 2^36
+  long long* color = nullptr;         // [3 * num_tets] d_color * 2^36 (colour variant)
+  unsigned long long* bad = nullptr;  // dropped contributions (non-finite or |v| >= 2^26)
+};
+
 struct BinsView {
   const int64_t* starts;
   const int64_t* splat_off;
@@ -100,7 +108,7 @@ void ts_impl_backward(int tiles_x, int tiles_y, const ts::BinsView& b, int64_t M
                       const int32_t* n_proc, float* d_vert, float* d_color, cudaStream_t st,
                       const ts::ViewScratch* scr = nullptr, float* status = nullptr,
                       const int32_t* tiles = nullptr, int n_tiles = 0, float* rows_out = nullptr,
-                      const ts::Dyn* dyn = nullptr);
+                      const ts::Dyn* dyn = nullptr, const ts::Fx* fx = nullptr);
 void ts_impl_list_flags(int T, const int64_t* starts, const int32_t* items, const double* md, double near_,
                         double far_, uint8_t* flags, cudaStream_t st);
 void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W, int H, const ts::BinsView& b,
@@ -108,9 +116,10 @@ void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W
                            const float4* pair_rec, const int32_t* n_proc, const int64_t* rec_off, int64_t* idx,
                            double* alpha, cudaStream_t st);
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
-                     float* d_vert, double* loss, cudaStream_t st);
+                     float* d_vert, double* loss, cudaStream_t st, const ts::Fx* fx = nullptr);
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
-                                double* loss, cudaStream_t st, void* scratch = nullptr);
+                                double* loss, cudaStream_t st, void* scratch = nullptr, const ts::Fx* fx = nullptr);
+void ts_impl_fx_to_f32(const long long* fx, int64_t n, float* out, float* status, cudaStream_t st);
 int64_t ts_impl_nc_scratch_bytes(int R);
 int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);
 int ts_impl_mt_run(const double* sdf, const double* deform, int R, void** handle, int64_t* nv, int64_t* nt,

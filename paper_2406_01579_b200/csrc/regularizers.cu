@@ -58,7 +58,8 @@ __device__ __forceinline__ void block_add_to(T v, T* out) {
 
 __global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __restrict__ tet_set, Grid G,
                                                  const double* __restrict__ sdf, const double* __restrict__ deform,
-                                                 float scale, float* __restrict__ d_vert, double* __restrict__ loss) {
+                                                 float scale, float* __restrict__ d_vert, double* __restrict__ loss,
+                                                 Fx fx) {
   double local = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t v[4];
@@ -72,9 +73,14 @@ __global__ void __launch_bounds__(256) k_eikonal(int64_t n, const int32_t* __res
       double dg[3] = {dmul(w, g[0]), dmul(w, g[1]), dmul(w, g[2])};
       double dfs[4];
       chain_coeffs(det, c1, c2, c3, dg, dfs);
-      for (int c = 0; c < 4; ++c)
-        red_add_v4(d_vert + (size_t)v[c] * 4, (float)(scale * dfs[c]), (float)(-scale * dfs[c] * g[0]),
-                   (float)(-scale * dfs[c] * g[1]), (float)(-scale * dfs[c] * g[2]));
+      for (int c = 0; c < 4; ++c) {
+        if (fx.vert)
+          fx_add4(fx.vert + (size_t)v[c] * 4, scale * dfs[c], -scale * dfs[c] * g[0], -scale * dfs[c] * g[1],
+                  -scale * dfs[c] * g[2], fx.bad);
+        else
+          red_add_v4(d_vert + (size_t)v[c] * 4, (float)(scale * dfs[c]), (float)(-scale * dfs[c] * g[0]),
+                     (float)(-scale * dfs[c] * g[1]), (float)(-scale * dfs[c] * g[2]));
+      }
     }
   }
   block_add_to(local, loss);
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t C, Grid G, const d
 // pass C: per-vertex gather of the per-tet chain terms
 __global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const float4* __restrict__ tdf,
                                                  const float4* __restrict__ tg, float scale,
-                                                 float* __restrict__ d_vert) {
+                                                 float* __restrict__ d_vert, Fx fx) {
   for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
@@ -348,8 +354,11 @@ __global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const float4
       dp[2] = dsub(dp[2], dmul(d, gq.z));
     });
     // atomic add: the fit step runs the regularizers concurrently with the views' chains
-    red_add_v4(d_vert + vid * 4, (float)(scale * ds), (float)(scale * dp[0]), (float)(scale * dp[1]),
-               (float)(scale * dp[2]));
+    if (fx.vert)
+      fx_add4(fx.vert + vid * 4, scale * ds, scale * dp[0], scale * dp[1], scale * dp[2], fx.bad);
+    else
+      red_add_v4(d_vert + vid * 4, (float)(scale * ds), (float)(scale * dp[0]), (float)(scale * dp[1]),
+                 (float)(scale * dp[2]));
   }
 }
 
@@ -397,9 +406,25 @@ __global__ void __launch_bounds__(256) k_finite_check(int64_t n4, const float4* 
   if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicAdd(flag, 1.0f);
 }
 
+// fixed-point gradients (deterministic mode) -> FP32; the dropped-contribution count fx[n]
+// goes to status[1] (non-finite gradient entries: Adam skips the step)
+__global__ void __launch_bounds__(256) k_fx_to_f32(int64_t n, const long long* __restrict__ fx,
+                                                   float* __restrict__ out, float* __restrict__ status) {
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < n; i += (int64_t)gridDim.x * blockDim.x) out[i] = fx_value(fx[i]);
+  if (status && i0 == 0 && fx[n] != 0) atomicAdd(status + 1, (float)fx[n]);
+}
+
 }  // namespace ts
 
 using namespace ts;
+
+void ts_impl_fx_to_f32(const long long* fx, int64_t n, float* out, float* status, cudaStream_t st) {
+  if (n <= 0) return;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_fx_to_f32<<<blocks, 256, 0, st>>>(n, fx, out, status);
+}
 
 void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, double* m_sdf, double* v_sdf,
                   double* m_def, double* v_def, double lr_sdf, double lr_def, double b1, double b2, int64_t t,
@@ -414,12 +439,12 @@ void ts_impl_adam(int64_t N, const float* g4, double* sdf, double* deform, doubl
 }
 
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
-                     float* d_vert, double* loss, cudaStream_t st) {
+                     float* d_vert, double* loss, cudaStream_t st, const Fx* fx) {
   cudaMemsetAsync(loss, 0, sizeof(double), st);
   if (n <= 0) return;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_eikonal<<<blocks, 256, 0, st>>>(n, tet_set, make_grid(R), sdf, deform, scale, d_vert, loss);
+  k_eikonal<<<blocks, 256, 0, st>>>(n, tet_set, make_grid(R), sdf, deform, scale, d_vert, loss, fx ? *fx : Fx{});
 }
 
 // scratch layout of the normal-consistency passes (16-byte aligned pieces)
@@ -438,7 +463,7 @@ int64_t ts_impl_nc_scratch_bytes(int R) {
 
 // scratch: ts_impl_nc_scratch_bytes(R) bytes of device memory, or nullptr (stream-ordered pool)
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
-                                double* loss, cudaStream_t st, void* scratch) {
+                                double* loss, cudaStream_t st, void* scratch, const Fx* fx) {
   const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
   cudaMemsetAsync(loss, 0, sizeof(double), st);
   int64_t off[8];
@@ -459,6 +484,6 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tn, nv, icnt);
   k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, icnt, dmi, loss);
   k_nc_tet_chain<<<cblocks, 256, 0, st>>>(C, G, sdf, deform, dmi, tdf, tg);
-  k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert);
+  k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert, fx ? *fx : Fx{});
   if (!scratch) cudaFreeAsync(base, st);
 }

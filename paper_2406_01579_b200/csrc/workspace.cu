@@ -410,13 +410,17 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   return TS_OK;
 }
 
-int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4], const float* const dmaps[4],
-                     float* d_vert, float* d_color, float* status, void* stream) {
+static int view_backward(ts_workspace* ws, const double* deform, const float* const maps[4],
+                         const float* const dmaps[4], float* d_vert, float* d_color, float* status, void* stream,
+                         const Fx* fx) {
   if (!ws || !ws->valid) return ws_fail(TS_EINVAL, "ts_view_backward: no forward state in the workspace");
-  if (!deform || !maps || !dmaps || !d_vert || !maps[0] || !maps[1] || !maps[2] || !dmaps[0] || !dmaps[1] ||
-      !dmaps[2])
+  if (!deform || !maps || !dmaps || !(d_vert || fx) || !maps[0] || !maps[1] || !maps[2] || !dmaps[0] ||
+      !dmaps[1] || !dmaps[2])
     return ws_fail(TS_EINVAL, "ts_view_backward: bad arguments");
   if (ws->K == 0 || ws->M == 0) return TS_OK;
+  // fixed-point rows are int64: twice the forward's kGr floats per list position (grow-only)
+  if (fx && !ws->rows.get<float>(2 * 24 * (size_t)(ws->K > ws->M ? ws->K : ws->M)))
+    return ws_fail(TS_ENOMEM, "ts_view_backward_fx: out of device memory");
   Dyn dyn;
   dyn.K = reinterpret_cast<int64_t*>(ws->need.p);
   dyn.ovf = reinterpret_cast<int*>(ws->ovf.p);
@@ -435,10 +439,29 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
                    reinterpret_cast<int64_t*>(ws->item_off.p), reinterpret_cast<uint32_t*>(ws->pair_bits.p),
                    reinterpret_cast<float4*>(ws->pair_rec.p), m4, d4,
                    reinterpret_cast<int32_t*>(ws->n_proc.p), d_vert, ws->color ? d_color : nullptr,
-                   reinterpret_cast<cudaStream_t>(stream), &scr, status, nullptr, 0, nullptr, ws->dyn ? &dyn : nullptr);
+                   reinterpret_cast<cudaStream_t>(stream), &scr, status, nullptr, 0, nullptr, ws->dyn ? &dyn : nullptr,
+                   fx);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return ws_fail(TS_ECUDA, cudaGetErrorString(e));
   return TS_OK;
+}
+
+int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4], const float* const dmaps[4],
+                     float* d_vert, float* d_color, float* status, void* stream) {
+  if (!d_vert) return ws_fail(TS_EINVAL, "ts_view_backward: bad arguments");
+  return view_backward(ws, deform, maps, dmaps, d_vert, d_color, status, stream, nullptr);
+}
+
+int ts_view_backward_fx(ts_workspace* ws, const double* deform, const float* const maps[4],
+                        const float* const dmaps[4], int64_t* d_vert_fx, int64_t* d_color_fx, float* status,
+                        void* stream) {
+  if (!ws || !d_vert_fx) return ws_fail(TS_EINVAL, "ts_view_backward_fx: bad arguments");
+  const int64_t n = (int64_t)ws->R + 1;
+  Fx fx;
+  fx.vert = reinterpret_cast<long long*>(d_vert_fx);
+  fx.color = reinterpret_cast<long long*>(d_color_fx);
+  fx.bad = reinterpret_cast<unsigned long long*>(d_vert_fx + 4 * n * n * n);
+  return view_backward(ws, deform, maps, dmaps, nullptr, nullptr, status, stream, &fx);
 }
 
 // n_blend of the last forward (H*W int32, device) — for parity checks

@@ -4,7 +4,7 @@ from __future__ import annotations
 import torch
 
 from . import _native
-from .raster import GradientBuffers, RenderMaps
+from .raster import FixedPointGradients, GradientBuffers, RenderMaps
 
 
 def eikonal_loss(grid, field, tet_set, out: GradientBuffers | None = None, scale: float = 1.0,
@@ -24,10 +24,13 @@ def eikonal_loss(grid, field, tet_set, out: GradientBuffers | None = None, scale
 
 
 def eikonal_loss_async(grid, field, tet_set, out, scale, loss, stream=None):
-    """Sync-free variant: loss (device f64[1]) is overwritten, gradients accumulated."""
-    _native.check(_native.lib().ts_eikonal(_native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution,
-                                           _native.ptr(tet_set), int(tet_set.numel()), float(scale),
-                                           _native.ptr(out.d_vert), _native.ptr(loss), _native.stream_ptr(stream)))
+    """Sync-free variant: loss (device f64[1]) is overwritten, gradients accumulated (into a
+    FixedPointGradients: fixed point, order-independent)."""
+    fixed = isinstance(out, FixedPointGradients)
+    fn = _native.lib().ts_eikonal_fx if fixed else _native.lib().ts_eikonal
+    _native.check(fn(_native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution,
+                     _native.ptr(tet_set), int(tet_set.numel()), float(scale),
+                     _native.ptr(out.fx if fixed else out.d_vert), _native.ptr(loss), _native.stream_ptr(stream)))
 
 
 def normal_consistency_loss(grid, field, out: GradientBuffers | None = None, scale: float = 1.0,
@@ -44,6 +47,11 @@ def normal_consistency_loss_async(grid, field, out, scale, loss, stream=None, sc
     """Sync-free variant; `scratch` (uint8 device tensor of nc_scratch_bytes(grid) bytes)
     avoids per-call stream-ordered allocations."""
     L = _native.lib()
+    if isinstance(out, FixedPointGradients):
+        _native.check(L.ts_normal_consistency_fx(_native.ptr(field.sdf), _native.ptr(field.deformation),
+                                                 grid.resolution, float(scale), _native.ptr(out.fx),
+                                                 _native.ptr(loss), _native.ptr(scratch), _native.stream_ptr(stream)))
+        return
     if scratch is not None:
         _native.check(L.ts_normal_consistency_ws(_native.ptr(field.sdf), _native.ptr(field.deformation),
                                                  grid.resolution, float(scale), _native.ptr(out.d_vert),

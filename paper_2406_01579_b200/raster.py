@@ -126,6 +126,61 @@ class GradientBuffers:
         return GradientBuffers(self.d_vert * w, None if self.d_color is None else self.d_color * w)
 
 
+FX_SCALE = 2.0 ** 36  # fixed-point gradients: value * 2^36 as int64 (include/tetsplat_b200.h)
+
+
+@dataclass
+class FixedPointGradients:
+    """Deterministic accumulation target.  The reference merges per-chunk private buffers in a
+    fixed order (raster.py:217-247), so its gradients are bitwise reproducible; here every
+    contribution is added as the int64 round(v * 2^36) (integer addition is associative, so
+    the sum does not depend on the order the atomics land in — across CTAs, streams and, all-
+    reduced as int64, ranks).  fx: int64[4N + 1], the interleaved [N,4] layout of
+    GradientBuffers.d_vert plus a count of dropped (non-finite or |v| >= 2^26) contributions;
+    fx_color: int64[T,3] or None.  `to_float` converts (resolution 2^-36 ~ 1.5e-11)."""
+
+    fx: torch.Tensor
+    fx_color: torch.Tensor | None = None
+
+    @classmethod
+    def zeros(cls, num_vertices, device="cuda", num_tets_color: int | None = None):
+        return cls(torch.zeros(4 * num_vertices + 1, dtype=torch.int64, device=device),
+                   None if num_tets_color is None else
+                   torch.zeros((num_tets_color, 3), dtype=torch.int64, device=device))
+
+    @property
+    def num_vertices(self) -> int:
+        return (self.fx.numel() - 1) // 4
+
+    @property
+    def dropped(self) -> torch.Tensor:
+        """device int64[1]: contributions dropped as non-finite or out of range"""
+        return self.fx[-1:]
+
+    def zero_(self):
+        self.fx.zero_()
+        if self.fx_color is not None:
+            self.fx_color.zero_()
+        return self
+
+    def to_float(self, out: GradientBuffers | None = None, status: torch.Tensor | None = None,
+                 stream=None) -> GradientBuffers:
+        """FP32 gradients (overwriting `out`); status[1] += dropped count when `status` is given."""
+        N = self.num_vertices
+        dev = self.fx.device
+        if out is None:
+            out = GradientBuffers(torch.empty((N, 4), dtype=torch.float32, device=dev),
+                                  None if self.fx_color is None else
+                                  torch.empty(self.fx_color.shape, dtype=torch.float32, device=dev))
+        L = _native.lib()
+        _native.check(L.ts_fx_to_f32(_native.ptr(self.fx), 4 * N, _native.ptr(out.d_vert), _native.ptr(status),
+                                     _native.stream_ptr(stream)))
+        if self.fx_color is not None and out.d_color is not None:
+            _native.check(L.ts_fx_to_f32(_native.ptr(self.fx_color), self.fx_color.numel(),
+                                         _native.ptr(out.d_color), None, _native.stream_ptr(stream)))
+        return out
+
+
 @dataclass
 class SavedState:
     """What the backward needs from the forward (raster.py:94-101).  Instead of per-pixel
@@ -248,9 +303,12 @@ def _as_f32(t, dev):
 
 
 def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d_maps: RenderMaps,
-                    out: GradientBuffers | None = None, stream=None, timing=None) -> GradientBuffers:
+                    out: GradientBuffers | FixedPointGradients | None = None, stream=None, timing=None,
+                    deterministic: bool = False) -> GradientBuffers | FixedPointGradients:
     """Exact reverse-mode pass: map gradients -> per-vertex SDF/deformation gradients
-    (raster.py:206-306).  With `out`, gradients are accumulated into it (fused batch)."""
+    (raster.py:206-306).  With `out`, gradients are accumulated into it (fused batch).
+    `deterministic` (or a FixedPointGradients `out`): bitwise-reproducible fixed-point
+    accumulation; without `out` the result is returned converted to FP32."""
     dev = scene.mean_depth.device
     dn, dd, do = _as_f32(d_maps.normal, dev), _as_f32(d_maps.depth, dev), _as_f32(d_maps.opacity, dev)
     for arr in (dn, dd, do):
@@ -258,11 +316,16 @@ def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d
             raise ValueError("non-finite incoming map gradients")
     with_color = scene.colors is not None and d_maps.color is not None
     dc = _as_f32(d_maps.color, dev) if with_color else None
+    convert = False
+    if out is None and deterministic:
+        out = FixedPointGradients.zeros(grid.num_vertices, dev, grid.num_tets if with_color else None)
+        convert = True
     if out is None:
         out = GradientBuffers.zeros(grid.num_vertices, dev, grid.num_tets if with_color else None)
+    fixed = isinstance(out, FixedPointGradients)
     K = len(scene)
     if K == 0 or saved.bins.num_pairs == 0:
-        return out
+        return out.to_float(stream=stream) if convert else out
     L = _native.lib()
     import ctypes
     maps = (ctypes.c_void_p * 4)(saved.maps.normal.data_ptr(), saved.maps.depth.data_ptr(),
@@ -271,14 +334,16 @@ def render_backward(saved: SavedState, scene: SplatScene, grid, field, camera, d
     dmaps = (ctypes.c_void_p * 4)(dn.data_ptr(), dd.data_ptr(), do.data_ptr(), dc.data_ptr() if with_color else None)
     if timing is not None:
         timing[0].record(stream if stream is not None else torch.cuda.current_stream())
-    _native.check(L.ts_render_backward(scene.abi(), K, _native.ptr(scene.colors), saved.bins.abi(),
-                                       saved.bins.num_pairs, camera.abi(), _native.ptr(saved.item_off),
-                                       _native.ptr(saved.pair_bits), _native.ptr(saved.pair_rec),
-                                       ctypes.cast(maps, ctypes.POINTER(ctypes.c_void_p)),
-                                       ctypes.cast(dmaps, ctypes.POINTER(ctypes.c_void_p)),
-                                       _native.ptr(saved.n_proc), _native.ptr(field.deformation), grid.resolution,
-                                       _native.ptr(out.d_vert), _native.ptr(out.d_color) if with_color else None,
-                                       _native.stream_ptr(stream)))
+    fn = L.ts_render_backward_fx if fixed else L.ts_render_backward
+    _native.check(fn(scene.abi(), K, _native.ptr(scene.colors), saved.bins.abi(),
+                     saved.bins.num_pairs, camera.abi(), _native.ptr(saved.item_off),
+                     _native.ptr(saved.pair_bits), _native.ptr(saved.pair_rec),
+                     ctypes.cast(maps, ctypes.POINTER(ctypes.c_void_p)),
+                     ctypes.cast(dmaps, ctypes.POINTER(ctypes.c_void_p)),
+                     _native.ptr(saved.n_proc), _native.ptr(field.deformation), grid.resolution,
+                     _native.ptr(out.fx if fixed else out.d_vert),
+                     (_native.ptr(out.fx_color if fixed else out.d_color)) if with_color else None,
+                     _native.stream_ptr(stream)))
     if timing is not None:
         timing[1].record(stream if stream is not None else torch.cuda.current_stream())
-    return out
+    return out.to_float(stream=stream) if convert else out

@@ -13,7 +13,7 @@ import ctypes
 import torch
 
 from . import _native
-from .raster import GradientBuffers, RenderMaps, DEFAULT_WINDOW
+from .raster import DEFAULT_WINDOW, FixedPointGradients, GradientBuffers, RenderMaps
 from .splat import T_STOP
 
 
@@ -74,9 +74,11 @@ class ViewRenderer:
         _native.check(self._L.ts_view_collect(self._ws, _native.ptr(status), _native.ptr(out5),
                                               _native.stream_ptr(stream)))
 
-    def backward(self, field, d_maps: RenderMaps, out: GradientBuffers, maps: RenderMaps | None = None,
+    def backward(self, field, d_maps: RenderMaps, out: GradientBuffers | FixedPointGradients,
+                 maps: RenderMaps | None = None,
                  stream=None, status: torch.Tensor | None = None) -> GradientBuffers:
-        """Accumulate the last view's dL/d(sdf, deform) (and dL/dcolor) into `out`.
+        """Accumulate the last view's dL/d(sdf, deform) (and dL/dcolor) into `out` (a
+        FixedPointGradients: bitwise-reproducible fixed-point accumulation).
 
         `status` (device f32, optional): incremented when a map gradient is non-finite — the
         fused path's form of raster.py:209-211, raised by the caller at its next sync
@@ -87,8 +89,11 @@ class ViewRenderer:
                     maps.color.data_ptr() if maps.color is not None else None)
         d = (P * 4)(d_maps.normal.data_ptr(), d_maps.depth.data_ptr(), d_maps.opacity.data_ptr(),
                     d_maps.color.data_ptr() if d_maps.color is not None else None)
-        _native.check(self._L.ts_view_backward(self._ws, _native.ptr(field.deformation),
-                                               ctypes.cast(m, ctypes.POINTER(P)), ctypes.cast(d, ctypes.POINTER(P)),
-                                               _native.ptr(out.d_vert), _native.ptr(out.d_color),
-                                               _native.ptr(status), _native.stream_ptr(stream)))
+        fixed = isinstance(out, FixedPointGradients)  # deterministic (fixed-point) accumulation
+        fn = self._L.ts_view_backward_fx if fixed else self._L.ts_view_backward
+        _native.check(fn(self._ws, _native.ptr(field.deformation),
+                         ctypes.cast(m, ctypes.POINTER(P)), ctypes.cast(d, ctypes.POINTER(P)),
+                         _native.ptr(out.fx if fixed else out.d_vert),
+                         _native.ptr(out.fx_color if fixed else out.d_color),
+                         _native.ptr(status), _native.stream_ptr(stream)))
         return out
