@@ -1147,7 +1147,6 @@ struct BwdSmem {
   static constexpr int GM = COLOR ? 7 : 4;    // map gradients per pixel (normal, depth, colour)
   Staged sh[kCh];
   float2 wg[kCap];      // items only — load: (alpha, 1-alpha); phase B: (w = T a, G)
-  float acc[kCh][AS];   // per-(tile, splat) gradient rows of the chunk
   float col[COLOR ? kCh : 1][3];  // colour variant only
   union {
     ChunkMask bmask[TS_TILE_PX];  // load + B: per pixel, chunk splats that blend (bit j)
@@ -1174,11 +1173,12 @@ static_assert(3 * (sizeof(BwdSmem<false>) + 1024) <= 228 * 1024, "backward: 3 CT
 
 // One warp, items [b0, b0 + m) of the chunk: face-hit backward of every item into its row,
 // then per run of equal splat (items are in pair order, i.e. grouped by splat) one lane per
-// component sums the run and adds it to the splat's row (shared atomics: a run may continue
-// in the neighbouring batch of another warp).
+// component sums the run and adds it to the splat's global row (zeroed per view) with one
+// RED.ADD.F32 — a splat's runs (in other batches, chunks and tiles) meet in L2; FP32 order
+// noise only, or int64 fixed point when DET (order-independent).
 template <bool COLOR, bool DET>
 __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, const float4* __restrict__ pair_rec,
-                                              int64_t ib0, long long* __restrict__ rows_fx,
+                                              int64_t ib0, float* __restrict__ rows,
                                               unsigned long long* __restrict__ fx_bad) {
   using SM = BwdSmem<COLOR>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1219,9 +1219,9 @@ __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, 
       float sum = 0.f;
       for (int i = s0; i < e0; ++i) sum += S.u.rows[warp][i][lane];
       if (DET)  // fixed point straight into the splat's row: order-independent
-        fx_add(rows_fx + (int64_t)S.sh[jj].k * SM::AS + lane, sum, fx_bad);
-      else
-        atomicAdd(&S.acc[jj][lane], sum);
+        fx_add(reinterpret_cast<long long*>(rows) + (int64_t)S.sh[jj].k * SM::AS + lane, sum, fx_bad);
+      else if (sum != 0.f)  // RED.ADD.F32 straight into the splat's row (L2)
+        atomicAdd(rows + (int64_t)S.sh[jj].k * SM::AS + lane, sum);
     }
   }
   __syncwarp();
@@ -1348,8 +1348,6 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
         }
       }
     }
-    if (!DET)
-      for (int i = threadIdx.x; i < n * SM::AS; i += TS_TILE_PX) (&S.acc[0][0])[i] = 0.f;
     cp_async_wait_all();
     if (threadIdx.x < kCh) prefetch_rec(S.pf, recs, maxproc - base - n);
     __syncthreads();
@@ -1408,20 +1406,9 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     __syncthreads();
     const int nitems = S.nitems;
     for (int b0 = warp * 32; b0 < nitems; b0 += TS_TILE_PX)
-      process_batch<COLOR, DET>(S, b0, min(32, nitems - b0), pair_rec, ib0, reinterpret_cast<long long*>(rows),
-                                fx_bad);
+      process_batch<COLOR, DET>(S, b0, min(32, nitems - b0), pair_rec, ib0, rows, fx_bad);
     __syncthreads();
     TS_PHASE(3);
-    // ---- the chunk's per-(tile, splat) rows, added into the splats' rows (zeroed per view;
-    //      a splat's tiles add in any order: FP32 rounding-level nondeterminism only) ----------
-    // (the deterministic variant added its rows in fixed point in process_batch)
-    for (int i = threadIdx.x; !DET && i < n * (SM::AS / 4); i += TS_TILE_PX) {
-      const int j = i / (SM::AS / 4), c = i % (SM::AS / 4);
-      const float4 v = reinterpret_cast<const float4*>(&S.acc[j][0])[c];
-      // the splat index from the list (S.sh may already hold the next chunk: staging threads
-      // do not wait for this loop)
-      red_add_v4(rows + (int64_t)__ldg(list + base + j) * SM::AS + 4 * c, v.x, v.y, v.z, v.w);
-    }
     base += n;
     TS_PHASE(4);
   }
