@@ -207,8 +207,9 @@ struct CullF {
       alpha_max_pass(f, s, 0.0, &am);
       out.amax[k] = am;
     }
-    out.rec[k] = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height);
-    if (out.prect) out.prect[k] = make_int2(out.rec[k].rx, out.rec[k].ry);
+    const SplatRec r = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height);
+    out.rec[k] = r;
+    if (out.prect) out.prect[k] = make_int2(r.rx, r.ry);
   }
 };
 
