@@ -194,6 +194,7 @@ struct Hit {
 __device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float py) {
   const float band = s.band;
   uint32_t m = s.flags & 16u;
+  float amin = INFINITY;  // smallest |min edge value| over the faces: within the band -> exact path
 #pragma unroll
   for (int fi = 0; fi < 4; ++fi) {
     const float u = fmaf(s.eux[fi], px, fmaf(s.euy[fi], py, s.cu[fi]));
@@ -201,9 +202,9 @@ __device__ __forceinline__ uint32_t face_mask(const Staged& s, float px, float p
     const float w = s.adet[fi] - u - v;
     const float mn = fminf(fminf(u, v), w);
     m |= mn > band ? (1u << fi) : 0u;
-    m |= (mn >= -band && !(mn > band)) ? 16u : 0u;
+    amin = fminf(amin, fabsf(mn));  // (a NaN edge value is ignored by fminf, as by the compares)
   }
-  return m;
+  return amin <= band ? (m | 16u) : m;
 }
 
 // Phase A2: entry / exit among the in-faces of mask m (face order, first hit seeds, strict
@@ -500,11 +501,13 @@ __device__ __forceinline__ bool tile_rect(int rx0, int rx1, int ry0, int ry1, in
 
 // Per-chunk pair table.
 struct RectTab {
-  int x0[kCh], y0[kCh], nx[kCh];
-  float inv[kCh];
-  int pre[kCh + 1];  // exclusive prefix of pair counts
+  // per splat, one 16-byte load for the pair decode: .x first pair (exclusive prefix of the
+  // pair counts), .y x0 | y0 << 16 (the clipped rectangle's first pixel), .z row length nx,
+  // .w 1/nx (float bits)
+  int4 rect[kCh];
   int wtot[kCh / 32], wok[kCh / 32];  // staging scan exchange
   int n;             // splats in this chunk
+  int total;         // pairs in this chunk
   int64_t ib0;       // global index of the chunk's first pair
   uint8_t jtab[kCap];  // splat of each pair
 };
@@ -566,22 +569,17 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
                                             const int64_t* __restrict__ item_off_tile) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int m = min(kCh, avail);
-  int cnt = 0;
+  int cnt = 0, x0 = 0, y0 = 0, nx = 1;
   cp_async_wait_all();
   if (t < m) {
     const int k = P.idx[t];
     stage<FOLD>(P.raw[t], k, sh[t]);
     const Staged& r = sh[t];
-    int x0, y0, nx;
     if (!tile_rect(r.rx0, r.rx1, r.ry0, r.ry1, tx0, ty0, x0, y0, nx, cnt)) {
       nx = 1;
       cnt = 0;
       x0 = y0 = 0;
     }
-    R.x0[t] = x0;
-    R.y0[t] = y0;
-    R.nx[t] = nx;
-    R.inv[t] = frcp((float)nx);
     if (color)
       for (int c = 0; c < 3; ++c) col[t][c] = colors[(int64_t)k * 3 + c];
   }
@@ -594,13 +592,14 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
   if (lane == 31) R.wtot[wid] = v;
   asm volatile("bar.sync 1, %0;" ::"n"(kCh));
   for (int w = 0; w < wid; ++w) v += R.wtot[w];
-  if (t < m) R.pre[t + 1] = v;
+  if (t < m) R.rect[t] = make_int4(v - cnt, x0 | (y0 << 16), nx, __float_as_int(frcp((float)nx)));
   // cut: the largest prefix with at most kCap pairs (one splat has <= 256 pairs)
   const unsigned ok = __ballot_sync(0xffffffffu, t < m && v <= kCap);
   if (lane == 0) R.wok[wid] = __popc(ok);
   asm volatile("bar.sync 1, %0;" ::"n"(kCh));
   int n = 0;
   for (int w = 0; w < kCh / 32; ++w) n += R.wok[w];
+  if (t == n - 1) R.total = v;
   if (t < n) {  // this splat's pair range of the pair -> splat table, word stores in the middle
     int a = v - cnt;
     for (; a < v && (a & 3); ++a) R.jtab[a] = (uint8_t)t;
@@ -609,7 +608,6 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
     for (; a < v; ++a) R.jtab[a] = (uint8_t)t;
   }
   if (t == 0) {
-    R.pre[0] = 0;
     R.n = n;
     R.ib0 = P.ib0;
   }
@@ -621,15 +619,16 @@ __device__ __forceinline__ int pair_splat(const RectTab& R, int it) { return R.j
 
 // pixel (tile-local index) of pair `it` of splat j
 __device__ __forceinline__ void pair_pixel(const RectTab& R, int j, int it, int& xi, int& yi) {
-  const int local = it - R.pre[j];
-  const int nx = R.nx[j];
-  const int yy = (int)(((float)local + 0.5f) * R.inv[j]);
-  xi = R.x0[j] + (local - yy * nx);
-  yi = R.y0[j] + yy;
+  const int4 r = R.rect[j];
+  const int local = it - r.x;
+  const int yy = (int)(((float)local + 0.5f) * __int_as_float(r.w));
+  xi = (r.y & 0xffff) + (local - yy * r.z);
+  yi = (r.y >> 16) + yy;
 }
 
 __device__ __forceinline__ int pair_index(const RectTab& R, int j, int xi, int yi) {
-  return R.pre[j] + (yi - R.y0[j]) * R.nx[j] + (xi - R.x0[j]);
+  const int4 r = R.rect[j];
+  return r.x + (yi - (r.y >> 16)) * r.z + (xi - (r.y & 0xffff));
 }
 
 struct FwdSmem {
@@ -653,7 +652,7 @@ struct FwdSmem {
 // word (flushed to pair_bits after the exact re-decisions), global pair record (backward)
 __device__ __forceinline__ void put_pair(FwdSmem& F, int it, int j, int q, const Blend& b, int64_t ib0,
                                          float4* __restrict__ pair_rec) {
-  TS_ASSERT(it >= 0 && it < F.R.pre[F.R.n] && j >= 0 && j < F.R.n && q >= 0 && q < TS_TILE_PX);
+  TS_ASSERT(it >= 0 && it < F.R.total && j >= 0 && j < F.R.n && q >= 0 && q < TS_TILE_PX);
   TS_ASSERT(ib0 + it < F.pair_end);
   const float2 c = encode(true, b);
   F.code[it] = c;
@@ -744,7 +743,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     if (threadIdx.x == 0) F.nex = 0;
     __syncthreads();
     TS_PHASE(0);
-    const int n = F.R.n, total = F.R.pre[n];
+    const int n = F.R.n, total = F.R.total;
     const int64_t ib0 = F.R.ib0;
     // ---- A: pair-parallel hit + opacity (FP32, error-bounded) ------------------------------
     //  A1: face containment of every pair (dense lanes); the pairs inside >= 2 faces or within
@@ -1311,7 +1310,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     S.u.bmask[pix] = 0ull;
     __syncthreads();
     TS_PHASE(0);
-    const int n = S.R.n, total = S.R.pre[n];
+    const int n = S.R.n, total = S.R.total;
     const int nblk = (total + TS_TILE_PX - 1) / TS_TILE_PX;  // <= kCap / 256
     const int64_t ib0 = S.R.ib0;
     // ---- load: blend bits (all words first), then the blending, not early-stopped pairs'
