@@ -1154,6 +1154,7 @@ struct BwdSmem {
   uint16_t items[kCap];  // C: the chunk's items (pair index) in pair order
   int wcnt[kCap / 32];   // items per 32-pair block -> exclusive offsets
   uint32_t lbits[kCap / 32];  // loaded (blending, not early-stopped) pairs, block k*8+warp
+  uint32_t wpre[kCap / 32 + 1];  // the chunk's blend-bit words, loaded by warps 2-4 during staging
   int lim[TS_TILE_PX];   // per pixel: list entries the forward consumed (n_proc)
   float gmap[TS_TILE_PX][GM];  // per pixel: dL/d(normal xyz, depth, colour) — read by phase C
   RectTab R;
@@ -1304,9 +1305,17 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     prefetch_idx(S.pf, list, item_off + lo, 0, maxproc);
     prefetch_rec(S.pf, recs, maxproc);
   }
+  // last blend-bit word of the tile's pair range (bounds the word prefetch)
+  const int64_t wlast = maxproc > 0 ? (item_off[starts[tile + 1]] - 1) >> 5 : 0;
   for (int base = 0; base < maxproc;) {
-    if (threadIdx.x < kCh)
+    if (threadIdx.x < kCh) {
       stage_chunk<false>(list, base, maxproc - base, S.pf, colors, COLOR, S.sh, S.col, S.R, tx0, ty0, item_off + lo);
+    } else if (threadIdx.x < kCh + kCap / 32 + 1) {
+      // the chunk's blend-bit words (at most kCap pairs from its first pair), loaded while the
+      // staging warps decode: the load phase reads them from shared memory
+      const int64_t w = (__ldg(item_off + lo + base) >> 5) + (threadIdx.x - kCh);
+      S.wpre[threadIdx.x - kCh] = w <= wlast ? __ldg(pair_bits + w) : 0u;
+    }
     S.u.bmask[pix] = 0ull;
     __syncthreads();
     TS_PHASE(0);
@@ -1320,7 +1329,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
 #pragma unroll
       for (int k = 0; k < kCap / TS_TILE_PX; ++k) {
         const int it = threadIdx.x + k * TS_TILE_PX;
-        wv[k] = (k < nblk && it < total) ? __ldg(pair_bits + ((ib0 + it) >> 5)) : 0u;
+        wv[k] = (k < nblk && it < total) ? S.wpre[((ib0 + it) >> 5) - (ib0 >> 5)] : 0u;
       }
 #pragma unroll
       for (int k = 0; k < kCap / TS_TILE_PX; ++k) {
