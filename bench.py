@@ -531,13 +531,15 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     # DRAM traffic, issue and FMA-pipe utilisation of the same kernel from the committed ncu
     # --set full capture (profiles/r02_ncu_compositing.json, else the round-1 traffic file)
     traffic, tsrc, ncu = None, None, None
-    key = {"render_forward": "void k_forward<0>", "render_backward": "void k_backward<0>"}[top]
+    keys = {"render_forward": ("void k_forward<0>",),
+            "render_backward": ("void k_backward<0, 0>", "void k_backward<0>")}[top]
     for fname in ("r02_ncu_compositing.json", "ncu_traffic.json"):
         tfile = os.path.join(ROOT, "profiles", fname)
         if not os.path.exists(tfile):
             continue
         tj = json.load(open(tfile))
-        if key in tj:
+        key = next((k for k in keys if k in tj), None)
+        if key is not None:
             traffic = tj[key]["dram_bytes_per_launch"]
             tsrc = f"profiles/{fname} <- {tj[key]['source']} ({key}, dram__bytes_read.sum + dram__bytes_write.sum)"
             ncu = {k: tj[key][k] for k in ("issue_active_pct", "fma_pipe_pct", "warps_active_pct", "top_stalls_pct")
