@@ -355,8 +355,13 @@ def run_gpu(args):
                 d_maps[vi].opacity.copy_(h_maps[vi][2], non_blocking=True)
                 view_ready[vi].record(copy_stream)
         step(s, views, maps_for, inputs_ready=deform_ready)
-        h_loss[0:1].copy_(step.eik_loss, non_blocking=True)
-        h_loss[1:2].copy_(step.nc_loss, non_blocking=True)
+        if world > 1:  # the regularizers are sharded: every rank holds partial loss sums
+            loss2 = torch.cat([step.eik_loss, step.nc_loss])
+            dist.all_reduce(loss2)
+            h_loss.copy_(loss2, non_blocking=True)
+        else:
+            h_loss[0:1].copy_(step.eik_loss, non_blocking=True)
+            h_loss[1:2].copy_(step.nc_loss, non_blocking=True)
 
     e2e_step()
     barrier()

@@ -186,6 +186,17 @@ int ts_normal_consistency_fx(const double* sdf, const double* deform, int32_t re
                              int64_t* d_vert_fx, double* loss, void* scratch, void* stream);
 int ts_fx_to_f32(const int64_t* fx, int64_t n, float* out, float* status, void* stream);
 
+/* Normal consistency of one z-slab of vertices (the per-batch regularizer sharded over ranks,
+ * SURVEY 8e): adds the gradient of vertex layers z0 <= z < z1 (ids [z0 (R+1)^2, z1 (R+1)^2)) and
+ * the penalty of the edges whose lower vertex lies there, computing each pass over the slab plus
+ * the halo layers it reads; slabs covering 0..R+1 sum to ts_normal_consistency's result (each
+ * vertex's gradient is formed by exactly one slab).  Exactly one of d_vert (f32 [N,4]) and
+ * d_vert_fx (fixed point, see ts_view_backward_fx) is given; scratch as for
+ * ts_normal_consistency_ws (nullable: stream-ordered allocation); loss is overwritten. */
+int ts_normal_consistency_slab(const double* sdf, const double* deform, int32_t resolution, double scale,
+                               float* d_vert, int64_t* d_vert_fx, double* loss, void* scratch, int32_t z0,
+                               int32_t z1, void* stream);
+
 /* Sync-free per-view path.  With capacities set (cap_M tile pairs, cap_P pixel pairs, cap_L the
  * longest tile list (0 = unbounded); cap_M or cap_P 0 = off)
  * ts_view_forward makes no host round trip: buffers are sized by the capacities (visible

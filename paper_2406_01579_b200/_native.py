@@ -91,6 +91,7 @@ def lib():
         "ts_eikonal_fx": ([P, P, I32, P, I64, D, P, P, P], ctypes.c_int),
         "ts_normal_consistency_fx": ([P, P, I32, D, P, P, P, P], ctypes.c_int),
         "ts_fx_to_f32": ([P, I64, P, P, P], ctypes.c_int),
+        "ts_normal_consistency_slab": ([P, P, I32, D, P, P, P, P, I32, I32, P], ctypes.c_int),
         "ts_workspace_set_caps": ([P, I64, I64, I64, P], ctypes.c_int),
         "ts_view_collect": ([P, P, P, P], ctypes.c_int),
         "ts_view_status": ([P, PI64, P], ctypes.c_int),

@@ -123,6 +123,9 @@ class StepConfig:
     # int64, so the step's gradients — and Adam's update — do not depend on atomic order,
     # lane scheduling or the number of ranks the views are split over
     deterministic: bool = False
+    # the per-batch regularizers split over the ranks (eikonal tets / normal-consistency vertex
+    # slabs) instead of all on rank 0
+    shard_regularizers: bool = True
 
 
 @dataclass
@@ -195,22 +198,32 @@ class FitStep:
             if inputs_ready is not None:
                 st.wait_event(inputs_ready)
             active.record_stream(st)
-        # regularizers once per batch, on rank 0 only (their gradient rides in the all-reduce);
-        # they depend only on the field, so they run on their own stream beside the views
-        # (every gradient kernel accumulates atomically)
-        rank0 = not (dist.is_available() and dist.is_initialized()) or dist.get_rank(self.group) == 0
-        if rank0:
+        # regularizers once per batch, sharded over the ranks (their gradient rides in the
+        # all-reduce): rank r takes the r-th slice of the eikonal's tets and the r-th z-slab of
+        # the normal-consistency vertices (SURVEY 8e "sharded by tet range"), so no rank carries
+        # the whole per-batch term; eik_loss / nc_loss hold this rank's partial sums (fit_field
+        # all-reduces them with the map losses).  They depend only on the field, so they run on
+        # their own stream beside the views (every gradient kernel accumulates atomically).
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+        rank, world = (dist.get_rank(self.group), dist.get_world_size(self.group)) if multi else (0, 1)
+        if not cfg.shard_regularizers and rank != 0:
+            rank, world = -1, 1  # rank-0-only mode: nothing here
+        if rank >= 0:
             with torch.cuda.stream(self.reg_stream):
                 if cfg.lambda_eik > 0:
                     if cfg.eik_all and self._all_tets is None:
                         self._all_tets = torch.arange(g.num_tets, dtype=torch.int32, device=active.device)
                     tets = self._all_tets if cfg.eik_all else active
+                    if world > 1:
+                        tets = tets[rank * tets.numel() // world:(rank + 1) * tets.numel() // world]
                     eikonal_loss_async(g, f, tets, self._acc, cfg.lambda_eik, self.eik_loss, self.reg_stream)
                 if cfg.lambda_nc > 0:
                     if self._nc_scratch is None:
                         self._nc_scratch = torch.empty(nc_scratch_bytes(g), dtype=torch.uint8, device=f.sdf.device)
+                    n = g.resolution + 1
+                    slab = (rank * n // world, (rank + 1) * n // world) if world > 1 else None
                     normal_consistency_loss_async(g, f, self._acc, cfg.lambda_nc, self.nc_loss, self.reg_stream,
-                                                  self._nc_scratch)
+                                                  self._nc_scratch, slab=slab)
         if cfg.sync_free:
             log = self._views_sync_free(s, list(views), d_maps_fn, active)
         else:

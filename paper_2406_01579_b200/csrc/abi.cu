@@ -341,6 +341,18 @@ int ts_normal_consistency_fx(const double* sdf, const double* deform, int32_t R,
   return check_cuda("ts_normal_consistency_fx");
 }
 
+int ts_normal_consistency_slab(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
+                               int64_t* d_vert_fx, double* loss, void* scratch, int32_t z0, int32_t z1,
+                               void* stream) {
+  if (!sdf || !deform || !loss || R < 1 || (!d_vert == !d_vert_fx) || z0 < 0 || z1 < z0 || z1 > R + 1)
+    return fail(TS_EINVAL, "ts_normal_consistency_slab: bad arguments");
+  if (!scratch) keep_pool_warm();
+  const Fx fx = d_vert_fx ? fx_of(R, d_vert_fx, nullptr) : Fx{};
+  ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream), scratch,
+                             d_vert_fx ? &fx : nullptr, z0, z1);
+  return check_cuda("ts_normal_consistency_slab");
+}
+
 int ts_fx_to_f32(const int64_t* fx, int64_t n, float* out, float* status, void* stream) {
   if (!fx || !out || n < 0) return fail(TS_EINVAL, "ts_fx_to_f32: bad arguments");
   ts_impl_fx_to_f32(reinterpret_cast<const long long*>(fx), n, out, status, ST(stream));

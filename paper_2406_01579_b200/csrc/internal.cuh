@@ -118,7 +118,8 @@ void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W
 void ts_impl_eikonal(const double* sdf, const double* deform, int R, const int32_t* tet_set, int64_t n, float scale,
                      float* d_vert, double* loss, cudaStream_t st, const ts::Fx* fx = nullptr);
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
-                                double* loss, cudaStream_t st, void* scratch = nullptr, const ts::Fx* fx = nullptr);
+                                double* loss, cudaStream_t st, void* scratch = nullptr, const ts::Fx* fx = nullptr,
+                                int z0 = 0, int z1 = -1);
 void ts_impl_fx_to_f32(const long long* fx, int64_t n, float* out, float* status, cudaStream_t st);
 int64_t ts_impl_nc_scratch_bytes(int R);
 int ts_impl_mt_count(const double* sdf, const double* deform, int R, int64_t* nv, int64_t* nt, cudaStream_t st);

@@ -164,9 +164,14 @@ __device__ __forceinline__ void t1_tet(const CellCorners& K, double4* __restrict
                           : make_double4(ddiv(g[0], nrm), ddiv(g[1], nrm), ddiv(g[2], nrm), 1.0);
 }
 
-__global__ void __launch_bounds__(256) k_nc_tet_normals(int64_t C, Grid G, const double* __restrict__ sdf,
+// Every pass runs over an index range (cells [c_lo, c_hi) / vertices [lo, hi), contiguous z-slabs
+// of the x-fastest ids): a rank computes the gradient of its vertex slab from its slab plus the
+// halo layers each pass reads (ts_impl_normal_consistency).
+__global__ void __launch_bounds__(256) k_nc_tet_normals(int64_t C, int64_t c_lo, int64_t c_hi, Grid G,
+                                                        const double* __restrict__ sdf,
                                                         const double* __restrict__ deform, double4* __restrict__ tn) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t c = c_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < c_hi;
+       c += (int64_t)gridDim.x * blockDim.x) {
     CellCorners K;
     load_cell((uint32_t)c, G, sdf, deform, K);
     t1_tet<0>(K, tn + c);
@@ -180,9 +185,10 @@ __global__ void __launch_bounds__(256) k_nc_tet_normals(int64_t C, Grid G, const
 
 // pass A: nv = normalized mean of incident unit normals, .w = |mean| (0 = undefined);
 // icnt = 1 / count (0 without a defined incident tet)
-__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, const double4* __restrict__ tn,
+__global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t lo, int64_t hi, Grid G,
+                                                           const double4* __restrict__ tn,
                                                            double4* __restrict__ nv, double* __restrict__ icnt) {
-  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+  for (int64_t vid = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < hi;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double s[3] = {0.0, 0.0, 0.0}, c = 0.0;
     for_incident_tets((uint32_t)vid, G, [&](uint32_t t, int) {
@@ -208,8 +214,11 @@ __global__ void __launch_bounds__(256) k_nc_vertex_normals(int64_t N, Grid G, co
 }
 
 // pass B: edge penalty and its gradient, pushed back through the vertex normalisation; the
-// result is stored pre-multiplied by 1/count (the factor the tet chain applies per vertex)
-__global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const double4* __restrict__ nv,
+// result is stored pre-multiplied by 1/count (the factor the tet chain applies per vertex).
+// Each edge's penalty is counted by its lower vertex, and only for vertices in [llo, lhi)
+// (the slab's own vertices: the halo's edges belong to the neighbouring slab).
+__global__ void __launch_bounds__(256) k_nc_edges(int64_t lo, int64_t hi, int64_t llo, int64_t lhi, Grid G,
+                                                  const double4* __restrict__ nv,
                                                   const double* __restrict__ icnt, double4* __restrict__ dmi,
                                                   double* __restrict__ loss) {
   const int64_t n = G.n;
@@ -217,10 +226,11 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const doubl
   const int64_t off[7] = {1, n, n + 1, n * n, n * n + 1, n * n + n, n * n + n + 1};
   const int ox[7] = {1, 0, 1, 0, 1, 0, 1}, oy[7] = {0, 1, 1, 0, 0, 1, 1}, oz[7] = {0, 0, 0, 1, 1, 1, 1};
   double local = 0.0;
-  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+  for (int64_t vid = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < hi;
        vid += (int64_t)gridDim.x * blockDim.x) {
     int x, y, z;
     vertex_xyz((uint32_t)vid, G, x, y, z);
+    const bool own = vid >= llo && vid < lhi;
     double d[3] = {0.0, 0.0, 0.0};
     const double4 A = nv[vid];
     const bool def = A.w != 0.0;
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(256) k_nc_edges(int64_t N, Grid G, const doubl
     for (int e = 0; e < 7; ++e) {
       const double4 B = nb[e];
       if (B.w == 0.0) continue;
-      local += dsub(1.0, dadd(dadd(dmul(A.x, B.x), dmul(A.y, B.y)), dmul(A.z, B.z)));
+      if (own) local += dsub(1.0, dadd(dadd(dmul(A.x, B.x), dmul(A.y, B.y)), dmul(A.z, B.z)));
       d[0] = dsub(d[0], B.x);
       d[1] = dsub(d[1], B.y);
       d[2] = dsub(d[2], B.z);
@@ -320,11 +330,13 @@ __device__ __forceinline__ void t2_tet(const CellCorners& K, const double4* __re
   *tg = og;
 }
 
-__global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t C, Grid G, const double* __restrict__ sdf,
+__global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t C, int64_t c_lo, int64_t c_hi, Grid G,
+                                                      const double* __restrict__ sdf,
                                                       const double* __restrict__ deform,
                                                       const double4* __restrict__ dmi, float4* __restrict__ tdf,
                                                       float4* __restrict__ tg) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t c = c_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < c_hi;
+       c += (int64_t)gridDim.x * blockDim.x) {
     CellCorners K;
     load_cell((uint32_t)c, G, sdf, deform, K);
     t2_tet<0>(K, dmi, tdf + c, tg + c);
@@ -337,10 +349,10 @@ __global__ void __launch_bounds__(256) k_nc_tet_chain(int64_t C, Grid G, const d
 }
 
 // pass C: per-vertex gather of the per-tet chain terms
-__global__ void __launch_bounds__(256) k_nc_grad(int64_t N, Grid G, const float4* __restrict__ tdf,
+__global__ void __launch_bounds__(256) k_nc_grad(int64_t lo, int64_t hi, Grid G, const float4* __restrict__ tdf,
                                                  const float4* __restrict__ tg, float scale,
                                                  float* __restrict__ d_vert, Fx fx) {
-  for (int64_t vid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < N;
+  for (int64_t vid = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; vid < hi;
        vid += (int64_t)gridDim.x * blockDim.x) {
     double ds = 0.0, dp[3] = {0.0, 0.0, 0.0};
     for_incident_tets((uint32_t)vid, G, [&](uint32_t t, int slot) {
@@ -462,8 +474,12 @@ int64_t ts_impl_nc_scratch_bytes(int R) {
 }
 
 // scratch: ts_impl_nc_scratch_bytes(R) bytes of device memory, or nullptr (stream-ordered pool)
+// z0 / z1: the vertex layers [z0, z1) whose gradient (and whose edges' penalty) this call adds
+// (default all); each pass covers the layers it needs: grad [z0, z1) <- tet chain cells
+// [z0 - 1, z1) <- edge terms [z0 - 1, z1 + 1) <- vertex normals [z0 - 2, z1 + 2) <- tet
+// normals cells [z0 - 3, z1 + 2), clamped to the grid.
 void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, float scale, float* d_vert,
-                                double* loss, cudaStream_t st, void* scratch, const Fx* fx) {
+                                double* loss, cudaStream_t st, void* scratch, const Fx* fx, int z0, int z1) {
   const int64_t n = R + 1, N = n * n * n, T = 6 * (int64_t)R * R * R;
   cudaMemsetAsync(loss, 0, sizeof(double), st);
   int64_t off[8];
@@ -478,12 +494,33 @@ void ts_impl_normal_consistency(const double* sdf, const double* deform, int R, 
   float4* tg = reinterpret_cast<float4*>(base + off[6]);
   const Grid G = make_grid(R);
   const int64_t C = T / 6;
-  const int vblocks = (int)((N + 255) / 256 < 148 * 8 ? (N + 255) / 256 : 148 * 8);
-  const int cblocks = (int)((C + 255) / 256 < 148 * 8 ? (C + 255) / 256 : 148 * 8);
-  k_nc_tet_normals<<<cblocks, 256, 0, st>>>(C, G, sdf, deform, tn);
-  k_nc_vertex_normals<<<vblocks, 256, 0, st>>>(N, G, tn, nv, icnt);
-  k_nc_edges<<<vblocks, 256, 0, st>>>(N, G, nv, icnt, dmi, loss);
-  k_nc_tet_chain<<<cblocks, 256, 0, st>>>(C, G, sdf, deform, dmi, tdf, tg);
-  k_nc_grad<<<vblocks, 256, 0, st>>>(N, G, tdf, tg, scale, d_vert, fx ? *fx : Fx{});
+  if (z1 < 0 || z1 > n) z1 = (int)n;
+  if (z0 < 0) z0 = 0;
+  auto vr = [&](int a, int b, int64_t& lo, int64_t& hi) {  // vertex layers [a, b) -> ids
+    lo = (int64_t)(a < 0 ? 0 : a) * n * n;
+    hi = (int64_t)(b > n ? n : b) * n * n;
+  };
+  auto cr = [&](int a, int b, int64_t& lo, int64_t& hi) {  // cell layers [a, b) -> ids
+    lo = (int64_t)(a < 0 ? 0 : a) * R * R;
+    hi = (int64_t)(b > R ? R : b) * R * R;
+  };
+  auto blocks = [](int64_t a, int64_t b) {
+    const int64_t k = (b - a + 255) / 256;
+    return (int)(k < 1 ? 1 : (k < 148 * 8 ? k : 148 * 8));
+  };
+  int64_t tn_lo, tn_hi, nv_lo, nv_hi, e_lo, e_hi, own_lo, own_hi, ch_lo, ch_hi;
+  cr(z0 - 3, z1 + 2, tn_lo, tn_hi);
+  vr(z0 - 2, z1 + 2, nv_lo, nv_hi);
+  vr(z0 - 1, z1 + 1, e_lo, e_hi);
+  vr(z0, z1, own_lo, own_hi);
+  cr(z0 - 1, z1, ch_lo, ch_hi);
+  if (z0 < z1) {
+    k_nc_tet_normals<<<blocks(tn_lo, tn_hi), 256, 0, st>>>(C, tn_lo, tn_hi, G, sdf, deform, tn);
+    k_nc_vertex_normals<<<blocks(nv_lo, nv_hi), 256, 0, st>>>(nv_lo, nv_hi, G, tn, nv, icnt);
+    k_nc_edges<<<blocks(e_lo, e_hi), 256, 0, st>>>(e_lo, e_hi, own_lo, own_hi, G, nv, icnt, dmi, loss);
+    k_nc_tet_chain<<<blocks(ch_lo, ch_hi), 256, 0, st>>>(C, ch_lo, ch_hi, G, sdf, deform, dmi, tdf, tg);
+    k_nc_grad<<<blocks(own_lo, own_hi), 256, 0, st>>>(own_lo, own_hi, G, tdf, tg, scale, d_vert, fx ? *fx : Fx{});
+  }
+  (void)N;
   if (!scratch) cudaFreeAsync(base, st);
 }

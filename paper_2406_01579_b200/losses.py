@@ -43,10 +43,19 @@ def normal_consistency_loss(grid, field, out: GradientBuffers | None = None, sca
     return float(loss.item()), out
 
 
-def normal_consistency_loss_async(grid, field, out, scale, loss, stream=None, scratch=None):
+def normal_consistency_loss_async(grid, field, out, scale, loss, stream=None, scratch=None, slab=None):
     """Sync-free variant; `scratch` (uint8 device tensor of nc_scratch_bytes(grid) bytes)
-    avoids per-call stream-ordered allocations."""
+    avoids per-call stream-ordered allocations.  `slab=(z0, z1)`: only the vertex layers
+    z0 <= z < z1 (their gradients and the penalty of the edges they start) — the regularizer
+    sharded over ranks; the slabs of all ranks sum to the full loss and gradient."""
     L = _native.lib()
+    if slab is not None:
+        fixed = isinstance(out, FixedPointGradients)
+        _native.check(L.ts_normal_consistency_slab(
+            _native.ptr(field.sdf), _native.ptr(field.deformation), grid.resolution, float(scale),
+            None if fixed else _native.ptr(out.d_vert), _native.ptr(out.fx) if fixed else None,
+            _native.ptr(loss), _native.ptr(scratch), int(slab[0]), int(slab[1]), _native.stream_ptr(stream)))
+        return
     if isinstance(out, FixedPointGradients):
         _native.check(L.ts_normal_consistency_fx(_native.ptr(field.sdf), _native.ptr(field.deformation),
                                                  grid.resolution, float(scale), _native.ptr(out.fx),
