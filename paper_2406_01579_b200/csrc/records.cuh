@@ -36,10 +36,132 @@ __host__ __device__ constexpr int face_vert(int fi, int j) {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Never-blend certificate ("back-facing splats").  The SDF is linear over the
+// tet: along the ray of pixel p (direction d_p scaled to unit depth from the camera centre o)
+// the SDF at depth z is f = A(p) z + f_lin(o) with A(p) = grad f . d_p affine in p, so
+// f_next - f_prev = A(p) (z_out - z_in).  When A > 0 at the four projected vertices
+// (A_i = grad f . (P_i - o) / z_i, hence over the whole hull) no ray through the tet sees the
+// SDF decrease, so the reference's alpha = 1 - exp(sp(-s f_prev) - sp(-s f_next)) is <= 0 —
+// up to its FP64 rounding, which can only matter where f_next - f_prev is tiny, i.e. near
+// the line of the edge e shared by the entry and exit faces F, B: with the w = 1/z planes
+// w_F, w_B of those faces, z_out - z_in = (w_F - w_B)(p) / (w_in w_out)
+// >= z_min^2 kappa_e dist(p, line e), kappa_e = |grad(w_F - w_B)| (w_F - w_B vanishes on e),
+// so f_next - f_prev >= A_min z_min^2 kappa_e dist(p, line e).  The certificate asks that no
+// pixel centre of the rectangle lies within r_e of any edge line, r_e covering the FP64 error
+// of the reference's f_prev - f_next (~1e-15 (1 + C M / |det|) max|f|, C the coordinate
+// magnitude, M the splat extent) and of its face-containment test (~1e-15 C M / |e|), both
+// taken 10^6 times larger, plus the FP32 error of this evaluation on the record's anchored
+// geometry (4e-5 px; gradients within 2%, enforced).  Then every pixel either misses the
+// hull (no two hits) or lies inside it away from all edges (exactly F and B hit,
+// f_next - f_prev > the error): no pixel of the splat blends in the reference, for any
+// steepness.  Its rectangle is emptied; the binning keeps the FP64 bbox, so tile lists, the
+// window and n_proc are unchanged.  About half of the splats of a closed surface face away
+// from the camera (tests/test_gpu_certificate.py: the certified set against the reference's
+// blends with early stop disabled).
+__device__ inline bool never_blends(const SplatRec& r, int nxr, int nyr, double amin, double C, double M,
+                                    double fabsmax, double fmx) {
+  // one exit, no early returns: lanes leave each edge's scan loop together (a divergent exit
+  // inside the unrolled edges kept warps at ~2 active lanes)
+  bool ok = nxr <= 64 && nyr <= 64;
+  float w[4], zmin = r.z[0], wmax = 0.f;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    ok &= r.z[v] > 0.f;
+    w[v] = __frcp_rn(r.z[v]);
+    zmin = fminf(zmin, r.z[v]);
+    wmax = fmaxf(wmax, w[v]);
+  }
+  float lmax = 0.f;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    const int va = e < 3 ? 0 : (e < 5 ? 1 : 2), vb = e < 3 ? e + 1 : (e < 5 ? e - 1 : 3);
+    lmax = fmaxf(lmax, hypotf(r.vx[vb] - r.vx[va], r.vy[vb] - r.vy[va]));
+  }
+  // 1/z plane gradients of the faces (pixel units) and their FP32 error bounds
+  float gx[4], gy[4], adet[4], gerr[4];
+#pragma unroll
+  for (int fi = 0; fi < 4; ++fi) {
+    const int ia = face_vert(fi, 0), ib = face_vert(fi, 1), ic = face_vert(fi, 2);
+    const float m00 = r.vx[ib] - r.vx[ia], m10 = r.vy[ib] - r.vy[ia];
+    const float m01 = r.vx[ic] - r.vx[ia], m11 = r.vy[ic] - r.vy[ia];
+    const float det = m00 * m11 - m01 * m10;
+    ok &= fabsf(det) > 1e-3f * lmax * lmax;  // thin face: not certified
+    const float inv = __frcp_rn(det), d1 = w[ib] - w[ia], d2 = w[ic] - w[ia];
+    gx[fi] = (d1 * m11 - m10 * d2) * inv;
+    gy[fi] = (m00 * d2 - m01 * d1) * inv;
+    adet[fi] = fabsf(det);
+    gerr[fi] = (5e-7f * wmax + 1e-5f * hypotf(gx[fi], gy[fi])) * 2.f * lmax * __frcp_rn(adet[fi]);
+  }
+  const float am = (float)amin, e64c = (float)(1e-9 * fabsmax), e64f = (float)(1e-9 * fmx);
+  const float cm = (float)(C * M);
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    const int va = e < 3 ? 0 : (e < 5 ? 1 : 2), vb = e < 3 ? e + 1 : (e < 5 ? e - 1 : 3);
+    // the two faces through edge (va, vb) omit the two other vertices
+    const int fa = (va != 0 && vb != 0) ? 0 : ((va != 1 && vb != 1) ? 1 : 2);
+    const int fb = 6 - va - vb - fa;
+    const float kappa = hypotf(gx[fa] - gx[fb], gy[fa] - gy[fb]);
+    ok &= kappa > 50.f * (gerr[fa] + gerr[fb]);
+    const float dx = r.vx[vb] - r.vx[va], dy = r.vy[vb] - r.vy[va];
+    const float len = hypotf(dx, dy), ilen = __frcp_rn(len);
+    const float e64 = e64c * (1.0f + cm * __frcp_rn(fminf(adet[fa], adet[fb]))) + e64f;
+    const float rad = fmaxf(2.f * e64 * __frcp_rn(am * zmin * zmin * kappa), 1e-9f * cm * ilen) + 4e-5f;
+    ok &= rad < 0.25f;  // (false on NaN)
+    const float nx = -dy * ilen, ny = dx * ilen;  // unit normal: dist(p) = |nx (px - xa) + ny (py - ya)|
+    const bool by_rows = fabsf(nx) >= fabsf(ny);
+    const int n_scan = ok ? (by_rows ? nyr : nxr) : 0;
+    const float n_across = (float)((by_rows ? nxr : nyr) - 1);
+    const float inu = __frcp_rn(by_rows ? nx : ny), slope = (by_rows ? ny : nx) * inu;
+    const float ua = by_rows ? r.vx[va] : r.vy[va], wa = by_rows ? r.vy[va] : r.vx[va];
+    const float half = rad * fabsf(inu) * 1.001f + 1e-6f;
+    bool near = false;
+    for (int i = 0; i < n_scan; ++i) {
+      const float c = ua - slope * (((float)i + 0.5f) - wa);  // the line's crossing of this row / column
+      const float j0 = ceilf(c - half - 0.5f), j1 = floorf(c + half - 0.5f);
+      near |= j0 <= j1 && j1 >= 0.f && j0 <= n_across;
+    }
+    ok &= !near;
+  }
+  return ok;
+}
+
+// A_min of the certificate from the projected vertices alone (scene_from_arrays): the SDF is
+// linear in Q = z (x, y, 1), a linear image of camera space, f = h.Q + f_lin(o), and
+// A_i = h.Q_i / z_i.  Returns 0 when the tet is not robustly back-facing.
+__device__ inline double backfacing_amin(const double proj[8], const double z[4], const double f[4]) {
+  double Q[4][3], a[3][3], b[3];
+  for (int v = 0; v < 4; ++v) {
+    Q[v][0] = z[v] * proj[2 * v];
+    Q[v][1] = z[v] * proj[2 * v + 1];
+    Q[v][2] = z[v];
+  }
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) a[i][j] = Q[i + 1][j] - Q[0][j];
+    b[i] = f[i + 1] - f[0];
+  }
+  const double c0 = a[1][1] * a[2][2] - a[1][2] * a[2][1], c1 = a[1][2] * a[2][0] - a[1][0] * a[2][2],
+               c2 = a[1][0] * a[2][1] - a[1][1] * a[2][0];
+  const double D = a[0][0] * c0 + a[0][1] * c1 + a[0][2] * c2;
+  double nrm = 1.0;
+  for (int i = 0; i < 3; ++i) nrm *= sqrt(a[i][0] * a[i][0] + a[i][1] * a[i][1] + a[i][2] * a[i][2]);
+  if (!(fabs(D) > 1e-9 * nrm)) return 0.0;
+  double h[3];
+  for (int c = 0; c < 3; ++c) {
+    double m[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) m[i][j] = j == c ? b[i] : a[i][j];
+    h[c] = (m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
+            m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0])) / D;
+  }
+  double amin = 1e300, hn = sqrt(h[0] * h[0] + h[1] * h[1] + h[2] * h[2]);
+  for (int v = 0; v < 4; ++v) amin = fmin(amin, (h[0] * Q[v][0] + h[1] * Q[v][1] + h[2] * Q[v][2]) / z[v]);
+  return amin > 1e-9 * hn ? amin : 0.0;
+}
+
 // Build the compact record from the FP64 scene values of one splat.
 __device__ inline SplatRec make_record(const double proj[8], const double depths[4], const double f[4],
                                        const double normal[3], double md, const double bbox[4],
-                                       int width, int height) {
+                                       int width, int height, double amin = 0.0) {
   SplatRec r;
   // pixel centres xi + 0.5 inside [xmin, xmax] (inclusive, _core.pyx:80): exact in FP64
   double fx0 = ceil(dsub(bbox[0], 0.5)), fx1 = floor(dsub(bbox[2], 0.5));
@@ -90,6 +212,22 @@ __device__ inline SplatRec make_record(const double proj[8], const double depths
   r.n[1] = (float)normal[1];
   r.n[2] = (float)normal[2];
   r.md = (float)md;
+#ifndef TS_NO_NEVER_BLEND
+  // certified never to blend (amin > 0: the caller found the tet back-facing): empty
+  // rectangle with the anchor kept, bit 5
+  if (amin > 0.0 && (r.flags & 31u) == 15u && ix0 <= ix1 && iy0 <= iy1) {
+    double C = 0.0, fabsmax = 0.0;
+    for (int v = 0; v < 4; ++v) {
+      C = fmax(C, fmax(fabs(proj[2 * v]), fabs(proj[2 * v + 1])));
+      fabsmax = fmax(fabsmax, fabs(f[v]));
+    }
+    const double fmx = fmax(fabs(f[1] - f[0]), fmax(fabs(f[2] - f[0]), fabs(f[3] - f[0])));
+    if (never_blends(r, ix1 - ix0 + 1, iy1 - iy0 + 1, amin, C + M, M, fabsmax, fmx)) {
+      r.rx = (ix0 & 0xffff) | ((ix0 - 1) << 16);
+      r.flags |= 32u;
+    }
+  }
+#endif
   return r;
 }
 

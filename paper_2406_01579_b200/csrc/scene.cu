@@ -207,7 +207,16 @@ struct CullF {
       alpha_max_pass(f, s, 0.0, &am);
       out.amax[k] = am;
     }
-    const SplatRec r = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height);
+    // never-blend certificate (records.cuh): A_i = grad f . (P_i - o) / z_i, o the camera centre
+    double amin = 1e300;
+    for (int c = 0; c < 4; ++c) {
+      double a = 0.0;
+      for (int q = 0; q < 3; ++q)
+        a += g[q] * (P[c][q] + (cam.R[q] * cam.t[0] + cam.R[3 + q] * cam.t[1] + cam.R[6 + q] * cam.t[2]));
+      amin = fmin(amin, a / z[c]);
+    }
+    const double gn2 = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    const SplatRec r = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height, amin > 1e-9 * gn2 ? amin : 0.0);
     out.rec[k] = r;
     if (out.prect) out.prect[k] = make_int2(r.rx, r.ry);
   }
@@ -223,7 +232,7 @@ __global__ void k_prepare_records(int64_t K, const double* __restrict__ proj, co
     for (int i = 0; i < 8; ++i) p[i] = proj[k * 8 + i];
     for (int i = 0; i < 4; ++i) { z[i] = depths[k * 4 + i]; ff[i] = f[k * 4 + i]; b[i] = bbox[k * 4 + i]; }
     for (int i = 0; i < 3; ++i) n[i] = normals[k * 3 + i];
-    rec[k] = make_record(p, z, ff, n, md[k], b, width, height);
+    rec[k] = make_record(p, z, ff, n, md[k], b, width, height, backfacing_amin(p, z, ff));
   }
 }
 
