@@ -62,7 +62,10 @@ typedef struct ts_bins {
   int32_t* items;     /* [M]    splat indices, sorted by (tile, q, index)   */
   int32_t* pos_of;    /* [M]    list position of each (splat, tile) pair     */
   uint8_t* nonmono;   /* [T]    1 when mean depth decreases along the list   */
-  int32_t* witems;    /* [M]    window-resorted lists (valid where nonmono)  */
+  int32_t* witems;    /* [M]    compositing lists: the window order without the */
+                      /*        entries whose pixel rectangle misses the tile  */
+  int32_t* cpos;      /* [M]    list position of each compositing-list entry   */
+  int32_t* clen;      /* [T]    compositing-list length per tile               */
 } ts_bins;
 
 const char* ts_last_error(void);

@@ -29,7 +29,8 @@ class ts_scene(ctypes.Structure):
 
 
 class ts_bins(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_void_p) for n in ("starts", "splat_off", "items", "pos_of", "nonmono", "witems")]
+    _fields_ = [(n, ctypes.c_void_p) for n in ("starts", "splat_off", "items", "pos_of", "nonmono", "witems", "cpos",
+                                                    "clen")]
 
 
 _lib = None

@@ -177,8 +177,10 @@ int ts_bin_sort(const double* bbox, const double* md, int64_t K, const ts_camera
 }
 
 static Scene64 s64_of(const ts_scene* sc) { return Scene64{sc->proj, sc->depths, sc->f, sc->bbox}; }
+// the compositing lists the forward writes and the backward / saved records read
+static bool lists_ok(const ts_bins* b, int64_t M) { return M <= 0 || (b->witems && b->cpos && b->clen); }
 static BinsView bv_of(const ts_bins* b) {
-  return BinsView{b->starts, b->splat_off, b->items, b->pos_of, b->nonmono, b->witems};
+  return BinsView{b->starts, b->splat_off, b->items, b->pos_of, b->nonmono, b->witems, b->cpos, b->clen};
 }
 
 int ts_forward_prepare(const ts_scene* sc, int64_t K, const ts_bins* b, int64_t M, const ts_camera* cam, int32_t n_w,
@@ -186,6 +188,7 @@ int ts_forward_prepare(const ts_scene* sc, int64_t K, const ts_bins* b, int64_t 
   if (n_w < 1) return fail(TS_EINVAL, "resorting window must be >= 1");
   if (!sc || !b || !cam || !item_off || !out_pairs || K < 0 || M < 0)
     return fail(TS_EINVAL, "ts_forward_prepare: bad arguments");
+  if (!lists_ok(b, M)) return fail(TS_EINVAL, "ts_forward_prepare: compositing lists (witems / cpos / clen) missing");
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   keep_pool_warm();
@@ -201,6 +204,7 @@ int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const 
   if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0 || n_pairs < 0 ||
       (M > 0 && (!item_off || !pair_bits || (n_pairs > 0 && !pair_rec))))
     return fail(TS_EINVAL, "ts_render_forward: bad arguments");
+  if (!lists_ok(b, M)) return fail(TS_EINVAL, "ts_render_forward: compositing lists (witems / cpos / clen) missing");
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   keep_pool_warm();
@@ -217,6 +221,7 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert || R < 1 || K < 0 || M < 0 ||
       (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_render_backward: bad arguments");
+  if (!lists_ok(b, M)) return fail(TS_EINVAL, "ts_render_backward: compositing lists (witems / cpos / clen) missing");
   for (int i = 0; i < 3; ++i)
     if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward: missing map");
   int tx, ty;
@@ -249,6 +254,7 @@ int ts_render_backward_fx(const ts_scene* sc, int64_t K, const float* colors, co
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert_fx || R < 1 || K < 0 || M < 0 ||
       (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_render_backward_fx: bad arguments");
+  if (!lists_ok(b, M)) return fail(TS_EINVAL, "ts_render_backward_fx: compositing lists (witems / cpos / clen) missing");
   for (int i = 0; i < 3; ++i)
     if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_render_backward_fx: missing map");
   int tx, ty;
@@ -278,6 +284,7 @@ int ts_saved_records(const ts_scene* sc, const ts_bins* b, const ts_camera* cam,
   if (!sc || !b || !cam || !n_proc || n_tiles < 0 || (n_tiles > 0 && (!tiles || !rec_off || !item_off ||
                                                                        !pair_bits || !pair_rec)))
     return fail(TS_EINVAL, "ts_saved_records: bad arguments");
+  if (!lists_ok(b, n_tiles)) return fail(TS_EINVAL, "ts_saved_records: compositing lists (witems / cpos / clen) missing");
   int tx, ty;
   if (int e = tiles_of(cam, TS_TILE, tx, ty)) return e;
   ts_impl_saved_records(tiles, n_tiles, tx, cam->width, cam->height, bv_of(b),
@@ -293,6 +300,7 @@ int ts_backward_tiles(const ts_scene* sc, int64_t K, const float* colors, const 
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !rows || K < 0 || M < 0 || n_tiles < 0 ||
       (n_tiles > 0 && !tiles) || (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_backward_tiles: bad arguments");
+  if (!lists_ok(b, M)) return fail(TS_EINVAL, "ts_backward_tiles: compositing lists (witems / cpos / clen) missing");
   for (int i = 0; i < 3; ++i)
     if (!maps[i] || !dmaps[i]) return fail(TS_EINVAL, "ts_backward_tiles: missing map");
   int tx, ty;

@@ -688,8 +688,8 @@ __device__ __forceinline__ void a2_candidates(FwdSmem& F, const uint16_t* cq, in
 
 template <bool COLOR>
 __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
-    const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
-    const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
+    const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ cpos, const int32_t* __restrict__ witems,
+    const int32_t* __restrict__ clen, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     Scene64 S64, int tiles_x, int W, int H, float s, double s64, float t_stop, bool clip_stops,
     const int64_t* __restrict__ item_off,
     uint32_t* __restrict__ pair_bits, float4* __restrict__ pair_rec, float* __restrict__ normal_map, float* __restrict__ depth_map, float* __restrict__ opacity_map,
@@ -717,8 +717,11 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
   const bool inside = xi < W && yi < H;
   const int64_t lo = starts[tile];
-  const int L = (int)(starts[tile + 1] - lo);
-  const int32_t* list = (nonmono[tile] ? witems : items) + lo;
+  // the compositing list: the tile's list (window order) without the splats whose pixel
+  // rectangle misses the tile (k_window_counts); cp = their list positions
+  const int L = clen[tile];
+  const int32_t* list = witems + lo;
+  const int32_t* cp = cpos + lo;
 #ifdef TS_BOUNDS_CHECKS
   if (threadIdx.x == 0) F.pair_end = item_off[lo + L];
 #endif
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
   Accum<COLOR> acc;
   acc.zero();
   bool done = !inside;
-  int nproc = inside ? L : 0, nb = 0;
+  int nproc = inside ? (int)(starts[tile + 1] - lo) : 0, nb = 0;
   {
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
@@ -837,7 +840,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
         // 1 - ALPHA_CLIP < t_stop (T <= 1), which FP32 T = 1e-4f would not see at T = 1
         if (T < t_stop || (c.y < 0.f && clip_stops)) {
           done = true;
-          nproc = base + j + 1;
+          nproc = cp[base + j] + 1;  // list entries consumed (the reference's position)
           break;
         }
       }
@@ -945,7 +948,7 @@ __global__ void k_list_flags(int T, const int64_t* __restrict__ starts, const in
 // order with their clipped alpha, at rec_off[tile index * 256 + pixel].
 __global__ void __launch_bounds__(TS_TILE_PX) k_saved_records(
     const int32_t* __restrict__ tiles, int tiles_x, int W, int H, const int64_t* __restrict__ starts,
-    const int32_t* __restrict__ items, const int32_t* __restrict__ witems, const uint8_t* __restrict__ nonmono,
+    const int32_t* __restrict__ cpos, const int32_t* __restrict__ witems, const int32_t* __restrict__ clen,
     const SplatRec* __restrict__ recs, const int64_t* __restrict__ item_off, const uint32_t* __restrict__ pair_bits,
     const float4* __restrict__ pair_rec, const int32_t* __restrict__ n_proc, const int64_t* __restrict__ rec_off,
     int64_t* __restrict__ idx_out, double* __restrict__ alpha_out) {
@@ -954,10 +957,11 @@ __global__ void __launch_bounds__(TS_TILE_PX) k_saved_records(
   const int xi = tx0 + (threadIdx.x & (TS_TILE - 1)), yi = ty0 + (threadIdx.x / TS_TILE);
   if (xi >= W || yi >= H) return;
   const int64_t lo = starts[tile];
-  const int32_t* list = (nonmono[tile] ? witems : items) + lo;
-  const int np = n_proc[(int64_t)yi * W + xi];
+  const int32_t* list = witems + lo;
+  const int32_t* cp = cpos + lo;
+  const int np = n_proc[(int64_t)yi * W + xi], Lc = clen[tile];
   int64_t o = rec_off[(int64_t)blockIdx.x * TS_TILE_PX + threadIdx.x];
-  for (int j = 0; j < np; ++j) {
+  for (int j = 0; j < Lc && cp[j] < np; ++j) {
     const int k = list[j];
     const int2 rr = *reinterpret_cast<const int2*>(recs + k);
     int x0, y0, nx, c;
@@ -986,7 +990,8 @@ __global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const
                                                        const SplatRec* __restrict__ recs, int32_t* __restrict__ cnt,
                                                        int32_t* __restrict__ widx_s, double* __restrict__ wz_s,
                                                        bool q_ready, const int* __restrict__ ovf,
-                                                       const int2* __restrict__ prect) {
+                                                       const int2* __restrict__ prect, int32_t* __restrict__ cpos,
+                                                       int32_t* __restrict__ clen) {
   const int t = blockIdx.x;
   if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
@@ -999,15 +1004,46 @@ __global__ void __launch_bounds__(256) k_window_counts(int T, int tiles_x, const
                 q_ready);
   const int tx0 = (t % tiles_x) * TS_TILE, ty0 = (t / tiles_x) * TS_TILE;
   const int32_t* list = nm ? witems : items;
-  for (int64_t p = lo + threadIdx.x; p < lo + L; p += blockDim.x) {
-    // the 8-byte rectangle: from the compact array when the scene build wrote one (one 32-byte
-    // sector holds four), else from the 96-byte record
-    const int2 rr = prect ? __ldg(prect + list[p]) : *reinterpret_cast<const int2*>(recs + list[p]);
-    int x0, y0, nx, c = 0;
-    tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0, y0, nx,
-              c);
-    cnt[p] = c;
+  // the compositing list: the positions whose pixel rectangle meets the tile (splats certified
+  // never to blend have none, records.cuh), in list order, with their list positions (cpos)
+  // and pair counts — a stable compaction in rounds of 256 positions, each round reading its
+  // entries before any write (witems is compacted in place); the tail counts are zero, so the
+  // pair numbering (item_off) is that of the compositing list
+  __shared__ int wc[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int kept = 0;
+  for (int64_t p0 = 0; p0 < L; p0 += 256) {
+    const int64_t p = p0 + threadIdx.x;
+    int c = 0, k = 0;
+    if (p < L) {
+      k = list[lo + p];
+      // the 8-byte rectangle: from the compact array when the scene build wrote one (one
+      // 32-byte sector holds four), else from the 96-byte record
+      const int2 rr = prect ? __ldg(prect + k) : *reinterpret_cast<const int2*>(recs + k);
+      int x0, y0, nx;
+      tile_rect((int)(short)(rr.x & 0xffff), rr.x >> 16, (int)(short)(rr.y & 0xffff), rr.y >> 16, tx0, ty0, x0, y0,
+                nx, c);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, c > 0);
+    if (lane == 0) wc[warp] = __popc(m);
+    __syncthreads();
+    int off = kept, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      off += w < warp ? wc[w] : 0;
+      tot += wc[w];
+    }
+    if (c > 0) {
+      off += __popc(m & ((1u << lane) - 1u));
+      witems[lo + off] = k;
+      cpos[lo + off] = (int32_t)p;
+      cnt[lo + off] = c;
+    }
+    kept += tot;
+    __syncthreads();
   }
+  for (int64_t p = kept + threadIdx.x; p < L; p += blockDim.x) cnt[lo + p] = 0;
+  if (threadIdx.x == 0) clen[t] = kept;
 }
 
 // the window of one non-monotone tile (all threads of the CTA; ends with a barrier)
@@ -1072,15 +1108,15 @@ __device__ void window_tile(int t, int64_t lo, int64_t L, const int32_t* __restr
 // Launch order of the compositing CTAs: tiles by decreasing list length (16-entry buckets),
 // so the long tiles start first and the short ones fill the tail (results do not depend on
 // the order).  One CTA, shared-memory counting sort.
-__global__ void __launch_bounds__(1024) k_tile_order(int T, const int64_t* __restrict__ starts,
+__global__ void __launch_bounds__(1024) k_tile_order(int T, const int32_t* __restrict__ clen,
                                                     int32_t* __restrict__ order) {
   __shared__ int cnt[1024];
   __shared__ int wsum[32];
   cnt[threadIdx.x] = 0;
   __syncthreads();
   auto bucket = [&](int t) {
-    const int64_t L = starts[t + 1] - starts[t];
-    return 1023 - (int)(L >> 4 < 1023 ? L >> 4 : 1023);
+    const int L = clen[t];
+    return 1023 - (L >> 4 < 1023 ? L >> 4 : 1023);
   };
   for (int t = threadIdx.x; t < T; t += 1024) atomicAdd(&cnt[bucket(t)], 1);
   __syncthreads();
@@ -1229,8 +1265,8 @@ __device__ __forceinline__ void process_batch(BwdSmem<COLOR>& S, int b0, int m, 
 
 template <bool COLOR, bool DET>
 __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
-    const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ items, const int32_t* __restrict__ witems,
-    const uint8_t* __restrict__ nonmono, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
+    const int32_t* __restrict__ torder, const int64_t* __restrict__ starts, const int32_t* __restrict__ cpos, const int32_t* __restrict__ witems,
+    const int32_t* __restrict__ clen, const SplatRec* __restrict__ recs, const float* __restrict__ colors,
     int tiles_x, int W, int H, const int64_t* __restrict__ item_off, const uint32_t* __restrict__ pair_bits,
     const float4* __restrict__ pair_rec, const float* __restrict__ normal_map,
     const float* __restrict__ depth_map, const float* __restrict__ opacity_map, const float* __restrict__ color_map,
@@ -1254,13 +1290,26 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   const int xi = tx0 + (pix & (TS_TILE - 1)), yi = ty0 + (pix / TS_TILE);
   const bool inside = xi < W && yi < H;
   const int64_t lo = starts[tile];
-  const int32_t* list = (nonmono[tile] ? witems : items) + lo;
+  const int32_t* list = witems + lo;  // the compositing list (k_window_counts)
   const int64_t p = inside ? (int64_t)yi * W + xi : 0;
-  const int nproc = inside ? n_proc[p] : 0;
+  const int np_list = inside ? n_proc[p] : 0;
 #ifdef TS_BOUNDS_CHECKS
   if (threadIdx.x == 0) S.pair_end = item_off[starts[tile + 1]];
-  TS_ASSERT(nproc >= 0 && nproc <= starts[tile + 1] - lo);
+  TS_ASSERT(np_list >= 0 && np_list <= starts[tile + 1] - lo);
 #endif
+  // list entries consumed -> compositing-list entries consumed: entries with list position
+  // below n_proc (cpos increases along the compositing list)
+  int nproc = 0;
+  if (np_list > 0) {
+    const int32_t* cp = cpos + lo;
+    int a = 0, b = clen[tile];
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (__ldg(cp + mid) < np_list) a = mid + 1;
+      else b = mid;
+    }
+    nproc = a;
+  }
   if (threadIdx.x == 0) S.maxproc = 0;
   S.lim[pix] = nproc;
   __syncthreads();
@@ -1586,7 +1635,7 @@ int64_t ts_impl_forward_prepare(int tiles_x, int tiles_y, const BinsView& b, int
   int64_t* scratch = take_tmp(sc.scan, compact_blocks(M), st);
   const int* ovf = dyn ? dyn->ovf : nullptr;
   k_window_counts<<<T, 256, 0, st>>>(T, tiles_x, b.starts, b.items, b.nonmono, md, n_w, near_, far_, b.witems, rec,
-                                     cnt, widx, wz, q_ready && sc.cnt, ovf, prect);
+                                     cnt, widx, wz, q_ready && sc.cnt, ovf, prect, b.cpos, b.clen);
   scan_counts(cnt, M, item_off, scratch, st, dyn ? M_dev : nullptr, ovf);
   if (dyn) {
     put_tmp(widx, sc.widx, st);
@@ -1622,14 +1671,14 @@ void ts_impl_forward(int tiles_x, int tiles_y, const BinsView& b, const SplatRec
   }();
   (void)attr;
   int32_t* torder = take_tmp(given_order, T, st);
-  k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
+  k_tile_order<<<1, 1024, 0, st>>>(T, b.clen, torder);
   const bool clip_stops = (1.0 - kAlphaClipD) < t_stop;  // splat.py:14-15: T (1 - ALPHA_CLIP) < T_STOP
   if (colors && cmap)
-    k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, colors, S64, tiles_x,
+    k_forward<true><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.cpos, b.witems, b.clen, rec, colors, S64, tiles_x,
                                                 W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
                                                 nmap, dmap, omap, cmap, n_proc, n_blend, ovf);
   else
-    k_forward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.items, b.witems, b.nonmono, rec, nullptr, S64,
+    k_forward<false><<<T, TS_TILE_PX, smem, st>>>(torder, b.starts, b.cpos, b.witems, b.clen, rec, nullptr, S64,
                                                  tiles_x, W, H, (float)s, s, (float)t_stop, clip_stops, item_off, pair_bits, pair_rec,
                                                  nmap, dmap, omap, nullptr, n_proc, n_blend, ovf);
   put_tmp(torder, given_order, st);
@@ -1665,14 +1714,14 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   float* rows = take_tmp(given_rows, (det ? 2 : 1) * kGr * (size_t)M, st);
   int32_t* torder = take_tmp(given_order, T, st);
   // the fused view path's workspace still holds this view's order from its forward
-  if (!given_order) k_tile_order<<<1, 1024, 0, st>>>(T, b.starts, torder);
+  if (!given_order) k_tile_order<<<1, 1024, 0, st>>>(T, b.clen, torder);
   const bool color = colors && maps[3] && dmaps[3] && (det ? fx->color != nullptr : (d_color || rows_out));
   if (!rows_out)
     cudaMemsetAsync(rows, 0,
                     (det ? 8 : 4) * (size_t)(color ? BwdSmem<true>::AS : BwdSmem<false>::AS) * (size_t)K, st);
   unsigned long long* bad = det ? fx->bad : nullptr;
 #define TS_BWD_ARGS(C)                                                                                              \
-  torder, b.starts, b.items, b.witems, b.nonmono, rec, C ? colors : nullptr, tiles_x, cam.width, cam.height,         \
+  torder, b.starts, b.cpos, b.witems, b.clen, rec, C ? colors : nullptr, tiles_x, cam.width, cam.height,         \
       item_off, pair_bits, pair_rec, maps[0], maps[1], maps[2], C ? maps[3] : nullptr, dmaps[0], dmaps[1], dmaps[2], \
       C ? dmaps[3] : nullptr, n_proc, rows, status, ovf, bad
   if (color && det)
@@ -1719,7 +1768,7 @@ void ts_impl_saved_records(const int32_t* tiles, int n_tiles, int tiles_x, int W
                            const float4* pair_rec, const int32_t* n_proc, const int64_t* rec_off, int64_t* idx,
                            double* alpha, cudaStream_t st) {
   if (n_tiles <= 0) return;
-  k_saved_records<<<n_tiles, TS_TILE_PX, 0, st>>>(tiles, tiles_x, W, H, b.starts, b.items, b.witems, b.nonmono, rec,
+  k_saved_records<<<n_tiles, TS_TILE_PX, 0, st>>>(tiles, tiles_x, W, H, b.starts, b.cpos, b.witems, b.clen, rec,
                                                   item_off, pair_bits, pair_rec, n_proc, rec_off, idx, alpha);
 }
 

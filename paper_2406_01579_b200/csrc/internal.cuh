@@ -66,7 +66,9 @@ struct BinsView {
   const int32_t* items;
   const int32_t* pos_of;
   const uint8_t* nonmono;
-  int32_t* witems;
+  int32_t* witems;  // the compositing lists (k_window_counts)
+  int32_t* cpos;    // [M] list position of each compositing-list entry
+  int32_t* clen;    // [T] compositing-list length per tile
 };
 
 }  // namespace ts

@@ -48,7 +48,7 @@ struct ts_workspace {
   // scene
   Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors, prect;
   // bins
-  Buf starts, splat_off, items, pos_of, nonmono, witems, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
+  Buf starts, splat_off, items, pos_of, nonmono, witems, cpos, clen, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
   // forward state
   Buf item_off, pair_bits, pair_rec, n_proc, n_blend;
   // per-view temporaries (kept so no view in flight allocates from the shared pool)
@@ -179,7 +179,7 @@ void ts_workspace_destroy(ts_workspace* ws) {
   if (!ws) return;
   Buf* all[] = {&ws->prect, &ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
                 &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
-                &ws->nonmono, &ws->witems, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
+                &ws->nonmono, &ws->witems, &ws->cpos, &ws->clen, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
                 &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
                 &ws->n_proc, &ws->widx, &ws->wz, &ws->pcnt, &ws->pscan, &ws->torder, &ws->rows, &ws->n_blend};
   cudaDeviceSynchronize();
@@ -229,6 +229,8 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   int32_t* items = ws->items.get<int32_t>(capM);
   int32_t* pos_of = ws->pos_of.get<int32_t>(capM);
   int32_t* witems = ws->witems.get<int32_t>(capM);
+  int32_t* cpos = ws->cpos.get<int32_t>(capM);
+  int32_t* clen = ws->clen.get<int32_t>(T);
   uint64_t* keys = ws->keys.get<uint64_t>(capM);
   uint64_t* gs = ws->capL > 16384 || ws->capL == 0 ? ws->gsort.get<uint64_t>(2 * capM) : keys;  // unused <= 16384
   int32_t* pcnt = ws->pcnt.get<int32_t>(capM);
@@ -245,7 +247,7 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(capP));
   float4* prec = ws->pair_rec.get<float4>(capP);
   if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !splat_off || !nonmono || !items ||
-      !pos_of || !witems || !keys || !gs || !pcnt || !item_off || !n_proc || !n_blend || !scr.widx || !scr.wz ||
+      !pos_of || !witems || !cpos || !clen || !keys || !gs || !pcnt || !item_off || !n_proc || !n_blend || !scr.widx || !scr.wz ||
       !scr.scan || !scr.torder || !scr.rows || !pbits || !prec)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   ts_impl_bin_count(cap, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, nullptr, nullptr, st, &dyn);
@@ -255,7 +257,7 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   k_caps_check<<<1, 1, 0, st>>>(starts + T, capM, ovf, need + 1, w.dev_i64 + 1, need + 3, capL, nullptr, nullptr);
   ts_impl_bin_sort(cap, tx, ty, so.md, w, starts, splat_off, capL, keys, gs, items, pos_of, nonmono, st,
                    reinterpret_cast<uint32_t*>(pcnt), &dyn);
-  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems};
+  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems, cpos, clen};
   const float* colors = nullptr;
   if (colors_tet && cmap) {
     float* c = ws->colors.get<float>(cap * 3);
@@ -335,9 +337,11 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   int32_t* items = ws->items.get<int32_t>(M);
   int32_t* pos_of = ws->pos_of.get<int32_t>(M);
   int32_t* witems = ws->witems.get<int32_t>(M);
+  int32_t* cpos = ws->cpos.get<int32_t>(M);
+  int32_t* clen = ws->clen.get<int32_t>(T);
   uint64_t* keys = ws->keys.get<uint64_t>(M);
   uint64_t* gs = maxL > 16384 ? ws->gsort.get<uint64_t>(2 * M) : nullptr;
-  if (!items || !pos_of || !witems || !keys || (maxL > 16384 && !gs))
+  if (!items || !pos_of || !witems || !cpos || !clen || !keys || (maxL > 16384 && !gs))
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   // the sort also writes each position's depth key into the pair-count scratch, which k_window
   // reads (each tile before k_window_counts overwrites it with the tile's pair counts)
@@ -347,7 +351,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
     ts_impl_bin_sort(K, tx, ty, so.md, w, starts, splat_off, maxL, keys, gs, items, pos_of, nonmono, st,
                      reinterpret_cast<uint32_t*>(pcnt));
   else cudaMemsetAsync(nonmono, 0, T, st);
-  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems};
+  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems, cpos, clen};
   // ---- colors of the visible splats ------------------------------------------------------
   const float* colors = nullptr;
   if (colors_tet && cmap && K > 0) {
@@ -431,7 +435,8 @@ static int view_backward(ts_workspace* ws, const double* deform, const float* co
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], ws->color ? dmaps[3] : nullptr};
   BinsView bv{reinterpret_cast<int64_t*>(ws->starts.p), reinterpret_cast<int64_t*>(ws->splat_off.p),
               reinterpret_cast<int32_t*>(ws->items.p), reinterpret_cast<int32_t*>(ws->pos_of.p),
-              reinterpret_cast<uint8_t*>(ws->nonmono.p), reinterpret_cast<int32_t*>(ws->witems.p)};
+              reinterpret_cast<uint8_t*>(ws->nonmono.p), reinterpret_cast<int32_t*>(ws->witems.p),
+              reinterpret_cast<int32_t*>(ws->cpos.p), reinterpret_cast<int32_t*>(ws->clen.p)};
   ts_impl_backward(ws->tiles_x, ws->tiles_y, bv, ws->M, ws->K, reinterpret_cast<SplatRec*>(ws->rec.p),
                    ws->color ? reinterpret_cast<float*>(ws->colors.p) : nullptr,
                    reinterpret_cast<double*>(ws->f.p), reinterpret_cast<int32_t*>(ws->vert_ids.p),

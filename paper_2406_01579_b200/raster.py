@@ -69,8 +69,10 @@ class TileBins:
     splat_off: torch.Tensor  # (K+1,) int64
     pos_of: torch.Tensor     # (M,) int32
     nonmono: torch.Tensor    # (T,) uint8
-    witems: torch.Tensor     # (M,) int32
+    witems: torch.Tensor     # (M,) int32 — compositing lists (written by each forward)
     max_len: int = 0
+    cpos: torch.Tensor | None = None  # (M,) int32 list position of each compositing entry
+    clen: torch.Tensor | None = None  # (T,) int32 compositing-list length per tile
 
     @property
     def num_tiles(self) -> int:
@@ -89,8 +91,9 @@ class TileBins:
 
     def abi(self) -> _native.ts_bins:
         b = _native.ts_bins()
-        for n in ("starts", "splat_off", "items", "pos_of", "nonmono", "witems"):
-            setattr(b, n, getattr(self, n).data_ptr())
+        for n in ("starts", "splat_off", "items", "pos_of", "nonmono", "witems", "cpos", "clen"):
+            t = getattr(self, n)
+            setattr(b, n, t.data_ptr() if t is not None else None)
         return b
 
 
@@ -252,9 +255,12 @@ def render_forward(scene: SplatScene, bins: TileBins, camera, n_w: int = DEFAULT
                 t.zero_()
     else:
         sp = _native.stream_ptr(stream)
-        # the window-resorted lists belong to this forward (a later forward on the same bins
-        # with another n_w must not change the order this SavedState's backward walks)
-        bins = dataclasses.replace(bins, witems=torch.empty(M, dtype=torch.int32, device=dev))
+        # the compositing lists (window order, with their list positions) belong to this
+        # forward: a later forward on the same bins with another n_w must not change the
+        # order this SavedState's backward walks
+        bins = dataclasses.replace(bins, witems=torch.empty(M, dtype=torch.int32, device=dev),
+                                   cpos=torch.empty(M, dtype=torch.int32, device=dev),
+                                   clen=torch.empty(bins.num_tiles, dtype=torch.int32, device=dev))
         sc_abi, b_abi, cam = scene.abi(), bins.abi(), camera.abi()
         item_off = torch.empty(M + 1, dtype=torch.int64, device=dev)
         npairs = _native.i64()
