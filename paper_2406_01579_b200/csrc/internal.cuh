@@ -16,6 +16,10 @@ struct SceneOut {
   double* bbox;       // [K,4]
   SplatRec* rec;      // [K]
   int2* prect = nullptr;  // [K] (nullable): the record's packed pixel rectangle (rx, ry) alone
+  // [kQBitWords] (nullable, the fused view path): bit qhash(q) set for every splat with a
+  // non-empty pixel rectangle (q its 32-bit depth key) — k_bin_count leaves out the splats
+  // with an empty rectangle whose depth key no such splat shares (records.cuh)
+  uint32_t* qbits = nullptr;
 };
 
 struct BinRec {  // 16 B per splat: first tile and tile-rect extent
@@ -86,7 +90,8 @@ void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths
                              ts::SplatRec* rec, cudaStream_t st);
 void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tiles_x, int tiles_y, double near_,
                        double far_, const ts::BinWork& w, int64_t* starts, int64_t* splat_off, int64_t* M_out,
-                       int64_t* maxL_out, cudaStream_t st, const ts::Dyn* dyn = nullptr);
+                       int64_t* maxL_out, cudaStream_t st, const ts::Dyn* dyn = nullptr,
+                       const int2* prect = nullptr, const uint32_t* qbits = nullptr);
 void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, const ts::BinWork& w,
                       const int64_t* starts, const int64_t* splat_off, int64_t maxL, uint64_t* keys,
                       uint64_t* gscratch, int32_t* items, int32_t* pos_of, uint8_t* nonmono, cudaStream_t st,

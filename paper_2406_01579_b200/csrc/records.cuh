@@ -158,6 +158,29 @@ __device__ inline double backfacing_amin(const double proj[8], const double z[4]
   return amin > 1e-9 * hn ? amin : 0.0;
 }
 
+// 32-bit depth key of a mean depth (raster.py:132-134, FP64, numpy order)
+__device__ __forceinline__ uint32_t depth_key(double md, double near_, double far_) {
+  double qq = ddiv(dsub(md, near_), dsub(far_, near_));
+  qq = qq < 0.0 ? 0.0 : qq;
+  qq = qq > 1.0 ? 1.0 : qq;
+  return (uint32_t)(unsigned long long)dmul(qq, 4294967295.0);
+}
+
+// Splats left out of the fused view path's tile lists.  A splat whose pixel rectangle is empty
+// (certified never to blend, or no pixel centre inside its bbox) is never composited, so the
+// only effect of its list entries is on the N_w window of its tile.  The window acts on each
+// run of equal depth key independently (a key change is a clean boundary: composite.cu
+// window_tile), so removing every member of a run leaves the pop order of the other entries
+// unchanged.  The fused path therefore drops such a splat only when no splat with a
+// non-empty rectangle has its depth key (anywhere: a hashed bitmap, false positives keep a
+// splat); list positions (n_proc) are internal to that path.
+constexpr int kQHashBits = 24;
+constexpr int kQBitWords = 1 << (kQHashBits - 5);
+__device__ __forceinline__ uint32_t qhash(uint32_t q) { return (q * 0x9E3779B1u) >> (32 - kQHashBits); }
+__device__ __forceinline__ bool rect_empty(int2 pr) {
+  return (int)(short)(pr.x & 0xffff) > (pr.x >> 16) || (int)(short)(pr.y & 0xffff) > (pr.y >> 16);
+}
+
 // Build the compact record from the FP64 scene values of one splat.
 __device__ inline SplatRec make_record(const double proj[8], const double depths[4], const double f[4],
                                        const double normal[3], double md, const double bbox[4],

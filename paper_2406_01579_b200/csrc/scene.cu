@@ -219,6 +219,10 @@ struct CullF {
     const SplatRec r = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height, amin > 1e-9 * gn2 ? amin : 0.0);
     out.rec[k] = r;
     if (out.prect) out.prect[k] = make_int2(r.rx, r.ry);
+    if (out.qbits && !rect_empty(make_int2(r.rx, r.ry))) {
+      const uint32_t h = qhash(depth_key(md, cam.near_, cam.far_));
+      atomicOr(out.qbits + (h >> 5), 1u << (h & 31));
+    }
   }
 };
 

@@ -46,7 +46,7 @@ struct Buf {
 
 struct ts_workspace {
   // scene
-  Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors, prect;
+  Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors, prect, qbits;
   // bins
   Buf starts, splat_off, items, pos_of, nonmono, witems, cpos, clen, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
   // forward state
@@ -177,7 +177,7 @@ const int32_t* ts_view_overflow(ts_workspace* ws) { return ws ? reinterpret_cast
 
 void ts_workspace_destroy(ts_workspace* ws) {
   if (!ws) return;
-  Buf* all[] = {&ws->prect, &ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
+  Buf* all[] = {&ws->prect, &ws->qbits, &ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
                 &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
                 &ws->nonmono, &ws->witems, &ws->cpos, &ws->clen, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
                 &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
@@ -204,8 +204,10 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
               ws->rec.get<SplatRec>(cap), ws->prect.get<int2>(cap)};
   const int64_t nmax = cap > T ? (cap > capM ? cap : capM) : (T > capM ? T : capM);
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks(nmax + 1, 1));
-  if (!need || !ovf || !so.tet_ids || !so.rec || !scratch)
+  so.qbits = ws->qbits.get<uint32_t>(kQBitWords);
+  if (!need || !ovf || !so.tet_ids || !so.rec || !scratch || !so.qbits)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  cudaMemsetAsync(so.qbits, 0, sizeof(uint32_t) * kQBitWords, st);
   cudaMemsetAsync(ovf, 0, sizeof(int), st);
   cudaMemsetAsync(need, 0, 4 * sizeof(int64_t), st);
   Dyn dyn;
@@ -250,7 +252,8 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
       !pos_of || !witems || !cpos || !clen || !keys || !gs || !pcnt || !item_off || !n_proc || !n_blend || !scr.widx || !scr.wz ||
       !scr.scan || !scr.torder || !scr.rows || !pbits || !prec)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
-  ts_impl_bin_count(cap, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, nullptr, nullptr, st, &dyn);
+  ts_impl_bin_count(cap, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, nullptr, nullptr, st, &dyn,
+                    so.prect, so.qbits);
   // tile pairs M = starts[T] (and the longest list) recorded; overflow when M > cap_M
   // (and the longest list: the sort kernels launched are those of lists up to cap_L)
   const int64_t capL = ws->capL > 0 ? ws->capL : ((int64_t)1 << 40);
@@ -317,7 +320,9 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
               ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
               ws->rec.get<SplatRec>(cap), ws->prect.get<int2>(cap)};
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1, 1));
-  if (!so.tet_ids || !so.rec || !scratch) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  so.qbits = ws->qbits.get<uint32_t>(kQBitWords);
+  if (!so.tet_ids || !so.rec || !scratch || !so.qbits) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  cudaMemsetAsync(so.qbits, 0, sizeof(uint32_t) * kQBitWords, st);
   const int64_t K = n_active > 0 ? ts_impl_build_scene(sdf, deform, R, cam, s, active, n_active, so, scratch, st) : 0;
   // ---- K3-K5 bins ----------------------------------------------------------------------------
   BinWork w;
@@ -333,7 +338,8 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !splat_off || !nonmono)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   int64_t M = 0, maxL = 0;
-  ts_impl_bin_count(K, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, &M, &maxL, st);
+  ts_impl_bin_count(K, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, &M, &maxL, st, nullptr,
+                    so.prect, so.qbits);
   int32_t* items = ws->items.get<int32_t>(M);
   int32_t* pos_of = ws->pos_of.get<int32_t>(M);
   int32_t* witems = ws->witems.get<int32_t>(M);

@@ -190,7 +190,9 @@ def test_fused_view_pipeline_matches_api(ts, case):
     gb = ts.render_backward(saved, sc, g, fs, cam, dm)
     vr = ViewRenderer()
     m2 = vr.forward(g, fs, cam, s, active)
-    assert vr.counts[0] == len(sc) and vr.counts[1] == b.num_pairs
+    # the fused path leaves out of its lists the splats with an empty pixel rectangle whose
+    # depth key no other splat shares (records.cuh): never composited, window unchanged
+    assert vr.counts[0] == len(sc) and vr.counts[1] <= b.num_pairs
     assert torch.equal(m2.normal, maps.normal) and torch.equal(m2.depth, maps.depth)
     assert torch.equal(m2.opacity, maps.opacity)
     gb2 = vr.backward(fs, dm, ts.GradientBuffers.zeros(g.num_vertices))
@@ -274,3 +276,35 @@ def test_bench_sort_windows_track_reference(ts):
     assert len(rows) == 3
     for r, w, mx, mean, ms in rows:
         assert float(mx) < 1e-3 and float(mean) < 1e-4
+
+
+@pytest.mark.parametrize("far,n_w", [(1e8, 1), (1e8, 5), (1e9, 3), (1e10, 2), (10.0, 9)])
+def test_fused_drop_keeps_window_order(ts, far, n_w):
+    """The fused path leaves out splats with an empty pixel rectangle unless a splat with
+    pixels shares their depth key (records.cuh).  A far plane far away coarsens the 32-bit
+    depth keys, so the tile lists become runs of equal key in splat order that the N_w window
+    reorders (mixed runs of dropped-candidate and composited splats everywhere): the fused
+    maps must still equal the full-list API's bit for bit, and its gradients to FP32 noise."""
+    from paper_2406_01579_b200.view import ViewRenderer
+    R, S, s = 20, 96, 50.0
+    g = ts.build_grid(R)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    f.sdf.add_(0.05 * torch.randn(f.sdf.shape, device="cuda", dtype=torch.float64, generator=gen))
+    cam = ts.orbit_camera(0, 8, width=S, height=S, far=far)
+    active = ts.prefilter(g, f, s)
+    sc = ts.build_scene(g, f, cam, s, active=active)
+    b = ts.bin_and_sort(sc, cam)
+    if far >= 1e8:  # depth-key quanta of 0.02-2 depth units: runs the window reorders
+        assert bool(b.nonmono.any()), "no list for the window to reorder"
+    maps, saved = ts.render_forward(sc, b, cam, n_w=n_w, save_state=True)
+    dm = ts.RenderMaps(torch.randn((S, S, 3), device="cuda", generator=gen),
+                       torch.randn((S, S), device="cuda", generator=gen), torch.randn((S, S), device="cuda", generator=gen))
+    gb = ts.render_backward(saved, sc, g, f, cam, dm)
+    vr = ViewRenderer()
+    m2 = vr.forward(g, f, cam, s, active, n_w=n_w)
+    assert vr.counts[0] == len(sc) and vr.counts[1] <= b.num_pairs
+    assert torch.equal(m2.normal, maps.normal) and torch.equal(m2.depth, maps.depth)
+    assert torch.equal(m2.opacity, maps.opacity)
+    gb2 = vr.backward(f, dm, ts.GradientBuffers.zeros(g.num_vertices))
+    assert torch.allclose(gb2.d_vert, gb.d_vert, rtol=1e-6, atol=1e-6 * float(gb.d_vert.abs().max()))
