@@ -31,16 +31,14 @@ __device__ __forceinline__ void tile_rect_q(const double* bb, double md, int til
   tx1 = tclip(bb[2], tiles_x - 1);
   ty0 = tclip(bb[1], tiles_y - 1);
   ty1 = tclip(bb[3], tiles_y - 1);
-  double qq = ddiv(dsub(md, near_), dsub(far_, near_));
-  qq = qq < 0.0 ? 0.0 : qq;
-  qq = qq > 1.0 ? 1.0 : qq;
-  q = (uint32_t)(unsigned long long)dmul(qq, 4294967295.0);
+  q = depth_key(md, near_, far_);
 }
 
 __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const double* __restrict__ md, int tiles_x,
                             int tiles_y, double near_, double far_, BinRec* __restrict__ br,
                             uint32_t* __restrict__ qout, int32_t* __restrict__ splat_cnt,
-                            int32_t* __restrict__ tile_cnt, const int64_t* __restrict__ Kdev) {
+                            int32_t* __restrict__ tile_cnt, const int64_t* __restrict__ Kdev,
+                            const int2* __restrict__ prect, const uint32_t* __restrict__ qbits) {
   // Kdev (nullable): the visible splats on the device; K is then the capacity and the
   // counts of [*Kdev, K) are written as 0 (the scans run over the capacity)
   const int64_t n = Kdev ? min(K, *Kdev) : K;
@@ -60,6 +58,10 @@ __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const do
       ny = ty1 - ty0 + 1;
       if (nx < 0) nx = 0;
       if (ny < 0) ny = 0;
+      if (qbits && rect_empty(__ldg(prect + k))) {  // fused path: left out (records.cuh)
+        const uint32_t h = qhash(q);
+        if (!((__ldg(qbits + (h >> 5)) >> (h & 31)) & 1u)) nx = ny = 0;
+      }
       br[k] = BinRec{tx0, ty0, nx, ny};
       qout[k] = q;
       splat_cnt[k] = nx * ny;
@@ -493,7 +495,8 @@ using namespace ts;
 // (M = starts[T] and the longest list dev_i64[1] stay on the device).
 void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tiles_x, int tiles_y, double near_,
                        double far_, const BinWork& w, int64_t* starts, int64_t* splat_off, int64_t* M_out,
-                       int64_t* maxL_out, cudaStream_t st, const Dyn* dyn) {
+                       int64_t* maxL_out, cudaStream_t st, const Dyn* dyn, const int2* prect,
+                       const uint32_t* qbits) {
   const int T = tiles_x * tiles_y;
   cudaMemsetAsync(w.tile_cnt, 0, sizeof(int32_t) * T, st);
   cudaMemsetAsync(w.dev_i64, 0, sizeof(int64_t) * 2, st);
@@ -501,7 +504,7 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
     int blocks = (int)((K + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_bin_count<<<blocks, 256, 0, st>>>(K, bbox, md, tiles_x, tiles_y, near_, far_, w.br, w.q, w.splat_cnt,
-                                        w.tile_cnt, dyn ? dyn->K : nullptr);
+                                        w.tile_cnt, dyn ? dyn->K : nullptr, prect, qbits);
   }
   scan_counts(w.tile_cnt, T, starts, w.scratch, st);
   scan_counts(w.splat_cnt, K, splat_off, w.scratch, st);
