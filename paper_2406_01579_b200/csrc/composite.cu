@@ -1483,11 +1483,14 @@ __global__ void __launch_bounds__(128, 6) k_chain(int64_t K, const float* __rest
                                                const double* __restrict__ deform, Grid G, Camera cam,
                                                float* __restrict__ d_vert, float* __restrict__ d_color,
                                                const int64_t* __restrict__ Kdev, const int* __restrict__ ovf,
-                                               Fx fxo) {
+                                               Fx fxo, const SplatRec* __restrict__ recs) {
   if (ovf && *ovf) return;
   if (Kdev) K = min(K, *Kdev);
   constexpr int NQ = COLOR ? 6 : 5;  // float4s of a row that carry data
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    // a splat with an empty pixel rectangle (certified never to blend, records.cuh) was never
+    // composited: its row is zero
+    if (rect_empty(__ldg(reinterpret_cast<const int2*>(recs + k)))) continue;
     float a[4 * NQ];
     if (DET) {  // fixed-point rows (k_backward<DET>)
       const longlong2* src = reinterpret_cast<const longlong2*>(rows) + k * (2 * NQ);
@@ -1743,16 +1746,16 @@ void ts_impl_backward(int tiles_x, int tiles_y, const BinsView& b, int64_t M, in
   const int64_t* Kd = dyn ? dyn->K : nullptr;
   if (color && det)
     k_chain<true, true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, nullptr,
-                                                nullptr, Kd, ovf, fxa);
+                                                nullptr, Kd, ovf, fxa, rec);
   else if (color)
     k_chain<true, false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, d_vert,
-                                                 d_color, Kd, ovf, fxa);
+                                                 d_color, Kd, ovf, fxa, rec);
   else if (det)
     k_chain<false, true><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, nullptr,
-                                                 nullptr, Kd, ovf, fxa);
+                                                 nullptr, Kd, ovf, fxa, rec);
   else
     k_chain<false, false><<<blocks, 128, 0, st>>>(K, rows, vert_ids, tet_ids, fsc, deform, make_grid(R), cam, d_vert,
-                                                  nullptr, Kd, ovf, fxa);
+                                                  nullptr, Kd, ovf, fxa, rec);
   put_tmp(rows, given_rows, st);
   put_tmp(torder, given_order, st);
 }
