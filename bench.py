@@ -495,11 +495,13 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     field.deformation.copy_(def0)
     reps = 5
     tf = tb = 0.0
-    for r in range(reps + 1):
+    for r in range(reps + 2):
+        # pass 0: the reference's own work counts (no never-blend certificate, flag 128: every
+        # bbox pair the reference evaluates); pass 1: the pairs the GPU evaluates; then timing
+        _native.check(_native.lib().ts_debug_set_flags({0: 16 | 128, 1: 16}.get(r, 0)))
         act = ts.prefilter(g, field, s)
         sc = ts.build_scene(g, field, cam, s, active=act)
         b = ts.bin_and_sort(sc, cam)
-        _native.check(_native.lib().ts_debug_set_flags(16 if r == 0 else 0))  # count evaluated pairs once
         _native.debug_counters(True)
         ef = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         eb = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -508,10 +510,14 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
         torch.cuda.synchronize()
         if r == 0:
             cnt = _native.debug_counters(True)
-            _native.check(_native.lib().ts_debug_set_flags(0))
             P_pop = int(sv.n_proc.sum())
             B = int(sv.n_blend.sum())
             K_a, K_v, M = int(act.numel()), len(sc), b.num_pairs
+            P_pairs_ref = int(sv.item_off[-1].item())
+            continue
+        if r == 1:
+            cnt_gpu = _native.debug_counters(True)
+            _native.check(_native.lib().ts_debug_set_flags(0))
             P_pairs = int(sv.item_off[-1].item())
             continue
         tf += ef[0].elapsed_time(ef[1])
@@ -519,6 +525,7 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     tf /= reps
     tb /= reps
     P_bbox = cnt[2]
+    P_bbox_gpu = cnt_gpu[2]
     fwd_flop = 8 * P_pop + 120 * P_bbox + 19 * B
     bwd_flop = 300 * B + 300 * K_v
     kern = {"render_forward": {"ms": tf, "lane_ops": fwd_flop}, "render_backward": {"ms": tb, "lane_ops": bwd_flop}}
@@ -530,7 +537,8 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     # the work the GPU algorithm actually executes: the N_w window is replayed once per tile (only
     # where a list is not mean-depth monotone), not popped per pixel, so the 8 P_pop term of the
     # SURVEY 8d model is not executed
-    kern["render_forward"]["lane_ops_gpu_executed"] = 120 * P_bbox + 19 * B
+    # and of the bbox pairs only those of splats not certified never to blend (records.cuh)
+    kern["render_forward"]["lane_ops_gpu_executed"] = 120 * P_bbox_gpu + 19 * B
     kern["render_forward"]["frac_gpu_executed"] = (kern["render_forward"]["lane_ops_gpu_executed"] / (tf * 1e-3)
                                                    / 1e12 / fp32_peak)
     # DRAM traffic, issue and FMA-pipe utilisation of the same kernel from the committed ncu
@@ -555,13 +563,14 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
             "traffic_source": tsrc,
             "work_model": "SURVEY 8d: 8 P_pop + 120 P_bbox + 19 B lane-ops (forward)",
             "frac_gpu_executed": kern[top].get("frac_gpu_executed"),
-            "gpu_executed_model": "120 P_bbox + 19 B (no per-pixel window pops: the GPU replays the window once per "
-                                  "non-monotone tile)",
+            "gpu_executed_model": "120 P_bbox_gpu + 19 B (no per-pixel window pops: the GPU replays the window once per "
+                                  "non-monotone tile; P_bbox_gpu leaves out the splats certified never to blend)",
             "ncu": ncu,
             "peak_source": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FP32 issue, SURVEY 8d; no tensor "
                            f"cores: not a dense contraction; DRAM traffic well under HBM bandwidth)"}
-    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "B": B, "K_a": K_a, "K_v": K_v, "M": M, "pixel_pairs": P_pairs,
-             "fp64_redecisions_edge": cnt[0], "fp64_redecisions_alpha": cnt[1]}
+    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "P_bbox_gpu": P_bbox_gpu, "B": B, "K_a": K_a, "K_v": K_v, "M": M,
+             "pixel_pairs": P_pairs_ref, "pixel_pairs_gpu": P_pairs,
+             "fp64_redecisions_edge": cnt_gpu[0], "fp64_redecisions_alpha": cnt_gpu[1]}
     return roof, {"compositing": kern, "counts": extra}
 
 

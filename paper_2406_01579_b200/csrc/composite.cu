@@ -83,9 +83,11 @@ __device__ unsigned long long g_ts_counters[8];
 // floor(-log2(|min(u, v, w)| / band)) of the nearest face edge (clamped to 15)
 __device__ unsigned long long g_ts_hist[32];
 // diagnostics only: bit 0 = skip the exact FP64 re-decisions (timing experiments; breaks parity),
-// bit 4 = count the pairs phase A evaluates (g_ts_counters[2])
+// bit 4 = count the pairs phase A evaluates (g_ts_counters[2]), bit 7 (host side, scene build)
+// = no never-blend certificate (the reference's own pair counts for bench.py's work model)
 __device__ int g_ts_debug_flags;
 static int h_debug_flags = 0;  // host copy of the debug flags
+int ts_impl_debug_flags() { return h_debug_flags; }
 // diagnostics only (flag bit 1): per-tile forward start/end globaltimer, SM id
 __device__ unsigned long long g_ts_tile_time[2 * 65536];
 __device__ unsigned int g_ts_tile_sm[65536];

@@ -20,7 +20,13 @@ struct SceneOut {
   // non-empty pixel rectangle (q its 32-bit depth key) — k_bin_count leaves out the splats
   // with an empty rectangle whose depth key no such splat shares (records.cuh)
   uint32_t* qbits = nullptr;
+  // never-blend certificate on (records.cuh); off only for the diagnostics flag 128 (the
+  // reference's work counts in bench.py's roofline)
+  bool certify = true;
 };
+
+// host copy of the debug flags (ts_debug_set_flags); bit 128: no never-blend certificate
+int ts_impl_debug_flags();
 
 struct BinRec {  // 16 B per splat: first tile and tile-rect extent
   int32_t tx0, ty0, nx, ny;

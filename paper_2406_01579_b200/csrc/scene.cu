@@ -216,7 +216,8 @@ struct CullF {
       amin = fmin(amin, a / z[c]);
     }
     const double gn2 = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-    const SplatRec r = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height, amin > 1e-9 * gn2 ? amin : 0.0);
+    const SplatRec r = make_record(proj, z, f, nrm, md, bb, cam.width, cam.height,
+                                   out.certify && amin > 1e-9 * gn2 ? amin : 0.0);
     out.rec[k] = r;
     if (out.prect) out.prect[k] = make_int2(r.rx, r.ry);
     if (out.qbits && !rect_empty(make_int2(r.rx, r.ry))) {
@@ -230,13 +231,13 @@ struct CullF {
 __global__ void k_prepare_records(int64_t K, const double* __restrict__ proj, const double* __restrict__ depths,
                                   const double* __restrict__ f, const double* __restrict__ normals,
                                   const double* __restrict__ md, const double* __restrict__ bbox, int width,
-                                  int height, SplatRec* __restrict__ rec) {
+                                  int height, SplatRec* __restrict__ rec, bool certify) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
     double p[8], z[4], ff[4], n[3], b[4];
     for (int i = 0; i < 8; ++i) p[i] = proj[k * 8 + i];
     for (int i = 0; i < 4; ++i) { z[i] = depths[k * 4 + i]; ff[i] = f[k * 4 + i]; b[i] = bbox[k * 4 + i]; }
     for (int i = 0; i < 3; ++i) n[i] = normals[k * 3 + i];
-    rec[k] = make_record(p, z, ff, n, md[k], b, width, height, backfacing_amin(p, z, ff));
+    rec[k] = make_record(p, z, ff, n, md[k], b, width, height, certify ? backfacing_amin(p, z, ff) : 0.0);
   }
 }
 
@@ -264,6 +265,7 @@ int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, cons
                             const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
                             cudaStream_t st) {
   CullF f{active, sdf, deform, make_grid(R), cam, s, out};
+  f.out.certify = !(ts_impl_debug_flags() & 128);
   int64_t* d_total = compact_state<CullF>(n_active, f, scratch, st);  // scratch: compact_blocks(n, 1)
   int64_t h = 0;
   cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
@@ -277,6 +279,7 @@ int64_t* ts_impl_build_scene_dev(const double* sdf, const double* deform, int R,
                                  const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
                                  cudaStream_t st) {
   CullF f{active, sdf, deform, make_grid(R), cam, s, out};
+  f.out.certify = !(ts_impl_debug_flags() & 128);
   return compact_state<CullF>(n_active, f, scratch, st);
 }
 
@@ -286,5 +289,6 @@ void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths
   if (K <= 0) return;
   int blocks = (int)((K + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_prepare_records<<<blocks, 256, 0, st>>>(K, proj, depths, f, normals, md, bbox, width, height, rec);
+  k_prepare_records<<<blocks, 256, 0, st>>>(K, proj, depths, f, normals, md, bbox, width, height, rec,
+                                            !(ts_impl_debug_flags() & 128));
 }
