@@ -113,12 +113,16 @@ __device__ inline bool never_blends(const SplatRec& r, int nxr, int nyr, double 
     const float n_across = (float)((by_rows ? nxr : nyr) - 1);
     const float inu = __frcp_rn(by_rows ? nx : ny), slope = (by_rows ? ny : nx) * inu;
     const float ua = by_rows ? r.vx[va] : r.vy[va], wa = by_rows ? r.vy[va] : r.vx[va];
-    const float half = rad * fabsf(inu) * 1.001f + 1e-6f;
+    const float half = rad * fabsf(inu) * 1.001f + 1e-6f;  // < 0.36: one candidate per row
+    // the line crosses row / column i at c(i) = c0 - slope i; pixel centres sit at j + 0.5, and
+    // only the nearest one can be within half of it
+    const float c0 = ua - slope * (0.5f - wa) - 0.5f;
     bool near = false;
+#pragma unroll 2
     for (int i = 0; i < n_scan; ++i) {
-      const float c = ua - slope * (((float)i + 0.5f) - wa);  // the line's crossing of this row / column
-      const float j0 = ceilf(c - half - 0.5f), j1 = floorf(c + half - 0.5f);
-      near |= j0 <= j1 && j1 >= 0.f && j0 <= n_across;
+      const float d = fmaf(-slope, (float)i, c0);
+      const float j = rintf(d);
+      near |= fabsf(d - j) <= half && j >= 0.f && j <= n_across;
     }
     ok &= !near;
   }
