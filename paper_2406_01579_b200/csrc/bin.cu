@@ -58,9 +58,14 @@ __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const do
       ny = ty1 - ty0 + 1;
       if (nx < 0) nx = 0;
       if (ny < 0) ny = 0;
-      if (qbits && rect_empty(__ldg(prect + k))) {  // fused path: left out (records.cuh)
-        const uint32_t h = qhash(q);
-        if (!((__ldg(qbits + (h >> 5)) >> (h & 31)) & 1u)) nx = ny = 0;
+      if (prect) {  // fused path: culled tets and splats left out (records.cuh)
+        const int2 pr = __ldg(prect + k);
+        if (pr.x == kCulledRect) {
+          nx = ny = 0;
+        } else if (qbits && rect_empty(pr)) {
+          const uint32_t h = qhash(q);
+          if (!((__ldg(qbits + (h >> 5)) >> (h & 31)) & 1u)) nx = ny = 0;
+        }
       }
       br[k] = BinRec{tx0, ty0, nx, ny};
       qout[k] = q;

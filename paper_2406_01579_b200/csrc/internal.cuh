@@ -88,8 +88,9 @@ int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_
 int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, const ts::Camera& cam, double s,
                             const int32_t* active, int64_t n_active, const ts::SceneOut& out, int64_t* scratch,
                             cudaStream_t st);
-int64_t* ts_impl_build_scene_dev(const double* sdf, const double* deform, int R, const ts::Camera& cam, double s,
-                                 const int32_t* active, int64_t n_active, const ts::SceneOut& out, int64_t* scratch,
+// fused view path: scene at the active index (culled tets keep their slot, kCulledRect)
+void ts_impl_build_scene_inplace(const double* sdf, const double* deform, int R, const ts::Camera& cam, double s,
+                                 const int32_t* active, int64_t n_active, const ts::SceneOut& out, int64_t* n_vis,
                                  cudaStream_t st);
 void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths, const double* f,
                              const double* normals, const double* md, const double* bbox, int width, int height,

@@ -51,13 +51,24 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 // of the reference's f_prev - f_next (~1e-15 (1 + C M / |det|) max|f|, C the coordinate
 // magnitude, M the splat extent) and of its face-containment test (~1e-15 C M / |e|), both
 // taken 10^6 times larger, plus the FP32 error of this evaluation on the record's anchored
-// geometry (4e-5 px; gradients within 2%, enforced).  Then every pixel either misses the
+// geometry (1e-4 px; gradients within 2%, enforced).  Then every pixel either misses the
 // hull (no two hits) or lies inside it away from all edges (exactly F and B hit,
 // f_next - f_prev > the error): no pixel of the splat blends in the reference, for any
 // steepness.  Its rectangle is emptied; the binning keeps the FP64 bbox, so tile lists, the
 // window and n_proc are unchanged.  About half of the splats of a closed surface face away
 // from the camera (tests/test_gpu_certificate.py: the certified set against the reference's
 // blends with early stop disabled).
+__device__ __forceinline__ float rcp_approx(float x) {  // <= 1 ulp (the certificate's margins budget for it)
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ inline bool never_blends(const SplatRec& r, int nxr, int nyr, double amin, double C, double M,
                                     double fabsmax, double fmx) {
   // one exit, no early returns: lanes leave each edge's scan loop together (a divergent exit
@@ -67,15 +78,18 @@ __device__ inline bool never_blends(const SplatRec& r, int nxr, int nyr, double 
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     ok &= r.z[v] > 0.f;
-    w[v] = __frcp_rn(r.z[v]);
+    w[v] = rcp_approx(r.z[v]);
     zmin = fminf(zmin, r.z[v]);
     wmax = fmaxf(wmax, w[v]);
   }
-  float lmax = 0.f;
+  float len[6], ilen[6], lmax = 0.f;
 #pragma unroll
   for (int e = 0; e < 6; ++e) {
     const int va = e < 3 ? 0 : (e < 5 ? 1 : 2), vb = e < 3 ? e + 1 : (e < 5 ? e - 1 : 3);
-    lmax = fmaxf(lmax, hypotf(r.vx[vb] - r.vx[va], r.vy[vb] - r.vy[va]));
+    const float dx = r.vx[vb] - r.vx[va], dy = r.vy[vb] - r.vy[va], d2 = dx * dx + dy * dy;
+    ilen[e] = rsqrt_approx(d2);
+    len[e] = d2 * ilen[e];
+    lmax = fmaxf(lmax, len[e]);
   }
   // 1/z plane gradients of the faces (pixel units) and their FP32 error bounds
   float gx[4], gy[4], adet[4], gerr[4];
@@ -86,11 +100,12 @@ __device__ inline bool never_blends(const SplatRec& r, int nxr, int nyr, double 
     const float m01 = r.vx[ic] - r.vx[ia], m11 = r.vy[ic] - r.vy[ia];
     const float det = m00 * m11 - m01 * m10;
     ok &= fabsf(det) > 1e-3f * lmax * lmax;  // thin face: not certified
-    const float inv = __frcp_rn(det), d1 = w[ib] - w[ia], d2 = w[ic] - w[ia];
+    const float inv = rcp_approx(det), d1 = w[ib] - w[ia], d2 = w[ic] - w[ia];
     gx[fi] = (d1 * m11 - m10 * d2) * inv;
     gy[fi] = (m00 * d2 - m01 * d1) * inv;
     adet[fi] = fabsf(det);
-    gerr[fi] = (5e-7f * wmax + 1e-5f * hypotf(gx[fi], gy[fi])) * 2.f * lmax * __frcp_rn(adet[fi]);
+    const float g2 = gx[fi] * gx[fi] + gy[fi] * gy[fi];
+    gerr[fi] = (5e-7f * wmax + 1e-5f * g2 * rsqrt_approx(g2)) * 2.f * lmax * fabsf(inv);
   }
   const float am = (float)amin, e64c = (float)(1e-9 * fabsmax), e64f = (float)(1e-9 * fmx);
   const float cm = (float)(C * M);
@@ -100,27 +115,28 @@ __device__ inline bool never_blends(const SplatRec& r, int nxr, int nyr, double 
     // the two faces through edge (va, vb) omit the two other vertices
     const int fa = (va != 0 && vb != 0) ? 0 : ((va != 1 && vb != 1) ? 1 : 2);
     const int fb = 6 - va - vb - fa;
-    const float kappa = hypotf(gx[fa] - gx[fb], gy[fa] - gy[fb]);
+    const float kx = gx[fa] - gx[fb], ky = gy[fa] - gy[fb], k2 = kx * kx + ky * ky;
+    const float kappa = k2 * rsqrt_approx(k2);
     ok &= kappa > 50.f * (gerr[fa] + gerr[fb]);
     const float dx = r.vx[vb] - r.vx[va], dy = r.vy[vb] - r.vy[va];
-    const float len = hypotf(dx, dy), ilen = __frcp_rn(len);
-    const float e64 = e64c * (1.0f + cm * __frcp_rn(fminf(adet[fa], adet[fb]))) + e64f;
-    const float rad = fmaxf(2.f * e64 * __frcp_rn(am * zmin * zmin * kappa), 1e-9f * cm * ilen) + 4e-5f;
+    const float e64 = e64c * (1.0f + cm * rcp_approx(fminf(adet[fa], adet[fb]))) + e64f;
+    const float rad = fmaxf(2.f * e64 * rcp_approx(am * zmin * zmin * kappa), 1e-9f * cm * ilen[e]) + 1e-4f;
     ok &= rad < 0.25f;  // (false on NaN)
-    const float nx = -dy * ilen, ny = dx * ilen;  // unit normal: dist(p) = |nx (px - xa) + ny (py - ya)|
-    const bool by_rows = fabsf(nx) >= fabsf(ny);
+    // distance to the line = |dy (px - xa) - dx (py - ya)| / len: scanned by rows when the line
+    // is steeper than 45 degrees (|dy| >= |dx|), else by columns
+    const bool by_rows = fabsf(dy) >= fabsf(dx);
     const int n_scan = ok ? (by_rows ? nyr : nxr) : 0;
     const float n_across = (float)((by_rows ? nxr : nyr) - 1);
-    const float inu = __frcp_rn(by_rows ? nx : ny), slope = (by_rows ? ny : nx) * inu;
+    const float iu = rcp_approx(by_rows ? dy : dx), slope = (by_rows ? dx : dy) * iu;
     const float ua = by_rows ? r.vx[va] : r.vy[va], wa = by_rows ? r.vy[va] : r.vx[va];
-    const float half = rad * fabsf(inu) * 1.001f + 1e-6f;  // < 0.36: one candidate per row
-    // the line crosses row / column i at c(i) = c0 - slope i; pixel centres sit at j + 0.5, and
+    const float half = rad * len[e] * fabsf(iu) * 1.001f + 1e-6f;  // < 0.36: one candidate per row
+    // the line crosses row / column i at c(i) = c0 + slope i; pixel centres sit at j + 0.5, and
     // only the nearest one can be within half of it
-    const float c0 = ua - slope * (0.5f - wa) - 0.5f;
+    const float c0 = ua + slope * (0.5f - wa) - 0.5f;
     bool near = false;
 #pragma unroll 2
     for (int i = 0; i < n_scan; ++i) {
-      const float d = fmaf(-slope, (float)i, c0);
+      const float d = fmaf(slope, (float)i, c0);
       const float j = rintf(d);
       near |= fabsf(d - j) <= half && j >= 0.f && j <= n_across;
     }
@@ -181,6 +197,10 @@ __device__ __forceinline__ uint32_t depth_key(double md, double near_, double fa
 constexpr int kQHashBits = 24;
 constexpr int kQBitWords = 1 << (kQHashBits - 5);
 __device__ __forceinline__ uint32_t qhash(uint32_t q) { return (q * 0x9E3779B1u) >> (32 - kQHashBits); }
+// fused view path: the packed rectangle of an active tet the view culls (no splat; the scene
+// is indexed by active tet there, composite.cu never sees it) — distinct from every empty
+// rectangle a record can carry
+constexpr int kCulledRect = (int)0x80000000;
 __device__ __forceinline__ bool rect_empty(int2 pr) {
   return (int)(short)(pr.x & 0xffff) > (pr.x >> 16) || (int)(short)(pr.y & 0xffff) > (pr.y >> 16);
 }

@@ -159,6 +159,12 @@ struct CullF {
     project4(i, st.v, P, st.px, st.py, st.z);
     return visible(st.px, st.py, st.z);
   }
+  // fused view path: an active tet this view culls keeps its slot (records.cuh kCulledRect)
+  __device__ void cull(int64_t i) const {
+    out.tet_ids[i] = active[i];
+    out.prect[i] = make_int2(kCulledRect, kCulledRect);
+    *reinterpret_cast<int2*>(out.rec + i) = make_int2(kCulledRect, kCulledRect);
+  }
   __device__ void emit(int64_t i, int64_t k, const State& st) const {
     const uint32_t* v = st.v;
     double P[4][3];
@@ -220,7 +226,7 @@ struct CullF {
                                    out.certify && amin > 1e-9 * gn2 ? amin : 0.0);
     out.rec[k] = r;
     if (out.prect) out.prect[k] = make_int2(r.rx, r.ry);
-    if (out.qbits && !rect_empty(make_int2(r.rx, r.ry))) {
+    if (out.qbits && !rect_empty(make_int2(r.rx, r.ry))) {  // (fused path)
       const uint32_t h = qhash(depth_key(md, cam.near_, cam.far_));
       atomicOr(out.qbits + (h >> 5), 1u << (h & 31));
     }
@@ -241,9 +247,52 @@ __global__ void k_prepare_records(int64_t K, const double* __restrict__ proj, co
   }
 }
 
+// Fused view path: the scene indexed by active tet (its scene is internal, so no compaction:
+// no look-back, one projection per tet); culled tets get the kCulledRect sentinel, which
+// k_bin_count and k_chain skip.  n_vis receives the visible count (reported only).
+#ifndef TS_CULL_MINB
+#define TS_CULL_MINB 1
+#endif
+__global__ void __launch_bounds__(256, TS_CULL_MINB) k_cull_emit(int64_t n, CullF f, unsigned long long* __restrict__ n_vis) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool vis = false;
+    if (i < n) {
+      CullF::State st;
+      vis = f.pred(i, st);
+      if (vis) f.emit(i, i, st);
+      else f.cull(i);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, vis);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_vis, (unsigned long long)__popc(m));
+  }
+}
+
+__global__ void k_cull_slot0(SceneOut out) {
+  out.tet_ids[0] = 0;
+  out.prect[0] = make_int2(kCulledRect, kCulledRect);
+  *reinterpret_cast<int2*>(out.rec) = make_int2(kCulledRect, kCulledRect);
+}
+
 }  // namespace ts
 
 using namespace ts;
+
+void ts_impl_build_scene_inplace(const double* sdf, const double* deform, int R, const Camera& cam, double s,
+                                 const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* n_vis,
+                                 cudaStream_t st) {
+  cudaMemsetAsync(n_vis, 0, sizeof(int64_t), st);
+  if (n_active <= 0) {  // the one capacity slot holds no splat
+    k_cull_slot0<<<1, 1, 0, st>>>(out);
+    return;
+  }
+  CullF f{active, sdf, deform, make_grid(R), cam, s, out};
+  f.out.certify = !(ts_impl_debug_flags() & 128);
+  int blocks = (int)((n_active + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_cull_emit<<<blocks, 256, 0, st>>>(n_active, f, reinterpret_cast<unsigned long long*>(n_vis));
+}
 
 // host entry points used by abi.cu
 int64_t ts_impl_prefilter(const double* sdf, int R, double s, double thr, int32_t* out_active,
@@ -273,15 +322,6 @@ int64_t ts_impl_build_scene(const double* sdf, const double* deform, int R, cons
   return h;
 }
 
-// sync-free variant: the visible-splat count stays on the device (the returned pointer lives
-// in `scratch`, valid until the next user of the scratch)
-int64_t* ts_impl_build_scene_dev(const double* sdf, const double* deform, int R, const Camera& cam, double s,
-                                 const int32_t* active, int64_t n_active, const SceneOut& out, int64_t* scratch,
-                                 cudaStream_t st) {
-  CullF f{active, sdf, deform, make_grid(R), cam, s, out};
-  f.out.certify = !(ts_impl_debug_flags() & 128);
-  return compact_state<CullF>(n_active, f, scratch, st);
-}
 
 void ts_impl_prepare_records(int64_t K, const double* proj, const double* depths, const double* f,
                              const double* normals, const double* md, const double* bbox, int width, int height,

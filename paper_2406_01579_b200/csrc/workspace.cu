@@ -60,6 +60,7 @@ struct ts_workspace {
   bool dyn = false;
   // view description of the last forward (capacities on the sync-free path)
   int64_t K = 0, M = 0, P = 0, maxL = 0;
+  int64_t Kvis = 0;  // visible splats (reported; the fused scene keeps every active tet's slot)
   int tiles_x = 0, tiles_y = 0, R = 0;
   Camera cam{};
   double s = 0.0;
@@ -132,7 +133,7 @@ int ts_view_status(ts_workspace* ws, int64_t* out5, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!ws->dyn) {
     out5[0] = 0;
-    out5[1] = ws->K;
+    out5[1] = ws->Kvis;
     out5[2] = ws->M;
     out5[3] = ws->P;
     out5[4] = ws->maxL;
@@ -163,7 +164,7 @@ int ts_view_collect(ts_workspace* ws, float* status, int64_t* out5, void* stream
     k_view_collect<<<1, 1, 0, st>>>(reinterpret_cast<int64_t*>(ws->need.p), reinterpret_cast<int*>(ws->ovf.p), status,
                                     out5);
   else {
-    const int64_t h[5] = {ws->K, ws->M, ws->P, ws->maxL, 0};
+    const int64_t h[5] = {ws->Kvis, ws->M, ws->P, ws->maxL, 0};
     cudaMemcpyAsync(out5, h, sizeof(h), cudaMemcpyHostToDevice, st);
     cudaStreamSynchronize(st);  // h is a stack buffer (sizing path: the host already waited)
   }
@@ -211,12 +212,10 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   cudaMemsetAsync(ovf, 0, sizeof(int), st);
   cudaMemsetAsync(need, 0, 4 * sizeof(int64_t), st);
   Dyn dyn;
-  dyn.K = need;
+  dyn.K = nullptr;  // the scene is indexed by active tet: all cap slots are valid (culled ones skipped)
   dyn.ovf = ovf;
-  if (n_active > 0) {
-    const int64_t* dK = ts_impl_build_scene_dev(sdf, deform, R, cam, s, active, n_active, so, scratch, st);
-    cudaMemcpyAsync(need, dK, sizeof(int64_t), cudaMemcpyDeviceToDevice, st);  // the scratch is reused below
-  }
+  // need[0] receives the visible count (reported only)
+  ts_impl_build_scene_inplace(sdf, deform, R, cam, s, active, n_active, so, need, st);
   // ---- bins (capacity-sized, counts on the device) ----------------------------------------
   BinWork w;
   w.br = reinterpret_cast<BinRec*>(ws->br.get<int4>(cap));
@@ -266,7 +265,7 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
     float* c = ws->colors.get<float>(cap * 3);
     if (!c) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
     k_gather_colors<<<(int)((cap + 255) / 256 < 4096 ? (cap + 255) / 256 : 4096), 256, 0, st>>>(cap, so.tet_ids,
-                                                                                                colors_tet, c, need);
+                                                                                                colors_tet, c, nullptr);
     colors = c;
   }
   // window + pair numbering over the M capacity (the M valid positions scanned)
@@ -323,7 +322,14 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   so.qbits = ws->qbits.get<uint32_t>(kQBitWords);
   if (!so.tet_ids || !so.rec || !scratch || !so.qbits) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   cudaMemsetAsync(so.qbits, 0, sizeof(uint32_t) * kQBitWords, st);
-  const int64_t K = n_active > 0 ? ts_impl_build_scene(sdf, deform, R, cam, s, active, n_active, so, scratch, st) : 0;
+  // the scene indexed by active tet (k_cull_emit: no compaction, culled tets keep their slot)
+  int64_t* nvis_dev = ws->dev_i64.get<int64_t>(2);
+  if (!nvis_dev) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
+  int64_t Kvis = 0;
+  ts_impl_build_scene_inplace(sdf, deform, R, cam, s, active, n_active, so, nvis_dev, st);
+  cudaMemcpyAsync(&Kvis, nvis_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);  // (the bin count below syncs anyway)
+  const int64_t K = n_active > 0 ? n_active : 0;
   // ---- K3-K5 bins ----------------------------------------------------------------------------
   BinWork w;
   w.br = reinterpret_cast<BinRec*>(ws->br.get<int4>(cap));
@@ -379,7 +385,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   scr.cnt = pcnt;
   scr.scan = ws->pscan.get<int64_t>(compact_blocks(M));
   scr.torder = ws->torder.get<int32_t>(T);
-  scr.rows = ws->rows.get<float>(24 * (M > 0 ? M : 1));  // kGr floats per list position
+  scr.rows = ws->rows.get<float>(24 * (M > K ? M : (K > 0 ? K : 1)));  // kGr floats per splat
   if (!scr.widx || !scr.wz || !scr.cnt || !scr.scan || !scr.torder || !scr.rows)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (K > 0 && M > 0)
@@ -401,6 +407,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
     cudaMemsetAsync(n_blend, 0, sizeof(int32_t) * HW, st);
   }
   ws->K = K;
+  ws->Kvis = Kvis;
   ws->M = M;
   ws->P = P;
   ws->maxL = maxL;
@@ -411,7 +418,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   ws->s = s;
   ws->color = colors != nullptr;
   ws->valid = true;
-  out_counts[0] = K;
+  out_counts[0] = Kvis;
   out_counts[1] = M;
   out_counts[2] = P;
   out_counts[3] = maxL;
@@ -432,7 +439,7 @@ static int view_backward(ts_workspace* ws, const double* deform, const float* co
   if (fx && !ws->rows.get<float>(2 * 24 * (size_t)(ws->K > ws->M ? ws->K : ws->M)))
     return ws_fail(TS_ENOMEM, "ts_view_backward_fx: out of device memory");
   Dyn dyn;
-  dyn.K = reinterpret_cast<int64_t*>(ws->need.p);
+  dyn.K = nullptr;  // every scene slot is valid (culled ones skipped by k_chain)
   dyn.ovf = reinterpret_cast<int*>(ws->ovf.p);
   ViewScratch scr;  // sized by the forward of this view
   scr.torder = reinterpret_cast<int32_t*>(ws->torder.p);
