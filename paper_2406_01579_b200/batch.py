@@ -182,6 +182,10 @@ class FitStep:
         must be valid on the current stream); everything but the prefilter waits for it.
         `update`: run the Adam step at the end (default: when the config has an optimizer);
         `fit_field` passes False and calls `apply_update` after its host-side checks."""
+        with torch.cuda.nvtx.range("FitStep"):  # (the ABI calls open their own ranges inside)
+            return self._step(s, views, d_maps_fn, stats, inputs_ready, update)
+
+    def _step(self, s, views, d_maps_fn, stats, inputs_ready, update):
         g, f, cfg = self.grid, self.field, self.cfg
         self._flat.zero_()
         if self._fx is not None:
@@ -240,7 +244,8 @@ class FitStep:
                 dist.all_reduce(self.status, op=dist.ReduceOp.SUM, group=self.group)
             self._fx.to_float(self.grads, status=self.status)
         elif multi:
-            dist.all_reduce(self._flat, op=dist.ReduceOp.SUM, group=self.group)
+            with torch.cuda.nvtx.range("gradient all-reduce"):
+                dist.all_reduce(self._flat, op=dist.ReduceOp.SUM, group=self.group)
         if update is None:
             update = self.opt is not None
         if update:

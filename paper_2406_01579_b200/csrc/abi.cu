@@ -77,6 +77,7 @@ const char* ts_last_error(void) { return g_err.c_str(); }
 int ts_version(void) { return 1; }
 
 int ts_prefilter(const double* sdf, int32_t R, double s, double thr, int32_t* out, int64_t* count, void* stream) {
+  TS_NVTX("ts_prefilter");
   if (!sdf || !out || !count || R < 1) return fail(TS_EINVAL, "ts_prefilter: bad arguments");
   cudaStream_t st = ST(stream);
   const int64_t K = 6ll * R * R * R;
@@ -89,6 +90,7 @@ int ts_prefilter(const double* sdf, int32_t R, double s, double thr, int32_t* ou
 
 int ts_build_scene(const double* sdf, const double* deform, int32_t R, const ts_camera* cam, double s,
                    const int32_t* active, int64_t n_active, const ts_scene* out, int64_t* count, void* stream) {
+  TS_NVTX("ts_build_scene");
   if (!sdf || !deform || !cam || !out || !count || R < 1 || n_active < 0 || (n_active > 0 && !active))
     return fail(TS_EINVAL, "ts_build_scene: bad arguments");
   cudaStream_t st = ST(stream);
@@ -102,6 +104,7 @@ int ts_build_scene(const double* sdf, const double* deform, int32_t R, const ts_
 }
 
 int ts_prepare_records(const ts_scene* sc, int64_t K, int32_t W, int32_t H, void* stream) {
+  TS_NVTX("ts_prepare_records");
   if (!sc || K < 0 || W < 1 || H < 1 || W > 32767 || H > 32767) return fail(TS_EINVAL, "ts_prepare_records: bad arguments");
   ts_impl_prepare_records(K, sc->proj, sc->depths, sc->f, sc->normals, sc->mean_depth, sc->bbox, W, H,
                           reinterpret_cast<SplatRec*>(sc->records), ST(stream));
@@ -119,6 +122,7 @@ static int tiles_of(const ts_camera* cam, int tile, int& tx, int& ty) {
 
 int ts_bin_count(const double* bbox, const double* md, int64_t K, const ts_camera* cam, int32_t tile,
                  int64_t* starts, int64_t* splat_off, int64_t* M, int64_t* maxL, void* stream) {
+  TS_NVTX("ts_bin_count");
   if (!cam || !starts || !splat_off || !M || !maxL || K < 0 || (K > 0 && (!bbox || !md)))
     return fail(TS_EINVAL, "ts_bin_count: bad arguments");
   int tx, ty;
@@ -142,6 +146,7 @@ int ts_bin_count(const double* bbox, const double* md, int64_t K, const ts_camer
 
 int ts_bin_sort(const double* bbox, const double* md, int64_t K, const ts_camera* cam, int32_t tile,
                 const ts_bins* b, int64_t M, int64_t maxL, void* stream) {
+  TS_NVTX("ts_bin_sort");
   if (!cam || !b || K < 0 || M < 0 || (M > 0 && (!b->items || !b->pos_of || !b->starts || !b->splat_off)) || !b->nonmono)
     return fail(TS_EINVAL, "ts_bin_sort: bad arguments");
   int tx, ty;
@@ -185,6 +190,7 @@ static BinsView bv_of(const ts_bins* b) {
 
 int ts_forward_prepare(const ts_scene* sc, int64_t K, const ts_bins* b, int64_t M, const ts_camera* cam, int32_t n_w,
                        int64_t* item_off, int64_t* out_pairs, void* stream) {
+  TS_NVTX("ts_forward_prepare");
   if (n_w < 1) return fail(TS_EINVAL, "resorting window must be >= 1");
   if (!sc || !b || !cam || !item_off || !out_pairs || K < 0 || M < 0)
     return fail(TS_EINVAL, "ts_forward_prepare: bad arguments");
@@ -201,6 +207,7 @@ int ts_render_forward(const ts_scene* sc, int64_t K, const float* colors, const 
                       const ts_camera* cam, double s, double t_stop, const int64_t* item_off, int64_t n_pairs,
                       uint32_t* pair_bits, void* pair_rec, float* nmap, float* dmap, float* omap, float* cmap,
                       int32_t* n_proc, int32_t* n_blend, void* stream) {
+  TS_NVTX("ts_render_forward");
   if (!sc || !b || !cam || !nmap || !dmap || !omap || !n_proc || !n_blend || K < 0 || M < 0 || n_pairs < 0 ||
       (M > 0 && (!item_off || !pair_bits || (n_pairs > 0 && !pair_rec))))
     return fail(TS_EINVAL, "ts_render_forward: bad arguments");
@@ -218,6 +225,7 @@ int ts_render_backward(const ts_scene* sc, int64_t K, const float* colors, const
                        const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits, const void* pair_rec,
                        const float* const maps[4], const float* const dmaps[4], const int32_t* n_proc,
                        const double* deform, int32_t R, float* d_vert, float* d_color, void* stream) {
+  TS_NVTX("ts_render_backward");
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert || R < 1 || K < 0 || M < 0 ||
       (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_render_backward: bad arguments");
@@ -251,6 +259,7 @@ int ts_render_backward_fx(const ts_scene* sc, int64_t K, const float* colors, co
                           const void* pair_rec, const float* const maps[4], const float* const dmaps[4],
                           const int32_t* n_proc, const double* deform, int32_t R, int64_t* d_vert_fx,
                           int64_t* d_color_fx, void* stream) {
+  TS_NVTX("ts_render_backward_fx");
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !deform || !d_vert_fx || R < 1 || K < 0 || M < 0 ||
       (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_render_backward_fx: bad arguments");
@@ -281,6 +290,7 @@ int ts_bins_from_lists(const int64_t* starts, const int32_t* items, int32_t T, c
 int ts_saved_records(const ts_scene* sc, const ts_bins* b, const ts_camera* cam, const int64_t* item_off,
                      const uint32_t* pair_bits, const void* pair_rec, const int32_t* n_proc, const int32_t* tiles,
                      int32_t n_tiles, const int64_t* rec_off, int64_t* idx, double* alpha, void* stream) {
+  TS_NVTX("ts_saved_records");
   if (!sc || !b || !cam || !n_proc || n_tiles < 0 || (n_tiles > 0 && (!tiles || !rec_off || !item_off ||
                                                                        !pair_bits || !pair_rec)))
     return fail(TS_EINVAL, "ts_saved_records: bad arguments");
@@ -297,6 +307,7 @@ int ts_backward_tiles(const ts_scene* sc, int64_t K, const float* colors, const 
                       const ts_camera* cam, const int64_t* item_off, const uint32_t* pair_bits, const void* pair_rec,
                       const float* const maps[4], const float* const dmaps[4], const int32_t* n_proc,
                       const int32_t* tiles, int32_t n_tiles, float* rows, void* stream) {
+  TS_NVTX("ts_backward_tiles");
   if (!sc || !b || !cam || !maps || !dmaps || !n_proc || !rows || K < 0 || M < 0 || n_tiles < 0 ||
       (n_tiles > 0 && !tiles) || (M > 0 && (!item_off || !pair_bits)))
     return fail(TS_EINVAL, "ts_backward_tiles: bad arguments");
@@ -317,6 +328,7 @@ int ts_backward_tiles(const ts_scene* sc, int64_t K, const float* colors, const 
 
 int ts_eikonal(const double* sdf, const double* deform, int32_t R, const int32_t* tet_set, int64_t n, double scale,
                float* d_vert, double* loss, void* stream) {
+  TS_NVTX("ts_eikonal");
   if (!sdf || !deform || !d_vert || !loss || R < 1 || n < 0 || (n > 0 && !tet_set))
     return fail(TS_EINVAL, "ts_eikonal: bad arguments");
   ts_impl_eikonal(sdf, deform, R, tet_set, n, (float)scale, d_vert, loss, ST(stream));
@@ -325,6 +337,7 @@ int ts_eikonal(const double* sdf, const double* deform, int32_t R, const int32_t
 
 int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
                           double* loss, void* stream) {
+  TS_NVTX("ts_normal_consistency");
   if (!sdf || !deform || !d_vert || !loss || R < 1) return fail(TS_EINVAL, "ts_normal_consistency: bad arguments");
   keep_pool_warm();
   ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream));
@@ -333,6 +346,7 @@ int ts_normal_consistency(const double* sdf, const double* deform, int32_t R, do
 
 int ts_eikonal_fx(const double* sdf, const double* deform, int32_t R, const int32_t* tet_set, int64_t n,
                   double scale, int64_t* d_vert_fx, double* loss, void* stream) {
+  TS_NVTX("ts_eikonal_fx");
   if (!sdf || !deform || !d_vert_fx || !loss || R < 1 || n < 0 || (n > 0 && !tet_set))
     return fail(TS_EINVAL, "ts_eikonal_fx: bad arguments");
   const Fx fx = fx_of(R, d_vert_fx, nullptr);
@@ -342,6 +356,7 @@ int ts_eikonal_fx(const double* sdf, const double* deform, int32_t R, const int3
 
 int ts_normal_consistency_fx(const double* sdf, const double* deform, int32_t R, double scale, int64_t* d_vert_fx,
                              double* loss, void* scratch, void* stream) {
+  TS_NVTX("ts_normal_consistency_fx");
   if (!sdf || !deform || !d_vert_fx || !loss || R < 1) return fail(TS_EINVAL, "ts_normal_consistency_fx: bad arguments");
   if (!scratch) keep_pool_warm();
   const Fx fx = fx_of(R, d_vert_fx, nullptr);
@@ -352,6 +367,7 @@ int ts_normal_consistency_fx(const double* sdf, const double* deform, int32_t R,
 int ts_normal_consistency_slab(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
                                int64_t* d_vert_fx, double* loss, void* scratch, int32_t z0, int32_t z1,
                                void* stream) {
+  TS_NVTX("ts_normal_consistency_slab");
   if (!sdf || !deform || !loss || R < 1 || (!d_vert == !d_vert_fx) || z0 < 0 || z1 < z0 || z1 > R + 1)
     return fail(TS_EINVAL, "ts_normal_consistency_slab: bad arguments");
   if (!scratch) keep_pool_warm();
@@ -370,6 +386,7 @@ int ts_fx_to_f32(const int64_t* fx, int64_t n, float* out, float* status, void* 
 int ts_adam_step(int32_t R, const float* d_vert, double* sdf, double* deform, double* m_sdf, double* v_sdf,
                  double* m_def, double* v_def, double lr_sdf, double lr_def, double beta1, double beta2, int64_t t,
                  double eps, double deform_limit, float* status, void* stream) {
+  TS_NVTX("ts_adam_step");
   if (!d_vert || !sdf || !deform || !m_sdf || !v_sdf || !m_def || !v_def || R < 1 || t < 1)
     return fail(TS_EINVAL, "ts_adam_step: bad arguments");
   const int64_t n = (int64_t)R + 1;
@@ -382,6 +399,7 @@ int64_t ts_normal_consistency_scratch_bytes(int32_t R) { return R < 1 ? 0 : ts_i
 
 int ts_normal_consistency_ws(const double* sdf, const double* deform, int32_t R, double scale, float* d_vert,
                              double* loss, void* scratch, void* stream) {
+  TS_NVTX("ts_normal_consistency_ws");
   if (!sdf || !deform || !d_vert || !loss || !scratch || R < 1)
     return fail(TS_EINVAL, "ts_normal_consistency_ws: bad arguments");
   ts_impl_normal_consistency(sdf, deform, R, (float)scale, d_vert, loss, ST(stream), scratch);
@@ -399,6 +417,7 @@ int ts_marching_tets_count(const double* sdf, const double* deform, int32_t R, i
 
 int ts_marching_tets_run(const double* sdf, const double* deform, int32_t R, void** handle, int64_t* nv,
                          int64_t* nt, void* stream) {
+  TS_NVTX("ts_marching_tets_run");
   keep_pool_warm();
   if (!sdf || !deform || !handle || !nv || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets_run: bad arguments");
   *handle = nullptr;
@@ -421,6 +440,7 @@ int ts_marching_tets_release(void* handle) {
 
 int ts_marching_tets(const double* sdf, const double* deform, int32_t R, double* verts, int64_t* tris,
                      int64_t* nt, void* stream) {
+  TS_NVTX("ts_marching_tets");
   keep_pool_warm();
   if (!sdf || !deform || !nt || R < 1) return fail(TS_EINVAL, "ts_marching_tets: bad arguments");
   int rc = ts_impl_mt(sdf, deform, R, verts, tris, nt, ST(stream));
@@ -430,6 +450,7 @@ int ts_marching_tets(const double* sdf, const double* deform, int32_t R, double*
 
 int ts_rasterize_mesh(const double* vertices, int64_t V, const int64_t* triangles, int64_t F, const ts_camera* cam,
                       uint8_t* mask, double* depth, double* normal, void* stream) {
+  TS_NVTX("ts_rasterize_mesh");
   if (!cam || !mask || !depth || !normal || V < 0 || F < 0 || (V > 0 && !vertices) || (F > 0 && !triangles))
     return fail(TS_EINVAL, "ts_rasterize_mesh: bad arguments");
   if (cam->width < 1 || cam->height < 1) return fail(TS_EINVAL, "ts_rasterize_mesh: bad image size");

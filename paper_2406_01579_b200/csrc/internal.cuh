@@ -1,6 +1,20 @@
 // internal.cuh — structs and host-side entry points shared between the translation units.
 #pragma once
+#include <nvtx3/nvToolsExt.h>
+
 #include "records.cuh"
+
+// Tracing: every ABI entry point opens an NVTX range on the calling host thread
+// (header-only NVTX 3: a no-op unless a tool such as nsys / ncu --nvtx is attached).
+struct TsNvtxRange {
+  explicit TsNvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~TsNvtxRange() { nvtxRangePop(); }
+  TsNvtxRange(const TsNvtxRange&) = delete;
+  TsNvtxRange& operator=(const TsNvtxRange&) = delete;
+};
+#define TS_NVTX_CAT2(a, b) a##b
+#define TS_NVTX_CAT(a, b) TS_NVTX_CAT2(a, b)
+#define TS_NVTX(name) TsNvtxRange TS_NVTX_CAT(ts_nvtx_, __LINE__)(name)
 
 namespace ts {
 

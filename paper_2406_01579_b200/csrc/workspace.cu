@@ -158,6 +158,7 @@ __global__ void k_view_collect(const int64_t* __restrict__ need, const int* __re
 }
 
 int ts_view_collect(ts_workspace* ws, float* status, int64_t* out5, void* stream) {
+  TS_NVTX("ts_view_collect");
   if (!ws || !out5) return ws_fail(TS_EINVAL, "ts_view_collect: bad arguments");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (ws->dyn)
@@ -297,6 +298,7 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
                     double s, const int32_t* active, int64_t n_active, int32_t n_w, double t_stop,
                     const float* colors_tet, float* nmap, float* dmap, float* omap, float* cmap,
                     int64_t* out_counts, void* stream) {
+  TS_NVTX("ts_view_forward");
   if (!ws || !sdf || !deform || !camp || R < 1 || n_active < 0 || (n_active > 0 && !active) || !nmap || !dmap ||
       !omap || !out_counts)
     return ws_fail(TS_EINVAL, "ts_view_forward: bad arguments");
@@ -466,6 +468,7 @@ static int view_backward(ts_workspace* ws, const double* deform, const float* co
 
 int ts_view_backward(ts_workspace* ws, const double* deform, const float* const maps[4], const float* const dmaps[4],
                      float* d_vert, float* d_color, float* status, void* stream) {
+  TS_NVTX("ts_view_backward");
   if (!d_vert) return ws_fail(TS_EINVAL, "ts_view_backward: bad arguments");
   return view_backward(ws, deform, maps, dmaps, d_vert, d_color, status, stream, nullptr);
 }
@@ -473,6 +476,7 @@ int ts_view_backward(ts_workspace* ws, const double* deform, const float* const 
 int ts_view_backward_fx(ts_workspace* ws, const double* deform, const float* const maps[4],
                         const float* const dmaps[4], int64_t* d_vert_fx, int64_t* d_color_fx, float* status,
                         void* stream) {
+  TS_NVTX("ts_view_backward_fx");
   if (!ws || !d_vert_fx) return ws_fail(TS_EINVAL, "ts_view_backward_fx: bad arguments");
   const int64_t n = (int64_t)ws->R + 1;
   Fx fx;
