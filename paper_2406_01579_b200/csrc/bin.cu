@@ -139,6 +139,7 @@ __device__ __forceinline__ void emit_sorted(uint64_t key, int64_t p, int tile, i
   int k = (int)(uint32_t)key;
   items[p] = k;
   if (qsorted) qsorted[p] = (uint32_t)(key >> 32);  // the depth key per position (k_window)
+  if (!pos_of) return;  // (the fused view path keeps no pos_of)
   BinRec b = br[k];
   int tx = tile % tiles_x, ty = tile / tiles_x;
   int local = (ty - b.ty0) * b.nx + (tx - b.tx0);
@@ -512,7 +513,7 @@ void ts_impl_bin_count(int64_t K, const double* bbox, const double* md, int tile
                                         w.tile_cnt, dyn ? dyn->K : nullptr, prect, qbits);
   }
   scan_counts(w.tile_cnt, T, starts, w.scratch, st);
-  scan_counts(w.splat_cnt, K, splat_off, w.scratch, st);
+  if (splat_off) scan_counts(w.splat_cnt, K, splat_off, w.scratch, st);  // (pos_of's offsets; API path)
   k_max_len<<<8, 256, 0, st>>>(T, starts, w.dev_i64 + 1);
   if (dyn) return;
   int64_t h[2];

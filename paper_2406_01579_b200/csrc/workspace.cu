@@ -48,7 +48,7 @@ struct ts_workspace {
   // scene
   Buf tet_ids, vert_ids, proj, depths, f, normals, md, amax, bbox, rec, colors, prect, qbits;
   // bins
-  Buf starts, splat_off, items, pos_of, nonmono, witems, cpos, clen, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
+  Buf starts, items, nonmono, witems, cpos, clen, br, q, splat_cnt, tile_cnt, scratch, dev_i64, keys, gsort;
   // forward state
   Buf item_off, pair_bits, pair_rec, n_proc, n_blend;
   // per-view temporaries (kept so no view in flight allocates from the shared pool)
@@ -180,7 +180,7 @@ const int32_t* ts_view_overflow(ts_workspace* ws) { return ws ? reinterpret_cast
 void ts_workspace_destroy(ts_workspace* ws) {
   if (!ws) return;
   Buf* all[] = {&ws->prect, &ws->qbits, &ws->need, &ws->ovf, &ws->tet_ids, &ws->vert_ids, &ws->proj, &ws->depths, &ws->f, &ws->normals, &ws->md, &ws->amax,
-                &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->splat_off, &ws->items, &ws->pos_of,
+                &ws->bbox, &ws->rec, &ws->colors, &ws->starts, &ws->items,
                 &ws->nonmono, &ws->witems, &ws->cpos, &ws->clen, &ws->br, &ws->q, &ws->splat_cnt, &ws->tile_cnt, &ws->scratch,
                 &ws->dev_i64, &ws->keys, &ws->gsort, &ws->item_off, &ws->pair_bits, &ws->pair_rec,
                 &ws->n_proc, &ws->widx, &ws->wz, &ws->pcnt, &ws->pscan, &ws->torder, &ws->rows, &ws->n_blend};
@@ -226,10 +226,8 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   w.scratch = scratch;
   w.dev_i64 = ws->dev_i64.get<int64_t>(2);
   int64_t* starts = ws->starts.get<int64_t>(T + 1);
-  int64_t* splat_off = ws->splat_off.get<int64_t>(cap + 1);
   uint8_t* nonmono = ws->nonmono.get<uint8_t>(T);
   int32_t* items = ws->items.get<int32_t>(capM);
-  int32_t* pos_of = ws->pos_of.get<int32_t>(capM);
   int32_t* witems = ws->witems.get<int32_t>(capM);
   int32_t* cpos = ws->cpos.get<int32_t>(capM);
   int32_t* clen = ws->clen.get<int32_t>(T);
@@ -248,19 +246,20 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
   scr.rows = ws->rows.get<float>(24 * cap);
   uint32_t* pbits = ws->pair_bits.get<uint32_t>(TS_PAIR_BIT_WORDS(capP));
   float4* prec = ws->pair_rec.get<float4>(capP);
-  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !splat_off || !nonmono || !items ||
-      !pos_of || !witems || !cpos || !clen || !keys || !gs || !pcnt || !item_off || !n_proc || !n_blend || !scr.widx || !scr.wz ||
+  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !nonmono || !items ||
+      !witems || !cpos || !clen || !keys || !gs || !pcnt || !item_off || !n_proc || !n_blend || !scr.widx || !scr.wz ||
       !scr.scan || !scr.torder || !scr.rows || !pbits || !prec)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
-  ts_impl_bin_count(cap, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, nullptr, nullptr, st, &dyn,
+  // (no splat_off / pos_of: the fused path never maps splats to their list positions)
+  ts_impl_bin_count(cap, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, nullptr, nullptr, nullptr, st, &dyn,
                     so.prect, so.qbits);
   // tile pairs M = starts[T] (and the longest list) recorded; overflow when M > cap_M
   // (and the longest list: the sort kernels launched are those of lists up to cap_L)
   const int64_t capL = ws->capL > 0 ? ws->capL : ((int64_t)1 << 40);
   k_caps_check<<<1, 1, 0, st>>>(starts + T, capM, ovf, need + 1, w.dev_i64 + 1, need + 3, capL, nullptr, nullptr);
-  ts_impl_bin_sort(cap, tx, ty, so.md, w, starts, splat_off, capL, keys, gs, items, pos_of, nonmono, st,
+  ts_impl_bin_sort(cap, tx, ty, so.md, w, starts, nullptr, capL, keys, gs, items, nullptr, nonmono, st,
                    reinterpret_cast<uint32_t*>(pcnt), &dyn);
-  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems, cpos, clen};
+  BinsView bv{starts, nullptr, items, nullptr, nonmono, witems, cpos, clen};
   const float* colors = nullptr;
   if (colors_tet && cmap) {
     float* c = ws->colors.get<float>(cap * 3);
@@ -341,31 +340,29 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   w.scratch = scratch;
   w.dev_i64 = ws->dev_i64.get<int64_t>(2);
   int64_t* starts = ws->starts.get<int64_t>(T + 1);
-  int64_t* splat_off = ws->splat_off.get<int64_t>(cap + 1);
   uint8_t* nonmono = ws->nonmono.get<uint8_t>(T);
-  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !splat_off || !nonmono)
+  if (!w.br || !w.q || !w.splat_cnt || !w.tile_cnt || !w.dev_i64 || !starts || !nonmono)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   int64_t M = 0, maxL = 0;
-  ts_impl_bin_count(K, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, splat_off, &M, &maxL, st, nullptr,
+  ts_impl_bin_count(K, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, nullptr, &M, &maxL, st, nullptr,
                     so.prect, so.qbits);
   int32_t* items = ws->items.get<int32_t>(M);
-  int32_t* pos_of = ws->pos_of.get<int32_t>(M);
   int32_t* witems = ws->witems.get<int32_t>(M);
   int32_t* cpos = ws->cpos.get<int32_t>(M);
   int32_t* clen = ws->clen.get<int32_t>(T);
   uint64_t* keys = ws->keys.get<uint64_t>(M);
   uint64_t* gs = maxL > 16384 ? ws->gsort.get<uint64_t>(2 * M) : nullptr;
-  if (!items || !pos_of || !witems || !cpos || !clen || !keys || (maxL > 16384 && !gs))
+  if (!items || !witems || !cpos || !clen || !keys || (maxL > 16384 && !gs))
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   // the sort also writes each position's depth key into the pair-count scratch, which k_window
   // reads (each tile before k_window_counts overwrites it with the tile's pair counts)
   int32_t* pcnt = ws->pcnt.get<int32_t>(M);
   if (!pcnt) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   if (M > 0)
-    ts_impl_bin_sort(K, tx, ty, so.md, w, starts, splat_off, maxL, keys, gs, items, pos_of, nonmono, st,
+    ts_impl_bin_sort(K, tx, ty, so.md, w, starts, nullptr, maxL, keys, gs, items, nullptr, nonmono, st,
                      reinterpret_cast<uint32_t*>(pcnt));
   else cudaMemsetAsync(nonmono, 0, T, st);
-  BinsView bv{starts, splat_off, items, pos_of, nonmono, witems, cpos, clen};
+  BinsView bv{starts, nullptr, items, nullptr, nonmono, witems, cpos, clen};
   // ---- colors of the visible splats ------------------------------------------------------
   const float* colors = nullptr;
   if (colors_tet && cmap && K > 0) {
@@ -448,8 +445,7 @@ static int view_backward(ts_workspace* ws, const double* deform, const float* co
   scr.rows = reinterpret_cast<float*>(ws->rows.p);
   const float* m4[4] = {maps[0], maps[1], maps[2], ws->color ? maps[3] : nullptr};
   const float* d4[4] = {dmaps[0], dmaps[1], dmaps[2], ws->color ? dmaps[3] : nullptr};
-  BinsView bv{reinterpret_cast<int64_t*>(ws->starts.p), reinterpret_cast<int64_t*>(ws->splat_off.p),
-              reinterpret_cast<int32_t*>(ws->items.p), reinterpret_cast<int32_t*>(ws->pos_of.p),
+  BinsView bv{reinterpret_cast<int64_t*>(ws->starts.p), nullptr, reinterpret_cast<int32_t*>(ws->items.p), nullptr,
               reinterpret_cast<uint8_t*>(ws->nonmono.p), reinterpret_cast<int32_t*>(ws->witems.p),
               reinterpret_cast<int32_t*>(ws->cpos.p), reinterpret_cast<int32_t*>(ws->clen.p)};
   ts_impl_backward(ws->tiles_x, ws->tiles_y, bv, ws->M, ws->K, reinterpret_cast<SplatRec*>(ws->rec.p),
