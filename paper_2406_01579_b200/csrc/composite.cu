@@ -523,7 +523,48 @@ struct Prefetch {
   SplatRec raw[kCh];
   int32_t idx[kCh];
   int64_t ib0;  // item_off of the next chunk's first list position
+#ifdef TS_TMA_RECORDS
+  // TMA variant (A/B experiment, profiles/r02_experiments.md): each record is one bulk copy
+  // (cp.async.bulk, 96 B) completing on this mbarrier; ph = each staging thread's next parity
+  unsigned long long bar;
+  uint8_t ph[kCh];
+#endif
 };
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+#ifdef TS_TMA_RECORDS
+__device__ __forceinline__ void tma_wait(Prefetch& P) {
+  const unsigned bar = smem_u32(&P.bar), par = P.ph[threadIdx.x];
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(bar), "r"(par)
+                 : "memory");
+  P.ph[threadIdx.x] = (uint8_t)(par ^ 1u);
+}
+#endif
+// threads [0, kCh) before the CTA exits: the one record prefetch still in flight lands first
+// (a bulk copy must not write the shared memory of a CTA that has left)
+__device__ __forceinline__ void tma_drain(Prefetch& P) {
+#ifdef TS_TMA_RECORDS
+  if (threadIdx.x < kCh) tma_wait(P);
+#else
+  (void)P;
+#endif
+}
+// threads [0, kCh), before the first prefetch (TMA variant only)
+__device__ __forceinline__ void tma_init(Prefetch& P) {
+#ifdef TS_TMA_RECORDS
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.bar)) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  P.ph[threadIdx.x] = 0;
+  asm volatile("bar.sync 1, %0;" ::"n"(kCh));
+#else
+  (void)P;
+#endif
+}
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
@@ -551,6 +592,24 @@ __device__ __forceinline__ void prefetch_idx(Prefetch& P, const int32_t* __restr
 __device__ __forceinline__ void prefetch_rec(Prefetch& P, const SplatRec* __restrict__ recs, int avail) {
   const int t = threadIdx.x;
   cp_async_wait_all();
+#ifdef TS_TMA_RECORDS
+  {
+    const int m = max(0, min(kCh, avail));
+    const unsigned bar = smem_u32(&P.bar);
+    if (t == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(m * (int)sizeof(SplatRec))
+                   : "memory");
+    if (t < m) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // this slot's reads before the async write
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(&P.raw[t])),
+          "l"(recs + P.idx[t]), "n"((int)sizeof(SplatRec)), "r"(bar)
+          : "memory");
+    }
+    return;
+  }
+#endif
   if (t < min(kCh, avail)) {
     const float4* src = reinterpret_cast<const float4*>(recs + P.idx[t]);
     float4* dst = reinterpret_cast<float4*>(&P.raw[t]);
@@ -573,6 +632,9 @@ __device__ __forceinline__ void stage_chunk(const int32_t* __restrict__ list, in
   const int m = min(kCh, avail);
   int cnt = 0, x0 = 0, y0 = 0, nx = 1;
   cp_async_wait_all();
+#ifdef TS_TMA_RECORDS
+  tma_wait(P);
+#endif
   if (t < m) {
     const int k = P.idx[t];
     stage<FOLD>(P.raw[t], k, sh[t]);
@@ -737,6 +799,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
   }
   if (threadIdx.x < kCh) {
+    tma_init(F.pf);
     prefetch_idx(F.pf, list, item_off + lo, 0, L);
     prefetch_rec(F.pf, recs, L);
   }
@@ -854,6 +917,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     TS_PHASE(3);
     if (all_done) break;
   }
+  tma_drain(F.pf);
   if (inside) {
     const int64_t p = (int64_t)yi * W + xi;
     opacity_map[p] = acc.o;
@@ -1353,6 +1417,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
   P.zero();
   if (ptime) pacc[7] = clock64();
   if (threadIdx.x < kCh) {
+    tma_init(S.pf);
     prefetch_idx(S.pf, list, item_off + lo, 0, maxproc);
     prefetch_rec(S.pf, recs, maxproc);
   }
@@ -1471,6 +1536,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 3) k_backward(
     base += n;
     TS_PHASE(4);
   }
+  tma_drain(S.pf);
   if (ptime)
     for (int k = 0; k < 5; ++k) atomicAdd(&g_ts_phase[8 + k], (unsigned long long)pacc[k]);
 }
