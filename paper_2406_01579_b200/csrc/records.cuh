@@ -200,7 +200,7 @@ __device__ __forceinline__ uint32_t qhash(uint32_t q) { return (q * 0x9E3779B1u)
 // fused view path: the packed rectangle of an active tet the view culls (no splat; the scene
 // is indexed by active tet there, composite.cu never sees it) — distinct from every empty
 // rectangle a record can carry
-constexpr int kCulledRect = (int)0x80000000;
+constexpr int kCulledRect = INT32_MIN;
 __device__ __forceinline__ bool rect_empty(int2 pr) {
   return (int)(short)(pr.x & 0xffff) > (pr.x >> 16) || (int)(short)(pr.y & 0xffff) > (pr.y >> 16);
 }
@@ -270,7 +270,7 @@ __device__ inline SplatRec make_record(const double proj[8], const double depths
     }
     const double fmx = fmax(fabs(f[1] - f[0]), fmax(fabs(f[2] - f[0]), fabs(f[3] - f[0])));
     if (never_blends(r, ix1 - ix0 + 1, iy1 - iy0 + 1, amin, C + M, M, fabsmax, fmx)) {
-      r.rx = (ix0 & 0xffff) | ((ix0 - 1) << 16);
+      r.rx = (int32_t)((uint32_t)(ix0 & 0xffff) | ((uint32_t)(ix0 - 1) << 16));
       r.flags |= 32u;
     }
   }

@@ -324,12 +324,9 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   if (!so.tet_ids || !so.rec || !scratch || !so.qbits) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
   cudaMemsetAsync(so.qbits, 0, sizeof(uint32_t) * kQBitWords, st);
   // the scene indexed by active tet (k_cull_emit: no compaction, culled tets keep their slot)
-  int64_t* nvis_dev = ws->dev_i64.get<int64_t>(2);
+  int64_t* nvis_dev = ws->need.get<int64_t>(4);  // (the sync-free path's counts; free here)
   if (!nvis_dev) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
-  int64_t Kvis = 0;
   ts_impl_build_scene_inplace(sdf, deform, R, cam, s, active, n_active, so, nvis_dev, st);
-  cudaMemcpyAsync(&Kvis, nvis_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaStreamSynchronize(st);  // (the bin count below syncs anyway)
   const int64_t K = n_active > 0 ? n_active : 0;
   // ---- K3-K5 bins ----------------------------------------------------------------------------
   BinWork w;
@@ -346,6 +343,8 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
   int64_t M = 0, maxL = 0;
   ts_impl_bin_count(K, so.bbox, so.md, tx, ty, cam.near_, cam.far_, w, starts, nullptr, &M, &maxL, st, nullptr,
                     so.prect, so.qbits);
+  int64_t Kvis = 0;  // reported only; the bin count above already waited for the scene build
+  cudaMemcpyAsync(&Kvis, nvis_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st);  // pageable: returns when done
   int32_t* items = ws->items.get<int32_t>(M);
   int32_t* witems = ws->witems.get<int32_t>(M);
   int32_t* cpos = ws->cpos.get<int32_t>(M);
