@@ -63,8 +63,9 @@ __global__ void k_bin_count(int64_t K, const double* __restrict__ bbox, const do
         if (pr.x == kCulledRect) {
           nx = ny = 0;
         } else if (qbits && rect_empty(pr)) {
-          const uint32_t h = qhash(q);
-          if (!((__ldg(qbits + (h >> 5)) >> (h & 31)) & 1u)) nx = ny = 0;
+          const uint32_t h = qhash(q), h2 = qhash2(q);
+          const unsigned long long* mx = qtab_max(qbits);
+          if (!((__ldg(qbits + (h >> 5)) >> (h & 31)) & 1u) || __ldg(mx + h2) == __ldg(mx + kQTab + h2)) nx = ny = 0;
         }
       }
       br[k] = BinRec{tx0, ty0, nx, ny};
@@ -314,7 +315,30 @@ __device__ __forceinline__ void radix_sort_keys(uint32_t* kq, uint32_t* kv, uint
   }
 }
 
-// one CTA per tile for the tiles with 0 < L <= cap (bitonic up to 512 entries, radix above)
+// one CTA per tile for the tiles with 0 < L <= 512: bitonic in 4 KB of shared memory, few
+// registers (several CTAs per SM: most lists are this short once the fused path leaves out the
+// never-composited splats)
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) k_tile_sort_bitonic(int T, const int64_t* __restrict__ starts,
+                                                              const uint64_t* __restrict__ keys, int tiles_x,
+                                                              const BinRec* __restrict__ br,
+                                                              const int64_t* __restrict__ splat_off,
+                                                              const double* __restrict__ md,
+                                                              int32_t* __restrict__ items,
+                                                              int32_t* __restrict__ pos_of,
+                                                              uint8_t* __restrict__ nonmono,
+                                                              uint32_t* __restrict__ qsorted,
+                                                              const int* __restrict__ ovf) {
+  __shared__ uint64_t s[512];
+  __shared__ int bad;
+  const int t = blockIdx.x;
+  if (t >= T || (ovf && *ovf)) return;
+  const int64_t L = starts[t + 1] - starts[t];
+  if (L <= 0 || L > 512) return;
+  sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono, qsorted);
+}
+
+// one CTA per tile for the tiles with 512 < L <= cap (radix)
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, int passes_lo,
                                                             const int64_t* __restrict__ starts,
@@ -330,11 +354,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   const int t = blockIdx.x;
   if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
-  if (L <= 0 || L > cap) return;
-  if (L <= 512) {  // short lists: bitonic
-    sort_tile<THREADS>(s, bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of, nonmono, qsorted);
-    return;
-  }
+  if (L <= 512 || L > cap) return;  // (L <= 512: k_tile_sort_bitonic)
   // longer lists: the radix sort of k_tile_sort_long at THREADS threads (kq / kv alias s)
   uint32_t* kq = reinterpret_cast<uint32_t*>(s);
   uint32_t* kv = kq + cap;
@@ -556,8 +576,11 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
       return true;
     }();
     (void)attr_s;
-    k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, kSmemSortCap, (kbits + 7) / 8, starts, keys, tiles_x, w.br, splat_off,
-                                                  md, items, pos_of, nonmono, qsorted, ovf);
+    k_tile_sort_bitonic<256><<<T, 256, 0, st>>>(T, starts, keys, tiles_x, w.br, splat_off, md, items, pos_of, nonmono,
+                                                qsorted, ovf);
+    if (dyn || maxL > 512)
+      k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, kSmemSortCap, (kbits + 7) / 8, starts, keys, tiles_x, w.br,
+                                                    splat_off, md, items, pos_of, nonmono, qsorted, ovf);
     // the attribute is set once, to the 16384-entry cap (a thread-safe static: views in
     // flight launch from several host threads); the launch asks for what it needs
     static const bool attr = [] {

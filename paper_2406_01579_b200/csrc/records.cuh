@@ -190,13 +190,29 @@ __device__ __forceinline__ uint32_t depth_key(double md, double near_, double fa
 // (certified never to blend, or no pixel centre inside its bbox) is never composited, so the
 // only effect of its list entries is on the N_w window of its tile.  The window acts on each
 // run of equal depth key independently (a key change is a clean boundary: composite.cu
-// window_tile), so removing every member of a run leaves the pop order of the other entries
-// unchanged.  The fused path therefore drops such a splat only when no splat with a
-// non-empty rectangle has its depth key (anywhere: a hashed bitmap, false positives keep a
-// splat); list positions (n_proc) are internal to that path.
+// window_tile), and inside a run whose members all have the same mean depth it pops in list
+// order (ties go to the earlier position).  So removing such a splat leaves the pop order of
+// every other entry unchanged when (a) no splat with a non-empty rectangle has its depth key,
+// or (b) every splat with its depth key has the same mean depth (lattice-aligned views tie
+// thousands of splats per key).  The fused path tests both with hashed tables filled by the
+// scene build — a bitmap of the keys of splats with pixels, and per key bucket the min / max
+// mean-depth bit pattern (md > 0, so the bits order like the values); hash collisions only
+// keep a splat.  List positions (n_proc) are internal to that path.
 constexpr int kQHashBits = 24;
 constexpr int kQBitWords = 1 << (kQHashBits - 5);
+constexpr int kQTabBits = 20;  // mean-depth range buckets
+constexpr int kQTab = 1 << kQTabBits;
+// one buffer: [kQBitWords] u32 key bitmap | [kQTab] u64 max md bits | [kQTab] u64 min md bits
+constexpr size_t kQBytesZero = sizeof(uint32_t) * kQBitWords + sizeof(unsigned long long) * kQTab;
+constexpr size_t kQBytes = kQBytesZero + sizeof(unsigned long long) * kQTab;  // the min table starts at ~0
 __device__ __forceinline__ uint32_t qhash(uint32_t q) { return (q * 0x9E3779B1u) >> (32 - kQHashBits); }
+__device__ __forceinline__ uint32_t qhash2(uint32_t q) { return (q * 0x9E3779B1u) >> (32 - kQTabBits); }
+__device__ __forceinline__ unsigned long long* qtab_max(uint32_t* qbits) {
+  return reinterpret_cast<unsigned long long*>(qbits + kQBitWords);
+}
+__device__ __forceinline__ const unsigned long long* qtab_max(const uint32_t* qbits) {
+  return reinterpret_cast<const unsigned long long*>(qbits + kQBitWords);
+}
 // fused view path: the packed rectangle of an active tet the view culls (no splat; the scene
 // is indexed by active tet there, composite.cu never sees it) — distinct from every empty
 // rectangle a record can carry

@@ -226,9 +226,16 @@ struct CullF {
                                    out.certify && amin > 1e-9 * gn2 ? amin : 0.0);
     out.rec[k] = r;
     if (out.prect) out.prect[k] = make_int2(r.rx, r.ry);
-    if (out.qbits && !rect_empty(make_int2(r.rx, r.ry))) {  // (fused path)
-      const uint32_t h = qhash(depth_key(md, cam.near_, cam.far_));
-      atomicOr(out.qbits + (h >> 5), 1u << (h & 31));
+    if (out.qbits) {  // (fused path) the drop tables of records.cuh
+      const uint32_t q = depth_key(md, cam.near_, cam.far_);
+      if (!rect_empty(make_int2(r.rx, r.ry))) {
+        const uint32_t h = qhash(q);
+        atomicOr(out.qbits + (h >> 5), 1u << (h & 31));
+      }
+      unsigned long long* mx = qtab_max(out.qbits);
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(md), h2 = qhash2(q);
+      atomicMax(mx + h2, bits);
+      atomicMin(mx + kQTab + h2, bits);
     }
   }
 };

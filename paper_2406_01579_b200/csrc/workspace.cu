@@ -206,10 +206,11 @@ static int view_forward_dyn(ts_workspace* ws, const double* sdf, const double* d
               ws->rec.get<SplatRec>(cap), ws->prect.get<int2>(cap)};
   const int64_t nmax = cap > T ? (cap > capM ? cap : capM) : (T > capM ? T : capM);
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks(nmax + 1, 1));
-  so.qbits = ws->qbits.get<uint32_t>(kQBitWords);
+  so.qbits = reinterpret_cast<uint32_t*>(ws->qbits.get<unsigned char>(kQBytes));
   if (!need || !ovf || !so.tet_ids || !so.rec || !scratch || !so.qbits)
     return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
-  cudaMemsetAsync(so.qbits, 0, sizeof(uint32_t) * kQBitWords, st);
+  cudaMemsetAsync(so.qbits, 0, kQBytesZero, st);                                          // keys, max md
+  cudaMemsetAsync(reinterpret_cast<unsigned char*>(so.qbits) + kQBytesZero, 0xff, kQBytes - kQBytesZero, st);  // min md
   cudaMemsetAsync(ovf, 0, sizeof(int), st);
   cudaMemsetAsync(need, 0, 4 * sizeof(int64_t), st);
   Dyn dyn;
@@ -320,9 +321,10 @@ int ts_view_forward(ts_workspace* ws, const double* sdf, const double* deform, i
               ws->md.get<double>(cap), nullptr, ws->bbox.get<double>(cap * 4),
               ws->rec.get<SplatRec>(cap), ws->prect.get<int2>(cap)};
   int64_t* scratch = ws->scratch.get<int64_t>(compact_blocks((cap > T ? cap : T) + 1, 1));
-  so.qbits = ws->qbits.get<uint32_t>(kQBitWords);
+  so.qbits = reinterpret_cast<uint32_t*>(ws->qbits.get<unsigned char>(kQBytes));
   if (!so.tet_ids || !so.rec || !scratch || !so.qbits) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");
-  cudaMemsetAsync(so.qbits, 0, sizeof(uint32_t) * kQBitWords, st);
+  cudaMemsetAsync(so.qbits, 0, kQBytesZero, st);                                          // keys, max md
+  cudaMemsetAsync(reinterpret_cast<unsigned char*>(so.qbits) + kQBytesZero, 0xff, kQBytes - kQBytesZero, st);  // min md
   // the scene indexed by active tet (k_cull_emit: no compaction, culled tets keep their slot)
   int64_t* nvis_dev = ws->need.get<int64_t>(4);  // (the sync-free path's counts; free here)
   if (!nvis_dev) return ws_fail(TS_ENOMEM, "ts_view_forward: out of device memory");

@@ -308,3 +308,35 @@ def test_fused_drop_keeps_window_order(ts, far, n_w):
     assert torch.equal(m2.opacity, maps.opacity)
     gb2 = vr.backward(f, dm, ts.GradientBuffers.zeros(g.num_vertices))
     assert torch.allclose(gb2.d_vert, gb.d_vert, rtol=1e-6, atol=1e-6 * float(gb.d_vert.abs().max()))
+
+
+@pytest.mark.parametrize("n_w", [1, 3, 8])
+def test_fused_drop_tied_depth_runs(ts, n_w):
+    """Lattice-aligned views tie thousands of splats per depth key with identical mean depths;
+    inside such a run the window pops in list order, so the fused path also drops
+    never-composited splats that share a key with composited ones when every splat of the key
+    has the same mean depth (records.cuh, rule (b)).  The fused lists must be much shorter
+    than the API's (the rule is active) and the maps equal bit for bit."""
+    from paper_2406_01579_b200.view import ViewRenderer
+    R, S, s = 32, 256, 100.0
+    g = ts.build_grid(R)
+    f = ts.init_from_shape(g, ts.AnalyticShape("sphere", (0.5,)))
+    cam = ts.orbit_camera(0, 8, width=S, height=S)
+    active = ts.prefilter(g, f, s)
+    sc = ts.build_scene(g, f, cam, s, active=active)
+    md = sc.mean_depth
+    q = (((md - cam.near) / (cam.far - cam.near)).clamp(0, 1) * 4294967295.0).to(torch.int64)
+    assert torch.unique(q).numel() < len(sc) // 4, "no tied depth keys in this view"
+    b = ts.bin_and_sort(sc, cam)
+    maps, saved = ts.render_forward(sc, b, cam, n_w=n_w, save_state=True)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    dm = ts.RenderMaps(torch.randn((S, S, 3), device="cuda", generator=gen),
+                       torch.randn((S, S), device="cuda", generator=gen), torch.randn((S, S), device="cuda", generator=gen))
+    gb = ts.render_backward(saved, sc, g, f, cam, dm)
+    vr = ViewRenderer()
+    m2 = vr.forward(g, f, cam, s, active, n_w=n_w)
+    assert vr.counts[0] == len(sc) and vr.counts[1] < 0.8 * b.num_pairs, (vr.counts, b.num_pairs)
+    assert torch.equal(m2.normal, maps.normal) and torch.equal(m2.depth, maps.depth)
+    assert torch.equal(m2.opacity, maps.opacity)
+    gb2 = vr.backward(f, dm, ts.GradientBuffers.zeros(g.num_vertices))
+    assert torch.allclose(gb2.d_vert, gb.d_vert, rtol=1e-6, atol=1e-6 * float(gb.d_vert.abs().max()))
