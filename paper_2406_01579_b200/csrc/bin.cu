@@ -354,7 +354,16 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   const int t = blockIdx.x;
   if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
+#ifdef TS_SORT_NOSPLIT
+  if (L <= 0 || L > cap) return;
+  if (L <= 512) {  // (A/B: short lists here too, at this kernel's occupancy)
+    sort_tile<THREADS>(reinterpret_cast<uint64_t*>(s), bad, t, starts, keys, tiles_x, br, splat_off, md, items, pos_of,
+                       nonmono, qsorted);
+    return;
+  }
+#else
   if (L <= 512 || L > cap) return;  // (L <= 512: k_tile_sort_bitonic)
+#endif
   // longer lists: the radix sort of k_tile_sort_long at THREADS threads (kq / kv alias s)
   uint32_t* kq = reinterpret_cast<uint32_t*>(s);
   uint32_t* kv = kq + cap;
@@ -576,9 +585,11 @@ void ts_impl_bin_sort(int64_t K, int tiles_x, int tiles_y, const double* md, con
       return true;
     }();
     (void)attr_s;
+#ifndef TS_SORT_NOSPLIT
     k_tile_sort_bitonic<256><<<T, 256, 0, st>>>(T, starts, keys, tiles_x, w.br, splat_off, md, items, pos_of, nonmono,
                                                 qsorted, ovf);
     if (dyn || maxL > 512)
+#endif
       k_tile_sort_smem<256><<<T, 256, smem_s, st>>>(T, kSmemSortCap, (kbits + 7) / 8, starts, keys, tiles_x, w.br,
                                                     splat_off, md, items, pos_of, nonmono, qsorted, ovf);
     // the attribute is set once, to the 16384-entry cap (a thread-safe static: views in
