@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(logs))
     tmp = lib + ".tmp"
-    subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "--no-undefined", "-o", tmp, *objs])
     os.replace(tmp, lib)
     if verbose:
         print("\n".join(logs))

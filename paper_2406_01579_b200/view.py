@@ -59,6 +59,16 @@ class ViewRenderer:
         self._last = maps
         return maps
 
+    def n_blend(self) -> torch.Tensor:
+        """(H, W) int32 blends per pixel of the last forward (a copy; stream-ordered on the
+        current stream) — for parity checks."""
+        H, W = self._last.depth.shape
+        p = self._L.ts_view_n_blend(self._ws)
+
+        class _Dev:  # the workspace buffer seen through __cuda_array_interface__
+            __cuda_array_interface__ = {"shape": (H, W), "typestr": "<i4", "data": (int(p), False), "version": 2}
+        return torch.as_tensor(_Dev(), device=self.device).clone()
+
     def set_caps(self, cap_pairs: int = 0, cap_pixel_pairs: int = 0, cap_list: int = 0,
                  need_out: torch.Tensor | None = None):
         """Capacities of the sync-free forward (tile pairs M, pixel pairs P, the longest tile
