@@ -8,10 +8,12 @@
 // connectivity:
 //   E1  per vertex a: 7 sign-change flags for its forward Kuhn edges (deltas 1, n, n+1, n^2,
 //       n^2+1, n^2+n, n^2+n+1 — ascending, so (a, slot) order IS the lexicographic edge
-//       order) -> exclusive scan = the index of each crossing edge in np.unique's output
+//       order) -> per-32-vertex-word counts, exclusive scan + in-word popcounts = the index
+//       of each crossing edge in np.unique's output; the crossing edges listed in that order
 //   E2  crossing positions p = (f_b v_a - f_a v_b) / (f_b - f_a) in FP64 without
-//       contraction, endpoint snap on f == 0 (grid.py:120-133)
-//   T1  per tet class counts in 2048-tet chunks, scans -> group-ordered output slots
+//       contraction, endpoint snap on f == 0 (grid.py:120-133), one thread per edge
+//   T1  per tet class counts in 2048-tet chunks, scans -> group-ordered output slots (with
+//       R % 8 == 0 from z-fastest sign rows: eight cells per four word windows)
 //   T2  per crossing tet: slot edges, quad diagonal rule (np.isclose + min-parent key),
 //       orientation against the cross-product tet gradient
 //   W   weld: merge sort (1024-key shared-memory block sorts, then merge-path passes) of the
@@ -37,19 +39,23 @@ __device__ __forceinline__ void edge_off(int s, int& ox, int& oy, int& oz) {
   oz = (s >= 3);
 }
 
-// E1: per-vertex crossing flags (bit s) and counts; negbits = one "f < 0" bit per vertex
-// (2 MB at 256^3: the per-cell classification reads it from L2 instead of the FP64 field)
+// E1: per-vertex crossing flags (bit s: the sign differs across forward edge s), negbits = one
+// "f < 0" bit per vertex (2 MB at 256^3: the per-cell classification reads it from L2), and the
+// crossing-edge count of every 32-vertex word (scanned into per-word bases: a vertex's first
+// edge index = its word's base + the flag popcounts of the vertices before it in the word —
+// no per-vertex count / offset arrays)
 __global__ void k_mt_vflags(int64_t N, Grid G, const double* __restrict__ sdf, uint8_t* __restrict__ flags,
-                            int32_t* __restrict__ cnt, uint32_t* __restrict__ negbits) {
+                            int32_t* __restrict__ wcnt, uint32_t* __restrict__ negbits) {
   for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); a0 < N;
        a0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = a0 + (threadIdx.x & 31);
     bool na = false;
+    uint32_t fl = 0;
     if (a < N) {
       int x, y, z;
       vertex_xyz((uint32_t)a, G, x, y, z);
       na = sdf[a] < 0.0;
-      uint32_t fl = 0;
+#pragma unroll
       for (int s = 0; s < 7; ++s) {
         int ox, oy, oz;
         edge_off(s, ox, oy, oz);
@@ -58,11 +64,56 @@ __global__ void k_mt_vflags(int64_t N, Grid G, const double* __restrict__ sdf, u
         if ((sdf[b] < 0.0) != na) fl |= 1u << s;
       }
       flags[a] = (uint8_t)fl;
-      cnt[a] = __popc(fl);
     }
     const unsigned w = __ballot_sync(0xffffffffu, na);
-    if ((threadIdx.x & 31) == 0) negbits[a0 >> 5] = w;
+    const int c = warp_sum(__popc(fl));
+    if ((threadIdx.x & 31) == 0) {
+      negbits[a0 >> 5] = w;
+      wcnt[a0 >> 5] = c;
+    }
   }
+}
+
+// E1b: the crossing edges in np.unique order, elist[e] = a << 3 | s — one warp per 32-vertex
+// word with crossings (the words' bases from the scan, ranks by a warp scan of the counts)
+__global__ void k_mt_elist(int64_t N, const uint8_t* __restrict__ flags, const int64_t* __restrict__ wbase,
+                           int64_t* __restrict__ elist) {
+  const int64_t nw = (N + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t e0 = __ldg(wbase + w);
+    if (__ldg(wbase + w + 1) == e0) continue;  // (warp-uniform)
+    const int64_t a = (w << 5) + lane;
+    const uint32_t fl = a < N ? flags[a] : 0u;
+    const int c = __popc(fl);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int64_t e = e0 + incl - c;
+    for (uint32_t m = fl; m; m &= m - 1u) elist[e++] = (a << 3) | (__ffs(m) - 1);
+  }
+}
+
+// first crossing-edge index of vertex a: its word's base + the flag popcounts of the vertices
+// a0 .. a - 1 of the word (flags padded to whole 32-byte words)
+__device__ __forceinline__ int64_t vbase(const uint8_t* __restrict__ flags, const int64_t* __restrict__ wbase,
+                                         int64_t a) {
+  const int r = (int)(a & 31);
+  const uint4* f4 = reinterpret_cast<const uint4*>(flags + (a - r));
+  const uint4 lo = __ldg(f4), hi = __ldg(f4 + 1);
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int nb = r - 4 * k;  // bytes of word k before a
+    const uint32_t m = nb >= 4 ? 0xffffffffu : (nb <= 0 ? 0u : (1u << (8 * nb)) - 1u);
+    c += __popc(w[k] & m);
+  }
+  return wbase[a >> 5] + c;
 }
 
 __device__ __forceinline__ int64_t edge_index(const uint8_t* flags, const int64_t* ebase, int64_t a, int64_t b,
@@ -74,39 +125,30 @@ __device__ __forceinline__ int64_t edge_index(const uint8_t* flags, const int64_
   }
   const int64_t d = b - a;
   int s = d == 1 ? 0 : d == n ? 1 : d == n + 1 ? 2 : d == n * n ? 3 : d == n * n + 1 ? 4 : d == n * n + n ? 5 : 6;
-  return ebase[a] + __popc((uint32_t)flags[a] & ((1u << s) - 1u));
+  return vbase(flags, ebase, a) + __popc((uint32_t)flags[a] & ((1u << s) - 1u));
 }
 
-// E2: crossing positions (_edge_crossings, grid.py:120-133)
-__global__ void k_mt_verts(int64_t N, Grid G, const double* __restrict__ sdf, const double* __restrict__ deform,
-                           const uint8_t* __restrict__ flags, const int64_t* __restrict__ ebase,
-                           double* __restrict__ verts) {
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < N; a += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t fl = flags[a];
-    if (!fl) continue;
-    double pa[3], pb[3];
+// E2: crossing positions (_edge_crossings, grid.py:120-133), one thread per crossing edge
+__global__ void k_mt_verts(int64_t V, Grid G, const double* __restrict__ sdf, const double* __restrict__ deform,
+                           const int64_t* __restrict__ elist, double* __restrict__ verts) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < V; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t code = __ldg(elist + e);
+    const int64_t a = code >> 3, b = a + edge_delta((int)(code & 7), G.n);
+    const double fa = sdf[a], fb = sdf[b];
+    double pa[3], pb[3], p[3];
     vertex_position((uint32_t)a, G, deform, pa);
-    const double fa = sdf[a];
-    int64_t e = ebase[a];
-    for (int s = 0; s < 7; ++s) {
-      if (!((fl >> s) & 1u)) continue;
-      const int64_t b = a + edge_delta(s, G.n);
-      vertex_position((uint32_t)b, G, deform, pb);
-      const double fb = sdf[b];
-      double p[3];
-      if (fa == 0.0) {
-        p[0] = pa[0]; p[1] = pa[1]; p[2] = pa[2];
-      } else if (fb == 0.0) {
-        p[0] = pb[0]; p[1] = pb[1]; p[2] = pb[2];
-      } else {
-        const double den = dsub(fb, fa);
-        for (int c = 0; c < 3; ++c) p[c] = ddiv(dsub(dmul(fb, pa[c]), dmul(fa, pb[c])), den);
-      }
-      verts[e * 3 + 0] = p[0];
-      verts[e * 3 + 1] = p[1];
-      verts[e * 3 + 2] = p[2];
-      ++e;
+    vertex_position((uint32_t)b, G, deform, pb);
+    if (fa == 0.0) {
+      p[0] = pa[0]; p[1] = pa[1]; p[2] = pa[2];
+    } else if (fb == 0.0) {
+      p[0] = pb[0]; p[1] = pb[1]; p[2] = pb[2];
+    } else {
+      const double den = dsub(fb, fa);
+      for (int c = 0; c < 3; ++c) p[c] = ddiv(dsub(dmul(fb, pa[c]), dmul(fa, pb[c])), den);
     }
+    verts[e * 3 + 0] = p[0];
+    verts[e * 3 + 1] = p[1];
+    verts[e * 3 + 2] = p[2];
   }
 }
 
@@ -138,6 +180,67 @@ __device__ __forceinline__ uint32_t cell_negmask(uint32_t c, const Grid& G, cons
   return m;
 }
 
+// The same signs with z fastest: row (x, y) = ww words holding bit z of vertex (x, y, z),
+// z = 0..R (32 x 32 bit blocks of negbits transposed).  With R % 8 == 0 a thread's
+// eight cells c0..c0+7 share (ix, iy), so their 4 x 9 corner bits are four shifted row windows
+// — two word loads each instead of 64 scattered bit loads — and the eight cells are skipped at
+// once when all 36 bits agree (no crossing: almost every cell of the grid).
+__global__ void k_mt_zbits(Grid G, const uint32_t* __restrict__ negbits, uint32_t* __restrict__ zbits, int ww) {
+  // one warp per (y, 32-x block, 32-z block): lane l takes the 32 x-bits of z = z0 + l (a
+  // funnel shift of two words: x rows are not word-aligned), then 32 ballots transpose the
+  // 32 x 32 bit block so lane x holds the z word of row (x0 + x, y)
+  const int n = G.n, nxb = (n + 31) / 32;
+  const int64_t ntask = (int64_t)n * nxb * ww;
+  const int lane = threadIdx.x & 31;
+  for (int64_t task = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; task < ntask;
+       task += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int zb = (int)(task % ww);
+    const int64_t rest = task / ww;
+    const int xb = (int)(rest % nxb), y = (int)(rest / nxb);
+    const int z = zb * 32 + lane;
+    uint32_t wl = 0;
+    if (z < n) {
+      const int64_t v = (int64_t)xb * 32 + (int64_t)n * (y + (int64_t)n * z);
+      const int sh = (int)(v & 31);
+      const uint32_t lo = __ldg(negbits + (v >> 5)), hi = __ldg(negbits + (v >> 5) + 1);  // (padded)
+      wl = sh ? (lo >> sh) | (hi << (32 - sh)) : lo;
+    }
+    uint32_t out = 0;
+#pragma unroll
+    for (int x = 0; x < 32; ++x) {
+      const unsigned m = __ballot_sync(0xffffffffu, (wl >> x) & 1u);
+      if (lane == x) out = m;
+    }
+    const int xx = xb * 32 + lane;
+    if (xx < n) zbits[((int64_t)xx * n + y) * ww + zb] = out;
+  }
+}
+
+// the 9-bit z windows iz0..iz0+8 of the four corner rows (dx | dy << 1) of cells c0..c0+7
+// (c0 % 8 == 0, R % 8 == 0); false when all 36 bits agree
+__device__ __forceinline__ bool cell_rows8(uint32_t c0, const Grid& G, const uint32_t* __restrict__ zbits, int ww,
+                                           uint32_t (&r)[4]) {
+  const uint32_t q = G.dR.div(c0);  // ix*R + iy
+  const uint32_t iz0 = c0 - q * (uint32_t)G.R;
+  const uint32_t ix = G.dR.div(q);
+  const uint32_t iy = q - ix * (uint32_t)G.R;
+  const uint32_t n = (uint32_t)G.n, sh = iz0 & 31u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t* p = zbits + (size_t)((ix + (k & 1)) * n + iy + (k >> 1)) * ww + (iz0 >> 5);
+    const uint64_t w = (uint64_t)__ldg(p) | (sh > 23u ? (uint64_t)__ldg(p + 1) << 32 : 0ull);
+    r[k] = (uint32_t)(w >> sh) & 0x1ffu;
+  }
+  return (r[0] | r[1] | r[2] | r[3]) != 0u && (r[0] & r[1] & r[2] & r[3]) != 0x1ffu;
+}
+// negative-corner mask of cell c0 + k from its rows (corner lc = dx | dy << 1 | dz << 2)
+__device__ __forceinline__ uint32_t cell_mask8(const uint32_t (&r)[4], int k) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int lc = 0; lc < 8; ++lc) m |= ((r[lc & 3] >> (k + (lc >> 2))) & 1u) << lc;
+  return m;
+}
+
 // class counts of a cell's 6 tets, packed n1 | n3 << 8 | n2 << 16
 __device__ __forceinline__ uint32_t cell_counts(uint32_t m) {
   if (m == 0u || m == 0xffu) return 0u;
@@ -151,14 +254,23 @@ __device__ __forceinline__ uint32_t cell_counts(uint32_t m) {
 }
 
 // T1: per-chunk counts of the three groups
+// (zbits != null: the z-fastest rows, R % 8 == 0)
 __global__ void __launch_bounds__(kScanThreads) k_mt_ccount(int64_t C, Grid G, const uint32_t* __restrict__ negbits,
                                                            int64_t* __restrict__ c1, int64_t* __restrict__ c3,
-                                                           int64_t* __restrict__ c2) {
+                                                           int64_t* __restrict__ c2, const uint32_t* __restrict__ zbits,
+                                                           int ww) {
   const int64_t c0 = (int64_t)blockIdx.x * kCellChunk + (int64_t)threadIdx.x * kCellsPerThread;
   uint32_t acc = 0;  // <= 8 cells x 6 tets per field
+  if (zbits) {
+    uint32_t r[4];
+    if (c0 < C && cell_rows8((uint32_t)c0, G, zbits, ww, r))
 #pragma unroll
-  for (int k = 0; k < kCellsPerThread; ++k)
-    if (c0 + k < C) acc += cell_counts(cell_negmask((uint32_t)(c0 + k), G, negbits));
+      for (int k = 0; k < kCellsPerThread; ++k) acc += cell_counts(cell_mask8(r, k));
+  } else {
+#pragma unroll
+    for (int k = 0; k < kCellsPerThread; ++k)
+      if (c0 + k < C) acc += cell_counts(cell_negmask((uint32_t)(c0 + k), G, negbits));
+  }
   int n1 = warp_sum((int)(acc & 0xffu)), n3 = warp_sum((int)((acc >> 8) & 0xffu)), n2 = warp_sum((int)(acc >> 16));
   __shared__ int s[3][kScanThreads / 32];
   if ((threadIdx.x & 31) == 0) {
@@ -282,14 +394,25 @@ __device__ void emit_quad(uint32_t t, int64_t s1, int64_t s2, const Grid& G, con
 __global__ void __launch_bounds__(kScanThreads) k_mt_clist(int64_t C, Grid G, const uint32_t* __restrict__ negbits,
                                                           const int64_t* __restrict__ o1, const int64_t* __restrict__ o3,
                                                           const int64_t* __restrict__ o2, int64_t n1, int64_t n3,
-                                                          uint32_t* __restrict__ tlist) {
+                                                          uint32_t* __restrict__ tlist, const uint32_t* __restrict__ zbits,
+                                                          int ww) {
   const int64_t c0 = (int64_t)blockIdx.x * kCellChunk + (int64_t)threadIdx.x * kCellsPerThread;
   uint32_t masks[kCellsPerThread];
   uint32_t acc = 0;
+  if (zbits) {
+    uint32_t r[4];
+    const bool any = c0 < C && cell_rows8((uint32_t)c0, G, zbits, ww, r);
 #pragma unroll
-  for (int k = 0; k < kCellsPerThread; ++k) {
-    masks[k] = c0 + k < C ? cell_negmask((uint32_t)(c0 + k), G, negbits) : 0u;
-    acc += cell_counts(masks[k]);
+    for (int k = 0; k < kCellsPerThread; ++k) {
+      masks[k] = any ? cell_mask8(r, k) : 0u;
+      acc += cell_counts(masks[k]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kCellsPerThread; ++k) {
+      masks[k] = c0 + k < C ? cell_negmask((uint32_t)(c0 + k), G, negbits) : 0u;
+      acc += cell_counts(masks[k]);
+    }
   }
   // block exclusive scan of the three counts (16-bit fields: <= 12288 per CTA, no carries)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -410,30 +533,72 @@ __global__ void __launch_bounds__(kLocalSort / 2) k_mt_block_sort(VKey* __restri
   for (int i = threadIdx.x; i < kLocalSort; i += blockDim.x) keys[b0 + i] = sk[i];
 }
 
-// One merge pass: runs of `w` sorted keys merged pairwise into `out` (merge path: every thread
-// finds where its kMergeItems outputs start on the two runs by a binary search on the
-// cross diagonal, then merges them sequentially).  Keys are unique (idx tie-break).
 constexpr int kMergeItems = 4;
+// first i in [max(0, d - w), min(d, w)] with B[d - 1 - i] < A[i] (the merge path's split of
+// output diagonal d between runs A and B), by a 32-way search of one warp: each round tests 32
+// evenly spaced candidates with independent loads (~4 rounds for a 2^18 run, instead of 18
+// dependent loads of a binary search)
+__device__ __forceinline__ int64_t warp_merge_path(const VKey* __restrict__ A, const VKey* __restrict__ B, int64_t w,
+                                                   int64_t d) {
+  int64_t lo = d > w ? d - w : 0, hi = d < w ? d : w;  // the answer is in [lo, hi] (hi: sentinel)
+  const int lane = threadIdx.x & 31;
+  while (lo < hi) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t i = lo + (int64_t)lane * step;
+    const bool p = i >= hi || vless(B[d - 1 - i], A[i]);
+    const unsigned m = __ballot_sync(0xffffffffu, p);
+    if (m == 0u) {  // all 32 candidates below the split
+      lo += 31 * step + 1;
+      continue;
+    }
+    const int f = __ffs(m) - 1;
+    if (f == 0) break;  // the split is lo
+    hi = min(hi, lo + (int64_t)f * step);
+    lo += (int64_t)(f - 1) * step + 1;
+  }
+  return lo;
+}
+
+// One merge pass: runs of `w` sorted keys merged pairwise into `out`.  Each CTA produces
+// kMergeTile consecutive outputs: warps 0 / 1 find the split of its first / last diagonal,
+// the two input windows are staged in shared memory (coalesced), and every thread merges
+// kMergeItems outputs after a merge-path search inside the windows.  Keys are unique (idx
+// tie-break).
+constexpr int kMergeTile = 256 * kMergeItems;
 __global__ void __launch_bounds__(256) k_mt_merge(int64_t P, int64_t w, const VKey* __restrict__ in,
                                                  VKey* __restrict__ out) {
-  const int64_t o0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergeItems;
-  if (o0 >= P) return;
-  const int64_t pair0 = o0 / (2 * w) * (2 * w);  // first key of this run pair
+  __shared__ VKey sk[kMergeTile];
+  __shared__ int64_t split[2];
+  const int64_t o0 = (int64_t)blockIdx.x * kMergeTile;
+  const int64_t pair0 = o0 / (2 * w) * (2 * w);  // first key of this run pair (2w % kMergeTile == 0)
   const VKey* A = in + pair0;
   const VKey* B = A + w;
-  const int64_t d = o0 - pair0;  // output position inside the pair
-  // merge path: i keys from A and d - i from B precede output d
-  int64_t lo = d > w ? d - w : 0, hi = d < w ? d : w;
+  const int64_t d0 = o0 - pair0;
+  const int warp = threadIdx.x >> 5;
+  if (warp < 2) {
+    const int64_t d = d0 + warp * kMergeTile;
+    const int64_t sp = d >= 2 * w ? w : warp_merge_path(A, B, w, d);
+    if ((threadIdx.x & 31) == 0) split[warp] = sp;
+  }
+  __syncthreads();
+  const int64_t a0 = split[0], b0 = d0 - a0;
+  const int na = (int)(split[1] - a0), nb = kMergeTile - na;
+  for (int k = threadIdx.x; k < kMergeTile; k += 256) sk[k] = k < na ? A[a0 + k] : B[b0 + (k - na)];
+  __syncthreads();
+  const VKey* sa = sk;
+  const VKey* sb = sk + na;
+  const int dd = threadIdx.x * kMergeItems;
+  int lo = dd > nb ? dd - nb : 0, hi = dd < na ? dd : na;
   while (lo < hi) {
-    const int64_t i = (lo + hi) >> 1;
-    if (vless(B[d - 1 - i], A[i])) hi = i;
+    const int i = (lo + hi) >> 1;
+    if (vless(sb[dd - 1 - i], sa[i])) hi = i;
     else lo = i + 1;
   }
-  int64_t i = lo, j = d - lo;
+  int i = lo, j = dd - lo;
 #pragma unroll
   for (int k = 0; k < kMergeItems; ++k) {
-    const bool takeA = j >= w || (i < w && vless(A[i], B[j]));
-    out[o0 + k] = takeA ? A[i] : B[j];
+    const bool takeA = j >= nb || (i < na && vless(sa[i], sb[j]));
+    out[o0 + dd + k] = takeA ? sa[i] : sb[j];
     if (takeA) ++i;
     else ++j;
   }
@@ -501,8 +666,7 @@ static void merge_sort(VKey*& keys, VKey*& tmp, int64_t P, cudaStream_t st) {
   // P is a power of two >= kLocalSort
   k_mt_block_sort<<<(unsigned)(P / kLocalSort), kLocalSort / 2, 0, st>>>(keys);
   for (int64_t w = kLocalSort; w < P; w <<= 1) {
-    const int64_t threads = P / kMergeItems;
-    k_mt_merge<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(P, w, keys, tmp);
+    k_mt_merge<<<(unsigned)(P / kMergeTile), 256, 0, st>>>(P, w, keys, tmp);
     VKey* t = keys;
     keys = tmp;
     tmp = t;
@@ -520,29 +684,34 @@ static int mt_run(const double* sdf, const double* deform, int R, MtResult& out,
   const Grid G = make_grid(R);
   const int64_t n = R + 1, N = n * n * n, C = (int64_t)R * R * R;
   out.st = st;
-  // E1: crossing edges per vertex -> edge index bases
+  // E1: crossing edges per vertex -> per-32-vertex-word edge index bases
+  const int64_t NW = (N + 31) / 32;
   uint8_t* flags = nullptr;
   int32_t* cnt = nullptr;
   int64_t *ebase = nullptr, *scratch = nullptr;
-  cudaMallocAsync(&flags, N, st);
-  cudaMallocAsync(&cnt, sizeof(int32_t) * N, st);
-  cudaMallocAsync(&ebase, sizeof(int64_t) * (N + 1), st);
-  cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(N), st);
+  cudaMallocAsync(&flags, 32 * NW, st);
+  cudaMallocAsync(&cnt, sizeof(int32_t) * NW, st);
+  cudaMallocAsync(&ebase, sizeof(int64_t) * (NW + 1), st);
+  cudaMallocAsync(&scratch, sizeof(int64_t) * compact_blocks(NW), st);
   uint32_t* negbits = nullptr;
-  cudaMallocAsync(&negbits, sizeof(uint32_t) * ((N + 31) / 32 + 8), st);
+  cudaMallocAsync(&negbits, sizeof(uint32_t) * (NW + 8), st);
   k_mt_vflags<<<grid_blocks(N), 256, 0, st>>>(N, G, sdf, flags, cnt, negbits);
-  scan_counts(cnt, N, ebase, scratch, st);
+  scan_counts(cnt, NW, ebase, scratch, st);
   // T1: per-chunk group counts over cells, exclusive scans
   const int64_t nb = (C + kCellChunk - 1) / kCellChunk;
   int64_t* off = nullptr;  // o1 | o3 | o2, nb + 1 each
   cudaMallocAsync(&off, sizeof(int64_t) * 3 * (nb + 1), st);
   int64_t *o1 = off, *o3 = off + (nb + 1), *o2 = off + 2 * (nb + 1);
-  k_mt_ccount<<<(unsigned)nb, kScanThreads, 0, st>>>(C, G, negbits, o1, o3, o2);
-  k_scan_i64<<<1, 1024, 0, st>>>(o1, nb);
-  k_scan_i64<<<1, 1024, 0, st>>>(o3, nb);
-  k_scan_i64<<<1, 1024, 0, st>>>(o2, nb);
+  uint32_t* zbits = nullptr;
+  const int ww = (int)((n + 31) / 32);
+  if (R % 8 == 0) {
+    cudaMallocAsync(&zbits, sizeof(uint32_t) * (size_t)(n * n * ww), st);
+    k_mt_zbits<<<grid_blocks(32 * n * ((n + 31) / 32) * ww), 256, 0, st>>>(G, negbits, zbits, ww);
+  }
+  k_mt_ccount<<<(unsigned)nb, kScanThreads, 0, st>>>(C, G, negbits, o1, o3, o2, zbits, ww);
+  k_scan_i64<<<3, 1024, 0, st>>>(o1, nb, nb + 1);  // o1, o3, o2
   int64_t h[4];
-  cudaMemcpyAsync(&h[0], ebase + N, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[0], ebase + NW, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&h[1], o1 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&h[2], o3 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&h[3], o2 + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
@@ -550,7 +719,7 @@ static int mt_run(const double* sdf, const double* deform, int R, MtResult& out,
   cudaStreamSynchronize(st);
   const int64_t V = h[0], n1 = h[1], n3 = h[2], n2 = h[3], F = n1 + n3 + 2 * n2;
   if (V == 0 || F == 0) {
-    free_all({flags, ebase, scratch, off, negbits}, st);
+    free_all({flags, ebase, scratch, off, negbits, zbits}, st);
     cudaStreamSynchronize(st);
     return 0;
   }
@@ -559,11 +728,14 @@ static int mt_run(const double* sdf, const double* deform, int R, MtResult& out,
   int64_t* tris = nullptr;
   cudaMallocAsync(&verts, sizeof(double) * 3 * V, st);
   cudaMallocAsync(&tris, sizeof(int64_t) * 3 * F, st);
-  k_mt_verts<<<grid_blocks(N), 256, 0, st>>>(N, G, sdf, deform, flags, ebase, verts);
+  int64_t* elist = nullptr;
+  cudaMallocAsync(&elist, sizeof(int64_t) * V, st);
+  k_mt_elist<<<grid_blocks(32 * NW), 256, 0, st>>>(N, flags, ebase, elist);
+  k_mt_verts<<<grid_blocks(V), 256, 0, st>>>(V, G, sdf, deform, elist, verts);
   uint32_t* tlist = nullptr;
   const int64_t ncross = n1 + n3 + n2;
   cudaMallocAsync(&tlist, sizeof(uint32_t) * ncross, st);
-  k_mt_clist<<<(unsigned)nb, kScanThreads, 0, st>>>(C, G, negbits, o1, o3, o2, n1, n3, tlist);
+  k_mt_clist<<<(unsigned)nb, kScanThreads, 0, st>>>(C, G, negbits, o1, o3, o2, n1, n3, tlist, zbits, ww);
   k_mt_emit<<<grid_blocks(ncross), 256, 0, st>>>(ncross, G, sdf, deform, flags, ebase, verts, tlist, n1, n3, n2, tris);
   // W: weld equal positions (np.unique over rows: lexicographic), remap, drop degenerates
   int64_t P = kLocalSort;
@@ -588,7 +760,7 @@ static int mt_run(const double* sdf, const double* deform, int R, MtResult& out,
   int64_t* d_total = compact(F, tk, scratch2, st);
   cudaMemcpyAsync(&h[0], d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(&h[1], excl + V, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  free_all({flags, ebase, scratch, off, negbits, tlist, verts, tris, keys, ktmp, first, excl, remap, scratch2}, st);
+  free_all({flags, ebase, scratch, off, negbits, zbits, elist, tlist, verts, tris, keys, ktmp, first, excl, remap, scratch2}, st);
   cudaStreamSynchronize(st);
   out.nt = h[0];
   out.nv = h[1];

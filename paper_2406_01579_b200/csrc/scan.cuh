@@ -78,8 +78,10 @@ __global__ void __launch_bounds__(kScanThreads) k_count(int64_t n, F f, int64_t*
   }
 }
 
-// exclusive scan of n int64 values in place, total written to a[n] (one CTA, 1024 threads)
-static __global__ void __launch_bounds__(1024) k_scan_i64(int64_t* __restrict__ a, int64_t n) {
+// exclusive scan of n int64 values in place, total written to a[n] (one CTA, 1024 threads);
+// CTA b scans the array at a + b * stride (several equal-length arrays in one launch)
+static __global__ void __launch_bounds__(1024) k_scan_i64(int64_t* __restrict__ a, int64_t n, int64_t stride = 0) {
+  a += blockIdx.x * stride;
   __shared__ int64_t wtot[32];
   __shared__ int64_t carry_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -72,3 +72,20 @@ def test_two_phase_abi_matches_one_pass(ts):
     assert counts[0] == nt.value and counts[1] == nv.value
     assert np.array_equal(V.cpu().numpy(), ref.vertices)
     assert np.array_equal(F.cpu().numpy(), ref.triangles)
+
+
+@pytest.mark.parametrize("R", [20, 40])
+def test_grids_match_oracle(ts, R):
+    """R % 8 != 0 (per-cell corner bits) and R % 8 == 0 (z-fastest sign rows, eight cells per
+    window) on a noisy, deformed field with exact zeros (f = 0 counts as outside; endpoint
+    snaps), bit for bit against the oracle's restatement of grid.py:136-239."""
+    from oracle import ts_oracle as O
+    og = O.build_grid(R)
+    of = O.noisy_field(og, noise=0.1, deform=0.4, seed=R)
+    sdf = of.sdf.copy()
+    sdf[::7] = 0.0
+    V, F = O.marching_tetrahedra(og, O.FieldState(sdf, of.deformation, of.deform_limit))
+    m = _mt(ts, R, sdf, of.deformation)
+    assert len(F) > 0
+    assert np.array_equal(m.vertices, V)
+    assert np.array_equal(m.triangles, F)
