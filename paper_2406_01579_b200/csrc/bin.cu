@@ -189,9 +189,19 @@ constexpr int kSmemSortCap = TS_SMEM_SORT_CAP;  // longest list sorted by one 25
 constexpr int kRadixThreads = 1024;
 constexpr int kRadixWarps = kRadixThreads / 32;
 
+// qdiff / vdiff: OR of (key XOR first key) over the real keys — a pass whose digit is the same
+// for every real key is skipped (a stable pass with one occupied bucket, and the padding
+// ~0 keys already last, leaves the order unchanged); tiles span a narrow depth band, so the
+// top byte of q rarely varies
+__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int NT, int E>
 __device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint32_t* H, uint32_t* dbase,
-                                                int passes_lo) {
+                                                int passes_lo, uint32_t qdiff, uint32_t vdiff) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int base = w * 32 * E + lane;
@@ -199,6 +209,7 @@ __device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint
   for (int pass = 0; pass < passes_lo + 4; ++pass) {
     const bool hi = pass >= passes_lo;
     const int shift = (hi ? pass - passes_lo : pass) * 8;
+    if ((((hi ? qdiff : vdiff) >> shift) & 255u) == 0u) continue;  // (CTA-uniform)
     for (int i = threadIdx.x; i < NW * 256; i += NT) H[i] = 0u;
     uint32_t q[E], v[E], rk[E];
 #pragma unroll
@@ -269,26 +280,26 @@ __device__ __forceinline__ void radix_sort_tile(uint32_t* kq, uint32_t* kv, uint
 // scratch int.
 template <int NT, int MAXE>
 __device__ __forceinline__ void radix_sort_keys(uint32_t* kq, uint32_t* kv, uint32_t* H, uint32_t* dbase, int P,
-                                                int L, int passes_lo, int& flag) {
+                                                int L, int passes_lo, int& flag, uint32_t qdiff, uint32_t vdiff) {
   constexpr int kMaxRun = 64;
   if (threadIdx.x == 0) flag = 0;
   for (int full = 0; full < 2; ++full) {
     const int plo = full ? passes_lo : 0;
     if (MAXE == 8) {
       if (P == 4 * NT)
-        radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo);
+        radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo, qdiff, vdiff);
       else
-        radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo);
+        radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo, qdiff, vdiff);
     } else {  // P = NT * E with E = ceil(L / NT) (>= 3): no power-of-two padding
       switch (P / NT) {
-        case 3: radix_sort_tile<NT, 3>(kq, kv, H, dbase, plo); break;
-        case 4: radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo); break;
-        case 5: radix_sort_tile<NT, 5>(kq, kv, H, dbase, plo); break;
-        case 6: radix_sort_tile<NT, 6>(kq, kv, H, dbase, plo); break;
-        case 7: radix_sort_tile<NT, 7>(kq, kv, H, dbase, plo); break;
-        case 8: radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo); break;
-        case 12: radix_sort_tile<NT, 12>(kq, kv, H, dbase, plo); break;
-        default: radix_sort_tile<NT, MAXE>(kq, kv, H, dbase, plo); break;
+        case 3: radix_sort_tile<NT, 3>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        case 4: radix_sort_tile<NT, 4>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        case 5: radix_sort_tile<NT, 5>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        case 6: radix_sort_tile<NT, 6>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        case 7: radix_sort_tile<NT, 7>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        case 8: radix_sort_tile<NT, 8>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        case 12: radix_sort_tile<NT, 12>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
+        default: radix_sort_tile<NT, MAXE>(kq, kv, H, dbase, plo, qdiff, vdiff); break;
       }
     }
     if (full) break;
@@ -351,6 +362,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
                                                             const int* __restrict__ ovf) {
   extern __shared__ uint64_t s[];
   __shared__ int bad, longrun;
+  __shared__ unsigned long long kdiff;
   const int t = blockIdx.x;
   if (t >= T || (ovf && *ovf)) return;
   const int64_t lo = starts[t], L = starts[t + 1] - lo;
@@ -373,14 +385,24 @@ __global__ void __launch_bounds__(THREADS) k_tile_sort_smem(int T, int64_t cap, 
   int E = (int)((L + THREADS - 1) / THREADS);
   E = E < 3 ? 3 : (E <= 8 ? E : (E <= 12 ? 12 : 16));
   const int P = E * THREADS;
+  const uint64_t k0 = keys[lo];
+  uint64_t diff = 0;
   for (int i = threadIdx.x; i < P; i += THREADS) {
     const uint64_t k = i < L ? keys[lo + i] : ~0ull;
+    if (i < L) diff |= k ^ k0;
     kq[i] = (uint32_t)(k >> 32);
     kv[i] = (uint32_t)k;
   }
-  if (threadIdx.x == 0) bad = 0;
+  if (threadIdx.x == 0) {
+    bad = 0;
+    kdiff = 0;
+  }
   __syncthreads();
-  radix_sort_keys<THREADS, 16>(kq, kv, H, dbase, P, (int)L, passes_lo, longrun);
+  diff = warp_or64(diff);
+  if ((threadIdx.x & 31) == 0 && diff) atomicOr(&kdiff, (unsigned long long)diff);
+  __syncthreads();
+  radix_sort_keys<THREADS, 16>(kq, kv, H, dbase, P, (int)L, passes_lo, longrun, (uint32_t)(kdiff >> 32),
+                               (uint32_t)kdiff);
   int mybad = 0;
   for (int i = threadIdx.x; i < L; i += THREADS) {
     emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
@@ -400,6 +422,7 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
   if (ovf && *ovf) return;
   extern __shared__ uint32_t sm32[];
   __shared__ int longrun;
+  __shared__ unsigned long long kdiff;
   uint32_t* kq = sm32;
   uint32_t* kv = sm32 + cap;
   uint32_t* H = sm32 + 2 * cap;
@@ -414,14 +437,24 @@ __global__ void __launch_bounds__(kRadixThreads, 1) k_tile_sort_long(
     int E = (L + kRadixThreads - 1) / kRadixThreads;
     E = E < 3 ? 3 : (E <= 8 ? E : (E <= 12 ? 12 : 16));
     const int P = E * kRadixThreads;
+    const uint64_t k0 = keys[lo];
+    uint64_t diff = 0;
     for (int i = threadIdx.x; i < P; i += kRadixThreads) {
       const uint64_t k = i < L ? keys[lo + i] : ~0ull;  // padding sorts last
+      if (i < L) diff |= k ^ k0;
       kq[i] = (uint32_t)(k >> 32);
       kv[i] = (uint32_t)k;
     }
-    if (threadIdx.x == 0) bad = 0;
+    if (threadIdx.x == 0) {
+      bad = 0;
+      kdiff = 0;
+    }
     __syncthreads();
-    radix_sort_keys<kRadixThreads, 16>(kq, kv, H, dbase, P, L, passes_lo, longrun);
+    diff = warp_or64(diff);
+    if ((threadIdx.x & 31) == 0 && diff) atomicOr(&kdiff, (unsigned long long)diff);
+    __syncthreads();
+    radix_sort_keys<kRadixThreads, 16>(kq, kv, H, dbase, P, L, passes_lo, longrun, (uint32_t)(kdiff >> 32),
+                                       (uint32_t)kdiff);
     int mybad = 0;
     for (int i = threadIdx.x; i < L; i += kRadixThreads) {
       emit_sorted(((uint64_t)kq[i] << 32) | kv[i], lo + i, t, tiles_x, br, splat_off, items, pos_of, qsorted);
