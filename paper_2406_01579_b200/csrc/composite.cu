@@ -701,6 +701,7 @@ struct FwdSmem {
   ChunkMask bmask[TS_TILE_PX];  // per pixel: chunk splats that blend (bit j)
   float col[kCh][3];
   uint32_t skip[TS_TILE_PX / 32];
+  uint32_t pend[TS_TILE_PX / 32];  // pixels with a pair queued for the exact re-decision
   uint16_t exq[kCap];  // pairs queued for the exact FP64 re-decision
   uint16_t cand[kWarps][64];  // per warp: candidate pairs (it | face mask << 11) of phase A1
   uint32_t cbits[kCap / 32];  // the chunk's blend bits (pair index within the chunk)
@@ -742,6 +743,8 @@ __device__ __forceinline__ void a2_candidates(FwdSmem& F, const uint16_t* cq, in
       const int slot = atomicAdd(&F.nex, 1);
       TS_ASSERT(slot < kCap);
       F.exq[slot] = (uint16_t)itc;
+      const int q = (py_ - ty0) * TS_TILE + (px_ - tx0);
+      atomicOr(&F.pend[q >> 5], 1u << (q & 31));
       prefetch_exact(S64, r.k);
     } else if (e == 1) {
       put_pair(F, itc, j, (py_ - ty0) * TS_TILE + (px_ - tx0), b, ib0, pair_rec);
@@ -808,6 +811,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       stage_chunk<true>(list, base, L - base, F.pf, colors, COLOR, F.sh, F.col, F.R, tx0, ty0, item_off + lo);
     F.bmask[pix] = 0ull;
     if (threadIdx.x < kCap / 32) F.cbits[threadIdx.x] = 0u;
+    if (threadIdx.x < TS_TILE_PX / 32) F.pend[threadIdx.x] = 0u;
     if (threadIdx.x == 0) F.nex = 0;
     __syncthreads();
     TS_PHASE(0);
@@ -863,8 +867,35 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
     // ---- A': exact FP64 re-decisions, 8 pairs per warp, one face per lane ------------------
     //      (F.nex is CTA-uniform after the barrier: chunks without queued pairs skip the pass
     //      and its barrier)
+    // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
+    auto blend = [&]() {
+      if (done) return;
+      ChunkMask m = F.bmask[pix];
+      while (m) {
+        const int j = __ffsll(m) - 1;
+        m &= m - 1ull;
+        const float2 c = F.code[pair_index(F.R, j, xi, yi)];
+        acc.add(__fmul_rn(T, c.x), F.sh[j], COLOR ? F.col[j] : nullptr);
+        T = __fmul_rn(T, fabsf(c.y));
+        ++nb;
+        // a clipped blend leaves T * (1 - ALPHA_CLIP) < T_STOP in the FP64 reference whenever
+        // 1 - ALPHA_CLIP < t_stop (T <= 1), which FP32 T = 1e-4f would not see at T = 1
+        if (T < t_stop || (c.y < 0.f && clip_stops)) {
+          done = true;
+          nproc = cp[base + j] + 1;  // list entries consumed (the reference's position)
+          break;
+        }
+      }
+    };
+    bool blended = false;
     const int nex = F.nex;
     if (nex > 0) {
+      // a warp with no re-decision to make whose pixels have none pending blends them now,
+      // while the re-decisions' FP64 chains run (its codes and masks are final)
+      if ((threadIdx.x >> 5) * 8 >= nex && F.pend[threadIdx.x >> 5] == 0u) {
+        blend();
+        blended = true;
+      }
       for (int q0 = (threadIdx.x >> 5) * 8; q0 < nex; q0 += kWarps * 8) {
         const int qi = q0 + ((threadIdx.x & 31) >> 2);
         const bool act = qi < nex;
@@ -891,25 +922,7 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       pacc[6] += F.nex;
       if (F.nex > (int)g_ts_phase[7]) atomicMax(&g_ts_phase[7], (unsigned long long)F.nex);
     }
-    // ---- B: pixel-serial blend over this pixel's blending splats (bit order = list order) --
-    if (!done) {
-      ChunkMask m = F.bmask[pix];
-      while (m) {
-        const int j = __ffsll(m) - 1;
-        m &= m - 1ull;
-        const float2 c = F.code[pair_index(F.R, j, xi, yi)];
-        acc.add(__fmul_rn(T, c.x), F.sh[j], COLOR ? F.col[j] : nullptr);
-        T = __fmul_rn(T, fabsf(c.y));
-        ++nb;
-        // a clipped blend leaves T * (1 - ALPHA_CLIP) < T_STOP in the FP64 reference whenever
-        // 1 - ALPHA_CLIP < t_stop (T <= 1), which FP32 T = 1e-4f would not see at T = 1
-        if (T < t_stop || (c.y < 0.f && clip_stops)) {
-          done = true;
-          nproc = cp[base + j] + 1;  // list entries consumed (the reference's position)
-          break;
-        }
-      }
-    }
+    if (!blended) blend();
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if ((threadIdx.x & 31) == 0) F.skip[threadIdx.x >> 5] = m;
     base += n;
