@@ -893,14 +893,12 @@ __global__ void __launch_bounds__(TS_TILE_PX, 4) k_forward(
       // re-decision batches (8 pairs each) on warps 0, 1, ..; a warp with no batch and no
       // pending pixel blends now, while the re-decisions' FP64 chains run (its codes and masks
       // are final).  (Routing the batches to the warps with pending pixels measured no better.)
-      const int warp = threadIdx.x >> 5, nbat = (nex + 7) >> 3;
-      const bool mine = F.pend[warp] != 0u;
-      const int first = warp;
-      if (!mine && first >= nbat) {
+      const int warp = threadIdx.x >> 5;
+      if (warp * 8 >= nex && F.pend[warp] == 0u) {
         blend();
         blended = true;
       }
-      for (int q0 = first * 8; q0 < nex; q0 += kWarps * 8) {
+      for (int q0 = warp * 8; q0 < nex; q0 += kWarps * 8) {
         const int qi = q0 + ((threadIdx.x & 31) >> 2);
         const bool act = qi < nex;
         const int it = act ? F.exq[qi] : 0;
