@@ -86,7 +86,12 @@ def test_fitstep_sync_free_equals_threaded(ts):
             step.check_status()
             grads.append(gr.d_vert.clone())
             assert st.views == 4 and all(k > 0 for k in st.splats)
-        out[mode] = (grads, f.sdf.clone(), step.opt.t, dict(step.view_counts))
+            if it == 0:
+                # the view sizes of the first step (same field in both modes: the FP32-atomic
+                # gradients make the later fields differ in the last bits, which can move a
+                # splat across a tile boundary)
+                counts = dict(step.view_counts)
+        out[mode] = (grads, f.sdf.clone(), step.opt.t, counts)
     (ga, sa, ta, ca), (gb, sb, tb, cb) = out["threaded"], out["sync_free"]
     assert ta == tb == 3
     assert ca == cb
