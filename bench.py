@@ -517,6 +517,11 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
             continue
         if r == 1:
             cnt_gpu = _native.debug_counters(True)
+            # splats with a non-empty pixel rectangle (the others are certified never to blend:
+            # no pairs, no chain work)
+            rr = sc.records[:, :8].contiguous().view(torch.int32).view(-1, 2).to(torch.int64)
+            lo16 = lambda v: ((v & 0xFFFF) ^ 0x8000) - 0x8000
+            K_ne = int(((lo16(rr[:, 0]) <= (rr[:, 0] >> 16)) & (lo16(rr[:, 1]) <= (rr[:, 1] >> 16))).sum())
             _native.check(_native.lib().ts_debug_set_flags(0))
             P_pairs = int(sv.item_off[-1].item())
             continue
@@ -541,6 +546,11 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     kern["render_forward"]["lane_ops_gpu_executed"] = 120 * P_bbox_gpu + 19 * B
     kern["render_forward"]["frac_gpu_executed"] = (kern["render_forward"]["lane_ops_gpu_executed"] / (tf * 1e-3)
                                                    / 1e12 / fp32_peak)
+    # backward: the same per-pair and per-splat terms, the chain only over splats with a
+    # non-empty rectangle
+    kern["render_backward"]["lane_ops_gpu_executed"] = 300 * B + 300 * K_ne
+    kern["render_backward"]["frac_gpu_executed"] = (kern["render_backward"]["lane_ops_gpu_executed"] / (tb * 1e-3)
+                                                    / 1e12 / fp32_peak)
     # DRAM traffic, issue and FMA-pipe utilisation of the same kernel from the committed ncu
     # --set full capture (profiles/r02_ncu_compositing.json, else the round-1 traffic file)
     traffic, tsrc, ncu = None, None, None
@@ -561,14 +571,19 @@ def roofline_probe(ts, _native, g, field, cam, dm, s, sdf0, def0):
     roof = {"kernel": top, "bound": "fp32", "achieved": d["achieved_Tlaneops"], "peak": fp32_peak,
             "unit": "T lane-op/s", "frac": d["frac_of_fp32_issue"], "traffic": traffic, "traffic_unit": "bytes/launch",
             "traffic_source": tsrc,
-            "work_model": "SURVEY 8d: 8 P_pop + 120 P_bbox + 19 B lane-ops (forward)",
+            "work_model": {"render_forward": "SURVEY 8d: 8 P_pop + 120 P_bbox + 19 B lane-ops",
+                           "render_backward": "SURVEY 8d: 300 B + 300 K_v lane-ops"}[top],
             "frac_gpu_executed": kern[top].get("frac_gpu_executed"),
-            "gpu_executed_model": "120 P_bbox_gpu + 19 B (no per-pixel window pops: the GPU replays the window once per "
-                                  "non-monotone tile; P_bbox_gpu leaves out the splats certified never to blend)",
+            "gpu_executed_model": {"render_forward": "120 P_bbox_gpu + 19 B (no per-pixel window pops: the GPU replays "
+                                                     "the window once per non-monotone tile; P_bbox_gpu leaves out the "
+                                                     "splats certified never to blend)",
+                                   "render_backward": "300 B + 300 K_ne (the vertex chain runs only over the splats "
+                                                      "with a non-empty pixel rectangle)"}[top],
             "ncu": ncu,
             "peak_source": f"{n_sm} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (FP32 issue, SURVEY 8d; no tensor "
                            f"cores: not a dense contraction; DRAM traffic well under HBM bandwidth)"}
-    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "P_bbox_gpu": P_bbox_gpu, "B": B, "K_a": K_a, "K_v": K_v, "M": M,
+    extra = {"P_pop": P_pop, "P_bbox": P_bbox, "P_bbox_gpu": P_bbox_gpu, "B": B, "K_a": K_a, "K_v": K_v, "K_ne": K_ne,
+             "M": M,
              "pixel_pairs": P_pairs_ref, "pixel_pairs_gpu": P_pairs,
              "fp64_redecisions_edge": cnt_gpu[0], "fp64_redecisions_alpha": cnt_gpu[1]}
     return roof, {"compositing": kern, "counts": extra}
