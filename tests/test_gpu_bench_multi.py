@@ -25,8 +25,11 @@ def _torchrun(args, port, extra_env):
     return json.loads(lines[0])
 
 
-def test_bench_two_ranks_one_json_line():
-    d = _torchrun(["--steps", "1", "--warmup", "3"], 29611, {"TS_BENCH_ONE_GPU": "1"})
+@pytest.mark.parametrize("sync_free", ["0", "1"])
+def test_bench_two_ranks_one_json_line(sync_free):
+    """threaded lanes and the sync-free path (the default when ranks share few host CPUs)"""
+    d = _torchrun(["--steps", "1", "--warmup", "3"], 29611 + int(sync_free),
+                  {"TS_BENCH_ONE_GPU": "1", "TS_SYNC_FREE": sync_free})
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["steps"] == 1 and d["warmup"] == 3
     assert d["config"]["global_batch_views"] == 2 * d["config"]["views_per_gpu"]
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
@@ -34,6 +37,6 @@ def test_bench_two_ranks_one_json_line():
 
 
 def test_reference_arm_two_ranks():
-    d = _torchrun(["--impl", "reference", "--steps", "1", "--warmup", "1"], 29612, {})
+    d = _torchrun(["--impl", "reference", "--steps", "1", "--warmup", "1"], 29613, {})
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] >= 1
