@@ -533,7 +533,9 @@ __global__ void __launch_bounds__(kLocalSort / 2) k_mt_block_sort(VKey* __restri
   for (int i = threadIdx.x; i < kLocalSort; i += blockDim.x) keys[b0 + i] = sk[i];
 }
 
-constexpr int kMergeItems = 4;
+// outputs per thread of a merge pass: one (256-output CTAs, 4x the CTAs of four per thread:
+// the passes are latency-bound, 0.93 vs 1.01-1.04 ms per extraction at 256^3)
+constexpr int kMergeItems = 1;
 // first i in [max(0, d - w), min(d, w)] with B[d - 1 - i] < A[i] (the merge path's split of
 // output diagonal d between runs A and B), by a 32-way search of one warp: each round tests 32
 // evenly spaced candidates with independent loads (~4 rounds for a 2^18 run, instead of 18
